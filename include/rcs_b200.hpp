@@ -1,0 +1,243 @@
+// rcs_b200.hpp — C++ host API of the B200-native sampler (namespace rcs).
+//
+// Drop-in surface for the reference's hot path (/root/reference/proj/include/rcs):
+// same type names, field meanings, function signatures, result semantics and
+// exception types, so a caller of the reference's
+//   contract / contract_group / execute_assignment   (contraction_engine.hpp:54-76)
+//   top_k_select / direct_sample / xeb               (sampling.hpp:42-51)
+// switches by including this header and linking libpaper_2406_18889_b200.so.
+// The inputs to that path (circuit, network, plan, candidate set) are
+// re-implemented host-side with identical semantics so plans and candidate sets
+// are bit-identical to the reference's.  Contraction and post-processing run on
+// the GPU through the C ABI in rcsg.h; there is no CPU execution path.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace rcs {
+
+using cplx = std::complex<double>;
+using Label = int;
+
+// ---- errors (reference errors.hpp:9-25; exit codes 2/3/4)
+struct Error : std::runtime_error {
+    Error(std::string msg, int code) : std::runtime_error(std::move(msg)), exit_code(code) {}
+    int exit_code;
+};
+struct ConfigError : Error {
+    explicit ConfigError(std::string msg) : Error(std::move(msg), 2) {}
+};
+struct NumericFault : Error {
+    NumericFault(std::string msg, int step) : Error(std::move(msg), 3), step_index(step) {}
+    int step_index;
+};
+struct CapacityError : Error {
+    explicit CapacityError(std::string msg) : Error(std::move(msg), 4) {}
+};
+// CUDA / NCCL runtime failure (C-ABI status 5; CLI exit 1).
+struct DeviceError : Error {
+    explicit DeviceError(std::string msg) : Error(std::move(msg), 1) {}
+};
+
+// ---- SplitMix64 stream (reference rng.hpp:10-45); counter-based form in rcs_rng.h
+class Rng {
+  public:
+    explicit Rng(std::uint64_t seed) : s_(seed) {}
+    std::uint64_t next_u64();
+    double next_double();
+    std::uint64_t next_below(std::uint64_t bound);
+    bool next_bool() { return (next_u64() >> 63) != 0; }
+    Rng split(std::uint64_t tag) const;
+    std::uint64_t state() const { return s_; }
+
+  private:
+    std::uint64_t s_;
+};
+
+// ---- circuit (reference circuit.hpp:13-63)
+enum class GateKind { SqrtX, SqrtY, SqrtW, TwoQubit };
+const char* gate_kind_name(GateKind kind);
+GateKind gate_kind_from_name(const std::string& name);
+std::vector<cplx> gate_unitary(GateKind kind);
+
+struct Gate {
+    GateKind kind;
+    std::vector<int> targets;
+    std::vector<cplx> unitary;
+    int matrix_dim() const { return targets.size() == 1 ? 2 : 4; }
+};
+struct Layer {
+    std::vector<Gate> gates;
+};
+struct Circuit {
+    int n_qubits = 0;
+    std::uint64_t seed = 0;
+    std::string topology;
+    std::vector<Layer> layers;
+    bool exceeds_exact_cap = false;
+    int n_cycles() const { return static_cast<int>(layers.size()) / 2; }
+};
+struct Topology {
+    std::string name;
+    int n_qubits = 0;
+    std::vector<std::vector<std::pair<int, int>>> patterns;
+    std::vector<int> sequence;
+};
+// "line", "ring", "grid(R,C)" as in the reference, plus "sycamore53" (new).
+Topology make_topology(const std::string& name, int n_qubits);
+Circuit gen_random_circuit(int n_qubits, int n_cycles, const std::string& topology,
+                           std::uint64_t seed);
+
+// ---- tensor network (reference tensor_network.hpp:12-48)
+struct Tensor {
+    std::vector<Label> labels;  // labels[0] is the most significant index bit
+    std::vector<cplx> data;
+    int rank() const { return static_cast<int>(labels.size()); }
+    std::uint64_t size() const { return data.size(); }
+};
+struct WireEdge {
+    Label label;
+    int qubit;
+    int layer;
+};
+struct TensorNetwork {
+    std::vector<Tensor> tensors;
+    std::vector<std::string> label_names;
+    std::vector<Label> output_labels;
+    std::vector<Label> open_labels;
+    std::vector<int> open_qubits;
+    std::vector<WireEdge> wire_edges;
+    int n_qubits = 0;
+    int n_layers = 0;
+    const std::string& label_name(Label l) const { return label_names[l]; }
+    Label label_by_name(const std::string& name) const;
+    bool is_open(Label l) const;
+};
+TensorNetwork circuit_to_network(const Circuit& circuit, const std::vector<int>& open_qubits);
+
+// ---- contraction plan (reference contraction_plan.hpp:11-74)
+struct PlanStep {
+    int lhs = -1, rhs = -1, result = -1;
+    std::vector<Label> result_labels;  // sorted ascending (not the executor layout)
+    std::uint64_t summed = 0;
+    std::uint64_t flops = 0;  // 8 real FLOPs per complex multiply-add
+    std::uint64_t result_bytes = 0;
+};
+struct ContractionPlan {
+    std::vector<PlanStep> steps;
+    std::vector<Label> sliced;
+    std::vector<Label> broken;
+    std::vector<Label> fixed_outputs;
+    std::uint64_t flops_per_slice = 0;
+    std::uint64_t traffic_bytes_per_slice = 0;
+    std::uint64_t peak_bytes = 0;
+    std::uint64_t memory_budget_bytes = 0;
+    std::uint64_t n_slices() const { return std::uint64_t{1} << sliced.size(); }
+    std::uint64_t subtask_flops() const { return flops_per_slice * n_slices(); }
+    std::uint64_t subtask_traffic_bytes() const { return traffic_bytes_per_slice * n_slices(); }
+};
+enum class SearchEffort { Low, Medium, High };
+ContractionPlan find_contraction_path(const TensorNetwork& network,
+                                      std::uint64_t memory_budget_bytes,
+                                      SearchEffort effort = SearchEffort::Medium,
+                                      std::uint64_t seed = 0,
+                                      const std::vector<Label>& broken = {});
+std::vector<Label> select_broken_edges(const TensorNetwork& network, int k_edges,
+                                       std::uint64_t seed = 0);
+
+// ---- executor (reference contraction_engine.hpp:13-86)
+struct BrokenEdgeConfig {
+    std::vector<Label> broken_labels;
+    std::vector<std::uint64_t> configurations;
+    int k() const { return static_cast<int>(broken_labels.size()); }
+    std::uint64_t m() const { return configurations.size(); }
+    double predicted_fidelity() const;
+};
+BrokenEdgeConfig make_broken_config(std::vector<Label> broken_labels, std::uint64_t m,
+                                    std::uint64_t seed);
+
+struct ExecutionStats {
+    std::uint64_t flops = 0;       // plan-equivalent FLOPs (8 per complex MAC)
+    std::uint64_t peak_bytes = 0;  // device arena bytes
+};
+struct SubtaskTiming {
+    std::uint64_t subtask_id = 0;
+    std::uint64_t config_bits = 0;
+    double wall_ms = 0;
+    std::uint64_t flops = 0;
+};
+struct AmplitudeBatch {
+    std::uint64_t group_id = 0;
+    int n_open = 0;
+    std::uint64_t fixed_bits = 0;
+    std::vector<cplx> amplitudes;
+};
+struct ContractResult {
+    std::vector<cplx> amplitudes;
+    std::vector<SubtaskTiming> timings;
+    ExecutionStats stats;
+};
+
+std::vector<cplx> execute_assignment(const TensorNetwork& network, const ContractionPlan& plan,
+                                     const std::map<Label, int>& assignment,
+                                     ExecutionStats* stats = nullptr);
+// `workers` is accepted for signature compatibility; results never depend on it.
+ContractResult contract(const TensorNetwork& network, const ContractionPlan& plan,
+                        const BrokenEdgeConfig* config,
+                        const std::map<Label, int>& fixed_outputs = {}, int workers = 1);
+AmplitudeBatch contract_group(const TensorNetwork& network, const ContractionPlan& plan,
+                              const BrokenEdgeConfig* config, std::uint64_t group_id,
+                              std::uint64_t fixed_bits);
+// Group-batched production path (new): amplitudes of every group, [M][2^l].
+std::vector<AmplitudeBatch> contract_groups(const TensorNetwork& network,
+                                            const ContractionPlan& plan,
+                                            const BrokenEdgeConfig* config,
+                                            const std::vector<std::uint64_t>& group_fixed);
+
+struct FidelityResult {
+    double value = 0;
+    bool zero_norm_warning = false;
+};
+FidelityResult state_fidelity(std::span<const cplx> approx, std::span<const cplx> exact);
+
+// Precision of the device executor: "f64" (default; reference-grade), "f32",
+// "tf32" (tcgen05 tensor cores), "3xtf32" (split-tf32 tensor cores, fp32-grade).
+void set_precision(const std::string& precision);
+std::string get_precision();
+
+// ---- sampler (reference sampling.hpp:10-85)
+using ProbFn = std::function<double(std::uint64_t)>;
+struct CandidateSet {
+    int n_qubits = 0;
+    std::vector<int> open_qubits;
+    std::vector<std::uint64_t> group_fixed;
+    int duplicate_groups = 0;
+    int l() const { return static_cast<int>(open_qubits.size()); }
+    std::uint64_t n_groups() const { return group_fixed.size(); }
+    std::uint64_t size() const { return n_groups() << l(); }
+    std::uint64_t member(std::uint64_t group, std::uint64_t i) const;
+};
+CandidateSet build_candidate_set(int n_qubits, std::vector<int> open_qubits,
+                                 std::uint64_t n_groups, std::uint64_t seed);
+enum class Provenance { Direct, TopK };
+struct SampleSet {
+    int n_qubits = 0;
+    std::vector<std::uint64_t> bitstrings;
+    Provenance provenance = Provenance::Direct;
+    std::uint64_t k = 0;
+};
+double xeb(const SampleSet& samples, const ProbFn& q);
+SampleSet top_k_select(const CandidateSet& candidates, const ProbFn& p, std::uint64_t k);
+SampleSet direct_sample(const CandidateSet& candidates, const ProbFn& p, std::uint64_t rng_seed);
+double predicted_topk_xeb(double fidelity, std::uint64_t candidate_size, std::uint64_t k);
+std::uint64_t lexicographic_key(std::uint64_t index, int n_qubits);
+
+}  // namespace rcs

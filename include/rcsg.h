@@ -1,0 +1,178 @@
+/* rcsg.h — C ABI of the B200-native contraction + sampling path.
+ *
+ * Plain C types only (pointers, sizes, status codes); no torch / C++ types.
+ * This is the boundary the host C++ API (rcs_b200.hpp, namespace rcs) calls,
+ * and what a reference-side FFI (ctypes / pybind / dlopen) binds; see
+ * INTEGRATION.md.  Each entry point names the reference interface it replaces
+ * (file:line into /root/reference/proj).
+ *
+ * Status codes mirror the reference's error taxonomy (include/rcs/errors.hpp:9-25):
+ *   0 ok, 2 ConfigError, 3 NumericFault (step index via rcsg_last_error),
+ *   4 CapacityError, 5 CUDA/NCCL runtime failure.
+ *
+ * Layout conventions (parity-critical):
+ *   - leaf data row-major, labels[0] = most significant index bit, complex as
+ *     interleaved (re, im) float64;
+ *   - amplitudes of a group: bit j of the index <-> j-th smallest open qubit
+ *     (contraction_engine.cpp:193-207);
+ *   - group fixed bits: bit b <-> b-th non-open qubit in ascending order
+ *     (contraction_engine.cpp:310-318, sampling.cpp:14-27);
+ *   - slice s: bit b <-> plan.sliced[b]; broken config: bit b <-> plan.broken[b]
+ *     (contraction_engine.cpp:242-248).
+ */
+#ifndef RCSG_H
+#define RCSG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RCSG_OK = 0,
+    RCSG_ERR_CONFIG = 2,
+    RCSG_ERR_NUMERIC = 3,
+    RCSG_ERR_CAPACITY = 4,
+    RCSG_ERR_DEVICE = 5
+};
+
+/* Arithmetic of the contraction kernels. */
+enum {
+    RCSG_PREC_F64 = 0,   /* fp64 SIMT: reference-grade (<= 1e-10 norm-relative) */
+    RCSG_PREC_F32 = 1,   /* fp32 SIMT */
+    RCSG_PREC_TF32 = 2,  /* tcgen05 kind::tf32, fp32 accumulate in TMEM */
+    RCSG_PREC_3XTF32 = 3 /* split tf32 (hi*hi + hi*lo + lo*hi) on tcgen05: fp32-grade */
+};
+
+/* TensorNetwork (tensor_network.hpp:26-43), flattened. */
+typedef struct rcsg_network_desc {
+    int32_t n_leaves;
+    const int32_t* leaf_rank;   /* [n_leaves] */
+    const int32_t* leaf_labels; /* concatenated, sum(rank) */
+    const double* leaf_data;    /* concatenated 2^rank complex (interleaved) */
+    int32_t n_labels;
+    int32_t n_qubits;
+    const int32_t* output_labels; /* [n_qubits] final wire label per qubit */
+    int32_t n_open;
+    const int32_t* open_labels; /* [n_open], ascending qubit */
+    const int32_t* open_qubits; /* [n_open], ascending */
+} rcsg_network_desc;
+
+/* ContractionPlan (contraction_plan.hpp:19-36), flattened. */
+typedef struct rcsg_plan_desc {
+    int32_t n_steps;
+    const int32_t* steps; /* [n_steps][3] = lhs, rhs, result node ids (post-order) */
+    int32_t n_sliced;
+    const int32_t* sliced;
+    int32_t n_broken;
+    const int32_t* broken;
+    int32_t n_fixed;
+    const int32_t* fixed_outputs;
+} rcsg_plan_desc;
+
+typedef struct rcsg_stats {
+    uint64_t plan_flops;       /* sum over assignments of plan.flops_per_slice (reference-equivalent) */
+    uint64_t executed_flops;   /* 8*m*k*n actually issued on the device (after group sharing) */
+    uint64_t arena_bytes;      /* device arena size */
+    uint64_t kernel_launches;  /* our kernels launched */
+    uint64_t passes;           /* (config, slice, group-chunk) passes */
+    double device_ms;          /* CUDA-event time of the contraction on the program's stream */
+} rcsg_stats;
+
+typedef struct rcsg_program rcsg_program;
+
+/* Last error message of this thread; *step = NumericFault step index or -1. */
+const char* rcsg_last_error(int32_t* step);
+
+/* Bind the calling thread to CUDA device `device` (one process per GPU). */
+int rcsg_set_device(int32_t device);
+
+/* Compile (network, plan) into a device step program.  Deep-copies the
+ * descriptors (the plan stays immutable, contraction_plan.hpp:17-18).
+ * `mem_budget_bytes` bounds the device arena (0 = 70% of free memory).
+ * Replaces: the per-call interpretation of the plan in contract()
+ * (contraction_engine.cpp:153-208). */
+int rcsg_compile(const rcsg_network_desc* net, const rcsg_plan_desc* plan, int32_t precision,
+                 uint64_t mem_budget_bytes, rcsg_program** out);
+int rcsg_program_free(rcsg_program* prog);
+
+/* Amplitudes of n_groups candidate groups: for each group g,
+ *   sum over configs (compensated, list order) of
+ *   sum over slices s in [slice_begin, slice_end) (ascending)
+ * of the plan executed under (group_fixed[g], slice s, config).
+ * n_configs == 0: exact contraction (the plan must have no broken edges).
+ * out_amps: HOST [n_groups][2^l] interleaved float64.
+ * Replaces: contract_group (contraction_engine.cpp:307-325) and contract()
+ * with fixed_outputs (:210-305), batched over groups. */
+int rcsg_contract_groups(rcsg_program* prog, uint64_t n_groups, const uint64_t* group_fixed,
+                         uint64_t n_configs, const uint64_t* configs, uint64_t slice_begin,
+                         uint64_t slice_end, double* out_amps, rcsg_stats* stats);
+
+/* Same, but accumulates (+=) into a DEVICE buffer d_acc [n_groups][2^l]
+ * interleaved float64 on the program's stream, without host synchronisation
+ * when `sync` == 0.  Used by the slice scheduler (one call per rank shard)
+ * before the cross-GPU reduction. */
+int rcsg_contract_groups_device(rcsg_program* prog, uint64_t n_groups,
+                                const uint64_t* group_fixed, uint64_t n_configs,
+                                const uint64_t* configs, uint64_t slice_begin,
+                                uint64_t slice_end, double* d_acc, int32_t sync,
+                                rcsg_stats* stats);
+
+/* Compile with explicit pins instead of group variants: pinned[label] in {0,1}
+ * fixes a label for every execution (-1 = not pinned); sliced / broken labels
+ * still come from the pass.  Every non-open output must be pinned, otherwise
+ * RCSG_ERR_CONFIG ("assignment incomplete").  Run it with one group (fixed
+ * bits ignored).  Serves contract() with arbitrary fixed_outputs
+ * (contraction_engine.cpp:210-305). */
+int rcsg_compile_pinned(const rcsg_network_desc* net, const rcsg_plan_desc* plan, int32_t precision,
+                        uint64_t mem_budget_bytes, const int8_t* pinned, rcsg_program** out);
+
+/* execute_assignment (contraction_engine.cpp:153-208): every label with
+ * assign[label] in {0,1} pinned, -1 free.  out: host, 2^(#free) complex in
+ * canonical open-qubit order; *n_out = count.  Free labels must be open outputs. */
+int rcsg_execute_assignment(const rcsg_network_desc* net, const rcsg_plan_desc* plan,
+                            int32_t precision, const int8_t* assign, double* out,
+                            uint64_t* n_out);
+
+/* ---- post-processing (sampling.cpp) on device amplitudes ------------------ */
+
+/* Candidate-set description (CandidateSet, sampling.hpp:17-31). */
+typedef struct rcsg_candidates {
+    int32_t n_qubits;
+    int32_t l;
+    const int32_t* open_qubits; /* [l] ascending */
+    uint64_t n_groups;
+    const uint64_t* group_fixed; /* HOST [n_groups] */
+} rcsg_candidates;
+
+/* top_k_select (sampling.cpp:82-114): global top-k of |a|^2 over all
+ * n_groups*2^l candidates, ordered by (prob desc, lexicographic asc).
+ * d_amps: DEVICE [n_groups][2^l] interleaved float64.  out: HOST k indices. */
+int rcsg_topk(const rcsg_candidates* cs, const double* d_amps, uint64_t k, uint64_t* out);
+
+/* Same selection from DEVICE probabilities [n_groups][2^l] (the reference's
+ * ProbFn values), bit-exact with top_k_select on identical inputs. */
+int rcsg_topk_probs(const rcsg_candidates* cs, const double* d_probs, uint64_t k, uint64_t* out);
+
+/* direct_sample (sampling.cpp:116-145): one inverse-CDF draw per group with the
+ * counter-based SplitMix64 stream of rng_seed.  out: HOST [n_groups]. */
+int rcsg_direct_sample(const rcsg_candidates* cs, const double* d_amps, uint64_t rng_seed,
+                       uint64_t* out);
+
+int rcsg_direct_sample_probs(const rcsg_candidates* cs, const double* d_probs, uint64_t rng_seed,
+                             uint64_t* out);
+
+/* xeb (sampling.cpp:62-73): (2^n / count) * sum q - 1 over HOST q[count]. */
+int rcsg_xeb(int32_t n_qubits, uint64_t count, const double* q, double* out);
+
+/* Device buffers for the post-processing entry points (thin cudaMalloc wrappers
+ * so FFI callers need no CUDA runtime of their own). */
+int rcsg_device_alloc(uint64_t bytes, void** out);
+int rcsg_device_free(void* p);
+int rcsg_memcpy(void* dst, const void* src, uint64_t bytes, int32_t kind /*1 H2D, 2 D2H, 3 D2D*/);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

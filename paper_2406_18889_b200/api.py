@@ -1,0 +1,415 @@
+"""Python mirror of the reference's hot-path API (namespace ``rcs``), over the C ABI.
+
+Names, argument meaning and errors follow the reference
+(/root/reference/proj/include/rcs/{contraction_engine,sampling}.hpp):
+``contract``, ``contract_group``, ``execute_assignment``, ``build_candidate_set``,
+``top_k_select``, ``direct_sample``, ``xeb``; ``ConfigError`` / ``NumericFault`` /
+``CapacityError`` carry the reference's exit codes 2 / 3 / 4.  The pipeline
+inputs (circuit, network, plan) are built by the library's C++ host code,
+which reproduces the reference planner bit for bit.  Every contraction and
+selection runs on the GPU; nothing here computes amplitudes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from ._native import (PRECISIONS, rcsg_candidates, rcsg_network_desc, rcsg_plan_desc,
+                      rcsg_stats)
+
+
+class Error(RuntimeError):
+    exit_code = 1
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.msg = msg
+
+
+class ConfigError(Error):
+    exit_code = 2
+
+
+class NumericFault(Error):
+    exit_code = 3
+
+    def __init__(self, msg: str, step_index: int):
+        super().__init__(msg)
+        self.step_index = step_index
+
+
+class CapacityError(Error):
+    exit_code = 4
+
+
+class DeviceError(Error):
+    exit_code = 5
+
+
+def _raise(rc: int, msg: str, step: int):
+    if rc == _native.RCSG_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == _native.RCSG_ERR_NUMERIC:
+        raise NumericFault(msg, step)
+    if rc == _native.RCSG_ERR_CAPACITY:
+        raise CapacityError(msg)
+    raise DeviceError(msg)
+
+
+def _check_h(rc: int):
+    if rc:
+        step = C.c_int(-1)
+        msg = _native.lib().rcsh_last_error(C.byref(step)).decode()
+        _raise(rc, msg, step.value)
+
+
+def _check_g(rc: int):
+    if rc:
+        step = C.c_int32(-1)
+        msg = _native.lib().rcsg_last_error(C.byref(step)).decode()
+        _raise(rc, msg, step.value)
+
+
+def _p(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+def _u64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
+
+
+EFFORT = {"low": 0, "medium": 1, "high": 2}
+
+
+def _prec(p) -> int:
+    if isinstance(p, str):
+        if p not in PRECISIONS:
+            raise ConfigError("precision must be f64, f32, tf32 or 3xtf32")
+        return PRECISIONS[p]
+    return int(p)
+
+
+@dataclass
+class Problem:
+    """circuit -> network(open) -> broken edges -> plan -> configs, built by the C++ host code.
+
+    Mirrors the reference pipeline used by contract_group callers
+    (harness.cpp:131-152 with open = the group's open qubits).
+    """
+
+    n: int
+    cycles: int
+    topology: str
+    seed: int
+    open: list
+    budget: int
+    effort: str = "low"
+    k_broken: int = 0
+    m: int = 1
+    handle: int = 0
+    net: dict = field(default_factory=dict)
+    plan: dict = field(default_factory=dict)
+
+    def build(self):
+        h = C.c_void_p()
+        op = _i32(self.open)
+        _check_h(_native.lib().rcsh_build(self.n, self.cycles, self.topology.encode(),
+                                          C.c_uint64(self.seed), _p(op, C.c_int), len(self.open),
+                                          C.c_uint64(self.budget), EFFORT[self.effort], self.k_broken,
+                                          C.c_uint64(self.m), C.byref(h)))
+        self.handle = h
+        self._export()
+        return self
+
+    @classmethod
+    def from_network(cls, leaf_rank, leaf_labels, leaf_data, names, n_qubits, output_labels,
+                     open_labels, open_qubits, budget=1 << 30, effort="medium", seed=0, broken=()):
+        """find_contraction_path over a hand-built TensorNetwork (tensor_network.hpp:26-43)."""
+        self = cls(n=n_qubits, cycles=0, topology="custom", seed=seed, open=list(open_qubits),
+                   budget=budget, effort=effort)
+        h = C.c_void_p()
+        rk, lb = _i32(leaf_rank), _i32(leaf_labels)
+        data = np.ascontiguousarray(np.asarray(leaf_data, np.complex128)).view(np.float64)
+        ol, opl, opq, br = _i32(output_labels), _i32(open_labels or [0]), _i32(open_qubits or [0]), _i32(list(broken) or [0])
+        _check_h(_native.lib().rcsh_build_network(
+            len(rk), _p(rk, C.c_int), _p(lb, C.c_int), _p(data, C.c_double), "\n".join(names).encode(),
+            n_qubits, _p(ol, C.c_int), len(open_labels), _p(opl, C.c_int), _p(opq, C.c_int),
+            C.c_uint64(budget), EFFORT[effort], C.c_uint64(seed), len(broken), _p(br, C.c_int),
+            C.byref(h)))
+        self.handle = h
+        self._export()
+        return self
+
+    def __del__(self):
+        if self.handle and _native._lib is not None:
+            _native._lib.rcsh_free(self.handle)
+            self.handle = 0
+
+    def _export(self):
+        L = _native.lib()
+        sz = np.zeros(8, np.int64)
+        L.rcsh_net_sizes(self.handle, _p(sz, C.c_int64))
+        n_leaves, n_labels, n_q, n_open, sum_rank, sum_amps, n_layers, n_edges = map(int, sz)
+        rank = np.zeros(n_leaves, np.int32)
+        labels = np.zeros(max(sum_rank, 1), np.int32)
+        data = np.zeros(2 * sum_amps, np.float64)
+        out_l = np.zeros(max(n_q, 1), np.int32)
+        open_l = np.zeros(max(n_open, 1), np.int32)
+        open_q = np.zeros(max(n_open, 1), np.int32)
+        L.rcsh_net_export(self.handle, _p(rank, C.c_int), _p(labels, C.c_int), _p(data, C.c_double),
+                          _p(out_l, C.c_int), _p(open_l, C.c_int), _p(open_q, C.c_int))
+        nbytes = L.rcsh_label_names(self.handle, None, 0)
+        buf = C.create_string_buffer(int(nbytes) + 1)
+        L.rcsh_label_names(self.handle, buf, nbytes + 1)
+        names = buf.value.decode().split("\n")[:-1]
+        edges = np.zeros(3 * max(n_edges, 1), np.int32)
+        L.rcsh_wire_edges(self.handle, _p(edges, C.c_int))
+        self.net = dict(leaf_rank=rank, leaf_labels=labels[:sum_rank], leaf_data=data,
+                        n_labels=n_labels, n_qubits=n_q, output_labels=out_l[:n_q],
+                        open_labels=open_l[:n_open], open_qubits=open_q[:n_open], label_names=names,
+                        n_layers=n_layers, wire_edges=edges[:3 * n_edges].reshape(-1, 3))
+        ps = np.zeros(5, np.int64)
+        L.rcsh_plan_sizes(self.handle, _p(ps, C.c_int64))
+        n_steps, n_sl, n_br, n_fx, n_cfg = map(int, ps)
+        steps = np.zeros((max(n_steps, 1), 6), np.int64)
+        sl = np.zeros(max(n_sl, 1), np.int32)
+        br = np.zeros(max(n_br, 1), np.int32)
+        fx = np.zeros(max(n_fx, 1), np.int32)
+        cf = np.zeros(max(n_cfg, 1), np.uint64)
+        tot = np.zeros(4, np.uint64)
+        L.rcsh_plan_export(self.handle, _p(steps, C.c_int64), _p(sl, C.c_int), _p(br, C.c_int),
+                           _p(fx, C.c_int), _p(cf, C.c_uint64), _p(tot, C.c_uint64))
+        self.plan = dict(steps=steps[:n_steps], sliced=sl[:n_sl], broken=br[:n_br],
+                         fixed_outputs=fx[:n_fx], configs=cf[:n_cfg],
+                         flops_per_slice=int(tot[0]), traffic_bytes_per_slice=int(tot[1]),
+                         peak_bytes=int(tot[2]), memory_budget_bytes=int(tot[3]))
+
+    @property
+    def n_open(self) -> int:
+        return len(self.net["open_labels"])
+
+    @property
+    def n_slices(self) -> int:
+        return 1 << len(self.plan["sliced"])
+
+    def gates(self) -> np.ndarray:
+        n = _native.lib().rcsh_circuit_gates(self.handle, None)
+        out = np.zeros(4 * max(n, 1), np.int32)
+        _native.lib().rcsh_circuit_gates(self.handle, _p(out, C.c_int))
+        return out[:4 * n].reshape(-1, 4)
+
+    # ---- hot path ---------------------------------------------------------
+    def contract_groups(self, fixed, precision="f64", configs="all", slices=None, budget=0,
+                        stats: rcsg_stats | None = None) -> np.ndarray:
+        """Amplitudes [G][2^l] of every group (rcsg_contract_groups).
+
+        configs: "all" -> the plan's BrokenEdgeConfig; None -> exact; list -> those bits.
+        slices: (begin, end) slice range, default all.
+        """
+        fixed = _u64(fixed)
+        s0, s1 = slices if slices is not None else (0, self.n_slices)
+        if isinstance(configs, str):
+            n_cfg, cf = -1, _u64([0])
+        elif configs is None:
+            n_cfg, cf = 0, _u64([0])
+        else:
+            cf = _u64(configs)
+            n_cfg = len(cf)
+        out = np.zeros(2 * (len(fixed) << self.n_open), np.float64)
+        st = stats if stats is not None else rcsg_stats()
+        _check_h(_native.lib().rcsh_contract_groups(
+            self.handle, _prec(precision), C.c_uint64(budget), C.c_uint64(len(fixed)),
+            _p(fixed, C.c_uint64), n_cfg, _p(cf, C.c_uint64), C.c_uint64(s0), C.c_uint64(s1),
+            _p(out, C.c_double), C.byref(st)))
+        return out.view(np.complex128).reshape(len(fixed), -1)
+
+    def contract_groups_device(self, fixed, d_acc: int, precision="tf32", configs="all",
+                               slices=None, budget=0, stats: rcsg_stats | None = None):
+        """Accumulate into a DEVICE float64 buffer (e.g. a torch tensor's data_ptr())."""
+        fixed = _u64(fixed)
+        s0, s1 = slices if slices is not None else (0, self.n_slices)
+        if isinstance(configs, str):
+            n_cfg, cf = -1, _u64([0])
+        elif configs is None:
+            n_cfg, cf = 0, _u64([0])
+        else:
+            cf = _u64(configs)
+            n_cfg = len(cf)
+        st = stats if stats is not None else rcsg_stats()
+        _check_h(_native.lib().rcsh_contract_groups_device(
+            self.handle, _prec(precision), C.c_uint64(budget), C.c_uint64(len(fixed)),
+            _p(fixed, C.c_uint64), n_cfg, _p(cf, C.c_uint64), C.c_uint64(s0), C.c_uint64(s1),
+            C.c_void_p(d_acc), C.byref(st)))
+        return st
+
+    def contract_group(self, fixed_bits: int, precision="f64") -> np.ndarray:
+        """contract_group (contraction_engine.cpp:307-325)."""
+        return self.contract_groups([fixed_bits], precision=precision)[0]
+
+    def contract(self, fixed: dict | None = None, configs=None, precision="f64"):
+        """contract (contraction_engine.cpp:210-305) -> (amplitudes, flops)."""
+        fixed = fixed or {}
+        fl = _i32(list(fixed.keys()) or [0])
+        fv = _i32(list(fixed.values()) or [0])
+        n_cfg = 0 if configs is None else (-1 if isinstance(configs, str) else len(configs))
+        cf = _u64([0] if configs is None or isinstance(configs, str) else configs)
+        n_free = sum(1 for l in self.net["open_labels"] if int(l) not in fixed)
+        out = np.zeros(2 << n_free, np.float64)
+        flops = C.c_uint64()
+        _check_h(_native.lib().rcsh_contract(self.handle, _prec(precision), len(fixed), _p(fl, C.c_int),
+                                             _p(fv, C.c_int), n_cfg, _p(cf, C.c_uint64),
+                                             _p(out, C.c_double), C.byref(flops)))
+        return out.view(np.complex128), flops.value
+
+    def execute(self, assignment: dict, precision="f64") -> np.ndarray:
+        """execute_assignment (contraction_engine.cpp:153-208)."""
+        ls = _i32(list(assignment.keys()) or [0])
+        vs = _i32(list(assignment.values()) or [0])
+        n = C.c_int64()
+        _check_h(_native.lib().rcsh_execute(self.handle, _prec(precision), len(assignment),
+                                            _p(ls, C.c_int), _p(vs, C.c_int), None, C.byref(n)))
+        out = np.zeros(2 * n.value, np.float64)
+        _check_h(_native.lib().rcsh_execute(self.handle, _prec(precision), len(assignment),
+                                            _p(ls, C.c_int), _p(vs, C.c_int), _p(out, C.c_double),
+                                            C.byref(n)))
+        return out.view(np.complex128)
+
+    def assignment_gsc(self, fixed_bits: int, slice_idx: int, config_bits: int = 0) -> dict:
+        """The assignment contract()/contract_group() build for (group, slice, config)
+        (contraction_engine.cpp:242-248, 310-318)."""
+        a = {}
+        open_q = set(int(q) for q in self.net["open_qubits"])
+        b = 0
+        for q in range(self.net["n_qubits"]):
+            if q in open_q:
+                continue
+            a[int(self.net["output_labels"][q])] = (fixed_bits >> b) & 1
+            b += 1
+        for i, l in enumerate(self.plan["broken"]):
+            a[int(l)] = (config_bits >> i) & 1
+        for i, l in enumerate(self.plan["sliced"]):
+            a[int(l)] = (slice_idx >> i) & 1
+        return a
+
+
+# ---- descriptor-level entry (hand-built networks, KATs) --------------------
+def execute_desc(net: dict, steps, assign, precision="f64") -> np.ndarray:
+    """rcsg_execute_assignment on raw arrays: net = dict(leaf_rank, leaf_labels, leaf_data
+    (complex), n_labels, n_qubits, output_labels, open_labels, open_qubits); steps = [(l, r, res)]."""
+    rk, lb = _i32(net["leaf_rank"]), _i32(list(net["leaf_labels"]) or [0])
+    data = np.ascontiguousarray(np.asarray(net["leaf_data"], np.complex128)).view(np.float64)
+    ol = _i32(list(net["output_labels"]) or [0])
+    opl, opq = _i32(list(net["open_labels"]) or [0]), _i32(list(net["open_qubits"]) or [0])
+    st = _i32(np.asarray(steps, np.int32).reshape(-1)[:].tolist() or [0])
+    nd = rcsg_network_desc(len(rk), _p(rk, C.c_int32), _p(lb, C.c_int32), _p(data, C.c_double),
+                           int(net["n_labels"]), int(net["n_qubits"]), _p(ol, C.c_int32),
+                           len(net["open_labels"]), _p(opl, C.c_int32), _p(opq, C.c_int32))
+    z = _i32([0])
+    pd = rcsg_plan_desc(len(steps), _p(st, C.c_int32), 0, _p(z, C.c_int32), 0, _p(z, C.c_int32), 0,
+                        _p(z, C.c_int32))
+    a = np.ascontiguousarray(np.asarray(assign, np.int8))
+    n = C.c_uint64()
+    _check_g(_native.lib().rcsg_execute_assignment(C.byref(nd), C.byref(pd), _prec(precision),
+                                                   _p(a, C.c_int8), None, C.byref(n)))
+    out = np.zeros(2 * n.value, np.float64)
+    _check_g(_native.lib().rcsg_execute_assignment(C.byref(nd), C.byref(pd), _prec(precision),
+                                                   _p(a, C.c_int8), _p(out, C.c_double), C.byref(n)))
+    return out.view(np.complex128)
+
+
+# ---- sampler ---------------------------------------------------------------
+def build_candidate_set(n: int, open_qubits, n_groups: int, seed: int):
+    """build_candidate_set (sampling.cpp:29-60) -> (group_fixed, duplicate_groups)."""
+    op = _i32(sorted(open_qubits) or [0])
+    out = np.zeros(max(n_groups, 1), np.uint64)
+    dup = C.c_int()
+    _check_h(_native.lib().rcsh_candidates(n, _p(op, C.c_int), len(open_qubits), C.c_uint64(n_groups),
+                                           C.c_uint64(seed), _p(out, C.c_uint64), C.byref(dup)))
+    return out, dup.value
+
+
+def member(n: int, open_qubits, fixed: int, i: int) -> int:
+    op = _i32(sorted(open_qubits) or [0])
+    return int(_native.lib().rcsh_member(n, _p(op, C.c_int), len(open_qubits), C.c_uint64(fixed),
+                                         C.c_uint64(i)))
+
+
+def top_k_select(n, open_qubits, fixed, probs, k) -> np.ndarray:
+    """top_k_select with probs [G][2^l] as the ProbFn (GPU selection)."""
+    op = _i32(sorted(open_qubits) or [0])
+    fixed = _u64(fixed)
+    probs = np.ascontiguousarray(probs, np.float64)
+    out = np.zeros(max(int(k), 1), np.uint64)
+    _check_h(_native.lib().rcsh_topk(n, _p(op, C.c_int), len(open_qubits), C.c_uint64(len(fixed)),
+                                     _p(fixed, C.c_uint64), _p(probs, C.c_double), C.c_uint64(k),
+                                     _p(out, C.c_uint64)))
+    return out[:k]
+
+
+def direct_sample(n, open_qubits, fixed, probs, seed) -> np.ndarray:
+    """direct_sample with probs [G][2^l] as the ProbFn (GPU sampling)."""
+    op = _i32(sorted(open_qubits) or [0])
+    fixed = _u64(fixed)
+    probs = np.ascontiguousarray(probs, np.float64)
+    out = np.zeros(len(fixed), np.uint64)
+    _check_h(_native.lib().rcsh_direct(n, _p(op, C.c_int), len(open_qubits), C.c_uint64(len(fixed)),
+                                       _p(fixed, C.c_uint64), _p(probs, C.c_double),
+                                       C.c_uint64(seed), _p(out, C.c_uint64)))
+    return out
+
+
+def _cands(n, open_qubits, fixed):
+    op = _i32(sorted(open_qubits) or [0])
+    fx = _u64(fixed)
+    cs = rcsg_candidates(n, len(open_qubits), _p(op, C.c_int32), len(fx), _p(fx, C.c_uint64))
+    return cs, (op, fx)
+
+
+def top_k_from_device_amps(n, open_qubits, fixed, d_amps: int, k: int) -> np.ndarray:
+    """Fused |a|^2 + global top-k on DEVICE amplitudes [G][2^l] (rcsg_topk)."""
+    cs, keep = _cands(n, open_qubits, fixed)
+    out = np.zeros(k, np.uint64)
+    _check_g(_native.lib().rcsg_topk(C.byref(cs), C.c_void_p(d_amps), C.c_uint64(k), _p(out, C.c_uint64)))
+    return out
+
+
+def direct_from_device_amps(n, open_qubits, fixed, d_amps: int, seed: int) -> np.ndarray:
+    cs, keep = _cands(n, open_qubits, fixed)
+    out = np.zeros(len(keep[1]), np.uint64)
+    _check_g(_native.lib().rcsg_direct_sample(C.byref(cs), C.c_void_p(d_amps), C.c_uint64(seed),
+                                              _p(out, C.c_uint64)))
+    return out
+
+
+def xeb(n: int, q) -> float:
+    """xeb (sampling.cpp:62-73) over the ideal probabilities q of the samples."""
+    q = np.ascontiguousarray(q, np.float64)
+    out = C.c_double()
+    _check_g(_native.lib().rcsg_xeb(n, C.c_uint64(len(q)), _p(q, C.c_double), C.byref(out)))
+    return out.value
+
+
+def split_next(seed: int, tag: int) -> int:
+    """Rng(seed).split(tag).next_u64() (rng.hpp:36-41)."""
+    return int(_native.lib().rcsh_rng_split_next(C.c_uint64(seed), C.c_uint64(tag)))
+
+
+def lexkey(index: int, n: int) -> int:
+    return int(_native.lib().rcsh_lexkey(C.c_uint64(index), n))
+
+
+def broken_configs(k: int, m: int, seed: int) -> np.ndarray:
+    out = np.zeros(max(m, 1), np.uint64)
+    _check_h(_native.lib().rcsh_broken_configs(k, C.c_uint64(m), C.c_uint64(seed), _p(out, C.c_uint64)))
+    return out[:m]
+
+
+def set_device(device: int):
+    _check_g(_native.lib().rcsg_set_device(device))

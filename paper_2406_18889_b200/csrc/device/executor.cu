@@ -1,0 +1,653 @@
+// Step-program executor; see executor.hpp for the design.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "executor.hpp"
+
+namespace rcsg {
+
+#define CUDA_OK(x)                                                                      \
+    do {                                                                                \
+        cudaError_t e_ = (x);                                                           \
+        if (e_ != cudaSuccess)                                                          \
+            throw Failure{RCSG_ERR_DEVICE, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                               " at " #x};                              \
+    } while (0)
+
+namespace {
+
+constexpr int64_t kAlign = 64;  // elements; keeps every plane 256-B aligned
+
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// First-fit allocator simulation (offsets in elements).
+struct FirstFit {
+    std::map<int64_t, int64_t> free_;  // offset -> size
+    int64_t top = 0, peak = 0;
+    int64_t alloc(int64_t size) {
+        size = align_up(std::max<int64_t>(size, 1));
+        for (auto it = free_.begin(); it != free_.end(); ++it)
+            if (it->second >= size) {
+                const int64_t off = it->first, rem = it->second - size;
+                free_.erase(it);
+                if (rem) free_[off + size] = rem;
+                return off;
+            }
+        // extend the top (merging a trailing free block)
+        int64_t off = top;
+        if (!free_.empty()) {
+            auto last = std::prev(free_.end());
+            if (last->first + last->second == top) {
+                off = last->first;
+                free_.erase(last);
+            }
+        }
+        top = off + size;
+        peak = std::max(peak, top);
+        return off;
+    }
+    void release(int64_t off, int64_t size) {
+        size = align_up(std::max<int64_t>(size, 1));
+        auto it = free_.emplace(off, size).first;
+        auto nx = std::next(it);
+        if (nx != free_.end() && it->first + it->second == nx->first) {
+            it->second += nx->second;
+            free_.erase(nx);
+        }
+        if (it != free_.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second == it->first) {
+                pv->second += it->second;
+                free_.erase(it);
+                it = pv;
+            }
+        }
+        if (it->first + it->second == top) {
+            top = it->first;
+            free_.erase(it);
+        }
+    }
+};
+
+int64_t pos_in(const std::vector<int>& v, int x) {
+    for (size_t i = 0; i < v.size(); ++i)
+        if (v[i] == x) return static_cast<int64_t>(i);
+    return -1;
+}
+
+// src_bit for permuting layout `from` into layout `to` (both MSB-first label lists)
+void permute_bits(const std::vector<int>& from, const std::vector<int>& to, std::vector<int>& src_bit) {
+    const int r = static_cast<int>(to.size());
+    src_bit.assign(r, 0);
+    for (int q = 0; q < r; ++q) {
+        const int label = to[r - 1 - q];
+        src_bit[q] = r - 1 - static_cast<int>(pos_in(from, label));
+    }
+}
+
+}  // namespace
+
+Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
+                 const std::vector<LabelRole>& roles, int precision, uint64_t mem_budget)
+    : precision_(precision), mem_budget_(mem_budget), roles_(roles) {
+    if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_3XTF32)
+        throw Failure{RCSG_ERR_CONFIG, "unknown precision"};
+    elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : 4;
+    build_nodes(net, plan);
+    build_steps();
+    CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    // leaf data + pass sources + canonical map
+    CUDA_OK(cudaMalloc(&d_leaf_data_, std::max<size_t>(leaf_data_.size(), 2) * sizeof(double)));
+    CUDA_OK(cudaMemcpy(d_leaf_data_, leaf_data_.data(), leaf_data_.size() * sizeof(double),
+                       cudaMemcpyHostToDevice));
+    std::vector<PassSrc> src(roles_.size());
+    for (size_t l = 0; l < roles_.size(); ++l) src[l] = roles_[l].src;
+    CUDA_OK(cudaMalloc(&d_pass_src_, std::max<size_t>(src.size(), 1) * sizeof(PassSrc)));
+    CUDA_OK(cudaMemcpy(d_pass_src_, src.data(), src.size() * sizeof(PassSrc), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMalloc(&d_state_, sizeof(PassState)));
+    CUDA_OK(cudaMemset(d_state_, 0, sizeof(PassState)));
+    CUDA_OK(cudaMalloc(&d_canon_, std::max<size_t>(root_canon_src_.size(), 1) * sizeof(int32_t)));
+    CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMalloc(&d_fault_, sizeof(int32_t)));
+}
+
+Program::~Program() {
+    free_chunks();
+    cudaFree(arena_);
+    cudaFree(d_leaf_data_);
+    cudaFree(d_pass_src_);
+    cudaFree(d_state_);
+    cudaFree(d_canon_);
+    cudaFree(d_fault_);
+    cudaFree(d_part_);
+    cudaFree(d_res_);
+    cudaFree(d_comp_);
+    for (auto* p : d_static_jobs_) cudaFree(p);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan) {
+    n_leaves_ = net.n_leaves;
+    const int n_nodes = net.n_leaves + plan.n_steps;
+    if (net.n_leaves < 1) throw Failure{RCSG_ERR_CONFIG, "network has no tensors"};
+    if (static_cast<int>(roles_.size()) != net.n_labels)
+        throw Failure{RCSG_ERR_CONFIG, "label role table does not match the network"};
+    nodes_.assign(n_nodes, NodeInfo{});
+    canon_qubit_.assign(net.n_labels, -1);
+    for (int j = 0; j < net.n_open; ++j) canon_qubit_[net.open_labels[j]] = net.open_qubits[j];
+    // leaves: project away pinned labels (reference project_leaf keeps free labels in order)
+    int64_t lo = 0, doff = 0;
+    for (int i = 0; i < net.n_leaves; ++i) {
+        NodeInfo& nd = nodes_[i];
+        nd.is_leaf = true;
+        nd.rank0 = net.leaf_rank[i];
+        if (nd.rank0 > kMaxLeafRank) throw Failure{RCSG_ERR_CONFIG, "leaf tensor rank above 8 is unsupported"};
+        nd.data_off = doff;
+        bool pass = false;
+        for (int p = 0; p < nd.rank0; ++p) {
+            const int l = net.leaf_labels[lo + p];
+            if (l < 0 || l >= net.n_labels) throw Failure{RCSG_ERR_CONFIG, "leaf label out of range"};
+            nd.labels0.push_back(l);
+            const LabelRole& rl = roles_[l];
+            if (rl.role == kFree) nd.labels.push_back(l);
+            else if (rl.role == kPass) pass = true;
+            else nd.var_mask |= uint64_t{1} << rl.var_bit;
+        }
+        nd.level = nd.var_mask ? 2 : (pass ? 1 : 0);
+        nd.payload = int64_t{1} << nd.labels.size();
+        lo += nd.rank0;
+        doff += int64_t{1} << nd.rank0;
+    }
+    leaf_data_.assign(net.leaf_data, net.leaf_data + 2 * doff);
+    // internal nodes: result of each step (post-order)
+    std::vector<char> made(n_nodes, 0), used(n_nodes, 0);
+    for (int i = 0; i < net.n_leaves; ++i) made[i] = 1;
+    steps_.clear();
+    plan_flops_ = 0;
+    for (int s = 0; s < plan.n_steps; ++s) {
+        const int a = plan.steps[3 * s], b = plan.steps[3 * s + 1], r = plan.steps[3 * s + 2];
+        if (a < 0 || b < 0 || r < 0 || a >= n_nodes || b >= n_nodes || r >= n_nodes || a == b ||
+            !made[a] || !made[b] || used[a] || used[b] || made[r])
+            throw Failure{RCSG_ERR_CONFIG, "malformed contraction plan at step " + std::to_string(s)};
+        used[a] = used[b] = 1;
+        made[r] = 1;
+        const NodeInfo &na = nodes_[a], &nb = nodes_[b];
+        NodeInfo& nr = nodes_[r];
+        nr.var_mask = na.var_mask | nb.var_mask;
+        nr.level = std::max(na.level, nb.level);
+        StepInfo st;
+        st.plan_index = s;
+        st.a = a;
+        st.b = b;
+        st.r = r;
+        st.level = nr.level;
+        nodes_[a].consumer = s;
+        nodes_[b].consumer = s;
+        steps_.push_back(st);
+        // result layout is decided in build_steps (needs operand roles)
+        nr.labels.clear();
+    }
+    root_ = plan.n_steps ? plan.steps[3 * (plan.n_steps - 1) + 2] : 0;
+    if (plan.n_steps == 0 && net.n_leaves != 1)
+        throw Failure{RCSG_ERR_CONFIG, "plan has no steps but the network has several tensors"};
+    for (int i = 0; i < n_nodes; ++i)
+        if (i != root_ && made[i] && !used[i])
+            throw Failure{RCSG_ERR_CONFIG, "plan leaves node " + std::to_string(i) + " unconsumed"};
+}
+
+void Program::build_steps() {
+    for (StepInfo& st : steps_) {
+        NodeInfo* A = &nodes_[st.a];
+        NodeInfo* B = &nodes_[st.b];
+        const bool va = A->level == 2, vb = B->level == 2;
+        int shared_n = 0;
+        for (int l : A->labels) shared_n += pos_in(B->labels, l) >= 0;
+        const int ka = static_cast<int>(A->labels.size()) - shared_n;
+        const int kb = static_cast<int>(B->labels.size()) - shared_n;
+        bool swap = false;
+        if (vb && !va) swap = true;
+        else if (!va && !vb && kb > ka) swap = true;
+        if (swap) {
+            std::swap(st.a, st.b);
+            std::swap(A, B);
+        }
+        st.mode = (A->level == 2) ? ((B->level == 2) ? 2 : 1) : 0;
+        std::vector<int> shared, keep_a, keep_b;
+        for (int l : A->labels) (pos_in(B->labels, l) >= 0 ? shared : keep_a).push_back(l);
+        for (int l : B->labels)
+            if (pos_in(shared, l) < 0) keep_b.push_back(l);
+        // shared order: reuse an operand's existing suffix when possible
+        auto suffix_is_shared = [&](const std::vector<int>& lab) {
+            const size_t s = shared.size();
+            for (size_t i = lab.size() - s; i < lab.size(); ++i)
+                if (pos_in(shared, lab[i]) < 0) return false;
+            return true;
+        };
+        std::vector<int> sh_order = shared;
+        if (!shared.empty()) {
+            if (suffix_is_shared(A->labels))
+                sh_order.assign(A->labels.end() - shared.size(), A->labels.end());
+            else if (suffix_is_shared(B->labels))
+                sh_order.assign(B->labels.end() - shared.size(), B->labels.end());
+        }
+        std::vector<int> ta = keep_a, tb = keep_b;
+        ta.insert(ta.end(), sh_order.begin(), sh_order.end());
+        tb.insert(tb.end(), sh_order.begin(), sh_order.end());
+        std::vector<int> bits;
+        st.perm_a = ta != A->labels;
+        if (st.perm_a) {
+            permute_bits(A->labels, ta, bits);
+            st.pa = make_permute(static_cast<int>(ta.size()), bits.data());
+        }
+        st.perm_b = tb != B->labels;
+        if (st.perm_b) {
+            permute_bits(B->labels, tb, bits);
+            st.pb = make_permute(static_cast<int>(tb.size()), bits.data());
+        }
+        st.m = int64_t{1} << keep_a.size();
+        st.n = int64_t{1} << keep_b.size();
+        st.k = int64_t{1} << shared.size();
+        st.flops_per_variant = 8ull * st.m * st.n * st.k;
+        plan_flops_ += st.flops_per_variant;
+        NodeInfo& R = nodes_[st.r];
+        R.labels = keep_a;
+        R.labels.insert(R.labels.end(), keep_b.begin(), keep_b.end());
+        if (R.labels.size() > static_cast<size_t>(kMaxRank))
+            throw Failure{RCSG_ERR_CAPACITY, "intermediate rank exceeds the executor limit"};
+        R.payload = int64_t{1} << R.labels.size();
+    }
+    // canonical output order of the root: bit j <-> j-th smallest open qubit
+    // among the root's labels (contraction_engine.cpp:193-207)
+    const NodeInfo& root = nodes_[root_];
+    out_rank_ = static_cast<int>(root.labels.size());
+    std::vector<std::pair<int, int>> q_pos;  // (qubit, layout position)
+    for (int p = 0; p < out_rank_; ++p) {
+        const int q = canon_qubit_[root.labels[p]];
+        if (q < 0)
+            throw Failure{RCSG_ERR_CONFIG, "free label " + std::to_string(root.labels[p]) +
+                                               " is not an open output; assignment incomplete"};
+        q_pos.push_back({q, p});
+    }
+    std::sort(q_pos.begin(), q_pos.end());
+    root_canon_src_.assign(out_rank_, 0);
+    for (int j = 0; j < out_rank_; ++j) root_canon_src_[j] = out_rank_ - 1 - q_pos[j].second;
+}
+
+// Arena layout by first-fit simulation of one run's leveled schedule.
+int64_t Program::plan_arena(int64_t cap, bool assign) {
+    FirstFit ff;
+    auto var_cap = [&](const NodeInfo& nd) -> int64_t {
+        if (nd.level < 2) return 1;
+        const int bits = __builtin_popcountll(nd.var_mask);
+        return bits >= 62 ? cap : std::min<int64_t>(cap, int64_t{1} << bits);
+    };
+    auto place = [&](int id) {
+        NodeInfo& nd = nodes_[id];
+        nd.max_var = var_cap(nd);
+        nd.plane = align_up(nd.max_var * nd.payload);
+        nd.off = ff.alloc(2 * nd.plane);
+    };
+    // leaves: persistent
+    for (int i = 0; i < n_leaves_; ++i) place(i);
+    std::vector<int> persist_until_pass_end;
+    for (int level = 0; level <= 2; ++level) {
+        for (StepInfo& st : steps_) {
+            if (st.level != level) continue;
+            const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b];
+            if (st.perm_a) {
+                st.sa_plane = align_up(var_cap(A) * A.payload);
+                st.sa_off = ff.alloc(2 * st.sa_plane);
+            }
+            if (st.perm_b) {
+                st.sb_plane = align_up(var_cap(B) * B.payload);
+                st.sb_off = ff.alloc(2 * st.sb_plane);
+            }
+            place(st.r);
+            if (st.perm_a) ff.release(st.sa_off, 2 * st.sa_plane);
+            if (st.perm_b) ff.release(st.sb_off, 2 * st.sb_plane);
+            for (int op : {st.a, st.b}) {
+                NodeInfo& o = nodes_[op];
+                if (o.is_leaf) continue;
+                if (o.level == level) ff.release(o.off, 2 * o.plane);
+                else if (o.level == 1 && level == 2) persist_until_pass_end.push_back(op);
+                // level-0 operands of deeper steps persist for the whole run
+            }
+        }
+        if (level == 2) {
+            // the root is read by the finalize of every chunk
+            if (nodes_[root_].level == 2 && !nodes_[root_].is_leaf)
+                ff.release(nodes_[root_].off, 2 * nodes_[root_].plane);
+            for (int id : persist_until_pass_end) ff.release(nodes_[id].off, 2 * nodes_[id].plane);
+        }
+    }
+    (void)assign;
+    return ff.peak;
+}
+
+void Program::free_chunks() {
+    for (ChunkData& c : chunks_) {
+        cudaFree(c.d_codes);
+        cudaFree(c.d_idx);
+        cudaFree(c.d_groups);
+        cudaFree(c.d_vid);
+        cudaFree(c.d_leaf_jobs);
+    }
+    chunks_.clear();
+}
+
+void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
+    free_chunks();
+    // distinct group codes, ascending; duplicates share every variant
+    std::vector<uint64_t> uniq = groups;
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    std::map<uint64_t, std::vector<int32_t>> members;
+    for (size_t g = 0; g < groups.size(); ++g) members[groups[g]].push_back(static_cast<int32_t>(g));
+    const int64_t n_nodes = static_cast<int64_t>(nodes_.size());
+    for (size_t u0 = 0; u0 < uniq.size(); u0 += static_cast<size_t>(cap)) {
+        const size_t u1 = std::min(uniq.size(), u0 + static_cast<size_t>(cap));
+        ChunkData ch;
+        ch.codes_off.assign(n_nodes, -1);
+        ch.nvar.assign(n_nodes, 1);
+        std::vector<std::vector<uint64_t>> node_codes(n_nodes);
+        for (int64_t i = 0; i < n_nodes; ++i) {
+            const NodeInfo& nd = nodes_[i];
+            if (nd.level != 2) continue;
+            std::vector<uint64_t>& c = node_codes[i];
+            for (size_t u = u0; u < u1; ++u) c.push_back(uniq[u] & nd.var_mask);
+            std::sort(c.begin(), c.end());
+            c.erase(std::unique(c.begin(), c.end()), c.end());
+            ch.codes_off[i] = static_cast<int64_t>(ch.codes.size());
+            ch.nvar[i] = static_cast<int64_t>(c.size());
+            ch.codes.insert(ch.codes.end(), c.begin(), c.end());
+        }
+        auto find_code = [&](int node, uint64_t code) -> int32_t {
+            const auto& c = node_codes[node];
+            return static_cast<int32_t>(std::lower_bound(c.begin(), c.end(), code) - c.begin());
+        };
+        ch.ia_off.assign(steps_.size(), -1);
+        ch.ib_off.assign(steps_.size(), -1);
+        for (size_t s = 0; s < steps_.size(); ++s) {
+            const StepInfo& st = steps_[s];
+            if (st.mode != 2) continue;
+            ch.ia_off[s] = static_cast<int64_t>(ch.idx.size());
+            for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.a, c & nodes_[st.a].var_mask));
+            ch.ib_off[s] = static_cast<int64_t>(ch.idx.size());
+            for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.b, c & nodes_[st.b].var_mask));
+        }
+        for (size_t u = u0; u < u1; ++u)
+            for (int32_t g : members[uniq[u]]) {
+                ch.groups.push_back(g);
+                ch.vid.push_back(nodes_[root_].level == 2 ? find_code(root_, uniq[u] & nodes_[root_].var_mask) : 0);
+            }
+        // level-2 leaf jobs of this chunk
+        std::vector<LeafJob> jobs;
+        for (int i = 0; i < n_leaves_; ++i) {
+            const NodeInfo& nd = nodes_[i];
+            if (nd.level != 2) continue;
+            LeafJob j{};
+            j.out_off = nd.off;
+            j.out_plane = nd.plane;
+            j.data_off = nd.data_off;
+            j.rank = nd.rank0;
+            j.out_rank = static_cast<int32_t>(nd.labels.size());
+            j.n_var = static_cast<int32_t>(ch.nvar[i]);
+            j.codes_off = static_cast<int32_t>(ch.codes_off[i]);
+            for (int p = 0; p < nd.rank0; ++p) {
+                const LabelRole& rl = roles_[nd.labels0[p]];
+                j.kind[p] = rl.role;
+                j.arg[p] = static_cast<int16_t>(rl.role == kVar ? rl.var_bit : nd.labels0[p]);
+            }
+            jobs.push_back(j);
+        }
+        ch.n_leaf_jobs = static_cast<int>(jobs.size());
+        CUDA_OK(cudaMalloc(&ch.d_codes, std::max<size_t>(ch.codes.size(), 1) * sizeof(uint64_t)));
+        CUDA_OK(cudaMemcpy(ch.d_codes, ch.codes.data(), ch.codes.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMalloc(&ch.d_idx, std::max<size_t>(ch.idx.size(), 1) * sizeof(int32_t)));
+        CUDA_OK(cudaMemcpy(ch.d_idx, ch.idx.data(), ch.idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMalloc(&ch.d_groups, std::max<size_t>(ch.groups.size(), 1) * sizeof(int32_t)));
+        CUDA_OK(cudaMemcpy(ch.d_groups, ch.groups.data(), ch.groups.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMalloc(&ch.d_vid, std::max<size_t>(ch.vid.size(), 1) * sizeof(int32_t)));
+        CUDA_OK(cudaMemcpy(ch.d_vid, ch.vid.data(), ch.vid.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMalloc(&ch.d_leaf_jobs, std::max<size_t>(jobs.size(), 1) * sizeof(LeafJob)));
+        CUDA_OK(cudaMemcpy(ch.d_leaf_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), cudaMemcpyHostToDevice));
+        chunks_.push_back(std::move(ch));
+    }
+}
+
+void* Program::buf(int64_t off) const {
+    return static_cast<char*>(arena_) + off * elem_bytes_;
+}
+
+template <typename R>
+void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
+    const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b], &Rn = nodes_[st.r];
+    const int64_t va = (A.level == 2 && ch) ? ch->nvar[st.a] : 1;
+    const int64_t vb = (B.level == 2 && ch) ? ch->nvar[st.b] : 1;
+    const int64_t vr = (Rn.level == 2 && ch) ? ch->nvar[st.r] : 1;
+    const R* a_ptr = static_cast<const R*>(buf(A.off));
+    int64_t a_plane = A.plane;
+    if (st.perm_a) {
+        R* dst = static_cast<R*>(buf(st.sa_off));
+        launch_permute<R>(a_ptr, A.plane, dst, st.sa_plane, va, st.pa, stream_);
+        ++launches_;
+        a_ptr = dst;
+        a_plane = st.sa_plane;
+    }
+    const R* b_ptr = static_cast<const R*>(buf(B.off));
+    int64_t b_plane = B.plane;
+    if (st.perm_b) {
+        R* dst = static_cast<R*>(buf(st.sb_off));
+        launch_permute<R>(b_ptr, B.plane, dst, st.sb_plane, vb, st.pb, stream_);
+        ++launches_;
+        b_ptr = dst;
+        b_plane = st.sb_plane;
+    }
+    GemmArgs g{};
+    g.a = a_ptr;
+    g.a_plane = a_plane;
+    g.b = b_ptr;
+    g.b_plane = b_plane;
+    g.c = buf(Rn.off);
+    g.c_plane = Rn.plane;
+    g.k = st.k;
+    g.n = st.n;
+    g.step = st.plan_index;
+    g.fault = d_fault_;
+    if (st.mode == 2) {
+        g.m = st.m;
+        g.batch = vr;
+        g.a_batch = st.m * st.k;
+        g.b_batch = st.n * st.k;
+        g.c_batch = st.m * st.n;
+        g.ia = ch->d_idx + ch->ia_off[&st - steps_.data()];
+        g.ib = ch->d_idx + ch->ib_off[&st - steps_.data()];
+    } else {
+        g.m = st.m * va;  // mode 1: the variants fold into M
+        g.batch = 1;
+    }
+    exec_flops_ += st.flops_per_variant * static_cast<uint64_t>(vr);
+    if constexpr (sizeof(R) == 4) {
+        if (precision_ >= RCSG_PREC_TF32 && gemm_tc_supported(g)) {
+            launch_gemm_tc(g, precision_ == RCSG_PREC_3XTF32 ? 3 : 1, stream_);
+            ++launches_;
+            return;
+        }
+    }
+    launch_gemm_simt<R>(g, stream_);
+    ++launches_;
+}
+
+void Program::exec_step(const StepInfo& st, const ChunkData* ch) {
+    if (elem_bytes_ == 8) exec_step_t<double>(st, ch);
+    else exec_step_t<float>(st, ch);
+}
+
+void Program::exec_level(int level, const ChunkData* ch) {
+    // leaves of this level
+    if (level < 2) {
+        if (!static_jobs_[level].empty()) {
+            if (elem_bytes_ == 8)
+                launch_leaf_project<double>(d_static_jobs_[level], static_cast<int>(static_jobs_[level].size()),
+                                            d_leaf_data_, nullptr, d_pass_src_, d_state_, static_cast<double*>(arena_), stream_);
+            else
+                launch_leaf_project<float>(d_static_jobs_[level], static_cast<int>(static_jobs_[level].size()),
+                                           d_leaf_data_, nullptr, d_pass_src_, d_state_, static_cast<float*>(arena_), stream_);
+            ++launches_;
+        }
+    } else if (ch->n_leaf_jobs) {
+        if (elem_bytes_ == 8)
+            launch_leaf_project<double>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes, d_pass_src_,
+                                        d_state_, static_cast<double*>(arena_), stream_);
+        else
+            launch_leaf_project<float>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes, d_pass_src_,
+                                       d_state_, static_cast<float*>(arena_), stream_);
+        ++launches_;
+    }
+    for (const StepInfo& st : steps_)
+        if (st.level == level) exec_step(st, ch);
+}
+
+void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
+                  uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats) {
+    if (groups.empty()) throw Failure{RCSG_ERR_CONFIG, "group count must be >= 1"};
+    if (slice_end <= slice_begin) throw Failure{RCSG_ERR_CONFIG, "empty slice range"};
+    // chunk capacity: the largest group chunk whose arena fits the budget
+    std::vector<uint64_t> uniq = groups;
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    uint64_t budget = mem_budget_;
+    if (!budget) {
+        size_t fr = 0, tot = 0;
+        CUDA_OK(cudaMemGetInfo(&fr, &tot));
+        budget = static_cast<uint64_t>(fr * 0.7);
+    }
+    const int64_t n_uniq = static_cast<int64_t>(uniq.size());
+    int64_t lo = 1, hi = n_uniq;
+    if (static_cast<uint64_t>(plan_arena(1, false)) * elem_bytes_ > budget)
+        throw Failure{RCSG_ERR_CAPACITY, "device arena for one group (" +
+                                             std::to_string(plan_arena(1, false) * elem_bytes_) +
+                                             " B) exceeds the memory budget"};
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (static_cast<uint64_t>(plan_arena(mid, false)) * elem_bytes_ <= budget) lo = mid;
+        else hi = mid - 1;
+    }
+    const int64_t cap = lo;
+    const int64_t need = plan_arena(cap, true);
+    if (need > arena_elems_) {
+        cudaFree(arena_);
+        arena_ = nullptr;
+        CUDA_OK(cudaMalloc(&arena_, static_cast<size_t>(need) * elem_bytes_));
+        arena_elems_ = need;
+    }
+    // static leaf jobs (offsets depend on the arena plan)
+    for (int level = 0; level < 2; ++level) {
+        static_jobs_[level].clear();
+        for (int i = 0; i < n_leaves_; ++i) {
+            const NodeInfo& nd = nodes_[i];
+            if (nd.level != level) continue;
+            LeafJob j{};
+            j.out_off = nd.off;
+            j.out_plane = nd.plane;
+            j.data_off = nd.data_off;
+            j.rank = nd.rank0;
+            j.out_rank = static_cast<int32_t>(nd.labels.size());
+            j.n_var = 1;
+            j.codes_off = -1;
+            for (int p = 0; p < nd.rank0; ++p) {
+                const LabelRole& rl = roles_[nd.labels0[p]];
+                j.kind[p] = rl.role;
+                j.arg[p] = static_cast<int16_t>(nd.labels0[p]);
+            }
+            static_jobs_[level].push_back(j);
+        }
+        cudaFree(d_static_jobs_[level]);
+        d_static_jobs_[level] = nullptr;
+        CUDA_OK(cudaMalloc(&d_static_jobs_[level], std::max<size_t>(static_jobs_[level].size(), 1) * sizeof(LeafJob)));
+        CUDA_OK(cudaMemcpy(d_static_jobs_[level], static_jobs_[level].data(),
+                           static_jobs_[level].size() * sizeof(LeafJob), cudaMemcpyHostToDevice));
+    }
+    prepare_chunks(groups, cap);
+    chunk_cap_ = cap;
+    const int64_t P = nodes_[root_].payload;
+    const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
+    if (acc_n > acc_cap_) {
+        cudaFree(d_part_);
+        cudaFree(d_res_);
+        cudaFree(d_comp_);
+        CUDA_OK(cudaMalloc(&d_part_, acc_n * sizeof(double)));
+        CUDA_OK(cudaMalloc(&d_res_, acc_n * sizeof(double)));
+        CUDA_OK(cudaMalloc(&d_comp_, acc_n * sizeof(double)));
+        acc_cap_ = acc_n;
+    }
+    const int32_t no_fault = INT_MAX;
+    CUDA_OK(cudaMemcpyAsync(d_fault_, &no_fault, sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+    launch_fill(d_res_, 0.0, acc_n, stream_);
+    launch_fill(d_comp_, 0.0, acc_n, stream_);
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    CUDA_OK(cudaEventRecord(e0, stream_));
+    launches_ = 0;
+    exec_flops_ = 0;
+    uint64_t passes = 0;
+    const std::vector<uint64_t> no_cfg{0};
+    const std::vector<uint64_t>& cfgs = configs.empty() ? no_cfg : configs;
+    for (size_t ci = 0; ci < cfgs.size(); ++ci) {
+        launch_fill(d_part_, 0.0, acc_n, stream_);
+        ++launches_;
+        launch_set_pass(d_state_, slice_begin, cfgs[ci], stream_);
+        exec_level(0, nullptr);
+        for (uint64_t s = slice_begin; s < slice_end; ++s) {
+            launch_set_pass(d_state_, s, cfgs[ci], stream_);
+            ++launches_;
+            exec_level(1, nullptr);
+            for (const ChunkData& ch : chunks_) {
+                exec_level(2, &ch);
+                const NodeInfo& root = nodes_[root_];
+                if (elem_bytes_ == 8)
+                    launch_finalize<double>(static_cast<const double*>(buf(root.off)), root.plane, P,
+                                            static_cast<int>(root.labels.size()), d_canon_, ch.d_vid,
+                                            ch.d_groups, static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
+                else
+                    launch_finalize<float>(static_cast<const float*>(buf(root.off)), root.plane, P,
+                                           static_cast<int>(root.labels.size()), d_canon_, ch.d_vid,
+                                           ch.d_groups, static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
+                ++launches_;
+                ++passes;
+            }
+        }
+        launch_kahan(d_res_, d_comp_, d_part_, acc_n, stream_);
+        ++launches_;
+    }
+    // d_acc += res
+    launch_fill(d_comp_, 0.0, acc_n, stream_);
+    launch_kahan(d_acc, d_comp_, d_res_, acc_n, stream_);
+    launches_ += 2;
+    CUDA_OK(cudaEventRecord(e1, stream_));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    int32_t fault = INT_MAX;
+    CUDA_OK(cudaMemcpy(&fault, d_fault_, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (fault != INT_MAX)
+        throw Failure{RCSG_ERR_NUMERIC, "non-finite intermediate at contraction step " + std::to_string(fault), fault};
+    if (stats) {
+        stats->plan_flops += plan_flops_ * static_cast<uint64_t>(groups.size()) * cfgs.size() * (slice_end - slice_begin);
+        stats->executed_flops += exec_flops_;
+        stats->arena_bytes = static_cast<uint64_t>(arena_elems_) * elem_bytes_;
+        stats->kernel_launches += launches_;
+        stats->passes += passes;
+        stats->device_ms += ms;
+    }
+}
+
+}  // namespace rcsg

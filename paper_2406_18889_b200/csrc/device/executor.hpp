@@ -1,0 +1,162 @@
+// Device step-program executor (host side of the contraction path).
+//
+// compile(): turns (network, plan, label roles) into a static program:
+//   - every tree node gets a LEVEL: 0 = depends on nothing that changes
+//     (computed once per run), 1 = depends on per-pass labels (slice /
+//     broken-edge / pinned bits; recomputed each pass), 2 = depends on the
+//     candidate group (the non-open output legs; recomputed per group chunk);
+//   - level-2 nodes are stored as [variants][payload]: one variant per DISTINCT
+//     projection of the chunk's group prefixes onto the output legs inside the
+//     node's subtree, so work shared by groups is done once (sparse-state
+//     group batching);
+//   - each plan step becomes permute(s) + one complex GEMM whose operand roles
+//     and layouts are fixed at compile time (TTGT, contraction_engine.cpp:87-128);
+//   - buffer offsets come from a first-fit simulation over the leveled
+//     schedule, so one arena allocation serves the whole run.
+// run(): loops configs x slices x group chunks, accumulating canonical-order
+// amplitudes per group (slices ascending, then compensated sum over configs,
+// contraction_engine.cpp:241-302).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "rcsg.h"
+
+namespace rcsg {
+
+struct Status {
+    int code = RCSG_OK;
+    std::string msg;
+    int step = -1;
+};
+
+// Thrown inside the library, converted to status codes at the C ABI.
+struct Failure {
+    int code;
+    std::string msg;
+    int step = -1;
+};
+
+enum Role : int8_t { kFree = 0, kPass = 1, kVar = 2 };
+
+struct LabelRole {
+    int8_t role = kFree;
+    int16_t var_bit = -1;  // kVar: bit position in the group code
+    PassSrc src{};         // kPass: where the value comes from
+};
+
+struct NodeInfo {
+    std::vector<int> labels;  // device layout, most significant first
+    uint64_t var_mask = 0;    // group-code bits of the output legs in the subtree
+    int level = 0;
+    int consumer = -1;        // program step consuming this node (-1: root)
+    int64_t payload = 1;
+    int64_t max_var = 1;
+    int64_t off = -1;         // arena element offset of the real plane
+    int64_t plane = 0;        // elements per plane (capacity)
+    bool is_leaf = false;
+    int64_t data_off = 0;     // leaves: complex offset into the packed leaf data
+    int rank0 = 0;            // leaves: original rank
+    std::vector<int> labels0; // leaves: original labels (MSB first)
+};
+
+struct StepInfo {
+    int plan_index = 0;
+    int a = -1, b = -1, r = -1;  // A-role operand, B-role operand, result (node ids)
+    int level = 0;
+    int mode = 0;  // 0 plain, 1 A-variant folded into M, 2 gathered batch
+    bool perm_a = false, perm_b = false;
+    PermuteDesc pa{}, pb{};
+    int64_t sa_off = -1, sa_plane = 0, sb_off = -1, sb_plane = 0;  // permute scratch
+    int64_t m = 1, n = 1, k = 1;
+    uint64_t flops_per_variant = 0;  // 8*m*n*k
+};
+
+struct ChunkData {
+    std::vector<uint64_t> codes;      // per node: variant codes (concatenated)
+    std::vector<int64_t> codes_off;   // per node offset into codes (-1 if level < 2)
+    std::vector<int64_t> nvar;        // per node variant count
+    std::vector<int32_t> idx;         // ia/ib arrays of gathered steps (concatenated)
+    std::vector<int64_t> ia_off, ib_off;  // per step
+    std::vector<int32_t> groups;      // original group indices in this chunk
+    std::vector<int32_t> vid;         // root variant of each group
+    // device copies
+    uint64_t* d_codes = nullptr;
+    int32_t* d_idx = nullptr;
+    int32_t* d_groups = nullptr;
+    int32_t* d_vid = nullptr;
+    LeafJob* d_leaf_jobs = nullptr;
+    int n_leaf_jobs = 0;
+};
+
+class Program {
+  public:
+    Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan, const std::vector<LabelRole>& roles,
+            int precision, uint64_t mem_budget);
+    ~Program();
+    Program(const Program&) = delete;
+    Program& operator=(const Program&) = delete;
+
+    // groups: code per group (bits at var_bit positions).  configs empty ->
+    // one pass per slice with config bits 0.  d_acc: device double
+    // [n_groups][2^out_rank] interleaved; accumulates (+=) the result.
+    void run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
+             uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats);
+
+    int out_rank() const { return out_rank_; }
+    cudaStream_t stream() const { return stream_; }
+    int precision() const { return precision_; }
+    uint64_t plan_flops_per_pass() const { return plan_flops_; }
+
+  private:
+    void build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan);
+    void build_steps();
+    int64_t plan_arena(int64_t chunk_cap, bool assign);
+    void prepare_chunks(const std::vector<uint64_t>& groups, int64_t chunk_cap);
+    void free_chunks();
+    void exec_level(int level, const ChunkData* ch);
+    void exec_step(const StepInfo& s, const ChunkData* ch);
+    void* buf(int64_t off) const;
+    template <typename R>
+    void exec_step_t(const StepInfo& s, const ChunkData* ch);
+
+    int precision_;
+    int elem_bytes_;
+    uint64_t mem_budget_;
+    std::vector<LabelRole> roles_;
+    std::vector<NodeInfo> nodes_;
+    std::vector<StepInfo> steps_;
+    std::vector<int> root_canon_src_;  // payload bit of canonical output bit j
+    std::vector<int> canon_qubit_;     // label -> open qubit (-1 if not open)
+    int root_ = 0;
+    int n_leaves_ = 0;
+    int out_rank_ = 0;
+    uint64_t plan_flops_ = 0;
+    std::vector<double> leaf_data_;
+    std::vector<LeafJob> static_jobs_[2];  // level 0 and level 1 leaf jobs
+
+    // device state
+    cudaStream_t stream_ = nullptr;
+    void* arena_ = nullptr;
+    int64_t arena_elems_ = 0;
+    int64_t chunk_cap_ = 0;
+    double* d_leaf_data_ = nullptr;
+    PassSrc* d_pass_src_ = nullptr;
+    PassState* d_state_ = nullptr;
+    LeafJob* d_static_jobs_[2] = {nullptr, nullptr};
+    int32_t* d_canon_ = nullptr;
+    int32_t* d_fault_ = nullptr;
+    double* d_part_ = nullptr;   // per-config accumulator
+    double* d_res_ = nullptr;
+    double* d_comp_ = nullptr;
+    int64_t acc_cap_ = 0;
+    std::vector<ChunkData> chunks_;
+    uint64_t launches_ = 0;
+    uint64_t exec_flops_ = 0;
+};
+
+}  // namespace rcsg

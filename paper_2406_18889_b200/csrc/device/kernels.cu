@@ -1,0 +1,380 @@
+// Device kernels of the contraction path: leaf projection, bit-permutation
+// transpose, SIMT complex GEMM, pass finalisation and compensated reduction.
+// See kernels.cuh for the storage convention.
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace rcsg {
+
+static inline int grid_cap() { return 148 * 16; }
+
+// ------------------------------------------------------------------ leaves
+// One CTA per leaf job; threads stride over (variant, element).
+template <typename R>
+__global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
+                                    const double* __restrict__ leaf_data,
+                                    const uint64_t* __restrict__ codes,
+                                    const PassSrc* __restrict__ pass_src,
+                                    const PassState* __restrict__ state, R* __restrict__ arena) {
+    const LeafJob j = jobs[blockIdx.x];
+    const PassState ps = *state;
+    // bits fixed by pass labels, and per-free-position source bit
+    uint64_t fixed = 0;
+    int free_src[kMaxLeafRank];
+    int nf = 0;
+    for (int p = 0; p < j.rank; ++p) {
+        const int bitpos = j.rank - 1 - p;
+        if (j.kind[p] == 0) {
+            free_src[nf++] = bitpos;
+        } else if (j.kind[p] == 1) {
+            const PassSrc s = pass_src[j.arg[p]];
+            const int v = s.kind == 0 ? s.value
+                                      : static_cast<int>(((s.kind == 1 ? ps.slice : ps.config) >> s.bit) & 1);
+            fixed |= static_cast<uint64_t>(v) << bitpos;
+        }
+    }
+    const int64_t payload = int64_t{1} << j.out_rank;
+    const int64_t total = payload * j.n_var;
+    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const int64_t v = t / payload;
+        const int64_t i = t - v * payload;
+        uint64_t src = fixed;
+        if (j.codes_off >= 0) {
+            const uint64_t code = codes[j.codes_off + v];
+            for (int p = 0; p < j.rank; ++p)
+                if (j.kind[p] == 2) src |= ((code >> j.arg[p]) & 1) << (j.rank - 1 - p);
+        }
+        // free positions keep their order: output bit (out_rank-1-q) <- free_src[q]
+        for (int q = 0; q < nf; ++q) src |= static_cast<uint64_t>((i >> (nf - 1 - q)) & 1) << free_src[q];
+        const double re = leaf_data[2 * (j.data_off + src)];
+        const double im = leaf_data[2 * (j.data_off + src) + 1];
+        arena[j.out_off + t] = static_cast<R>(re);
+        arena[j.out_off + j.out_plane + t] = static_cast<R>(im);
+    }
+}
+
+template <typename R>
+void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf_data,
+                         const uint64_t* d_codes, const PassSrc* d_pass_src,
+                         const PassState* d_state, R* arena, cudaStream_t st) {
+    if (n_jobs == 0) return;
+    leaf_project_kernel<R><<<n_jobs, 64, 0, st>>>(d_jobs, d_leaf_data, d_codes, d_pass_src,
+                                                   d_state, arena);
+}
+template void launch_leaf_project<float>(const LeafJob*, int, const double*, const uint64_t*,
+                                         const PassSrc*, const PassState*, float*, cudaStream_t);
+template void launch_leaf_project<double>(const LeafJob*, int, const double*, const uint64_t*,
+                                          const PassSrc*, const PassState*, double*, cudaStream_t);
+
+// ------------------------------------------------------------------ permute
+PermuteDesc make_permute(int rank, const int* src_bit) {
+    if (rank > kMaxRank) throw std::runtime_error("tensor rank exceeds kMaxRank");
+    PermuteDesc d{};
+    d.rank = rank;
+    std::vector<int> dst_of(rank);
+    for (int q = 0; q < rank; ++q) dst_of[src_bit[q]] = q;
+    std::vector<char> inU(rank, 0);
+    int nU = 0, lo_in = 0, lo_out = 0;
+    const int cap = std::min(10, rank);
+    auto take = [&](int pos) {
+        if (inU[pos]) return true;
+        if (nU >= cap) return false;
+        inU[pos] = 1;
+        ++nU;
+        return true;
+    };
+    // grow the tile alternately along the input's and the output's fastest
+    // bits; bits already inside the tile extend the runs for free
+    for (bool progress = true; progress;) {
+        progress = false;
+        if (lo_in < rank && take(lo_in)) {
+            ++lo_in;
+            progress = true;
+        }
+        if (lo_out < rank && take(src_bit[lo_out])) {
+            ++lo_out;
+            progress = true;
+        }
+    }
+    // e ordering: U ascending by input position (input bits 0..lo_in-1 lowest)
+    std::vector<int> U;
+    for (int p = 0; p < rank; ++p)
+        if (inU[p]) U.push_back(p);
+    std::vector<int> e_of_pos(rank, -1);
+    for (int j = 0; j < nU; ++j) e_of_pos[U[j]] = j;
+    // f ordering: output positions 0..lo_out-1 first, then the rest of U by output position
+    std::vector<int> F;
+    for (int q = 0; q < lo_out; ++q) F.push_back(q);
+    std::vector<int> rest;
+    for (int p : U)
+        if (dst_of[p] >= lo_out) rest.push_back(dst_of[p]);
+    std::sort(rest.begin(), rest.end());
+    for (int q : rest) F.push_back(q);
+    d.tile_bits = nU;
+    for (int x = 0; x < 32; ++x) {
+        int64_t il = 0, ih = 0, ol = 0, oh = 0, el = 0, eh = 0;
+        for (int b = 0; b < 5; ++b) {
+            if (!((x >> b) & 1)) continue;
+            if (b < nU) {
+                il += int64_t{1} << U[b];
+                ol += int64_t{1} << F[b];
+                el += int64_t{1} << e_of_pos[src_bit[F[b]]];
+            }
+            if (b + 5 < nU) {
+                ih += int64_t{1} << U[b + 5];
+                oh += int64_t{1} << F[b + 5];
+                eh += int64_t{1} << e_of_pos[src_bit[F[b + 5]]];
+            }
+        }
+        d.in_lo[x] = static_cast<int32_t>(il);
+        d.in_hi[x] = static_cast<int32_t>(ih);
+        d.out_lo[x] = static_cast<int32_t>(ol);
+        d.out_hi[x] = static_cast<int32_t>(oh);
+        d.e_lo[x] = static_cast<int32_t>(el);
+        d.e_hi[x] = static_cast<int32_t>(eh);
+    }
+    int j = 0;
+    for (int p = 0; p < rank; ++p)
+        if (!inU[p]) {
+            d.outer_in[j] = int64_t{1} << p;
+            d.outer_out[j] = int64_t{1} << dst_of[p];
+            ++j;
+        }
+    d.n_outer = j;
+    return d;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) permute_kernel(const R* __restrict__ in, int64_t in_plane,
+                                                      R* __restrict__ out, int64_t out_plane,
+                                                      int64_t n_var, const PermuteDesc d) {
+    __shared__ int32_t tab[6][32];
+    __shared__ R s_re[1024 + 32], s_im[1024 + 32];
+    if (threadIdx.x < 32) {
+        tab[0][threadIdx.x] = d.in_lo[threadIdx.x];
+        tab[1][threadIdx.x] = d.in_hi[threadIdx.x];
+        tab[2][threadIdx.x] = d.out_lo[threadIdx.x];
+        tab[3][threadIdx.x] = d.out_hi[threadIdx.x];
+        tab[4][threadIdx.x] = d.e_lo[threadIdx.x];
+        tab[5][threadIdx.x] = d.e_hi[threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t payload = int64_t{1} << d.rank;
+    const int T = 1 << d.tile_bits;
+    const int64_t outer = int64_t{1} << d.n_outer;
+    const int64_t total = outer * n_var;
+    for (int64_t cta = blockIdx.x; cta < total; cta += gridDim.x) {
+        const int64_t v = cta >> d.n_outer;
+        const int64_t c = cta & (outer - 1);
+        int64_t bi = v * payload, bo = v * payload;
+        for (int j = 0; j < d.n_outer; ++j)
+            if ((c >> j) & 1) {
+                bi += d.outer_in[j];
+                bo += d.outer_out[j];
+            }
+        for (int e = threadIdx.x; e < T; e += blockDim.x) {
+            const int64_t off = bi + tab[0][e & 31] + tab[1][e >> 5];
+            s_re[e + (e >> 5)] = in[off];
+            s_im[e + (e >> 5)] = in[in_plane + off];
+        }
+        __syncthreads();
+        for (int f = threadIdx.x; f < T; f += blockDim.x) {
+            const int e = tab[4][f & 31] + tab[5][f >> 5];
+            const int64_t off = bo + tab[2][f & 31] + tab[3][f >> 5];
+            out[off] = s_re[e + (e >> 5)];
+            out[out_plane + off] = s_im[e + (e >> 5)];
+        }
+        __syncthreads();
+    }
+}
+
+template <typename R>
+void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, int64_t n_var,
+                    const PermuteDesc& d, cudaStream_t st) {
+    const int64_t total = (int64_t{1} << d.n_outer) * n_var;
+    const int grid = static_cast<int>(std::min<int64_t>(total, grid_cap()));
+    const int threads = d.tile_bits >= 8 ? 256 : (d.tile_bits >= 6 ? 64 : 32);
+    permute_kernel<R><<<grid, threads, 0, st>>>(in, in_plane, out, out_plane, n_var, d);
+}
+template void launch_permute<float>(const float*, int64_t, float*, int64_t, int64_t,
+                                    const PermuteDesc&, cudaStream_t);
+template void launch_permute<double>(const double*, int64_t, double*, int64_t, int64_t,
+                                     const PermuteDesc&, cudaStream_t);
+
+// ------------------------------------------------------------------ SIMT GEMM
+// 64x64 complex tile per CTA, 16x16 threads, 4x4 complex outputs per thread,
+// K step 16.  Used for fp64 (reference-grade parity) and for shapes the
+// tensor-core kernel does not cover (tiny m/n/k).
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename R>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
+    __shared__ R As_re[BK][BM + 1], As_im[BK][BM + 1];
+    __shared__ R Bs_re[BK][BN + 1], Bs_im[BK][BN + 1];
+    const R* A = static_cast<const R*>(g.a);
+    const R* B = static_cast<const R*>(g.b);
+    R* Cm = static_cast<R*>(g.c);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+    for (int64_t v = blockIdx.z; v < g.batch; v += gridDim.z) {
+        const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
+        const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
+        const R* Ab = A + av * g.a_batch;
+        const R* Bb = B + bv * g.b_batch;
+        R acc_re[4][4], acc_im[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc_re[i][j] = acc_im[i][j] = R(0);
+        for (int64_t k0 = 0; k0 < g.k; k0 += BK) {
+            // 64 rows x 16 k per operand: 1024 elements, 4 per thread
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int e = tid + r * 256;
+                const int row = e >> 4, kk = e & 15;
+                const int64_t gk = k0 + kk;
+                R ar = 0, ai = 0, br = 0, bi = 0;
+                if (gk < g.k) {
+                    if (m0 + row < g.m) {
+                        const int64_t o = (m0 + row) * g.k + gk;
+                        ar = Ab[o];
+                        ai = Ab[g.a_plane + o];
+                    }
+                    if (n0 + row < g.n) {
+                        const int64_t o = (n0 + row) * g.k + gk;
+                        br = Bb[o];
+                        bi = Bb[g.b_plane + o];
+                    }
+                }
+                As_re[kk][row] = ar;
+                As_im[kk][row] = ai;
+                Bs_re[kk][row] = br;
+                Bs_im[kk][row] = bi;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                R a_r[4], a_i[4], b_r[4], b_i[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a_r[i] = As_re[kk][ty + 16 * i];
+                    a_i[i] = As_im[kk][ty + 16 * i];
+                    b_r[i] = Bs_re[kk][tx + 16 * i];
+                    b_i[i] = Bs_im[kk][tx + 16 * i];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc_re[i][j] = fma(a_r[i], b_r[j], acc_re[i][j]);
+                        acc_re[i][j] = fma(-a_i[i], b_i[j], acc_re[i][j]);
+                        acc_im[i][j] = fma(a_r[i], b_i[j], acc_im[i][j]);
+                        acc_im[i][j] = fma(a_i[i], b_r[j], acc_im[i][j]);
+                    }
+            }
+            __syncthreads();
+        }
+        R* Cb = Cm + v * g.c_batch;
+        bool bad = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+                if (m < g.m && n < g.n) {
+                    const int64_t o = m * g.n + n;
+                    Cb[o] = acc_re[i][j];
+                    Cb[g.c_plane + o] = acc_im[i][j];
+                    bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
+                }
+            }
+        if (bad && g.fault) atomicMin(g.fault, g.step);
+    }
+}
+
+template <typename R>
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
+    dim3 block(16, 16);
+    dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM),
+              static_cast<unsigned>(std::min<int64_t>(g.batch, 65535)));
+    if (grid.y > 65535) throw std::runtime_error("gemm m too large for SIMT path");
+    gemm_simt_kernel<R><<<grid, block, 0, st>>>(g);
+}
+template void launch_gemm_simt<float>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_simt<double>(const GemmArgs&, cudaStream_t);
+
+// ------------------------------------------------------------------ finalize
+template <typename R>
+__global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, int64_t payload,
+                                int rank, const int32_t* __restrict__ src_bit,
+                                const int32_t* __restrict__ vid, const int32_t* __restrict__ gidx,
+                                int64_t n_groups, double* __restrict__ acc) {
+    const int64_t total = n_groups * payload;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t gl = t / payload;
+        const int64_t i = t - gl * payload;
+        int64_t p = 0;
+        for (int j = 0; j < rank; ++j) p |= ((i >> j) & 1) << src_bit[j];
+        const int64_t v = vid ? vid[gl] : 0;
+        const int64_t o = v * payload + p;
+        const int64_t g = gidx ? gidx[gl] : gl;
+        acc[2 * (g * payload + i)] += static_cast<double>(root[o]);
+        acc[2 * (g * payload + i) + 1] += static_cast<double>(root[root_plane + o]);
+    }
+}
+
+template <typename R>
+void launch_finalize(const R* root, int64_t root_plane, int64_t payload, int rank,
+                     const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
+                     const int32_t* d_gidx, int64_t n_groups_chunk, double* acc, cudaStream_t st) {
+    const int64_t total = n_groups_chunk * payload;
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, grid_cap()));
+    finalize_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(root, root_plane, payload, rank,
+                                                          d_src_bit_of_canon, d_vid, d_gidx,
+                                                          n_groups_chunk, acc);
+}
+template void launch_finalize<float>(const float*, int64_t, int64_t, int, const int32_t*,
+                                     const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
+template void launch_finalize<double>(const double*, int64_t, int64_t, int, const int32_t*,
+                                      const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
+
+// ------------------------------------------------------------------ misc
+__global__ void kahan_kernel(double* res, double* comp, const double* part, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double y = part[i] - comp[i];
+        const double s = __dadd_rn(res[i], y);
+        comp[i] = __dsub_rn(__dsub_rn(s, res[i]), y);
+        res[i] = s;
+    }
+}
+void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, grid_cap()));
+    kahan_kernel<<<std::max(grid, 1), 256, 0, st>>>(res, comp, part, n);
+}
+
+__global__ void fill_kernel(double* p, double v, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+void launch_fill(double* p, double v, int64_t n, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, grid_cap()));
+    fill_kernel<<<std::max(grid, 1), 256, 0, st>>>(p, v, n);
+}
+
+__global__ void set_pass_kernel(PassState* s, uint64_t slice, uint64_t config) {
+    s->slice = slice;
+    s->config = config;
+}
+void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, cudaStream_t st) {
+    set_pass_kernel<<<1, 1, 0, st>>>(d_state, slice, config);
+}
+
+}  // namespace rcsg

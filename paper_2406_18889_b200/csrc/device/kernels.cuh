@@ -1,0 +1,109 @@
+// Device kernels of the contraction path (declarations + launch wrappers).
+//
+// Storage: every tensor is PLANAR complex — a real plane of N elements followed
+// by an imaginary plane of N elements — with a leading "variant" axis
+// (distinct group projections, see executor.cpp) outermost:
+//   re[v * payload + i], im[(total) + v * payload + i].
+// Real type R is double (RCSG_PREC_F64) or float (all other precisions).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rcsg {
+
+constexpr int kMaxRank = 40;
+constexpr int kMaxLeafRank = 8;
+
+// ---- leaf projection (reference project_leaf, contraction_engine.cpp:27-52,
+// batched over all leaves of one level and all of their variants).
+struct LeafJob {
+    int64_t out_off;      // element offset of the output re-plane
+    int64_t out_plane;    // elements per plane of the output buffer
+    int64_t data_off;     // complex offset into the packed leaf data (double, interleaved)
+    int32_t rank;         // original rank
+    int32_t out_rank;     // free labels kept
+    int32_t n_var;        // number of variants (>= 1)
+    int32_t codes_off;    // offset into the variant code table (-1: single variant)
+    // per original position p (MSB first): kind 0 free (kept), 1 pass label, 2 variant label
+    int8_t kind[kMaxLeafRank];
+    int16_t arg[kMaxLeafRank];  // pass: label id; variant: bit position in the group code
+};
+
+struct PassState {
+    uint64_t slice;        // current slice index (bit b <-> sliced[b])
+    uint64_t config;       // current broken-edge configuration bits
+};
+
+// Pass-label source table: for a pass label, where its value comes from.
+struct PassSrc {
+    int8_t kind;   // 0 const, 1 slice bit, 2 config bit
+    int8_t value;  // const value
+    int16_t bit;
+};
+
+template <typename R>
+void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf_data,
+                         const uint64_t* d_codes, const PassSrc* d_pass_src,
+                         const PassState* d_state, R* arena, cudaStream_t st);
+
+// ---- bit-permutation transpose of a [V][2^rank] planar tensor.
+// Output bit q (LSB=0) takes input bit src_bit[q].
+// Built on the host by make_permute(); the kernel moves one tile of up to
+// 2^10 elements per CTA through shared memory so both the reads (input-order
+// runs) and the writes (output-order runs) are coalesced.
+struct PermuteDesc {
+    int32_t rank;
+    int32_t tile_bits;          // |U|: bits enumerated inside a tile
+    int32_t n_outer;            // rank - tile_bits: bits enumerated across CTAs
+    int64_t outer_in[kMaxRank];   // input stride of outer bit j
+    int64_t outer_out[kMaxRank];  // output stride of outer bit j
+    int32_t in_lo[32], in_hi[32];    // input offset of tile index e (split 5/5 bits)
+    int32_t out_lo[32], out_hi[32];  // output offset of tile index f
+    int32_t e_lo[32], e_hi[32];      // tile index e holding output element f
+};
+PermuteDesc make_permute(int rank, const int* src_bit);
+template <typename R>
+void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, int64_t n_var,
+                    const PermuteDesc& d, cudaStream_t st);
+
+// ---- complex GEMM, both operands K-contiguous ("TN"):
+//   C[v][m][n] = sum_k A[ia(v)][m][k] * B[ib(v)][n][k]
+// ia / ib: device index arrays or nullptr (identity for ia, 0 for ib... see GemmArgs).
+struct GemmArgs {
+    const void* a;
+    int64_t a_plane;   // elements per plane of A's buffer
+    int64_t a_batch;   // stride between A variants (elements)
+    const void* b;
+    int64_t b_plane;
+    int64_t b_batch;
+    void* c;
+    int64_t c_plane;
+    int64_t c_batch;
+    int64_t m, n, k;
+    int64_t batch;          // number of C variants
+    const int32_t* ia;      // nullptr -> A variant = v * (a_batch != 0)
+    const int32_t* ib;      // nullptr -> B variant = v * (b_batch != 0)
+    int32_t step;           // plan step index for the non-finite flag
+    int32_t* fault;         // device flag: min step index with a non-finite output
+};
+template <typename R>
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
+
+// tcgen05 tensor-core path (float storage; kind::tf32, 1 or 3 passes).
+bool gemm_tc_supported(const GemmArgs& g);
+void launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t st);
+
+// ---- finalize a pass: acc[g][i] += root[vid[g]][perm(i)]   (acc: double interleaved)
+template <typename R>
+void launch_finalize(const R* root, int64_t root_plane, int64_t payload, int rank,
+                     const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
+                     const int32_t* d_gidx, int64_t n_groups_chunk, double* acc,
+                     cudaStream_t st);
+
+// compensated accumulation in configuration order (contraction_engine.cpp:289-302)
+void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st);
+void launch_fill(double* p, double v, int64_t n, cudaStream_t st);
+void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, cudaStream_t st);
+
+}  // namespace rcsg

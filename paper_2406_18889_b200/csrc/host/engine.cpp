@@ -1,0 +1,217 @@
+// Host C++ API (namespace rcs) of the hot path, implemented over the C ABI.
+//
+// Same signatures, validation, error types and result semantics as the
+// reference executor (contraction_engine.cpp:132-354); every contraction runs
+// on the GPU (rcsg.h) — there is no CPU execution path.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "rcs_b200.hpp"
+#include "flat.hpp"
+#include "rcsg.h"
+
+namespace rcs {
+namespace {
+
+int g_precision = RCSG_PREC_F64;
+
+[[noreturn]] void raise(int rc) {
+    int32_t step = -1;
+    const std::string msg = rcsg_last_error(&step);
+    switch (rc) {
+        case RCSG_ERR_CONFIG: throw ConfigError(msg);
+        case RCSG_ERR_NUMERIC: throw NumericFault(msg, step);
+        case RCSG_ERR_CAPACITY: throw CapacityError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+void ok(int rc) {
+    if (rc) raise(rc);
+}
+
+struct ProgramHandle {
+    rcsg_program* p = nullptr;
+    ~ProgramHandle() {
+        if (p) rcsg_program_free(p);
+    }
+};
+
+void check_config(const ContractionPlan& plan, const BrokenEdgeConfig* config) {
+    if (config) {
+        if (config->broken_labels != plan.broken)
+            throw ConfigError("broken-edge labels do not match the plan");
+        if (config->configurations.empty()) throw ConfigError("broken-edge configuration list is empty");
+    } else if (!plan.broken.empty()) {
+        throw ConfigError("plan has broken edges; exact contraction needs a plan without them");
+    }
+}
+
+std::vector<cplx> to_cplx(const std::vector<double>& v) {
+    std::vector<cplx> out(v.size() / 2);
+    for (std::size_t i = 0; i < out.size(); ++i) out[i] = cplx(v[2 * i], v[2 * i + 1]);
+    return out;
+}
+
+}  // namespace
+
+void set_precision(const std::string& p) {
+    if (p == "f64") g_precision = RCSG_PREC_F64;
+    else if (p == "f32") g_precision = RCSG_PREC_F32;
+    else if (p == "tf32") g_precision = RCSG_PREC_TF32;
+    else if (p == "3xtf32") g_precision = RCSG_PREC_3XTF32;
+    else throw ConfigError("precision must be f64, f32, tf32 or 3xtf32");
+}
+
+std::string get_precision() {
+    static const char* names[] = {"f64", "f32", "tf32", "3xtf32"};
+    return names[g_precision];
+}
+
+double BrokenEdgeConfig::predicted_fidelity() const {
+    return static_cast<double>(m()) * std::pow(2.0, -k());
+}
+
+BrokenEdgeConfig make_broken_config(std::vector<Label> broken_labels, std::uint64_t m, std::uint64_t seed) {
+    const int k = static_cast<int>(broken_labels.size());
+    if (k > 62) throw ConfigError("too many broken edges");
+    const std::uint64_t full = std::uint64_t{1} << k;
+    if (m < 1 || m > full)
+        throw ConfigError("configuration count m=" + std::to_string(m) + " outside [1, 2^" +
+                          std::to_string(k) + "]");
+    BrokenEdgeConfig c;
+    c.broken_labels = std::move(broken_labels);
+    // Gray-code walk from a seeded start (contraction_engine.cpp:136-151)
+    const std::uint64_t start = Rng(seed ^ 0xb20ced6eULL).next_below(full);
+    for (std::uint64_t i = 0; i < m; ++i) c.configurations.push_back(start ^ i ^ (i >> 1));
+    return c;
+}
+
+std::vector<cplx> execute_assignment(const TensorNetwork& network, const ContractionPlan& plan,
+                                     const std::map<Label, int>& assignment, ExecutionStats* stats) {
+    const int n_labels = static_cast<int>(network.label_names.size());
+    std::vector<int8_t> pin(n_labels, -1);
+    for (const auto& [l, v] : assignment) {
+        if (l < 0 || l >= n_labels) throw ConfigError("assignment label " + std::to_string(l) + " not in network");
+        if (v != 0 && v != 1) throw ConfigError("assignment values must be 0/1");
+        pin[l] = static_cast<int8_t>(v);
+    }
+    auto f = flatten(network, plan);
+    uint64_t n = 0;
+    ok(rcsg_execute_assignment(&f->net, &f->plan, g_precision, pin.data(), nullptr, &n));
+    std::vector<double> out(2 * n);
+    ok(rcsg_execute_assignment(&f->net, &f->plan, g_precision, pin.data(), out.data(), &n));
+    if (stats) stats->flops += plan.flops_per_slice;
+    return to_cplx(out);
+}
+
+ContractResult contract(const TensorNetwork& network, const ContractionPlan& plan,
+                        const BrokenEdgeConfig* config, const std::map<Label, int>& fixed_outputs,
+                        int workers) {
+    if (workers < 1) throw ConfigError("workers must be >= 1");
+    check_config(plan, config);
+    const int n_labels = static_cast<int>(network.label_names.size());
+    std::vector<int8_t> pin(n_labels, -1);
+    for (const auto& [l, v] : fixed_outputs) {
+        if (l < 0 || l >= n_labels) throw ConfigError("assignment label " + std::to_string(l) + " not in network");
+        if (v != 0 && v != 1) throw ConfigError("assignment values must be 0/1");
+        pin[l] = static_cast<int8_t>(v);
+    }
+    auto f = flatten(network, plan);
+    ProgramHandle h;
+    ok(rcsg_compile_pinned(&f->net, &f->plan, g_precision, 0, pin.data(), &h.p));
+    const std::vector<std::uint64_t> none{0};
+    const std::vector<std::uint64_t>& cfgs = config ? config->configurations : none;
+    ContractResult res;
+    std::vector<double> sum, comp;
+    const std::uint64_t group = 0;
+    for (std::size_t t = 0; t < cfgs.size(); ++t) {
+        rcsg_stats st{};
+        const auto t0 = std::chrono::steady_clock::now();
+        // one subtask = one configuration over every slice (contraction_engine.cpp:237-262);
+        // the result has one index bit per open leg that is not pinned
+        std::size_t n = std::size_t{1} << network.open_labels.size();
+        for (Label l : network.open_labels)
+            if (pin[l] >= 0) n >>= 1;
+        std::vector<double> buf(2 * n, 0.0);
+        ok(rcsg_contract_groups(h.p, 1, &group, config ? 1 : 0, config ? &cfgs[t] : nullptr, 0,
+                                plan.n_slices(), buf.data(), &st));
+        const auto t1 = std::chrono::steady_clock::now();
+        if (sum.empty()) {
+            sum.assign(buf.size(), 0.0);
+            comp.assign(buf.size(), 0.0);
+        }
+        // compensated reduction in ascending configuration order (:289-302)
+        for (std::size_t i = 0; i < buf.size(); ++i) {
+            const double y = buf[i] - comp[i];
+            const double s = sum[i] + y;
+            comp[i] = (s - sum[i]) - y;
+            sum[i] = s;
+        }
+        res.timings.push_back({t, cfgs[t], std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                               plan.flops_per_slice * plan.n_slices()});
+        res.stats.flops += plan.flops_per_slice * plan.n_slices();
+        res.stats.peak_bytes = std::max<std::uint64_t>(res.stats.peak_bytes, st.arena_bytes);
+    }
+    res.amplitudes = to_cplx(sum);
+    return res;
+}
+
+AmplitudeBatch contract_group(const TensorNetwork& network, const ContractionPlan& plan,
+                              const BrokenEdgeConfig* config, std::uint64_t group_id,
+                              std::uint64_t fixed_bits) {
+    auto all = contract_groups(network, plan, config, {fixed_bits});
+    AmplitudeBatch b = std::move(all[0]);
+    b.group_id = group_id;
+    return b;
+}
+
+std::vector<AmplitudeBatch> contract_groups(const TensorNetwork& network, const ContractionPlan& plan,
+                                            const BrokenEdgeConfig* config,
+                                            const std::vector<std::uint64_t>& group_fixed) {
+    check_config(plan, config);
+    if (group_fixed.empty()) throw ConfigError("group count must be >= 1");
+    auto f = flatten(network, plan);
+    ProgramHandle h;
+    ok(rcsg_compile(&f->net, &f->plan, g_precision, 0, &h.p));
+    const int l = static_cast<int>(network.open_labels.size());
+    const std::size_t per = std::size_t{1} << l;
+    std::vector<double> out(2 * per * group_fixed.size());
+    const std::size_t n_cfg = config ? config->configurations.size() : 0;
+    ok(rcsg_contract_groups(h.p, group_fixed.size(), group_fixed.data(), n_cfg,
+                            config ? config->configurations.data() : nullptr, 0, plan.n_slices(),
+                            out.data(), nullptr));
+    std::vector<AmplitudeBatch> res(group_fixed.size());
+    for (std::size_t g = 0; g < group_fixed.size(); ++g) {
+        res[g].group_id = g;
+        res[g].n_open = l;
+        res[g].fixed_bits = group_fixed[g];
+        res[g].amplitudes.resize(per);
+        for (std::size_t i = 0; i < per; ++i)
+            res[g].amplitudes[i] = cplx(out[2 * (g * per + i)], out[2 * (g * per + i) + 1]);
+    }
+    return res;
+}
+
+FidelityResult state_fidelity(std::span<const cplx> approx, std::span<const cplx> exact) {
+    if (approx.size() != exact.size()) throw ConfigError("fidelity requires identical index sets");
+    cplx overlap(0.0, 0.0);
+    double na = 0.0, ne = 0.0;
+    for (std::size_t i = 0; i < approx.size(); ++i) {
+        overlap += std::conj(exact[i]) * approx[i];
+        na += std::norm(approx[i]);
+        ne += std::norm(exact[i]);
+    }
+    if (ne == 0.0) throw ConfigError("exact collection has zero norm");
+    FidelityResult r;
+    if (na == 0.0) {
+        r.zero_norm_warning = true;
+        return r;
+    }
+    r.value = std::norm(overlap) / (na * ne);
+    return r;
+}
+
+}  // namespace rcs
