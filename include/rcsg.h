@@ -78,6 +78,14 @@ typedef struct rcsg_stats {
     uint64_t kernel_launches;  /* our kernels launched */
     uint64_t passes;           /* (config, slice, group-chunk) passes */
     double device_ms;          /* CUDA-event time of the contraction on the program's stream */
+    /* filled only when profiling is on (rcsg_program_set_profile): CUDA-event
+     * time of each kernel class on the program's stream, plus its work */
+    double gemm_ms;            /* complex GEMM launches (tensor-core + SIMT) */
+    double gemm_tc_ms;         /* tensor-core (tcgen05) GEMM launches only */
+    uint64_t gemm_tc_flops;    /* 8*m*n*k issued by tensor-core launches */
+    double permute_ms;         /* bit-permutation launches */
+    uint64_t permute_bytes;    /* bytes read + written by permutes */
+    uint64_t gemm_tc_launches;
 } rcsg_stats;
 
 typedef struct rcsg_program rcsg_program;
@@ -96,6 +104,14 @@ int rcsg_set_device(int32_t device);
 int rcsg_compile(const rcsg_network_desc* net, const rcsg_plan_desc* plan, int32_t precision,
                  uint64_t mem_budget_bytes, rcsg_program** out);
 int rcsg_program_free(rcsg_program* prog);
+
+/* Per-kernel-class CUDA-event timing (fills the *_ms fields of rcsg_stats).
+ * Adds two event records per launch; off by default. */
+int rcsg_program_set_profile(rcsg_program* prog, int32_t on);
+
+/* The CUDA stream (cudaStream_t) the program launches on, for callers that
+ * time it with their own events or order work after it. */
+int rcsg_program_stream(rcsg_program* prog, void** out);
 
 /* Amplitudes of n_groups candidate groups: for each group g,
  *   sum over configs (compensated, list order) of

@@ -34,7 +34,10 @@ class rcsg_plan_desc(C.Structure):
 class rcsg_stats(C.Structure):
     _fields_ = [("plan_flops", C.c_uint64), ("executed_flops", C.c_uint64),
                 ("arena_bytes", C.c_uint64), ("kernel_launches", C.c_uint64),
-                ("passes", C.c_uint64), ("device_ms", C.c_double)]
+                ("passes", C.c_uint64), ("device_ms", C.c_double), ("gemm_ms", C.c_double),
+                ("gemm_tc_ms", C.c_double), ("gemm_tc_flops", C.c_uint64),
+                ("permute_ms", C.c_double), ("permute_bytes", C.c_uint64),
+                ("gemm_tc_launches", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -48,6 +51,7 @@ class rcsg_candidates(C.Structure):
 # exported symbols and their restypes (everything else returns int status)
 RCSG_SYMBOLS = [
     "rcsg_last_error", "rcsg_set_device", "rcsg_compile", "rcsg_compile_pinned", "rcsg_program_free",
+    "rcsg_program_set_profile", "rcsg_program_stream", "rcsg_gemm_selftest",
     "rcsg_contract_groups", "rcsg_contract_groups_device", "rcsg_execute_assignment", "rcsg_topk",
     "rcsg_topk_probs", "rcsg_direct_sample", "rcsg_direct_sample_probs", "rcsg_xeb",
     "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy",
@@ -57,7 +61,8 @@ RCSH_SYMBOLS = [
     "rcsh_net_export", "rcsh_label_names", "rcsh_wire_edges", "rcsh_plan_sizes", "rcsh_plan_export",
     "rcsh_circuit_gates", "rcsh_contract_groups", "rcsh_contract_groups_device", "rcsh_contract",
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
-    "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs",
+    "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
+    "rcsh_program_stream",
 ]
 
 _lib = None
@@ -76,6 +81,7 @@ def lib():
         L.rcsg_last_error.restype = C.c_char_p
         L.rcsh_last_error.restype = C.c_char_p
         L.rcsh_free.restype = None
+        L.rcsh_set_profile.restype = None
         L.rcsh_net_sizes.restype = None
         L.rcsh_net_export.restype = None
         L.rcsh_wire_edges.restype = None

@@ -191,6 +191,17 @@ class Problem:
                          flops_per_slice=int(tot[0]), traffic_bytes_per_slice=int(tot[1]),
                          peak_bytes=int(tot[2]), memory_budget_bytes=int(tot[3]))
 
+    def stream(self, precision="tf32", budget=0) -> int:
+        """cudaStream_t (as int) the compiled program launches on."""
+        out = C.c_void_p()
+        _check_h(_native.lib().rcsh_program_stream(self.handle, _prec(precision), C.c_uint64(budget),
+                                                   C.byref(out)))
+        return out.value or 0
+
+    def set_profile(self, on: bool):
+        """Per-kernel-class CUDA-event timing into rcsg_stats (gemm_ms, permute_ms, ...)."""
+        _native.lib().rcsh_set_profile(self.handle, 1 if on else 0)
+
     @property
     def n_open(self) -> int:
         return len(self.net["open_labels"])

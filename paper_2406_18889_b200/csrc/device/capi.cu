@@ -150,6 +150,20 @@ int rcsg_program_free(rcsg_program* prog) {
     return guard([&] { delete prog; });
 }
 
+int rcsg_program_stream(rcsg_program* prog, void** out) {
+    return guard([&] {
+        if (!prog || !out) throw Failure{RCSG_ERR_CONFIG, "null argument"};
+        *out = static_cast<void*>(prog->prog->stream());
+    });
+}
+
+int rcsg_program_set_profile(rcsg_program* prog, int32_t on) {
+    return guard([&] {
+        if (!prog) throw Failure{RCSG_ERR_CONFIG, "null program"};
+        prog->prog->set_profile(on != 0);
+    });
+}
+
 int rcsg_contract_groups_device(rcsg_program* prog, uint64_t n_groups, const uint64_t* group_fixed,
                                 uint64_t n_configs, const uint64_t* configs, uint64_t slice_begin,
                                 uint64_t slice_end, double* d_acc, int32_t sync, rcsg_stats* stats) {

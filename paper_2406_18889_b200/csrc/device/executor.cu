@@ -1,6 +1,8 @@
 // Step-program executor; see executor.hpp for the design.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -127,6 +129,7 @@ Program::~Program() {
     cudaFree(d_res_);
     cudaFree(d_comp_);
     for (auto* p : d_static_jobs_) cudaFree(p);
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -433,7 +436,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     int64_t a_plane = A.plane;
     if (st.perm_a) {
         R* dst = static_cast<R*>(buf(st.sa_off));
+        const int mk = mark_begin();
         launch_permute<R>(a_ptr, A.plane, dst, st.sa_plane, va, st.pa, stream_);
+        mark_end(mk, kCatPermute, 4ull * sizeof(R) * va * A.payload, st.plan_index, va, A.payload, 0, 0);
         ++launches_;
         a_ptr = dst;
         a_plane = st.sa_plane;
@@ -442,7 +447,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     int64_t b_plane = B.plane;
     if (st.perm_b) {
         R* dst = static_cast<R*>(buf(st.sb_off));
+        const int mk = mark_begin();
         launch_permute<R>(b_ptr, B.plane, dst, st.sb_plane, vb, st.pb, stream_);
+        mark_end(mk, kCatPermute, 4ull * sizeof(R) * vb * B.payload, st.plan_index, vb, B.payload, 0, 0);
         ++launches_;
         b_ptr = dst;
         b_plane = st.sb_plane;
@@ -470,16 +477,84 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         g.m = st.m * va;  // mode 1: the variants fold into M
         g.batch = 1;
     }
-    exec_flops_ += st.flops_per_variant * static_cast<uint64_t>(vr);
+    const uint64_t flops = st.flops_per_variant * static_cast<uint64_t>(vr);
+    exec_flops_ += flops;
+    const int mk = mark_begin();
+    if (gemv_supported(g)) {
+        launch_gemv<R>(g, stream_);
+        mark_end(mk, kCatGemv, flops, st.plan_index, g.m, g.n, g.k, g.batch);
+        ++launches_;
+        return;
+    }
     if constexpr (sizeof(R) == 4) {
-        if (precision_ >= RCSG_PREC_TF32 && gemm_tc_supported(g)) {
+        // 3xTF32 stays on the fp32 SIMT kernel until its split-operand tensor-core path lands
+        if (precision_ == RCSG_PREC_TF32 && gemm_tc_supported(g)) {
             launch_gemm_tc(g, precision_ == RCSG_PREC_3XTF32 ? 3 : 1, stream_);
+            mark_end(mk, kCatGemmTc, flops, st.plan_index, g.m, g.n, g.k, g.batch);
             ++launches_;
             return;
         }
     }
     launch_gemm_simt<R>(g, stream_);
+    mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
     ++launches_;
+}
+
+int Program::mark_begin() {
+    if (!profile_) return -1;
+    const size_t i = marks_.size();
+    if (ev_pool_.size() < 2 * (i + 1)) {
+        cudaEvent_t a, b;
+        CUDA_OK(cudaEventCreate(&a));
+        CUDA_OK(cudaEventCreate(&b));
+        ev_pool_.push_back(a);
+        ev_pool_.push_back(b);
+    }
+    marks_.push_back({-1, 0, -1, 0, 0, 0, 0});
+    CUDA_OK(cudaEventRecord(ev_pool_[2 * i], stream_));
+    return static_cast<int>(i);
+}
+
+void Program::mark_end(int idx, int cat, uint64_t work, int step, int64_t m, int64_t n, int64_t k,
+                       int64_t batch) {
+    if (idx < 0) return;
+    marks_[idx] = {cat, work, step, m, n, k, batch};
+    CUDA_OK(cudaEventRecord(ev_pool_[2 * idx + 1], stream_));
+}
+
+void Program::collect_marks(rcsg_stats* stats) {
+    // RCSG_PROFILE_STEPS=N prints the N most expensive launches (stderr)
+    const char* env = getenv("RCSG_PROFILE_STEPS");
+    std::vector<std::pair<float, size_t>> order;
+    for (size_t i = 0; i < marks_.size(); ++i) {
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, ev_pool_[2 * i], ev_pool_[2 * i + 1]));
+        order.push_back({ms, i});
+        if (!stats) continue;
+        const Mark& m = marks_[i];
+        if (m.cat == kCatGemmSimt || m.cat == kCatGemmTc || m.cat == kCatGemv) stats->gemm_ms += ms;
+        if (m.cat == kCatGemmTc) {
+            stats->gemm_tc_ms += ms;
+            stats->gemm_tc_flops += m.work;
+            stats->gemm_tc_launches += 1;
+        }
+        if (m.cat == kCatPermute) {
+            stats->permute_ms += ms;
+            stats->permute_bytes += m.work;
+        }
+    }
+    if (env) {
+        std::sort(order.rbegin(), order.rend());
+        static const char* names[] = {"gemm_simt", "gemm_tc", "permute", "gemv"};
+        const size_t top = std::min<size_t>(order.size(), static_cast<size_t>(atoi(env)));
+        for (size_t j = 0; j < top; ++j) {
+            const Mark& m = marks_[order[j].second];
+            fprintf(stderr, "[rcsg] %8.3f ms %-9s step %4d m=%lld n=%lld k=%lld batch=%lld work=%.3e\n", order[j].first,
+                    m.cat >= 0 ? names[m.cat] : "?", m.step, (long long)m.m, (long long)m.n, (long long)m.k,
+                    (long long)m.batch, (double)m.work);
+        }
+    }
+    marks_.clear();
 }
 
 void Program::exec_step(const StepInfo& st, const ChunkData* ch) {
@@ -516,6 +591,17 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
                   uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats) {
     if (groups.empty()) throw Failure{RCSG_ERR_CONFIG, "group count must be >= 1"};
     if (slice_end <= slice_begin) throw Failure{RCSG_ERR_CONFIG, "empty slice range"};
+    // (re)bind the program to this group list: chunk capacity, arena, chunk
+    // index tables.  Repeated calls with the same groups (one call per slice
+    // range) reuse everything.
+    if (groups != bound_groups_) bind_groups(groups);
+    const int64_t P = nodes_[root_].payload;
+    const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
+    run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n);
+}
+
+void Program::bind_groups(const std::vector<uint64_t>& groups) {
+    bound_groups_.clear();
     // chunk capacity: the largest group chunk whose arena fits the budget
     std::vector<uint64_t> uniq = groups;
     std::sort(uniq.begin(), uniq.end());
@@ -574,8 +660,11 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     }
     prepare_chunks(groups, cap);
     chunk_cap_ = cap;
-    const int64_t P = nodes_[root_].payload;
-    const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
+    bound_groups_ = groups;
+}
+
+void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
+                        uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n) {
     if (acc_n > acc_cap_) {
         cudaFree(d_part_);
         cudaFree(d_res_);
@@ -636,12 +725,13 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    collect_marks(stats);
     int32_t fault = INT_MAX;
     CUDA_OK(cudaMemcpy(&fault, d_fault_, sizeof(int32_t), cudaMemcpyDeviceToHost));
     if (fault != INT_MAX)
         throw Failure{RCSG_ERR_NUMERIC, "non-finite intermediate at contraction step " + std::to_string(fault), fault};
     if (stats) {
-        stats->plan_flops += plan_flops_ * static_cast<uint64_t>(groups.size()) * cfgs.size() * (slice_end - slice_begin);
+        stats->plan_flops += plan_flops_ * static_cast<uint64_t>(n_groups) * cfgs.size() * (slice_end - slice_begin);
         stats->executed_flops += exec_flops_;
         stats->arena_bytes = static_cast<uint64_t>(arena_elems_) * elem_bytes_;
         stats->kernel_launches += launches_;

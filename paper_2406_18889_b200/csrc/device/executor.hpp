@@ -108,6 +108,7 @@ class Program {
              uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats);
 
     int out_rank() const { return out_rank_; }
+    void set_profile(bool on) { profile_ = on; }
     cudaStream_t stream() const { return stream_; }
     int precision() const { return precision_; }
     uint64_t plan_flops_per_pass() const { return plan_flops_; }
@@ -117,6 +118,9 @@ class Program {
     void build_steps();
     int64_t plan_arena(int64_t chunk_cap, bool assign);
     void prepare_chunks(const std::vector<uint64_t>& groups, int64_t chunk_cap);
+    void bind_groups(const std::vector<uint64_t>& groups);
+    void run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
+                   uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n);
     void free_chunks();
     void exec_level(int level, const ChunkData* ch);
     void exec_step(const StepInfo& s, const ChunkData* ch);
@@ -155,8 +159,25 @@ class Program {
     double* d_comp_ = nullptr;
     int64_t acc_cap_ = 0;
     std::vector<ChunkData> chunks_;
+    std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
     uint64_t launches_ = 0;
     uint64_t exec_flops_ = 0;
+
+    // profiling: event pairs around launches, by kernel class
+    enum Cat { kCatGemmSimt = 0, kCatGemmTc = 1, kCatPermute = 2, kCatGemv = 3 };
+    struct Mark {
+        int cat;
+        uint64_t work;
+        int step;  // program step index
+        int64_t m, n, k, batch;
+    };
+    bool profile_ = false;
+    std::vector<cudaEvent_t> ev_pool_;
+    std::vector<Mark> marks_;
+    int mark_begin();
+    void mark_end(int idx, int cat, uint64_t work, int step = -1, int64_t m = 0, int64_t n = 0,
+                  int64_t k = 0, int64_t batch = 0);
+    void collect_marks(rcsg_stats* stats);
 };
 
 }  // namespace rcsg

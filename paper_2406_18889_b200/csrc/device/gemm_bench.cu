@@ -1,0 +1,124 @@
+// Isolated complex-GEMM check + timing (C ABI rcsg_gemm_selftest), used by the
+// GPU tests and the kernel-tuning scripts: random planar operands, tensor-core
+// result vs the fp32 SIMT kernel, CUDA-event time per launch.
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "executor.hpp"
+#include "kernels.cuh"
+
+namespace rcsg {
+namespace {
+
+__global__ void fill_rand(float* p, int64_t n, uint64_t seed) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        p[i] = static_cast<float>(static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    }
+}
+
+__global__ void diff_kernel(const float* a, const float* b, int64_t n, double* out) {
+    double num = 0, den = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double d = static_cast<double>(a[i]) - b[i];
+        num += d * d;
+        den += static_cast<double>(b[i]) * b[i];
+    }
+    atomicAdd(out, num);
+    atomicAdd(out + 1, den);
+}
+
+}  // namespace
+}  // namespace rcsg
+
+using namespace rcsg;
+
+extern "C" int rcsg_gemm_selftest(int64_t m, int64_t n, int64_t k, int64_t batch, int32_t gathered, int32_t iters,
+                                  double* out_rel_err, double* out_ms_tc, double* out_ms_simt) {
+    try {
+        // A: [batch][m][k] (or [m*batch][k] folded), B: [batch or 1][n][k], C: [batch][m][n]
+        const int64_t a_el = batch * m * k, b_el = (gathered ? batch : 1) * n * k, c_el = batch * m * n;
+        float *a, *b, *c1, *c2;
+        double* d;
+        int32_t *ia, *ib, *fault;
+        if (cudaMalloc(&a, 2 * a_el * 4) || cudaMalloc(&b, 2 * b_el * 4) || cudaMalloc(&c1, 2 * c_el * 4) ||
+            cudaMalloc(&c2, 2 * c_el * 4) || cudaMalloc(&d, 16) || cudaMalloc(&ia, batch * 4) ||
+            cudaMalloc(&ib, batch * 4) || cudaMalloc(&fault, 4))
+            return RCSG_ERR_DEVICE;
+        fill_rand<<<1024, 256>>>(a, 2 * a_el, 1);
+        fill_rand<<<1024, 256>>>(b, 2 * b_el, 2);
+        std::vector<int32_t> idx(batch);
+        for (int64_t i = 0; i < batch; ++i) idx[i] = static_cast<int32_t>(i);
+        cudaMemcpy(ia, idx.data(), batch * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(ib, idx.data(), batch * 4, cudaMemcpyHostToDevice);
+        GemmArgs g{};
+        g.a = a;
+        g.a_plane = a_el;
+        g.b = b;
+        g.b_plane = b_el;
+        g.k = k;
+        g.n = n;
+        g.fault = fault;
+        if (gathered) {
+            g.m = m;
+            g.batch = batch;
+            g.a_batch = m * k;
+            g.b_batch = n * k;
+            g.c_batch = m * n;
+            g.ia = ia;
+            g.ib = ib;
+        } else {
+            g.m = m * batch;
+            g.batch = 1;
+        }
+        g.c_plane = c_el;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float ms_tc = 0, ms_simt = 0;
+        g.c = c1;
+        const bool tc = gemm_tc_supported(g);
+        if (tc) {
+            launch_gemm_tc(g, 1, 0);
+            cudaEventRecord(e0);
+            for (int i = 0; i < iters; ++i) launch_gemm_tc(g, 1, 0);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms_tc, e0, e1);
+        }
+        g.c = c2;
+        launch_gemm_simt<float>(g, 0);
+        cudaEventRecord(e0);
+        for (int i = 0; i < std::max(1, iters / 4); ++i) launch_gemm_simt<float>(g, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms_simt, e0, e1);
+        cudaMemset(d, 0, 16);
+        if (tc) diff_kernel<<<1024, 256>>>(c1, c2, 2 * c_el, d);
+        double h[2] = {0, 1};
+        cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+        const cudaError_t err = cudaGetLastError();
+        *out_rel_err = tc ? std::sqrt(h[0] / h[1]) : -1.0;
+        *out_ms_tc = tc ? ms_tc / iters : -1.0;
+        *out_ms_simt = ms_simt / std::max(1, iters / 4);
+        cudaFree(a);
+        cudaFree(b);
+        cudaFree(c1);
+        cudaFree(c2);
+        cudaFree(d);
+        cudaFree(ia);
+        cudaFree(ib);
+        cudaFree(fault);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return err == cudaSuccess ? RCSG_OK : RCSG_ERR_DEVICE;
+    } catch (...) {
+        return RCSG_ERR_DEVICE;
+    }
+}

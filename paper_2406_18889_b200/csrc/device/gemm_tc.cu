@@ -1,7 +1,397 @@
-// tcgen05 tensor-core complex GEMM (placeholder until the sm_100a kernel lands).
+// tcgen05 tensor-core complex GEMM for sm_100a (kind::tf32, fp32 accumulate in TMEM).
+//
+//   C[v][m][n] = sum_k A[ia(v)][m][k] * B[ib(v)][n][k]      (planar complex, K-major)
+//
+// 4M complex product on real tensor cores: two TMEM accumulators per tile,
+//   Re += Ar*Br + (-Ai)*Bi      (the second MMA sets the A-negate bit of the
+//   Im += Ar*Bi +   Ai *Br       instruction descriptor)
+// CTA = 128 threads: warp 0 lane 0 issues TMA (4 planes per stage into a
+// 3-4 stage SWIZZLE_128B ring guarded by mbarriers), warp 1 lane 0 issues the
+// MMAs and commits stages back to the producer; after the last k-block all four
+// warps drain TMEM (tcgen05.ld 32x32b) and store fp32 planes with a non-finite
+// check.  Small output grids use split-K with a fixed-order reduction kernel
+// (deterministic).  Replaces the reference's naive ikj complex<double> loop
+// (contraction_engine.cpp:115-123).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
 #include "kernels.cuh"
 
 namespace rcsg {
-bool gemm_tc_supported(const GemmArgs&) { return false; }
-void launch_gemm_tc(const GemmArgs&, int, cudaStream_t) {}
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;  // fp32 elements = 128 B = one swizzle row
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 "version 1"):
+// start address >> 4, SBO = 1024 B between 8-row atoms, layout type 2.
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    uint64_t d = (addr >> 4) & 0x3FFF;
+    d |= uint64_t{1} << 16;             // LBO (unused for swizzled K-major)
+    d |= uint64_t{1024 >> 4} << 32;     // SBO
+    d |= uint64_t{1} << 46;             // descriptor version (sm_100)
+    d |= uint64_t{2} << 61;             // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N=bn.
+__host__ __device__ constexpr uint32_t idesc_tf32(int bn, bool neg_a) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (neg_a ? (1u << 13) : 0u) |
+           (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcParams {
+    int64_t m, n, k;        // per-variant GEMM shape
+    int64_t batch;          // C variants
+    int64_t mt, nt;         // tiles per variant
+    int64_t k_chunk;        // k elements per split
+    int splits;
+    const int32_t* ia;      // gather tables (mode 2) or nullptr
+    const int32_t* ib;
+    int a_batched, b_batched;
+    float* c;               // C re-plane (or split-K workspace)
+    int64_t c_plane, c_batch;
+    int64_t ws_split;       // workspace elements per split (split-K), 0 otherwise
+    int32_t step;
+    int32_t* fault;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+    static constexpr int kATile = kBM * kBK * 4;  // bytes per A plane tile
+    static constexpr int kBTile = BN * kBK * 4;
+    static constexpr int kStage = 2 * kATile + 2 * kBTile;
+    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
+                   const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
+                   const TcParams p) {
+    using S = Smem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // tile coordinates
+    int64_t t = blockIdx.x;
+    const int split = static_cast<int>(t % p.splits);
+    t /= p.splits;
+    const int64_t ntile = t % p.nt;
+    t /= p.nt;
+    const int64_t mtile = t % p.mt;
+    const int64_t v = t / p.mt;
+    const int m0 = static_cast<int>(mtile * kBM), n0 = static_cast<int>(ntile * BN);
+    const int av = p.ia ? p.ia[v] : (p.a_batched ? static_cast<int>(v) : 0);
+    const int bv = p.ib ? p.ib[v] : (p.b_batched ? static_cast<int>(v) : 0);
+    const int64_t k_begin = split * p.k_chunk;
+    const int64_t k_end = min(p.k, k_begin + p.k_chunk);
+    const int kblocks = static_cast<int>((k_end - k_begin + kBK - 1) / kBK);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % STAGES;
+            const uint32_t round = kb / STAGES;
+            if (kb >= STAGES) mbar_wait(&empty[s], (round - 1) & 1);
+            uint8_t* st = smem + s * S::kStage;
+            mbar_expect_tx(&full[s], S::kStage);
+            const int kc = static_cast<int>(k_begin) + kb * kBK;
+            tma_load_3d(st, &map_ar, &full[s], kc, m0, av);
+            tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, m0, av);
+            tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, n0, bv);
+            tma_load_3d(st + 2 * S::kATile + S::kBTile, &map_bi, &full[s], kc, n0, bv);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer (single thread)
+        constexpr uint32_t id_pos = idesc_tf32(BN, false), id_neg = idesc_tf32(BN, true);
+        const uint32_t t_re = tmem, t_im = tmem + BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(&full[s], (kb / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint8_t* st = smem + s * S::kStage;
+            const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
+            const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
+#pragma unroll
+            for (int j = 0; j < kBK / 8; ++j) {
+                const uint64_t o = static_cast<uint64_t>(j * 32) >> 4;  // 8 tf32 = 32 B along K
+                const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+                mma_tf32(t_re, dar + o, dbr + o, id_pos, acc);
+                mma_tf32(t_re, dai + o, dbi + o, id_neg, 1u);
+                mma_tf32(t_im, dar + o, dbi + o, id_pos, acc);
+                mma_tf32(t_im, dai + o, dbr + o, id_pos, 1u);
+            }
+            mma_commit(&empty[s]);  // frees the stage once these MMAs retire
+        }
+        mma_commit(done);
+    }
+    __syncwarp();
+
+    // ---- epilogue: all 4 warps, warp w owns TMEM lanes [32w, 32w+32) = tile rows
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t row = m0 + warp * 32 + lane;
+    float* cre = p.c + split * p.ws_split + v * p.c_batch;
+    float* cim = cre + p.c_plane;
+    bool bad = false;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        float re[32], im[32];
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        tmem_ld32(tmem + lane_base + c0, re);
+        tmem_ld32(tmem + lane_base + BN + c0, im);
+        if (kblocks == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) re[i] = im[i] = 0.f;
+        }
+        if (row < p.m) {
+            const int64_t col0 = n0 + c0;
+            float* pr = cre + row * p.n + col0;
+            float* pi = cim + row * p.n + col0;
+            if (col0 + 32 <= p.n && (p.n & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
+                    *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
+            } else {
+                for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+                    pr[i] = re[i];
+                    pi[i] = im[i];
+                    bad |= !isfinite(re[i]) || !isfinite(im[i]);
+                }
+            }
+        }
+    }
+    if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+}
+
+// Fixed-order split-K reduction: C = sum_z W[z]  (planar; W laid out like C per split).
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int64_t ws_split, int splits,
+                                     float* __restrict__ c, int64_t c_plane, int64_t total_per_plane,
+                                     int32_t step, int32_t* fault) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 2 * total_per_plane;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int plane = i >= total_per_plane;
+        const int64_t e = i - plane * total_per_plane;
+        float s = 0.f;
+        for (int z = 0; z < splits; ++z) s += ws[z * ws_split + plane * total_per_plane + e];
+        c[plane * c_plane + e] = s;
+        bad |= !isfinite(s);
+    }
+    if (bad && fault) atomicMin(fault, step);
+}
+
+// ---- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+// 3D map over a [batch][rows][k] fp32 plane, box {32 k, box_rows, 1}, SWIZZLE_128B.
+CUtensorMap make_map(const void* base, int64_t k, int64_t rows, int64_t batch, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows),
+                          static_cast<cuuint64_t>(std::max<int64_t>(batch, 1))};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * 4), static_cast<cuuint64_t>(k * rows * 4)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <int BN, int STAGES>
+void launch(const GemmArgs& g, cudaStream_t st) {
+    using S = Smem<BN, STAGES>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+        configured = true;
+    }
+    const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
+    const int64_t a_batches = g.a_batch ? std::max<int64_t>(1, g.a_plane / std::max<int64_t>(g.a_batch, 1)) : 1;
+    const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
+    const float* a = static_cast<const float*>(g.a);
+    const float* b = static_cast<const float*>(g.b);
+    const CUtensorMap ar = make_map(a, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap ai = make_map(a + g.a_plane, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap br = make_map(b, g.k, g.n, b_batches, BN);
+    const CUtensorMap bi = make_map(b + g.b_plane, g.k, g.n, b_batches, BN);
+    TcParams p{};
+    p.m = g.m;
+    p.n = g.n;
+    p.k = g.k;
+    p.batch = g.batch;
+    p.mt = (g.m + kBM - 1) / kBM;
+    p.nt = (g.n + BN - 1) / BN;
+    p.ia = g.ia;
+    p.ib = g.ib;
+    p.a_batched = g.a_batch != 0;
+    p.b_batched = g.b_batch != 0;
+    p.step = g.step;
+    p.fault = g.fault;
+    const int64_t tiles = p.mt * p.nt * g.batch;
+    const int64_t kblocks = (g.k + kBK - 1) / kBK;
+    // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
+    int splits = 1;
+    while (tiles * splits < 296 && kblocks / (splits * 2) >= 8) splits *= 2;
+    p.splits = splits;
+    p.k_chunk = ((kblocks + splits - 1) / splits) * kBK;
+    const int64_t c_elems = g.batch * g.m * g.n;  // per plane
+    if (splits == 1) {
+        p.c = static_cast<float*>(g.c);
+        p.c_plane = g.c_plane;
+        p.c_batch = g.c_batch ? g.c_batch : g.m * g.n;
+        p.ws_split = 0;
+    } else {
+        float* ws = static_cast<float*>(device_workspace(static_cast<size_t>(splits) * 2 * c_elems * sizeof(float), st));
+        p.c = ws;
+        p.c_plane = c_elems;
+        p.c_batch = g.m * g.n;
+        p.ws_split = 2 * c_elems;
+    }
+    gemm_tc_kernel<BN, STAGES><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br, bi, p);
+    if (splits > 1) {
+        const int grid = static_cast<int>(std::min<int64_t>((2 * c_elems + 255) / 256, 148 * 16));
+        splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.c, p.ws_split, splits, static_cast<float*>(g.c), g.c_plane,
+                                                   c_elems, g.step, g.fault);
+    }
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& g) {
+    // tensor-core tiles need >= 64 rows, >= 16 columns and a 16-B aligned K stride;
+    // tiny contractions stay on the SIMT kernel (launch-bound either way).
+    if (g.m < 64 || g.n < 16 || g.k < 4) return false;
+    if (g.m * g.n * g.k < (int64_t{1} << 21)) return false;
+    if (g.batch > 1 && !g.ia) return false;  // batched GEMMs are always gathered here
+    if (g.k > (int64_t{1} << 31) || g.m * std::max<int64_t>(g.batch, 1) > (int64_t{1} << 31)) return false;
+    return true;
+}
+
+void launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t st) {
+    (void)passes;
+    if (g.n >= 128) launch<128, 3>(g, st);
+    else launch<64, 4>(g, st);
+}
+
 }  // namespace rcsg

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <stdexcept>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "kernels.cuh"
@@ -211,17 +213,30 @@ template void launch_permute<double>(const double*, int64_t, double*, int64_t, i
 // tensor-core kernel does not cover (tiny m/n/k).
 constexpr int BM = 64, BN = 64, BK = 16;
 
+struct SplitK {
+    int splits;
+    int64_t k_chunk;
+    void* ws;          // nullptr: write C directly
+    int64_t ws_split;  // elements per split (both planes)
+};
+
 template <typename R>
-__global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const SplitK sk) {
     __shared__ R As_re[BK][BM + 1], As_im[BK][BM + 1];
     __shared__ R Bs_re[BK][BN + 1], Bs_im[BK][BN + 1];
     const R* A = static_cast<const R*>(g.a);
     const R* B = static_cast<const R*>(g.b);
     R* Cm = static_cast<R*>(g.c);
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
-    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
-    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
-    for (int64_t v = blockIdx.z; v < g.batch; v += gridDim.z) {
+    const int64_t mt = (g.m + BM - 1) / BM, nt = (g.n + BN - 1) / BN;
+    const int64_t tiles = mt * nt * g.batch * sk.splits;
+    for (int64_t tile_s = blockIdx.x; tile_s < tiles; tile_s += gridDim.x) {
+        const int split = static_cast<int>(tile_s % sk.splits);
+        const int64_t tile = tile_s / sk.splits;
+        const int64_t k_lo = split * sk.k_chunk, k_hi = min(g.k, k_lo + sk.k_chunk);
+        const int64_t v = tile / (mt * nt);
+        const int64_t rem = tile - v * mt * nt;
+        const int64_t m0 = (rem / nt) * BM, n0 = (rem % nt) * BN;
         const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
         const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
         const R* Ab = A + av * g.a_batch;
@@ -231,7 +246,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc_re[i][j] = acc_im[i][j] = R(0);
-        for (int64_t k0 = 0; k0 < g.k; k0 += BK) {
+        for (int64_t k0 = k_lo; k0 < k_hi; k0 += BK) {
             // 64 rows x 16 k per operand: 1024 elements, 4 per thread
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
                 const int row = e >> 4, kk = e & 15;
                 const int64_t gk = k0 + kk;
                 R ar = 0, ai = 0, br = 0, bi = 0;
-                if (gk < g.k) {
+                if (gk < k_hi) {
                     if (m0 + row < g.m) {
                         const int64_t o = (m0 + row) * g.k + gk;
                         ar = Ab[o];
@@ -279,7 +294,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
             }
             __syncthreads();
         }
-        R* Cb = Cm + v * g.c_batch;
+        R* Cb = sk.ws ? static_cast<R*>(sk.ws) + split * sk.ws_split + v * g.m * g.n : Cm + v * g.c_batch;
+        const int64_t cplane = sk.ws ? g.batch * g.m * g.n : g.c_plane;
         bool bad = false;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -289,21 +305,70 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
                 if (m < g.m && n < g.n) {
                     const int64_t o = m * g.n + n;
                     Cb[o] = acc_re[i][j];
-                    Cb[g.c_plane + o] = acc_im[i][j];
+                    Cb[cplane + o] = acc_im[i][j];
                     bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
                 }
             }
-        if (bad && g.fault) atomicMin(g.fault, g.step);
+        if (bad && g.fault && !sk.ws) atomicMin(g.fault, g.step);
     }
+}
+
+// Fixed-order split-K reduction: C = sum_z W[z] (W planar [batch][m][n] per split).
+template <typename R>
+__global__ void splitk_reduce_simt(const R* __restrict__ ws, int64_t ws_split, int splits, R* __restrict__ c,
+                                   int64_t c_plane, int64_t per_plane, int32_t step, int32_t* fault) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 2 * per_plane;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int plane = i >= per_plane;
+        const int64_t e = i - plane * per_plane;
+        R s = 0;
+        for (int z = 0; z < splits; ++z) s += ws[z * ws_split + plane * per_plane + e];
+        c[plane * c_plane + e] = s;
+        bad |= !isfinite(s);
+    }
+    if (bad && fault) atomicMin(fault, step);
 }
 
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
     dim3 block(16, 16);
-    dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM),
-              static_cast<unsigned>(std::min<int64_t>(g.batch, 65535)));
-    if (grid.y > 65535) throw std::runtime_error("gemm m too large for SIMT path");
-    gemm_simt_kernel<R><<<grid, block, 0, st>>>(g);
+    const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
+    // split long K loops until the grid covers two waves (deterministic reduction)
+    SplitK sk{1, g.k, nullptr, 0};
+    while (tiles * sk.splits < 296 && g.k / (sk.splits * 2) >= 256) sk.splits *= 2;
+    if (sk.splits > 1) {
+        sk.k_chunk = (g.k + sk.splits - 1) / sk.splits;
+        sk.ws_split = 2 * g.batch * g.m * g.n;
+        sk.ws = device_workspace(static_cast<size_t>(sk.splits) * sk.ws_split * sizeof(R), st);
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(tiles * sk.splits, 148 * 32));
+    gemm_simt_kernel<R><<<grid, block, 0, st>>>(g, sk);
+    if (sk.splits > 1) {
+        const int64_t per_plane = g.batch * g.m * g.n;
+        const int rg = static_cast<int>(std::min<int64_t>((2 * per_plane + 255) / 256, 148 * 16));
+        splitk_reduce_simt<R><<<std::max(rg, 1), 256, 0, st>>>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits,
+                                                               static_cast<R*>(g.c), g.c_plane, per_plane, g.step,
+                                                               g.fault);
+    }
+}
+
+void* device_workspace(size_t bytes, cudaStream_t st) {
+    // one growing scratch buffer per stream (launches on a stream are ordered)
+    static std::map<cudaStream_t, std::pair<void*, size_t>> pool;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& e = pool[st];
+    if (bytes > e.second) {
+        if (e.first) {
+            cudaStreamSynchronize(st);
+            cudaFree(e.first);
+        }
+        e.first = nullptr;
+        if (cudaMalloc(&e.first, bytes) != cudaSuccess) throw std::runtime_error("workspace allocation failed");
+        e.second = bytes;
+    }
+    return e.first;
 }
 template void launch_gemm_simt<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_simt<double>(const GemmArgs&, cudaStream_t);

@@ -90,6 +90,14 @@ struct GemmArgs {
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
 
+// Batched complex GEMV for steps with <= 4 output columns (or rows) and long K.
+bool gemv_supported(const GemmArgs& g);
+template <typename R>
+void launch_gemv(const GemmArgs& g, cudaStream_t st);
+
+// Scratch buffer for split-K partials, one per stream (grown on demand).
+void* device_workspace(size_t bytes, cudaStream_t st);
+
 // tcgen05 tensor-core path (float storage; kind::tf32, 1 or 3 passes).
 bool gemm_tc_supported(const GemmArgs& g);
 void launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t st);

@@ -57,17 +57,22 @@ struct Handle {
     bool has_config = false;
     std::unique_ptr<Flat> flat;
     std::map<std::pair<int, std::uint64_t>, rcsg_program*> programs;
+    bool profile = false;
     ~Handle() {
         for (auto& [k, p] : programs) rcsg_program_free(p);
     }
     rcsg_program* program(int precision, std::uint64_t budget) {
         auto key = std::make_pair(precision, budget);
         auto it = programs.find(key);
-        if (it != programs.end()) return it->second;
-        if (!flat) flat = flatten(net, plan);
         rcsg_program* p = nullptr;
-        if (int rc = rcsg_compile(&flat->net, &flat->plan, precision, budget, &p)) raise_rcsg(rc);
-        programs[key] = p;
+        if (it != programs.end()) {
+            p = it->second;
+        } else {
+            if (!flat) flat = flatten(net, plan);
+            if (int rc = rcsg_compile(&flat->net, &flat->plan, precision, budget, &p)) raise_rcsg(rc);
+            programs[key] = p;
+        }
+        rcsg_program_set_profile(p, profile ? 1 : 0);
         return p;
     }
 };
@@ -167,6 +172,16 @@ int rcsh_build_network(int n_leaves, const int* leaf_rank, const int* leaf_label
 }
 
 void rcsh_free(void* h) { delete static_cast<Handle*>(h); }
+
+void rcsh_set_profile(void* h, int on) { static_cast<Handle*>(h)->profile = on != 0; }
+
+// Stream of the handle's compiled program for (precision, budget); compiles it if needed.
+int rcsh_program_stream(void* hp, int precision, std::uint64_t budget, void** out) {
+    return guarded([&] {
+        rcsg_program* p = static_cast<Handle*>(hp)->program(precision, budget);
+        if (int rc = rcsg_program_stream(p, out)) raise_rcsg(rc);
+    });
+}
 
 void rcsh_net_sizes(void* hp, std::int64_t* sizes) {
     const Handle* h = static_cast<Handle*>(hp);

@@ -1,0 +1,143 @@
+"""GPU parity of the contraction path against the CPU oracle (reference library
+oracle/_ref and the C restatement oracle/port), on the same circuits, seeds and
+plans.  Tolerances are norm-wise relative error per group, per precision mode
+(SURVEY §8c): f64 1e-10, f32 1e-5, tf32 1e-2, 3xtf32 1e-5.
+"""
+import numpy as np
+import pytest
+
+import paper_2406_18889_b200 as pb
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-10, "f32": 2e-5, "tf32": 1e-2, "3xtf32": 2e-5}
+
+
+def rel(a, b):
+    a = np.asarray(a).reshape(-1)
+    b = np.asarray(b).reshape(-1)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def cfg1(M=64):
+    p = pb.Problem(12, 8, "grid(3,4)", 1, [0, 1, 2], 1 << 30, "low").build()
+    fixed, _ = pb.build_candidate_set(12, [0, 1, 2], M, pb.split_next(1, 0xCA11D))
+    return p, fixed
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32", "tf32", "3xtf32"])
+def test_cfg1_groups_match_oracle(precision):
+    p, fixed = cfg1(64)
+    pn = port.PortNet(p.net, p.plan)
+    got = p.contract_groups(fixed, precision=precision)
+    for g, fb in enumerate(fixed):
+        want = pn.contract_group(int(fb))
+        assert rel(got[g], want) < TOL[precision], (g, rel(got[g], want))
+
+
+def test_cfg1_group_batching_equals_single_groups():
+    p, fixed = cfg1(128)
+    batch = p.contract_groups(fixed)
+    for g in range(0, 128, 17):
+        single = p.contract_group(int(fixed[g]))
+        assert rel(batch[g], single) < 1e-13
+
+
+def test_sliced_plan_matches_oracle_and_slice_sum():
+    p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
+    assert len(p.plan["sliced"]) >= 3
+    pn = port.PortNet(p.net, p.plan)
+    fixed = np.array([0, 5, 22, 63], np.uint64)
+    got = p.contract_groups(fixed)
+    for g, fb in enumerate(fixed):
+        assert rel(got[g], pn.contract_group(int(fb))) < 1e-10
+    # linearity over disjoint slice ranges
+    half = p.n_slices // 2
+    a = p.contract_groups(fixed, slices=(0, half))
+    b = p.contract_groups(fixed, slices=(half, p.n_slices))
+    assert rel(a + b, got) < 1e-12
+
+
+def test_broken_edges_path_sum_matches_oracle():
+    p = pb.Problem(10, 10, "ring", 62, list(range(10)), 1 << 30, "low", 5, 16).build()
+    pn = port.PortNet(p.net, p.plan)
+    want = pn.contract_group(0, configs=p.plan["configs"])
+    got = p.contract_groups([0])[0]
+    assert rel(got, want) < 1e-10
+    amps, flops = p.contract(configs="all")
+    assert rel(amps, want) < 1e-10
+    assert flops == p.plan["flops_per_slice"] * p.n_slices * len(p.plan["configs"])
+
+
+def test_complete_path_sum_reproduces_exact():
+    # test_contraction.cpp:55-67 — summing all 2^K configurations is exact
+    for K in (2, 4):
+        p = pb.Problem(10, 10, "line", 40 + K, list(range(10)), 1 << 30, "low", K, 1 << K).build()
+        exact = pb.Problem(10, 10, "line", 40 + K, list(range(10)), 1 << 30, "low").build()
+        full = exact.contract_groups([0], configs=None)[0]
+        summed = p.contract_groups([0])[0]
+        assert rel(summed, full) < 1e-10
+
+
+def test_contract_group_matches_statevector_slice():
+    # test_tensor_network.cpp:84-109 / test_contraction.cpp:174-198
+    n = 12
+    p = pb.Problem(n, n, "line", 31, [0, 2, 5, 7], 1 << 30, "low").build()
+    sv = port.statevector(n, p.gates())
+    fixed_q = [q for q in range(n) if q not in (0, 2, 5, 7)]
+    for fb in (0, 0b101101, (1 << len(fixed_q)) - 1):
+        amps = p.contract_group(fb)
+        for i in range(16):
+            full = sum(1 << q for j, q in enumerate((0, 2, 5, 7)) if (i >> j) & 1)
+            full |= sum(1 << q for b, q in enumerate(fixed_q) if (fb >> b) & 1)
+            assert abs(amps[i] - sv[full]) <= 1e-8 * max(abs(sv[full]), 1e-14)
+
+
+def test_execute_assignment_matches_oracle():
+    p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
+    pn = port.PortNet(p.net, p.plan)
+    for s in (0, 3, p.n_slices - 1):
+        a = p.assignment_gsc(0b101001, s)
+        assert rel(p.execute(a), pn.execute(a)) < 1e-10
+
+
+def test_numeric_fault_reports_step():
+    inf = float("inf")
+    net = dict(leaf_rank=[2, 1], leaf_labels=[0, 1, 1], leaf_data=[inf, 0, 0, 1, 1, 1], n_labels=2,
+               n_qubits=1, output_labels=[0], open_labels=[0], open_qubits=[0])
+    with pytest.raises(pb.NumericFault) as e:
+        pb.execute_desc(net, [(0, 1, 2)], [-1, -1])
+    assert e.value.step_index == 0 and e.value.exit_code == 3
+
+
+def test_two_by_two_product_layout():
+    # test_tensor_network.cpp:147-178: output index (c<<1)|a
+    A = [1, 2j, -1 + 1j, 3]
+    B = [1j, 2, 1 - 1j, 0]
+    net = dict(leaf_rank=[2, 2], leaf_labels=[0, 1, 1, 2], leaf_data=A + B, n_labels=3, n_qubits=2,
+               output_labels=[0, 2], open_labels=[0, 2], open_qubits=[0, 1])
+    out = pb.execute_desc(net, [(0, 1, 2)], [-1, -1, -1])
+    for a in range(2):
+        for c in range(2):
+            want = A[a * 2] * B[c] + A[a * 2 + 1] * B[2 + c]
+            assert abs(out[(c << 1) | a] - want) < 1e-12
+
+
+def test_empty_circuit_scalar():
+    # test_tensor_network.cpp:43-61 — three |0> caps, all outputs pinned
+    p = pb.Problem.from_network([1, 1, 1], [0, 1, 2], [1, 0, 1, 0, 1, 0], ["q0.in", "q1.in", "q2.in"],
+                                3, [0, 1, 2], [], [])
+    assert p.contract_groups([0], configs=None)[0][0] == pytest.approx(1.0)
+    assert abs(p.contract_groups([0b010], configs=None)[0][0]) < 1e-12
+
+
+def test_error_taxonomy():
+    p = pb.Problem(6, 6, "line", 9, list(range(6)), 1 << 30, "low").build()
+    with pytest.raises(pb.ConfigError):
+        p.execute({9999: 0})
+    with pytest.raises(pb.ConfigError):
+        p.execute({0: 2})
+    with pytest.raises(pb.ConfigError):  # exact contraction of a plan with broken edges
+        q = pb.Problem(6, 6, "line", 9, list(range(6)), 1 << 30, "low", 2, 2).build()
+        q.contract_groups([0], configs=None)
