@@ -1,10 +1,12 @@
 // Step-program executor; see executor.hpp for the design.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <iterator>
 #include <numeric>
 
 #include "executor.hpp"
@@ -203,43 +205,127 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
 }
 
 void Program::build_steps() {
+    // Layout planning.  Every step contracts its shared labels in canonical
+    // (ascending label id) order, and orders its output as
+    //   [labels its consumer keeps | labels its consumer contracts, canonical]
+    // whenever that is achievable as [keep(M side) | keep(N side)] and cheaper
+    // than letting the consumer permute the result.  Producers that comply
+    // hand their consumer an operand that needs no permute at all.
+    const int n_nodes = static_cast<int>(nodes_.size());
+    std::vector<std::vector<int>> lset(n_nodes);
+    for (int i = 0; i < n_leaves_; ++i) {
+        lset[i] = nodes_[i].labels;
+        std::sort(lset[i].begin(), lset[i].end());
+    }
+    std::vector<int> sibling(n_nodes, -1), consumer(n_nodes, -1);
+    for (size_t s = 0; s < steps_.size(); ++s) {
+        const StepInfo& st = steps_[s];
+        std::vector<int>& out = lset[st.r];
+        out.clear();
+        std::set_symmetric_difference(lset[st.a].begin(), lset[st.a].end(), lset[st.b].begin(), lset[st.b].end(),
+                                      std::back_inserter(out));
+        sibling[st.a] = st.b;
+        sibling[st.b] = st.a;
+        consumer[st.a] = consumer[st.b] = static_cast<int>(s);
+    }
+    auto size_of = [&](int id) {
+        const NodeInfo& nd = nodes_[id];
+        const int vb = nd.level == 2 ? std::min(6, __builtin_popcountll(nd.var_mask)) : 0;
+        return std::ldexp(1.0, static_cast<int>(lset[id].size()) + vb);
+    };
+    auto minus = [](const std::vector<int>& v, const std::vector<int>& sorted_set) {
+        std::vector<int> o;
+        for (int x : v)
+            if (!std::binary_search(sorted_set.begin(), sorted_set.end(), x)) o.push_back(x);
+        return o;
+    };
     for (StepInfo& st : steps_) {
+        const int x = st.a, y = st.b, r = st.r;
+        std::vector<int> shared;  // canonical contraction order
+        std::set_intersection(lset[x].begin(), lset[x].end(), lset[y].begin(), lset[y].end(),
+                              std::back_inserter(shared));
+        // consumer request on the result: [K (any order) | S canonical]
+        const bool has_req = consumer[r] >= 0;
+        std::vector<int> req_s;
+        if (has_req)
+            std::set_intersection(lset[r].begin(), lset[r].end(), lset[sibling[r]].begin(), lset[sibling[r]].end(),
+                                  std::back_inserter(req_s));
+        // satisfied when the consumer-contracted labels form the suffix (any order)
+        auto satisfies = [&](const std::vector<int>& out) {
+            if (!has_req || req_s.empty()) return true;
+            std::vector<int> tail(out.end() - req_s.size(), out.end());
+            std::sort(tail.begin(), tail.end());
+            return tail == req_s;
+        };
+        // candidate contraction orders: an operand's existing suffix, else canonical
+        auto suffix_order = [&](int id, std::vector<int>& o) {
+            const std::vector<int>& lab = nodes_[id].labels;
+            if (lab.size() < shared.size()) return false;
+            o.assign(lab.end() - shared.size(), lab.end());
+            std::vector<int> t = o;
+            std::sort(t.begin(), t.end());
+            return t == shared;
+        };
+        std::vector<std::vector<int>> sh_orders{shared};
+        for (int id : {x, y}) {
+            std::vector<int> o;
+            if (!shared.empty() && suffix_order(id, o) && o != shared) sh_orders.push_back(o);
+        }
+        const bool vx = nodes_[x].level == 2, vy = nodes_[y].level == 2;
+        std::vector<std::pair<int, int>> roles;
+        if (vx && !vy) roles = {{x, y}};
+        else if (vy && !vx) roles = {{y, x}};
+        else roles = {{x, y}, {y, x}};
+        struct Choice {
+            double cost = 1e300;
+            int f = -1, s = -1;
+            std::vector<int> tf, ts, out;
+            size_t kf = 0;
+        } best;
+        for (auto [f, sc] : roles) {
+            const std::vector<int> keep_f = minus(nodes_[f].labels, shared), keep_s = minus(nodes_[sc].labels, shared);
+            std::vector<std::vector<int>> outs;
+            // natural order: operands' current keep orders
+            std::vector<int> nat = keep_f;
+            nat.insert(nat.end(), keep_s.begin(), keep_s.end());
+            outs.push_back(nat);
+            if (has_req) {
+                // requested order: consumer-kept labels first, then the contracted ones
+                std::vector<int> d, tail;
+                for (int l : nat)
+                    (std::binary_search(req_s.begin(), req_s.end(), l) ? tail : d).push_back(l);
+                d.insert(d.end(), tail.begin(), tail.end());
+                std::vector<int> pre(d.begin(), d.begin() + keep_f.size()), kf_sorted = keep_f;
+                std::sort(pre.begin(), pre.end());
+                std::sort(kf_sorted.begin(), kf_sorted.end());
+                if (pre == kf_sorted) outs.push_back(d);
+            }
+            for (const auto& out : outs)
+            for (const auto& sh : sh_orders) {
+                std::vector<int> tf(out.begin(), out.begin() + keep_f.size()), ts(out.begin() + keep_f.size(), out.end());
+                tf.insert(tf.end(), sh.begin(), sh.end());
+                ts.insert(ts.end(), sh.begin(), sh.end());
+                double c = 0;
+                if (tf != nodes_[f].labels) c += size_of(f);
+                if (ts != nodes_[sc].labels) c += size_of(sc);
+                if (!satisfies(out)) c += size_of(r);
+                // ties: prefer the larger M side (tensor-core tiles are 128 rows)
+                const bool better = c < best.cost || (c == best.cost && keep_f.size() > best.kf);
+                if (better) best = Choice{c, f, sc, tf, ts, out, keep_f.size()};
+            }
+        }
+        st.a = best.f;
+        st.b = best.s;
         NodeInfo* A = &nodes_[st.a];
         NodeInfo* B = &nodes_[st.b];
-        const bool va = A->level == 2, vb = B->level == 2;
-        int shared_n = 0;
-        for (int l : A->labels) shared_n += pos_in(B->labels, l) >= 0;
-        const int ka = static_cast<int>(A->labels.size()) - shared_n;
-        const int kb = static_cast<int>(B->labels.size()) - shared_n;
-        bool swap = false;
-        if (vb && !va) swap = true;
-        else if (!va && !vb && kb > ka) swap = true;
-        if (swap) {
-            std::swap(st.a, st.b);
-            std::swap(A, B);
-        }
         st.mode = (A->level == 2) ? ((B->level == 2) ? 2 : 1) : 0;
-        std::vector<int> shared, keep_a, keep_b;
-        for (int l : A->labels) (pos_in(B->labels, l) >= 0 ? shared : keep_a).push_back(l);
-        for (int l : B->labels)
-            if (pos_in(shared, l) < 0) keep_b.push_back(l);
-        // shared order: reuse an operand's existing suffix when possible
-        auto suffix_is_shared = [&](const std::vector<int>& lab) {
-            const size_t s = shared.size();
-            for (size_t i = lab.size() - s; i < lab.size(); ++i)
-                if (pos_in(shared, lab[i]) < 0) return false;
-            return true;
-        };
-        std::vector<int> sh_order = shared;
-        if (!shared.empty()) {
-            if (suffix_is_shared(A->labels))
-                sh_order.assign(A->labels.end() - shared.size(), A->labels.end());
-            else if (suffix_is_shared(B->labels))
-                sh_order.assign(B->labels.end() - shared.size(), B->labels.end());
-        }
-        std::vector<int> ta = keep_a, tb = keep_b;
-        ta.insert(ta.end(), sh_order.begin(), sh_order.end());
-        tb.insert(tb.end(), sh_order.begin(), sh_order.end());
+        const std::vector<int>& ta = best.tf;
+        const std::vector<int>& tb = best.ts;
+        if (getenv("RCSG_DUMP_STEPS") && (A->labels.size() >= 16 || B->labels.size() >= 16))
+            fprintf(stderr, "step %d lvl A%d B%d perm_a %d perm_b %d out_ok %d |A|=%zu |B|=%zu |R|=%zu\n",
+                    st.plan_index, A->level, B->level, ta != A->labels, tb != B->labels,
+                    has_req ? static_cast<int>(satisfies(best.out)) : -1, A->labels.size(), B->labels.size(),
+                    best.out.size());
         std::vector<int> bits;
         st.perm_a = ta != A->labels;
         if (st.perm_a) {
@@ -251,14 +337,13 @@ void Program::build_steps() {
             permute_bits(B->labels, tb, bits);
             st.pb = make_permute(static_cast<int>(tb.size()), bits.data());
         }
-        st.m = int64_t{1} << keep_a.size();
-        st.n = int64_t{1} << keep_b.size();
+        st.m = int64_t{1} << (ta.size() - shared.size());
+        st.n = int64_t{1} << (tb.size() - shared.size());
         st.k = int64_t{1} << shared.size();
         st.flops_per_variant = 8ull * st.m * st.n * st.k;
         plan_flops_ += st.flops_per_variant;
         NodeInfo& R = nodes_[st.r];
-        R.labels = keep_a;
-        R.labels.insert(R.labels.end(), keep_b.begin(), keep_b.end());
+        R.labels = best.out;
         if (R.labels.size() > static_cast<size_t>(kMaxRank))
             throw Failure{RCSG_ERR_CAPACITY, "intermediate rank exceeds the executor limit"};
         R.payload = int64_t{1} << R.labels.size();
@@ -480,6 +565,12 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     const uint64_t flops = st.flops_per_variant * static_cast<uint64_t>(vr);
     exec_flops_ += flops;
     const int mk = mark_begin();
+    if (gemm_smallk_supported(g)) {
+        launch_gemm_smallk<R>(g, stream_);
+        mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
+        ++launches_;
+        return;
+    }
     if (gemv_supported(g)) {
         launch_gemv<R>(g, stream_);
         mark_end(mk, kCatGemv, flops, st.plan_index, g.m, g.n, g.k, g.batch);

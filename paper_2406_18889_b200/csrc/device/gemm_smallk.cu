@@ -1,0 +1,90 @@
+// Complex GEMM for steps with K <= 16 summed elements: these are outer-product
+// like (output-write bound), so instead of tensor-core tiles each thread keeps
+// one B row (K complex values) in registers and streams output rows, writing
+// consecutive columns across the warp (128-B coalesced stores).
+//   C[v][m][n] = sum_{k<K} A[ia(v)][m][k] * B[ib(v)][n][k]
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace rcsg {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRows = 64;  // output rows per CTA
+
+template <typename R, int K>
+__global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
+    __shared__ R a_re[kRows][K], a_im[kRows][K];
+    const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + kRows - 1) / kRows;
+    const int col = threadIdx.x % nb, rsub = threadIdx.x / nb, rstep = kThreads / nb;
+    bool bad = false;
+    for (int64_t tile = blockIdx.x; tile < g.batch * mtiles * ntiles; tile += gridDim.x) {
+        const int64_t nt = tile % ntiles;
+        const int64_t mt = (tile / ntiles) % mtiles;
+        const int64_t v = tile / (ntiles * mtiles);
+        const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
+        const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
+        const R* A = static_cast<const R*>(g.a) + av * g.a_batch;
+        const R* B = static_cast<const R*>(g.b) + bv * g.b_batch;
+        R* C = static_cast<R*>(g.c) + v * g.c_batch;
+        const int64_t m0 = mt * kRows, n = nt * nb + col;
+        __syncthreads();
+        for (int e = threadIdx.x; e < kRows * K; e += kThreads) {
+            const int r = e / K, kk = e % K;
+            const bool ok = m0 + r < g.m && kk < g.k;
+            a_re[r][kk] = ok ? A[(m0 + r) * g.k + kk] : R(0);
+            a_im[r][kk] = ok ? A[g.a_plane + (m0 + r) * g.k + kk] : R(0);
+        }
+        R b_re[K], b_im[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+            const bool ok = n < g.n && kk < g.k;
+            b_re[kk] = ok ? B[n * g.k + kk] : R(0);
+            b_im[kk] = ok ? B[g.b_plane + n * g.k + kk] : R(0);
+        }
+        __syncthreads();
+        if (n < g.n) {
+            for (int r = rsub; r < kRows && m0 + r < g.m; r += rstep) {
+                R cr = 0, ci = 0;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    cr = fma(a_re[r][kk], b_re[kk], cr);
+                    cr = fma(-a_im[r][kk], b_im[kk], cr);
+                    ci = fma(a_re[r][kk], b_im[kk], ci);
+                    ci = fma(a_im[r][kk], b_re[kk], ci);
+                }
+                const int64_t o = (m0 + r) * g.n + n;
+                C[o] = cr;
+                C[g.c_plane + o] = ci;
+                bad |= !isfinite(cr) || !isfinite(ci);
+            }
+        }
+    }
+    if (bad && g.fault) atomicMin(g.fault, g.step);
+}
+
+template <typename R, int K>
+void launch_k(const GemmArgs& g, cudaStream_t st) {
+    const int nb = static_cast<int>(std::min<int64_t>(g.n, kThreads));
+    const int64_t tiles = g.batch * ((g.m + kRows - 1) / kRows) * ((g.n + nb - 1) / nb);
+    const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
+    smallk_kernel<R, K><<<std::max(grid, 1), kThreads, 0, st>>>(g, nb);
+}
+
+}  // namespace
+
+bool gemm_smallk_supported(const GemmArgs& g) { return g.k <= 16; }
+
+template <typename R>
+void launch_gemm_smallk(const GemmArgs& g, cudaStream_t st) {
+    if (g.k <= 1) launch_k<R, 1>(g, st);
+    else if (g.k <= 2) launch_k<R, 2>(g, st);
+    else if (g.k <= 4) launch_k<R, 4>(g, st);
+    else if (g.k <= 8) launch_k<R, 8>(g, st);
+    else launch_k<R, 16>(g, st);
+}
+template void launch_gemm_smallk<float>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_smallk<double>(const GemmArgs&, cudaStream_t);
+
+}  // namespace rcsg

@@ -118,6 +118,7 @@ struct TcParams {
     int64_t m, n, k;        // per-variant GEMM shape
     int64_t batch;          // C variants
     int64_t mt, nt;         // tiles per variant
+    int m_fast;             // raster order: m-tile index varies fastest
     int64_t k_chunk;        // k elements per split
     int splits;
     const int32_t* ia;      // gather tables (mode 2) or nullptr
@@ -153,13 +154,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // tile coordinates
+    // raster: the tile dimension with fewer tiles varies fastest, so CTAs that
+    // run together share the larger operand's tile through L2
     int64_t t = blockIdx.x;
     const int split = static_cast<int>(t % p.splits);
     t /= p.splits;
-    const int64_t ntile = t % p.nt;
-    t /= p.nt;
-    const int64_t mtile = t % p.mt;
-    const int64_t v = t / p.mt;
+    int64_t ntile, mtile;
+    if (p.m_fast) {
+        mtile = t % p.mt;
+        t /= p.mt;
+        ntile = t % p.nt;
+        t /= p.nt;
+    } else {
+        ntile = t % p.nt;
+        t /= p.nt;
+        mtile = t % p.mt;
+        t /= p.mt;
+    }
+    const int64_t v = t;
     const int m0 = static_cast<int>(mtile * kBM), n0 = static_cast<int>(ntile * BN);
     const int av = p.ia ? p.ia[v] : (p.a_batched ? static_cast<int>(v) : 0);
     const int bv = p.ib ? p.ib[v] : (p.b_batched ? static_cast<int>(v) : 0);
@@ -342,6 +354,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.batch = g.batch;
     p.mt = (g.m + kBM - 1) / kBM;
     p.nt = (g.n + BN - 1) / BN;
+    p.m_fast = p.mt < p.nt ? 1 : 0;
     p.ia = g.ia;
     p.ib = g.ib;
     p.a_batched = g.a_batch != 0;

@@ -72,141 +72,6 @@ template void launch_leaf_project<float>(const LeafJob*, int, const double*, con
 template void launch_leaf_project<double>(const LeafJob*, int, const double*, const uint64_t*,
                                           const PassSrc*, const PassState*, double*, cudaStream_t);
 
-// ------------------------------------------------------------------ permute
-PermuteDesc make_permute(int rank, const int* src_bit) {
-    if (rank > kMaxRank) throw std::runtime_error("tensor rank exceeds kMaxRank");
-    PermuteDesc d{};
-    d.rank = rank;
-    std::vector<int> dst_of(rank);
-    for (int q = 0; q < rank; ++q) dst_of[src_bit[q]] = q;
-    std::vector<char> inU(rank, 0);
-    int nU = 0, lo_in = 0, lo_out = 0;
-    const int cap = std::min(10, rank);
-    auto take = [&](int pos) {
-        if (inU[pos]) return true;
-        if (nU >= cap) return false;
-        inU[pos] = 1;
-        ++nU;
-        return true;
-    };
-    // grow the tile alternately along the input's and the output's fastest
-    // bits; bits already inside the tile extend the runs for free
-    for (bool progress = true; progress;) {
-        progress = false;
-        if (lo_in < rank && take(lo_in)) {
-            ++lo_in;
-            progress = true;
-        }
-        if (lo_out < rank && take(src_bit[lo_out])) {
-            ++lo_out;
-            progress = true;
-        }
-    }
-    // e ordering: U ascending by input position (input bits 0..lo_in-1 lowest)
-    std::vector<int> U;
-    for (int p = 0; p < rank; ++p)
-        if (inU[p]) U.push_back(p);
-    std::vector<int> e_of_pos(rank, -1);
-    for (int j = 0; j < nU; ++j) e_of_pos[U[j]] = j;
-    // f ordering: output positions 0..lo_out-1 first, then the rest of U by output position
-    std::vector<int> F;
-    for (int q = 0; q < lo_out; ++q) F.push_back(q);
-    std::vector<int> rest;
-    for (int p : U)
-        if (dst_of[p] >= lo_out) rest.push_back(dst_of[p]);
-    std::sort(rest.begin(), rest.end());
-    for (int q : rest) F.push_back(q);
-    d.tile_bits = nU;
-    for (int x = 0; x < 32; ++x) {
-        int64_t il = 0, ih = 0, ol = 0, oh = 0, el = 0, eh = 0;
-        for (int b = 0; b < 5; ++b) {
-            if (!((x >> b) & 1)) continue;
-            if (b < nU) {
-                il += int64_t{1} << U[b];
-                ol += int64_t{1} << F[b];
-                el += int64_t{1} << e_of_pos[src_bit[F[b]]];
-            }
-            if (b + 5 < nU) {
-                ih += int64_t{1} << U[b + 5];
-                oh += int64_t{1} << F[b + 5];
-                eh += int64_t{1} << e_of_pos[src_bit[F[b + 5]]];
-            }
-        }
-        d.in_lo[x] = static_cast<int32_t>(il);
-        d.in_hi[x] = static_cast<int32_t>(ih);
-        d.out_lo[x] = static_cast<int32_t>(ol);
-        d.out_hi[x] = static_cast<int32_t>(oh);
-        d.e_lo[x] = static_cast<int32_t>(el);
-        d.e_hi[x] = static_cast<int32_t>(eh);
-    }
-    int j = 0;
-    for (int p = 0; p < rank; ++p)
-        if (!inU[p]) {
-            d.outer_in[j] = int64_t{1} << p;
-            d.outer_out[j] = int64_t{1} << dst_of[p];
-            ++j;
-        }
-    d.n_outer = j;
-    return d;
-}
-
-template <typename R>
-__global__ void __launch_bounds__(256) permute_kernel(const R* __restrict__ in, int64_t in_plane,
-                                                      R* __restrict__ out, int64_t out_plane,
-                                                      int64_t n_var, const PermuteDesc d) {
-    __shared__ int32_t tab[6][32];
-    __shared__ R s_re[1024 + 32], s_im[1024 + 32];
-    if (threadIdx.x < 32) {
-        tab[0][threadIdx.x] = d.in_lo[threadIdx.x];
-        tab[1][threadIdx.x] = d.in_hi[threadIdx.x];
-        tab[2][threadIdx.x] = d.out_lo[threadIdx.x];
-        tab[3][threadIdx.x] = d.out_hi[threadIdx.x];
-        tab[4][threadIdx.x] = d.e_lo[threadIdx.x];
-        tab[5][threadIdx.x] = d.e_hi[threadIdx.x];
-    }
-    __syncthreads();
-    const int64_t payload = int64_t{1} << d.rank;
-    const int T = 1 << d.tile_bits;
-    const int64_t outer = int64_t{1} << d.n_outer;
-    const int64_t total = outer * n_var;
-    for (int64_t cta = blockIdx.x; cta < total; cta += gridDim.x) {
-        const int64_t v = cta >> d.n_outer;
-        const int64_t c = cta & (outer - 1);
-        int64_t bi = v * payload, bo = v * payload;
-        for (int j = 0; j < d.n_outer; ++j)
-            if ((c >> j) & 1) {
-                bi += d.outer_in[j];
-                bo += d.outer_out[j];
-            }
-        for (int e = threadIdx.x; e < T; e += blockDim.x) {
-            const int64_t off = bi + tab[0][e & 31] + tab[1][e >> 5];
-            s_re[e + (e >> 5)] = in[off];
-            s_im[e + (e >> 5)] = in[in_plane + off];
-        }
-        __syncthreads();
-        for (int f = threadIdx.x; f < T; f += blockDim.x) {
-            const int e = tab[4][f & 31] + tab[5][f >> 5];
-            const int64_t off = bo + tab[2][f & 31] + tab[3][f >> 5];
-            out[off] = s_re[e + (e >> 5)];
-            out[out_plane + off] = s_im[e + (e >> 5)];
-        }
-        __syncthreads();
-    }
-}
-
-template <typename R>
-void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, int64_t n_var,
-                    const PermuteDesc& d, cudaStream_t st) {
-    const int64_t total = (int64_t{1} << d.n_outer) * n_var;
-    const int grid = static_cast<int>(std::min<int64_t>(total, grid_cap()));
-    const int threads = d.tile_bits >= 8 ? 256 : (d.tile_bits >= 6 ? 64 : 32);
-    permute_kernel<R><<<grid, threads, 0, st>>>(in, in_plane, out, out_plane, n_var, d);
-}
-template void launch_permute<float>(const float*, int64_t, float*, int64_t, int64_t,
-                                    const PermuteDesc&, cudaStream_t);
-template void launch_permute<double>(const double*, int64_t, double*, int64_t, int64_t,
-                                     const PermuteDesc&, cudaStream_t);
-
 // ------------------------------------------------------------------ SIMT GEMM
 // 64x64 complex tile per CTA, 16x16 threads, 4x4 complex outputs per thread,
 // K step 16.  Used for fp64 (reference-grade parity) and for shapes the

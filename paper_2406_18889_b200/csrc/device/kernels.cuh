@@ -47,20 +47,22 @@ void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf
                          const uint64_t* d_codes, const PassSrc* d_pass_src,
                          const PassState* d_state, R* arena, cudaStream_t st);
 
-// ---- bit-permutation transpose of a [V][2^rank] planar tensor.
-// Output bit q (LSB=0) takes input bit src_bit[q].
-// Built on the host by make_permute(); the kernel moves one tile of up to
-// 2^10 elements per CTA through shared memory so both the reads (input-order
-// runs) and the writes (output-order runs) are coalesced.
+// ---- bit-permutation transpose of a [V][2^rank] planar tensor (permute.cu).
+// Output bit q (LSB=0) takes input bit src_bit[q].  Built on the host by
+// make_permute(); each CTA moves tiles of up to 2^11 elements through shared
+// memory so reads follow the input's contiguous runs and writes the output's,
+// both as 16-byte vectors.
+constexpr int kPermTileBits = 11;
 struct PermuteDesc {
     int32_t rank;
-    int32_t tile_bits;          // |U|: bits enumerated inside a tile
-    int32_t n_outer;            // rank - tile_bits: bits enumerated across CTAs
-    int64_t outer_in[kMaxRank];   // input stride of outer bit j
-    int64_t outer_out[kMaxRank];  // output stride of outer bit j
-    int32_t in_lo[32], in_hi[32];    // input offset of tile index e (split 5/5 bits)
-    int32_t out_lo[32], out_hi[32];  // output offset of tile index f
-    int32_t e_lo[32], e_hi[32];      // tile index e holding output element f
+    int32_t tile_bits;             // |U|: bits enumerated inside a tile
+    int32_t n_outer;               // rank - tile_bits: bits enumerated across tiles
+    int32_t vec;                   // 1: input bits 0,1 and output bits 0,1 are inside the tile runs
+    int64_t outer_in[kMaxRank];    // input stride of outer bit j
+    int64_t outer_out[kMaxRank];   // output stride of outer bit j
+    int32_t in_lo[32], in_hi[64];  // input offset of tile index e (low 5 / high 6 bits)
+    int32_t out_lo[32], out_hi[64];  // output offset of tile index f
+    int32_t e_lo[32], e_hi[64];      // tile index e holding output element f
 };
 PermuteDesc make_permute(int rank, const int* src_bit);
 template <typename R>
@@ -89,6 +91,11 @@ struct GemmArgs {
 };
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
+
+// Outer-product-like steps (K <= 16): register-blocked, coalesced output writes.
+bool gemm_smallk_supported(const GemmArgs& g);
+template <typename R>
+void launch_gemm_smallk(const GemmArgs& g, cudaStream_t st);
 
 // Batched complex GEMV for steps with <= 4 output columns (or rows) and long K.
 bool gemv_supported(const GemmArgs& g);

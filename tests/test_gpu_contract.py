@@ -141,3 +141,59 @@ def test_error_taxonomy():
     with pytest.raises(pb.ConfigError):  # exact contraction of a plan with broken edges
         q = pb.Problem(6, 6, "line", 9, list(range(6)), 1 << 30, "low", 2, 2).build()
         q.contract_groups([0], configs=None)
+
+
+# ---- against the reference's own outputs (golden fixtures, tests/golden/) -----
+GOLDEN_CASES = ["cfg1", "sliced_line10", "broken_ring10", "grid44_sliced_broken"]
+
+
+@pytest.mark.parametrize("precision", ["f64", "tf32"])
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_gpu_matches_reference_fixture(name, precision):
+    import os
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz")))
+    spec = eval(str(g["spec"]))
+    p = pb.Problem(*spec).build()
+    got = p.contract_groups(g["group_fixed"], precision=precision)
+    for i in range(len(g["group_fixed"])):
+        assert rel(got[i], g["amplitudes"][i]) < TOL[precision], (name, i)
+
+
+# ---- full-size (BASELINE cfg2 circuit, n = 30) -------------------------------
+def test_cfg2_circuit_pair_matches_live_reference(ref):
+    """One (group, slice) of the 30-qubit cfg2 circuit, planned at 2^27 B so the
+    reference executor finishes in seconds; GPU f64 and tf32 vs the reference."""
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 1 << 27, "low")
+    r = ref.RefProblem(*spec).build()
+    p = pb.Problem(*spec).build()
+    assert np.array_equal(r.plan["steps"], p.plan["steps"])
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), 2, pb.split_next(1, 0xCA11D))
+    want = r.execute_gsc(int(fixed[0]), 3)
+    for precision in ("f64", "tf32"):
+        got = p.contract_groups(fixed[:1], precision=precision, configs=None, slices=(3, 4))[0]
+        assert rel(got, want) < TOL[precision], precision
+
+
+def test_cfg2_full_size_properties():
+    """BASELINE cfg2 plan (2^8 slices): slice-range linearity, group batching vs
+    single groups, tf32 vs f64 on the same slices."""
+    p = pb.Problem(30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low").build()
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), 8, pb.split_next(1, 0xCA11D))
+    both = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 2))
+    s0 = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 1))
+    s1 = p.contract_groups(fixed, precision="tf32", configs=None, slices=(1, 2))
+    assert rel(s0 + s1, both) < 1e-6
+    single = p.contract_groups(fixed[3:4], precision="tf32", configs=None, slices=(0, 2))[0]
+    assert rel(single, both[3]) < 1e-5
+    exact = p.contract_groups(fixed[:2], precision="f64", configs=None, slices=(0, 2))
+    for g in range(2):
+        assert rel(both[g], exact[g]) < TOL["tf32"]
+
+
+def test_scheduler_blocks_on_gpu_equal_single_call():
+    from paper_2406_18889_b200 import scheduler
+    p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
+    fixed = np.array([0, 5, 22, 63], np.uint64)
+    full = p.contract_groups(fixed, precision="f64", configs=None)
+    got = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "f64"), p.n_slices)
+    assert rel(got, full) < 1e-12

@@ -9,9 +9,11 @@ from oracle import port
 pytestmark = pytest.mark.gpu
 
 
-def probs_for(fixed, l, seed):
+def probs_for(fixed, l, seed, n=12, open_q=(0, 1, 2)):
+    # a function of the bitstring index, like the reference's ProbFn
     rng = np.random.default_rng(seed)
-    return rng.exponential(size=(len(fixed), 1 << l)) / 2**12
+    table = rng.exponential(size=1 << n) / 2**n
+    return np.array([[table[pb.member(n, list(open_q), int(f), i)] for i in range(1 << l)] for f in fixed])
 
 
 @pytest.mark.parametrize("k", [1, 7, 64, 512, 4096])
@@ -43,7 +45,7 @@ def test_topk_range_errors():
 
 def test_direct_sample_bit_exact(ref):
     fixed, _ = ref.candidates(20, [0, 5, 9, 13], 4096, 77)
-    probs = probs_for(fixed, 4, 3)
+    probs = probs_for(fixed, 4, 3, n=20, open_q=(0, 5, 9, 13))
     seed = ref.split_next(1, 0xD1EC7)
     assert np.array_equal(pb.direct_sample(20, [0, 5, 9, 13], fixed, probs, seed),
                           ref.direct(20, [0, 5, 9, 13], fixed, probs, seed))
