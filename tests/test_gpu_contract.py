@@ -183,8 +183,12 @@ def test_cfg2_full_size_properties():
     s0 = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 1))
     s1 = p.contract_groups(fixed, precision="tf32", configs=None, slices=(1, 2))
     assert rel(s0 + s1, both) < 1e-6
+    # a different batch changes GEMM shapes (M fold, split-K), hence tf32 rounding
     single = p.contract_groups(fixed[3:4], precision="tf32", configs=None, slices=(0, 2))[0]
-    assert rel(single, both[3]) < 1e-5
+    assert rel(single, both[3]) < 1e-3
+    # the same call is deterministic bit for bit (fixed-order reductions, no float atomics)
+    again = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 2))
+    assert np.array_equal(again, both)
     exact = p.contract_groups(fixed[:2], precision="f64", configs=None, slices=(0, 2))
     for g in range(2):
         assert rel(both[g], exact[g]) < TOL["tf32"]
