@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -28,6 +29,16 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements = 128 B = one swizzle row
 constexpr int kThreads = 128;
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -282,6 +293,188 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
 }
 
+// ---- persistent variant: one CTA per SM loops over tiles; the accumulators are
+// double-buffered in TMEM (2 x {Re, Im} x BN columns) so the four epilogue
+// warps drain tile i while the MMA warp already accumulates tile i+1.
+//   warp 0: TMA producer   warp 1: MMA issuer   warps 2-5: epilogue (TMEM lane quarter = warp % 4)
+constexpr int kPThreads = 192;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct TileCoord {
+    int64_t v;
+    int m0, n0, split, kblocks;
+    int64_t k_begin;
+};
+
+template <int BN>
+__device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t) {
+    TileCoord c;
+    c.split = static_cast<int>(t % p.splits);
+    t /= p.splits;
+    int64_t ntile, mtile;
+    if (p.m_fast) {
+        mtile = t % p.mt;
+        t /= p.mt;
+        ntile = t % p.nt;
+        t /= p.nt;
+    } else {
+        ntile = t % p.nt;
+        t /= p.nt;
+        mtile = t % p.mt;
+        t /= p.mt;
+    }
+    c.v = t;
+    c.m0 = static_cast<int>(mtile * kBM);
+    c.n0 = static_cast<int>(ntile * BN);
+    c.k_begin = c.split * p.k_chunk;
+    const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
+    c.kblocks = static_cast<int>((k_end - c.k_begin + kBK - 1) / kBK);
+    return c;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kPThreads, 1)
+    gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
+                       const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
+                       const TcParams p, int64_t total_tiles) {
+    using S = Smem<BN, STAGES>;
+    constexpr uint32_t kCols = 4 * BN;  // 2 buffers x {Re, Im}
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            uint32_t it = 0;
+            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const TileCoord c = tile_coord<BN>(p, t);
+                const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
+                const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
+                for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                    uint8_t* st = smem + s * S::kStage;
+                    mbar_expect_tx(&full[s], S::kStage);
+                    const int kc = static_cast<int>(c.k_begin) + kb * kBK;
+                    tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
+                    tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
+                    tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
+                    tma_load_3d(st + 2 * S::kATile + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            constexpr uint32_t id_pos = idesc_tf32(BN, false), id_neg = idesc_tf32(BN, true);
+            uint32_t it = 0, j = 0;
+            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
+                const TileCoord c = tile_coord<BN>(p, t);
+                const uint32_t ab = j & 1;
+                if (j >= 2) mbar_wait(&tempty[ab], ((j >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t t_re = tmem + ab * 2 * BN, t_im = t_re + BN;
+                for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint8_t* st = smem + s * S::kStage;
+                    const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
+                    const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
+#pragma unroll
+                    for (int jj = 0; jj < kBK / 8; ++jj) {
+                        const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
+                        const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
+                        mma_tf32(t_re, dar + o, dbr + o, id_pos, acc);
+                        mma_tf32(t_re, dai + o, dbi + o, id_neg, 1u);
+                        mma_tf32(t_im, dar + o, dbi + o, id_pos, acc);
+                        mma_tf32(t_im, dai + o, dbr + o, id_pos, 1u);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[ab]);
+            }
+        }
+    } else {  // ---- epilogue warps 2..5
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        bool bad = false;
+        uint32_t j = 0;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
+            const TileCoord c = tile_coord<BN>(p, t);
+            const uint32_t ab = j & 1;
+            mbar_wait(&tfull[ab], (j >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row = c.m0 + q * 32 + lane;
+            float* cre = p.c + c.split * p.ws_split + c.v * p.c_batch;
+            float* cim = cre + p.c_plane;
+            const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float re[32], im[32];
+                tmem_ld32(base + c0, re);
+                tmem_ld32(base + BN + c0, im);
+                if (row < p.m) {
+                    const int64_t col0 = c.n0 + c0;
+                    float* pr = cre + row * p.n + col0;
+                    float* pi = cim + row * p.n + col0;
+                    if (col0 + 32 <= p.n && (p.n & 3) == 0) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
+                            *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
+                    } else {
+                        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+                            pr[i] = re[i];
+                            pi[i] = im[i];
+                            bad |= !isfinite(re[i]) || !isfinite(im[i]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+        }
+        if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
+    }
+    __syncwarp();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
 // Fixed-order split-K reduction: C = sum_z W[z]  (planar; W laid out like C per split).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int64_t ws_split, int splits,
                                      float* __restrict__ c, int64_t c_plane, int64_t total_per_plane,
@@ -366,8 +559,10 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
     int splits = 1;
     while (tiles * splits < 296 && kblocks / (splits * 2) >= 8) splits *= 2;
+    const int64_t chunk_blocks = (kblocks + splits - 1) / splits;
+    splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
-    p.k_chunk = ((kblocks + splits - 1) / splits) * kBK;
+    p.k_chunk = chunk_blocks * kBK;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     if (splits == 1) {
         p.c = static_cast<float*>(g.c);
@@ -381,7 +576,24 @@ void launch(const GemmArgs& g, cudaStream_t st) {
         p.c_batch = g.m * g.n;
         p.ws_split = 2 * c_elems;
     }
-    gemm_tc_kernel<BN, STAGES><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br, bi, p);
+    // persistent double-buffered kernel when tiles are short (epilogue-bound);
+    // one CTA per tile for long-K tiles (mainloop-bound, no scheduling tail)
+    static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
+    const bool persistent = mode == 1 || (mode == 0 && chunk_blocks <= 32);
+    if (persistent) {
+        static bool pconf = false;
+        if (!pconf) {
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 S::kBytes);
+            pconf = true;
+        }
+        const int64_t total = tiles * splits;
+        const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
+        gemm_tc_persistent<BN, STAGES><<<grid, kPThreads, S::kBytes, st>>>(ar, ai, br, bi, p, total);
+    } else {
+        gemm_tc_kernel<BN, STAGES><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br,
+                                                                                                        bi, p);
+    }
     if (splits > 1) {
         const int grid = static_cast<int>(std::min<int64_t>((2 * c_elems + 255) / 256, 148 * 16));
         splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.c, p.ws_split, splits, static_cast<float*>(g.c), g.c_plane,
