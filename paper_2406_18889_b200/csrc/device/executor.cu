@@ -205,148 +205,169 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
 }
 
 void Program::build_steps() {
-    // Layout planning.  Every step contracts its shared labels in canonical
-    // (ascending label id) order, and orders its output as
-    //   [labels its consumer keeps | labels its consumer contracts, canonical]
-    // whenever that is achievable as [keep(M side) | keep(N side)] and cheaper
-    // than letting the consumer permute the result.  Producers that comply
-    // hand their consumer an operand that needs no permute at all.
+    // Consumer-driven layouts.  Every operand is consumed as [kept labels |
+    // contracted labels] (K-major GEMM operands).  Steps are planned from the
+    // root backwards: each step fixes the layout of its two operands, and the
+    // producer of an operand (a GEMM epilogue or the leaf projection) writes its
+    // result directly in that layout through a bit-scatter store map, so no
+    // intermediate tensor is ever permuted.  Key choices:
+    //   * M side: the group-variant operand (variants fold into M), else the
+    //     operand with more kept labels;
+    //   * kept-label orders end with the run of output bits the consumer needs
+    //     fastest, so the epilogue's stores stay coalesced;
+    //   * the contraction order puts last the shared labels that sit on the same
+    //     side of both producers (their fastest output bits).
     const int n_nodes = static_cast<int>(nodes_.size());
     std::vector<std::vector<int>> lset(n_nodes);
     for (int i = 0; i < n_leaves_; ++i) {
         lset[i] = nodes_[i].labels;
         std::sort(lset[i].begin(), lset[i].end());
     }
-    std::vector<int> sibling(n_nodes, -1), consumer(n_nodes, -1);
+    std::vector<int> producer(n_nodes, -1);
+    std::vector<std::vector<int>> keep_m(steps_.size()), keep_n(steps_.size()), shared(steps_.size());
     for (size_t s = 0; s < steps_.size(); ++s) {
-        const StepInfo& st = steps_[s];
-        std::vector<int>& out = lset[st.r];
-        out.clear();
+        StepInfo& st = steps_[s];
+        std::vector<int> sh, kx, ky;
+        std::set_intersection(lset[st.a].begin(), lset[st.a].end(), lset[st.b].begin(), lset[st.b].end(),
+                              std::back_inserter(sh));
+        std::set_difference(lset[st.a].begin(), lset[st.a].end(), sh.begin(), sh.end(), std::back_inserter(kx));
+        std::set_difference(lset[st.b].begin(), lset[st.b].end(), sh.begin(), sh.end(), std::back_inserter(ky));
+        const bool vx = nodes_[st.a].level == 2, vy = nodes_[st.b].level == 2;
+        bool swap = false;
+        if (vy && !vx) swap = true;
+        else if (vx == vy && ky.size() > kx.size()) swap = true;
+        if (swap) {
+            std::swap(st.a, st.b);
+            std::swap(kx, ky);
+        }
+        st.mode = nodes_[st.a].level == 2 ? (nodes_[st.b].level == 2 ? 2 : 1) : 0;
+        keep_m[s] = kx;
+        keep_n[s] = ky;
+        shared[s] = sh;
         std::set_symmetric_difference(lset[st.a].begin(), lset[st.a].end(), lset[st.b].begin(), lset[st.b].end(),
-                                      std::back_inserter(out));
-        sibling[st.a] = st.b;
-        sibling[st.b] = st.a;
-        consumer[st.a] = consumer[st.b] = static_cast<int>(s);
+                                      std::back_inserter(lset[st.r]));
+        producer[st.r] = static_cast<int>(s);
     }
-    auto size_of = [&](int id) {
-        const NodeInfo& nd = nodes_[id];
-        const int vb = nd.level == 2 ? std::min(6, __builtin_popcountll(nd.var_mask)) : 0;
-        return std::ldexp(1.0, static_cast<int>(lset[id].size()) + vb);
+    // side of label l in the output of node `id`'s producer: 0 M, 1 N, 2 leaf
+    auto side = [&](int id, int l) {
+        const int p = producer[id];
+        if (p < 0) return 2;
+        return std::binary_search(keep_m[p].begin(), keep_m[p].end(), l) ? 0 : 1;
     };
-    auto minus = [](const std::vector<int>& v, const std::vector<int>& sorted_set) {
-        std::vector<int> o;
-        for (int x : v)
-            if (!std::binary_search(sorted_set.begin(), sorted_set.end(), x)) o.push_back(x);
-        return o;
-    };
-    for (StepInfo& st : steps_) {
-        const int x = st.a, y = st.b, r = st.r;
-        std::vector<int> shared;  // canonical contraction order
-        std::set_intersection(lset[x].begin(), lset[x].end(), lset[y].begin(), lset[y].end(),
-                              std::back_inserter(shared));
-        // consumer request on the result: [K (any order) | S canonical]
-        const bool has_req = consumer[r] >= 0;
-        std::vector<int> req_s;
-        if (has_req)
-            std::set_intersection(lset[r].begin(), lset[r].end(), lset[sibling[r]].begin(), lset[sibling[r]].end(),
-                                  std::back_inserter(req_s));
-        // satisfied when the consumer-contracted labels form the suffix (any order)
-        auto satisfies = [&](const std::vector<int>& out) {
-            if (!has_req || req_s.empty()) return true;
-            std::vector<int> tail(out.end() - req_s.size(), out.end());
-            std::sort(tail.begin(), tail.end());
-            return tail == req_s;
-        };
-        // candidate contraction orders: an operand's existing suffix, else canonical
-        auto suffix_order = [&](int id, std::vector<int>& o) {
-            const std::vector<int>& lab = nodes_[id].labels;
-            if (lab.size() < shared.size()) return false;
-            o.assign(lab.end() - shared.size(), lab.end());
-            std::vector<int> t = o;
-            std::sort(t.begin(), t.end());
-            return t == shared;
-        };
-        std::vector<std::vector<int>> sh_orders{shared};
-        for (int id : {x, y}) {
-            std::vector<int> o;
-            if (!shared.empty() && suffix_order(id, o) && o != shared) sh_orders.push_back(o);
+    std::vector<std::vector<int>> layout(n_nodes);  // required (or chosen) layout of every node
+    std::vector<std::vector<int>> ord_m(steps_.size()), ord_n(steps_.size());
+    for (int s = static_cast<int>(steps_.size()) - 1; s >= 0; --s) {
+        StepInfo& st = steps_[s];
+        std::vector<int>& L = layout[st.r];
+        if (L.empty()) {  // the root: any layout (finalize reads it through a map)
+            L = keep_m[s];
+            L.insert(L.end(), keep_n[s].begin(), keep_n[s].end());
         }
-        const bool vx = nodes_[x].level == 2, vy = nodes_[y].level == 2;
-        std::vector<std::pair<int, int>> roles;
-        if (vx && !vy) roles = {{x, y}};
-        else if (vy && !vx) roles = {{y, x}};
-        else roles = {{x, y}, {y, x}};
-        struct Choice {
-            double cost = 1e300;
-            int f = -1, s = -1;
-            std::vector<int> tf, ts, out;
-            size_t kf = 0;
-        } best;
-        for (auto [f, sc] : roles) {
-            const std::vector<int> keep_f = minus(nodes_[f].labels, shared), keep_s = minus(nodes_[sc].labels, shared);
-            std::vector<std::vector<int>> outs;
-            // natural order: operands' current keep orders
-            std::vector<int> nat = keep_f;
-            nat.insert(nat.end(), keep_s.begin(), keep_s.end());
-            outs.push_back(nat);
-            if (has_req) {
-                // requested order: consumer-kept labels first, then the contracted ones
-                std::vector<int> d, tail;
-                for (int l : nat)
-                    (std::binary_search(req_s.begin(), req_s.end(), l) ? tail : d).push_back(l);
-                d.insert(d.end(), tail.begin(), tail.end());
-                std::vector<int> pre(d.begin(), d.begin() + keep_f.size()), kf_sorted = keep_f;
-                std::sort(pre.begin(), pre.end());
-                std::sort(kf_sorted.begin(), kf_sorted.end());
-                if (pre == kf_sorted) outs.push_back(d);
-            }
-            for (const auto& out : outs)
-            for (const auto& sh : sh_orders) {
-                std::vector<int> tf(out.begin(), out.begin() + keep_f.size()), ts(out.begin() + keep_f.size(), out.end());
-                tf.insert(tf.end(), sh.begin(), sh.end());
-                ts.insert(ts.end(), sh.begin(), sh.end());
-                double c = 0;
-                if (tf != nodes_[f].labels) c += size_of(f);
-                if (ts != nodes_[sc].labels) c += size_of(sc);
-                if (!satisfies(out)) c += size_of(r);
-                // ties: prefer the larger M side (tensor-core tiles are 128 rows)
-                const bool better = c < best.cost || (c == best.cost && keep_f.size() > best.kf);
-                if (better) best = Choice{c, f, sc, tf, ts, out, keep_f.size()};
+        // kept-label orders: the output's fastest run (one side) goes last on its side
+        auto in = [](const std::vector<int>& v, int l) { return std::binary_search(v.begin(), v.end(), l); };
+        std::vector<int> om, on;
+        for (int l : L) (in(keep_m[s], l) ? om : on).push_back(l);
+        if (!L.empty()) {
+            const bool last_m = in(keep_m[s], L.back());
+            std::vector<int> tail;
+            for (auto it = L.rbegin(); it != L.rend() && in(last_m ? keep_m[s] : keep_n[s], *it) == true; ++it)
+                tail.insert(tail.begin(), *it);
+            std::vector<int>& side_ord = last_m ? om : on;
+            std::vector<int> head;
+            for (int l : side_ord)
+                if (std::find(tail.begin(), tail.end(), l) == tail.end()) head.push_back(l);
+            head.insert(head.end(), tail.begin(), tail.end());
+            side_ord = head;
+        }
+        ord_m[s] = om;
+        ord_n[s] = on;
+        // contraction order: the largest group of shared labels lying on the same
+        // side of both producers goes last (fastest), canonical inside groups
+        std::map<int, std::vector<int>> groups;
+        for (int l : shared[s]) groups[side(st.a, l) * 3 + side(st.b, l)].push_back(l);
+        // score: run length (capped at the 32-element coalescing width), then
+        // prefer the producers' column side (all epilogues store columns
+        // contiguously; row-fast stores need the row-mode kernels)
+        int best_key = -1;
+        double best_score = -1;
+        for (auto& [k, v] : groups) {
+            const int sa = k / 3, sb = k % 3;
+            const double score = std::min<size_t>(v.size(), 5) * 10.0 + (sa != 0) + (sb != 0) + 0.01 * v.size();
+            if (score > best_score) {
+                best_score = score;
+                best_key = k;
             }
         }
-        st.a = best.f;
-        st.b = best.s;
-        NodeInfo* A = &nodes_[st.a];
-        NodeInfo* B = &nodes_[st.b];
-        st.mode = (A->level == 2) ? ((B->level == 2) ? 2 : 1) : 0;
-        const std::vector<int>& ta = best.tf;
-        const std::vector<int>& tb = best.ts;
-        if (getenv("RCSG_DUMP_STEPS") && (A->labels.size() >= 16 || B->labels.size() >= 16))
-            fprintf(stderr, "step %d lvl A%d B%d perm_a %d perm_b %d out_ok %d |A|=%zu |B|=%zu |R|=%zu\n",
-                    st.plan_index, A->level, B->level, ta != A->labels, tb != B->labels,
-                    has_req ? static_cast<int>(satisfies(best.out)) : -1, A->labels.size(), B->labels.size(),
-                    best.out.size());
+        std::vector<int> sigma;
+        for (auto& [k, v] : groups)
+            if (k != best_key) sigma.insert(sigma.end(), v.begin(), v.end());
+        if (best_key >= 0) sigma.insert(sigma.end(), groups[best_key].begin(), groups[best_key].end());
+        layout[st.a] = om;
+        layout[st.a].insert(layout[st.a].end(), sigma.begin(), sigma.end());
+        layout[st.b] = on;
+        layout[st.b].insert(layout[st.b].end(), sigma.begin(), sigma.end());
+    }
+    // leaves take their required layouts (the leaf projection writes them)
+    for (int i = 0; i < n_leaves_; ++i)
+        if (!layout[i].empty()) nodes_[i].labels = layout[i];
+    // forward: operand layouts, GEMM shapes, output scatter maps
+    for (size_t s = 0; s < steps_.size(); ++s) {
+        StepInfo& st = steps_[s];
+        NodeInfo& A = nodes_[st.a];
+        NodeInfo& B = nodes_[st.b];
+        std::vector<int> ta = ord_m[s], tb = ord_n[s];
+        const std::vector<int> sigma(layout[st.a].end() - shared[s].size(), layout[st.a].end());
+        ta.insert(ta.end(), sigma.begin(), sigma.end());
+        tb.insert(tb.end(), sigma.begin(), sigma.end());
         std::vector<int> bits;
-        st.perm_a = ta != A->labels;
+        st.perm_a = ta != A.labels;  // only if a producer could not comply (should not happen)
         if (st.perm_a) {
-            permute_bits(A->labels, ta, bits);
+            permute_bits(A.labels, ta, bits);
             st.pa = make_permute(static_cast<int>(ta.size()), bits.data());
         }
-        st.perm_b = tb != B->labels;
+        st.perm_b = tb != B.labels;
         if (st.perm_b) {
-            permute_bits(B->labels, tb, bits);
+            permute_bits(B.labels, tb, bits);
             st.pb = make_permute(static_cast<int>(tb.size()), bits.data());
         }
-        st.m = int64_t{1} << (ta.size() - shared.size());
-        st.n = int64_t{1} << (tb.size() - shared.size());
-        st.k = int64_t{1} << shared.size();
+        st.m = int64_t{1} << ord_m[s].size();
+        st.n = int64_t{1} << ord_n[s].size();
+        st.k = int64_t{1} << shared[s].size();
         st.flops_per_variant = 8ull * st.m * st.n * st.k;
         plan_flops_ += st.flops_per_variant;
         NodeInfo& R = nodes_[st.r];
-        R.labels = best.out;
+        R.labels = layout[st.r];
         if (R.labels.size() > static_cast<size_t>(kMaxRank))
             throw Failure{RCSG_ERR_CAPACITY, "intermediate rank exceeds the executor limit"};
         R.payload = int64_t{1} << R.labels.size();
+        // scatter map: bit j of the row index (LSB = last label of ord_m) -> output bit
+        OutMap& om = st.om;
+        om.m_bits = static_cast<int32_t>(ord_m[s].size());
+        om.n_bits = static_cast<int32_t>(ord_n[s].size());
+        const int rr = static_cast<int>(R.labels.size());
+        bool ident = true;
+        for (int j = 0; j < om.m_bits; ++j) {
+            const int l = ord_m[s][om.m_bits - 1 - j];
+            om.m_pos[j] = static_cast<int8_t>(rr - 1 - pos_in(R.labels, l));
+            ident &= om.m_pos[j] == j + om.n_bits;
+        }
+        for (int j = 0; j < om.n_bits; ++j) {
+            const int l = ord_n[s][om.n_bits - 1 - j];
+            om.n_pos[j] = static_cast<int8_t>(rr - 1 - pos_in(R.labels, l));
+            ident &= om.n_pos[j] == j;
+        }
+        om.scatter = ident ? 0 : 1;
+        if (getenv("RCSG_DUMP_STEPS") && (A.labels.size() >= 16 || B.labels.size() >= 16 || R.labels.size() >= 20))
+            fprintf(stderr, "step %d mode %d m=2^%d n=2^%d k=2^%zu perm_a %d perm_b %d scatter %d low-bit m_pos0=%d n_pos0=%d\n",
+                    st.plan_index, st.mode, om.m_bits, om.n_bits, shared[s].size(), st.perm_a, st.perm_b,
+                    om.scatter, om.m_bits ? om.m_pos[0] : -1, om.n_bits ? om.n_pos[0] : -1);
+        if (getenv("RCSG_DUMP_STEPS") && R.labels.size() >= 20) {
+            fprintf(stderr, "   m_pos:");
+            for (int j = 0; j < om.m_bits; ++j) fprintf(stderr, " %d", om.m_pos[j]);
+            fprintf(stderr, "\n   n_pos:");
+            for (int j = 0; j < om.n_bits; ++j) fprintf(stderr, " %d", om.n_pos[j]);
+            fprintf(stderr, "\n");
+        }
     }
     // canonical output order of the root: bit j <-> j-th smallest open qubit
     // among the root's labels (contraction_engine.cpp:193-207)
@@ -489,6 +510,7 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
                 const LabelRole& rl = roles_[nd.labels0[p]];
                 j.kind[p] = rl.role;
                 j.arg[p] = static_cast<int16_t>(rl.role == kVar ? rl.var_bit : nd.labels0[p]);
+                j.obit[p] = rl.role == kFree ? static_cast<int8_t>(nd.labels.size() - 1 - pos_in(nd.labels, nd.labels0[p])) : 0;
             }
             jobs.push_back(j);
         }
@@ -550,6 +572,7 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     g.n = st.n;
     g.step = st.plan_index;
     g.fault = d_fault_;
+    g.om = st.om;
     if (st.mode == 2) {
         g.m = st.m;
         g.batch = vr;
@@ -740,6 +763,7 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
                 const LabelRole& rl = roles_[nd.labels0[p]];
                 j.kind[p] = rl.role;
                 j.arg[p] = static_cast<int16_t>(nd.labels0[p]);
+                j.obit[p] = rl.role == kFree ? static_cast<int8_t>(nd.labels.size() - 1 - pos_in(nd.labels, nd.labels0[p])) : 0;
             }
             static_jobs_[level].push_back(j);
         }

@@ -74,6 +74,7 @@ struct StepInfo {
     int64_t sa_off = -1, sa_plane = 0, sb_off = -1, sb_plane = 0;  // permute scratch
     int64_t m = 1, n = 1, k = 1;
     uint64_t flops_per_variant = 0;  // 8*m*n*k
+    OutMap om{};                     // epilogue scatter into the consumer's layout
 };
 
 struct ChunkData {

@@ -16,6 +16,7 @@ constexpr int kRows = 64;  // output rows per CTA
 template <typename R, int K>
 __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
     __shared__ R a_re[kRows][K], a_im[kRows][K];
+    __shared__ int64_t row_off[kRows];
     const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + kRows - 1) / kRows;
     const int col = threadIdx.x % nb, rsub = threadIdx.x / nb, rstep = kThreads / nb;
     bool bad = false;
@@ -36,6 +37,8 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
             a_re[r][kk] = ok ? A[(m0 + r) * g.k + kk] : R(0);
             a_im[r][kk] = ok ? A[g.a_plane + (m0 + r) * g.k + kk] : R(0);
         }
+        for (int r = threadIdx.x; r < kRows; r += kThreads) row_off[r] = out_row_off(g.om, g.n, m0 + r);
+        const int64_t col_off = out_col_off(g.om, n);
         R b_re[K], b_im[K];
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
@@ -54,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
                     ci = fma(a_re[r][kk], b_im[kk], ci);
                     ci = fma(a_im[r][kk], b_re[kk], ci);
                 }
-                const int64_t o = (m0 + r) * g.n + n;
+                const int64_t o = row_off[r] + col_off;
                 C[o] = cr;
                 C[g.c_plane + o] = ci;
                 bad |= !isfinite(cr) || !isfinite(ci);
@@ -64,8 +67,74 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
     if (bad && g.fault) atomicMin(g.fault, g.step);
 }
 
+// Row mode, for outputs whose fastest bits come from the row index: one thread
+// per row keeps its A row in registers; a CTA covers 256 rows x kColTile
+// columns, the B tile is staged in shared memory (read as broadcasts) and
+// consecutive threads store consecutive addresses.
+constexpr int kColTile = 64;
+
+template <typename R, int K>
+__global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g) {
+    __shared__ R b_re[kColTile][K], b_im[kColTile][K];
+    __shared__ int64_t col_off[kColTile];
+    bool bad = false;
+    const int64_t rtiles = (g.m + kThreads - 1) / kThreads, ctiles = (g.n + kColTile - 1) / kColTile;
+    for (int64_t tile = blockIdx.x; tile < g.batch * rtiles * ctiles; tile += gridDim.x) {
+        const int64_t ct = tile % ctiles;
+        const int64_t rt = (tile / ctiles) % rtiles;
+        const int64_t v = tile / (ctiles * rtiles);
+        const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
+        const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
+        const R* A = static_cast<const R*>(g.a) + av * g.a_batch;
+        const R* B = static_cast<const R*>(g.b) + bv * g.b_batch;
+        R* C = static_cast<R*>(g.c) + v * g.c_batch;
+        const int64_t n0 = ct * kColTile, r = rt * kThreads + threadIdx.x;
+        __syncthreads();
+        for (int e = threadIdx.x; e < kColTile * K; e += kThreads) {
+            const int c = e / K, kk = e % K;
+            const bool ok = n0 + c < g.n && kk < g.k;
+            b_re[c][kk] = ok ? B[(n0 + c) * g.k + kk] : R(0);
+            b_im[c][kk] = ok ? B[g.b_plane + (n0 + c) * g.k + kk] : R(0);
+        }
+        for (int c = threadIdx.x; c < kColTile; c += kThreads) col_off[c] = out_col_off(g.om, n0 + c);
+        __syncthreads();
+        if (r >= g.m) continue;
+        R a_re[K], a_im[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+            const bool ok = kk < g.k;
+            a_re[kk] = ok ? A[r * g.k + kk] : R(0);
+            a_im[kk] = ok ? A[g.a_plane + r * g.k + kk] : R(0);
+        }
+        const int64_t roff = out_row_off(g.om, g.n, r);
+        const int cend = static_cast<int>(g.n - n0 < kColTile ? g.n - n0 : kColTile);
+#pragma unroll 4
+        for (int c = 0; c < cend; ++c) {
+            R cr = 0, ci = 0;
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                cr = fma(a_re[kk], b_re[c][kk], cr);
+                cr = fma(-a_im[kk], b_im[c][kk], cr);
+                ci = fma(a_re[kk], b_im[c][kk], ci);
+                ci = fma(a_im[kk], b_re[c][kk], ci);
+            }
+            const int64_t o = roff + col_off[c];
+            C[o] = cr;
+            C[g.c_plane + o] = ci;
+            bad |= !isfinite(cr) || !isfinite(ci);
+        }
+    }
+    if (bad && g.fault) atomicMin(g.fault, g.step);
+}
+
 template <typename R, int K>
 void launch_k(const GemmArgs& g, cudaStream_t st) {
+    if (g.om.scatter && g.om.m_bits >= 5 && g.om.m_pos[0] == 0 && g.om.m_pos[1] == 1) {
+        const int64_t tiles = g.batch * ((g.m + kThreads - 1) / kThreads) * ((g.n + kColTile - 1) / kColTile);
+        const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
+        smallk_rows_kernel<R, K><<<std::max(grid, 1), kThreads, 0, st>>>(g);
+        return;
+    }
     const int nb = static_cast<int>(std::min<int64_t>(g.n, kThreads));
     const int64_t tiles = g.batch * ((g.m + kRows - 1) / kRows) * ((g.n + nb - 1) / nb);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));

@@ -140,7 +140,48 @@ struct TcParams {
     int64_t ws_split;       // workspace elements per split (split-K), 0 otherwise
     int32_t step;
     int32_t* fault;
+    OutMap om;              // output scatter map (applied when not split)
 };
+
+// Store one 32-column chunk of a thread's row: row-major (vectorised) or
+// through the output scatter map into the consumer's layout.
+__device__ __forceinline__ bool store_chunk(const TcParams& p, float* cre, float* cim, int64_t row, int64_t col0,
+                                            const float* re, const float* im, const int64_t* tn_lo) {
+    bool bad = false;
+    if (!p.om.scatter || p.ws_split) {
+        float* pr = cre + row * p.n + col0;
+        float* pi = cim + row * p.n + col0;
+        if (col0 + 32 <= p.n && (p.n & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
+                *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
+            }
+        } else {
+            for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+                pr[i] = re[i];
+                pi[i] = im[i];
+            }
+        }
+    } else {
+        const int64_t base = out_row_off(p.om, p.n, row) + out_col_off(p.om, col0);
+        if (col0 + 32 <= p.n && p.om.n_pos[0] == 0 && p.om.n_pos[1] == 1) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                *reinterpret_cast<float4*>(cre + base + tn_lo[i]) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
+                *reinterpret_cast<float4*>(cim + base + tn_lo[i]) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
+            }
+        } else {
+            for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+                cre[base + tn_lo[i]] = re[i];
+                cim[base + tn_lo[i]] = im[i];
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
+    return bad;
+}
 
 template <int BN, int STAGES>
 struct Smem {
@@ -164,6 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ int64_t tn_lo[32];
+    if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
     // tile coordinates
     // raster: the tile dimension with fewer tiles varies fastest, so CTAs that
     // run together share the larger operand's tile through L2
@@ -266,26 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) re[i] = im[i] = 0.f;
         }
-        if (row < p.m) {
-            const int64_t col0 = n0 + c0;
-            float* pr = cre + row * p.n + col0;
-            float* pi = cim + row * p.n + col0;
-            if (col0 + 32 <= p.n && (p.n & 3) == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
-                    *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
-                }
-#pragma unroll
-                for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
-            } else {
-                for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-                    pr[i] = re[i];
-                    pi[i] = im[i];
-                    bad |= !isfinite(re[i]) || !isfinite(im[i]);
-                }
-            }
-        }
+        if (row < p.m) bad |= store_chunk(p, cre, cim, row, n0 + c0, re, im, tn_lo);
     }
     if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -350,6 +374,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ int64_t tn_lo[32];
+    if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -442,26 +468,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 float re[32], im[32];
                 tmem_ld32(base + c0, re);
                 tmem_ld32(base + BN + c0, im);
-                if (row < p.m) {
-                    const int64_t col0 = c.n0 + c0;
-                    float* pr = cre + row * p.n + col0;
-                    float* pi = cim + row * p.n + col0;
-                    if (col0 + 32 <= p.n && (p.n & 3) == 0) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4) {
-                            *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
-                            *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
-                    } else {
-                        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-                            pr[i] = re[i];
-                            pi[i] = im[i];
-                            bad |= !isfinite(re[i]) || !isfinite(im[i]);
-                        }
-                    }
-                }
+                if (row < p.m) bad |= store_chunk(p, cre, cim, row, c.n0 + c0, re, im, tn_lo);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -473,23 +480,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
-}
-
-// Fixed-order split-K reduction: C = sum_z W[z]  (planar; W laid out like C per split).
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int64_t ws_split, int splits,
-                                     float* __restrict__ c, int64_t c_plane, int64_t total_per_plane,
-                                     int32_t step, int32_t* fault) {
-    bool bad = false;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 2 * total_per_plane;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int plane = i >= total_per_plane;
-        const int64_t e = i - plane * total_per_plane;
-        float s = 0.f;
-        for (int z = 0; z < splits; ++z) s += ws[z * ws_split + plane * total_per_plane + e];
-        c[plane * c_plane + e] = s;
-        bad |= !isfinite(s);
-    }
-    if (bad && fault) atomicMin(fault, step);
 }
 
 // ---- host side
@@ -554,6 +544,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.b_batched = g.b_batch != 0;
     p.step = g.step;
     p.fault = g.fault;
+    p.om = g.om;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + kBK - 1) / kBK;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
@@ -594,11 +585,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
         gemm_tc_kernel<BN, STAGES><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br,
                                                                                                         bi, p);
     }
-    if (splits > 1) {
-        const int grid = static_cast<int>(std::min<int64_t>((2 * c_elems + 255) / 256, 148 * 16));
-        splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.c, p.ws_split, splits, static_cast<float*>(g.c), g.c_plane,
-                                                   c_elems, g.step, g.fault);
-    }
+    if (splits > 1) launch_splitk_reduce<float>(p.c, p.ws_split, splits, g, st);
 }
 
 }  // namespace

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const int64_t mi = long_is_a ? row : j, ni = long_is_a ? j : row;
                 const int64_t o = v * g.m * g.n + mi * g.n + ni;
                 if (splits == 1) {
-                    R* C = static_cast<R*>(g.c) + v * g.c_batch + mi * g.n + ni;
+                    R* C = static_cast<R*>(g.c) + v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
                     C[0] = acc_re[j];
                     C[g.c_plane] = acc_im[j];
                     if (g.fault && (!isfinite(acc_re[j]) || !isfinite(acc_im[j]))) atomicMin(g.fault, g.step);
@@ -112,26 +112,6 @@ __global__ void __launch_bounds__(kWarps * 32)
             }
         }
     }
-}
-
-template <typename R>
-__global__ void gemv_reduce(const R* __restrict__ ws, int64_t ws_split, int splits, const GemmArgs g) {
-    const int64_t per_plane = g.batch * g.m * g.n;
-    bool bad = false;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < per_plane;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        R re = 0, im = 0;
-        for (int z = 0; z < splits; ++z) {
-            re += ws[z * ws_split + i];
-            im += ws[z * ws_split + ws_split / 2 + i];
-        }
-        const int64_t v = i / (g.m * g.n), e = i - v * g.m * g.n;
-        R* C = static_cast<R*>(g.c) + v * g.c_batch + e;
-        C[0] = re;
-        C[g.c_plane] = im;
-        bad |= !isfinite(re) || !isfinite(im);
-    }
-    if (bad && g.fault) atomicMin(g.fault, g.step);
 }
 
 }  // namespace
@@ -158,11 +138,7 @@ void launch_gemv(const GemmArgs& g, cudaStream_t st) {
     const int64_t warps = g.batch * rows * splits;
     const int grid = static_cast<int>(std::min<int64_t>((warps + kWarps - 1) / kWarps, 148 * 64));
     gemv_kernel<R><<<grid, kWarps * 32, 0, st>>>(g, rows, shorts, long_is_a ? 1 : 0, k_chunk, splits, ws, ws_split);
-    if (splits > 1) {
-        const int64_t n = g.batch * g.m * g.n;
-        const int rg = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
-        gemv_reduce<R><<<std::max(rg, 1), 256, 0, st>>>(ws, ws_split, splits, g);
-    }
+    if (splits > 1) launch_splitk_reduce<R>(ws, ws_split, splits, g, st);
 }
 template void launch_gemv<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemv<double>(const GemmArgs&, cudaStream_t);

@@ -26,12 +26,13 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
     const PassState ps = *state;
     // bits fixed by pass labels, and per-free-position source bit
     uint64_t fixed = 0;
-    int free_src[kMaxLeafRank];
+    int free_src[kMaxLeafRank], free_obit[kMaxLeafRank];
     int nf = 0;
     for (int p = 0; p < j.rank; ++p) {
         const int bitpos = j.rank - 1 - p;
         if (j.kind[p] == 0) {
-            free_src[nf++] = bitpos;
+            free_src[nf] = bitpos;
+            free_obit[nf++] = j.obit[p];
         } else if (j.kind[p] == 1) {
             const PassSrc s = pass_src[j.arg[p]];
             const int v = s.kind == 0 ? s.value
@@ -50,8 +51,8 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
             for (int p = 0; p < j.rank; ++p)
                 if (j.kind[p] == 2) src |= ((code >> j.arg[p]) & 1) << (j.rank - 1 - p);
         }
-        // free positions keep their order: output bit (out_rank-1-q) <- free_src[q]
-        for (int q = 0; q < nf; ++q) src |= static_cast<uint64_t>((i >> (nf - 1 - q)) & 1) << free_src[q];
+        // free positions land on their planned output bits
+        for (int q = 0; q < nf; ++q) src |= static_cast<uint64_t>((i >> free_obit[q]) & 1) << free_src[q];
         const double re = leaf_data[2 * (j.data_off + src)];
         const double im = leaf_data[2 * (j.data_off + src) + 1];
         arena[j.out_off + t] = static_cast<R>(re);
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
             for (int j = 0; j < 4; ++j) {
                 const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
                 if (m < g.m && n < g.n) {
-                    const int64_t o = m * g.n + n;
+                    const int64_t o = sk.ws ? m * g.n + n : out_row_off(g.om, g.n, m) + out_col_off(g.om, n);
                     Cb[o] = acc_re[i][j];
                     Cb[cplane + o] = acc_im[i][j];
                     bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
@@ -178,22 +179,37 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
     }
 }
 
-// Fixed-order split-K reduction: C = sum_z W[z] (W planar [batch][m][n] per split).
+// Fixed-order split-K reduction shared by every GEMM kernel: C = sum_z W[z],
+// W planar [plane][batch][m][n] per split, C written through the output map.
 template <typename R>
-__global__ void splitk_reduce_simt(const R* __restrict__ ws, int64_t ws_split, int splits, R* __restrict__ c,
-                                   int64_t c_plane, int64_t per_plane, int32_t step, int32_t* fault) {
+__global__ void splitk_reduce_kernel(const R* __restrict__ ws, int64_t ws_split, int splits, const GemmArgs g) {
+    const int64_t mn = g.m * g.n, per_plane = g.batch * mn;
+    R* C = static_cast<R*>(g.c);
     bool bad = false;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 2 * per_plane;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < per_plane;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int plane = i >= per_plane;
-        const int64_t e = i - plane * per_plane;
-        R s = 0;
-        for (int z = 0; z < splits; ++z) s += ws[z * ws_split + plane * per_plane + e];
-        c[plane * c_plane + e] = s;
-        bad |= !isfinite(s);
+        R re = 0, im = 0;
+        for (int z = 0; z < splits; ++z) {
+            re += ws[z * ws_split + i];
+            im += ws[z * ws_split + per_plane + i];
+        }
+        const int64_t v = i / mn, e = i - v * mn, mi = e / g.n, ni = e - mi * g.n;
+        const int64_t o = v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
+        C[o] = re;
+        C[g.c_plane + o] = im;
+        bad |= !isfinite(re) || !isfinite(im);
     }
-    if (bad && fault) atomicMin(fault, step);
+    if (bad && g.fault) atomicMin(g.fault, g.step);
 }
+
+template <typename R>
+void launch_splitk_reduce(const R* ws, int64_t ws_split, int splits, const GemmArgs& g, cudaStream_t st) {
+    const int64_t per_plane = g.batch * g.m * g.n;
+    const int grid = static_cast<int>(std::min<int64_t>((per_plane + 255) / 256, 148 * 16));
+    splitk_reduce_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(ws, ws_split, splits, g);
+}
+template void launch_splitk_reduce<float>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
+template void launch_splitk_reduce<double>(const double*, int64_t, int, const GemmArgs&, cudaStream_t);
 
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
@@ -209,13 +225,7 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
     }
     const int grid = static_cast<int>(std::min<int64_t>(tiles * sk.splits, 148 * 32));
     gemm_simt_kernel<R><<<grid, block, 0, st>>>(g, sk);
-    if (sk.splits > 1) {
-        const int64_t per_plane = g.batch * g.m * g.n;
-        const int rg = static_cast<int>(std::min<int64_t>((2 * per_plane + 255) / 256, 148 * 16));
-        splitk_reduce_simt<R><<<std::max(rg, 1), 256, 0, st>>>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits,
-                                                               static_cast<R*>(g.c), g.c_plane, per_plane, g.step,
-                                                               g.fault);
-    }
+    if (sk.splits > 1) launch_splitk_reduce<R>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
 }
 
 void* device_workspace(size_t bytes, cudaStream_t st) {

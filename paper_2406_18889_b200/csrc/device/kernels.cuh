@@ -28,6 +28,7 @@ struct LeafJob {
     // per original position p (MSB first): kind 0 free (kept), 1 pass label, 2 variant label
     int8_t kind[kMaxLeafRank];
     int16_t arg[kMaxLeafRank];  // pass: label id; variant: bit position in the group code
+    int8_t obit[kMaxLeafRank];  // free: output index bit the position lands on (planned layout)
 };
 
 struct PassState {
@@ -69,6 +70,31 @@ template <typename R>
 void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, int64_t n_var,
                     const PermuteDesc& d, cudaStream_t st);
 
+// ---- GEMM output scatter map.  scatter == 0: row-major C.  Otherwise element
+// (row m, column n) of a variant block lands at
+//   (m >> m_bits) * 2^(m_bits+n_bits) + sum_j bit_j(m) << m_pos[j] + sum_j bit_j(n) << n_pos[j]
+// i.e. directly in the layout the consumer step reads (no separate permute).
+struct OutMap {
+    int32_t scatter;
+    int32_t m_bits, n_bits;
+    int8_t m_pos[kMaxRank];
+    int8_t n_pos[kMaxRank];
+};
+__host__ __device__ __forceinline__ int64_t scatter_bits(const int8_t* pos, int bits, int64_t x) {
+    int64_t o = 0;
+    for (int j = 0; j < bits; ++j) o |= ((x >> j) & int64_t{1}) << pos[j];
+    return o;
+}
+// row part / column part of the output offset (additive: offset = row_off + col_off)
+__host__ __device__ __forceinline__ int64_t out_row_off(const OutMap& om, int64_t n_cols, int64_t m) {
+    if (!om.scatter) return m * n_cols;
+    return ((m >> om.m_bits) << (om.m_bits + om.n_bits)) +
+           scatter_bits(om.m_pos, om.m_bits, m & ((int64_t{1} << om.m_bits) - 1));
+}
+__host__ __device__ __forceinline__ int64_t out_col_off(const OutMap& om, int64_t n) {
+    return om.scatter ? scatter_bits(om.n_pos, om.n_bits, n) : n;
+}
+
 // ---- complex GEMM, both operands K-contiguous ("TN"):
 //   C[v][m][n] = sum_k A[ia(v)][m][k] * B[ib(v)][n][k]
 // ia / ib: device index arrays or nullptr (identity for ia, 0 for ib... see GemmArgs).
@@ -88,6 +114,7 @@ struct GemmArgs {
     const int32_t* ib;      // nullptr -> B variant = v * (b_batch != 0)
     int32_t step;           // plan step index for the non-finite flag
     int32_t* fault;         // device flag: min step index with a non-finite output
+    OutMap om;              // where C elements land inside their variant block
 };
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
@@ -101,6 +128,11 @@ void launch_gemm_smallk(const GemmArgs& g, cudaStream_t st);
 bool gemv_supported(const GemmArgs& g);
 template <typename R>
 void launch_gemv(const GemmArgs& g, cudaStream_t st);
+
+// Fixed-order split-K reduction (W planar [split][plane][batch][m][n]) writing C
+// through g.om; shared by all GEMM kernels.
+template <typename R>
+void launch_splitk_reduce(const R* ws, int64_t ws_split, int splits, const GemmArgs& g, cudaStream_t st);
 
 // Scratch buffer for split-K partials, one per stream (grown on demand).
 void* device_workspace(size_t bytes, cudaStream_t st);
