@@ -132,6 +132,7 @@ Program::~Program() {
     cudaFree(d_comp_);
     for (auto* p : d_static_jobs_) cudaFree(p);
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -716,6 +717,7 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
 
 void Program::bind_groups(const std::vector<uint64_t>& groups) {
     bound_groups_.clear();
+    reset_graph();
     // chunk capacity: the largest group chunk whose arena fits the budget
     std::vector<uint64_t> uniq = groups;
     std::sort(uniq.begin(), uniq.end());
@@ -778,12 +780,66 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
     bound_groups_ = groups;
 }
 
+// One (configuration, slice) pass after set_pass: level-1 steps, then every
+// group chunk's level-2 steps and finalisation.  Replayed as a CUDA graph once
+// the first pass has sized the workspaces (every pass launches the same
+// kernels; the slice / configuration bits are read from device memory).
+void Program::exec_pass_body(int64_t P) {
+    exec_level(1, nullptr);
+    for (const ChunkData& ch : chunks_) {
+        exec_level(2, &ch);
+        const NodeInfo& root = nodes_[root_];
+        if (elem_bytes_ == 8)
+            launch_finalize<double>(static_cast<const double*>(buf(root.off)), root.plane, P,
+                                    static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
+                                    static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
+        else
+            launch_finalize<float>(static_cast<const float*>(buf(root.off)), root.plane, P,
+                                   static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
+                                   static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
+        ++launches_;
+    }
+}
+
+void Program::reset_graph() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    graph_warm_ = false;
+}
+
+void Program::run_pass_body(int64_t P) {
+    static const bool no_graph = getenv("RCSG_NO_GRAPH") != nullptr;
+    if (profile_ || no_graph) {
+        exec_pass_body(P);
+        return;
+    }
+    if (!graph_exec_ && !graph_warm_) {  // first pass: eager, sizes split-K workspaces
+        exec_pass_body(P);
+        graph_warm_ = true;
+        return;
+    }
+    if (!graph_exec_) {
+        const uint64_t before = launches_;
+        cudaGraph_t graph;
+        CUDA_OK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        exec_pass_body(P);
+        CUDA_OK(cudaStreamEndCapture(stream_, &graph));
+        CUDA_OK(cudaGraphInstantiate(&graph_exec_, graph, 0));
+        cudaGraphDestroy(graph);
+        graph_launches_ = launches_ - before;
+        launches_ = before;
+    }
+    CUDA_OK(cudaGraphLaunch(graph_exec_, stream_));
+    launches_ += graph_launches_;
+}
+
 void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
                         uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n) {
     if (acc_n > acc_cap_) {
         cudaFree(d_part_);
         cudaFree(d_res_);
         cudaFree(d_comp_);
+        reset_graph();
         CUDA_OK(cudaMalloc(&d_part_, acc_n * sizeof(double)));
         CUDA_OK(cudaMalloc(&d_res_, acc_n * sizeof(double)));
         CUDA_OK(cudaMalloc(&d_comp_, acc_n * sizeof(double)));
@@ -810,21 +866,8 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
         for (uint64_t s = slice_begin; s < slice_end; ++s) {
             launch_set_pass(d_state_, s, cfgs[ci], stream_);
             ++launches_;
-            exec_level(1, nullptr);
-            for (const ChunkData& ch : chunks_) {
-                exec_level(2, &ch);
-                const NodeInfo& root = nodes_[root_];
-                if (elem_bytes_ == 8)
-                    launch_finalize<double>(static_cast<const double*>(buf(root.off)), root.plane, P,
-                                            static_cast<int>(root.labels.size()), d_canon_, ch.d_vid,
-                                            ch.d_groups, static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
-                else
-                    launch_finalize<float>(static_cast<const float*>(buf(root.off)), root.plane, P,
-                                           static_cast<int>(root.labels.size()), d_canon_, ch.d_vid,
-                                           ch.d_groups, static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
-                ++launches_;
-                ++passes;
-            }
+            run_pass_body(P);
+            passes += chunks_.size();
         }
         launch_kahan(d_res_, d_comp_, d_part_, acc_n, stream_);
         ++launches_;

@@ -120,6 +120,9 @@ class Program {
     int64_t plan_arena(int64_t chunk_cap, bool assign);
     void prepare_chunks(const std::vector<uint64_t>& groups, int64_t chunk_cap);
     void bind_groups(const std::vector<uint64_t>& groups);
+    void exec_pass_body(int64_t P);
+    void run_pass_body(int64_t P);
+    void reset_graph();
     void run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
                    uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n);
     void free_chunks();
@@ -161,6 +164,9 @@ class Program {
     int64_t acc_cap_ = 0;
     std::vector<ChunkData> chunks_;
     std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
+    cudaGraphExec_t graph_exec_ = nullptr;  // captured pass body (level 1 + chunks)
+    bool graph_warm_ = false;
+    uint64_t graph_launches_ = 0;
     uint64_t launches_ = 0;
     uint64_t exec_flops_ = 0;
 
