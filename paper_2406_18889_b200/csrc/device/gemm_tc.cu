@@ -165,7 +165,17 @@ __device__ __forceinline__ bool store_chunk(const TcParams& p, float* cre, float
         }
     } else {
         const int64_t base = out_row_off(p.om, p.n, row) + out_col_off(p.om, col0);
-        if (col0 + 32 <= p.n && p.om.n_pos[0] == 0 && p.om.n_pos[1] == 1) {
+        const int sh = p.om.n_pos[0];
+        const bool contig = p.om.n_bits >= 5 && p.om.n_pos[1] == sh + 1 && p.om.n_pos[2] == sh + 2 &&
+                            p.om.n_pos[3] == sh + 3 && p.om.n_pos[4] == sh + 4;
+        if (col0 + 32 <= p.n && contig && sh > 0) {
+            // column bits contiguous at bit sh: stores of equal i are lane-coalesced when rows are fastest
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                cre[base + (static_cast<int64_t>(i) << sh)] = re[i];
+                cim[base + (static_cast<int64_t>(i) << sh)] = im[i];
+            }
+        } else if (col0 + 32 <= p.n && p.om.n_pos[0] == 0 && p.om.n_pos[1] == 1) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
                 *reinterpret_cast<float4*>(cre + base + tn_lo[i]) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
@@ -321,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // double-buffered in TMEM (2 x {Re, Im} x BN columns) so the four epilogue
 // warps drain tile i while the MMA warp already accumulates tile i+1.
 //   warp 0: TMA producer   warp 1: MMA issuer   warps 2-5: epilogue (TMEM lane quarter = warp % 4)
-constexpr int kPThreads = 192;
+constexpr int kPThreads = 320;  // 2 role warps + 8 epilogue warps (2 per TMEM lane quarter)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -384,7 +394,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
+            mbar_init(&tempty[b], 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -450,8 +460,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 mma_commit(&tfull[ab]);
             }
         }
-    } else {  // ---- epilogue warps 2..5
+    } else {  // ---- epilogue warps 2..9: lane quarter warp % 4, column half (warp - 2) / 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int half = (warp - 2) >> 2;
         bool bad = false;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             float* cim = cre + p.c_plane;
             const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
                 float re[32], im[32];
                 tmem_ld32(base + c0, re);
                 tmem_ld32(base + BN + c0, im);
