@@ -819,7 +819,7 @@ void Program::run_pass_body(int64_t P) {
         return;
     }
     if (!graph_exec_) {
-        const uint64_t before = launches_;
+        const uint64_t before = launches_, flops_before = exec_flops_;
         cudaGraph_t graph;
         CUDA_OK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         exec_pass_body(P);
@@ -827,10 +827,13 @@ void Program::run_pass_body(int64_t P) {
         CUDA_OK(cudaGraphInstantiate(&graph_exec_, graph, 0));
         cudaGraphDestroy(graph);
         graph_launches_ = launches_ - before;
+        graph_flops_ = exec_flops_ - flops_before;
         launches_ = before;
+        exec_flops_ = flops_before;
     }
     CUDA_OK(cudaGraphLaunch(graph_exec_, stream_));
     launches_ += graph_launches_;
+    exec_flops_ += graph_flops_;
 }
 
 void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,

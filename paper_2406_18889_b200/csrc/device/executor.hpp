@@ -167,6 +167,7 @@ class Program {
     cudaGraphExec_t graph_exec_ = nullptr;  // captured pass body (level 1 + chunks)
     bool graph_warm_ = false;
     uint64_t graph_launches_ = 0;
+    uint64_t graph_flops_ = 0;
     uint64_t launches_ = 0;
     uint64_t exec_flops_ = 0;
 
