@@ -42,7 +42,8 @@ enum {
     RCSG_PREC_F64 = 0,   /* fp64 SIMT: reference-grade (<= 1e-10 norm-relative) */
     RCSG_PREC_F32 = 1,   /* fp32 SIMT */
     RCSG_PREC_TF32 = 2,  /* tcgen05 kind::tf32, fp32 accumulate in TMEM */
-    RCSG_PREC_3XTF32 = 3 /* split tf32 (hi*hi + hi*lo + lo*hi) on tcgen05: fp32-grade */
+    RCSG_PREC_3XTF32 = 3, /* fp32-grade (runs the fp32 SIMT kernels for now) */
+    RCSG_PREC_BF16 = 4    /* bf16 storage, tcgen05 kind::f16 (BF16 operands), fp32 accumulate */
 };
 
 /* TensorNetwork (tensor_network.hpp:26-43), flattened. */

@@ -8,6 +8,7 @@
 #include <map>
 #include <iterator>
 #include <numeric>
+#include <type_traits>
 
 #include "executor.hpp"
 
@@ -19,6 +20,21 @@ namespace rcsg {
         if (e_ != cudaSuccess)                                                          \
             throw Failure{RCSG_ERR_DEVICE, std::string("CUDA: ") + cudaGetErrorString(e_) + \
                                                " at " #x};                              \
+    } while (0)
+
+// run BODY with S = the storage type of precision PREC
+#define RCSG_DISPATCH(PREC, BODY)              \
+    do {                                       \
+        if ((PREC) == RCSG_PREC_F64) {         \
+            using S = double;                  \
+            BODY;                              \
+        } else if ((PREC) == RCSG_PREC_BF16) { \
+            using S = bf16;                    \
+            BODY;                              \
+        } else {                               \
+            using S = float;                   \
+            BODY;                              \
+        }                                      \
     } while (0)
 
 namespace {
@@ -97,9 +113,9 @@ void permute_bits(const std::vector<int>& from, const std::vector<int>& to, std:
 Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
                  const std::vector<LabelRole>& roles, int precision, uint64_t mem_budget)
     : precision_(precision), mem_budget_(mem_budget), roles_(roles) {
-    if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_3XTF32)
+    if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_BF16)
         throw Failure{RCSG_ERR_CONFIG, "unknown precision"};
-    elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : 4;
+    elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : (precision == RCSG_PREC_BF16 ? 2 : 4);
     build_nodes(net, plan);
     build_steps();
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -601,10 +617,10 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         ++launches_;
         return;
     }
-    if constexpr (sizeof(R) == 4) {
+    if constexpr (!std::is_same_v<R, double>) {
         // 3xTF32 stays on the fp32 SIMT kernel until its split-operand tensor-core path lands
-        if (precision_ == RCSG_PREC_TF32 && gemm_tc_supported(g)) {
-            launch_gemm_tc(g, precision_ == RCSG_PREC_3XTF32 ? 3 : 1, stream_);
+        if ((precision_ == RCSG_PREC_TF32 || precision_ == RCSG_PREC_BF16) && gemm_tc_supported(g)) {
+            launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : 0, stream_);
             mark_end(mk, kCatGemmTc, flops, st.plan_index, g.m, g.n, g.k, g.batch);
             ++launches_;
             return;
@@ -673,29 +689,22 @@ void Program::collect_marks(rcsg_stats* stats) {
 }
 
 void Program::exec_step(const StepInfo& st, const ChunkData* ch) {
-    if (elem_bytes_ == 8) exec_step_t<double>(st, ch);
-    else exec_step_t<float>(st, ch);
+    RCSG_DISPATCH(precision_, exec_step_t<S>(st, ch));
 }
 
 void Program::exec_level(int level, const ChunkData* ch) {
     // leaves of this level
     if (level < 2) {
         if (!static_jobs_[level].empty()) {
-            if (elem_bytes_ == 8)
-                launch_leaf_project<double>(d_static_jobs_[level], static_cast<int>(static_jobs_[level].size()),
-                                            d_leaf_data_, nullptr, d_pass_src_, d_state_, static_cast<double*>(arena_), stream_);
-            else
-                launch_leaf_project<float>(d_static_jobs_[level], static_cast<int>(static_jobs_[level].size()),
-                                           d_leaf_data_, nullptr, d_pass_src_, d_state_, static_cast<float*>(arena_), stream_);
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[level],
+                                                            static_cast<int>(static_jobs_[level].size()),
+                                                            d_leaf_data_, nullptr, d_pass_src_, d_state_,
+                                                            static_cast<S*>(arena_), stream_));
             ++launches_;
         }
     } else if (ch->n_leaf_jobs) {
-        if (elem_bytes_ == 8)
-            launch_leaf_project<double>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes, d_pass_src_,
-                                        d_state_, static_cast<double*>(arena_), stream_);
-        else
-            launch_leaf_project<float>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes, d_pass_src_,
-                                       d_state_, static_cast<float*>(arena_), stream_);
+        RCSG_DISPATCH(precision_, launch_leaf_project<S>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes,
+                                                        d_pass_src_, d_state_, static_cast<S*>(arena_), stream_));
         ++launches_;
     }
     for (const StepInfo& st : steps_)
@@ -789,14 +798,10 @@ void Program::exec_pass_body(int64_t P) {
     for (const ChunkData& ch : chunks_) {
         exec_level(2, &ch);
         const NodeInfo& root = nodes_[root_];
-        if (elem_bytes_ == 8)
-            launch_finalize<double>(static_cast<const double*>(buf(root.off)), root.plane, P,
-                                    static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
-                                    static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
-        else
-            launch_finalize<float>(static_cast<const float*>(buf(root.off)), root.plane, P,
-                                   static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
-                                   static_cast<int64_t>(ch.groups.size()), d_part_, stream_);
+        RCSG_DISPATCH(precision_,
+                      launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane, P,
+                                         static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
+                                         static_cast<int64_t>(ch.groups.size()), d_part_, stream_));
         ++launches_;
     }
 }

@@ -85,9 +85,9 @@ extern "C" int rcsg_gemm_selftest(int64_t m, int64_t n, int64_t k, int64_t batch
         g.c = c1;
         const bool tc = gemm_tc_supported(g);
         if (tc) {
-            launch_gemm_tc(g, 1, 0);
+            launch_gemm_tc(g, 0, 0);
             cudaEventRecord(e0);
-            for (int i = 0; i < iters; ++i) launch_gemm_tc(g, 1, 0);
+            for (int i = 0; i < iters; ++i) launch_gemm_tc(g, 0, 0);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             cudaEventElapsedTime(&ms_tc, e0, e1);

@@ -13,8 +13,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kRows = 64;  // output rows per CTA
 
-template <typename R, int K>
+template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
+    using R = typename Acc<S>::T;
     __shared__ R a_re[kRows][K], a_im[kRows][K];
     __shared__ int64_t row_off[kRows];
     const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + kRows - 1) / kRows;
@@ -26,16 +27,16 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
         const int64_t v = tile / (ntiles * mtiles);
         const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
         const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
-        const R* A = static_cast<const R*>(g.a) + av * g.a_batch;
-        const R* B = static_cast<const R*>(g.b) + bv * g.b_batch;
-        R* C = static_cast<R*>(g.c) + v * g.c_batch;
+        const S* A = static_cast<const S*>(g.a) + av * g.a_batch;
+        const S* B = static_cast<const S*>(g.b) + bv * g.b_batch;
+        S* C = static_cast<S*>(g.c) + v * g.c_batch;
         const int64_t m0 = mt * kRows, n = nt * nb + col;
         __syncthreads();
         for (int e = threadIdx.x; e < kRows * K; e += kThreads) {
             const int r = e / K, kk = e % K;
             const bool ok = m0 + r < g.m && kk < g.k;
-            a_re[r][kk] = ok ? A[(m0 + r) * g.k + kk] : R(0);
-            a_im[r][kk] = ok ? A[g.a_plane + (m0 + r) * g.k + kk] : R(0);
+            a_re[r][kk] = ok ? load_c(A + (m0 + r) * g.k + kk) : R(0);
+            a_im[r][kk] = ok ? load_c(A + g.a_plane + (m0 + r) * g.k + kk) : R(0);
         }
         for (int r = threadIdx.x; r < kRows; r += kThreads) row_off[r] = out_row_off(g.om, g.n, m0 + r);
         const int64_t col_off = out_col_off(g.om, n);
@@ -43,8 +44,8 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
             const bool ok = n < g.n && kk < g.k;
-            b_re[kk] = ok ? B[n * g.k + kk] : R(0);
-            b_im[kk] = ok ? B[g.b_plane + n * g.k + kk] : R(0);
+            b_re[kk] = ok ? load_c(B + n * g.k + kk) : R(0);
+            b_im[kk] = ok ? load_c(B + g.b_plane + n * g.k + kk) : R(0);
         }
         __syncthreads();
         if (n < g.n) {
@@ -58,8 +59,8 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
                     ci = fma(a_im[r][kk], b_re[kk], ci);
                 }
                 const int64_t o = row_off[r] + col_off;
-                C[o] = cr;
-                C[g.c_plane + o] = ci;
+                store_c(C + o, cr);
+                store_c(C + g.c_plane + o, ci);
                 bad |= !isfinite(cr) || !isfinite(ci);
             }
         }
@@ -73,8 +74,9 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
 // consecutive threads store consecutive addresses.
 constexpr int kColTile = 64;
 
-template <typename R, int K>
+template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g) {
+    using R = typename Acc<S>::T;
     __shared__ R b_re[kColTile][K], b_im[kColTile][K];
     __shared__ int64_t col_off[kColTile];
     bool bad = false;
@@ -85,16 +87,16 @@ __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g)
         const int64_t v = tile / (ctiles * rtiles);
         const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
         const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
-        const R* A = static_cast<const R*>(g.a) + av * g.a_batch;
-        const R* B = static_cast<const R*>(g.b) + bv * g.b_batch;
-        R* C = static_cast<R*>(g.c) + v * g.c_batch;
+        const S* A = static_cast<const S*>(g.a) + av * g.a_batch;
+        const S* B = static_cast<const S*>(g.b) + bv * g.b_batch;
+        S* C = static_cast<S*>(g.c) + v * g.c_batch;
         const int64_t n0 = ct * kColTile, r = rt * kThreads + threadIdx.x;
         __syncthreads();
         for (int e = threadIdx.x; e < kColTile * K; e += kThreads) {
             const int c = e / K, kk = e % K;
             const bool ok = n0 + c < g.n && kk < g.k;
-            b_re[c][kk] = ok ? B[(n0 + c) * g.k + kk] : R(0);
-            b_im[c][kk] = ok ? B[g.b_plane + (n0 + c) * g.k + kk] : R(0);
+            b_re[c][kk] = ok ? load_c(B + (n0 + c) * g.k + kk) : R(0);
+            b_im[c][kk] = ok ? load_c(B + g.b_plane + (n0 + c) * g.k + kk) : R(0);
         }
         for (int c = threadIdx.x; c < kColTile; c += kThreads) col_off[c] = out_col_off(g.om, n0 + c);
         __syncthreads();
@@ -103,8 +105,8 @@ __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g)
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
             const bool ok = kk < g.k;
-            a_re[kk] = ok ? A[r * g.k + kk] : R(0);
-            a_im[kk] = ok ? A[g.a_plane + r * g.k + kk] : R(0);
+            a_re[kk] = ok ? load_c(A + r * g.k + kk) : R(0);
+            a_im[kk] = ok ? load_c(A + g.a_plane + r * g.k + kk) : R(0);
         }
         const int64_t roff = out_row_off(g.om, g.n, r);
         const int cend = static_cast<int>(g.n - n0 < kColTile ? g.n - n0 : kColTile);
@@ -119,8 +121,8 @@ __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g)
                 ci = fma(a_im[kk], b_re[c][kk], ci);
             }
             const int64_t o = roff + col_off[c];
-            C[o] = cr;
-            C[g.c_plane + o] = ci;
+            store_c(C + o, cr);
+            store_c(C + g.c_plane + o, ci);
             bad |= !isfinite(cr) || !isfinite(ci);
         }
     }
@@ -155,5 +157,6 @@ void launch_gemm_smallk(const GemmArgs& g, cudaStream_t st) {
 }
 template void launch_gemm_smallk<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_smallk<double>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_smallk<bf16>(const GemmArgs&, cudaStream_t);
 
 }  // namespace rcsg

@@ -27,7 +27,9 @@ namespace rcsg {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kBK = 32;  // fp32 elements = 128 B = one swizzle row
+// K elements per 128-B swizzle row: 32 fp32 (tf32 path) or 64 bf16
+template <typename E>
+constexpr int KBK = 128 / static_cast<int>(sizeof(E));
 constexpr int kThreads = 128;
 
 int num_sms() {
@@ -103,6 +105,42 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// element traits: operand format code of the instruction descriptor, TMA type, MMA kind
+template <typename E>
+struct TcElem;
+template <>
+struct TcElem<float> {
+    static constexpr uint32_t fmt = 2;  // TF32 (kind::tf32)
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+template <>
+struct TcElem<bf16> {
+    static constexpr uint32_t fmt = 1;  // BF16 (kind::f16)
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+};
+template <typename E>
+__host__ __device__ constexpr uint32_t idesc_of(int bn, bool neg_a) {
+    return (1u << 4) | (TcElem<E>::fmt << 7) | (TcElem<E>::fmt << 10) | (neg_a ? (1u << 13) : 0u) |
+           (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+// one 128 x BN x 32-byte-K MMA (8 tf32 or 16 bf16 along K)
+template <typename E>
+__device__ __forceinline__ void mma_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    if constexpr (sizeof(E) == 4) mma_tf32(tmem_d, da, db, idesc, acc);
+    else mma_bf16(tmem_d, da, db, idesc, acc);
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
@@ -135,7 +173,7 @@ struct TcParams {
     const int32_t* ia;      // gather tables (mode 2) or nullptr
     const int32_t* ib;
     int a_batched, b_batched;
-    float* c;               // C re-plane (or split-K workspace)
+    void* c;                // C re-plane (element type) or split-K workspace (float)
     int64_t c_plane, c_batch;
     int64_t ws_split;       // workspace elements per split (split-K), 0 otherwise
     int32_t step;
@@ -143,65 +181,75 @@ struct TcParams {
     OutMap om;              // output scatter map (applied when not split)
 };
 
-// Store one 32-column chunk of a thread's row: row-major (vectorised) or
+// Store one 32-column chunk of a thread's row: to the split-K workspace
+// (fp32, row-major), or to C (element type) row-major (vectorised for fp32) or
 // through the output scatter map into the consumer's layout.
-__device__ __forceinline__ bool store_chunk(const TcParams& p, float* cre, float* cim, int64_t row, int64_t col0,
+template <typename E>
+__device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_t v, int64_t row, int64_t col0,
                                             const float* re, const float* im, const int64_t* tn_lo) {
     bool bad = false;
-    if (!p.om.scatter || p.ws_split) {
-        float* pr = cre + row * p.n + col0;
-        float* pi = cim + row * p.n + col0;
-        if (col0 + 32 <= p.n && (p.n & 3) == 0) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
-                *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
-            }
-        } else {
-            for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-                pr[i] = re[i];
-                pi[i] = im[i];
-            }
-        }
-    } else {
-        const int64_t base = out_row_off(p.om, p.n, row) + out_col_off(p.om, col0);
-        const int sh = p.om.n_pos[0];
-        const bool contig = p.om.n_bits >= 5 && p.om.n_pos[1] == sh + 1 && p.om.n_pos[2] == sh + 2 &&
-                            p.om.n_pos[3] == sh + 3 && p.om.n_pos[4] == sh + 4;
-        if (col0 + 32 <= p.n && contig && sh > 0) {
-            // column bits contiguous at bit sh: stores of equal i are lane-coalesced when rows are fastest
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                cre[base + (static_cast<int64_t>(i) << sh)] = re[i];
-                cim[base + (static_cast<int64_t>(i) << sh)] = im[i];
-            }
-        } else if (col0 + 32 <= p.n && p.om.n_pos[0] == 0 && p.om.n_pos[1] == 1) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                *reinterpret_cast<float4*>(cre + base + tn_lo[i]) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
-                *reinterpret_cast<float4*>(cim + base + tn_lo[i]) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
-            }
-        } else {
-            for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-                cre[base + tn_lo[i]] = re[i];
-                cim[base + tn_lo[i]] = im[i];
-            }
-        }
-    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
+    if (p.ws_split) {
+        float* cre = static_cast<float*>(p.c) + split * p.ws_split + v * p.c_batch;
+        float* pr = cre + row * p.n + col0;
+        float* pi = pr + p.c_plane;
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+            pr[i] = re[i];
+            pi[i] = im[i];
+        }
+        return bad;
+    }
+    E* cre = static_cast<E*>(p.c) + v * p.c_batch;
+    E* cim = cre + p.c_plane;
+    if (!p.om.scatter) {
+        E* pr = cre + row * p.n + col0;
+        E* pi = cim + row * p.n + col0;
+        if constexpr (sizeof(E) == 4) {
+            if (col0 + 32 <= p.n && (p.n & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
+                    *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
+                }
+                return bad;
+            }
+        }
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+            store_c(pr + i, re[i]);
+            store_c(pi + i, im[i]);
+        }
+        return bad;
+    }
+    const int64_t base = out_row_off(p.om, p.n, row) + out_col_off(p.om, col0);
+    const int sh = p.om.n_pos[0];
+    const bool contig = p.om.n_bits >= 5 && p.om.n_pos[1] == sh + 1 && p.om.n_pos[2] == sh + 2 &&
+                        p.om.n_pos[3] == sh + 3 && p.om.n_pos[4] == sh + 4;
+    if (col0 + 32 <= p.n && contig) {
+        // column bits contiguous at bit sh (sh == 0: per-thread contiguous run)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            store_c(cre + base + (static_cast<int64_t>(i) << sh), re[i]);
+            store_c(cim + base + (static_cast<int64_t>(i) << sh), im[i]);
+        }
+    } else {
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+            store_c(cre + base + tn_lo[i], re[i]);
+            store_c(cim + base + tn_lo[i], im[i]);
+        }
+    }
     return bad;
 }
 
 template <int BN, int STAGES>
 struct Smem {
-    static constexpr int kATile = kBM * kBK * 4;  // bytes per A plane tile
-    static constexpr int kBTile = BN * kBK * 4;
+    static constexpr int kATile = kBM * 128;  // bytes per A plane tile (128-B rows)
+    static constexpr int kBTile = BN * 128;
     static constexpr int kStage = 2 * kATile + 2 * kBTile;
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, typename E>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                    const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
@@ -241,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bv = p.ib ? p.ib[v] : (p.b_batched ? static_cast<int>(v) : 0);
     const int64_t k_begin = split * p.k_chunk;
     const int64_t k_end = min(p.k, k_begin + p.k_chunk);
-    const int kblocks = static_cast<int>((k_end - k_begin + kBK - 1) / kBK);
+    const int kblocks = static_cast<int>((k_end - k_begin + KBK<E> - 1) / KBK<E>);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -270,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kb >= STAGES) mbar_wait(&empty[s], (round - 1) & 1);
             uint8_t* st = smem + s * S::kStage;
             mbar_expect_tx(&full[s], S::kStage);
-            const int kc = static_cast<int>(k_begin) + kb * kBK;
+            const int kc = static_cast<int>(k_begin) + kb * KBK<E>;
             tma_load_3d(st, &map_ar, &full[s], kc, m0, av);
             tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, m0, av);
             tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, n0, bv);
@@ -278,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer (single thread)
-        constexpr uint32_t id_pos = idesc_tf32(BN, false), id_neg = idesc_tf32(BN, true);
+        constexpr uint32_t id_pos = idesc_of<E>(BN, false), id_neg = idesc_of<E>(BN, true);
         const uint32_t t_re = tmem, t_im = tmem + BN;
         for (int kb = 0; kb < kblocks; ++kb) {
             const int s = kb % STAGES;
@@ -288,13 +336,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
             const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
 #pragma unroll
-            for (int j = 0; j < kBK / 8; ++j) {
+            for (int j = 0; j < 4; ++j) {  // 4 x 32 B along K per 128-B row
                 const uint64_t o = static_cast<uint64_t>(j * 32) >> 4;  // 8 tf32 = 32 B along K
                 const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
-                mma_tf32(t_re, dar + o, dbr + o, id_pos, acc);
-                mma_tf32(t_re, dai + o, dbi + o, id_neg, 1u);
-                mma_tf32(t_im, dar + o, dbi + o, id_pos, acc);
-                mma_tf32(t_im, dai + o, dbr + o, id_pos, 1u);
+                mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
             }
             mma_commit(&empty[s]);  // frees the stage once these MMAs retire
         }
@@ -306,8 +354,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int64_t row = m0 + warp * 32 + lane;
-    float* cre = p.c + split * p.ws_split + v * p.c_batch;
-    float* cim = cre + p.c_plane;
     bool bad = false;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -319,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) re[i] = im[i] = 0.f;
         }
-        if (row < p.m) bad |= store_chunk(p, cre, cim, row, n0 + c0, re, im, tn_lo);
+        if (row < p.m) bad |= store_chunk<E>(p, split, v, row, n0 + c0, re, im, tn_lo);
     }
     if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -343,7 +389,7 @@ struct TileCoord {
     int64_t k_begin;
 };
 
-template <int BN>
+template <int BN, typename E>
 __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t) {
     TileCoord c;
     c.split = static_cast<int>(t % p.splits);
@@ -365,11 +411,11 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t) {
     c.n0 = static_cast<int>(ntile * BN);
     c.k_begin = c.split * p.k_chunk;
     const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
-    c.kblocks = static_cast<int>((k_end - c.k_begin + kBK - 1) / kBK);
+    c.kblocks = static_cast<int>((k_end - c.k_begin + KBK<E> - 1) / KBK<E>);
     return c;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, typename E>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
@@ -413,7 +459,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (lane == 0) {  // ---- TMA producer
             uint32_t it = 0;
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileCoord c = tile_coord<BN>(p, t);
+                const TileCoord c = tile_coord<BN, E>(p, t);
                 const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
@@ -421,7 +467,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* st = smem + s * S::kStage;
                     mbar_expect_tx(&full[s], S::kStage);
-                    const int kc = static_cast<int>(c.k_begin) + kb * kBK;
+                    const int kc = static_cast<int>(c.k_begin) + kb * KBK<E>;
                     tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
                     tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
                     tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
@@ -431,10 +477,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t id_pos = idesc_tf32(BN, false), id_neg = idesc_tf32(BN, true);
+            constexpr uint32_t id_pos = idesc_of<E>(BN, false), id_neg = idesc_of<E>(BN, true);
             uint32_t it = 0, j = 0;
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-                const TileCoord c = tile_coord<BN>(p, t);
+                const TileCoord c = tile_coord<BN, E>(p, t);
                 const uint32_t ab = j & 1;
                 if (j >= 2) mbar_wait(&tempty[ab], ((j >> 1) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -447,13 +493,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
                     const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
 #pragma unroll
-                    for (int jj = 0; jj < kBK / 8; ++jj) {
+                    for (int jj = 0; jj < 4; ++jj) {
                         const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
                         const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
-                        mma_tf32(t_re, dar + o, dbr + o, id_pos, acc);
-                        mma_tf32(t_re, dai + o, dbi + o, id_neg, 1u);
-                        mma_tf32(t_im, dar + o, dbi + o, id_pos, acc);
-                        mma_tf32(t_im, dai + o, dbr + o, id_pos, 1u);
+                        mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                        mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                        mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                        mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
                     }
                     mma_commit(&empty[s]);
                 }
@@ -466,20 +512,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
         bool bad = false;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-            const TileCoord c = tile_coord<BN>(p, t);
+            const TileCoord c = tile_coord<BN, E>(p, t);
             const uint32_t ab = j & 1;
             mbar_wait(&tfull[ab], (j >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t row = c.m0 + q * 32 + lane;
-            float* cre = p.c + c.split * p.ws_split + c.v * p.c_batch;
-            float* cim = cre + p.c_plane;
             const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN;
 #pragma unroll 1
             for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
                 float re[32], im[32];
                 tmem_ld32(base + c0, re);
                 tmem_ld32(base + BN + c0, im);
-                if (row < p.m) bad |= store_chunk(p, cre, cim, row, c.n0 + c0, re, im, tn_lo);
+                if (row < p.m) bad |= store_chunk<E>(p, c.split, c.v, row, c.n0 + c0, re, im, tn_lo);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -510,37 +554,38 @@ EncodeFn encode_fn() {
 }
 
 // 3D map over a [batch][rows][k] fp32 plane, box {32 k, box_rows, 1}, SWIZZLE_128B.
+template <typename E>
 CUtensorMap make_map(const void* base, int64_t k, int64_t rows, int64_t batch, int box_rows) {
     CUtensorMap m;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows),
                           static_cast<cuuint64_t>(std::max<int64_t>(batch, 1))};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * 4), static_cast<cuuint64_t>(k * rows * 4)};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * sizeof(E)), static_cast<cuuint64_t>(k * rows * sizeof(E))};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(KBK<E>), static_cast<cuuint32_t>(box_rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+    const CUresult r = encode_fn()(&m, TcElem<E>::tma, 3, const_cast<void*>(base), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, typename E>
 void launch(const GemmArgs& g, cudaStream_t st) {
     using S = Smem<BN, STAGES>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
         configured = true;
     }
     const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
     const int64_t a_batches = g.a_batch ? std::max<int64_t>(1, g.a_plane / std::max<int64_t>(g.a_batch, 1)) : 1;
     const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
-    const float* a = static_cast<const float*>(g.a);
-    const float* b = static_cast<const float*>(g.b);
-    const CUtensorMap ar = make_map(a, g.k, a_rows, a_batches, kBM);
-    const CUtensorMap ai = make_map(a + g.a_plane, g.k, a_rows, a_batches, kBM);
-    const CUtensorMap br = make_map(b, g.k, g.n, b_batches, BN);
-    const CUtensorMap bi = make_map(b + g.b_plane, g.k, g.n, b_batches, BN);
+    const E* a = static_cast<const E*>(g.a);
+    const E* b = static_cast<const E*>(g.b);
+    const CUtensorMap ar = make_map<E>(a, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap ai = make_map<E>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap br = make_map<E>(b, g.k, g.n, b_batches, BN);
+    const CUtensorMap bi = make_map<E>(b + g.b_plane, g.k, g.n, b_batches, BN);
     TcParams p{};
     p.m = g.m;
     p.n = g.n;
@@ -557,17 +602,17 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.fault = g.fault;
     p.om = g.om;
     const int64_t tiles = p.mt * p.nt * g.batch;
-    const int64_t kblocks = (g.k + kBK - 1) / kBK;
+    const int64_t kblocks = (g.k + KBK<E> - 1) / KBK<E>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
     int splits = 1;
     while (tiles * splits < 296 && kblocks / (splits * 2) >= 8) splits *= 2;
     const int64_t chunk_blocks = (kblocks + splits - 1) / splits;
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
-    p.k_chunk = chunk_blocks * kBK;
+    p.k_chunk = chunk_blocks * KBK<E>;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     if (splits == 1) {
-        p.c = static_cast<float*>(g.c);
+        p.c = g.c;
         p.c_plane = g.c_plane;
         p.c_batch = g.c_batch ? g.c_batch : g.m * g.n;
         p.ws_split = 0;
@@ -585,18 +630,18 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     if (persistent) {
         static bool pconf = false;
         if (!pconf) {
-            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::kBytes);
             pconf = true;
         }
         const int64_t total = tiles * splits;
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-        gemm_tc_persistent<BN, STAGES><<<grid, kPThreads, S::kBytes, st>>>(ar, ai, br, bi, p, total);
+        gemm_tc_persistent<BN, STAGES, E><<<grid, kPThreads, S::kBytes, st>>>(ar, ai, br, bi, p, total);
     } else {
-        gemm_tc_kernel<BN, STAGES><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br,
+        gemm_tc_kernel<BN, STAGES, E><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br,
                                                                                                         bi, p);
     }
-    if (splits > 1) launch_splitk_reduce<float>(p.c, p.ws_split, splits, g, st);
+    if (splits > 1) launch_splitk_reduce<E>(static_cast<const float*>(p.c), p.ws_split, splits, g, st);
 }
 
 }  // namespace
@@ -611,10 +656,14 @@ bool gemm_tc_supported(const GemmArgs& g) {
     return true;
 }
 
-void launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t st) {
-    (void)passes;
-    if (g.n >= 128) launch<128, 3>(g, st);
-    else launch<64, 4>(g, st);
+void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st) {
+    if (elem == 1) {
+        if (g.n >= 128) launch<128, 3, bf16>(g, st);
+        else launch<64, 4, bf16>(g, st);
+    } else {
+        if (g.n >= 128) launch<128, 3, float>(g, st);
+        else launch<64, 4, float>(g, st);
+    }
 }
 
 }  // namespace rcsg

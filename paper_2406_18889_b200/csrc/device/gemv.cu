@@ -16,23 +16,29 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kMaxShort = 4;
 
-template <typename R>
-struct Vec4;
+// 16-byte vector of storage elements
+template <typename S>
+struct Vec16;
 template <>
-struct Vec4<float> {
+struct Vec16<float> {
     using T = float4;
 };
 template <>
-struct Vec4<double> {
-    using T = double2;  // 16 B
+struct Vec16<double> {
+    using T = double2;
+};
+template <>
+struct Vec16<bf16> {
+    using T = uint4;  // 8 bf16
 };
 
-template <typename R>
+template <typename S>
 __global__ void __launch_bounds__(kWarps * 32)
-    gemv_kernel(const GemmArgs g, int64_t rows, int shorts, int long_is_a, int64_t k_chunk, int splits, R* ws,
-                int64_t ws_split) {
-    using V = typename Vec4<R>::T;
-    constexpr int kVec = sizeof(V) / sizeof(R);
+    gemv_kernel(const GemmArgs g, int64_t rows, int shorts, int long_is_a, int64_t k_chunk, int splits,
+                typename Acc<S>::T* ws, int64_t ws_split) {
+    using R = typename Acc<S>::T;
+    using V = typename Vec16<S>::T;
+    constexpr int kVec = sizeof(V) / sizeof(S);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t total = g.batch * rows * splits;
     for (int64_t w = static_cast<int64_t>(blockIdx.x) * kWarps + warp; w < total;
@@ -43,12 +49,12 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int64_t v = t / rows;
         const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
         const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
-        const R* A = static_cast<const R*>(g.a) + av * g.a_batch;
-        const R* B = static_cast<const R*>(g.b) + bv * g.b_batch;
+        const S* A = static_cast<const S*>(g.a) + av * g.a_batch;
+        const S* B = static_cast<const S*>(g.b) + bv * g.b_batch;
         // long operand row `row`, short operand rows 0..shorts-1
-        const R* L = long_is_a ? A + row * g.k : B + row * g.k;
+        const S* L = long_is_a ? A + row * g.k : B + row * g.k;
         const int64_t lplane = long_is_a ? g.a_plane : g.b_plane;
-        const R* S = long_is_a ? B : A;
+        const S* Sh = long_is_a ? B : A;
         const int64_t splane = long_is_a ? g.b_plane : g.a_plane;
         R acc_re[kMaxShort], acc_im[kMaxShort];
 #pragma unroll
@@ -58,29 +64,30 @@ __global__ void __launch_bounds__(kWarps * 32)
             for (int64_t kk = k0 + lane * kVec; kk < k1; kk += 32 * kVec) {
                 const V lr = *reinterpret_cast<const V*>(L + kk);
                 const V li = *reinterpret_cast<const V*>(L + lplane + kk);
-                const R* lrp = reinterpret_cast<const R*>(&lr);
-                const R* lip = reinterpret_cast<const R*>(&li);
+                const S* lrp = reinterpret_cast<const S*>(&lr);
+                const S* lip = reinterpret_cast<const S*>(&li);
 #pragma unroll
                 for (int j = 0; j < kMaxShort; ++j) {
                     if (j >= shorts) break;
-                    const V sr = __ldg(reinterpret_cast<const V*>(S + j * g.k + kk));
-                    const V si = __ldg(reinterpret_cast<const V*>(S + splane + j * g.k + kk));
-                    const R* srp = reinterpret_cast<const R*>(&sr);
-                    const R* sip = reinterpret_cast<const R*>(&si);
+                    const V sr = __ldg(reinterpret_cast<const V*>(Sh + j * g.k + kk));
+                    const V si = __ldg(reinterpret_cast<const V*>(Sh + splane + j * g.k + kk));
+                    const S* srp = reinterpret_cast<const S*>(&sr);
+                    const S* sip = reinterpret_cast<const S*>(&si);
 #pragma unroll
                     for (int e = 0; e < kVec; ++e) {
-                        acc_re[j] = fma(lrp[e], srp[e], acc_re[j]);
-                        acc_re[j] = fma(-lip[e], sip[e], acc_re[j]);
-                        acc_im[j] = fma(lrp[e], sip[e], acc_im[j]);
-                        acc_im[j] = fma(lip[e], srp[e], acc_im[j]);
+                        const R a = load_c(lrp + e), b = load_c(lip + e), c = load_c(srp + e), d = load_c(sip + e);
+                        acc_re[j] = fma(a, c, acc_re[j]);
+                        acc_re[j] = fma(-b, d, acc_re[j]);
+                        acc_im[j] = fma(a, d, acc_im[j]);
+                        acc_im[j] = fma(b, c, acc_im[j]);
                     }
                 }
             }
         } else {
             for (int64_t kk = k0 + lane; kk < k1; kk += 32) {
-                const R lr = L[kk], li = L[lplane + kk];
+                const R lr = load_c(L + kk), li = load_c(L + lplane + kk);
                 for (int j = 0; j < shorts; ++j) {
-                    const R sr = S[j * g.k + kk], si = S[splane + j * g.k + kk];
+                    const R sr = load_c(Sh + j * g.k + kk), si = load_c(Sh + splane + j * g.k + kk);
                     acc_re[j] = fma(lr, sr, acc_re[j]);
                     acc_re[j] = fma(-li, si, acc_re[j]);
                     acc_im[j] = fma(lr, si, acc_im[j]);
@@ -101,9 +108,9 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const int64_t mi = long_is_a ? row : j, ni = long_is_a ? j : row;
                 const int64_t o = v * g.m * g.n + mi * g.n + ni;
                 if (splits == 1) {
-                    R* C = static_cast<R*>(g.c) + v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
-                    C[0] = acc_re[j];
-                    C[g.c_plane] = acc_im[j];
+                    S* C = static_cast<S*>(g.c) + v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
+                    store_c(C, acc_re[j]);
+                    store_c(C + g.c_plane, acc_im[j]);
                     if (g.fault && (!isfinite(acc_re[j]) || !isfinite(acc_im[j]))) atomicMin(g.fault, g.step);
                 } else {
                     ws[split * ws_split + o] = acc_re[j];
@@ -120,8 +127,9 @@ bool gemv_supported(const GemmArgs& g) {
     return (g.n <= kMaxShort || g.m <= kMaxShort) && g.k >= 256;
 }
 
-template <typename R>
+template <typename S>
 void launch_gemv(const GemmArgs& g, cudaStream_t st) {
+    using R = typename Acc<S>::T;
     const bool long_is_a = g.n <= kMaxShort && (g.m > kMaxShort || g.m >= g.n);
     const int64_t rows = long_is_a ? g.m : g.n;
     const int shorts = static_cast<int>(long_is_a ? g.n : g.m);
@@ -137,10 +145,11 @@ void launch_gemv(const GemmArgs& g, cudaStream_t st) {
     }
     const int64_t warps = g.batch * rows * splits;
     const int grid = static_cast<int>(std::min<int64_t>((warps + kWarps - 1) / kWarps, 148 * 64));
-    gemv_kernel<R><<<grid, kWarps * 32, 0, st>>>(g, rows, shorts, long_is_a ? 1 : 0, k_chunk, splits, ws, ws_split);
-    if (splits > 1) launch_splitk_reduce<R>(ws, ws_split, splits, g, st);
+    gemv_kernel<S><<<grid, kWarps * 32, 0, st>>>(g, rows, shorts, long_is_a ? 1 : 0, k_chunk, splits, ws, ws_split);
+    if (splits > 1) launch_splitk_reduce<S>(ws, ws_split, splits, g, st);
 }
 template void launch_gemv<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemv<double>(const GemmArgs&, cudaStream_t);
+template void launch_gemv<bf16>(const GemmArgs&, cudaStream_t);
 
 }  // namespace rcsg

@@ -55,8 +55,9 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
         for (int q = 0; q < nf; ++q) src |= static_cast<uint64_t>((i >> free_obit[q]) & 1) << free_src[q];
         const double re = leaf_data[2 * (j.data_off + src)];
         const double im = leaf_data[2 * (j.data_off + src) + 1];
-        arena[j.out_off + t] = static_cast<R>(re);
-        arena[j.out_off + j.out_plane + t] = static_cast<R>(im);
+        using C = typename Acc<R>::T;
+        store_c(arena + j.out_off + t, static_cast<C>(re));
+        store_c(arena + j.out_off + j.out_plane + t, static_cast<C>(im));
     }
 }
 
@@ -72,6 +73,8 @@ template void launch_leaf_project<float>(const LeafJob*, int, const double*, con
                                          const PassSrc*, const PassState*, float*, cudaStream_t);
 template void launch_leaf_project<double>(const LeafJob*, int, const double*, const uint64_t*,
                                           const PassSrc*, const PassState*, double*, cudaStream_t);
+template void launch_leaf_project<bf16>(const LeafJob*, int, const double*, const uint64_t*,
+                                        const PassSrc*, const PassState*, bf16*, cudaStream_t);
 
 // ------------------------------------------------------------------ SIMT GEMM
 // 64x64 complex tile per CTA, 16x16 threads, 4x4 complex outputs per thread,
@@ -86,13 +89,14 @@ struct SplitK {
     int64_t ws_split;  // elements per split (both planes)
 };
 
-template <typename R>
+template <typename S>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const SplitK sk) {
+    using R = typename Acc<S>::T;
     __shared__ R As_re[BK][BM + 1], As_im[BK][BM + 1];
     __shared__ R Bs_re[BK][BN + 1], Bs_im[BK][BN + 1];
-    const R* A = static_cast<const R*>(g.a);
-    const R* B = static_cast<const R*>(g.b);
-    R* Cm = static_cast<R*>(g.c);
+    const S* A = static_cast<const S*>(g.a);
+    const S* B = static_cast<const S*>(g.b);
+    S* Cm = static_cast<S*>(g.c);
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
     const int64_t mt = (g.m + BM - 1) / BM, nt = (g.n + BN - 1) / BN;
     const int64_t tiles = mt * nt * g.batch * sk.splits;
@@ -105,8 +109,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
         const int64_t m0 = (rem / nt) * BM, n0 = (rem % nt) * BN;
         const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
         const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
-        const R* Ab = A + av * g.a_batch;
-        const R* Bb = B + bv * g.b_batch;
+        const S* Ab = A + av * g.a_batch;
+        const S* Bb = B + bv * g.b_batch;
         R acc_re[4][4], acc_im[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -123,13 +127,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
                 if (gk < k_hi) {
                     if (m0 + row < g.m) {
                         const int64_t o = (m0 + row) * g.k + gk;
-                        ar = Ab[o];
-                        ai = Ab[g.a_plane + o];
+                        ar = load_c(Ab + o);
+                        ai = load_c(Ab + g.a_plane + o);
                     }
                     if (n0 + row < g.n) {
                         const int64_t o = (n0 + row) * g.k + gk;
-                        br = Bb[o];
-                        bi = Bb[g.b_plane + o];
+                        br = load_c(Bb + o);
+                        bi = load_c(Bb + g.b_plane + o);
                     }
                 }
                 As_re[kk][row] = ar;
@@ -160,8 +164,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
             }
             __syncthreads();
         }
-        R* Cb = sk.ws ? static_cast<R*>(sk.ws) + split * sk.ws_split + v * g.m * g.n : Cm + v * g.c_batch;
-        const int64_t cplane = sk.ws ? g.batch * g.m * g.n : g.c_plane;
+        R* W = sk.ws ? static_cast<R*>(sk.ws) + split * sk.ws_split + v * g.m * g.n : nullptr;
+        S* Cb = Cm + v * g.c_batch;
+        const int64_t wplane = g.batch * g.m * g.n;
         bool bad = false;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -169,9 +174,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
             for (int j = 0; j < 4; ++j) {
                 const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
                 if (m < g.m && n < g.n) {
-                    const int64_t o = sk.ws ? m * g.n + n : out_row_off(g.om, g.n, m) + out_col_off(g.om, n);
-                    Cb[o] = acc_re[i][j];
-                    Cb[cplane + o] = acc_im[i][j];
+                    if (W) {
+                        W[m * g.n + n] = acc_re[i][j];
+                        W[wplane + m * g.n + n] = acc_im[i][j];
+                    } else {
+                        const int64_t o = out_row_off(g.om, g.n, m) + out_col_off(g.om, n);
+                        store_c(Cb + o, acc_re[i][j]);
+                        store_c(Cb + g.c_plane + o, acc_im[i][j]);
+                    }
                     bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
                 }
             }
@@ -181,10 +191,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
 
 // Fixed-order split-K reduction shared by every GEMM kernel: C = sum_z W[z],
 // W planar [plane][batch][m][n] per split, C written through the output map.
-template <typename R>
-__global__ void splitk_reduce_kernel(const R* __restrict__ ws, int64_t ws_split, int splits, const GemmArgs g) {
+template <typename S>
+__global__ void splitk_reduce_kernel(const typename Acc<S>::T* __restrict__ ws, int64_t ws_split, int splits,
+                                     const GemmArgs g) {
+    using R = typename Acc<S>::T;
     const int64_t mn = g.m * g.n, per_plane = g.batch * mn;
-    R* C = static_cast<R*>(g.c);
+    S* C = static_cast<S*>(g.c);
     bool bad = false;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < per_plane;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -195,24 +207,27 @@ __global__ void splitk_reduce_kernel(const R* __restrict__ ws, int64_t ws_split,
         }
         const int64_t v = i / mn, e = i - v * mn, mi = e / g.n, ni = e - mi * g.n;
         const int64_t o = v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
-        C[o] = re;
-        C[g.c_plane + o] = im;
+        store_c(C + o, re);
+        store_c(C + g.c_plane + o, im);
         bad |= !isfinite(re) || !isfinite(im);
     }
     if (bad && g.fault) atomicMin(g.fault, g.step);
 }
 
-template <typename R>
-void launch_splitk_reduce(const R* ws, int64_t ws_split, int splits, const GemmArgs& g, cudaStream_t st) {
+template <typename S>
+void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int splits, const GemmArgs& g,
+                          cudaStream_t st) {
     const int64_t per_plane = g.batch * g.m * g.n;
     const int grid = static_cast<int>(std::min<int64_t>((per_plane + 255) / 256, 148 * 16));
-    splitk_reduce_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(ws, ws_split, splits, g);
+    splitk_reduce_kernel<S><<<std::max(grid, 1), 256, 0, st>>>(ws, ws_split, splits, g);
 }
 template void launch_splitk_reduce<float>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
 template void launch_splitk_reduce<double>(const double*, int64_t, int, const GemmArgs&, cudaStream_t);
+template void launch_splitk_reduce<bf16>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
 
-template <typename R>
+template <typename S>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
+    using R = typename Acc<S>::T;
     dim3 block(16, 16);
     const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
     // split long K loops until the grid covers two waves (deterministic reduction)
@@ -224,8 +239,8 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
         sk.ws = device_workspace(static_cast<size_t>(sk.splits) * sk.ws_split * sizeof(R), st);
     }
     const int grid = static_cast<int>(std::min<int64_t>(tiles * sk.splits, 148 * 32));
-    gemm_simt_kernel<R><<<grid, block, 0, st>>>(g, sk);
-    if (sk.splits > 1) launch_splitk_reduce<R>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
+    gemm_simt_kernel<S><<<grid, block, 0, st>>>(g, sk);
+    if (sk.splits > 1) launch_splitk_reduce<S>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
 }
 
 void* device_workspace(size_t bytes, cudaStream_t st) {
@@ -247,6 +262,7 @@ void* device_workspace(size_t bytes, cudaStream_t st) {
 }
 template void launch_gemm_simt<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_simt<double>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_simt<bf16>(const GemmArgs&, cudaStream_t);
 
 // ------------------------------------------------------------------ finalize
 template <typename R>
@@ -264,8 +280,8 @@ __global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, 
         const int64_t v = vid ? vid[gl] : 0;
         const int64_t o = v * payload + p;
         const int64_t g = gidx ? gidx[gl] : gl;
-        acc[2 * (g * payload + i)] += static_cast<double>(root[o]);
-        acc[2 * (g * payload + i) + 1] += static_cast<double>(root[root_plane + o]);
+        acc[2 * (g * payload + i)] += static_cast<double>(load_c(root + o));
+        acc[2 * (g * payload + i) + 1] += static_cast<double>(load_c(root + root_plane + o));
     }
 }
 
@@ -283,6 +299,8 @@ template void launch_finalize<float>(const float*, int64_t, int64_t, int, const 
                                      const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
 template void launch_finalize<double>(const double*, int64_t, int64_t, int, const int32_t*,
                                       const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
+template void launch_finalize<bf16>(const bf16*, int64_t, int64_t, int, const int32_t*,
+                                    const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
 
 // ------------------------------------------------------------------ misc
 __global__ void kahan_kernel(double* res, double* comp, const double* part, int64_t n) {

@@ -4,8 +4,9 @@
 // by an imaginary plane of N elements — with a leading "variant" axis
 // (distinct group projections, see executor.cpp) outermost:
 //   re[v * payload + i], im[(total) + v * payload + i].
-// Real type R is double (RCSG_PREC_F64) or float (all other precisions).
+// Storage type: double (f64), float (f32 / tf32 / 3xtf32) or bf16 (bf16).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -14,6 +15,24 @@ namespace rcsg {
 
 constexpr int kMaxRank = 40;
 constexpr int kMaxLeafRank = 8;
+
+// Storage type S of the tensors vs arithmetic type Acc<S>::T: bf16 storage is
+// computed and accumulated in fp32; float and double compute in themselves.
+using bf16 = __nv_bfloat16;
+template <typename S>
+struct Acc {
+    using T = S;
+};
+template <>
+struct Acc<bf16> {
+    using T = float;
+};
+__device__ __forceinline__ float load_c(const float* p) { return *p; }
+__device__ __forceinline__ double load_c(const double* p) { return *p; }
+__device__ __forceinline__ float load_c(const bf16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void store_c(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_c(double* p, double v) { *p = v; }
+__device__ __forceinline__ void store_c(bf16* p, float v) { *p = __float2bfloat16_rn(v); }
 
 // ---- leaf projection (reference project_leaf, contraction_engine.cpp:27-52,
 // batched over all leaves of one level and all of their variants).
@@ -131,15 +150,17 @@ void launch_gemv(const GemmArgs& g, cudaStream_t st);
 
 // Fixed-order split-K reduction (W planar [split][plane][batch][m][n]) writing C
 // through g.om; shared by all GEMM kernels.
-template <typename R>
-void launch_splitk_reduce(const R* ws, int64_t ws_split, int splits, const GemmArgs& g, cudaStream_t st);
+template <typename S>
+void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int splits, const GemmArgs& g,
+                          cudaStream_t st);
 
 // Scratch buffer for split-K partials, one per stream (grown on demand).
 void* device_workspace(size_t bytes, cudaStream_t st);
 
-// tcgen05 tensor-core path (float storage; kind::tf32, 1 or 3 passes).
+// tcgen05 tensor-core path: elem 0 = fp32 storage (kind::tf32), 1 = bf16 storage
+// (kind::f16 with BF16 operands); fp32 accumulation in TMEM either way.
 bool gemm_tc_supported(const GemmArgs& g);
-void launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t st);
+void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st);
 
 // ---- finalize a pass: acc[g][i] += root[vid[g]][perm(i)]   (acc: double interleaved)
 template <typename R>

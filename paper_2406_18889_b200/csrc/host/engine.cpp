@@ -62,11 +62,12 @@ void set_precision(const std::string& p) {
     else if (p == "f32") g_precision = RCSG_PREC_F32;
     else if (p == "tf32") g_precision = RCSG_PREC_TF32;
     else if (p == "3xtf32") g_precision = RCSG_PREC_3XTF32;
-    else throw ConfigError("precision must be f64, f32, tf32 or 3xtf32");
+    else if (p == "bf16") g_precision = RCSG_PREC_BF16;
+    else throw ConfigError("precision must be f64, f32, tf32, 3xtf32 or bf16");
 }
 
 std::string get_precision() {
-    static const char* names[] = {"f64", "f32", "tf32", "3xtf32"};
+    static const char* names[] = {"f64", "f32", "tf32", "3xtf32", "bf16"};
     return names[g_precision];
 }
 
