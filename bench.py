@@ -35,6 +35,10 @@ CFG2 = dict(n=30, cycles=14, topology="grid(5,6)", seed=1, open=list(range(6)), 
             effort="low")
 WORKLOAD = "cfg2: grid(5,6) n=30 cycles=14 seed=1 l=6 open={0..5}, 2^8 slices (budget 3*2^30 B), K=0"
 METRIC = "slice contractions/s"
+DTYPES = {"f16": "f16 storage (per-tensor 2^e scales), tcgen05 kind::f16, f32 accumulate",
+          "tf32": "f32 storage, tcgen05 kind::tf32, f32 accumulate",
+          "bf16": "bf16 storage, tcgen05 kind::f16 (bf16), f32 accumulate",
+          "f32": "f32 (SIMT)", "f64": "f64 (SIMT)"}
 UNIT = "slice-contractions/s"
 
 
@@ -44,7 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--groups", type=int, default=64)
-    ap.add_argument("--precision", default="tf32")
+    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "bf16", "f32", "f64"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -264,7 +268,10 @@ def main():
     step(args.warmup + args.steps, pst)
     p.set_profile(False)
     tc_tflops = pst.gemm_tc_flops / (pst.gemm_tc_ms * 1e-3) / 1e12 if pst.gemm_tc_ms else 0.0
-    tf32_peak = bf16_peak / 2.0
+    # dense tensor peak of the MMA kind the precision uses: fp16/bf16 = measured bf16; tf32 = half of it
+    tc_peak = bf16_peak / 2.0 if args.precision == "tf32" else bf16_peak
+    peak_note = (f"tf32 dense = 1/2 of {peak_kind} bf16 {bf16_peak:.1f} TF/s" if args.precision == "tf32"
+                 else f"{peak_kind} dense bf16/fp16 peak {bf16_peak:.1f} TF/s")
 
     # end-to-end through the public API with host buffers (rank 0 work pattern on each rank)
     e2e = None
@@ -308,8 +315,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (tf32 tensor-core, fp32 accumulate)"
-            if args.precision == "tf32" else args.precision, "data": "synthetic (random circuit of the named shape)",
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[args.precision],
+            "data": "synthetic (random circuit of the named shape)",
             "config": {"workload": WORKLOAD, "groups_per_slice": M, "duplicate_groups": int(dups),
                        "precision": args.precision, "l2": "inputs larger than L2 (arena "
                        f"{st.arena_bytes / 2**30:.1f} GiB per GPU)", "parallelism": f"slice-sharded x{world}"},
@@ -317,10 +324,12 @@ def main():
             "complex_tflops_executed": exec_flops * world / (ms_max * 1e-3) / 1e12,
             "complex_tflops_reference_equivalent": plan_flops * world / (ms_max * 1e-3) / 1e12,
             "gpu_launches": int(st.kernel_launches),
-            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05 kind::tf32, 4M complex)",
-                         "achieved": tc_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": tc_tflops / tf32_peak,
+            "roofline": {"bound": "tensor",
+                         "kernel": "gemm_tc_kernel/gemm_tc_persistent (tcgen05 " +
+                                   ("kind::tf32" if args.precision == "tf32" else "kind::f16") + ", 4M complex)",
+                         "achieved": tc_tflops, "peak": tc_peak, "unit": "TFLOP/s", "frac": tc_tflops / tc_peak,
                          "traffic": None,
-                         "peak_note": f"tf32 dense = 1/2 of {peak_kind} bf16 {bf16_peak:.1f} TF/s",
+                         "peak_note": peak_note,
                          "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None},
             "kernel_breakdown_ms": {"step": pst.device_ms, "gemm_tc": pst.gemm_tc_ms,
                                     "gemm_other": pst.gemm_ms - pst.gemm_tc_ms, "permute": pst.permute_ms,

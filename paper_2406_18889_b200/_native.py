@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_native", "libpaper_2406_18889_b200.so")
 
 RCSG_OK, RCSG_ERR_CONFIG, RCSG_ERR_NUMERIC, RCSG_ERR_CAPACITY, RCSG_ERR_DEVICE = 0, 2, 3, 4, 5
-PRECISIONS = {"f64": 0, "f32": 1, "tf32": 2, "3xtf32": 3, "bf16": 4}
+PRECISIONS = {"f64": 0, "f32": 1, "tf32": 2, "3xtf32": 3, "bf16": 4, "f16": 5}
 
 
 class rcsg_network_desc(C.Structure):

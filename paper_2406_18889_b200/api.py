@@ -91,7 +91,7 @@ EFFORT = {"low": 0, "medium": 1, "high": 2}
 def _prec(p) -> int:
     if isinstance(p, str):
         if p not in PRECISIONS:
-            raise ConfigError("precision must be f64, f32, tf32, 3xtf32 or bf16")
+            raise ConfigError("precision must be f64, f32, tf32, 3xtf32, bf16 or f16")
         return PRECISIONS[p]
     return int(p)
 

@@ -31,6 +31,9 @@ namespace rcsg {
         } else if ((PREC) == RCSG_PREC_BF16) { \
             using S = bf16;                    \
             BODY;                              \
+        } else if ((PREC) == RCSG_PREC_F16) {  \
+            using S = f16;                     \
+            BODY;                              \
         } else {                               \
             using S = float;                   \
             BODY;                              \
@@ -113,11 +116,29 @@ void permute_bits(const std::vector<int>& from, const std::vector<int>& to, std:
 Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
                  const std::vector<LabelRole>& roles, int precision, uint64_t mem_budget)
     : precision_(precision), mem_budget_(mem_budget), roles_(roles) {
-    if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_BF16)
+    if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_F16)
         throw Failure{RCSG_ERR_CONFIG, "unknown precision"};
-    elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : (precision == RCSG_PREC_BF16 ? 2 : 4);
+    elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : (precision >= RCSG_PREC_BF16 ? 2 : 4);
     build_nodes(net, plan);
     build_steps();
+    node_exp_.assign(nodes_.size(), 0);
+    if (precision == RCSG_PREC_F16) {  // keep the inputs for the calibration program
+        calib_net_ = net;
+        calib_plan_ = plan;
+        const int64_t amps = static_cast<int64_t>(leaf_data_.size()) / 2;
+        (void)amps;
+        c_rank_.assign(net.leaf_rank, net.leaf_rank + net.n_leaves);
+        int64_t nl = 0;
+        for (int i = 0; i < net.n_leaves; ++i) nl += net.leaf_rank[i];
+        c_labels_.assign(net.leaf_labels, net.leaf_labels + nl);
+        c_out_.assign(net.output_labels, net.output_labels + net.n_qubits);
+        c_openl_.assign(net.open_labels, net.open_labels + net.n_open);
+        c_openq_.assign(net.open_qubits, net.open_qubits + net.n_open);
+        c_steps_.assign(plan.steps, plan.steps + 3 * plan.n_steps);
+        c_sliced_.assign(plan.sliced, plan.sliced + plan.n_sliced);
+        c_broken_.assign(plan.broken, plan.broken + plan.n_broken);
+        c_fixed_.assign(plan.fixed_outputs, plan.fixed_outputs + plan.n_fixed);
+    }
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     // leaf data + pass sources + canonical map
     CUDA_OK(cudaMalloc(&d_leaf_data_, std::max<size_t>(leaf_data_.size(), 2) * sizeof(double)));
@@ -590,6 +611,7 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     g.step = st.plan_index;
     g.fault = d_fault_;
     g.om = st.om;
+    g.scale_exp = node_exp_[st.a] + node_exp_[st.b] - node_exp_[st.r];
     if (st.mode == 2) {
         g.m = st.m;
         g.batch = vr;
@@ -619,8 +641,8 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     }
     if constexpr (!std::is_same_v<R, double>) {
         // 3xTF32 stays on the fp32 SIMT kernel until its split-operand tensor-core path lands
-        if ((precision_ == RCSG_PREC_TF32 || precision_ == RCSG_PREC_BF16) && gemm_tc_supported(g)) {
-            launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : 0, stream_);
+        if ((precision_ == RCSG_PREC_TF32 || precision_ >= RCSG_PREC_BF16) && gemm_tc_supported(g)) {
+            launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : (precision_ == RCSG_PREC_F16 ? 2 : 0), stream_);
             mark_end(mk, kCatGemmTc, flops, st.plan_index, g.m, g.n, g.k, g.batch);
             ++launches_;
             return;
@@ -690,6 +712,11 @@ void Program::collect_marks(rcsg_stats* stats) {
 
 void Program::exec_step(const StepInfo& st, const ChunkData* ch) {
     RCSG_DISPATCH(precision_, exec_step_t<S>(st, ch));
+    if (record_max_) {  // calibration: max |value| of the step's output
+        const NodeInfo& R = nodes_[st.r];
+        const int64_t vr = (R.level == 2 && ch) ? ch->nvar[st.r] : 1;
+        launch_maxabs(static_cast<const float*>(buf(R.off)), R.plane, vr * R.payload, d_max_ + st.r, stream_);
+    }
 }
 
 void Program::exec_level(int level, const ChunkData* ch) {
@@ -718,10 +745,68 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     // (re)bind the program to this group list: chunk capacity, arena, chunk
     // index tables.  Repeated calls with the same groups (one call per slice
     // range) reuse everything.
+    if (precision_ == RCSG_PREC_F16 && !calibrated_)
+        calibrate(groups, configs.empty() ? 0 : configs[0], slice_begin);
     if (groups != bound_groups_) bind_groups(groups);
     const int64_t P = nodes_[root_].payload;
     const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
     run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n);
+}
+
+// fp16 mode: per-tensor power-of-two scales.  A transient tf32 program runs one
+// pass (first slice, first configuration, up to 16 of the groups) and records
+// every node's max |value|; node r is then stored times 2^-e_r with
+// e_r = ceil(log2 max_r) - 10, i.e. at most 2^10 in magnitude (64x headroom
+// below the fp16 maximum for other slices and groups).  Each GEMM multiplies
+// its fp32 result by 2^(e_a + e_b - e_r) before rounding to fp16; finalize
+// multiplies the root by 2^e_root.
+void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, uint64_t slice) {
+    rcsg_network_desc net = calib_net_;
+    net.leaf_rank = c_rank_.data();
+    net.leaf_labels = c_labels_.data();
+    net.leaf_data = leaf_data_.data();
+    net.output_labels = c_out_.data();
+    net.open_labels = c_openl_.data();
+    net.open_qubits = c_openq_.data();
+    rcsg_plan_desc plan = calib_plan_;
+    plan.steps = c_steps_.data();
+    plan.sliced = c_sliced_.data();
+    plan.broken = c_broken_.data();
+    plan.fixed_outputs = c_fixed_.data();
+    std::vector<uint64_t> sub(groups.begin(), groups.begin() + std::min<size_t>(groups.size(), 16));
+    std::vector<float> mx(nodes_.size(), 0.f);
+    {
+        size_t fr = 0, tot = 0;
+        CUDA_OK(cudaMemGetInfo(&fr, &tot));
+        Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.4));
+        CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
+        CUDA_OK(cudaMemset(cal.d_max_, 0, nodes_.size() * sizeof(float)));
+        cal.record_max_ = true;
+        double* d_acc = nullptr;
+        CUDA_OK(cudaMalloc(&d_acc, sub.size() * (size_t{1} << out_rank_) * 2 * sizeof(double)));
+        CUDA_OK(cudaMemset(d_acc, 0, sub.size() * (size_t{1} << out_rank_) * 2 * sizeof(double)));
+        std::vector<uint64_t> cfg;
+        if (calib_plan_.n_broken) cfg.push_back(config);
+        try {
+            cal.run(sub, cfg, slice, slice + 1, d_acc, nullptr);
+        } catch (...) {
+            cudaFree(d_acc);
+            cudaFree(cal.d_max_);
+            cal.d_max_ = nullptr;
+            throw;
+        }
+        CUDA_OK(cudaMemcpy(mx.data(), cal.d_max_, mx.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        cudaFree(d_acc);
+        cudaFree(cal.d_max_);
+        cal.d_max_ = nullptr;
+    }
+    for (const StepInfo& st : steps_) {
+        const float m = mx[st.r];
+        node_exp_[st.r] = m > 0.f && std::isfinite(m) ? static_cast<int>(std::ceil(std::log2(m))) - 10
+                                                      : node_exp_[st.a] + node_exp_[st.b];
+    }
+    calibrated_ = true;
+    reset_graph();
 }
 
 void Program::bind_groups(const std::vector<uint64_t>& groups) {
@@ -799,7 +884,8 @@ void Program::exec_pass_body(int64_t P) {
         exec_level(2, &ch);
         const NodeInfo& root = nodes_[root_];
         RCSG_DISPATCH(precision_,
-                      launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane, P,
+                      launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane,
+                                         std::ldexp(1.0, node_exp_[root_]), P,
                                          static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
                                          static_cast<int64_t>(ch.groups.size()), d_part_, stream_));
         ++launches_;

@@ -120,6 +120,7 @@ class Program {
     int64_t plan_arena(int64_t chunk_cap, bool assign);
     void prepare_chunks(const std::vector<uint64_t>& groups, int64_t chunk_cap);
     void bind_groups(const std::vector<uint64_t>& groups);
+    void calibrate(const std::vector<uint64_t>& groups, uint64_t config, uint64_t slice);
     void exec_pass_body(int64_t P);
     void run_pass_body(int64_t P);
     void reset_graph();
@@ -164,6 +165,15 @@ class Program {
     int64_t acc_cap_ = 0;
     std::vector<ChunkData> chunks_;
     std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
+    // fp16 mode: per-node storage exponents (value stored times 2^-e) and the
+    // inputs kept to build the calibration program
+    std::vector<int> node_exp_;
+    bool calibrated_ = false;
+    bool record_max_ = false;
+    float* d_max_ = nullptr;
+    rcsg_network_desc calib_net_{};
+    rcsg_plan_desc calib_plan_{};
+    std::vector<int32_t> c_rank_, c_labels_, c_out_, c_openl_, c_openq_, c_steps_, c_sliced_, c_broken_, c_fixed_;
     cudaGraphExec_t graph_exec_ = nullptr;  // captured pass body (level 1 + chunks)
     bool graph_warm_ = false;
     uint64_t graph_launches_ = 0;

@@ -16,6 +16,7 @@ constexpr int kRows = 64;  // output rows per CTA
 template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
     using R = typename Acc<S>::T;
+    const R sc = pow2<R>(g.scale_exp);
     __shared__ R a_re[kRows][K], a_im[kRows][K];
     __shared__ int64_t row_off[kRows];
     const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + kRows - 1) / kRows;
@@ -59,9 +60,11 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
                     ci = fma(a_im[r][kk], b_re[kk], ci);
                 }
                 const int64_t o = row_off[r] + col_off;
+                cr *= sc;
+                ci *= sc;
                 store_c(C + o, cr);
                 store_c(C + g.c_plane + o, ci);
-                bad |= !isfinite(cr) || !isfinite(ci);
+                bad |= unstorable<S>(cr) || unstorable<S>(ci);
             }
         }
     }
@@ -77,6 +80,7 @@ constexpr int kColTile = 64;
 template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g) {
     using R = typename Acc<S>::T;
+    const R sc = pow2<R>(g.scale_exp);
     __shared__ R b_re[kColTile][K], b_im[kColTile][K];
     __shared__ int64_t col_off[kColTile];
     bool bad = false;
@@ -121,9 +125,11 @@ __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g)
                 ci = fma(a_im[kk], b_re[c][kk], ci);
             }
             const int64_t o = roff + col_off[c];
+            cr *= sc;
+            ci *= sc;
             store_c(C + o, cr);
             store_c(C + g.c_plane + o, ci);
-            bad |= !isfinite(cr) || !isfinite(ci);
+            bad |= unstorable<S>(cr) || unstorable<S>(ci);
         }
     }
     if (bad && g.fault) atomicMin(g.fault, g.step);
@@ -158,5 +164,6 @@ void launch_gemm_smallk(const GemmArgs& g, cudaStream_t st) {
 template void launch_gemm_smallk<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_smallk<double>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_smallk<bf16>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_smallk<f16>(const GemmArgs&, cudaStream_t);
 
 }  // namespace rcsg

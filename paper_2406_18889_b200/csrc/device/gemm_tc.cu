@@ -129,6 +129,11 @@ struct TcElem<bf16> {
     static constexpr uint32_t fmt = 1;  // BF16 (kind::f16)
     static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };
+template <>
+struct TcElem<f16> {
+    static constexpr uint32_t fmt = 0;  // F16 (kind::f16)
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+};
 template <typename E>
 __host__ __device__ constexpr uint32_t idesc_of(int bn, bool neg_a) {
     return (1u << 4) | (TcElem<E>::fmt << 7) | (TcElem<E>::fmt << 10) | (neg_a ? (1u << 13) : 0u) |
@@ -179,6 +184,7 @@ struct TcParams {
     int32_t step;
     int32_t* fault;
     OutMap om;              // output scatter map (applied when not split)
+    int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
 };
 
 // Store one 32-column chunk of a thread's row: to the split-K workspace
@@ -186,11 +192,11 @@ struct TcParams {
 // through the output scatter map into the consumer's layout.
 template <typename E>
 __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_t v, int64_t row, int64_t col0,
-                                            const float* re, const float* im, const int64_t* tn_lo) {
+                                            float* re, float* im, const int64_t* tn_lo) {
     bool bad = false;
+    if (p.ws_split) {  // raw partials; the reduction scales and checks
 #pragma unroll
-    for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
-    if (p.ws_split) {
+        for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
         float* cre = static_cast<float*>(p.c) + split * p.ws_split + v * p.c_batch;
         float* pr = cre + row * p.n + col0;
         float* pi = pr + p.c_plane;
@@ -200,6 +206,16 @@ __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_
         }
         return bad;
     }
+    if (p.scale_exp) {
+        const float sc = exp2f(static_cast<float>(p.scale_exp));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            re[i] *= sc;
+            im[i] *= sc;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bad |= unstorable<E>(re[i]) || unstorable<E>(im[i]);
     E* cre = static_cast<E*>(p.c) + v * p.c_batch;
     E* cim = cre + p.c_plane;
     if (!p.om.scatter) {
@@ -601,6 +617,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.step = g.step;
     p.fault = g.fault;
     p.om = g.om;
+    p.scale_exp = g.scale_exp;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + KBK<E> - 1) / KBK<E>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
@@ -660,6 +677,9 @@ void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st) {
     if (elem == 1) {
         if (g.n >= 128) launch<128, 3, bf16>(g, st);
         else launch<64, 4, bf16>(g, st);
+    } else if (elem == 2) {
+        if (g.n >= 128) launch<128, 3, f16>(g, st);
+        else launch<64, 4, f16>(g, st);
     } else {
         if (g.n >= 128) launch<128, 3, float>(g, st);
         else launch<64, 4, float>(g, st);

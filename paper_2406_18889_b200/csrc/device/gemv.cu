@@ -31,6 +31,10 @@ template <>
 struct Vec16<bf16> {
     using T = uint4;  // 8 bf16
 };
+template <>
+struct Vec16<f16> {
+    using T = uint4;  // 8 fp16
+};
 
 template <typename S>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -109,9 +113,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const int64_t o = v * g.m * g.n + mi * g.n + ni;
                 if (splits == 1) {
                     S* C = static_cast<S*>(g.c) + v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
-                    store_c(C, acc_re[j]);
-                    store_c(C + g.c_plane, acc_im[j]);
-                    if (g.fault && (!isfinite(acc_re[j]) || !isfinite(acc_im[j]))) atomicMin(g.fault, g.step);
+                    const R sc = pow2<R>(g.scale_exp), vr = acc_re[j] * sc, vi = acc_im[j] * sc;
+                    store_c(C, vr);
+                    store_c(C + g.c_plane, vi);
+                    if (g.fault && (unstorable<S>(vr) || unstorable<S>(vi))) atomicMin(g.fault, g.step);
                 } else {
                     ws[split * ws_split + o] = acc_re[j];
                     ws[split * ws_split + ws_split / 2 + o] = acc_im[j];
@@ -151,5 +156,6 @@ void launch_gemv(const GemmArgs& g, cudaStream_t st) {
 template void launch_gemv<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemv<double>(const GemmArgs&, cudaStream_t);
 template void launch_gemv<bf16>(const GemmArgs&, cudaStream_t);
+template void launch_gemv<f16>(const GemmArgs&, cudaStream_t);
 
 }  // namespace rcsg

@@ -75,6 +75,8 @@ template void launch_leaf_project<double>(const LeafJob*, int, const double*, co
                                           const PassSrc*, const PassState*, double*, cudaStream_t);
 template void launch_leaf_project<bf16>(const LeafJob*, int, const double*, const uint64_t*,
                                         const PassSrc*, const PassState*, bf16*, cudaStream_t);
+template void launch_leaf_project<f16>(const LeafJob*, int, const double*, const uint64_t*,
+                                       const PassSrc*, const PassState*, f16*, cudaStream_t);
 
 // ------------------------------------------------------------------ SIMT GEMM
 // 64x64 complex tile per CTA, 16x16 threads, 4x4 complex outputs per thread,
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
     const S* B = static_cast<const S*>(g.b);
     S* Cm = static_cast<S*>(g.c);
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
+    const R sc = pow2<R>(g.scale_exp);
     const int64_t mt = (g.m + BM - 1) / BM, nt = (g.n + BN - 1) / BN;
     const int64_t tiles = mt * nt * g.batch * sk.splits;
     for (int64_t tile_s = blockIdx.x; tile_s < tiles; tile_s += gridDim.x) {
@@ -177,12 +180,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
                     if (W) {
                         W[m * g.n + n] = acc_re[i][j];
                         W[wplane + m * g.n + n] = acc_im[i][j];
+                        bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
                     } else {
                         const int64_t o = out_row_off(g.om, g.n, m) + out_col_off(g.om, n);
-                        store_c(Cb + o, acc_re[i][j]);
-                        store_c(Cb + g.c_plane + o, acc_im[i][j]);
+                        const R vr = acc_re[i][j] * sc, vi = acc_im[i][j] * sc;
+                        store_c(Cb + o, vr);
+                        store_c(Cb + g.c_plane + o, vi);
+                        bad |= unstorable<S>(vr) || unstorable<S>(vi);
                     }
-                    bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
                 }
             }
         if (bad && g.fault && !sk.ws) atomicMin(g.fault, g.step);
@@ -196,6 +201,7 @@ __global__ void splitk_reduce_kernel(const typename Acc<S>::T* __restrict__ ws, 
                                      const GemmArgs g) {
     using R = typename Acc<S>::T;
     const int64_t mn = g.m * g.n, per_plane = g.batch * mn;
+    const R sc = pow2<R>(g.scale_exp);
     S* C = static_cast<S*>(g.c);
     bool bad = false;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < per_plane;
@@ -207,9 +213,11 @@ __global__ void splitk_reduce_kernel(const typename Acc<S>::T* __restrict__ ws, 
         }
         const int64_t v = i / mn, e = i - v * mn, mi = e / g.n, ni = e - mi * g.n;
         const int64_t o = v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
+        re *= sc;
+        im *= sc;
         store_c(C + o, re);
         store_c(C + g.c_plane + o, im);
-        bad |= !isfinite(re) || !isfinite(im);
+        bad |= unstorable<S>(re) || unstorable<S>(im);
     }
     if (bad && g.fault) atomicMin(g.fault, g.step);
 }
@@ -224,6 +232,7 @@ void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int sp
 template void launch_splitk_reduce<float>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
 template void launch_splitk_reduce<double>(const double*, int64_t, int, const GemmArgs&, cudaStream_t);
 template void launch_splitk_reduce<bf16>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
+template void launch_splitk_reduce<f16>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
 
 template <typename S>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
@@ -263,10 +272,11 @@ void* device_workspace(size_t bytes, cudaStream_t st) {
 template void launch_gemm_simt<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_simt<double>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_simt<bf16>(const GemmArgs&, cudaStream_t);
+template void launch_gemm_simt<f16>(const GemmArgs&, cudaStream_t);
 
 // ------------------------------------------------------------------ finalize
 template <typename R>
-__global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, int64_t payload,
+__global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, double root_scale, int64_t payload,
                                 int rank, const int32_t* __restrict__ src_bit,
                                 const int32_t* __restrict__ vid, const int32_t* __restrict__ gidx,
                                 int64_t n_groups, double* __restrict__ acc) {
@@ -280,27 +290,29 @@ __global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, 
         const int64_t v = vid ? vid[gl] : 0;
         const int64_t o = v * payload + p;
         const int64_t g = gidx ? gidx[gl] : gl;
-        acc[2 * (g * payload + i)] += static_cast<double>(load_c(root + o));
-        acc[2 * (g * payload + i) + 1] += static_cast<double>(load_c(root + root_plane + o));
+        acc[2 * (g * payload + i)] += static_cast<double>(load_c(root + o)) * root_scale;
+        acc[2 * (g * payload + i) + 1] += static_cast<double>(load_c(root + root_plane + o)) * root_scale;
     }
 }
 
 template <typename R>
-void launch_finalize(const R* root, int64_t root_plane, int64_t payload, int rank,
+void launch_finalize(const R* root, int64_t root_plane, double root_scale, int64_t payload, int rank,
                      const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
                      const int32_t* d_gidx, int64_t n_groups_chunk, double* acc, cudaStream_t st) {
     const int64_t total = n_groups_chunk * payload;
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, grid_cap()));
-    finalize_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(root, root_plane, payload, rank,
+    finalize_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(root, root_plane, root_scale, payload, rank,
                                                           d_src_bit_of_canon, d_vid, d_gidx,
                                                           n_groups_chunk, acc);
 }
-template void launch_finalize<float>(const float*, int64_t, int64_t, int, const int32_t*,
+template void launch_finalize<float>(const float*, int64_t, double, int64_t, int, const int32_t*,
                                      const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
-template void launch_finalize<double>(const double*, int64_t, int64_t, int, const int32_t*,
+template void launch_finalize<double>(const double*, int64_t, double, int64_t, int, const int32_t*,
                                       const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
-template void launch_finalize<bf16>(const bf16*, int64_t, int64_t, int, const int32_t*,
+template void launch_finalize<bf16>(const bf16*, int64_t, double, int64_t, int, const int32_t*,
                                     const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
+template void launch_finalize<f16>(const f16*, int64_t, double, int64_t, int, const int32_t*,
+                                   const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
 
 // ------------------------------------------------------------------ misc
 __global__ void kahan_kernel(double* res, double* comp, const double* part, int64_t n) {
@@ -315,6 +327,19 @@ __global__ void kahan_kernel(double* res, double* comp, const double* part, int6
 void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, grid_cap()));
     kahan_kernel<<<std::max(grid, 1), 256, 0, st>>>(res, comp, part, n);
+}
+
+__global__ void maxabs_kernel(const float* buf, int64_t plane, int64_t count, float* out) {
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = fmaxf(m, fmaxf(fabsf(buf[i]), fabsf(buf[plane + i])));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(m));  // m >= 0
+}
+void launch_maxabs(const float* buf, int64_t plane, int64_t count, float* out, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((count + 255) / 256, grid_cap()));
+    maxabs_kernel<<<std::max(grid, 1), 256, 0, st>>>(buf, plane, count, out);
 }
 
 __global__ void fill_kernel(double* p, double v, int64_t n) {

@@ -7,9 +7,11 @@
 // Storage type: double (f64), float (f32 / tf32 / 3xtf32) or bf16 (bf16).
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace rcsg {
 
@@ -27,12 +29,30 @@ template <>
 struct Acc<bf16> {
     using T = float;
 };
+using f16 = __half;
+template <>
+struct Acc<f16> {
+    using T = float;
+};
 __device__ __forceinline__ float load_c(const float* p) { return *p; }
 __device__ __forceinline__ double load_c(const double* p) { return *p; }
 __device__ __forceinline__ float load_c(const bf16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ void store_c(float* p, float v) { *p = v; }
 __device__ __forceinline__ void store_c(double* p, double v) { *p = v; }
 __device__ __forceinline__ void store_c(bf16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ float load_c(const f16* p) { return __half2float(*p); }
+__device__ __forceinline__ void store_c(f16* p, float v) { *p = __float2half_rn(v); }
+// value not representable in storage type S (non-finite, or beyond the fp16 range)
+template <typename S>
+__device__ __forceinline__ bool unstorable(typename Acc<S>::T v) {
+    if constexpr (sizeof(S) == 2 && !std::is_same_v<S, bf16>) return !(fabsf(v) <= 65504.f);
+    else return !isfinite(v);
+}
+// 2^e as the compute type (GEMM output scaling of the fp16 mode; 1 elsewhere)
+template <typename R>
+__device__ __forceinline__ R pow2(int e) {
+    return static_cast<R>(exp2f(static_cast<float>(e)));
+}
 
 // ---- leaf projection (reference project_leaf, contraction_engine.cpp:27-52,
 // batched over all leaves of one level and all of their variants).
@@ -134,6 +154,7 @@ struct GemmArgs {
     int32_t step;           // plan step index for the non-finite flag
     int32_t* fault;         // device flag: min step index with a non-finite output
     OutMap om;              // where C elements land inside their variant block
+    int32_t scale_exp;      // outputs are stored times 2^scale_exp (fp16 per-tensor scaling; 0 otherwise)
 };
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
@@ -164,10 +185,13 @@ void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st);
 
 // ---- finalize a pass: acc[g][i] += root[vid[g]][perm(i)]   (acc: double interleaved)
 template <typename R>
-void launch_finalize(const R* root, int64_t root_plane, int64_t payload, int rank,
+void launch_finalize(const R* root, int64_t root_plane, double root_scale, int64_t payload, int rank,
                      const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
                      const int32_t* d_gidx, int64_t n_groups_chunk, double* acc,
                      cudaStream_t st);
+
+// max |value| over both planes of a float buffer (atomicMax into *out; calibration)
+void launch_maxabs(const float* buf, int64_t plane, int64_t count, float* out, cudaStream_t st);
 
 // compensated accumulation in configuration order (contraction_engine.cpp:289-302)
 void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st);

@@ -113,6 +113,11 @@ struct Vec<bf16> {
     using T = uint2;  // 4 bf16, same run requirement as float
     static constexpr int N = 4;
 };
+template <>
+struct Vec<f16> {
+    using T = uint2;
+    static constexpr int N = 4;
+};
 
 constexpr int kThreads = 256;
 
@@ -213,5 +218,6 @@ template void launch_permute<float>(const float*, int64_t, float*, int64_t, int6
 template void launch_permute<double>(const double*, int64_t, double*, int64_t, int64_t, const PermuteDesc&,
                                      cudaStream_t);
 template void launch_permute<bf16>(const bf16*, int64_t, bf16*, int64_t, int64_t, const PermuteDesc&, cudaStream_t);
+template void launch_permute<f16>(const f16*, int64_t, f16*, int64_t, int64_t, const PermuteDesc&, cudaStream_t);
 
 }  // namespace rcsg

@@ -63,11 +63,12 @@ void set_precision(const std::string& p) {
     else if (p == "tf32") g_precision = RCSG_PREC_TF32;
     else if (p == "3xtf32") g_precision = RCSG_PREC_3XTF32;
     else if (p == "bf16") g_precision = RCSG_PREC_BF16;
-    else throw ConfigError("precision must be f64, f32, tf32, 3xtf32 or bf16");
+    else if (p == "f16") g_precision = RCSG_PREC_F16;
+    else throw ConfigError("precision must be f64, f32, tf32, 3xtf32, bf16 or f16");
 }
 
 std::string get_precision() {
-    static const char* names[] = {"f64", "f32", "tf32", "3xtf32", "bf16"};
+    static const char* names[] = {"f64", "f32", "tf32", "3xtf32", "bf16", "f16"};
     return names[g_precision];
 }
 

@@ -325,7 +325,7 @@ int rcsh_contract(void* hp, int precision, int n_fixed, const int* labels, const
                   const std::uint64_t* cfgs, double* out, std::uint64_t* flops) {
     return guarded([&] {
         Handle* h = static_cast<Handle*>(hp);
-        set_precision(precision == 0 ? "f64" : precision == 1 ? "f32" : precision == 2 ? "tf32" : precision == 3 ? "3xtf32" : "bf16");
+        set_precision(precision == 0 ? "f64" : precision == 1 ? "f32" : precision == 2 ? "tf32" : precision == 3 ? "3xtf32" : precision == 4 ? "bf16" : "f16");
         std::map<Label, int> fixed;
         for (int i = 0; i < n_fixed; ++i) fixed[labels[i]] = values[i];
         BrokenEdgeConfig cfg = h->config;
@@ -342,7 +342,7 @@ int rcsh_execute(void* hp, int precision, int n, const int* labels, const int* v
                  std::int64_t* n_out) {
     return guarded([&] {
         Handle* h = static_cast<Handle*>(hp);
-        set_precision(precision == 0 ? "f64" : precision == 1 ? "f32" : precision == 2 ? "tf32" : precision == 3 ? "3xtf32" : "bf16");
+        set_precision(precision == 0 ? "f64" : precision == 1 ? "f32" : precision == 2 ? "tf32" : precision == 3 ? "3xtf32" : precision == 4 ? "bf16" : "f16");
         std::map<Label, int> a;
         for (int i = 0; i < n; ++i) a[labels[i]] = values[i];
         std::vector<cplx> v = execute_assignment(h->net, h->plan, a);

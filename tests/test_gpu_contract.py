@@ -11,7 +11,7 @@ from oracle import port
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"f64": 1e-10, "f32": 2e-5, "tf32": 1e-2, "3xtf32": 2e-5, "bf16": 1.5e-1}
+TOL = {"f64": 1e-10, "f32": 2e-5, "tf32": 1e-2, "3xtf32": 2e-5, "bf16": 1.5e-1, "f16": 1e-2}
 
 
 def rel(a, b):
@@ -26,7 +26,7 @@ def cfg1(M=64):
     return p, fixed
 
 
-@pytest.mark.parametrize("precision", ["f64", "f32", "tf32", "3xtf32", "bf16"])
+@pytest.mark.parametrize("precision", ["f64", "f32", "tf32", "3xtf32", "bf16", "f16"])
 def test_cfg1_groups_match_oracle(precision):
     p, fixed = cfg1(64)
     pn = port.PortNet(p.net, p.plan)
@@ -147,7 +147,7 @@ def test_error_taxonomy():
 GOLDEN_CASES = ["cfg1", "sliced_line10", "broken_ring10", "grid44_sliced_broken"]
 
 
-@pytest.mark.parametrize("precision", ["f64", "tf32", "bf16"])
+@pytest.mark.parametrize("precision", ["f64", "tf32", "bf16", "f16"])
 @pytest.mark.parametrize("name", GOLDEN_CASES)
 def test_gpu_matches_reference_fixture(name, precision):
     import os
@@ -169,7 +169,7 @@ def test_cfg2_circuit_pair_matches_live_reference(ref):
     assert np.array_equal(r.plan["steps"], p.plan["steps"])
     fixed, _ = pb.build_candidate_set(30, list(range(6)), 2, pb.split_next(1, 0xCA11D))
     want = r.execute_gsc(int(fixed[0]), 3)
-    for precision in ("f64", "tf32", "bf16"):
+    for precision in ("f64", "tf32", "bf16", "f16"):
         got = p.contract_groups(fixed[:1], precision=precision, configs=None, slices=(3, 4))[0]
         print(precision, rel(got, want))
         assert rel(got, want) < TOL[precision], precision
