@@ -225,34 +225,39 @@ def main():
     def slice_of(i):
         return (rank + i * world) % p.n_slices
 
-    def step(i, st=None):
+    def step(i, st=None, sync=True):
         s = slice_of(i)
         return p.contract_groups_device(fixed, acc.data_ptr(), precision=args.precision, configs=None,
-                                        slices=(s, s + 1), stats=st)
+                                        slices=(s, s + 1), stats=st, sync=sync)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # L2 flush between timed steps: a 256 MiB write (> 126 MB L2) on the program's
+    # stream, outside each step's event pair
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     clocks = Clocks(local)
     st = rcsg_stats()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ev0.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i, st)
-    ev1.record(stream)
-    if world > 1:
-        with torch.cuda.stream(stream):
-            dist.all_reduce(acc)  # the slice sum across ranks
-        ev1.record(stream)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step(args.warmup + i, st, sync=False)  # enqueue only; checked by p.sync below
+            if i == args.steps - 1 and world > 1:
+                dist.all_reduce(acc)  # the slice sum across ranks
+            evs[i][1].record(stream)
+    p.sync(args.precision)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
     clk = clocks.stop()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -318,8 +323,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[args.precision],
             "data": "synthetic (random circuit of the named shape)",
             "config": {"workload": WORKLOAD, "groups_per_slice": M, "duplicate_groups": int(dups),
-                       "precision": args.precision, "l2": "inputs larger than L2 (arena "
-                       f"{st.arena_bytes / 2**30:.1f} GiB per GPU)", "parallelism": f"slice-sharded x{world}"},
+                       "precision": args.precision, "l2": "flushed between timed steps (256 MiB write, "
+                       f"outside the per-step events); arena {st.arena_bytes / 2**30:.2f} GiB per GPU",
+                       "parallelism": f"slice-sharded x{world}"},
             "group_slice_pairs_per_s": value * M,
             "complex_tflops_executed": exec_flops * world / (ms_max * 1e-3) / 1e12,
             "complex_tflops_reference_equivalent": plan_flops * world / (ms_max * 1e-3) / 1e12,

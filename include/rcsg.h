@@ -137,6 +137,10 @@ int rcsg_contract_groups_device(rcsg_program* prog, uint64_t n_groups,
                                 uint64_t slice_end, double* d_acc, int32_t sync,
                                 rcsg_stats* stats);
 
+/* Wait for the program's stream; reports (RCSG_ERR_NUMERIC) a non-finite
+ * intermediate of an earlier sync == 0 call. */
+int rcsg_program_sync(rcsg_program* prog);
+
 /* Compile with explicit pins instead of group variants: pinned[label] in {0,1}
  * fixes a label for every execution (-1 = not pinned); sliced / broken labels
  * still come from the pass.  Every non-open output must be pinned, otherwise

@@ -242,8 +242,12 @@ class Problem:
         return out.view(np.complex128).reshape(len(fixed), -1)
 
     def contract_groups_device(self, fixed, d_acc: int, precision="tf32", configs="all",
-                               slices=None, budget=0, stats: rcsg_stats | None = None):
-        """Accumulate into a DEVICE float64 buffer (e.g. a torch tensor's data_ptr())."""
+                               slices=None, budget=0, stats: rcsg_stats | None = None, sync=True):
+        """Accumulate into a DEVICE float64 buffer (e.g. a torch tensor's data_ptr()).
+
+        sync=False returns once the work is enqueued on the program's stream
+        (self.stream(precision)); a NumericFault is then raised by the next
+        synchronous call or by self.sync(precision)."""
         fixed = _u64(fixed)
         s0, s1 = slices if slices is not None else (0, self.n_slices)
         if isinstance(configs, str):
@@ -257,8 +261,12 @@ class Problem:
         _check_h(_native.lib().rcsh_contract_groups_device(
             self.handle, _prec(precision), C.c_uint64(budget), C.c_uint64(len(fixed)),
             _p(fixed, C.c_uint64), n_cfg, _p(cf, C.c_uint64), C.c_uint64(s0), C.c_uint64(s1),
-            C.c_void_p(d_acc), C.byref(st)))
+            C.c_void_p(d_acc), C.byref(st), int(bool(sync))))
         return st
+
+    def sync(self, precision="tf32", budget=0):
+        """Wait for the program's stream; raises a deferred NumericFault."""
+        _check_h(_native.lib().rcsh_program_sync(self.handle, _prec(precision), C.c_uint64(budget)))
 
     def contract_group(self, fixed_bits: int, precision="f64") -> np.ndarray:
         """contract_group (contraction_engine.cpp:307-325)."""

@@ -178,8 +178,14 @@ int rcsg_contract_groups_device(rcsg_program* prog, uint64_t n_groups, const uin
             throw Failure{RCSG_ERR_CONFIG, "slice range outside [0, 2^|sliced|)"};
         std::vector<uint64_t> groups(group_fixed, group_fixed + n_groups);
         std::vector<uint64_t> cfgs(configs, configs + n_configs);
-        prog->prog->run(groups, cfgs, slice_begin, slice_end, d_acc, stats);
-        (void)sync;  // run() completes on its stream before returning
+        prog->prog->run(groups, cfgs, slice_begin, slice_end, d_acc, stats, sync != 0);
+    });
+}
+
+int rcsg_program_sync(rcsg_program* prog) {
+    return guard([&] {
+        if (!prog) throw Failure{RCSG_ERR_CONFIG, "null program"};
+        prog->prog->sync();
     });
 }
 

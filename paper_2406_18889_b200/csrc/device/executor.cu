@@ -111,6 +111,148 @@ void permute_bits(const std::vector<int>& from, const std::vector<int>& to, std:
     }
 }
 
+// ---- batch-aware reassociation of the contraction tree -------------------
+// The reference plans one group's network (var legs projected).  With a group
+// batch, a node's cost is multiplied by its variant count (distinct
+// projections of the batch's prefixes onto the output legs in its subtree),
+// so the single-group optimum pushes group-dependent work into the big stem
+// steps.  Local rotations fix that: for P = (Z, W) with Z = (X, Y), try
+// P = (X, (Y, W)) and P = (Y, (X, W)); keep a rotation when the modelled time
+// of the two steps drops.  P's labels and subtree are unchanged, so the
+// result is the same tensor (up to rounding); slices, configurations and the
+// canonical output order are untouched.  SURVEY §8f row 2 ("group batching as
+// a plan transform", the paper's sparse-state stage).
+struct TreeNode {
+    std::vector<int> labels;  // free labels, sorted
+    uint64_t mask = 0;        // group-code bits in the subtree
+    int level = 0;            // 0 constant, 1 per pass, 2 per group
+    int a = -1, b = -1;       // children (internal nodes)
+};
+
+struct TreeCost {
+    const std::vector<uint64_t>& groups;
+    double pf, bw, elem;
+    std::map<uint64_t, double> nv_cache;
+    double nvar(uint64_t mask) {
+        if (!mask) return 1.0;
+        auto it = nv_cache.find(mask);
+        if (it != nv_cache.end()) return it->second;
+        std::vector<uint64_t> v;
+        v.reserve(groups.size());
+        for (uint64_t g : groups) v.push_back(g & mask);
+        std::sort(v.begin(), v.end());
+        const double n = static_cast<double>(std::unique(v.begin(), v.end()) - v.begin());
+        nv_cache[mask] = n;
+        return n;
+    }
+    // modelled seconds of one contraction step (the executor's GEMM modes)
+    double step(const TreeNode& x, const TreeNode& y) {
+        std::vector<int> sh;
+        std::set_intersection(x.labels.begin(), x.labels.end(), y.labels.begin(), y.labels.end(),
+                              std::back_inserter(sh));
+        const double la = std::ldexp(1.0, static_cast<int>(x.labels.size()));
+        const double lb = std::ldexp(1.0, static_cast<int>(y.labels.size()));
+        const double lz = std::ldexp(1.0, static_cast<int>(x.labels.size() + y.labels.size() - 2 * sh.size()));
+        const double un = std::ldexp(1.0, static_cast<int>(x.labels.size() + y.labels.size() - sh.size()));
+        const double va = nvar(x.mask), vb = nvar(y.mask), vz = nvar(x.mask | y.mask);
+        double mult, rd;
+        if (x.mask && y.mask) {  // gathered batch: one GEMM per result variant
+            mult = vz;
+            rd = vz * (la + lb);
+        } else {  // the varying operand's variants fold into M
+            mult = std::max(va, vb);
+            rd = va * la + vb * lb;
+        }
+        const double t = std::max(8.0 * un * mult / pf, 2.0 * elem * (rd + vz * lz) / bw) + 4e-6;
+        // level-0 steps run once per call, not per pass
+        return std::max(x.level, y.level) == 0 ? 0.01 * t : t;
+    }
+};
+
+void combine(std::vector<TreeNode>& t, int r) {
+    TreeNode& z = t[r];
+    const TreeNode &x = t[z.a], &y = t[z.b];
+    z.labels.clear();
+    std::set_symmetric_difference(x.labels.begin(), x.labels.end(), y.labels.begin(), y.labels.end(),
+                                  std::back_inserter(z.labels));
+    z.mask = x.mask | y.mask;
+    z.level = std::max(x.level, y.level);
+}
+
+// steps: (a, b, r) triples, rewritten in place; origin[i]: plan index of step i.
+// Returns the number of rotations applied.
+int reassociate(std::vector<TreeNode>& t, std::vector<int32_t>& steps, std::vector<int32_t>& origin,
+                TreeCost& cost, double max_elems) {
+    const int n_steps = static_cast<int>(steps.size() / 3);
+    std::vector<int> pos(t.size(), -1);  // node -> step producing it
+    auto reindex = [&] {
+        for (int i = 0; i < n_steps; ++i) pos[steps[3 * i + 2]] = i;
+    };
+    reindex();
+    int rotations = 0;
+    for (int round = 0; round < 64; ++round) {
+        bool improved = false;
+        for (int i = 0; i < n_steps; ++i) {
+            const int P = steps[3 * i + 2];
+            for (int zi = 0; zi < 2; ++zi) {
+                const int Z = zi == 0 ? t[P].a : t[P].b;
+                const int W = zi == 0 ? t[P].b : t[P].a;
+                if (pos[Z] < 0) continue;  // a leaf
+                const int X = t[Z].a, Y = t[Z].b;
+                const double base = cost.step(t[X], t[Y]) + cost.step(t[Z], t[W]);
+                double best = base * 0.999;
+                int bu = -1, bv = -1;
+                for (int o = 0; o < 2; ++o) {
+                    const int u = o == 0 ? X : Y, v = o == 0 ? Y : X;
+                    std::vector<int> sh;
+                    std::set_intersection(t[v].labels.begin(), t[v].labels.end(), t[W].labels.begin(),
+                                          t[W].labels.end(), std::back_inserter(sh));
+                    if (sh.empty() && !(t[v].mask && t[W].mask)) continue;
+                    TreeNode z2;
+                    z2.a = v;
+                    z2.b = W;
+                    std::set_symmetric_difference(t[v].labels.begin(), t[v].labels.end(), t[W].labels.begin(),
+                                                  t[W].labels.end(), std::back_inserter(z2.labels));
+                    z2.mask = t[v].mask | t[W].mask;
+                    z2.level = std::max(t[v].level, t[W].level);
+                    if (z2.labels.size() > static_cast<size_t>(kMaxRank) ||
+                        cost.nvar(z2.mask) * std::ldexp(1.0, static_cast<int>(z2.labels.size())) > max_elems)
+                        continue;
+                    const double c = cost.step(t[v], t[W]) + cost.step(t[u], z2);
+                    if (c < best) {
+                        best = c;
+                        bu = u;
+                        bv = v;
+                    }
+                }
+                if (bu < 0) continue;
+                // apply: Z = (bv, W) computed right before P; P = (bu, Z)
+                t[Z].a = bv;
+                t[Z].b = W;
+                combine(t, Z);
+                t[P].a = bu;
+                t[P].b = Z;
+                const int zs = pos[Z];
+                const int32_t zo = origin[zs];
+                steps.erase(steps.begin() + 3 * zs, steps.begin() + 3 * zs + 3);
+                origin.erase(origin.begin() + zs);
+                const int ps = pos[P] - 1;  // P's step moved up by one
+                const int32_t tri[3] = {bv, W, Z};
+                steps.insert(steps.begin() + 3 * ps, tri, tri + 3);
+                origin.insert(origin.begin() + ps, zo);
+                steps[3 * (ps + 1)] = bu;
+                steps[3 * (ps + 1) + 1] = Z;
+                reindex();
+                ++rotations;
+                improved = true;
+                break;
+            }
+        }
+        if (!improved) break;
+    }
+    return rotations;
+}
+
 }  // namespace
 
 Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
@@ -122,23 +264,21 @@ Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
     build_nodes(net, plan);
     build_steps();
     node_exp_.assign(nodes_.size(), 0);
-    if (precision == RCSG_PREC_F16) {  // keep the inputs for the calibration program
-        calib_net_ = net;
-        calib_plan_ = plan;
-        const int64_t amps = static_cast<int64_t>(leaf_data_.size()) / 2;
-        (void)amps;
-        c_rank_.assign(net.leaf_rank, net.leaf_rank + net.n_leaves);
-        int64_t nl = 0;
-        for (int i = 0; i < net.n_leaves; ++i) nl += net.leaf_rank[i];
-        c_labels_.assign(net.leaf_labels, net.leaf_labels + nl);
-        c_out_.assign(net.output_labels, net.output_labels + net.n_qubits);
-        c_openl_.assign(net.open_labels, net.open_labels + net.n_open);
-        c_openq_.assign(net.open_qubits, net.open_qubits + net.n_open);
-        c_steps_.assign(plan.steps, plan.steps + 3 * plan.n_steps);
-        c_sliced_.assign(plan.sliced, plan.sliced + plan.n_sliced);
-        c_broken_.assign(plan.broken, plan.broken + plan.n_broken);
-        c_fixed_.assign(plan.fixed_outputs, plan.fixed_outputs + plan.n_fixed);
-    }
+    // keep the inputs: the first run may reassociate the tree (retree) and the
+    // fp16 mode builds its calibration program from them
+    calib_net_ = net;
+    calib_plan_ = plan;
+    c_rank_.assign(net.leaf_rank, net.leaf_rank + net.n_leaves);
+    int64_t nl = 0;
+    for (int i = 0; i < net.n_leaves; ++i) nl += net.leaf_rank[i];
+    c_labels_.assign(net.leaf_labels, net.leaf_labels + nl);
+    c_out_.assign(net.output_labels, net.output_labels + net.n_qubits);
+    c_openl_.assign(net.open_labels, net.open_labels + net.n_open);
+    c_openq_.assign(net.open_qubits, net.open_qubits + net.n_open);
+    c_steps_.assign(plan.steps, plan.steps + 3 * plan.n_steps);
+    c_sliced_.assign(plan.sliced, plan.sliced + plan.n_sliced);
+    c_broken_.assign(plan.broken, plan.broken + plan.n_broken);
+    c_fixed_.assign(plan.fixed_outputs, plan.fixed_outputs + plan.n_fixed);
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     // leaf data + pass sources + canonical map
     CUDA_OK(cudaMalloc(&d_leaf_data_, std::max<size_t>(leaf_data_.size(), 2) * sizeof(double)));
@@ -223,7 +363,7 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
         nr.var_mask = na.var_mask | nb.var_mask;
         nr.level = std::max(na.level, nb.level);
         StepInfo st;
-        st.plan_index = s;
+        st.plan_index = step_origin_.empty() ? s : step_origin_[s];
         st.a = a;
         st.b = b;
         st.r = r;
@@ -626,6 +766,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     }
     const uint64_t flops = st.flops_per_variant * static_cast<uint64_t>(vr);
     exec_flops_ += flops;
+    if (profile_ && getenv("RCSG_DUMP_VARS") && flops > (1ull << 32))
+        fprintf(stderr, "[rcsg] step %d mode %d va %lld vb %lld vr %lld m %lld n %lld k %lld\n", st.plan_index, st.mode,
+                (long long)va, (long long)vb, (long long)vr, (long long)st.m, (long long)st.n, (long long)st.k);
     const int mk = mark_begin();
     if (gemm_smallk_supported(g)) {
         launch_gemm_smallk<R>(g, stream_);
@@ -739,18 +882,98 @@ void Program::exec_level(int level, const ChunkData* ch) {
 }
 
 void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
-                  uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats) {
+                  uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats, bool sync) {
     if (groups.empty()) throw Failure{RCSG_ERR_CONFIG, "group count must be >= 1"};
     if (slice_end <= slice_begin) throw Failure{RCSG_ERR_CONFIG, "empty slice range"};
     // (re)bind the program to this group list: chunk capacity, arena, chunk
     // index tables.  Repeated calls with the same groups (one call per slice
     // range) reuse everything.
+    if (!tree_fixed_) {
+        tree_fixed_ = true;
+        retree(groups);
+    }
     if (precision_ == RCSG_PREC_F16 && !calibrated_)
         calibrate(groups, configs.empty() ? 0 : configs[0], slice_begin);
     if (groups != bound_groups_) bind_groups(groups);
     const int64_t P = nodes_[root_].payload;
     const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
-    run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n);
+    run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n, sync || profile_);
+}
+
+void Program::sync() {
+    CUDA_OK(cudaStreamSynchronize(stream_));
+    if (!fault_pending_) return;
+    fault_pending_ = false;
+    int32_t fault = INT_MAX;
+    CUDA_OK(cudaMemcpy(&fault, d_fault_, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (fault != INT_MAX)
+        throw Failure{RCSG_ERR_NUMERIC, "non-finite intermediate at contraction step " + std::to_string(fault), fault};
+}
+
+rcsg_network_desc Program::stored_net() {
+    rcsg_network_desc net = calib_net_;
+    net.leaf_rank = c_rank_.data();
+    net.leaf_labels = c_labels_.data();
+    net.leaf_data = leaf_data_.data();
+    net.output_labels = c_out_.data();
+    net.open_labels = c_openl_.data();
+    net.open_qubits = c_openq_.data();
+    return net;
+}
+
+rcsg_plan_desc Program::stored_plan() {
+    rcsg_plan_desc plan = calib_plan_;
+    plan.steps = c_steps_.data();
+    plan.n_steps = static_cast<int32_t>(c_steps_.size() / 3);
+    plan.sliced = c_sliced_.data();
+    plan.broken = c_broken_.data();
+    plan.fixed_outputs = c_fixed_.data();
+    return plan;
+}
+
+// First run: reassociate the tree for this group batch (see reassociate()),
+// then rebuild the program from the rotated steps.  RCSG_TREE=plan keeps the
+// plan's tree as given.
+void Program::retree(const std::vector<uint64_t>& groups) {
+    const char* env = getenv("RCSG_TREE");
+    if (env && std::string(env) == "plan") return;
+    const int n_steps = static_cast<int>(c_steps_.size() / 3);
+    if (n_steps < 2) return;
+    std::vector<TreeNode> t(nodes_.size());
+    double max_elems = 1;
+    std::vector<uint64_t> uniq = groups;
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    const double pf = precision_ >= RCSG_PREC_BF16 ? 1.2e15 : (precision_ == RCSG_PREC_TF32 ? 6e14 : 5e13);
+    TreeCost cost{uniq, pf, 6e12, static_cast<double>(elem_bytes_), {}};
+    for (int i = 0; i < n_leaves_; ++i) {
+        t[i].labels = nodes_[i].labels;
+        std::sort(t[i].labels.begin(), t[i].labels.end());
+        t[i].mask = nodes_[i].var_mask;
+        t[i].level = nodes_[i].level;
+    }
+    for (int s = 0; s < n_steps; ++s) {
+        const int r = c_steps_[3 * s + 2];
+        t[r].a = c_steps_[3 * s];
+        t[r].b = c_steps_[3 * s + 1];
+        combine(t, r);
+        max_elems = std::max(max_elems, cost.nvar(t[r].mask) * std::ldexp(1.0, static_cast<int>(t[r].labels.size())));
+    }
+    std::vector<int32_t> steps = c_steps_;
+    std::vector<int32_t> origin(n_steps);
+    std::iota(origin.begin(), origin.end(), 0);
+    const int rot = reassociate(t, steps, origin, cost, max_elems);
+    if (getenv("RCSG_DUMP_TREE")) fprintf(stderr, "[rcsg] reassociation: %d rotations\n", rot);
+    if (!rot) return;
+    c_steps_ = steps;
+    step_origin_ = origin;
+    const rcsg_network_desc net = stored_net();
+    const rcsg_plan_desc plan = stored_plan();
+    build_nodes(net, plan);
+    build_steps();
+    node_exp_.assign(nodes_.size(), 0);
+    CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
 }
 
 // fp16 mode: per-tensor power-of-two scales.  A transient tf32 program runs one
@@ -761,24 +984,16 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
 // its fp32 result by 2^(e_a + e_b - e_r) before rounding to fp16; finalize
 // multiplies the root by 2^e_root.
 void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, uint64_t slice) {
-    rcsg_network_desc net = calib_net_;
-    net.leaf_rank = c_rank_.data();
-    net.leaf_labels = c_labels_.data();
-    net.leaf_data = leaf_data_.data();
-    net.output_labels = c_out_.data();
-    net.open_labels = c_openl_.data();
-    net.open_qubits = c_openq_.data();
-    rcsg_plan_desc plan = calib_plan_;
-    plan.steps = c_steps_.data();
-    plan.sliced = c_sliced_.data();
-    plan.broken = c_broken_.data();
-    plan.fixed_outputs = c_fixed_.data();
+    rcsg_network_desc net = stored_net();
+    rcsg_plan_desc plan = stored_plan();
     std::vector<uint64_t> sub(groups.begin(), groups.begin() + std::min<size_t>(groups.size(), 16));
     std::vector<float> mx(nodes_.size(), 0.f);
     {
         size_t fr = 0, tot = 0;
         CUDA_OK(cudaMemGetInfo(&fr, &tot));
         Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.4));
+        cal.tree_fixed_ = true;  // the steps are already this program's (reassociated) tree
+        cal.step_origin_ = step_origin_;
         CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
         CUDA_OK(cudaMemset(cal.d_max_, 0, nodes_.size() * sizeof(float)));
         cal.record_max_ = true;
@@ -811,6 +1026,7 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
 
 void Program::bind_groups(const std::vector<uint64_t>& groups) {
     bound_groups_.clear();
+    level0_valid_ = false;
     reset_graph();
     // chunk capacity: the largest group chunk whose arena fits the budget
     std::vector<uint64_t> uniq = groups;
@@ -928,7 +1144,8 @@ void Program::run_pass_body(int64_t P) {
 }
 
 void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
-                        uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n) {
+                        uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n,
+                        bool sync) {
     if (acc_n > acc_cap_) {
         cudaFree(d_part_);
         cudaFree(d_res_);
@@ -939,24 +1156,33 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
         CUDA_OK(cudaMalloc(&d_comp_, acc_n * sizeof(double)));
         acc_cap_ = acc_n;
     }
-    const int32_t no_fault = INT_MAX;
-    CUDA_OK(cudaMemcpyAsync(d_fault_, &no_fault, sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+    if (!fault_pending_) {  // the flag still holds an unchecked async run's fault otherwise
+        static const int32_t no_fault = INT_MAX;
+        CUDA_OK(cudaMemcpyAsync(d_fault_, &no_fault, sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+    }
     launch_fill(d_res_, 0.0, acc_n, stream_);
     launch_fill(d_comp_, 0.0, acc_n, stream_);
-    cudaEvent_t e0, e1;
-    CUDA_OK(cudaEventCreate(&e0));
-    CUDA_OK(cudaEventCreate(&e1));
-    CUDA_OK(cudaEventRecord(e0, stream_));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (sync) {
+        CUDA_OK(cudaEventCreate(&e0));
+        CUDA_OK(cudaEventCreate(&e1));
+        CUDA_OK(cudaEventRecord(e0, stream_));
+    }
     launches_ = 0;
     exec_flops_ = 0;
     uint64_t passes = 0;
     const std::vector<uint64_t> no_cfg{0};
     const std::vector<uint64_t>& cfgs = configs.empty() ? no_cfg : configs;
+    // level 0 depends on no slice, configuration or group: computed once per
+    // arena binding and kept (its results persist in the arena across calls)
+    if (!level0_valid_) {
+        launch_set_pass(d_state_, slice_begin, cfgs[0], stream_);
+        exec_level(0, nullptr);
+        level0_valid_ = true;
+    }
     for (size_t ci = 0; ci < cfgs.size(); ++ci) {
         launch_fill(d_part_, 0.0, acc_n, stream_);
         ++launches_;
-        launch_set_pass(d_state_, slice_begin, cfgs[ci], stream_);
-        exec_level(0, nullptr);
         for (uint64_t s = slice_begin; s < slice_end; ++s) {
             launch_set_pass(d_state_, s, cfgs[ci], stream_);
             ++launches_;
@@ -970,18 +1196,18 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     launch_fill(d_comp_, 0.0, acc_n, stream_);
     launch_kahan(d_acc, d_comp_, d_res_, acc_n, stream_);
     launches_ += 2;
-    CUDA_OK(cudaEventRecord(e1, stream_));
-    CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaEventSynchronize(e1));
     float ms = 0;
-    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    collect_marks(stats);
-    int32_t fault = INT_MAX;
-    CUDA_OK(cudaMemcpy(&fault, d_fault_, sizeof(int32_t), cudaMemcpyDeviceToHost));
-    if (fault != INT_MAX)
-        throw Failure{RCSG_ERR_NUMERIC, "non-finite intermediate at contraction step " + std::to_string(fault), fault};
+    CUDA_OK(cudaGetLastError());
+    if (sync) {
+        CUDA_OK(cudaEventRecord(e1, stream_));
+        CUDA_OK(cudaEventSynchronize(e1));
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        collect_marks(stats);
+    }
+    fault_pending_ = true;
+    if (sync) this->sync();
     if (stats) {
         stats->plan_flops += plan_flops_ * static_cast<uint64_t>(n_groups) * cfgs.size() * (slice_end - slice_begin);
         stats->executed_flops += exec_flops_;

@@ -105,8 +105,12 @@ class Program {
     // groups: code per group (bits at var_bit positions).  configs empty ->
     // one pass per slice with config bits 0.  d_acc: device double
     // [n_groups][2^out_rank] interleaved; accumulates (+=) the result.
+    // sync == false: return once the work is enqueued on stream(); a
+    // non-finite intermediate is then reported by the next synchronous call
+    // or by sync().
     void run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
-             uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats);
+             uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats, bool sync = true);
+    void sync();
 
     int out_rank() const { return out_rank_; }
     void set_profile(bool on) { profile_ = on; }
@@ -116,6 +120,9 @@ class Program {
 
   private:
     void build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan);
+    void retree(const std::vector<uint64_t>& groups);
+    rcsg_network_desc stored_net();
+    rcsg_plan_desc stored_plan();
     void build_steps();
     int64_t plan_arena(int64_t chunk_cap, bool assign);
     void prepare_chunks(const std::vector<uint64_t>& groups, int64_t chunk_cap);
@@ -125,7 +132,7 @@ class Program {
     void run_pass_body(int64_t P);
     void reset_graph();
     void run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
-                   uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n);
+                   uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n, bool sync);
     void free_chunks();
     void exec_level(int level, const ChunkData* ch);
     void exec_step(const StepInfo& s, const ChunkData* ch);
@@ -165,12 +172,18 @@ class Program {
     int64_t acc_cap_ = 0;
     std::vector<ChunkData> chunks_;
     std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
-    // fp16 mode: per-node storage exponents (value stored times 2^-e) and the
-    // inputs kept to build the calibration program
+    // batch-aware reassociation: done once, at the first run (group codes known)
+    bool tree_fixed_ = false;
+    bool level0_valid_ = false;  // level-0 (constant) results live in the arena
+    bool fault_pending_ = false; // async runs whose fault flag is not checked yet
+    std::vector<int32_t> step_origin_;  // program step -> index of the plan step it came from
+    // fp16 mode: per-node storage exponents (value stored times 2^-e)
     std::vector<int> node_exp_;
     bool calibrated_ = false;
     bool record_max_ = false;
     float* d_max_ = nullptr;
+    // copies of the compile inputs (re-tree and the fp16 calibration program);
+    // c_steps_ holds the steps actually executed (after reassociation)
     rcsg_network_desc calib_net_{};
     rcsg_plan_desc calib_plan_{};
     std::vector<int32_t> c_rank_, c_labels_, c_out_, c_openl_, c_openq_, c_steps_, c_sliced_, c_broken_, c_fixed_;

@@ -306,7 +306,7 @@ int rcsh_contract_groups(void* hp, int precision, std::uint64_t budget, std::uin
 
 int rcsh_contract_groups_device(void* hp, int precision, std::uint64_t budget, std::uint64_t n_groups,
                                 const std::uint64_t* fixed, int n_cfg, const std::uint64_t* cfgs,
-                                std::uint64_t s0, std::uint64_t s1, double* d_acc, rcsg_stats* st) {
+                                std::uint64_t s0, std::uint64_t s1, double* d_acc, rcsg_stats* st, int sync) {
     return guarded([&] {
         Handle* h = static_cast<Handle*>(hp);
         rcsg_program* p = h->program(precision, budget);
@@ -316,7 +316,15 @@ int rcsh_contract_groups_device(void* hp, int precision, std::uint64_t budget, s
             c = h->config.configurations.data();
             nc = h->has_config ? h->config.configurations.size() : 0;
         }
-        if (int rc = rcsg_contract_groups_device(p, n_groups, fixed, nc, c, s0, s1, d_acc, 1, st)) raise_rcsg(rc);
+        if (int rc = rcsg_contract_groups_device(p, n_groups, fixed, nc, c, s0, s1, d_acc, sync, st)) raise_rcsg(rc);
+    });
+}
+
+// wait for a program's stream and report a deferred NumericFault
+int rcsh_program_sync(void* hp, int precision, std::uint64_t budget) {
+    return guarded([&] {
+        Handle* h = static_cast<Handle*>(hp);
+        if (int rc = rcsg_program_sync(h->program(precision, budget))) raise_rcsg(rc);
     });
 }
 
