@@ -45,7 +45,7 @@ UNIT = "slice-contractions/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=256)  # all 2^8 slices of cfg2
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--groups", type=int, default=64)
     ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "bf16", "f32", "f64"])
@@ -86,7 +86,7 @@ class Clocks:
                 ["nvidia-smi", f"--id={index}",
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "40"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -117,18 +117,25 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_sample(threads: int):
+_REF_PROBLEM = []
+
+
+def cpu_reference_sample(threads: int, n_pairs: int | None = None, first: int = 0):
     """The reference executor (oracle/_ref, unmodified reference sources) on the
-    host cores: execute_assignment on `threads` distinct (group, slice) pairs of
-    the same circuit planned with a tighter budget (2^27 B -> 15 sliced labels,
-    ~1e10 FLOP per pair) so one sample takes seconds; returns measured FLOP/s."""
+    host cores: execute_assignment on `n_pairs` (default `threads`) distinct
+    (group, slice) pairs, spread over `threads` threads, of the same circuit
+    planned with a tighter budget (2^27 B -> 15 sliced labels, ~1e10 FLOP per
+    pair) so one pair takes seconds; returns measured FLOP/s."""
     from oracle import ref  # CPU baseline leg only
-    p = ref.RefProblem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"], CFG2["open"], 1 << 27,
-                       "low").build()
+    if not _REF_PROBLEM:
+        _REF_PROBLEM.append(ref.RefProblem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"],
+                                           CFG2["open"], 1 << 27, "low").build())
+    p = _REF_PROBLEM[0]
     fixed = ref.candidates(30, CFG2["open"], 1, ref.split_next(1, 0xCA11D))[0][0]
-    slices = list(range(threads))
+    n_pairs = n_pairs or threads
+    slices = [(first + i) % (1 << len(p.plan["sliced"])) for i in range(n_pairs)]
     _, secs = p.slices_mt(int(fixed), slices, threads)
-    flops = threads * p.plan["flops_per_slice"]
+    flops = n_pairs * p.plan["flops_per_slice"]
     return flops / secs, secs, p.plan["flops_per_slice"], len(p.plan["sliced"])
 
 
@@ -140,12 +147,10 @@ def run_reference(args, rank, world):
     p = pb.Problem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"], CFG2["open"], CFG2["budget"],
                    CFG2["effort"]).build()
     fps = p.plan["flops_per_slice"]
-    vals = []
-    for i in range(args.warmup + args.steps):
-        rate, secs, f_sample, _ = cpu_reference_sample(threads)
-        if i >= args.warmup:
-            vals.append(rate)
-    rate = sum(vals) / len(vals)
+    # one step = one (group, slice) pair of the reference executor; the W warm-up
+    # pairs and then the K timed pairs each run spread over all host threads
+    cpu_reference_sample(threads, max(args.warmup, 1), 0)
+    rate, secs, f_sample, _ = cpu_reference_sample(threads, args.steps, args.warmup)
     pairs_per_s = rate / fps
     value = pairs_per_s / args.groups
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -153,8 +158,8 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
             "config": {"workload": WORKLOAD, "groups_per_slice": args.groups},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"reference execute_assignment on {threads} (group, slice) pairs in "
-                                       f"parallel, same circuit planned at budget 2^27 B "
+                             "sample": f"reference execute_assignment on {args.steps} (group, slice) pairs over "
+                                       f"{threads} threads in {secs:.1f} s, same circuit planned at budget 2^27 B "
                                        f"({f_sample:.3e} FLOP/pair); measured {rate / 1e9:.2f} GFLOP/s "
                                        f"extrapolated to the bench plan ({fps:.3e} FLOP/pair) x {args.groups} groups"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

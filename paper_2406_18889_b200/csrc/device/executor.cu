@@ -969,8 +969,10 @@ void Program::retree(const std::vector<uint64_t>& groups) {
     step_origin_ = origin;
     const rcsg_network_desc net = stored_net();
     const rcsg_plan_desc plan = stored_plan();
+    const uint64_t plan_flops = plan_flops_;  // stats report the plan's (reference-equivalent) FLOPs
     build_nodes(net, plan);
     build_steps();
+    plan_flops_ = plan_flops;
     node_exp_.assign(nodes_.size(), 0);
     CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice));

@@ -202,3 +202,48 @@ def test_scheduler_blocks_on_gpu_equal_single_call():
     full = p.contract_groups(fixed, precision="f64", configs=None)
     got = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "f64"), p.n_slices)
     assert rel(got, full) < 1e-12
+
+
+# ---- batch-aware reassociation, level-0 caching, async calls ------------------
+def test_reassociated_tree_matches_plan_tree(monkeypatch):
+    """The executor reassociates the plan's tree for the group batch (rotations
+    that keep every node's subtree); amplitudes equal the plan-tree execution
+    to rounding, and the executed FLOPs drop."""
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low")
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), 8, pb.split_next(1, 0xCA11D))
+    from paper_2406_18889_b200._native import rcsg_stats
+    st_r, st_p = rcsg_stats(), rcsg_stats()
+    got = pb.Problem(*spec).build().contract_groups(fixed, precision="f64", configs=None, slices=(5, 6), stats=st_r)
+    monkeypatch.setenv("RCSG_TREE", "plan")
+    want = pb.Problem(*spec).build().contract_groups(fixed, precision="f64", configs=None, slices=(5, 6),
+                                                     stats=st_p)
+    for g in range(len(fixed)):
+        assert rel(got[g], want[g]) < 1e-12, g
+    assert st_r.executed_flops * 4 < st_p.executed_flops, (st_r.executed_flops, st_p.executed_flops)
+    assert st_r.plan_flops == st_p.plan_flops  # reference-equivalent work is the plan's
+
+
+def test_level0_cache_across_calls_and_async():
+    """Level-0 results are computed once and reused by later calls; async calls
+    accumulate the same sums as synchronous ones."""
+    import torch
+    p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
+    fixed = np.array([0, 5, 22, 63], np.uint64)
+    full = p.contract_groups(fixed, precision="f64", configs=None)
+    acc = torch.zeros(len(fixed) * 16 * 2, dtype=torch.float64, device="cuda")
+    for s in range(p.n_slices):
+        p.contract_groups_device(fixed, acc.data_ptr(), precision="f64", configs=None, slices=(s, s + 1),
+                                 sync=False)
+    p.sync("f64")
+    got = acc.cpu().numpy().view(np.complex128).reshape(len(fixed), -1)
+    assert rel(got, full) < 1e-12
+
+
+def test_async_numeric_fault_is_deferred_to_sync():
+    import torch
+    inf = float("inf")
+    p = pb.Problem.from_network([2, 1], [0, 1, 1], [inf, 0, 0, 1, 1, 1], ["a", "b"], 1, [0], [0], [0])
+    acc = torch.zeros(4, dtype=torch.float64, device="cuda")
+    p.contract_groups_device([0], acc.data_ptr(), precision="f64", configs=None, sync=False)
+    with pytest.raises(pb.NumericFault):
+        p.sync("f64")
