@@ -280,6 +280,7 @@ Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
     c_broken_.assign(plan.broken, plan.broken + plan.n_broken);
     c_fixed_.assign(plan.fixed_outputs, plan.fixed_outputs + plan.n_fixed);
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    ls_ = stream_;
     // leaf data + pass sources + canonical map
     CUDA_OK(cudaMalloc(&d_leaf_data_, std::max<size_t>(leaf_data_.size(), 2) * sizeof(double)));
     CUDA_OK(cudaMemcpy(d_leaf_data_, leaf_data_.data(), leaf_data_.size() * sizeof(double),
@@ -310,6 +311,9 @@ Program::~Program() {
     for (auto* p : d_static_jobs_) cudaFree(p);
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    free_tasks();
+    for (cudaEvent_t e : lane_ev_) cudaEventDestroy(e);
+    for (cudaStream_t l : lanes_) cudaStreamDestroy(l);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -341,6 +345,7 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
             else nd.var_mask |= uint64_t{1} << rl.var_bit;
         }
         nd.level = nd.var_mask ? 2 : (pass ? 1 : 0);
+        nd.pass_dep = pass;
         nd.payload = int64_t{1} << nd.labels.size();
         lo += nd.rank0;
         doff += int64_t{1} << nd.rank0;
@@ -362,12 +367,14 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
         NodeInfo& nr = nodes_[r];
         nr.var_mask = na.var_mask | nb.var_mask;
         nr.level = std::max(na.level, nb.level);
+        nr.pass_dep = na.pass_dep || nb.pass_dep;
         StepInfo st;
         st.plan_index = step_origin_.empty() ? s : step_origin_[s];
         st.a = a;
         st.b = b;
         st.r = r;
         st.level = nr.level;
+        st.phase = nr.level < 2 ? nr.level : (nr.pass_dep ? 2 : 3);
         nodes_[a].consumer = s;
         nodes_[b].consumer = s;
         steps_.push_back(st);
@@ -580,10 +587,15 @@ int64_t Program::plan_arena(int64_t cap, bool assign) {
     };
     // leaves: persistent
     for (int i = 0; i < n_leaves_; ++i) place(i);
+    // phases in execution order: constant (0), group-only (3; cached when the
+    // groups fit one chunk), per pass (1), per pass and group (2).  Results
+    // consumed by a later phase persist; per-pass results read by phase 2
+    // persist until the pass ends.
+    auto phase_of = [&](const NodeInfo& nd) { return nd.level < 2 ? nd.level : (nd.pass_dep ? 2 : 3); };
     std::vector<int> persist_until_pass_end;
-    for (int level = 0; level <= 2; ++level) {
+    for (int ph : {0, 3, 1, 2}) {
         for (StepInfo& st : steps_) {
-            if (st.level != level) continue;
+            if (st.phase != ph) continue;
             const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b];
             if (st.perm_a) {
                 st.sa_plane = align_up(var_cap(A) * A.payload);
@@ -599,14 +611,14 @@ int64_t Program::plan_arena(int64_t cap, bool assign) {
             for (int op : {st.a, st.b}) {
                 NodeInfo& o = nodes_[op];
                 if (o.is_leaf) continue;
-                if (o.level == level) ff.release(o.off, 2 * o.plane);
-                else if (o.level == 1 && level == 2) persist_until_pass_end.push_back(op);
-                // level-0 operands of deeper steps persist for the whole run
+                if (phase_of(o) == ph) ff.release(o.off, 2 * o.plane);
+                else if (phase_of(o) == 1 && ph == 2) persist_until_pass_end.push_back(op);
+                // constant and group-only operands of later phases persist for the run
             }
         }
-        if (level == 2) {
+        if (ph == 2) {
             // the root is read by the finalize of every chunk
-            if (nodes_[root_].level == 2 && !nodes_[root_].is_leaf)
+            if (phase_of(nodes_[root_]) == 2 && !nodes_[root_].is_leaf)
                 ff.release(nodes_[root_].off, 2 * nodes_[root_].plane);
             for (int id : persist_until_pass_end) ff.release(nodes_[id].off, 2 * nodes_[id].plane);
         }
@@ -671,11 +683,15 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
                 ch.groups.push_back(g);
                 ch.vid.push_back(nodes_[root_].level == 2 ? find_code(root_, uniq[u] & nodes_[root_].var_mask) : 0);
             }
-        // level-2 leaf jobs of this chunk
+        // level-2 leaf jobs of this chunk: group-only leaves, then pass-dependent ones
         std::vector<LeafJob> jobs;
-        for (int i = 0; i < n_leaves_; ++i) {
+        std::vector<int> leaf_order;
+        for (int want_pass = 0; want_pass < 2; ++want_pass)
+            for (int i = 0; i < n_leaves_; ++i)
+                if (nodes_[i].level == 2 && nodes_[i].pass_dep == (want_pass == 1)) leaf_order.push_back(i);
+        for (int i : leaf_order) {
             const NodeInfo& nd = nodes_[i];
-            if (nd.level != 2) continue;
+            if (!nd.pass_dep) ++ch.n_leaf_jobs3;
             LeafJob j{};
             j.out_off = nd.off;
             j.out_plane = nd.plane;
@@ -722,7 +738,7 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     if (st.perm_a) {
         R* dst = static_cast<R*>(buf(st.sa_off));
         const int mk = mark_begin();
-        launch_permute<R>(a_ptr, A.plane, dst, st.sa_plane, va, st.pa, stream_);
+        launch_permute<R>(a_ptr, A.plane, dst, st.sa_plane, va, st.pa, ls_);
         mark_end(mk, kCatPermute, 4ull * sizeof(R) * va * A.payload, st.plan_index, va, A.payload, 0, 0);
         ++launches_;
         a_ptr = dst;
@@ -733,7 +749,7 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     if (st.perm_b) {
         R* dst = static_cast<R*>(buf(st.sb_off));
         const int mk = mark_begin();
-        launch_permute<R>(b_ptr, B.plane, dst, st.sb_plane, vb, st.pb, stream_);
+        launch_permute<R>(b_ptr, B.plane, dst, st.sb_plane, vb, st.pb, ls_);
         mark_end(mk, kCatPermute, 4ull * sizeof(R) * vb * B.payload, st.plan_index, vb, B.payload, 0, 0);
         ++launches_;
         b_ptr = dst;
@@ -771,13 +787,13 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
                 (long long)va, (long long)vb, (long long)vr, (long long)st.m, (long long)st.n, (long long)st.k);
     const int mk = mark_begin();
     if (gemm_smallk_supported(g)) {
-        launch_gemm_smallk<R>(g, stream_);
+        launch_gemm_smallk<R>(g, ls_);
         mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
         ++launches_;
         return;
     }
     if (gemv_supported(g)) {
-        launch_gemv<R>(g, stream_);
+        launch_gemv<R>(g, ls_);
         mark_end(mk, kCatGemv, flops, st.plan_index, g.m, g.n, g.k, g.batch);
         ++launches_;
         return;
@@ -785,13 +801,13 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     if constexpr (!std::is_same_v<R, double>) {
         // 3xTF32 stays on the fp32 SIMT kernel until its split-operand tensor-core path lands
         if ((precision_ == RCSG_PREC_TF32 || precision_ >= RCSG_PREC_BF16) && gemm_tc_supported(g)) {
-            launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : (precision_ == RCSG_PREC_F16 ? 2 : 0), stream_);
+            launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : (precision_ == RCSG_PREC_F16 ? 2 : 0), ls_);
             mark_end(mk, kCatGemmTc, flops, st.plan_index, g.m, g.n, g.k, g.batch);
             ++launches_;
             return;
         }
     }
-    launch_gemm_simt<R>(g, stream_);
+    launch_gemm_simt<R>(g, ls_);
     mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
     ++launches_;
 }
@@ -807,7 +823,7 @@ int Program::mark_begin() {
         ev_pool_.push_back(b);
     }
     marks_.push_back({-1, 0, -1, 0, 0, 0, 0});
-    CUDA_OK(cudaEventRecord(ev_pool_[2 * i], stream_));
+    CUDA_OK(cudaEventRecord(ev_pool_[2 * i], ls_));
     return static_cast<int>(i);
 }
 
@@ -815,7 +831,7 @@ void Program::mark_end(int idx, int cat, uint64_t work, int step, int64_t m, int
                        int64_t batch) {
     if (idx < 0) return;
     marks_[idx] = {cat, work, step, m, n, k, batch};
-    CUDA_OK(cudaEventRecord(ev_pool_[2 * idx + 1], stream_));
+    CUDA_OK(cudaEventRecord(ev_pool_[2 * idx + 1], ls_));
 }
 
 void Program::collect_marks(rcsg_stats* stats) {
@@ -858,27 +874,31 @@ void Program::exec_step(const StepInfo& st, const ChunkData* ch) {
     if (record_max_) {  // calibration: max |value| of the step's output
         const NodeInfo& R = nodes_[st.r];
         const int64_t vr = (R.level == 2 && ch) ? ch->nvar[st.r] : 1;
-        launch_maxabs(static_cast<const float*>(buf(R.off)), R.plane, vr * R.payload, d_max_ + st.r, stream_);
+        launch_maxabs(static_cast<const float*>(buf(R.off)), R.plane, vr * R.payload, d_max_ + st.r, ls_);
     }
 }
 
-void Program::exec_level(int level, const ChunkData* ch) {
-    // leaves of this level
-    if (level < 2) {
-        if (!static_jobs_[level].empty()) {
-            RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[level],
-                                                            static_cast<int>(static_jobs_[level].size()),
+void Program::exec_phase(int phase, const ChunkData* ch) {
+    // leaves of this phase
+    if (phase < 2) {
+        if (!static_jobs_[phase].empty()) {
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[phase],
+                                                            static_cast<int>(static_jobs_[phase].size()),
                                                             d_leaf_data_, nullptr, d_pass_src_, d_state_,
-                                                            static_cast<S*>(arena_), stream_));
+                                                            static_cast<S*>(arena_), ls_));
             ++launches_;
         }
-    } else if (ch->n_leaf_jobs) {
-        RCSG_DISPATCH(precision_, launch_leaf_project<S>(ch->d_leaf_jobs, ch->n_leaf_jobs, d_leaf_data_, ch->d_codes,
-                                                        d_pass_src_, d_state_, static_cast<S*>(arena_), stream_));
-        ++launches_;
+    } else {
+        const int j0 = phase == 3 ? 0 : ch->n_leaf_jobs3;
+        const int j1 = phase == 3 ? ch->n_leaf_jobs3 : ch->n_leaf_jobs;
+        if (j1 > j0) {
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(ch->d_leaf_jobs + j0, j1 - j0, d_leaf_data_, ch->d_codes,
+                                                            d_pass_src_, d_state_, static_cast<S*>(arena_), ls_));
+            ++launches_;
+        }
     }
     for (const StepInfo& st : steps_)
-        if (st.level == level) exec_step(st, ch);
+        if (st.phase == phase) exec_step(st, ch);
 }
 
 void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
@@ -1029,6 +1049,7 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
 void Program::bind_groups(const std::vector<uint64_t>& groups) {
     bound_groups_.clear();
     level0_valid_ = false;
+    phase3_valid_ = false;
     reset_graph();
     // chunk capacity: the largest group chunk whose arena fits the budget
     std::vector<uint64_t> uniq = groups;
@@ -1088,6 +1109,7 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
                            static_jobs_[level].size() * sizeof(LeafJob), cudaMemcpyHostToDevice));
     }
     prepare_chunks(groups, cap);
+    build_tasks();
     chunk_cap_ = cap;
     bound_groups_ = groups;
 }
@@ -1097,16 +1119,193 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
 // the first pass has sized the workspaces (every pass launches the same
 // kernels; the slice / configuration bits are read from device memory).
 void Program::exec_pass_body(int64_t P) {
-    exec_level(1, nullptr);
+    exec_phase(1, nullptr);
     for (const ChunkData& ch : chunks_) {
-        exec_level(2, &ch);
+        if (chunks_.size() > 1) exec_phase(3, &ch);  // one chunk: cached outside the pass
+        exec_phase(2, &ch);
         const NodeInfo& root = nodes_[root_];
         RCSG_DISPATCH(precision_,
                       launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane,
                                          std::ldexp(1.0, node_exp_[root_]), P,
                                          static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
-                                         static_cast<int64_t>(ch.groups.size()), d_part_, stream_));
+                                         static_cast<int64_t>(ch.groups.size()), d_part_, ls_));
         ++launches_;
+    }
+}
+
+void Program::free_tasks() {
+    for (cudaEvent_t e : task_ev_) cudaEventDestroy(e);
+    task_ev_.clear();
+    tasks_.clear();
+    task_wait_.clear();
+    task_lane_.clear();
+}
+
+// The pass body as tasks in program order, each with the arena regions it
+// reads and writes; task u must precede t when t writes memory u reads or
+// writes, or reads memory u writes.  Tasks go to kLanes streams (a dependency
+// chain stays on one lane); t waits only for the latest dependency per other
+// lane.  Same-lane order also serialises the per-stream split-K workspace.
+void Program::build_tasks() {
+    free_tasks();
+    constexpr int kLanes = 8;
+    using Region = std::pair<int64_t, int64_t>;
+    std::vector<std::vector<Region>> rd, wr;
+    auto node_region = [&](int id) { return Region{nodes_[id].off, nodes_[id].off + 2 * nodes_[id].plane}; };
+    auto add = [&](Task t, std::vector<Region> r, std::vector<Region> w) {
+        tasks_.push_back(t);
+        rd.push_back(std::move(r));
+        wr.push_back(std::move(w));
+    };
+    auto leaf_regions = [&](int phase) {
+        std::vector<Region> w;
+        for (int i = 0; i < n_leaves_; ++i) {
+            const NodeInfo& nd = nodes_[i];
+            if ((nd.level < 2 ? nd.level : (nd.pass_dep ? 2 : 3)) == phase) w.push_back(node_region(i));
+        }
+        return w;
+    };
+    auto add_steps = [&](int phase, const ChunkData* ch) {
+        for (const StepInfo& st : steps_) {
+            if (st.phase != phase) continue;
+            std::vector<Region> r{node_region(st.a), node_region(st.b)}, w{node_region(st.r)};
+            if (st.perm_a) w.push_back({st.sa_off, st.sa_off + 2 * st.sa_plane});
+            if (st.perm_b) w.push_back({st.sb_off, st.sb_off + 2 * st.sb_plane});
+            add({1, &st, ch}, r, w);
+        }
+    };
+    const Region part{-2, -1};  // the per-configuration accumulator
+    if (!static_jobs_[1].empty()) add({0, nullptr, nullptr}, {}, leaf_regions(1));
+    add_steps(1, nullptr);
+    for (const ChunkData& ch : chunks_) {
+        if (chunks_.size() > 1) {  // one chunk: phase 3 is cached outside the pass
+            if (ch.n_leaf_jobs3) add({4, nullptr, &ch}, {}, leaf_regions(3));
+            add_steps(3, &ch);
+        }
+        if (ch.n_leaf_jobs > ch.n_leaf_jobs3) add({2, nullptr, &ch}, {}, leaf_regions(2));
+        add_steps(2, &ch);
+        add({3, nullptr, &ch}, {node_region(root_)}, {part});
+    }
+    const int T = static_cast<int>(tasks_.size());
+    auto overlap = [](const std::vector<Region>& x, const std::vector<Region>& y) {
+        for (const Region& a : x)
+            for (const Region& b : y)
+                if (a.first < b.second && b.first < a.second) return true;
+        return false;
+    };
+    std::vector<int> tail(kLanes, -1);
+    task_lane_.assign(T, 0);
+    task_wait_.assign(T, {});
+    n_lanes_used_ = 1;
+    for (int t = 0; t < T; ++t) {
+        std::vector<int> deps;
+        for (int u = 0; u < t; ++u)
+            if (overlap(wr[t], rd[u]) || overlap(wr[t], wr[u]) || overlap(rd[t], wr[u])) deps.push_back(u);
+        int lane = -1;
+        for (auto it = deps.rbegin(); it != deps.rend() && lane < 0; ++it)
+            for (int l = 0; l < kLanes; ++l)
+                if (tail[l] == *it) lane = l;
+        if (lane < 0) {  // the least recently used lane
+            lane = 0;
+            for (int l = 1; l < kLanes; ++l)
+                if (tail[l] < tail[lane]) lane = l;
+        }
+        task_lane_[t] = lane;
+        tail[lane] = t;
+        n_lanes_used_ = std::max(n_lanes_used_, lane + 1);
+        std::vector<int> last(kLanes, -1);
+        for (int u : deps)
+            if (task_lane_[u] != lane) last[task_lane_[u]] = std::max(last[task_lane_[u]], u);
+        for (int l = 0; l < kLanes; ++l)
+            if (last[l] >= 0) task_wait_[t].push_back(last[l]);
+    }
+    if (getenv("RCSG_DUMP_TREE")) {  // longest dependency chain, in tasks
+        std::vector<int> depth(T, 1);
+        int longest = 0;
+        for (int t = 0; t < T; ++t) {
+            for (int u = 0; u < t; ++u)
+                if (overlap(wr[t], rd[u]) || overlap(wr[t], wr[u]) || overlap(rd[t], wr[u]))
+                    depth[t] = std::max(depth[t], depth[u] + 1);
+            longest = std::max(longest, depth[t]);
+        }
+        fprintf(stderr, "[rcsg] pass DAG: %d tasks on %d lanes, longest chain %d\n", T, n_lanes_used_, longest);
+        for (int t = 0; t < T; ++t) {
+            const Task& k = tasks_[t];
+            if (k.kind != 1) {
+                fprintf(stderr, "  task %3d kind %d depth %d\n", t, k.kind, depth[t]);
+                continue;
+            }
+            const StepInfo& st = *k.st;
+            auto nv = [&](int id) -> long long {
+                return (nodes_[id].level == 2 && k.ch) ? (long long)k.ch->nvar[id] : 1LL;
+            };
+            fprintf(stderr, "  task %3d step %4d L%d mode %d m %lld n %lld k %lld va %lld vb %lld vr %lld macs %.3g depth %d\n",
+                    t, st.plan_index, st.level, st.mode, (long long)st.m, (long long)st.n, (long long)st.k,
+                    nv(st.a), nv(st.b), nv(st.r), (double)st.m * st.n * st.k * (st.mode == 1 ? nv(st.a) : nv(st.r)),
+                    depth[t]);
+        }
+    }
+    task_ev_.resize(T);
+    for (int t = 0; t < T; ++t) CUDA_OK(cudaEventCreateWithFlags(&task_ev_[t], cudaEventDisableTiming));
+    while (static_cast<int>(lanes_.size()) < n_lanes_used_) {
+        cudaStream_t l;
+        CUDA_OK(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+        lanes_.push_back(l);
+    }
+    while (static_cast<int>(lane_ev_.size()) < n_lanes_used_ + 1) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        lane_ev_.push_back(e);
+    }
+}
+
+void Program::run_task(const Task& t, int64_t P) {
+    switch (t.kind) {
+        case 0:
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[1], static_cast<int>(static_jobs_[1].size()),
+                                                            d_leaf_data_, nullptr, d_pass_src_, d_state_,
+                                                            static_cast<S*>(arena_), ls_));
+            ++launches_;
+            break;
+        case 1:
+            exec_step(*t.st, t.ch);
+            break;
+        case 2:
+        case 4: {
+            const int j0 = t.kind == 4 ? 0 : t.ch->n_leaf_jobs3;
+            const int j1 = t.kind == 4 ? t.ch->n_leaf_jobs3 : t.ch->n_leaf_jobs;
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(t.ch->d_leaf_jobs + j0, j1 - j0, d_leaf_data_,
+                                                            t.ch->d_codes, d_pass_src_, d_state_,
+                                                            static_cast<S*>(arena_), ls_));
+            ++launches_;
+            break;
+        }
+        default: {
+            const NodeInfo& root = nodes_[root_];
+            RCSG_DISPATCH(precision_,
+                          launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane,
+                                             std::ldexp(1.0, node_exp_[root_]), P,
+                                             static_cast<int>(root.labels.size()), d_canon_, t.ch->d_vid,
+                                             t.ch->d_groups, static_cast<int64_t>(t.ch->groups.size()), d_part_, ls_));
+            ++launches_;
+        }
+    }
+}
+
+// fork from stream_, run the tasks on their lanes, join back into stream_
+void Program::exec_pass_dag(int64_t P) {
+    CUDA_OK(cudaEventRecord(lane_ev_[0], stream_));
+    for (int l = 0; l < n_lanes_used_; ++l) CUDA_OK(cudaStreamWaitEvent(lanes_[l], lane_ev_[0], 0));
+    for (size_t t = 0; t < tasks_.size(); ++t) {
+        ls_ = lanes_[task_lane_[t]];
+        for (int u : task_wait_[t]) CUDA_OK(cudaStreamWaitEvent(ls_, task_ev_[u], 0));
+        run_task(tasks_[t], P);
+        CUDA_OK(cudaEventRecord(task_ev_[t], ls_));
+    }
+    ls_ = stream_;
+    for (int l = 0; l < n_lanes_used_; ++l) {
+        CUDA_OK(cudaEventRecord(lane_ev_[l + 1], lanes_[l]));
+        CUDA_OK(cudaStreamWaitEvent(stream_, lane_ev_[l + 1], 0));
     }
 }
 
@@ -1122,8 +1321,10 @@ void Program::run_pass_body(int64_t P) {
         exec_pass_body(P);
         return;
     }
-    if (!graph_exec_ && !graph_warm_) {  // first pass: eager, sizes split-K workspaces
-        exec_pass_body(P);
+    static const bool no_dag = getenv("RCSG_NO_DAG") != nullptr;
+    if (!graph_exec_ && !graph_warm_) {  // first pass: eager, sizes the lanes' split-K workspaces
+        if (no_dag) exec_pass_body(P);
+        else exec_pass_dag(P);
         graph_warm_ = true;
         return;
     }
@@ -1131,7 +1332,8 @@ void Program::run_pass_body(int64_t P) {
         const uint64_t before = launches_, flops_before = exec_flops_;
         cudaGraph_t graph;
         CUDA_OK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-        exec_pass_body(P);
+        if (no_dag) exec_pass_body(P);
+        else exec_pass_dag(P);
         CUDA_OK(cudaStreamEndCapture(stream_, &graph));
         CUDA_OK(cudaGraphInstantiate(&graph_exec_, graph, 0));
         cudaGraphDestroy(graph);
@@ -1179,8 +1381,12 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     // arena binding and kept (its results persist in the arena across calls)
     if (!level0_valid_) {
         launch_set_pass(d_state_, slice_begin, cfgs[0], stream_);
-        exec_level(0, nullptr);
+        exec_phase(0, nullptr);
         level0_valid_ = true;
+    }
+    if (!phase3_valid_ && chunks_.size() == 1) {  // group-only results of the single chunk
+        exec_phase(3, &chunks_[0]);
+        phase3_valid_ = true;
     }
     for (size_t ci = 0; ci < cfgs.size(); ++ci) {
         launch_fill(d_part_, 0.0, acc_n, stream_);

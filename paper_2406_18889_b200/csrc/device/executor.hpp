@@ -53,6 +53,7 @@ struct NodeInfo {
     std::vector<int> labels;  // device layout, most significant first
     uint64_t var_mask = 0;    // group-code bits of the output legs in the subtree
     int level = 0;
+    bool pass_dep = false;    // depends on slice / configuration bits
     int consumer = -1;        // program step consuming this node (-1: root)
     int64_t payload = 1;
     int64_t max_var = 1;
@@ -68,6 +69,7 @@ struct StepInfo {
     int plan_index = 0;
     int a = -1, b = -1, r = -1;  // A-role operand, B-role operand, result (node ids)
     int level = 0;
+    int phase = 0;  // 0 constant, 1 per pass, 2 per pass and group, 3 per group only (cached)
     int mode = 0;  // 0 plain, 1 A-variant folded into M, 2 gathered batch
     bool perm_a = false, perm_b = false;
     PermuteDesc pa{}, pb{};
@@ -90,8 +92,9 @@ struct ChunkData {
     int32_t* d_idx = nullptr;
     int32_t* d_groups = nullptr;
     int32_t* d_vid = nullptr;
-    LeafJob* d_leaf_jobs = nullptr;
+    LeafJob* d_leaf_jobs = nullptr;  // phase-3 leaves first, then phase-2 leaves
     int n_leaf_jobs = 0;
+    int n_leaf_jobs3 = 0;
 };
 
 class Program {
@@ -129,12 +132,24 @@ class Program {
     void bind_groups(const std::vector<uint64_t>& groups);
     void calibrate(const std::vector<uint64_t>& groups, uint64_t config, uint64_t slice);
     void exec_pass_body(int64_t P);
+    // per-pass task DAG: tasks run on lane streams ordered by arena hazards,
+    // so independent steps overlap (and the captured graph keeps the DAG)
+    struct Task {
+        int kind;  // 0 level-1 leaf projection, 1 step, 2 / 4 chunk leaf projection (phase 2 / 3),
+                   // 3 chunk finalize
+        const StepInfo* st;
+        const ChunkData* ch;
+    };
+    void build_tasks();
+    void free_tasks();
+    void exec_pass_dag(int64_t P);
+    void run_task(const Task& t, int64_t P);
     void run_pass_body(int64_t P);
     void reset_graph();
     void run_bound(size_t n_groups, const std::vector<uint64_t>& configs, uint64_t slice_begin,
                    uint64_t slice_end, double* d_acc, rcsg_stats* stats, int64_t P, int64_t acc_n, bool sync);
     void free_chunks();
-    void exec_level(int level, const ChunkData* ch);
+    void exec_phase(int phase, const ChunkData* ch);
     void exec_step(const StepInfo& s, const ChunkData* ch);
     void* buf(int64_t off) const;
     template <typename R>
@@ -157,6 +172,14 @@ class Program {
 
     // device state
     cudaStream_t stream_ = nullptr;
+    cudaStream_t ls_ = nullptr;  // stream the exec_* launches go to (stream_ or a lane)
+    std::vector<Task> tasks_;
+    std::vector<std::vector<int>> task_wait_;  // per task: tasks on other lanes to wait for
+    std::vector<int> task_lane_;
+    std::vector<cudaEvent_t> task_ev_;
+    std::vector<cudaStream_t> lanes_;
+    std::vector<cudaEvent_t> lane_ev_;  // fork (index 0) and per-lane join events
+    int n_lanes_used_ = 0;
     void* arena_ = nullptr;
     int64_t arena_elems_ = 0;
     int64_t chunk_cap_ = 0;
@@ -175,6 +198,7 @@ class Program {
     // batch-aware reassociation: done once, at the first run (group codes known)
     bool tree_fixed_ = false;
     bool level0_valid_ = false;  // level-0 (constant) results live in the arena
+    bool phase3_valid_ = false;  // single chunk: its group-only (phase-3) results live in the arena
     bool fault_pending_ = false; // async runs whose fault flag is not checked yet
     std::vector<int32_t> step_origin_;  // program step -> index of the plan step it came from
     // fp16 mode: per-node storage exponents (value stored times 2^-e)

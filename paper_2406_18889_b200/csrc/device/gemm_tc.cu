@@ -185,6 +185,8 @@ struct TcParams {
     int32_t* fault;
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
+    int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
+                            // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
 
 // Store one 32-column chunk of a thread's row: to the split-K workspace
@@ -257,12 +259,101 @@ __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_
     return bad;
 }
 
+// Staged epilogue for 2-byte outputs.  A lane holds one row's 32 columns;
+// when the output's fastest bits are column bits (epi 1, 2) or row bits
+// (epi 3) the scalar stores hit one 32-B sector per 2-B element.  Instead the
+// warp parks its 32x32 chunk in shared memory and re-reads it as 16-B vectors
+// of 8 output-contiguous elements: 8 consecutive columns of one row (epi 1:
+// lanes sweep a row's 4 vectors, epi 2: lanes sweep 32 rows, for outputs whose
+// row bit 0 sits right above a 3-bit column run) or 8 consecutive rows of one
+// column (epi 3).
+constexpr int kEpiPitch = 40;  // elements per staged row: 80 B, 16-B aligned, spreads banks
+constexpr int kEpiWarpElems = 32 * kEpiPitch;
+// staged element (r, c): 16-B slot c/8 XOR-swizzled by r/8, so 8-row gathers
+// of one column (epi 3) hit distinct banks
+__device__ __forceinline__ int epi_at(int r, int c) {
+    return r * kEpiPitch + ((((c >> 3) ^ (r >> 3)) & 3) << 3) + (c & 7);
+}
+
+template <typename E>
+__device__ __forceinline__ uint4 pack8(const float* x) {
+    union {
+        E e[8];
+        uint4 u;
+    } t;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) store_c(&t.e[i], x[i]);
+    return t.u;
+}
+
+template <typename E>
+__device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v, int64_t row0, int64_t col0,
+                                                   E* stage, float* re, float* im, const int64_t* tn_lo,
+                                                   int lane) {
+    bool bad = false;
+    if (p.scale_exp) {
+        const float sc = exp2f(static_cast<float>(p.scale_exp));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            re[i] *= sc;
+            im[i] *= sc;
+        }
+    }
+    const bool live = row0 + lane < p.m;
+    if (live) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) bad |= unstorable<E>(re[i]) || unstorable<E>(im[i]);
+    }
+    const int64_t my_off = live ? out_row_off(p.om, p.n, row0 + lane) : 0;
+    E* const cre = static_cast<E*>(p.c) + v * p.c_batch + out_col_off(p.om, col0);
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) {
+        const float* x = pl ? im : re;
+        uint4* srow = reinterpret_cast<uint4*>(stage + lane * kEpiPitch);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) srow[(i ^ (lane >> 3)) & 3] = pack8<E>(x + 8 * i);
+        __syncwarp();
+        E* const base = cre + (pl ? p.c_plane : 0);
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int id = it * 32 + lane;
+            int r;
+            int64_t coff;
+            uint4 val;
+            if (p.epi == 3) {  // 8 consecutive rows of column c
+                const int c = id >> 2;
+                r = (id & 3) * 8;
+                union {
+                    E e[8];
+                    uint4 u;
+                } t;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) t.e[e] = stage[epi_at(r + e, c)];
+                val = t.u;
+                coff = tn_lo[c];
+            } else {  // 8 consecutive columns of row r
+                const int cv = p.epi == 2 ? (id >> 5) : (id & 3);
+                r = p.epi == 2 ? (id & 31) : (id >> 2);
+                val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
+                coff = tn_lo[cv * 8];
+            }
+            const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
+            if (row0 + r < p.m) *reinterpret_cast<uint4*>(base + roff + coff) = val;
+        }
+        __syncwarp();
+    }
+    return bad;
+}
+
 template <int BN, int STAGES>
 struct Smem {
     static constexpr int kATile = kBM * 128;  // bytes per A plane tile (128-B rows)
     static constexpr int kBTile = BN * 128;
     static constexpr int kStage = 2 * kATile + 2 * kBTile;
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    // persistent kernel: + staged-epilogue buffers of the 8 epilogue warps (2-byte E)
+    template <typename E>
+    static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 8 * kEpiWarpElems * 2 : 0);
 };
 
 template <int BN, int STAGES, typename E>
@@ -525,6 +616,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     } else {  // ---- epilogue warps 2..9: lane quarter warp % 4, column half (warp - 2) / 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int half = (warp - 2) >> 2;
+        E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
         bool bad = false;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
@@ -539,6 +631,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 float re[32], im[32];
                 tmem_ld32(base + c0, re);
                 tmem_ld32(base + BN + c0, im);
+                if constexpr (sizeof(E) == 2) {
+                    if (p.epi && p.splits == 1 && c.n0 + c0 + 32 <= p.n) {
+                        bad |= store_chunk_staged<E>(p, c.v, c.m0 + q * 32, c.n0 + c0, stage, re, im, tn_lo, lane);
+                        continue;
+                    }
+                }
                 if (row < p.m) bad |= store_chunk<E>(p, c.split, c.v, row, c.n0 + c0, re, im, tn_lo);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -585,6 +683,21 @@ CUtensorMap make_map(const void* base, int64_t k, int64_t rows, int64_t batch, i
     return m;
 }
 
+// Staged-epilogue kind for a 2-byte output layout (see store_chunk_staged).
+int epilogue_kind(const OutMap& om, int64_t n) {
+    if (n % 32) return 0;
+    int cr = 0, rr = 0;  // column / row bits at output bits 0, 1, 2, ...
+    if (!om.scatter) {
+        cr = 64;
+    } else {
+        while (cr < om.n_bits && om.n_pos[cr] == cr) ++cr;
+        while (rr < om.m_bits && om.m_pos[rr] == rr) ++rr;
+    }
+    if (cr >= 3) return (cr == 3 && om.scatter && om.m_bits > 0 && om.m_pos[0] == 3) ? 2 : 1;
+    if (rr >= 3) return 3;
+    return 0;
+}
+
 template <int BN, int STAGES, typename E>
 void launch(const GemmArgs& g, cudaStream_t st) {
     using S = Smem<BN, STAGES>;
@@ -618,6 +731,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.fault = g.fault;
     p.om = g.om;
     p.scale_exp = g.scale_exp;
+    p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : 0;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + KBK<E> - 1) / KBK<E>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
@@ -648,12 +762,13 @@ void launch(const GemmArgs& g, cudaStream_t st) {
         static bool pconf = false;
         if (!pconf) {
             cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 S::kBytes);
+                                 S::template kPBytes<E>);
             pconf = true;
         }
         const int64_t total = tiles * splits;
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-        gemm_tc_persistent<BN, STAGES, E><<<grid, kPThreads, S::kBytes, st>>>(ar, ai, br, bi, p, total);
+        gemm_tc_persistent<BN, STAGES, E><<<grid, kPThreads, S::template kPBytes<E>, st>>>(ar, ai, br, bi, p,
+                                                                                            total);
     } else {
         gemm_tc_kernel<BN, STAGES, E><<<static_cast<unsigned>(tiles * splits), kThreads, S::kBytes, st>>>(ar, ai, br,
                                                                                                         bi, p);
