@@ -122,3 +122,56 @@ extern "C" int rcsg_gemm_selftest(int64_t m, int64_t n, int64_t k, int64_t batch
         return RCSG_ERR_DEVICE;
     }
 }
+
+// fp16 complex GEMM timing with an explicit output scatter map (kernel tuning):
+// C[m][n] (through the map) = A[m][k] B[n][k]^T; returns ms per launch.
+extern "C" int rcsg_gemm_bench_f16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                   const int8_t* m_pos, const int8_t* n_pos, int32_t iters, double* out_ms) {
+    try {
+        __half *a, *b, *c;
+        int32_t* fault;
+        if (cudaMalloc(&a, 2 * m * k * 2) || cudaMalloc(&b, 2 * n * k * 2) || cudaMalloc(&c, 2 * m * n * 2) ||
+            cudaMalloc(&fault, 4))
+            return RCSG_ERR_DEVICE;
+        cudaMemset(a, 0, 2 * m * k * 2);
+        cudaMemset(b, 0, 2 * n * k * 2);
+        GemmArgs g{};
+        g.a = a;
+        g.a_plane = m * k;
+        g.b = b;
+        g.b_plane = n * k;
+        g.c = c;
+        g.c_plane = m * n;
+        g.m = m;
+        g.n = n;
+        g.k = k;
+        g.batch = 1;
+        g.fault = fault;
+        g.om.m_bits = m_bits;
+        g.om.n_bits = n_bits;
+        g.om.scatter = m_bits + n_bits > 0;
+        for (int j = 0; j < m_bits; ++j) g.om.m_pos[j] = m_pos[j];
+        for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        launch_gemm_tc(g, 2, 0);
+        cudaEventRecord(e0);
+        for (int i = 0; i < iters; ++i) launch_gemm_tc(g, 2, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *out_ms = ms / iters;
+        const cudaError_t err = cudaGetLastError();
+        cudaFree(a);
+        cudaFree(b);
+        cudaFree(c);
+        cudaFree(fault);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return err == cudaSuccess ? RCSG_OK : RCSG_ERR_DEVICE;
+    } catch (...) {
+        return RCSG_ERR_DEVICE;
+    }
+}

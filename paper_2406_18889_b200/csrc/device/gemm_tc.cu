@@ -185,76 +185,58 @@ struct TcParams {
     int32_t* fault;
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
+    int32_t dbg;            // tuning knob (RCSG_TC_DBG): 1 = skip the epilogue's global stores
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
 
-// Store one 32-column chunk of a thread's row: to the split-K workspace
-// (fp32, row-major), or to C (element type) row-major (vectorised for fp32) or
-// through the output scatter map into the consumer's layout.
+// Store one 32-column chunk of one plane (0 Re, 1 Im) of a thread's row: to the
+// split-K workspace (fp32, row-major), or to C (element type) row-major
+// (vectorised for fp32) or through the output scatter map into the
+// consumer's layout.
 template <typename E>
 __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_t v, int64_t row, int64_t col0,
-                                            float* re, float* im, const int64_t* tn_lo) {
+                                            float* x, int plane, const int64_t* tn_lo, int64_t row_off,
+                                            int64_t col_base) {
     bool bad = false;
     if (p.ws_split) {  // raw partials; the reduction scales and checks
 #pragma unroll
-        for (int i = 0; i < 32; ++i) bad |= !isfinite(re[i]) || !isfinite(im[i]);
-        float* cre = static_cast<float*>(p.c) + split * p.ws_split + v * p.c_batch;
-        float* pr = cre + row * p.n + col0;
-        float* pi = pr + p.c_plane;
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-            pr[i] = re[i];
-            pi[i] = im[i];
-        }
+        for (int i = 0; i < 32; ++i) bad |= !isfinite(x[i]);
+        float* pr = static_cast<float*>(p.c) + split * p.ws_split + v * p.c_batch + plane * p.c_plane + row * p.n + col0;
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) pr[i] = x[i];
         return bad;
     }
     if (p.scale_exp) {
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            re[i] *= sc;
-            im[i] *= sc;
-        }
+        for (int i = 0; i < 32; ++i) x[i] *= sc;
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) bad |= unstorable<E>(re[i]) || unstorable<E>(im[i]);
-    E* cre = static_cast<E*>(p.c) + v * p.c_batch;
-    E* cim = cre + p.c_plane;
+    for (int i = 0; i < 32; ++i) bad |= unstorable<E>(x[i]);
+    E* cpl = static_cast<E*>(p.c) + v * p.c_batch + plane * p.c_plane;
     if (!p.om.scatter) {
-        E* pr = cre + row * p.n + col0;
-        E* pi = cim + row * p.n + col0;
+        E* pr = cpl + row * p.n + col0;
         if constexpr (sizeof(E) == 4) {
             if (col0 + 32 <= p.n && (p.n & 3) == 0) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    *reinterpret_cast<float4*>(pr + i) = make_float4(re[i], re[i + 1], re[i + 2], re[i + 3]);
-                    *reinterpret_cast<float4*>(pi + i) = make_float4(im[i], im[i + 1], im[i + 2], im[i + 3]);
-                }
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4*>(pr + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
                 return bad;
             }
         }
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-            store_c(pr + i, re[i]);
-            store_c(pi + i, im[i]);
-        }
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) store_c(pr + i, x[i]);
         return bad;
     }
-    const int64_t base = out_row_off(p.om, p.n, row) + out_col_off(p.om, col0);
+    const int64_t base = row_off + col_base;
     const int sh = p.om.n_pos[0];
     const bool contig = p.om.n_bits >= 5 && p.om.n_pos[1] == sh + 1 && p.om.n_pos[2] == sh + 2 &&
                         p.om.n_pos[3] == sh + 3 && p.om.n_pos[4] == sh + 4;
     if (col0 + 32 <= p.n && contig) {
         // column bits contiguous at bit sh (sh == 0: per-thread contiguous run)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            store_c(cre + base + (static_cast<int64_t>(i) << sh), re[i]);
-            store_c(cim + base + (static_cast<int64_t>(i) << sh), im[i]);
-        }
+        for (int i = 0; i < 32; ++i) store_c(cpl + base + (static_cast<int64_t>(i) << sh), x[i]);
     } else {
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-            store_c(cre + base + tn_lo[i], re[i]);
-            store_c(cim + base + tn_lo[i], im[i]);
-        }
+        for (int i = 0; i < 32 && col0 + i < p.n; ++i) store_c(cpl + base + tn_lo[i], x[i]);
     }
     return bad;
 }
@@ -267,12 +249,13 @@ __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_
 // lanes sweep a row's 4 vectors, epi 2: lanes sweep 32 rows, for outputs whose
 // row bit 0 sits right above a 3-bit column run) or 8 consecutive rows of one
 // column (epi 3).
-constexpr int kEpiPitch = 40;  // elements per staged row: 80 B, 16-B aligned, spreads banks
+constexpr int kEpiPitch = 32;  // elements per staged row (64 B)
 constexpr int kEpiWarpElems = 32 * kEpiPitch;
-// staged element (r, c): 16-B slot c/8 XOR-swizzled by r/8, so 8-row gathers
-// of one column (epi 3) hit distinct banks
+// staged element (r, c): 16-B slot c/8 XOR-swizzled by bits 1-2 and 3-4 of r,
+// so row writes, row-vector reads and 8-row column gathers (epi 3) are all
+// bank-conflict-free
 __device__ __forceinline__ int epi_at(int r, int c) {
-    return r * kEpiPitch + ((((c >> 3) ^ (r >> 3)) & 3) << 3) + (c & 7);
+    return r * kEpiPitch + ((((c >> 3) ^ (r >> 1) ^ (r >> 3)) & 3) << 3) + (c & 7);
 }
 
 template <typename E>
@@ -286,62 +269,63 @@ __device__ __forceinline__ uint4 pack8(const float* x) {
     return t.u;
 }
 
+// one plane of a warp's 32x32 chunk (rows row0.., columns col0..)
 template <typename E>
-__device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v, int64_t row0, int64_t col0,
-                                                   E* stage, float* re, float* im, const int64_t* tn_lo,
-                                                   int lane) {
+__device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v, int64_t row0, E* stage, float* x,
+                                                   int plane, const int64_t* tn_lo, int lane, int64_t my_off,
+                                                   int64_t col_base) {
     bool bad = false;
     if (p.scale_exp) {
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            re[i] *= sc;
-            im[i] *= sc;
-        }
+        for (int i = 0; i < 32; ++i) x[i] *= sc;
     }
     const bool live = row0 + lane < p.m;
-    if (live) {
+    if (live) {  // one range check on the max magnitude, plus NaN
+        float mx = 0.f;
+        bool nan = false;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) bad |= unstorable<E>(re[i]) || unstorable<E>(im[i]);
-    }
-    const int64_t my_off = live ? out_row_off(p.om, p.n, row0 + lane) : 0;
-    E* const cre = static_cast<E*>(p.c) + v * p.c_batch + out_col_off(p.om, col0);
-#pragma unroll
-    for (int pl = 0; pl < 2; ++pl) {
-        const float* x = pl ? im : re;
-        uint4* srow = reinterpret_cast<uint4*>(stage + lane * kEpiPitch);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) srow[(i ^ (lane >> 3)) & 3] = pack8<E>(x + 8 * i);
-        __syncwarp();
-        E* const base = cre + (pl ? p.c_plane : 0);
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int id = it * 32 + lane;
-            int r;
-            int64_t coff;
-            uint4 val;
-            if (p.epi == 3) {  // 8 consecutive rows of column c
-                const int c = id >> 2;
-                r = (id & 3) * 8;
-                union {
-                    E e[8];
-                    uint4 u;
-                } t;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) t.e[e] = stage[epi_at(r + e, c)];
-                val = t.u;
-                coff = tn_lo[c];
-            } else {  // 8 consecutive columns of row r
-                const int cv = p.epi == 2 ? (id >> 5) : (id & 3);
-                r = p.epi == 2 ? (id & 31) : (id >> 2);
-                val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
-                coff = tn_lo[cv * 8];
-            }
-            const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
-            if (row0 + r < p.m) *reinterpret_cast<uint4*>(base + roff + coff) = val;
+        for (int i = 0; i < 32; ++i) {
+            mx = fmaxf(mx, fabsf(x[i]));
+            nan |= x[i] != x[i];
         }
-        __syncwarp();
+        bad = nan || unstorable<E>(mx);
     }
+    E* const base = static_cast<E*>(p.c) + v * p.c_batch + plane * p.c_plane + col_base;
+    int64_t col_off[4];  // this lane's column offset in each of the 4 rounds
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int id = it * 32 + lane;
+        col_off[it] = p.epi == 3 ? tn_lo[id >> 2] : tn_lo[(p.epi == 2 ? (id >> 5) : (id & 3)) * 8];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<uint4*>(stage + epi_at(lane, 8 * i)) = pack8<E>(x + 8 * i);
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int id = it * 32 + lane;
+        int r;
+        uint4 val;
+        if (p.epi == 3) {  // 8 consecutive rows of column c
+            const int c = id >> 2;
+            r = (id & 3) * 8;
+            union {
+                E e[8];
+                uint4 u;
+            } t;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) t.e[e] = stage[epi_at(r + e, c)];
+            val = t.u;
+        } else {  // 8 consecutive columns of row r
+            const int cv = p.epi == 2 ? (id >> 5) : (id & 3);
+            r = p.epi == 2 ? (id & 31) : (id >> 2);
+            val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
+        }
+        const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
+        if (row0 + r < p.m && p.dbg != 1) *reinterpret_cast<uint4*>(base + roff + col_off[it]) = val;
+    }
+    __syncwarp();
     return bad;
 }
 
@@ -353,7 +337,7 @@ struct Smem {
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
     // persistent kernel: + staged-epilogue buffers of the 8 epilogue warps (2-byte E)
     template <typename E>
-    static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 8 * kEpiWarpElems * 2 : 0);
+    static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 16 * kEpiWarpElems * 2 : 0);
 };
 
 template <int BN, int STAGES, typename E>
@@ -472,7 +456,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) re[i] = im[i] = 0.f;
         }
-        if (row < p.m) bad |= store_chunk<E>(p, split, v, row, n0 + c0, re, im, tn_lo);
+        if (row < p.m) {
+            const int64_t ro = out_row_off(p.om, p.n, row), cb = out_col_off(p.om, n0 + c0);
+            bad |= store_chunk<E>(p, split, v, row, n0 + c0, re, 0, tn_lo, ro, cb);
+            bad |= store_chunk<E>(p, split, v, row, n0 + c0, im, 1, tn_lo, ro, cb);
+        }
     }
     if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -484,10 +472,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 // double-buffered in TMEM (2 x {Re, Im} x BN columns) so the four epilogue
 // warps drain tile i while the MMA warp already accumulates tile i+1.
 //   warp 0: TMA producer   warp 1: MMA issuer   warps 2-5: epilogue (TMEM lane quarter = warp % 4)
-constexpr int kPThreads = 320;  // 2 role warps + 8 epilogue warps (2 per TMEM lane quarter)
+constexpr int kPThreads = 576;  // 2 role warps + 16 epilogue warps (4 per TMEM lane quarter: plane x half)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// OR of a 64-bit value across the warp
+__device__ __forceinline__ int64_t warp_or64(int64_t v) {
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(v));
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32));
+    return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+}
+// scatter of bits [lo_bit, bits) of a warp-uniform x: lane j places bit j
+__device__ __forceinline__ int64_t warp_scatter(const int8_t* pos, int bits, int lo_bit, int64_t x, int lane) {
+    int64_t c = 0;
+    if (lane >= lo_bit && lane < bits) c = ((x >> lane) & int64_t{1}) << pos[lane];
+    return warp_or64(c);
 }
 
 struct TileCoord {
@@ -497,21 +498,30 @@ struct TileCoord {
 };
 
 template <int BN, typename E>
-__device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t) {
+__device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) {
+    // tile counts fit 32 bits (the host checks): 32-bit div/mod, not the 64-bit routine
     TileCoord c;
-    c.split = static_cast<int>(t % p.splits);
-    t /= p.splits;
-    int64_t ntile, mtile;
+    uint32_t t = static_cast<uint32_t>(t64);
+    const uint32_t splits = static_cast<uint32_t>(p.splits), mt = static_cast<uint32_t>(p.mt),
+                   nt = static_cast<uint32_t>(p.nt);
+    uint32_t q = splits == 1 ? t : t / splits;
+    c.split = static_cast<int>(t - q * splits);
+    t = q;
+    uint32_t ntile, mtile;
     if (p.m_fast) {
-        mtile = t % p.mt;
-        t /= p.mt;
-        ntile = t % p.nt;
-        t /= p.nt;
+        q = t / mt;
+        mtile = t - q * mt;
+        t = q;
+        q = t / nt;
+        ntile = t - q * nt;
+        t = q;
     } else {
-        ntile = t % p.nt;
-        t /= p.nt;
-        mtile = t % p.mt;
-        t /= p.mt;
+        q = t / nt;
+        ntile = t - q * nt;
+        t = q;
+        q = t / mt;
+        mtile = t - q * mt;
+        t = q;
     }
     c.v = t;
     c.m0 = static_cast<int>(mtile * kBM);
@@ -528,14 +538,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const TcParams p, int64_t total_tiles) {
     using S = Smem<BN, STAGES>;
-    constexpr uint32_t kCols = 4 * BN;  // 2 buffers x {Re, Im}
+    // TMEM accumulator buffers {Re, Im}: as many as fit in 512 columns (max 4),
+    // so the MMA runs ahead of the epilogue by NBUF - 1 tiles
+    constexpr uint32_t NBUF = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
+    constexpr uint32_t kCols = NBUF * 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ int64_t tn_lo[32];
     if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
@@ -545,9 +558,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < static_cast<int>(NBUF); ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 8);
+            mbar_init(&tempty[b], 16);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -573,6 +586,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const int s = it % STAGES;
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* st = smem + s * S::kStage;
+                    if (p.dbg == 3) {  // tuning: no loads
+                        mbar_expect_tx(&full[s], 0);
+                        continue;
+                    }
                     mbar_expect_tx(&full[s], S::kStage);
                     const int kc = static_cast<int>(c.k_begin) + kb * KBK<E>;
                     tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
@@ -588,8 +605,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
             uint32_t it = 0, j = 0;
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
                 const TileCoord c = tile_coord<BN, E>(p, t);
-                const uint32_t ab = j & 1;
-                if (j >= 2) mbar_wait(&tempty[ab], ((j >> 1) - 1) & 1);
+                const uint32_t ab = j % NBUF;
+                if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t t_re = tmem + ab * 2 * BN, t_im = t_re + BN;
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
@@ -599,45 +616,61 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const uint8_t* st = smem + s * S::kStage;
                     const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
                     const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
+                    if (p.dbg != 2) {  // tuning: dbg 2 skips the MMAs
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
-                        const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
-                        mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
-                        mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
-                        mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
-                        mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
+                            const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
+                            mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                            mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                            mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                            mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
+                        }
                     }
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[ab]);
             }
         }
-    } else {  // ---- epilogue warps 2..9: lane quarter warp % 4, column half (warp - 2) / 4
+    } else {  // ---- epilogue warps 2..17: TMEM lane quarter warp % 4; plane and column half from (warp - 2) / 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int half = (warp - 2) >> 2;
+        const int sub = (warp - 2) >> 2;
+        const int plane = sub & 1, half = sub >> 1;
         E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
+        // output row offset = tile part (bits >= 7 of the row, warp-uniform) + this
+        // lane's part (bits 0..6, fixed), when the map's row bits cover a tile
+        const int local = q * 32 + lane;
+        const bool split_rows = p.om.scatter && p.om.m_bits >= 7;
+        const int64_t lane_off = split_rows ? scatter_bits(p.om.m_pos, 7, local) : 0;
         bool bad = false;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
             const TileCoord c = tile_coord<BN, E>(p, t);
-            const uint32_t ab = j & 1;
-            mbar_wait(&tfull[ab], (j >> 1) & 1);
+            const uint32_t ab = j % NBUF;
+            const int64_t row = c.m0 + local;
+            int64_t row_off;
+            if (!p.om.scatter) row_off = row * p.n;
+            else if (split_rows)
+                row_off = ((static_cast<int64_t>(c.m0) >> p.om.m_bits) << (p.om.m_bits + p.om.n_bits)) +
+                          warp_scatter(p.om.m_pos, p.om.m_bits, 7, c.m0, lane) + lane_off;
+            else row_off = row < p.m ? out_row_off(p.om, p.n, row) : 0;
+            mbar_wait(&tfull[ab], (j / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t row = c.m0 + q * 32 + lane;
-            const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN;
+            const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
 #pragma unroll 1
             for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
-                float re[32], im[32];
-                tmem_ld32(base + c0, re);
-                tmem_ld32(base + BN + c0, im);
+                const int64_t col0 = c.n0 + c0;  // multiple of 32
+                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, 5, col0, lane) : col0;
+                float x[32];
+                tmem_ld32(base + c0, x);
                 if constexpr (sizeof(E) == 2) {
-                    if (p.epi && p.splits == 1 && c.n0 + c0 + 32 <= p.n) {
-                        bad |= store_chunk_staged<E>(p, c.v, c.m0 + q * 32, c.n0 + c0, stage, re, im, tn_lo, lane);
+                    if (p.epi && p.splits == 1 && col0 + 32 <= p.n) {
+                        bad |= store_chunk_staged<E>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
+                                                     row < p.m ? row_off : 0, col_base);
                         continue;
                     }
                 }
-                if (row < p.m) bad |= store_chunk<E>(p, c.split, c.v, row, c.n0 + c0, re, im, tn_lo);
+                if (row < p.m) bad |= store_chunk<E>(p, c.split, c.v, row, col0, x, plane, tn_lo, row_off, col_base);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -732,6 +765,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.om = g.om;
     p.scale_exp = g.scale_exp;
     p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : 0;
+    static const int dbg = getenv("RCSG_TC_DBG") ? atoi(getenv("RCSG_TC_DBG")) : 0;
+    p.dbg = dbg;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + KBK<E> - 1) / KBK<E>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
@@ -766,6 +801,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
             pconf = true;
         }
         const int64_t total = tiles * splits;
+        if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
         gemm_tc_persistent<BN, STAGES, E><<<grid, kPThreads, S::template kPBytes<E>, st>>>(ar, ai, br, bi, p,
                                                                                             total);
