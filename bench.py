@@ -227,13 +227,19 @@ def main():
     acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
     stream = torch.cuda.ExternalStream(p.stream(args.precision))
 
-    def slice_of(i):
-        return (rank + i * world) % p.n_slices
+    # a step is one slice contraction; one call contracts an aligned block of S
+    # consecutive slices (one device pass per slice, or per slice batch when the
+    # executor batches clean low sliced labels)
+    S = min(8, p.n_slices)
+    n_calls = (args.steps + S - 1) // S
 
-    def step(i, st=None, sync=True):
-        s = slice_of(i)
+    def block_of(i):
+        return (rank + i * world) % (p.n_slices // S)
+
+    def step(i, st=None, sync=True, count=None):
+        s = block_of(i) * S
         return p.contract_groups_device(fixed, acc.data_ptr(), precision=args.precision, configs=None,
-                                        slices=(s, s + 1), stats=st, sync=sync)
+                                        slices=(s, s + (count or S)), stats=st, sync=sync)
 
     for i in range(args.warmup):
         step(i)
@@ -244,18 +250,19 @@ def main():
     # stream, outside each step's event pair
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+           for _ in range(n_calls)]
     clocks = Clocks(local)
     st = rcsg_stats()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with torch.cuda.stream(stream):
-        for i in range(args.steps):
+        for i in range(n_calls):
             flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            step(args.warmup + i, st, sync=False)  # enqueue only; checked by p.sync below
-            if i == args.steps - 1 and world > 1:
+            count = min(S, args.steps - i * S)
+            step(args.warmup + i, st, sync=False, count=count)  # enqueue only; checked by p.sync below
+            if i == n_calls - 1 and world > 1:
                 dist.all_reduce(acc)  # the slice sum across ranks
             evs[i][1].record(stream)
     p.sync(args.precision)
@@ -286,15 +293,16 @@ def main():
     # end-to-end through the public API with host buffers (rank 0 work pattern on each rank)
     e2e = None
     if not args.no_e2e:
-        K = max(2, min(args.steps, 8))
+        K = max(2, min(n_calls, 8))  # calls of S slices each
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(K):
-            s = slice_of(i)
-            out = p.contract_groups(fixed, precision=args.precision, configs=None, slices=(s, s + 1))
+            s = block_of(i) * S
+            out = p.contract_groups(fixed, precision=args.precision, configs=None, slices=(s, s + S))
         t1 = time.perf_counter()
-        e2e = {"value": world * K / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": int(fixed.nbytes),
-               "d2h_bytes_per_step": int(out.nbytes), "api": "Problem.contract_groups (host in/out)"}
+        e2e = {"value": world * K * S / (t1 - t0), "unit": UNIT,
+               "h2d_bytes_per_step": int(fixed.nbytes) / S, "d2h_bytes_per_step": int(out.nbytes) / S,
+               "api": f"Problem.contract_groups (host in/out), {S} slices per call"}
         if world > 1:
             tt = torch.tensor([t1 - t0], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -328,6 +336,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[args.precision],
             "data": "synthetic (random circuit of the named shape)",
             "config": {"workload": WORKLOAD, "groups_per_slice": M, "duplicate_groups": int(dups),
+                       "slices_per_call": S,
                        "precision": args.precision, "l2": "flushed between timed steps (256 MiB write, "
                        f"outside the per-step events); arena {st.arena_bytes / 2**30:.2f} GiB per GPU",
                        "parallelism": f"slice-sharded x{world}"},
@@ -342,7 +351,8 @@ def main():
                          "traffic": None,
                          "peak_note": peak_note,
                          "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None},
-            "kernel_breakdown_ms": {"step": pst.device_ms, "gemm_tc": pst.gemm_tc_ms,
+            "kernel_breakdown_ms": {"per": f"one profiled pass of {S} slices (serialised launches)",
+                                    "step": pst.device_ms, "gemm_tc": pst.gemm_tc_ms,
                                     "gemm_other": pst.gemm_ms - pst.gemm_tc_ms, "permute": pst.permute_ms,
                                     "permute_gbs": pst.permute_bytes / (pst.permute_ms * 1e-3) / 1e9
                                     if pst.permute_ms else None, "hbm_peak_gbs": hbm_peak},

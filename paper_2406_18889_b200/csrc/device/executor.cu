@@ -1,5 +1,6 @@
 // Step-program executor; see executor.hpp for the design.
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -156,9 +157,13 @@ struct TreeCost {
         const double un = std::ldexp(1.0, static_cast<int>(x.labels.size() + y.labels.size() - sh.size()));
         const double va = nvar(x.mask), vb = nvar(y.mask), vz = nvar(x.mask | y.mask);
         double mult, rd;
-        if (x.mask && y.mask) {  // gathered batch: one GEMM per result variant
+        if (x.mask && y.mask) {
             mult = vz;
-            rd = vz * (la + lb);
+            const uint64_t hx = x.mask, hy = y.mask;
+            const bool separable = __builtin_ctzll(hx) > 63 - __builtin_clzll(hy) ||
+                                   __builtin_ctzll(hy) > 63 - __builtin_clzll(hx);
+            if (separable && vz == va * vb) rd = va * la + vb * lb;  // product: one GEMM, variants in M and N
+            else rd = vz * (la + lb);                                // gathered batch: one GEMM per variant
         } else {  // the varying operand's variants fold into M
             mult = std::max(va, vb);
             rd = va * la + vb * lb;
@@ -261,6 +266,8 @@ Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
     if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_F16)
         throw Failure{RCSG_ERR_CONFIG, "unknown precision"};
     elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : (precision >= RCSG_PREC_BF16 ? 2 : 4);
+    for (const LabelRole& r : roles_)
+        if (r.role == kVar) group_bits_ = std::max(group_bits_, r.var_bit + 1);
     build_nodes(net, plan);
     build_steps();
     node_exp_.assign(nodes_.size(), 0);
@@ -631,8 +638,7 @@ void Program::free_chunks() {
     for (ChunkData& c : chunks_) {
         cudaFree(c.d_codes);
         cudaFree(c.d_idx);
-        cudaFree(c.d_groups);
-        cudaFree(c.d_vid);
+        cudaFree(c.d_fin);
         cudaFree(c.d_leaf_jobs);
     }
     chunks_.clear();
@@ -678,11 +684,23 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
             ch.ib_off[s] = static_cast<int64_t>(ch.idx.size());
             for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.b, c & nodes_[st.b].var_mask));
         }
+        // codes are the run's (group, batched slice) combinations, index lo * G + g
+        const int64_t G = static_cast<int64_t>(n_ext_groups_);
+        std::vector<std::array<int32_t, 3>> ent;  // (group, lo, root variant)
         for (size_t u = u0; u < u1; ++u)
-            for (int32_t g : members[uniq[u]]) {
-                ch.groups.push_back(g);
-                ch.vid.push_back(nodes_[root_].level == 2 ? find_code(root_, uniq[u] & nodes_[root_].var_mask) : 0);
+            for (int32_t c : members[uniq[u]])
+                ent.push_back({static_cast<int32_t>(c % G), static_cast<int32_t>(c / G),
+                               nodes_[root_].level == 2 ? find_code(root_, uniq[u] & nodes_[root_].var_mask) : 0});
+        std::sort(ent.begin(), ent.end());
+        for (size_t e = 0; e < ent.size(); ++e) {
+            if (e == 0 || ent[e][0] != ent[e - 1][0]) {
+                ch.fin_g.push_back(ent[e][0]);
+                ch.fin_off.push_back(static_cast<int32_t>(e));
             }
+            ch.ent_lo.push_back(ent[e][1]);
+            ch.ent_vid.push_back(ent[e][2]);
+        }
+        ch.fin_off.push_back(static_cast<int32_t>(ent.size()));
         // level-2 leaf jobs of this chunk: group-only leaves, then pass-dependent ones
         std::vector<LeafJob> jobs;
         std::vector<int> leaf_order;
@@ -713,10 +731,14 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
         CUDA_OK(cudaMemcpy(ch.d_codes, ch.codes.data(), ch.codes.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
         CUDA_OK(cudaMalloc(&ch.d_idx, std::max<size_t>(ch.idx.size(), 1) * sizeof(int32_t)));
         CUDA_OK(cudaMemcpy(ch.d_idx, ch.idx.data(), ch.idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMalloc(&ch.d_groups, std::max<size_t>(ch.groups.size(), 1) * sizeof(int32_t)));
-        CUDA_OK(cudaMemcpy(ch.d_groups, ch.groups.data(), ch.groups.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMalloc(&ch.d_vid, std::max<size_t>(ch.vid.size(), 1) * sizeof(int32_t)));
-        CUDA_OK(cudaMemcpy(ch.d_vid, ch.vid.data(), ch.vid.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        {
+            std::vector<int32_t> fin = ch.fin_g;
+            fin.insert(fin.end(), ch.fin_off.begin(), ch.fin_off.end());
+            fin.insert(fin.end(), ch.ent_vid.begin(), ch.ent_vid.end());
+            fin.insert(fin.end(), ch.ent_lo.begin(), ch.ent_lo.end());
+            CUDA_OK(cudaMalloc(&ch.d_fin, fin.size() * sizeof(int32_t)));
+            CUDA_OK(cudaMemcpy(ch.d_fin, fin.data(), fin.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
         CUDA_OK(cudaMalloc(&ch.d_leaf_jobs, std::max<size_t>(jobs.size(), 1) * sizeof(LeafJob)));
         CUDA_OK(cudaMemcpy(ch.d_leaf_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), cudaMemcpyHostToDevice));
         chunks_.push_back(std::move(ch));
@@ -725,6 +747,75 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
 
 void* Program::buf(int64_t off) const {
     return static_cast<char*>(arena_) + off * elem_bytes_;
+}
+
+// GEMM arguments of a step on its (unpermuted) operand buffers
+GemmArgs Program::step_args(const StepInfo& st, const ChunkData* ch) const {
+    const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b], &Rn = nodes_[st.r];
+    const int64_t va = (A.level == 2 && ch) ? ch->nvar[st.a] : 1;
+    const int64_t vr = (Rn.level == 2 && ch) ? ch->nvar[st.r] : 1;
+    GemmArgs g{};
+    g.a = buf(A.off);
+    g.a_plane = A.plane;
+    g.b = buf(B.off);
+    g.b_plane = B.plane;
+    g.c = buf(Rn.off);
+    g.c_plane = Rn.plane;
+    g.k = st.k;
+    g.n = st.n;
+    g.step = st.plan_index;
+    g.fault = d_fault_;
+    g.om = st.om;
+    g.scale_exp = node_exp_[st.a] + node_exp_[st.b] - node_exp_[st.r];
+    const int64_t vb = (B.level == 2 && ch) ? ch->nvar[st.b] : 1;
+    const int prod = st.mode == 2 ? product_order(A.var_mask, B.var_mask, va, vb, vr) : 0;
+    if (prod) {
+        // every (A variant, B variant) pair is a result variant and one operand's
+        // code bits lie above the other's: the variants fold into M and N of one
+        // GEMM, result variant = b * va + a (B high) or a * vb + b (A high)
+        const int64_t mn = st.m * st.n;
+        g.m = st.m * va;
+        g.n = st.n * vb;
+        g.batch = 1;
+        if (!g.om.scatter) {  // identity layout as an explicit map
+            g.om.scatter = 1;
+            for (int j = 0; j < g.om.n_bits; ++j) g.om.n_pos[j] = static_cast<int8_t>(j);
+            for (int j = 0; j < g.om.m_bits; ++j) g.om.m_pos[j] = static_cast<int8_t>(g.om.n_bits + j);
+        }
+        g.om.m_vstride = prod == 2 ? mn : vb * mn;
+        g.om.n_vstride = prod == 2 ? va * mn : mn;
+    } else if (st.mode == 2) {
+        g.m = st.m;
+        g.batch = vr;
+        g.a_batch = st.m * st.k;
+        g.b_batch = st.n * st.k;
+        g.c_batch = st.m * st.n;
+        g.ia = ch->d_idx + ch->ia_off[&st - steps_.data()];
+        g.ib = ch->d_idx + ch->ib_off[&st - steps_.data()];
+    } else {
+        g.m = st.m * va;  // mode 1: the variants fold into M
+        g.batch = 1;
+    }
+    return g;
+}
+
+// 0: not a full product; 1: A's code bits above B's; 2: B's above A's
+int Program::product_order(uint64_t ma, uint64_t mb, int64_t va, int64_t vb, int64_t vr) {
+    if (!ma || !mb || vr != va * vb) return 0;
+    const int hi_a = 63 - __builtin_clzll(ma), lo_a = __builtin_ctzll(ma);
+    const int hi_b = 63 - __builtin_clzll(mb), lo_b = __builtin_ctzll(mb);
+    if (lo_a > hi_b) return 1;
+    if (lo_b > hi_a) return 2;
+    return 0;
+}
+
+// small enough for the one-CTA chain kernel (~1 us of work)
+bool Program::chainable(const StepInfo& st, const ChunkData* ch) const {
+    if (st.perm_a || st.perm_b || record_max_) return false;
+    const GemmArgs g = step_args(st, ch);
+    const NodeInfo& R = nodes_[st.r];
+    return static_cast<double>(g.batch) * g.m * g.n * g.k <= static_cast<double>(kChainMacs) &&
+           2 * R.plane < (int64_t{1} << 31);
 }
 
 template <typename R>
@@ -755,31 +846,11 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         b_ptr = dst;
         b_plane = st.sb_plane;
     }
-    GemmArgs g{};
+    GemmArgs g = step_args(st, ch);
     g.a = a_ptr;
     g.a_plane = a_plane;
     g.b = b_ptr;
     g.b_plane = b_plane;
-    g.c = buf(Rn.off);
-    g.c_plane = Rn.plane;
-    g.k = st.k;
-    g.n = st.n;
-    g.step = st.plan_index;
-    g.fault = d_fault_;
-    g.om = st.om;
-    g.scale_exp = node_exp_[st.a] + node_exp_[st.b] - node_exp_[st.r];
-    if (st.mode == 2) {
-        g.m = st.m;
-        g.batch = vr;
-        g.a_batch = st.m * st.k;
-        g.b_batch = st.n * st.k;
-        g.c_batch = st.m * st.n;
-        g.ia = ch->d_idx + ch->ia_off[&st - steps_.data()];
-        g.ib = ch->d_idx + ch->ib_off[&st - steps_.data()];
-    } else {
-        g.m = st.m * va;  // mode 1: the variants fold into M
-        g.batch = 1;
-    }
     const uint64_t flops = st.flops_per_variant * static_cast<uint64_t>(vr);
     exec_flops_ += flops;
     if (profile_ && getenv("RCSG_DUMP_VARS") && flops > (1ull << 32))
@@ -909,8 +980,12 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     // index tables.  Repeated calls with the same groups (one call per slice
     // range) reuse everything.
     if (!tree_fixed_) {
+        // the tree is chosen for the group batch alone (slice variants would steer
+        // the local search into mixed group/slice nodes); slice batching then
+        // runs that tree with the batched slice bits as extra variants
         tree_fixed_ = true;
-        retree(groups);
+        retree(groups, false);
+        if (setup_slice_batch()) retree({}, true);
     }
     if (precision_ == RCSG_PREC_F16 && !calibrated_)
         calibrate(groups, configs.empty() ? 0 : configs[0], slice_begin);
@@ -954,7 +1029,88 @@ rcsg_plan_desc Program::stored_plan() {
 // First run: reassociate the tree for this group batch (see reassociate()),
 // then rebuild the program from the rotated steps.  RCSG_TREE=plan keeps the
 // plan's tree as given.
-void Program::retree(const std::vector<uint64_t>& groups) {
+// run-level codes: every (group, batched slice lo) combination, lo-major
+std::vector<uint64_t> Program::expand(const std::vector<uint64_t>& groups) const {
+    std::vector<uint64_t> codes;
+    codes.reserve(groups.size() << sb_bits_);
+    for (uint64_t lo = 0; lo < (uint64_t{1} << sb_bits_); ++lo)
+        for (uint64_t g : groups) codes.push_back(g | (lo << group_bits_));
+    return codes;
+}
+
+// Slice batching: sliced[0 .. b) become variant labels (code bits group_bits_ + j),
+// so one pass computes 2^b consecutive slices with the group-variant machinery.
+// b = RCSG_SLICE_BATCH (default 3), capped by the sliced count and the 64-bit code.
+bool Program::setup_slice_batch() {
+    if (!allow_slice_batch_) return false;
+    const char* env = getenv("RCSG_SLICE_BATCH");
+    int b = env ? atoi(env) : 3;
+    int n_sliced = 0;
+    for (const LabelRole& r : roles_)
+        if (r.role == kPass && r.src.kind == 1) ++n_sliced;
+    b = std::max(0, std::min({b, n_sliced, 64 - group_bits_, 10}));
+    // only "clean" sliced labels: the step contracting the label (its two legs
+    // meet) has no group-dependent operand, so batching it never turns a step
+    // into a join on shared variant bits; b = longest clean prefix sliced[0..b)
+    {
+        const int n_nodes = static_cast<int>(nodes_.size());
+        std::vector<std::vector<int>> full(n_nodes);  // all labels incl. projected ones, sorted
+        for (int i = 0; i < n_leaves_; ++i) {
+            full[i] = nodes_[i].labels0;
+            std::sort(full[i].begin(), full[i].end());
+        }
+        std::vector<int> slice_label(n_sliced, -1);
+        for (size_t l = 0; l < roles_.size(); ++l)
+            if (roles_[l].role == kPass && roles_[l].src.kind == 1) slice_label[roles_[l].src.bit] = static_cast<int>(l);
+        std::vector<char> clean(n_sliced, 1);
+        for (const StepInfo& st : steps_) {
+            std::vector<int> sh;
+            std::set_intersection(full[st.a].begin(), full[st.a].end(), full[st.b].begin(), full[st.b].end(),
+                                  std::back_inserter(sh));
+            const bool grouped = nodes_[st.a].level == 2 || nodes_[st.b].level == 2;
+            for (int j = 0; j < n_sliced; ++j)
+                if (grouped && std::binary_search(sh.begin(), sh.end(), slice_label[j])) clean[j] = 0;
+            std::set_symmetric_difference(full[st.a].begin(), full[st.a].end(), full[st.b].begin(),
+                                          full[st.b].end(), std::back_inserter(full[st.r]));
+        }
+        int c = 0;
+        while (c < b && clean[c]) ++c;
+        if (getenv("RCSG_DUMP_TREE")) {
+            fprintf(stderr, "[rcsg] clean sliced labels:");
+            for (int j = 0; j < n_sliced; ++j) fprintf(stderr, " %d", clean[j]);
+            fprintf(stderr, " -> slice batch %d bits\n", c);
+        }
+        b = c;
+    }
+    if (b == 0) return false;
+    for (LabelRole& r : roles_)
+        if (r.role == kPass && r.src.kind == 1 && r.src.bit < b) {
+            r.role = kVar;
+            r.var_bit = static_cast<int16_t>(group_bits_ + r.src.bit);
+        }
+    sb_bits_ = b;
+    return true;
+}
+
+// First run: reassociate the tree for this batch of codes (see reassociate()),
+// then rebuild the program from the rotated steps (and from the label roles,
+// when slice batching changed them).  RCSG_TREE=plan keeps the plan's tree.
+void Program::retree(const std::vector<uint64_t>& groups, bool rebuild) {
+    const uint64_t plan_flops = plan_flops_;  // stats report the plan's (reference-equivalent) FLOPs
+    auto rebuild_program = [&] {
+        const rcsg_network_desc net = stored_net();
+        const rcsg_plan_desc plan = stored_plan();
+        build_nodes(net, plan);
+        build_steps();
+        plan_flops_ = plan_flops;
+        node_exp_.assign(nodes_.size(), 0);
+        CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+    };
+    if (rebuild) {  // roles changed: rebuild on the current steps, no new rotations
+        rebuild_program();
+        return;
+    }
     const char* env = getenv("RCSG_TREE");
     if (env && std::string(env) == "plan") return;
     const int n_steps = static_cast<int>(c_steps_.size() / 3);
@@ -987,15 +1143,7 @@ void Program::retree(const std::vector<uint64_t>& groups) {
     if (!rot) return;
     c_steps_ = steps;
     step_origin_ = origin;
-    const rcsg_network_desc net = stored_net();
-    const rcsg_plan_desc plan = stored_plan();
-    const uint64_t plan_flops = plan_flops_;  // stats report the plan's (reference-equivalent) FLOPs
-    build_nodes(net, plan);
-    build_steps();
-    plan_flops_ = plan_flops;
-    node_exp_.assign(nodes_.size(), 0);
-    CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
-                       cudaMemcpyHostToDevice));
+    rebuild_program();
 }
 
 // fp16 mode: per-tensor power-of-two scales.  A transient tf32 program runs one
@@ -1016,6 +1164,8 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
         Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.4));
         cal.tree_fixed_ = true;  // the steps are already this program's (reassociated) tree
         cal.step_origin_ = step_origin_;
+        cal.sb_bits_ = sb_bits_;  // and its roles already batch these sliced labels
+        cal.group_bits_ = group_bits_;
         CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
         CUDA_OK(cudaMemset(cal.d_max_, 0, nodes_.size() * sizeof(float)));
         cal.record_max_ = true;
@@ -1046,7 +1196,9 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
     reset_graph();
 }
 
-void Program::bind_groups(const std::vector<uint64_t>& groups) {
+void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
+    const std::vector<uint64_t> groups = expand(ext_groups);
+    n_ext_groups_ = ext_groups.size();
     bound_groups_.clear();
     level0_valid_ = false;
     phase3_valid_ = false;
@@ -1111,7 +1263,7 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
     prepare_chunks(groups, cap);
     build_tasks();
     chunk_cap_ = cap;
-    bound_groups_ = groups;
+    bound_groups_ = ext_groups;
 }
 
 // One (configuration, slice) pass after set_pass: level-1 steps, then every
@@ -1127,13 +1279,20 @@ void Program::exec_pass_body(int64_t P) {
         RCSG_DISPATCH(precision_,
                       launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane,
                                          std::ldexp(1.0, node_exp_[root_]), P,
-                                         static_cast<int>(root.labels.size()), d_canon_, ch.d_vid, ch.d_groups,
-                                         static_cast<int64_t>(ch.groups.size()), d_part_, ls_));
+                                         static_cast<int>(root.labels.size()), d_canon_,
+                                         static_cast<int>(ch.fin_g.size()), ch.d_fin, ch.d_fin + ch.fin_g.size(),
+                                         ch.d_fin + 2 * ch.fin_g.size() + 1,
+                                         ch.d_fin + 2 * ch.fin_g.size() + 1 + ch.ent_vid.size(), d_state_, d_part_,
+                                         ls_));
         ++launches_;
     }
 }
 
 void Program::free_tasks() {
+    cudaFree(d_chain_);
+    cudaFree(d_chain_tab_);
+    d_chain_ = nullptr;
+    d_chain_tab_ = nullptr;
     for (cudaEvent_t e : task_ev_) cudaEventDestroy(e);
     task_ev_.clear();
     tasks_.clear();
@@ -1165,14 +1324,52 @@ void Program::build_tasks() {
         }
         return w;
     };
+    // consecutive tiny steps become one chain task (one launch, one CTA)
+    std::vector<ChainOp> chain_ops;
+    std::vector<int32_t> chain_tab;
     auto add_steps = [&](int phase, const ChunkData* ch) {
+        std::vector<const StepInfo*> run;
+        auto flush = [&] {
+            if (run.size() == 1) {
+                add({1, run[0], ch}, {node_region(run[0]->a), node_region(run[0]->b)}, {node_region(run[0]->r)});
+            } else if (!run.empty()) {
+                Task t{5, nullptr, ch};
+                t.chain_off = static_cast<int>(chain_ops.size());
+                t.chain_len = static_cast<int>(run.size());
+                std::vector<Region> r, w;
+                for (const StepInfo* st : run) {
+                    ChainOp op{step_args(*st, ch), static_cast<int32_t>(chain_tab.size()), 0};
+                    for (int64_t i = 0; i < op.g.m; ++i)
+                        chain_tab.push_back(static_cast<int32_t>(out_row_off(op.g.om, op.g.n, i)));
+                    op.col_tab = static_cast<int32_t>(chain_tab.size());
+                    for (int64_t j = 0; j < op.g.n; ++j) chain_tab.push_back(static_cast<int32_t>(out_col_off(op.g.om, j)));
+                    chain_ops.push_back(op);
+                    const int64_t vr = (nodes_[st->r].level == 2 && ch) ? ch->nvar[st->r] : 1;
+                    t.chain_flops += st->flops_per_variant * static_cast<uint64_t>(vr);
+                    r.push_back(node_region(st->a));
+                    r.push_back(node_region(st->b));
+                    w.push_back(node_region(st->r));
+                }
+                add(t, r, w);
+            }
+            run.clear();
+        };
+        // opt-in (RCSG_CHAIN=1): on cfg2 the serial one-CTA chain measured slower
+        // than the tiny steps' own launches running concurrently in the DAG
+        static const bool use_chain = getenv("RCSG_CHAIN") != nullptr;
         for (const StepInfo& st : steps_) {
             if (st.phase != phase) continue;
+            if (use_chain && chainable(st, ch)) {
+                run.push_back(&st);
+                continue;
+            }
+            flush();
             std::vector<Region> r{node_region(st.a), node_region(st.b)}, w{node_region(st.r)};
             if (st.perm_a) w.push_back({st.sa_off, st.sa_off + 2 * st.sa_plane});
             if (st.perm_b) w.push_back({st.sb_off, st.sb_off + 2 * st.sb_plane});
             add({1, &st, ch}, r, w);
         }
+        flush();
     };
     const Region part{-2, -1};  // the per-configuration accumulator
     if (!static_jobs_[1].empty()) add({0, nullptr, nullptr}, {}, leaf_regions(1));
@@ -1185,6 +1382,12 @@ void Program::build_tasks() {
         if (ch.n_leaf_jobs > ch.n_leaf_jobs3) add({2, nullptr, &ch}, {}, leaf_regions(2));
         add_steps(2, &ch);
         add({3, nullptr, &ch}, {node_region(root_)}, {part});
+    }
+    if (!chain_ops.empty()) {
+        CUDA_OK(cudaMalloc(&d_chain_, chain_ops.size() * sizeof(ChainOp)));
+        CUDA_OK(cudaMemcpy(d_chain_, chain_ops.data(), chain_ops.size() * sizeof(ChainOp), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMalloc(&d_chain_tab_, chain_tab.size() * sizeof(int32_t)));
+        CUDA_OK(cudaMemcpy(d_chain_tab_, chain_tab.data(), chain_tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     const int T = static_cast<int>(tasks_.size());
     auto overlap = [](const std::vector<Region>& x, const std::vector<Region>& y) {
@@ -1232,7 +1435,8 @@ void Program::build_tasks() {
         for (int t = 0; t < T; ++t) {
             const Task& k = tasks_[t];
             if (k.kind != 1) {
-                fprintf(stderr, "  task %3d kind %d depth %d\n", t, k.kind, depth[t]);
+                fprintf(stderr, "  task %3d kind %d depth %d%s%d\n", t, k.kind, depth[t], k.kind == 5 ? " ops " : "",
+                        k.kind == 5 ? k.chain_len : 0);
                 continue;
             }
             const StepInfo& st = *k.st;
@@ -1270,6 +1474,11 @@ void Program::run_task(const Task& t, int64_t P) {
         case 1:
             exec_step(*t.st, t.ch);
             break;
+        case 5:
+            RCSG_DISPATCH(precision_, launch_gemm_chain<S>(d_chain_ + t.chain_off, t.chain_len, d_chain_tab_, ls_));
+            ++launches_;
+            exec_flops_ += t.chain_flops;
+            break;
         case 2:
         case 4: {
             const int j0 = t.kind == 4 ? 0 : t.ch->n_leaf_jobs3;
@@ -1285,8 +1494,11 @@ void Program::run_task(const Task& t, int64_t P) {
             RCSG_DISPATCH(precision_,
                           launch_finalize<S>(static_cast<const S*>(buf(root.off)), root.plane,
                                              std::ldexp(1.0, node_exp_[root_]), P,
-                                             static_cast<int>(root.labels.size()), d_canon_, t.ch->d_vid,
-                                             t.ch->d_groups, static_cast<int64_t>(t.ch->groups.size()), d_part_, ls_));
+                                             static_cast<int>(root.labels.size()), d_canon_,
+                                             static_cast<int>(t.ch->fin_g.size()), t.ch->d_fin,
+                                             t.ch->d_fin + t.ch->fin_g.size(), t.ch->d_fin + 2 * t.ch->fin_g.size() + 1,
+                                             t.ch->d_fin + 2 * t.ch->fin_g.size() + 1 + t.ch->ent_vid.size(), d_state_,
+                                             d_part_, ls_));
             ++launches_;
         }
     }
@@ -1379,8 +1591,9 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     const std::vector<uint64_t>& cfgs = configs.empty() ? no_cfg : configs;
     // level 0 depends on no slice, configuration or group: computed once per
     // arena binding and kept (its results persist in the arena across calls)
+    const uint64_t S = uint64_t{1} << sb_bits_;  // slices per pass (batched low slice bits)
     if (!level0_valid_) {
-        launch_set_pass(d_state_, slice_begin, cfgs[0], stream_);
+        launch_set_pass(d_state_, slice_begin & ~(S - 1), cfgs[0], 0, static_cast<uint32_t>(S), stream_);
         exec_phase(0, nullptr);
         level0_valid_ = true;
     }
@@ -1391,8 +1604,12 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     for (size_t ci = 0; ci < cfgs.size(); ++ci) {
         launch_fill(d_part_, 0.0, acc_n, stream_);
         ++launches_;
-        for (uint64_t s = slice_begin; s < slice_end; ++s) {
-            launch_set_pass(d_state_, s, cfgs[ci], stream_);
+        // one pass per block of S consecutive slices; its finalisation counts only
+        // the block's slices inside [slice_begin, slice_end), in ascending order
+        for (uint64_t base = slice_begin & ~(S - 1); base < slice_end; base += S) {
+            const uint64_t lo_b = std::max(slice_begin, base) - base, lo_e = std::min(slice_end, base + S) - base;
+            launch_set_pass(d_state_, base, cfgs[ci], static_cast<uint32_t>(lo_b), static_cast<uint32_t>(lo_e),
+                            stream_);
             ++launches_;
             run_pass_body(P);
             passes += chunks_.size();

@@ -85,13 +85,13 @@ struct ChunkData {
     std::vector<int64_t> nvar;        // per node variant count
     std::vector<int32_t> idx;         // ia/ib arrays of gathered steps (concatenated)
     std::vector<int64_t> ia_off, ib_off;  // per step
-    std::vector<int32_t> groups;      // original group indices in this chunk
-    std::vector<int32_t> vid;         // root variant of each group
+    // finalisation: per output group f of this chunk, its entries (root variant,
+    // batched slice lo) in ascending lo
+    std::vector<int32_t> fin_g, fin_off, ent_vid, ent_lo;
     // device copies
     uint64_t* d_codes = nullptr;
     int32_t* d_idx = nullptr;
-    int32_t* d_groups = nullptr;
-    int32_t* d_vid = nullptr;
+    int32_t* d_fin = nullptr;  // fin_g | fin_off | ent_vid | ent_lo
     LeafJob* d_leaf_jobs = nullptr;  // phase-3 leaves first, then phase-2 leaves
     int n_leaf_jobs = 0;
     int n_leaf_jobs3 = 0;
@@ -114,6 +114,9 @@ class Program {
     void run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
              uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats, bool sync = true);
     void sync();
+    // group path: batch the low sliced labels as variant bits (set before the first run)
+    void allow_slice_batch(bool on) { allow_slice_batch_ = on; }
+    int slice_batch_bits() const { return sb_bits_; }
 
     int out_rank() const { return out_rank_; }
     void set_profile(bool on) { profile_ = on; }
@@ -123,7 +126,9 @@ class Program {
 
   private:
     void build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan);
-    void retree(const std::vector<uint64_t>& groups);
+    void retree(const std::vector<uint64_t>& codes, bool rebuild);
+    bool setup_slice_batch();
+    std::vector<uint64_t> expand(const std::vector<uint64_t>& groups) const;
     rcsg_network_desc stored_net();
     rcsg_plan_desc stored_plan();
     void build_steps();
@@ -136,9 +141,11 @@ class Program {
     // so independent steps overlap (and the captured graph keeps the DAG)
     struct Task {
         int kind;  // 0 level-1 leaf projection, 1 step, 2 / 4 chunk leaf projection (phase 2 / 3),
-                   // 3 chunk finalize
+                   // 3 chunk finalize, 5 chain of tiny steps
         const StepInfo* st;
         const ChunkData* ch;
+        int chain_off = 0, chain_len = 0;  // kind 5: a run of tiny steps, ops in d_chain_
+        uint64_t chain_flops = 0;
     };
     void build_tasks();
     void free_tasks();
@@ -152,6 +159,10 @@ class Program {
     void exec_phase(int phase, const ChunkData* ch);
     void exec_step(const StepInfo& s, const ChunkData* ch);
     void* buf(int64_t off) const;
+    GemmArgs step_args(const StepInfo& st, const ChunkData* ch) const;
+    static int product_order(uint64_t ma, uint64_t mb, int64_t va, int64_t vb, int64_t vr);
+    static constexpr int64_t kChainMacs = int64_t{1} << 12;  // complex MACs per chained step
+    bool chainable(const StepInfo& st, const ChunkData* ch) const;
     template <typename R>
     void exec_step_t(const StepInfo& s, const ChunkData* ch);
 
@@ -177,6 +188,8 @@ class Program {
     std::vector<std::vector<int>> task_wait_;  // per task: tasks on other lanes to wait for
     std::vector<int> task_lane_;
     std::vector<cudaEvent_t> task_ev_;
+    ChainOp* d_chain_ = nullptr;      // device op lists of the chain tasks
+    int32_t* d_chain_tab_ = nullptr;  // their output-offset tables
     std::vector<cudaStream_t> lanes_;
     std::vector<cudaEvent_t> lane_ev_;  // fork (index 0) and per-lane join events
     int n_lanes_used_ = 0;
@@ -197,6 +210,10 @@ class Program {
     std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
     // batch-aware reassociation: done once, at the first run (group codes known)
     bool tree_fixed_ = false;
+    bool allow_slice_batch_ = false;
+    int sb_bits_ = 0;       // batched sliced labels: sliced[0 .. sb_bits_) are variant bits
+    int group_bits_ = 0;    // group-code width; batched slice bit j is code bit group_bits_ + j
+    size_t n_ext_groups_ = 0;  // caller's group count of the current binding
     bool level0_valid_ = false;  // level-0 (constant) results live in the arena
     bool phase3_valid_ = false;  // single chunk: its group-only (phase-3) results live in the arena
     bool fault_pending_ = false; // async runs whose fault flag is not checked yet

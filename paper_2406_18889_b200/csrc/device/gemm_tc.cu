@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             int64_t row_off;
             if (!p.om.scatter) row_off = row * p.n;
             else if (split_rows)
-                row_off = ((static_cast<int64_t>(c.m0) >> p.om.m_bits) << (p.om.m_bits + p.om.n_bits)) +
+                row_off = (static_cast<int64_t>(c.m0) >> p.om.m_bits) * out_row_vstride(p.om) +
                           warp_scatter(p.om.m_pos, p.om.m_bits, 7, c.m0, lane) + lane_off;
             else row_off = row < p.m ? out_row_off(p.om, p.n, row) : 0;
             mbar_wait(&tfull[ab], (j / NBUF) & 1);
@@ -660,7 +660,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll 1
             for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
                 const int64_t col0 = c.n0 + c0;  // multiple of 32
-                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, 5, col0, lane) : col0;
+                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, 5, col0, lane) +
+                                                            (col0 >> p.om.n_bits) * p.om.n_vstride
+                                                      : col0;
                 float x[32];
                 tmem_ld32(base + c0, x);
                 if constexpr (sizeof(E) == 2) {

@@ -252,6 +252,81 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
     if (sk.splits > 1) launch_splitk_reduce<S>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
 }
 
+// ------------------------------------------------------------------ chain
+template <typename S>
+__global__ void __launch_bounds__(1024) gemm_chain_kernel(const ChainOp* __restrict__ ops, int n_ops,
+                                                          const int32_t* __restrict__ tab) {
+    using R = typename Acc<S>::T;
+    __shared__ ChainOp buf[2];  // op o in buf[o & 1]; thread 0 fetches op o + 1 meanwhile
+    if (threadIdx.x == 0) buf[0] = ops[0];
+    __syncthreads();
+    for (int o = 0; o < n_ops; ++o) {
+        if (threadIdx.x == 0 && o + 1 < n_ops) buf[(o + 1) & 1] = ops[o + 1];
+        const GemmArgs& g = buf[o & 1].g;
+        const int32_t* row_tab = tab + buf[o & 1].row_tab;
+        const int32_t* col_tab = tab + buf[o & 1].col_tab;
+        const int m = static_cast<int>(g.m), n = static_cast<int>(g.n), k = static_cast<int>(g.k);
+        const S* A = static_cast<const S*>(g.a);
+        const S* B = static_cast<const S*>(g.b);
+        S* Cm = static_cast<S*>(g.c);
+        const R sc = pow2<R>(g.scale_exp);
+        const int mn = m * n;
+        const int total = mn * static_cast<int>(g.batch);
+        bool bad = false;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+            const int v = g.batch > 1 ? e / mn : 0, r = e - v * mn, i = r / n, j = r - i * n;
+            const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
+            const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
+            const S* a = A + av * g.a_batch + static_cast<int64_t>(i) * k;
+            const S* b = B + bv * g.b_batch + static_cast<int64_t>(j) * k;
+            R re = 0, im = 0;
+            int kk = 0;
+            for (; kk + 4 <= k; kk += 4) {  // loads first, then the k-ascending FMAs
+                R ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    ar[u] = load_c(a + kk + u);
+                    ai[u] = load_c(a + g.a_plane + kk + u);
+                    br[u] = load_c(b + kk + u);
+                    bi[u] = load_c(b + g.b_plane + kk + u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    re = fma(ar[u], br[u], re);
+                    re = fma(-ai[u], bi[u], re);
+                    im = fma(ar[u], bi[u], im);
+                    im = fma(ai[u], br[u], im);
+                }
+            }
+            for (; kk < k; ++kk) {
+                const R ar = load_c(a + kk), ai = load_c(a + g.a_plane + kk);
+                const R br = load_c(b + kk), bi = load_c(b + g.b_plane + kk);
+                re = fma(ar, br, re);
+                re = fma(-ai, bi, re);
+                im = fma(ar, bi, im);
+                im = fma(ai, br, im);
+            }
+            const int64_t off = v * g.c_batch + row_tab[i] + col_tab[j];
+            re *= sc;
+            im *= sc;
+            store_c(Cm + off, re);
+            store_c(Cm + g.c_plane + off, im);
+            bad |= unstorable<S>(re) || unstorable<S>(im);
+        }
+        if (bad && g.fault) atomicMin(g.fault, g.step);
+        __syncthreads();  // this op's outputs (and the next op's descriptor) are visible
+    }
+}
+
+template <typename S>
+void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st) {
+    if (n_ops > 0) gemm_chain_kernel<S><<<1, 1024, 0, st>>>(ops, n_ops, tab);
+}
+template void launch_gemm_chain<float>(const ChainOp*, int, const int32_t*, cudaStream_t);
+template void launch_gemm_chain<double>(const ChainOp*, int, const int32_t*, cudaStream_t);
+template void launch_gemm_chain<bf16>(const ChainOp*, int, const int32_t*, cudaStream_t);
+template void launch_gemm_chain<f16>(const ChainOp*, int, const int32_t*, cudaStream_t);
+
 void* device_workspace(size_t bytes, cudaStream_t st) {
     // one growing scratch buffer per stream (launches on a stream are ordered)
     static std::map<cudaStream_t, std::pair<void*, size_t>> pool;
@@ -277,42 +352,52 @@ template void launch_gemm_simt<f16>(const GemmArgs&, cudaStream_t);
 // ------------------------------------------------------------------ finalize
 template <typename R>
 __global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, double root_scale, int64_t payload,
-                                int rank, const int32_t* __restrict__ src_bit,
-                                const int32_t* __restrict__ vid, const int32_t* __restrict__ gidx,
-                                int64_t n_groups, double* __restrict__ acc) {
-    const int64_t total = n_groups * payload;
+                                int rank, const int32_t* __restrict__ src_bit, int n_fin,
+                                const int32_t* __restrict__ fin_g, const int32_t* __restrict__ fin_off,
+                                const int32_t* __restrict__ ent_vid, const int32_t* __restrict__ ent_lo,
+                                const PassState* __restrict__ state, double* __restrict__ acc) {
+    const int64_t total = n_fin * payload;
+    const uint32_t lo_b = state->lo_begin, lo_e = state->lo_end;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t gl = t / payload;
-        const int64_t i = t - gl * payload;
+        const int64_t f = t / payload;
+        const int64_t i = t - f * payload;
         int64_t p = 0;
         for (int j = 0; j < rank; ++j) p |= ((i >> j) & 1) << src_bit[j];
-        const int64_t v = vid ? vid[gl] : 0;
-        const int64_t o = v * payload + p;
-        const int64_t g = gidx ? gidx[gl] : gl;
-        acc[2 * (g * payload + i)] += static_cast<double>(load_c(root + o)) * root_scale;
-        acc[2 * (g * payload + i) + 1] += static_cast<double>(load_c(root + root_plane + o)) * root_scale;
+        const int64_t g = fin_g[f];
+        double re = acc[2 * (g * payload + i)], im = acc[2 * (g * payload + i) + 1];
+        for (int e = fin_off[f]; e < fin_off[f + 1]; ++e) {  // slices ascending
+            const uint32_t lo = static_cast<uint32_t>(ent_lo[e]);
+            if (lo < lo_b || lo >= lo_e) continue;
+            const int64_t o = static_cast<int64_t>(ent_vid[e]) * payload + p;
+            re += static_cast<double>(load_c(root + o)) * root_scale;
+            im += static_cast<double>(load_c(root + root_plane + o)) * root_scale;
+        }
+        acc[2 * (g * payload + i)] = re;
+        acc[2 * (g * payload + i) + 1] = im;
     }
 }
 
 template <typename R>
 void launch_finalize(const R* root, int64_t root_plane, double root_scale, int64_t payload, int rank,
-                     const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
-                     const int32_t* d_gidx, int64_t n_groups_chunk, double* acc, cudaStream_t st) {
-    const int64_t total = n_groups_chunk * payload;
+                     const int32_t* d_src_bit_of_canon, int n_fin, const int32_t* d_fin_g, const int32_t* d_fin_off,
+                     const int32_t* d_ent_vid, const int32_t* d_ent_lo, const PassState* d_state, double* acc,
+                     cudaStream_t st) {
+    const int64_t total = n_fin * payload;
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, grid_cap()));
     finalize_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(root, root_plane, root_scale, payload, rank,
-                                                          d_src_bit_of_canon, d_vid, d_gidx,
-                                                          n_groups_chunk, acc);
+                                                          d_src_bit_of_canon, n_fin, d_fin_g, d_fin_off, d_ent_vid,
+                                                          d_ent_lo, d_state, acc);
 }
-template void launch_finalize<float>(const float*, int64_t, double, int64_t, int, const int32_t*,
-                                     const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
-template void launch_finalize<double>(const double*, int64_t, double, int64_t, int, const int32_t*,
-                                      const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
-template void launch_finalize<bf16>(const bf16*, int64_t, double, int64_t, int, const int32_t*,
-                                    const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
-template void launch_finalize<f16>(const f16*, int64_t, double, int64_t, int, const int32_t*,
-                                   const int32_t*, const int32_t*, int64_t, double*, cudaStream_t);
+#define RCSG_FIN(R)                                                                                               \
+    template void launch_finalize<R>(const R*, int64_t, double, int64_t, int, const int32_t*, int, const int32_t*, \
+                                     const int32_t*, const int32_t*, const int32_t*, const PassState*, double*,    \
+                                     cudaStream_t);
+RCSG_FIN(float)
+RCSG_FIN(double)
+RCSG_FIN(bf16)
+RCSG_FIN(f16)
+#undef RCSG_FIN
 
 // ------------------------------------------------------------------ misc
 __global__ void kahan_kernel(double* res, double* comp, const double* part, int64_t n) {
@@ -352,12 +437,15 @@ void launch_fill(double* p, double v, int64_t n, cudaStream_t st) {
     fill_kernel<<<std::max(grid, 1), 256, 0, st>>>(p, v, n);
 }
 
-__global__ void set_pass_kernel(PassState* s, uint64_t slice, uint64_t config) {
+__global__ void set_pass_kernel(PassState* s, uint64_t slice, uint64_t config, uint32_t lo_begin, uint32_t lo_end) {
     s->slice = slice;
     s->config = config;
+    s->lo_begin = lo_begin;
+    s->lo_end = lo_end;
 }
-void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, cudaStream_t st) {
-    set_pass_kernel<<<1, 1, 0, st>>>(d_state, slice, config);
+void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, uint32_t lo_begin, uint32_t lo_end,
+                     cudaStream_t st) {
+    set_pass_kernel<<<1, 1, 0, st>>>(d_state, slice, config, lo_begin, lo_end);
 }
 
 }  // namespace rcsg

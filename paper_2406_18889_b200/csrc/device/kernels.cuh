@@ -71,8 +71,9 @@ struct LeafJob {
 };
 
 struct PassState {
-    uint64_t slice;        // current slice index (bit b <-> sliced[b])
+    uint64_t slice;        // current slice index (bit b <-> sliced[b]); batched low bits are 0
     uint64_t config;       // current broken-edge configuration bits
+    uint32_t lo_begin, lo_end;  // batched slices of this pass that count: slice + [lo_begin, lo_end)
 };
 
 // Pass-label source table: for a pass label, where its value comes from.
@@ -110,14 +111,18 @@ void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, in
                     const PermuteDesc& d, cudaStream_t st);
 
 // ---- GEMM output scatter map.  scatter == 0: row-major C.  Otherwise element
-// (row m, column n) of a variant block lands at
-//   (m >> m_bits) * 2^(m_bits+n_bits) + sum_j bit_j(m) << m_pos[j] + sum_j bit_j(n) << n_pos[j]
-// i.e. directly in the layout the consumer step reads (no separate permute).
+// (row m, column n) lands at
+//   (m >> m_bits) * m_vstride + (n >> n_bits) * n_vstride
+//     + sum_j bit_j(m) << m_pos[j] + sum_j bit_j(n) << n_pos[j]
+// i.e. directly in the layout the consumer step reads (no separate permute);
+// the high row / column index parts are variants folded into M / N
+// (m_vstride = 0 means the dense block stride 2^(m_bits+n_bits)).
 struct OutMap {
     int32_t scatter;
     int32_t m_bits, n_bits;
     int8_t m_pos[kMaxRank];
     int8_t n_pos[kMaxRank];
+    int64_t m_vstride, n_vstride;
 };
 __host__ __device__ __forceinline__ int64_t scatter_bits(const int8_t* pos, int bits, int64_t x) {
     int64_t o = 0;
@@ -125,13 +130,17 @@ __host__ __device__ __forceinline__ int64_t scatter_bits(const int8_t* pos, int 
     return o;
 }
 // row part / column part of the output offset (additive: offset = row_off + col_off)
+__host__ __device__ __forceinline__ int64_t out_row_vstride(const OutMap& om) {
+    return om.m_vstride ? om.m_vstride : (int64_t{1} << (om.m_bits + om.n_bits));
+}
 __host__ __device__ __forceinline__ int64_t out_row_off(const OutMap& om, int64_t n_cols, int64_t m) {
     if (!om.scatter) return m * n_cols;
-    return ((m >> om.m_bits) << (om.m_bits + om.n_bits)) +
+    return (m >> om.m_bits) * out_row_vstride(om) +
            scatter_bits(om.m_pos, om.m_bits, m & ((int64_t{1} << om.m_bits) - 1));
 }
 __host__ __device__ __forceinline__ int64_t out_col_off(const OutMap& om, int64_t n) {
-    return om.scatter ? scatter_bits(om.n_pos, om.n_bits, n) : n;
+    if (!om.scatter) return n;
+    return (n >> om.n_bits) * om.n_vstride + scatter_bits(om.n_pos, om.n_bits, n & ((int64_t{1} << om.n_bits) - 1));
 }
 
 // ---- complex GEMM, both operands K-contiguous ("TN"):
@@ -175,6 +184,17 @@ template <typename S>
 void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int splits, const GemmArgs& g,
                           cudaStream_t st);
 
+// A run of tiny GEMM steps executed back to back by one CTA (each would be a
+// latency-bound launch of its own); per op the semantics of gemm_simt_kernel.
+// ops: DEVICE array; tab: DEVICE int32 output offsets (row_tab / col_tab of
+// each op index into it).  Every op: batch * m * n * k < 2^31, offsets < 2^31.
+struct ChainOp {
+    GemmArgs g;
+    int32_t row_tab, col_tab;  // offsets into the table array: m row offsets, n column offsets
+};
+template <typename S>
+void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st);
+
 // Scratch buffer for split-K partials, one per stream (grown on demand).
 void* device_workspace(size_t bytes, cudaStream_t st);
 
@@ -184,10 +204,12 @@ bool gemm_tc_supported(const GemmArgs& g);
 void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st);
 
 // ---- finalize a pass: acc[g][i] += root[vid[g]][perm(i)]   (acc: double interleaved)
+// acc[fin_g[f]][i] += sum over entries e of f (ascending batched slice lo, only
+// lo in the pass's [lo_begin, lo_end)) of root[ent_vid[e]][perm(i)] * scale
 template <typename R>
 void launch_finalize(const R* root, int64_t root_plane, double root_scale, int64_t payload, int rank,
-                     const int32_t* d_src_bit_of_canon, const int32_t* d_vid,
-                     const int32_t* d_gidx, int64_t n_groups_chunk, double* acc,
+                     const int32_t* d_src_bit_of_canon, int n_fin, const int32_t* d_fin_g, const int32_t* d_fin_off,
+                     const int32_t* d_ent_vid, const int32_t* d_ent_lo, const PassState* d_state, double* acc,
                      cudaStream_t st);
 
 // max |value| over both planes of a float buffer (atomicMax into *out; calibration)
@@ -196,6 +218,7 @@ void launch_maxabs(const float* buf, int64_t plane, int64_t count, float* out, c
 // compensated accumulation in configuration order (contraction_engine.cpp:289-302)
 void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t st);
-void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, cudaStream_t st);
+void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, uint32_t lo_begin, uint32_t lo_end,
+                     cudaStream_t st);
 
 }  // namespace rcsg
