@@ -290,6 +290,37 @@ def main():
     peak_note = (f"tf32 dense = 1/2 of {peak_kind} bf16 {bf16_peak:.1f} TF/s" if args.precision == "tf32"
                  else f"{peak_kind} dense bf16/fp16 peak {bf16_peak:.1f} TF/s")
 
+    # roofline of the dominant kernel: the longest launch of the profiled pass,
+    # bound by its arithmetic intensity (algorithmic FLOPs / algorithmic bytes)
+    classes = {0: "SIMT GEMM", 1: "tcgen05 GEMM (gemm_tc_persistent / gemm_tc_kernel)", 2: "permute", 3: "GEMV"}
+    top_s = pst.top_ms * 1e-3
+    ai = pst.top_flops / pst.top_bytes if pst.top_bytes else float("inf")
+    ridge = tc_peak * 1e12 / (hbm_peak * 1e9)
+    if ai >= ridge:
+        bound, ach, peak, unit = "tensor", pst.top_flops / top_s / 1e12, tc_peak, "TFLOP/s"
+        pnote = peak_note
+        algo = pst.top_flops
+    else:
+        bound, ach, peak, unit = "hbm", pst.top_bytes / top_s / 1e9, hbm_peak, "GB/s"
+        pnote = f"{peak_kind} HBM copy bandwidth {hbm_peak:.1f} GB/s"
+        algo = pst.top_bytes
+    traffic = None
+    try:  # dram read + write of this launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "top_kernel_traffic.json")) as f:
+            tk = json.load(f)
+        if int(tk.get("plan_step", -1)) == int(pst.top_step) and tk.get("precision") == args.precision:
+            traffic = int(tk["dram_bytes"])
+    except Exception:
+        pass
+    roofline = {"bound": bound, "kernel": f"plan step {pst.top_step}: {classes.get(int(pst.top_class), '?')}",
+                "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": traffic,
+                "algorithmic_per_launch": algo, "launch_ms": pst.top_ms, "flops": pst.top_flops,
+                "bytes": pst.top_bytes, "intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
+                "peak_note": pnote,
+                "share_of_step": pst.top_ms * S / pst.device_ms if pst.device_ms else None,  # profiled call = S passes
+                "all_tensor_core_launches": {"achieved_tflops": tc_tflops, "frac_of_tensor_peak": tc_tflops / tc_peak,
+                                             "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None}}
+
     # end-to-end through the public API with host buffers (rank 0 work pattern on each rank)
     e2e = None
     if not args.no_e2e:
@@ -344,13 +375,7 @@ def main():
             "complex_tflops_executed": exec_flops * world / (ms_max * 1e-3) / 1e12,
             "complex_tflops_reference_equivalent": plan_flops * world / (ms_max * 1e-3) / 1e12,
             "gpu_launches": int(st.kernel_launches),
-            "roofline": {"bound": "tensor",
-                         "kernel": "gemm_tc_kernel/gemm_tc_persistent (tcgen05 " +
-                                   ("kind::tf32" if args.precision == "tf32" else "kind::f16") + ", 4M complex)",
-                         "achieved": tc_tflops, "peak": tc_peak, "unit": "TFLOP/s", "frac": tc_tflops / tc_peak,
-                         "traffic": None,
-                         "peak_note": peak_note,
-                         "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None},
+            "roofline": roofline,
             "kernel_breakdown_ms": {"per": f"one profiled pass of {S} slices (serialised launches)",
                                     "step": pst.device_ms, "gemm_tc": pst.gemm_tc_ms,
                                     "gemm_other": pst.gemm_ms - pst.gemm_tc_ms, "permute": pst.permute_ms,

@@ -88,6 +88,15 @@ typedef struct rcsg_stats {
     double permute_ms;         /* bit-permutation launches */
     uint64_t permute_bytes;    /* bytes read + written by permutes */
     uint64_t gemm_tc_launches;
+    /* the single longest launch of the profiled run (roofline of the dominant
+     * kernel): its time, algorithmic FLOPs and bytes (operands read once +
+     * result written once, at storage precision), plan step and kernel class
+     * (0 SIMT GEMM, 1 tensor-core GEMM, 2 permute, 3 GEMV) */
+    double top_ms;
+    uint64_t top_flops;
+    uint64_t top_bytes;
+    int64_t top_step;
+    int64_t top_class;
 } rcsg_stats;
 
 typedef struct rcsg_program rcsg_program;

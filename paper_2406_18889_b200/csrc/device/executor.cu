@@ -857,6 +857,10 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         fprintf(stderr, "[rcsg] step %d mode %d va %lld vb %lld vr %lld m %lld n %lld k %lld\n", st.plan_index, st.mode,
                 (long long)va, (long long)vb, (long long)vr, (long long)st.m, (long long)st.n, (long long)st.k);
     const int mk = mark_begin();
+    if (mk >= 0) {  // algorithmic bytes: every operand variant read once, the result written once
+        const int64_t eb = 2 * elem_bytes_;
+        marks_[mk].bytes = static_cast<uint64_t>(eb * (va * st.m * st.k + vb * st.n * st.k + vr * st.m * st.n));
+    }
     if (gemm_smallk_supported(g)) {
         launch_gemm_smallk<R>(g, ls_);
         mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
@@ -901,7 +905,8 @@ int Program::mark_begin() {
 void Program::mark_end(int idx, int cat, uint64_t work, int step, int64_t m, int64_t n, int64_t k,
                        int64_t batch) {
     if (idx < 0) return;
-    marks_[idx] = {cat, work, step, m, n, k, batch};
+    const uint64_t bytes = marks_[idx].bytes;
+    marks_[idx] = {cat, work, step, m, n, k, batch, bytes};
     CUDA_OK(cudaEventRecord(ev_pool_[2 * idx + 1], ls_));
 }
 
@@ -924,6 +929,13 @@ void Program::collect_marks(rcsg_stats* stats) {
         if (m.cat == kCatPermute) {
             stats->permute_ms += ms;
             stats->permute_bytes += m.work;
+        }
+        if (ms > stats->top_ms) {
+            stats->top_ms = ms;
+            stats->top_flops = m.cat == kCatPermute ? 0 : m.work;
+            stats->top_bytes = m.cat == kCatPermute ? m.work : m.bytes;
+            stats->top_step = m.step;
+            stats->top_class = m.cat;
         }
     }
     if (env) {

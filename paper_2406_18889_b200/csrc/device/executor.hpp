@@ -242,6 +242,7 @@ class Program {
         uint64_t work;
         int step;  // program step index
         int64_t m, n, k, batch;
+        uint64_t bytes = 0;  // algorithmic bytes (operands + result)
     };
     bool profile_ = false;
     std::vector<cudaEvent_t> ev_pool_;
