@@ -337,7 +337,7 @@ def main():
         if world > 1:
             tt = torch.tensor([t1 - t0], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * K / float(tt.item())
+            e2e["value"] = world * K * S / float(tt.item())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
