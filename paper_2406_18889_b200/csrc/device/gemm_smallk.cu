@@ -15,6 +15,7 @@ constexpr int kRows = 64;  // output rows per CTA
 
 template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     const R sc = pow2<R>(g.scale_exp);
     __shared__ R a_re[kRows][K], a_im[kRows][K];
@@ -79,6 +80,7 @@ constexpr int kColTile = 64;
 
 template <typename S, int K>
 __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     const R sc = pow2<R>(g.scale_exp);
     __shared__ R b_re[kColTile][K], b_im[kColTile][K];
@@ -140,13 +142,13 @@ void launch_k(const GemmArgs& g, cudaStream_t st) {
     if (g.om.scatter && g.om.m_bits >= 5 && g.om.m_pos[0] == 0 && g.om.m_pos[1] == 1) {
         const int64_t tiles = g.batch * ((g.m + kThreads - 1) / kThreads) * ((g.n + kColTile - 1) / kColTile);
         const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
-        smallk_rows_kernel<R, K><<<std::max(grid, 1), kThreads, 0, st>>>(g);
+        launch_pdl(smallk_rows_kernel<R, K>, dim3(std::max(grid, 1)), dim3(kThreads), 0, st, g);
         return;
     }
     const int nb = static_cast<int>(std::min<int64_t>(g.n, kThreads));
     const int64_t tiles = g.batch * ((g.m + kRows - 1) / kRows) * ((g.n + nb - 1) / nb);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
-    smallk_kernel<R, K><<<std::max(grid, 1), kThreads, 0, st>>>(g, nb);
+    launch_pdl(smallk_kernel<R, K>, dim3(std::max(grid, 1)), dim3(kThreads), 0, st, g, nb);
 }
 
 }  // namespace

@@ -40,6 +40,7 @@ template <typename S>
 __global__ void __launch_bounds__(kWarps * 32)
     gemv_kernel(const GemmArgs g, int64_t rows, int shorts, int long_is_a, int64_t k_chunk, int splits,
                 typename Acc<S>::T* ws, int64_t ws_split) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     using V = typename Vec16<S>::T;
     constexpr int kVec = sizeof(V) / sizeof(S);
@@ -150,7 +151,7 @@ void launch_gemv(const GemmArgs& g, cudaStream_t st) {
     }
     const int64_t warps = g.batch * rows * splits;
     const int grid = static_cast<int>(std::min<int64_t>((warps + kWarps - 1) / kWarps, 148 * 64));
-    gemv_kernel<S><<<grid, kWarps * 32, 0, st>>>(g, rows, shorts, long_is_a ? 1 : 0, k_chunk, splits, ws, ws_split);
+    launch_pdl(gemv_kernel<S>, dim3(grid), dim3(kWarps * 32), 0, st, g, rows, shorts, long_is_a ? 1 : 0, k_chunk, splits, ws, ws_split);
     if (splits > 1) launch_splitk_reduce<S>(ws, ws_split, splits, g, st);
 }
 template void launch_gemv<float>(const GemmArgs&, cudaStream_t);

@@ -22,6 +22,7 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
                                     const uint64_t* __restrict__ codes,
                                     const PassSrc* __restrict__ pass_src,
                                     const PassState* __restrict__ state, R* __restrict__ arena) {
+    pdl_enter();
     const LeafJob j = jobs[blockIdx.x];
     const PassState ps = *state;
     // bits fixed by pass labels, and per-free-position source bit
@@ -66,8 +67,8 @@ void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf
                          const uint64_t* d_codes, const PassSrc* d_pass_src,
                          const PassState* d_state, R* arena, cudaStream_t st) {
     if (n_jobs == 0) return;
-    leaf_project_kernel<R><<<n_jobs, 64, 0, st>>>(d_jobs, d_leaf_data, d_codes, d_pass_src,
-                                                   d_state, arena);
+    launch_pdl(leaf_project_kernel<R>, dim3(n_jobs), dim3(64), 0, st, d_jobs, d_leaf_data, d_codes, d_pass_src,
+               d_state, arena);
 }
 template void launch_leaf_project<float>(const LeafJob*, int, const double*, const uint64_t*,
                                          const PassSrc*, const PassState*, float*, cudaStream_t);
@@ -93,6 +94,7 @@ struct SplitK {
 
 template <typename S>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const SplitK sk) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     __shared__ R As_re[BK][BM + 1], As_im[BK][BM + 1];
     __shared__ R Bs_re[BK][BN + 1], Bs_im[BK][BN + 1];
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
 template <typename S>
 __global__ void splitk_reduce_kernel(const typename Acc<S>::T* __restrict__ ws, int64_t ws_split, int splits,
                                      const GemmArgs g) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     const int64_t mn = g.m * g.n, per_plane = g.batch * mn;
     const R sc = pow2<R>(g.scale_exp);
@@ -227,7 +230,7 @@ void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int sp
                           cudaStream_t st) {
     const int64_t per_plane = g.batch * g.m * g.n;
     const int grid = static_cast<int>(std::min<int64_t>((per_plane + 255) / 256, 148 * 16));
-    splitk_reduce_kernel<S><<<std::max(grid, 1), 256, 0, st>>>(ws, ws_split, splits, g);
+    launch_pdl(splitk_reduce_kernel<S>, dim3(std::max(grid, 1)), dim3(256), 0, st, ws, ws_split, splits, g);
 }
 template void launch_splitk_reduce<float>(const float*, int64_t, int, const GemmArgs&, cudaStream_t);
 template void launch_splitk_reduce<double>(const double*, int64_t, int, const GemmArgs&, cudaStream_t);
@@ -248,7 +251,7 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
         sk.ws = device_workspace(static_cast<size_t>(sk.splits) * sk.ws_split * sizeof(R), st);
     }
     const int grid = static_cast<int>(std::min<int64_t>(tiles * sk.splits, 148 * 32));
-    gemm_simt_kernel<S><<<grid, block, 0, st>>>(g, sk);
+    launch_pdl(gemm_simt_kernel<S>, dim3(grid), block, 0, st, g, sk);
     if (sk.splits > 1) launch_splitk_reduce<S>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
 }
 
@@ -256,6 +259,7 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
 template <typename S>
 __global__ void __launch_bounds__(1024) gemm_chain_kernel(const ChainOp* __restrict__ ops, int n_ops,
                                                           const int32_t* __restrict__ tab) {
+    pdl_enter();
     using R = typename Acc<S>::T;
     __shared__ ChainOp buf[2];  // op o in buf[o & 1]; thread 0 fetches op o + 1 meanwhile
     if (threadIdx.x == 0) buf[0] = ops[0];
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(1024) gemm_chain_kernel(const ChainOp* __restr
 
 template <typename S>
 void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st) {
-    if (n_ops > 0) gemm_chain_kernel<S><<<1, 1024, 0, st>>>(ops, n_ops, tab);
+    if (n_ops > 0) launch_pdl(gemm_chain_kernel<S>, dim3(1), dim3(1024), 0, st, ops, n_ops, tab);
 }
 template void launch_gemm_chain<float>(const ChainOp*, int, const int32_t*, cudaStream_t);
 template void launch_gemm_chain<double>(const ChainOp*, int, const int32_t*, cudaStream_t);
@@ -356,6 +360,7 @@ __global__ void finalize_kernel(const R* __restrict__ root, int64_t root_plane, 
                                 const int32_t* __restrict__ fin_g, const int32_t* __restrict__ fin_off,
                                 const int32_t* __restrict__ ent_vid, const int32_t* __restrict__ ent_lo,
                                 const PassState* __restrict__ state, double* __restrict__ acc) {
+    pdl_enter();
     const int64_t total = n_fin * payload;
     const uint32_t lo_b = state->lo_begin, lo_e = state->lo_end;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -385,9 +390,8 @@ void launch_finalize(const R* root, int64_t root_plane, double root_scale, int64
                      cudaStream_t st) {
     const int64_t total = n_fin * payload;
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, grid_cap()));
-    finalize_kernel<R><<<std::max(grid, 1), 256, 0, st>>>(root, root_plane, root_scale, payload, rank,
-                                                          d_src_bit_of_canon, n_fin, d_fin_g, d_fin_off, d_ent_vid,
-                                                          d_ent_lo, d_state, acc);
+    launch_pdl(finalize_kernel<R>, dim3(std::max(grid, 1)), dim3(256), 0, st, root, root_plane, root_scale, payload,
+               rank, d_src_bit_of_canon, n_fin, d_fin_g, d_fin_off, d_ent_vid, d_ent_lo, d_state, acc);
 }
 #define RCSG_FIN(R)                                                                                               \
     template void launch_finalize<R>(const R*, int64_t, double, int64_t, int, const int32_t*, int, const int32_t*, \
@@ -401,6 +405,7 @@ RCSG_FIN(f16)
 
 // ------------------------------------------------------------------ misc
 __global__ void kahan_kernel(double* res, double* comp, const double* part, int64_t n) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double y = part[i] - comp[i];
@@ -411,10 +416,11 @@ __global__ void kahan_kernel(double* res, double* comp, const double* part, int6
 }
 void launch_kahan(double* res, double* comp, const double* part, int64_t n, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, grid_cap()));
-    kahan_kernel<<<std::max(grid, 1), 256, 0, st>>>(res, comp, part, n);
+    launch_pdl(kahan_kernel, dim3(std::max(grid, 1)), dim3(256), 0, st, res, comp, part, n);
 }
 
 __global__ void maxabs_kernel(const float* buf, int64_t plane, int64_t count, float* out) {
+    pdl_enter();
     float m = 0.f;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -424,20 +430,22 @@ __global__ void maxabs_kernel(const float* buf, int64_t plane, int64_t count, fl
 }
 void launch_maxabs(const float* buf, int64_t plane, int64_t count, float* out, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((count + 255) / 256, grid_cap()));
-    maxabs_kernel<<<std::max(grid, 1), 256, 0, st>>>(buf, plane, count, out);
+    launch_pdl(maxabs_kernel, dim3(std::max(grid, 1)), dim3(256), 0, st, buf, plane, count, out);
 }
 
 __global__ void fill_kernel(double* p, double v, int64_t n) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         p[i] = v;
 }
 void launch_fill(double* p, double v, int64_t n, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, grid_cap()));
-    fill_kernel<<<std::max(grid, 1), 256, 0, st>>>(p, v, n);
+    launch_pdl(fill_kernel, dim3(std::max(grid, 1)), dim3(256), 0, st, p, v, n);
 }
 
 __global__ void set_pass_kernel(PassState* s, uint64_t slice, uint64_t config, uint32_t lo_begin, uint32_t lo_end) {
+    pdl_enter();
     s->slice = slice;
     s->config = config;
     s->lo_begin = lo_begin;
@@ -445,7 +453,7 @@ __global__ void set_pass_kernel(PassState* s, uint64_t slice, uint64_t config, u
 }
 void launch_set_pass(PassState* d_state, uint64_t slice, uint64_t config, uint32_t lo_begin, uint32_t lo_end,
                      cudaStream_t st) {
-    set_pass_kernel<<<1, 1, 0, st>>>(d_state, slice, config, lo_begin, lo_end);
+    launch_pdl(set_pass_kernel, dim3(1), dim3(1), 0, st, d_state, slice, config, lo_begin, lo_end);
 }
 
 }  // namespace rcsg

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 
 namespace rcsg {
 
@@ -109,6 +110,34 @@ PermuteDesc make_permute(int rank, const int* src_bit);
 template <typename R>
 void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, int64_t n_var,
                     const PermuteDesc& d, cudaStream_t st);
+
+// ---- programmatic dependent launch (PDL).  Every kernel of a pass is launched
+// with programmatic stream serialization; it waits (griddepcontrol.wait) for
+// its predecessor's grid to complete -- and its memory to be visible -- before
+// touching global memory, and triggers its own dependents at entry, so the
+// next kernel's launch and prologue overlap this one's tail.  (The dependent
+// launches only once every CTA of this grid has started.)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- GEMM output scatter map.  scatter == 0: row-major C.  Otherwise element
 // (row m, column n) lands at

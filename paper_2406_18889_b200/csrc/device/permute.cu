@@ -125,6 +125,7 @@ template <typename R>
 __global__ void __launch_bounds__(kThreads) permute_kernel(const R* __restrict__ in, int64_t in_plane,
                                                            R* __restrict__ out, int64_t out_plane, int64_t n_var,
                                                            const PermuteDesc d) {
+    pdl_enter();
     using V = typename Vec<R>::T;
     constexpr int VN = Vec<R>::N;
     __shared__ int32_t in_lo[32], in_hi[64], out_lo[32], out_hi[64], e_lo[32], e_hi[64];
@@ -211,7 +212,7 @@ void launch_permute(const R* in, int64_t in_plane, R* out, int64_t out_plane, in
     const int64_t total = (int64_t{1} << d.n_outer) * n_var;
     const int grid = static_cast<int>(std::min<int64_t>(total, 148 * 8));
     const size_t smem = 2 * (size_t{1} << kPermTileBits) * sizeof(R);
-    permute_kernel<R><<<grid, kThreads, smem, st>>>(in, in_plane, out, out_plane, n_var, d);
+    launch_pdl(permute_kernel<R>, dim3(grid), dim3(kThreads), smem, st, in, in_plane, out, out_plane, n_var, d);
 }
 template void launch_permute<float>(const float*, int64_t, float*, int64_t, int64_t, const PermuteDesc&,
                                     cudaStream_t);
