@@ -319,6 +319,8 @@ Program::~Program() {
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     free_tasks();
+    for (void* t : tab_mem_) cudaFree(t);
+    cudaFree(d_tab_jobs_);
     for (cudaEvent_t e : lane_ev_) cudaEventDestroy(e);
     for (cudaStream_t l : lanes_) cudaStreamDestroy(l);
     if (stream_) cudaStreamDestroy(stream_);
@@ -348,8 +350,11 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
             nd.labels0.push_back(l);
             const LabelRole& rl = roles_[l];
             if (rl.role == kFree) nd.labels.push_back(l);
-            else if (rl.role == kPass) pass = true;
-            else nd.var_mask |= uint64_t{1} << rl.var_bit;
+            else if (rl.role == kPass) {
+                pass = true;
+                if (rl.src.kind == 1) nd.slice_mask |= uint64_t{1} << rl.src.bit;
+                if (rl.src.kind == 2) nd.cfg_dep = true;
+            } else nd.var_mask |= uint64_t{1} << rl.var_bit;
         }
         nd.level = nd.var_mask ? 2 : (pass ? 1 : 0);
         nd.pass_dep = pass;
@@ -375,6 +380,8 @@ void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& pl
         nr.var_mask = na.var_mask | nb.var_mask;
         nr.level = std::max(na.level, nb.level);
         nr.pass_dep = na.pass_dep || nb.pass_dep;
+        nr.slice_mask = na.slice_mask | nb.slice_mask;
+        nr.cfg_dep = na.cfg_dep || nb.cfg_dep;
         StepInfo st;
         st.plan_index = step_origin_.empty() ? s : step_origin_[s];
         st.a = a;
@@ -598,11 +605,17 @@ int64_t Program::plan_arena(int64_t cap, bool assign) {
     // groups fit one chunk), per pass (1), per pass and group (2).  Results
     // consumed by a later phase persist; per-pass results read by phase 2
     // persist until the pass ends.
-    auto phase_of = [&](const NodeInfo& nd) { return nd.level < 2 ? nd.level : (nd.pass_dep ? 2 : 3); };
+    auto phase_of = [&](const NodeInfo& nd) {
+        if (nd.tab && !nd.is_leaf) return 4;  // slice-table steps (their own phase, see below)
+        return nd.level < 2 ? nd.level : (nd.pass_dep ? 2 : 3);
+    };
+    // the slice-table steps (phase 4) run before phase 1 in the simulation: their
+    // intermediates are free again afterwards, and the boundary nodes (gathered
+    // at pass start) stay allocated until their per-pass consumers run
     std::vector<int> persist_until_pass_end;
-    for (int ph : {0, 3, 1, 2}) {
+    for (int ph : {0, 3, 4, 1, 2}) {
         for (StepInfo& st : steps_) {
-            if (st.phase != ph) continue;
+            if ((st.tab ? 4 : st.phase) != ph) continue;
             const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b];
             if (st.perm_a) {
                 st.sa_plane = align_up(var_cap(A) * A.payload);
@@ -619,6 +632,8 @@ int64_t Program::plan_arena(int64_t cap, bool assign) {
                 NodeInfo& o = nodes_[op];
                 if (o.is_leaf) continue;
                 if (phase_of(o) == ph) ff.release(o.off, 2 * o.plane);
+                else if (phase_of(o) == 4 && ph == 2) persist_until_pass_end.push_back(op);  // boundary node
+                else if (phase_of(o) == 4) ff.release(o.off, 2 * o.plane);  // boundary node, consumed in phase 1
                 else if (phase_of(o) == 1 && ph == 2) persist_until_pass_end.push_back(op);
                 // constant and group-only operands of later phases persist for the run
             }
@@ -980,8 +995,12 @@ void Program::exec_phase(int phase, const ChunkData* ch) {
             ++launches_;
         }
     }
+    if (phase == 1 && !tab_jobs_.empty()) {  // this pass's entries of the slice tables
+        launch_table_io(d_tab_jobs_, static_cast<int>(tab_jobs_.size()), d_state_, arena_, elem_bytes_, 0, ls_);
+        ++launches_;
+    }
     for (const StepInfo& st : steps_)
-        if (st.phase == phase) exec_step(st, ch);
+        if (st.phase == phase && !st.tab) exec_step(st, ch);
 }
 
 void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
@@ -1214,6 +1233,7 @@ void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
     bound_groups_.clear();
     level0_valid_ = false;
     phase3_valid_ = false;
+    tables_valid_ = false;
     reset_graph();
     // chunk capacity: the largest group chunk whose arena fits the budget
     std::vector<uint64_t> uniq = groups;
@@ -1226,6 +1246,7 @@ void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
         budget = static_cast<uint64_t>(fr * 0.7);
     }
     const int64_t n_uniq = static_cast<int64_t>(uniq.size());
+    mark_tables();  // the arena plan keeps the tables' boundary nodes from pass start
     int64_t lo = 1, hi = n_uniq;
     if (static_cast<uint64_t>(plan_arena(1, false)) * elem_bytes_ > budget)
         throw Failure{RCSG_ERR_CAPACITY, "device arena for one group (" +
@@ -1273,6 +1294,7 @@ void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
                            static_jobs_[level].size() * sizeof(LeafJob), cudaMemcpyHostToDevice));
     }
     prepare_chunks(groups, cap);
+    plan_tables();
     build_tasks();
     chunk_cap_ = cap;
     bound_groups_ = ext_groups;
@@ -1370,7 +1392,7 @@ void Program::build_tasks() {
         // than the tiny steps' own launches running concurrently in the DAG
         static const bool use_chain = getenv("RCSG_CHAIN") != nullptr;
         for (const StepInfo& st : steps_) {
-            if (st.phase != phase) continue;
+            if (st.phase != phase || st.tab) continue;
             if (use_chain && chainable(st, ch)) {
                 run.push_back(&st);
                 continue;
@@ -1385,6 +1407,11 @@ void Program::build_tasks() {
     };
     const Region part{-2, -1};  // the per-configuration accumulator
     if (!static_jobs_[1].empty()) add({0, nullptr, nullptr}, {}, leaf_regions(1));
+    if (!tab_jobs_.empty()) {
+        std::vector<Region> w;
+        for (const TableJob& j : tab_jobs_) w.push_back({j.node_off, j.node_off + 2 * j.node_plane});
+        add({6, nullptr, nullptr}, {}, w);
+    }
     add_steps(1, nullptr);
     for (const ChunkData& ch : chunks_) {
         if (chunks_.size() > 1) {  // one chunk: phase 3 is cached outside the pass
@@ -1475,6 +1502,99 @@ void Program::build_tasks() {
     }
 }
 
+// Slice tables.  A per-pass step is tabulated when its result is small, does
+// not depend on the configuration, and each operand is a leaf, a constant node
+// or itself tabulated.  Boundary nodes (tabulated, consumed by a per-pass
+// step) get a table over the sliced labels in their subtree; the tables are
+// filled once per binding by evaluating the tabulated steps for every value of
+// the union of those labels (at most 2^10 evaluations), and each pass gathers
+// its entries with one launch.  RCSG_NO_TABLES=1 disables.
+void Program::mark_tables() {
+    tab_region_mask_ = 0;
+    tab_boundary_.clear();
+    for (NodeInfo& nd : nodes_) nd.tab = false;
+    for (StepInfo& st : steps_) st.tab = false;
+    if (getenv("RCSG_NO_TABLES") || record_max_) return;
+    constexpr int64_t kTabMaxPayload = int64_t{1} << 16;
+    auto usable = [&](int id) {
+        const NodeInfo& nd = nodes_[id];
+        return nd.is_leaf ? nd.level < 2 : (nd.level == 0 || nd.tab);
+    };
+    for (StepInfo& st : steps_) {
+        NodeInfo& R = nodes_[st.r];
+        if (st.phase != 1 || R.cfg_dep || R.payload > kTabMaxPayload || !usable(st.a) || !usable(st.b)) continue;
+        st.tab = R.tab = true;
+    }
+    std::vector<int>& boundary = tab_boundary_;
+    for (const StepInfo& st : steps_) {
+        if (!st.tab) continue;
+        const int c = nodes_[st.r].consumer;
+        bool consumed_by_tab = false;
+        for (const StepInfo& s2 : steps_)
+            if (c >= 0 && (&s2 - steps_.data()) == c) consumed_by_tab = s2.tab;
+        if (!consumed_by_tab) {
+            boundary.push_back(st.r);
+            tab_region_mask_ |= nodes_[st.r].slice_mask;
+        }
+    }
+    if (boundary.empty() || __builtin_popcountll(tab_region_mask_) > 10) {  // too many evaluations
+        for (NodeInfo& nd : nodes_) nd.tab = false;
+        for (StepInfo& st : steps_) st.tab = false;
+        tab_region_mask_ = 0;
+        boundary.clear();
+    }
+}
+
+// tables and gather jobs of the marked boundary nodes (arena offsets assigned)
+void Program::plan_tables() {
+    for (void* t : tab_mem_) cudaFree(t);
+    tab_mem_.clear();
+    cudaFree(d_tab_jobs_);
+    d_tab_jobs_ = nullptr;
+    tab_jobs_.clear();
+    const std::vector<int>& boundary = tab_boundary_;
+    if (boundary.empty()) return;
+    for (int id : boundary) {
+        const NodeInfo& nd = nodes_[id];
+        TableJob j{};
+        j.node_off = nd.off;
+        j.node_plane = nd.plane;
+        j.payload = nd.payload;
+        j.mask = nd.slice_mask;
+        const size_t bytes = (size_t{1} << __builtin_popcountll(j.mask)) * 2 * nd.payload * elem_bytes_;
+        CUDA_OK(cudaMalloc(&j.table, std::max<size_t>(bytes, 16)));
+        tab_mem_.push_back(j.table);
+        tab_jobs_.push_back(j);
+    }
+    CUDA_OK(cudaMalloc(&d_tab_jobs_, tab_jobs_.size() * sizeof(TableJob)));
+    CUDA_OK(cudaMemcpy(d_tab_jobs_, tab_jobs_.data(), tab_jobs_.size() * sizeof(TableJob), cudaMemcpyHostToDevice));
+    if (getenv("RCSG_DUMP_TREE")) {
+        int n_tab = 0;
+        for (const StepInfo& st : steps_) n_tab += st.tab;
+        fprintf(stderr, "[rcsg] slice tables: %d tabulated steps, %zu boundary nodes, %d sliced labels\n", n_tab,
+                boundary.size(), __builtin_popcountll(tab_region_mask_));
+    }
+}
+
+void Program::build_tables() {
+    const int bits = __builtin_popcountll(tab_region_mask_);
+    for (uint64_t combo = 0; combo < (uint64_t{1} << bits); ++combo) {
+        uint64_t slice = 0;  // deposit combo onto the region's sliced bits
+        int b = 0;
+        for (uint64_t m = tab_region_mask_; m; m &= m - 1, ++b)
+            if ((combo >> b) & 1) slice |= m & (~m + 1);
+        launch_set_pass(d_state_, slice, 0, 0, 1, stream_);
+        if (!static_jobs_[1].empty()) {
+            RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[1], static_cast<int>(static_jobs_[1].size()),
+                                                            d_leaf_data_, nullptr, d_pass_src_, d_state_,
+                                                            static_cast<S*>(arena_), stream_));
+        }
+        for (const StepInfo& st : steps_)
+            if (st.tab) exec_step(st, nullptr);
+        launch_table_io(d_tab_jobs_, static_cast<int>(tab_jobs_.size()), d_state_, arena_, elem_bytes_, 1, stream_);
+    }
+}
+
 void Program::run_task(const Task& t, int64_t P) {
     switch (t.kind) {
         case 0:
@@ -1485,6 +1605,10 @@ void Program::run_task(const Task& t, int64_t P) {
             break;
         case 1:
             exec_step(*t.st, t.ch);
+            break;
+        case 6:
+            launch_table_io(d_tab_jobs_, static_cast<int>(tab_jobs_.size()), d_state_, arena_, elem_bytes_, 0, ls_);
+            ++launches_;
             break;
         case 5:
             RCSG_DISPATCH(precision_, launch_gemm_chain<S>(d_chain_ + t.chain_off, t.chain_len, d_chain_tab_, ls_));
@@ -1612,6 +1736,10 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     if (!phase3_valid_ && chunks_.size() == 1) {  // group-only results of the single chunk
         exec_phase(3, &chunks_[0]);
         phase3_valid_ = true;
+    }
+    if (!tables_valid_ && !tab_jobs_.empty()) {
+        build_tables();
+        tables_valid_ = true;
     }
     for (size_t ci = 0; ci < cfgs.size(); ++ci) {
         launch_fill(d_part_, 0.0, acc_n, stream_);

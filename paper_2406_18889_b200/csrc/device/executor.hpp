@@ -54,6 +54,9 @@ struct NodeInfo {
     uint64_t var_mask = 0;    // group-code bits of the output legs in the subtree
     int level = 0;
     bool pass_dep = false;    // depends on slice / configuration bits
+    uint64_t slice_mask = 0;  // sliced-label bits in the subtree
+    bool cfg_dep = false;     // depends on broken-edge configuration bits
+    bool tab = false;         // computed into slice tables once per binding (see plan_tables)
     int consumer = -1;        // program step consuming this node (-1: root)
     int64_t payload = 1;
     int64_t max_var = 1;
@@ -70,6 +73,7 @@ struct StepInfo {
     int a = -1, b = -1, r = -1;  // A-role operand, B-role operand, result (node ids)
     int level = 0;
     int phase = 0;  // 0 constant, 1 per pass, 2 per pass and group, 3 per group only (cached)
+    bool tab = false;  // phase-1 step evaluated only while building the slice tables
     int mode = 0;  // 0 plain, 1 A-variant folded into M, 2 gathered batch
     bool perm_a = false, perm_b = false;
     PermuteDesc pa{}, pb{};
@@ -141,13 +145,16 @@ class Program {
     // so independent steps overlap (and the captured graph keeps the DAG)
     struct Task {
         int kind;  // 0 level-1 leaf projection, 1 step, 2 / 4 chunk leaf projection (phase 2 / 3),
-                   // 3 chunk finalize, 5 chain of tiny steps
+                   // 3 chunk finalize, 5 chain of tiny steps, 6 slice-table gather
         const StepInfo* st;
         const ChunkData* ch;
         int chain_off = 0, chain_len = 0;  // kind 5: a run of tiny steps, ops in d_chain_
         uint64_t chain_flops = 0;
     };
     void build_tasks();
+    void mark_tables();
+    void plan_tables();
+    void build_tables();
     void free_tasks();
     void exec_pass_dag(int64_t P);
     void run_task(const Task& t, int64_t P);
@@ -216,6 +223,15 @@ class Program {
     size_t n_ext_groups_ = 0;  // caller's group count of the current binding
     bool level0_valid_ = false;  // level-0 (constant) results live in the arena
     bool phase3_valid_ = false;  // single chunk: its group-only (phase-3) results live in the arena
+    // slice tables: small group-independent subtrees that depend on few sliced
+    // labels are evaluated for every value of those labels once per binding;
+    // each pass gathers the current slice's entries (one launch)
+    std::vector<TableJob> tab_jobs_;
+    TableJob* d_tab_jobs_ = nullptr;
+    std::vector<void*> tab_mem_;
+    uint64_t tab_region_mask_ = 0;
+    std::vector<int> tab_boundary_;
+    bool tables_valid_ = false;
     bool fault_pending_ = false; // async runs whose fault flag is not checked yet
     std::vector<int32_t> step_origin_;  // program step -> index of the plan step it came from
     // fp16 mode: per-node storage exponents (value stored times 2^-e)

@@ -331,6 +331,35 @@ template void launch_gemm_chain<double>(const ChainOp*, int, const int32_t*, cud
 template void launch_gemm_chain<bf16>(const ChainOp*, int, const int32_t*, cudaStream_t);
 template void launch_gemm_chain<f16>(const ChainOp*, int, const int32_t*, cudaStream_t);
 
+// ------------------------------------------------------------------ slice tables
+__global__ void table_io_kernel(const TableJob* __restrict__ jobs, const PassState* __restrict__ state,
+                                char* __restrict__ arena, int elem_bytes, int to_table) {
+    pdl_enter();
+    const TableJob j = jobs[blockIdx.y];
+    uint64_t idx = 0;  // pext(slice, mask)
+    int b = 0;
+    for (uint64_t m = j.mask; m; m &= m - 1, ++b)
+        if (state->slice & (m & (~m + 1))) idx |= uint64_t{1} << b;
+    const int64_t n = j.payload * elem_bytes;  // bytes per plane
+    char* node = arena + j.node_off * elem_bytes;
+    char* slot = static_cast<char*>(j.table) + idx * 2 * n;
+    for (int pl = 0; pl < 2; ++pl) {
+        char* a = node + pl * j.node_plane * elem_bytes;
+        char* t = slot + pl * n;
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            if (to_table) t[i] = a[i];
+            else a[i] = t[i];
+        }
+    }
+}
+void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, void* arena, int elem_bytes,
+                     int to_table, cudaStream_t st) {
+    if (n_jobs <= 0) return;
+    launch_pdl(table_io_kernel, dim3(4, n_jobs), dim3(256), 0, st, jobs, state, static_cast<char*>(arena),
+               elem_bytes, to_table);
+}
+
 void* device_workspace(size_t bytes, cudaStream_t st) {
     // one growing scratch buffer per stream (launches on a stream are ordered)
     static std::map<cudaStream_t, std::pair<void*, size_t>> pool;

@@ -224,6 +224,17 @@ struct ChainOp {
 template <typename S>
 void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st);
 
+// Slice tables: job j copies node buffer <-> table slot pext(state->slice, mask)
+// (both planes, `payload` elements each).  to_table: arena -> table (build),
+// else table -> arena (the per-pass gather).
+struct TableJob {
+    int64_t node_off, node_plane, payload;
+    void* table;        // [2^popcount(mask)][2][payload] elements
+    uint64_t mask;      // slice bits the node depends on
+};
+void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, void* arena, int elem_bytes,
+                     int to_table, cudaStream_t st);
+
 // Scratch buffer for split-K partials, one per stream (grown on demand).
 void* device_workspace(size_t bytes, cudaStream_t st);
 
