@@ -247,3 +247,25 @@ def test_async_numeric_fault_is_deferred_to_sync():
     p.contract_groups_device([0], acc.data_ptr(), precision="f64", configs=None, sync=False)
     with pytest.raises(pb.NumericFault):
         p.sync("f64")
+
+
+@pytest.mark.parametrize("precision", ["f64", "f16"])
+def test_slice_tables_match_per_pass_evaluation(monkeypatch, precision):
+    """Small per-pass subtrees are tabulated over their sliced labels once per
+    binding and gathered each pass; the amplitudes equal the per-pass
+    evaluation bit for bit (same kernels on the same data, evaluated earlier)."""
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low")
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), 8, pb.split_next(1, 0xCA11D))
+    tab = pb.Problem(*spec).build().contract_groups(fixed, precision=precision, configs=None, slices=(37, 41))
+    monkeypatch.setenv("RCSG_NO_TABLES", "1")
+    ref = pb.Problem(*spec).build().contract_groups(fixed, precision=precision, configs=None, slices=(37, 41))
+    assert np.array_equal(tab, ref)
+
+
+def test_slice_tables_on_sliced_line_against_oracle():
+    p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
+    pn = port.PortNet(p.net, p.plan)
+    fixed = np.array([0, 5, 22, 63], np.uint64)
+    got = p.contract_groups(fixed, precision="f64", configs=None)
+    for g, fb in enumerate(fixed):
+        assert rel(got[g], pn.contract_group(int(fb))) < 1e-10
