@@ -825,8 +825,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
 bool gemm_tc_supported(const GemmArgs& g) {
     // tensor-core tiles need >= 64 rows, >= 16 columns and a 16-B aligned K stride;
     // tiny contractions stay on the SIMT kernel (launch-bound either way).
-    if (g.m < 64 || g.n < 16 || g.k < 4) return false;
-    if (g.m * g.n * g.k < (int64_t{1} << 21)) return false;
+    if (g.m < 64 || g.n < 8 || g.k < 4) return false;  // narrow N: the TMA box zero-fills past n
+    if (g.m * g.n * g.k * std::max<int64_t>(g.batch, 1) < (int64_t{1} << 21)) return false;
     if (g.batch > 1 && !g.ia) return false;  // batched GEMMs are always gathered here
     if (g.k > (int64_t{1} << 31) || g.m * std::max<int64_t>(g.batch, 1) > (int64_t{1} << 31)) return false;
     return true;

@@ -343,20 +343,33 @@ __global__ void table_io_kernel(const TableJob* __restrict__ jobs, const PassSta
     const int64_t n = j.payload * elem_bytes;  // bytes per plane
     char* node = arena + j.node_off * elem_bytes;
     char* slot = static_cast<char*>(j.table) + idx * 2 * n;
+    const int64_t node_plane = j.node_plane * elem_bytes;
+    const bool vec = (n & 15) == 0 && (node_plane & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(node) | reinterpret_cast<uintptr_t>(slot)) & 15) == 0;
     for (int pl = 0; pl < 2; ++pl) {
-        char* a = node + pl * j.node_plane * elem_bytes;
+        char* a = node + pl * node_plane;
         char* t = slot + pl * n;
-        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-            if (to_table) t[i] = a[i];
-            else a[i] = t[i];
+        if (vec) {  // 16-B vectors
+            uint4* a4 = reinterpret_cast<uint4*>(a);
+            uint4* t4 = reinterpret_cast<uint4*>(t);
+            for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / 16;
+                 i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+                if (to_table) t4[i] = a4[i];
+                else a4[i] = t4[i];
+            }
+        } else {
+            for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+                 i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+                if (to_table) t[i] = a[i];
+                else a[i] = t[i];
+            }
         }
     }
 }
 void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, void* arena, int elem_bytes,
                      int to_table, cudaStream_t st) {
     if (n_jobs <= 0) return;
-    launch_pdl(table_io_kernel, dim3(4, n_jobs), dim3(256), 0, st, jobs, state, static_cast<char*>(arena),
+    launch_pdl(table_io_kernel, dim3(16, n_jobs), dim3(256), 0, st, jobs, state, static_cast<char*>(arena),
                elem_bytes, to_table);
 }
 
