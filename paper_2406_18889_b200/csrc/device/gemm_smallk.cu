@@ -14,13 +14,14 @@ constexpr int kThreads = 256;
 constexpr int kRows = 64;  // output rows per CTA
 
 template <typename S, int K>
-__global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb) {
+__global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int nb, int rows) {
     pdl_enter();
     using R = typename Acc<S>::T;
     const R sc = pow2<R>(g.scale_exp);
     __shared__ R a_re[kRows][K], a_im[kRows][K];
     __shared__ int64_t row_off[kRows];
-    const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + kRows - 1) / kRows;
+    // rows (<= kRows) output rows per tile: fewer for small grids, to spread them over the SMs
+    const int64_t ntiles = (g.n + nb - 1) / nb, mtiles = (g.m + rows - 1) / rows;
     const int col = threadIdx.x % nb, rsub = threadIdx.x / nb, rstep = kThreads / nb;
     bool bad = false;
     for (int64_t tile = blockIdx.x; tile < g.batch * mtiles * ntiles; tile += gridDim.x) {
@@ -32,15 +33,15 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
         const S* A = static_cast<const S*>(g.a) + av * g.a_batch;
         const S* B = static_cast<const S*>(g.b) + bv * g.b_batch;
         S* C = static_cast<S*>(g.c) + v * g.c_batch;
-        const int64_t m0 = mt * kRows, n = nt * nb + col;
+        const int64_t m0 = mt * rows, n = nt * nb + col;
         __syncthreads();
-        for (int e = threadIdx.x; e < kRows * K; e += kThreads) {
+        for (int e = threadIdx.x; e < rows * K; e += kThreads) {
             const int r = e / K, kk = e % K;
             const bool ok = m0 + r < g.m && kk < g.k;
             a_re[r][kk] = ok ? load_c(A + (m0 + r) * g.k + kk) : R(0);
             a_im[r][kk] = ok ? load_c(A + g.a_plane + (m0 + r) * g.k + kk) : R(0);
         }
-        for (int r = threadIdx.x; r < kRows; r += kThreads) row_off[r] = out_row_off(g.om, g.n, m0 + r);
+        for (int r = threadIdx.x; r < rows; r += kThreads) row_off[r] = out_row_off(g.om, g.n, m0 + r);
         const int64_t col_off = out_col_off(g.om, n);
         R b_re[K], b_im[K];
 #pragma unroll
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
         }
         __syncthreads();
         if (n < g.n) {
-            for (int r = rsub; r < kRows && m0 + r < g.m; r += rstep) {
+            for (int r = rsub; r < rows && m0 + r < g.m; r += rstep) {
                 R cr = 0, ci = 0;
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
@@ -146,9 +147,12 @@ void launch_k(const GemmArgs& g, cudaStream_t st) {
         return;
     }
     const int nb = static_cast<int>(std::min<int64_t>(g.n, kThreads));
-    const int64_t tiles = g.batch * ((g.m + kRows - 1) / kRows) * ((g.n + nb - 1) / nb);
+    const int64_t ntiles = g.batch * ((g.n + nb - 1) / nb);
+    int rows = kRows;  // at least ~2 CTAs per SM when the problem allows
+    while (rows > 4 && ntiles * ((g.m + rows - 1) / rows) < 296) rows /= 2;
+    const int64_t tiles = ntiles * ((g.m + rows - 1) / rows);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
-    launch_pdl(smallk_kernel<R, K>, dim3(std::max(grid, 1)), dim3(kThreads), 0, st, g, nb);
+    launch_pdl(smallk_kernel<R, K>, dim3(std::max(grid, 1)), dim3(kThreads), 0, st, g, nb, rows);
 }
 
 }  // namespace
