@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=256)  # all 2^8 slices of cfg2
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--groups", type=int, default=64)
+    ap.add_argument("--groups", type=int, default=1024)  # cfg2 smoke scale M = 2^10
     ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "bf16", "f32", "f64"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

