@@ -824,15 +824,6 @@ int Program::product_order(uint64_t ma, uint64_t mb, int64_t va, int64_t vb, int
     return 0;
 }
 
-// small enough for the one-CTA chain kernel (~1 us of work)
-bool Program::chainable(const StepInfo& st, const ChunkData* ch) const {
-    if (st.perm_a || st.perm_b || record_max_) return false;
-    const GemmArgs g = step_args(st, ch);
-    const NodeInfo& R = nodes_[st.r];
-    return static_cast<double>(g.batch) * g.m * g.n * g.k <= static_cast<double>(kChainMacs) &&
-           2 * R.plane < (int64_t{1} << 31);
-}
-
 template <typename R>
 void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b], &Rn = nodes_[st.r];
@@ -1329,10 +1320,6 @@ void Program::exec_pass_body(int64_t P) {
 }
 
 void Program::free_tasks() {
-    cudaFree(d_chain_);
-    cudaFree(d_chain_tab_);
-    d_chain_ = nullptr;
-    d_chain_tab_ = nullptr;
     for (cudaEvent_t e : task_ev_) cudaEventDestroy(e);
     task_ev_.clear();
     tasks_.clear();
@@ -1364,52 +1351,14 @@ void Program::build_tasks() {
         }
         return w;
     };
-    // consecutive tiny steps become one chain task (one launch, one CTA)
-    std::vector<ChainOp> chain_ops;
-    std::vector<int32_t> chain_tab;
     auto add_steps = [&](int phase, const ChunkData* ch) {
-        std::vector<const StepInfo*> run;
-        auto flush = [&] {
-            if (run.size() == 1) {
-                add({1, run[0], ch}, {node_region(run[0]->a), node_region(run[0]->b)}, {node_region(run[0]->r)});
-            } else if (!run.empty()) {
-                Task t{5, nullptr, ch};
-                t.chain_off = static_cast<int>(chain_ops.size());
-                t.chain_len = static_cast<int>(run.size());
-                std::vector<Region> r, w;
-                for (const StepInfo* st : run) {
-                    ChainOp op{step_args(*st, ch), static_cast<int32_t>(chain_tab.size()), 0};
-                    for (int64_t i = 0; i < op.g.m; ++i)
-                        chain_tab.push_back(static_cast<int32_t>(out_row_off(op.g.om, op.g.n, i)));
-                    op.col_tab = static_cast<int32_t>(chain_tab.size());
-                    for (int64_t j = 0; j < op.g.n; ++j) chain_tab.push_back(static_cast<int32_t>(out_col_off(op.g.om, j)));
-                    chain_ops.push_back(op);
-                    const int64_t vr = (nodes_[st->r].level == 2 && ch) ? ch->nvar[st->r] : 1;
-                    t.chain_flops += st->flops_per_variant * static_cast<uint64_t>(vr);
-                    r.push_back(node_region(st->a));
-                    r.push_back(node_region(st->b));
-                    w.push_back(node_region(st->r));
-                }
-                add(t, r, w);
-            }
-            run.clear();
-        };
-        // opt-in (RCSG_CHAIN=1): on cfg2 the serial one-CTA chain measured slower
-        // than the tiny steps' own launches running concurrently in the DAG
-        static const bool use_chain = getenv("RCSG_CHAIN") != nullptr;
         for (const StepInfo& st : steps_) {
             if (st.phase != phase || st.tab) continue;
-            if (use_chain && chainable(st, ch)) {
-                run.push_back(&st);
-                continue;
-            }
-            flush();
             std::vector<Region> r{node_region(st.a), node_region(st.b)}, w{node_region(st.r)};
             if (st.perm_a) w.push_back({st.sa_off, st.sa_off + 2 * st.sa_plane});
             if (st.perm_b) w.push_back({st.sb_off, st.sb_off + 2 * st.sb_plane});
             add({1, &st, ch}, r, w);
         }
-        flush();
     };
     const Region part{-2, -1};  // the per-configuration accumulator
     if (!static_jobs_[1].empty()) add({0, nullptr, nullptr}, {}, leaf_regions(1));
@@ -1427,12 +1376,6 @@ void Program::build_tasks() {
         if (ch.n_leaf_jobs > ch.n_leaf_jobs3) add({2, nullptr, &ch}, {}, leaf_regions(2));
         add_steps(2, &ch);
         add({3, nullptr, &ch}, {node_region(root_)}, {part});
-    }
-    if (!chain_ops.empty()) {
-        CUDA_OK(cudaMalloc(&d_chain_, chain_ops.size() * sizeof(ChainOp)));
-        CUDA_OK(cudaMemcpy(d_chain_, chain_ops.data(), chain_ops.size() * sizeof(ChainOp), cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMalloc(&d_chain_tab_, chain_tab.size() * sizeof(int32_t)));
-        CUDA_OK(cudaMemcpy(d_chain_tab_, chain_tab.data(), chain_tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     const int T = static_cast<int>(tasks_.size());
     auto overlap = [](const std::vector<Region>& x, const std::vector<Region>& y) {
@@ -1480,8 +1423,7 @@ void Program::build_tasks() {
         for (int t = 0; t < T; ++t) {
             const Task& k = tasks_[t];
             if (k.kind != 1) {
-                fprintf(stderr, "  task %3d kind %d depth %d%s%d\n", t, k.kind, depth[t], k.kind == 5 ? " ops " : "",
-                        k.kind == 5 ? k.chain_len : 0);
+                fprintf(stderr, "  task %3d kind %d depth %d\n", t, k.kind, depth[t]);
                 continue;
             }
             const StepInfo& st = *k.st;
@@ -1615,11 +1557,6 @@ void Program::run_task(const Task& t, int64_t P) {
         case 6:
             launch_table_io(d_tab_jobs_, static_cast<int>(tab_jobs_.size()), d_state_, arena_, elem_bytes_, 0, ls_);
             ++launches_;
-            break;
-        case 5:
-            RCSG_DISPATCH(precision_, launch_gemm_chain<S>(d_chain_ + t.chain_off, t.chain_len, d_chain_tab_, ls_));
-            ++launches_;
-            exec_flops_ += t.chain_flops;
             break;
         case 2:
         case 4: {

@@ -145,11 +145,9 @@ class Program {
     // so independent steps overlap (and the captured graph keeps the DAG)
     struct Task {
         int kind;  // 0 level-1 leaf projection, 1 step, 2 / 4 chunk leaf projection (phase 2 / 3),
-                   // 3 chunk finalize, 5 chain of tiny steps, 6 slice-table gather
+                   // 3 chunk finalize, 6 slice-table gather
         const StepInfo* st;
         const ChunkData* ch;
-        int chain_off = 0, chain_len = 0;  // kind 5: a run of tiny steps, ops in d_chain_
-        uint64_t chain_flops = 0;
     };
     void build_tasks();
     void mark_tables();
@@ -168,8 +166,6 @@ class Program {
     void* buf(int64_t off) const;
     GemmArgs step_args(const StepInfo& st, const ChunkData* ch) const;
     static int product_order(uint64_t ma, uint64_t mb, int64_t va, int64_t vb, int64_t vr);
-    static constexpr int64_t kChainMacs = int64_t{1} << 12;  // complex MACs per chained step
-    bool chainable(const StepInfo& st, const ChunkData* ch) const;
     template <typename R>
     void exec_step_t(const StepInfo& s, const ChunkData* ch);
 
@@ -195,8 +191,6 @@ class Program {
     std::vector<std::vector<int>> task_wait_;  // per task: tasks on other lanes to wait for
     std::vector<int> task_lane_;
     std::vector<cudaEvent_t> task_ev_;
-    ChainOp* d_chain_ = nullptr;      // device op lists of the chain tasks
-    int32_t* d_chain_tab_ = nullptr;  // their output-offset tables
     std::vector<cudaStream_t> lanes_;
     std::vector<cudaEvent_t> lane_ev_;  // fork (index 0) and per-lane join events
     int n_lanes_used_ = 0;

@@ -255,82 +255,6 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st) {
     if (sk.splits > 1) launch_splitk_reduce<S>(static_cast<const R*>(sk.ws), sk.ws_split, sk.splits, g, st);
 }
 
-// ------------------------------------------------------------------ chain
-template <typename S>
-__global__ void __launch_bounds__(1024) gemm_chain_kernel(const ChainOp* __restrict__ ops, int n_ops,
-                                                          const int32_t* __restrict__ tab) {
-    pdl_enter();
-    using R = typename Acc<S>::T;
-    __shared__ ChainOp buf[2];  // op o in buf[o & 1]; thread 0 fetches op o + 1 meanwhile
-    if (threadIdx.x == 0) buf[0] = ops[0];
-    __syncthreads();
-    for (int o = 0; o < n_ops; ++o) {
-        if (threadIdx.x == 0 && o + 1 < n_ops) buf[(o + 1) & 1] = ops[o + 1];
-        const GemmArgs& g = buf[o & 1].g;
-        const int32_t* row_tab = tab + buf[o & 1].row_tab;
-        const int32_t* col_tab = tab + buf[o & 1].col_tab;
-        const int m = static_cast<int>(g.m), n = static_cast<int>(g.n), k = static_cast<int>(g.k);
-        const S* A = static_cast<const S*>(g.a);
-        const S* B = static_cast<const S*>(g.b);
-        S* Cm = static_cast<S*>(g.c);
-        const R sc = pow2<R>(g.scale_exp);
-        const int mn = m * n;
-        const int total = mn * static_cast<int>(g.batch);
-        bool bad = false;
-        for (int e = threadIdx.x; e < total; e += blockDim.x) {
-            const int v = g.batch > 1 ? e / mn : 0, r = e - v * mn, i = r / n, j = r - i * n;
-            const int64_t av = g.ia ? g.ia[v] : (g.a_batch ? v : 0);
-            const int64_t bv = g.ib ? g.ib[v] : (g.b_batch ? v : 0);
-            const S* a = A + av * g.a_batch + static_cast<int64_t>(i) * k;
-            const S* b = B + bv * g.b_batch + static_cast<int64_t>(j) * k;
-            R re = 0, im = 0;
-            int kk = 0;
-            for (; kk + 4 <= k; kk += 4) {  // loads first, then the k-ascending FMAs
-                R ar[4], ai[4], br[4], bi[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    ar[u] = load_c(a + kk + u);
-                    ai[u] = load_c(a + g.a_plane + kk + u);
-                    br[u] = load_c(b + kk + u);
-                    bi[u] = load_c(b + g.b_plane + kk + u);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    re = fma(ar[u], br[u], re);
-                    re = fma(-ai[u], bi[u], re);
-                    im = fma(ar[u], bi[u], im);
-                    im = fma(ai[u], br[u], im);
-                }
-            }
-            for (; kk < k; ++kk) {
-                const R ar = load_c(a + kk), ai = load_c(a + g.a_plane + kk);
-                const R br = load_c(b + kk), bi = load_c(b + g.b_plane + kk);
-                re = fma(ar, br, re);
-                re = fma(-ai, bi, re);
-                im = fma(ar, bi, im);
-                im = fma(ai, br, im);
-            }
-            const int64_t off = v * g.c_batch + row_tab[i] + col_tab[j];
-            re *= sc;
-            im *= sc;
-            store_c(Cm + off, re);
-            store_c(Cm + g.c_plane + off, im);
-            bad |= unstorable<S>(re) || unstorable<S>(im);
-        }
-        if (bad && g.fault) atomicMin(g.fault, g.step);
-        __syncthreads();  // this op's outputs (and the next op's descriptor) are visible
-    }
-}
-
-template <typename S>
-void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st) {
-    if (n_ops > 0) launch_pdl(gemm_chain_kernel<S>, dim3(1), dim3(1024), 0, st, ops, n_ops, tab);
-}
-template void launch_gemm_chain<float>(const ChainOp*, int, const int32_t*, cudaStream_t);
-template void launch_gemm_chain<double>(const ChainOp*, int, const int32_t*, cudaStream_t);
-template void launch_gemm_chain<bf16>(const ChainOp*, int, const int32_t*, cudaStream_t);
-template void launch_gemm_chain<f16>(const ChainOp*, int, const int32_t*, cudaStream_t);
-
 // ------------------------------------------------------------------ slice tables
 __global__ void table_io_kernel(const TableJob* __restrict__ jobs, const PassState* __restrict__ state,
                                 char* __restrict__ arena, int elem_bytes, int to_table) {

@@ -213,17 +213,6 @@ template <typename S>
 void launch_splitk_reduce(const typename Acc<S>::T* ws, int64_t ws_split, int splits, const GemmArgs& g,
                           cudaStream_t st);
 
-// A run of tiny GEMM steps executed back to back by one CTA (each would be a
-// latency-bound launch of its own); per op the semantics of gemm_simt_kernel.
-// ops: DEVICE array; tab: DEVICE int32 output offsets (row_tab / col_tab of
-// each op index into it).  Every op: batch * m * n * k < 2^31, offsets < 2^31.
-struct ChainOp {
-    GemmArgs g;
-    int32_t row_tab, col_tab;  // offsets into the table array: m row offsets, n column offsets
-};
-template <typename S>
-void launch_gemm_chain(const ChainOp* ops, int n_ops, const int32_t* tab, cudaStream_t st);
-
 // Slice tables: job j copies node buffer <-> table slot pext(state->slice, mask)
 // (both planes, `payload` elements each).  to_table: arena -> table (build),
 // else table -> arena (the per-pass gather).
