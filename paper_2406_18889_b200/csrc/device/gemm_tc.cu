@@ -30,6 +30,9 @@ constexpr int kBM = 128;
 // K elements per 128-B swizzle row: 32 fp32 (tf32 path) or 64 bf16
 template <typename E>
 constexpr int KBK = 128 / static_cast<int>(sizeof(E));
+// K elements per stage row of RB bytes (128: SWIZZLE_128B; 64 / 32: narrow-K tiles)
+template <typename E, int RB>
+constexpr int kbk = RB / static_cast<int>(sizeof(E));
 constexpr int kThreads = 128;
 
 int num_sms() {
@@ -78,13 +81,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 "version 1"):
 // start address >> 4, SBO = 1024 B between 8-row atoms, layout type 2.
+// K-major operand tile with RB-byte rows, swizzled to match the TMA box:
+// SBO = one 8-row core-matrix group; layout type 2 / 4 / 6 = SWIZZLE_128B / 64B / 32B
+template <int RB = 128>
 __device__ __forceinline__ uint64_t smem_desc(const void* p) {
     const uint64_t addr = smem_u32(p);
     uint64_t d = (addr >> 4) & 0x3FFF;
-    d |= uint64_t{1} << 16;             // LBO (unused for swizzled K-major)
-    d |= uint64_t{1024 >> 4} << 32;     // SBO
-    d |= uint64_t{1} << 46;             // descriptor version (sm_100)
-    d |= uint64_t{2} << 61;             // SWIZZLE_128B
+    d |= uint64_t{1} << 16;                            // LBO (unused for swizzled K-major)
+    d |= uint64_t{(8 * RB) >> 4} << 32;                // SBO
+    d |= uint64_t{1} << 46;                            // descriptor version (sm_100)
+    d |= uint64_t{RB == 128 ? 2u : (RB == 64 ? 4u : 6u)} << 61;
     return d;
 }
 
@@ -329,12 +335,12 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
     return bad;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int RB = 128>
 struct Smem {
-    static constexpr int kATile = kBM * 128;  // bytes per A plane tile (128-B rows)
-    static constexpr int kBTile = BN * 128;
+    static constexpr int kATile = kBM * RB;  // bytes per A plane tile (RB-byte rows)
+    static constexpr int kBTile = BN * RB;
     static constexpr int kStage = 2 * kATile + 2 * kBTile;
-    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
     // persistent kernel: + staged-epilogue buffers of the 8 epilogue warps (2-byte E)
     template <typename E>
     static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 16 * kEpiWarpElems * 2 : 0);
@@ -498,7 +504,7 @@ struct TileCoord {
     int64_t k_begin;
 };
 
-template <int BN, typename E>
+template <int BN, typename E, int RB = 128>
 __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) {
     // tile counts fit 32 bits (the host checks): 32-bit div/mod, not the 64-bit routine
     TileCoord c;
@@ -529,16 +535,16 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) 
     c.n0 = static_cast<int>(ntile * BN);
     c.k_begin = c.split * p.k_chunk;
     const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
-    c.kblocks = static_cast<int>((k_end - c.k_begin + KBK<E> - 1) / KBK<E>);
+    c.kblocks = static_cast<int>((k_end - c.k_begin + kbk<E, RB> - 1) / kbk<E, RB>);
     return c;
 }
 
-template <int BN, int STAGES, typename E>
+template <int BN, int STAGES, typename E, int RB>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const TcParams p, int64_t total_tiles) {
-    using S = Smem<BN, STAGES>;
+    using S = Smem<BN, STAGES, RB>;
     // TMEM accumulator buffers {Re, Im}: as many as fit in 512 columns (max 4),
     // so the MMA runs ahead of the epilogue by NBUF - 1 tiles
     constexpr uint32_t NBUF = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (lane == 0) {  // ---- TMA producer
             uint32_t it = 0;
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileCoord c = tile_coord<BN, E>(p, t);
+                const TileCoord c = tile_coord<BN, E, RB>(p, t);
                 const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                         continue;
                     }
                     mbar_expect_tx(&full[s], S::kStage);
-                    const int kc = static_cast<int>(c.k_begin) + kb * KBK<E>;
+                    const int kc = static_cast<int>(c.k_begin) + kb * kbk<E, RB>;
                     tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
                     tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
                     tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
@@ -610,7 +616,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             constexpr uint32_t id_pos = idesc_of<E>(BN, false), id_neg = idesc_of<E>(BN, true);
             uint32_t it = 0, j = 0;
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-                const TileCoord c = tile_coord<BN, E>(p, t);
+                const TileCoord c = tile_coord<BN, E, RB>(p, t);
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -620,11 +626,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint8_t* st = smem + s * S::kStage;
-                    const uint64_t dar = smem_desc(st), dai = smem_desc(st + S::kATile);
-                    const uint64_t dbr = smem_desc(st + 2 * S::kATile), dbi = smem_desc(st + 2 * S::kATile + S::kBTile);
+                    const uint64_t dar = smem_desc<RB>(st), dai = smem_desc<RB>(st + S::kATile);
+                    const uint64_t dbr = smem_desc<RB>(st + 2 * S::kATile), dbi = smem_desc<RB>(st + 2 * S::kATile + S::kBTile);
                     if (p.dbg != 2) {  // tuning: dbg 2 skips the MMAs
 #pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) {
+                        for (int jj = 0; jj < RB / 32; ++jj) {  // 32-B K slices (one MMA K each)
                             const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
                             const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
                             mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
@@ -651,7 +657,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         bool bad = false;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-            const TileCoord c = tile_coord<BN, E>(p, t);
+            const TileCoord c = tile_coord<BN, E, RB>(p, t);
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
             int64_t row_off;
@@ -708,17 +714,19 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// 3D map over a [batch][rows][k] fp32 plane, box {32 k, box_rows, 1}, SWIZZLE_128B.
-template <typename E>
+// 3D map over a [batch][rows][k] plane, box {RB bytes of k, box_rows, 1}, swizzled to RB.
+template <typename E, int RB = 128>
 CUtensorMap make_map(const void* base, int64_t k, int64_t rows, int64_t batch, int box_rows) {
     CUtensorMap m;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows),
                           static_cast<cuuint64_t>(std::max<int64_t>(batch, 1))};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * sizeof(E)), static_cast<cuuint64_t>(k * rows * sizeof(E))};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(KBK<E>), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kbk<E, RB>), static_cast<cuuint32_t>(box_rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&m, TcElem<E>::tma, 3, const_cast<void*>(base), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                             : (RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
@@ -739,12 +747,13 @@ int epilogue_kind(const OutMap& om, int64_t n) {
     return 0;
 }
 
-template <int BN, int STAGES, typename E>
+template <int BN, int STAGES, typename E, int RB = 128>
 void launch(const GemmArgs& g, cudaStream_t st) {
-    using S = Smem<BN, STAGES>;
+    using S = Smem<BN, STAGES, RB>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Smem<BN, STAGES>::kBytes);
         configured = true;
     }
     const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
@@ -752,10 +761,10 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
     const E* a = static_cast<const E*>(g.a);
     const E* b = static_cast<const E*>(g.b);
-    const CUtensorMap ar = make_map<E>(a, g.k, a_rows, a_batches, kBM);
-    const CUtensorMap ai = make_map<E>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
-    const CUtensorMap br = make_map<E>(b, g.k, g.n, b_batches, BN);
-    const CUtensorMap bi = make_map<E>(b + g.b_plane, g.k, g.n, b_batches, BN);
+    const CUtensorMap ar = make_map<E, RB>(a, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap ai = make_map<E, RB>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
+    const CUtensorMap br = make_map<E, RB>(b, g.k, g.n, b_batches, BN);
+    const CUtensorMap bi = make_map<E, RB>(b + g.b_plane, g.k, g.n, b_batches, BN);
     TcParams p{};
     p.m = g.m;
     p.n = g.n;
@@ -776,14 +785,14 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     static const int dbg = getenv("RCSG_TC_DBG") ? atoi(getenv("RCSG_TC_DBG")) : 0;
     p.dbg = dbg;
     const int64_t tiles = p.mt * p.nt * g.batch;
-    const int64_t kblocks = (g.k + KBK<E> - 1) / KBK<E>;
+    const int64_t kblocks = (g.k + kbk<E, RB> - 1) / kbk<E, RB>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
     int splits = 1;
     while (tiles * splits < 296 && kblocks / (splits * 2) >= 8) splits *= 2;
     const int64_t chunk_blocks = (kblocks + splits - 1) / splits;
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
-    p.k_chunk = chunk_blocks * KBK<E>;
+    p.k_chunk = chunk_blocks * kbk<E, RB>;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     if (splits == 1) {
         p.c = g.c;
@@ -801,22 +810,22 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     // the epilogue overlaps the next tile's MMAs) for every shape: on long K it
     // measured ~1.9x the one-CTA-per-tile kernel (RCSG_TC_MODE=2 selects that one)
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
-    const bool persistent = mode != 2;
+    const bool persistent = mode != 2 || RB != 128;  // narrow-K tiles: persistent only
     if (persistent) {
         static bool pconf = false;
         if (!pconf) {
-            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::template kPBytes<E>);
             pconf = true;
         }
         const int64_t total = tiles * splits;
         if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-        launch_pdl(gemm_tc_persistent<BN, STAGES, E>, dim3(grid), dim3(kPThreads), S::template kPBytes<E>, st, ar, ai,
+        launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB>, dim3(grid), dim3(kPThreads), S::template kPBytes<E>, st, ar, ai,
                    br, bi, p, total);
     } else {
         launch_pdl(gemm_tc_kernel<BN, STAGES, E>, dim3(static_cast<unsigned>(tiles * splits)), dim3(kThreads),
-                   S::kBytes, st, ar, ai, br, bi, p);
+                   Smem<BN, STAGES>::kBytes, st, ar, ai, br, bi, p);
     }
     if (splits > 1) launch_splitk_reduce<E>(static_cast<const float*>(p.c), p.ws_split, splits, g, st);
 }
@@ -838,10 +847,15 @@ void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st) {
         if (g.n >= 128) launch<128, 3, bf16>(g, st);
         else launch<64, 4, bf16>(g, st);
     } else if (elem == 2) {
-        static const int cfg = getenv("RCSG_TC_CFG") ? atoi(getenv("RCSG_TC_CFG")) : 0;  // tuning knob
-        if (cfg == 1) launch<64, 4, f16>(g, st);
-        else if (cfg == 2) launch<128, 2, f16>(g, st);
-        else if (g.n >= 128) launch<128, 3, f16>(g, st);
+        // narrow K: 32-B / 64-B stage rows (fewer zero-filled K columns, deeper stage rings)
+        static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
+        if (narrow && g.k <= 16) {
+            if (g.n >= 128) launch<128, 12, f16, 32>(g, st);
+            else launch<64, 12, f16, 32>(g, st);
+        } else if (narrow && g.k <= 32) {
+            if (g.n >= 128) launch<128, 6, f16, 64>(g, st);
+            else launch<64, 8, f16, 64>(g, st);
+        } else if (g.n >= 128) launch<128, 3, f16>(g, st);
         else launch<64, 4, f16>(g, st);
     } else {
         if (g.n >= 128) launch<128, 3, float>(g, st);
