@@ -175,3 +175,85 @@ extern "C" int rcsg_gemm_bench_f16(int64_t m, int64_t n, int64_t k, int32_t m_bi
         return RCSG_ERR_DEVICE;
     }
 }
+
+namespace rcsg {
+namespace {
+__global__ void fill_half(__half* p, int64_t n, uint64_t seed) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        p[i] = __float2half(static_cast<float>(static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0));
+    }
+}
+__global__ void diff_half(const __half* a, const __half* b, int64_t n, double* out) {
+    double num = 0, den = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double x = __half2float(a[i]), y = __half2float(b[i]);
+        num += (x - y) * (x - y);
+        den += y * y;
+    }
+    atomicAdd(out, num);
+    atomicAdd(out + 1, den);
+}
+}  // namespace
+}  // namespace rcsg
+
+// fp16 tensor-core GEMM vs the fp16 SIMT kernel on random operands, through an
+// explicit output map (every epilogue kind / K-tile width); rel = ||TC-SIMT|| / ||SIMT||.
+extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                   const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+    try {
+        __half *a, *b, *c1, *c2;
+        int32_t* fault;
+        double* d;
+        const int64_t c_el = m * n;
+        if (cudaMalloc(&a, 2 * m * k * 2) || cudaMalloc(&b, 2 * n * k * 2) || cudaMalloc(&c1, 2 * c_el * 2) ||
+            cudaMalloc(&c2, 2 * c_el * 2) || cudaMalloc(&fault, 4) || cudaMalloc(&d, 16))
+            return RCSG_ERR_DEVICE;
+        fill_half<<<1024, 256>>>(a, 2 * m * k, 7);
+        fill_half<<<1024, 256>>>(b, 2 * n * k, 9);
+        cudaMemset(c1, 0, 2 * c_el * 2);
+        cudaMemset(c2, 0, 2 * c_el * 2);
+        GemmArgs g{};
+        g.a = a;
+        g.a_plane = m * k;
+        g.b = b;
+        g.b_plane = n * k;
+        g.c_plane = c_el;
+        g.m = m;
+        g.n = n;
+        g.k = k;
+        g.batch = 1;
+        g.fault = fault;
+        g.scale_exp = -4;  // keep |C| well inside fp16
+        g.om.m_bits = m_bits;
+        g.om.n_bits = n_bits;
+        g.om.scatter = m_bits + n_bits > 0;
+        for (int j = 0; j < m_bits; ++j) g.om.m_pos[j] = m_pos[j];
+        for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
+        if (!gemm_tc_supported(g)) return RCSG_ERR_CONFIG;
+        g.c = c1;
+        launch_gemm_tc(g, 2, 0);
+        g.c = c2;
+        launch_gemm_simt<f16>(g, 0);
+        cudaMemset(d, 0, 16);
+        diff_half<<<1024, 256>>>(c1, c2, 2 * c_el, d);
+        double h[2] = {0, 1};
+        cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+        const cudaError_t err = cudaGetLastError();
+        *out_rel = std::sqrt(h[0] / h[1]);
+        cudaFree(a);
+        cudaFree(b);
+        cudaFree(c1);
+        cudaFree(c2);
+        cudaFree(fault);
+        cudaFree(d);
+        return err == cudaSuccess ? RCSG_OK : RCSG_ERR_DEVICE;
+    } catch (...) {
+        return RCSG_ERR_DEVICE;
+    }
+}

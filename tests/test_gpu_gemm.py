@@ -1,0 +1,35 @@
+"""fp16 tensor-core complex GEMM (tcgen05, every epilogue kind and K-tile
+width) against the fp16 SIMT kernel on random operands through explicit output
+maps.  rel = ||TC - SIMT|| / ||SIMT||: both round the same fp32-accumulated
+values to fp16, so the bound is a few fp16 ulps (tolerance 2e-3)."""
+import ctypes as C
+
+import pytest
+
+from paper_2406_18889_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+R19 = [0, 1, 2, 3, 6, 7, 8, 9, 11, 12, 15, 16, 17, 18, 19, 20, 21, 22, 23]  # row run of 4 (epi 3)
+CASES = [
+    ("plain-k64", 1 << 15, 64, 64, [], []),
+    ("plain-k512", 4096, 256, 512, [], []),
+    ("row-run", 1 << 19, 64, 64, R19, [4, 5, 10, 13, 14, 24]),
+    ("col-run3-rows-follow", 1 << 14, 128, 128, list(range(3, 17)), [0, 1, 2, 17, 18, 19, 20]),
+    ("col-run7", 1 << 10, 1 << 14, 256, [7, 8, 9, 10, 11, 12, 13, 21, 22, 23], list(range(7)) + list(range(14, 21))),
+    ("mixed-low-bits", 1 << 12, 128, 64, [1, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13], [0, 2, 14, 15, 16, 17, 18]),
+    ("narrow-k16", 1 << 16, 32, 16, [0, 1, 2, 3, 4, 7, 8, 9, 10, 11, 13, 14, 15, 16, 17, 18], [5, 6, 12, 19, 20]),
+    ("narrow-k32-n128", 1 << 13, 128, 32, [], []),
+    ("narrow-n8", 1 << 12, 8, 64, [], []),
+]
+
+
+@pytest.mark.parametrize("name,m,n,k,mp,npos", CASES, ids=[c[0] for c in CASES])
+def test_tc_gemm_matches_simt(name, m, n, k, mp, npos):
+    lib = _native.lib()
+    a = (C.c_int8 * max(len(mp), 1))(*mp)
+    b = (C.c_int8 * max(len(npos), 1))(*npos)
+    rel = C.c_double()
+    rc = lib.rcsg_gemm_check_f16(C.c_int64(m), C.c_int64(n), C.c_int64(k), len(mp), len(npos), a, b, C.byref(rel))
+    assert rc == 0
+    assert rel.value < 2e-3, rel.value
