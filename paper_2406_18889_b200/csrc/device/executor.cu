@@ -612,8 +612,14 @@ int64_t Program::plan_arena(int64_t cap, bool assign) {
     // the slice-table steps (phase 4) run before phase 1 in the simulation: their
     // intermediates are free again afterwards, and the boundary nodes (gathered
     // at pass start) stay allocated until their per-pass consumers run
+    // one chunk: group-only results (phase 3) are computed once, before the
+    // passes; several chunks: each pass recomputes them per chunk after phase 1,
+    // so the simulation must follow that order (phase-3 intermediates may then
+    // not reuse memory of still-live per-pass results)
+    const bool multi_chunk = cap < plan_codes_;
     std::vector<int> persist_until_pass_end;
-    for (int ph : {0, 3, 4, 1, 2}) {
+    const std::vector<int> order = multi_chunk ? std::vector<int>{0, 4, 1, 3, 2} : std::vector<int>{0, 3, 4, 1, 2};
+    for (int ph : order) {
         for (StepInfo& st : steps_) {
             if ((st.tab ? 4 : st.phase) != ph) continue;
             const NodeInfo &A = nodes_[st.a], &B = nodes_[st.b];
@@ -1243,6 +1249,7 @@ void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
         budget = static_cast<uint64_t>(fr * 0.7);
     }
     const int64_t n_uniq = static_cast<int64_t>(uniq.size());
+    plan_codes_ = n_uniq;
     mark_tables();  // the arena plan keeps the tables' boundary nodes from pass start
     int64_t lo = 1, hi = n_uniq;
     if (static_cast<uint64_t>(plan_arena(1, false)) * elem_bytes_ > budget)

@@ -215,6 +215,7 @@ class Program {
     int sb_bits_ = 0;       // batched sliced labels: sliced[0 .. sb_bits_) are variant bits
     int group_bits_ = 0;    // group-code width; batched slice bit j is code bit group_bits_ + j
     size_t n_ext_groups_ = 0;  // caller's group count of the current binding
+    int64_t plan_codes_ = 0;   // distinct codes of the binding being planned (chunking test in plan_arena)
     bool level0_valid_ = false;  // level-0 (constant) results live in the arena
     bool phase3_valid_ = false;  // single chunk: its group-only (phase-3) results live in the arena
     // slice tables: small group-independent subtrees that depend on few sliced

@@ -269,3 +269,23 @@ def test_slice_tables_on_sliced_line_against_oracle():
     got = p.contract_groups(fixed, precision="f64", configs=None)
     for g, fb in enumerate(fixed):
         assert rel(got[g], pn.contract_group(int(fb))) < 1e-10
+
+
+def test_group_chunks_under_a_tight_memory_budget():
+    """A memory budget below the one-chunk arena splits the groups into chunks
+    (group-only subtrees then run inside every pass, per chunk); the amplitudes
+    equal the single-chunk run up to f64 summation order (chunk-sized GEMM
+    shapes change the split-K choices)."""
+    from paper_2406_18889_b200._native import rcsg_stats
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low")
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), 256, pb.split_next(1, 0xCA11D))
+    st0, st1, st2 = rcsg_stats(), rcsg_stats(), rcsg_stats()
+    pb.Problem(*spec).build().contract_groups(fixed[:1], precision="f64", configs=None, slices=(3, 4), stats=st0)
+    one = pb.Problem(*spec).build().contract_groups(fixed, precision="f64", configs=None, slices=(3, 5), stats=st1)
+    tight = int(st0.arena_bytes + (st1.arena_bytes - st0.arena_bytes) / 3)  # ~3 chunks
+    many = pb.Problem(*spec).build().contract_groups(fixed, precision="f64", configs=None, slices=(3, 5),
+                                                     budget=tight, stats=st2)
+    assert st2.arena_bytes < st1.arena_bytes
+    assert st2.passes > st1.passes  # passes count (config, slice, chunk) triples
+    for g in range(len(fixed)):
+        assert rel(many[g], one[g]) < 1e-12, g
