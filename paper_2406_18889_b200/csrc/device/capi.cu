@@ -110,7 +110,6 @@ int rcsg_compile(const rcsg_network_desc* net, const rcsg_plan_desc* plan, int32
         if (!net || !plan || !out) throw Failure{RCSG_ERR_CONFIG, "null argument"};
         auto p = std::make_unique<rcsg_program>();
         p->prog = std::make_unique<Program>(*net, *plan, group_roles(*net, *plan), precision, mem_budget_bytes);
-        p->prog->allow_slice_batch(true);
         p->n_broken = plan->n_broken;
         p->n_sliced = plan->n_sliced;
         *out = p.release();

@@ -266,8 +266,6 @@ Program::Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan,
     if (precision < RCSG_PREC_F64 || precision > RCSG_PREC_F16)
         throw Failure{RCSG_ERR_CONFIG, "unknown precision"};
     elem_bytes_ = precision == RCSG_PREC_F64 ? 8 : (precision >= RCSG_PREC_BF16 ? 2 : 4);
-    for (const LabelRole& r : roles_)
-        if (r.role == kVar) group_bits_ = std::max(group_bits_, r.var_bit + 1);
     build_nodes(net, plan);
     build_steps();
     node_exp_.assign(nodes_.size(), 0);
@@ -705,7 +703,6 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
             ch.ib_off[s] = static_cast<int64_t>(ch.idx.size());
             for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.b, c & nodes_[st.b].var_mask));
         }
-        // codes are the run's (group, batched slice) combinations, index lo * G + g
         const int64_t G = static_cast<int64_t>(n_ext_groups_);
         std::vector<std::array<int32_t, 3>> ent;  // (group, lo, root variant)
         for (size_t u = u0; u < u1; ++u)
@@ -1014,12 +1011,8 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     // index tables.  Repeated calls with the same groups (one call per slice
     // range) reuse everything.
     if (!tree_fixed_) {
-        // the tree is chosen for the group batch alone (slice variants would steer
-        // the local search into mixed group/slice nodes); slice batching then
-        // runs that tree with the batched slice bits as extra variants
         tree_fixed_ = true;
-        retree(groups, false);
-        if (setup_slice_batch()) retree({}, true);
+        retree(groups);
     }
     if (precision_ == RCSG_PREC_F16 && !calibrated_)
         calibrate(groups, configs.empty() ? 0 : configs[0], slice_begin);
@@ -1063,73 +1056,10 @@ rcsg_plan_desc Program::stored_plan() {
 // First run: reassociate the tree for this group batch (see reassociate()),
 // then rebuild the program from the rotated steps.  RCSG_TREE=plan keeps the
 // plan's tree as given.
-// run-level codes: every (group, batched slice lo) combination, lo-major
-std::vector<uint64_t> Program::expand(const std::vector<uint64_t>& groups) const {
-    std::vector<uint64_t> codes;
-    codes.reserve(groups.size() << sb_bits_);
-    for (uint64_t lo = 0; lo < (uint64_t{1} << sb_bits_); ++lo)
-        for (uint64_t g : groups) codes.push_back(g | (lo << group_bits_));
-    return codes;
-}
-
-// Slice batching: sliced[0 .. b) become variant labels (code bits group_bits_ + j),
-// so one pass computes 2^b consecutive slices with the group-variant machinery.
-// b = RCSG_SLICE_BATCH (default 3), capped by the sliced count and the 64-bit code.
-bool Program::setup_slice_batch() {
-    if (!allow_slice_batch_) return false;
-    const char* env = getenv("RCSG_SLICE_BATCH");
-    int b = env ? atoi(env) : 3;
-    int n_sliced = 0;
-    for (const LabelRole& r : roles_)
-        if (r.role == kPass && r.src.kind == 1) ++n_sliced;
-    b = std::max(0, std::min({b, n_sliced, 64 - group_bits_, 10}));
-    // only "clean" sliced labels: the step contracting the label (its two legs
-    // meet) has no group-dependent operand, so batching it never turns a step
-    // into a join on shared variant bits; b = longest clean prefix sliced[0..b)
-    {
-        const int n_nodes = static_cast<int>(nodes_.size());
-        std::vector<std::vector<int>> full(n_nodes);  // all labels incl. projected ones, sorted
-        for (int i = 0; i < n_leaves_; ++i) {
-            full[i] = nodes_[i].labels0;
-            std::sort(full[i].begin(), full[i].end());
-        }
-        std::vector<int> slice_label(n_sliced, -1);
-        for (size_t l = 0; l < roles_.size(); ++l)
-            if (roles_[l].role == kPass && roles_[l].src.kind == 1) slice_label[roles_[l].src.bit] = static_cast<int>(l);
-        std::vector<char> clean(n_sliced, 1);
-        for (const StepInfo& st : steps_) {
-            std::vector<int> sh;
-            std::set_intersection(full[st.a].begin(), full[st.a].end(), full[st.b].begin(), full[st.b].end(),
-                                  std::back_inserter(sh));
-            const bool grouped = nodes_[st.a].level == 2 || nodes_[st.b].level == 2;
-            for (int j = 0; j < n_sliced; ++j)
-                if (grouped && std::binary_search(sh.begin(), sh.end(), slice_label[j])) clean[j] = 0;
-            std::set_symmetric_difference(full[st.a].begin(), full[st.a].end(), full[st.b].begin(),
-                                          full[st.b].end(), std::back_inserter(full[st.r]));
-        }
-        int c = 0;
-        while (c < b && clean[c]) ++c;
-        if (getenv("RCSG_DUMP_TREE")) {
-            fprintf(stderr, "[rcsg] clean sliced labels:");
-            for (int j = 0; j < n_sliced; ++j) fprintf(stderr, " %d", clean[j]);
-            fprintf(stderr, " -> slice batch %d bits\n", c);
-        }
-        b = c;
-    }
-    if (b == 0) return false;
-    for (LabelRole& r : roles_)
-        if (r.role == kPass && r.src.kind == 1 && r.src.bit < b) {
-            r.role = kVar;
-            r.var_bit = static_cast<int16_t>(group_bits_ + r.src.bit);
-        }
-    sb_bits_ = b;
-    return true;
-}
-
-// First run: reassociate the tree for this batch of codes (see reassociate()),
-// then rebuild the program from the rotated steps (and from the label roles,
-// when slice batching changed them).  RCSG_TREE=plan keeps the plan's tree.
-void Program::retree(const std::vector<uint64_t>& groups, bool rebuild) {
+// First run: reassociate the tree for this group batch (see reassociate()),
+// then rebuild the program from the rotated steps.  RCSG_TREE=plan keeps the
+// plan's tree.
+void Program::retree(const std::vector<uint64_t>& groups) {
     const uint64_t plan_flops = plan_flops_;  // stats report the plan's (reference-equivalent) FLOPs
     auto rebuild_program = [&] {
         const rcsg_network_desc net = stored_net();
@@ -1141,10 +1071,6 @@ void Program::retree(const std::vector<uint64_t>& groups, bool rebuild) {
         CUDA_OK(cudaMemcpy(d_canon_, root_canon_src_.data(), root_canon_src_.size() * sizeof(int32_t),
                            cudaMemcpyHostToDevice));
     };
-    if (rebuild) {  // roles changed: rebuild on the current steps, no new rotations
-        rebuild_program();
-        return;
-    }
     const char* env = getenv("RCSG_TREE");
     if (env && std::string(env) == "plan") return;
     const int n_steps = static_cast<int>(c_steps_.size() / 3);
@@ -1198,8 +1124,6 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
         Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.4));
         cal.tree_fixed_ = true;  // the steps are already this program's (reassociated) tree
         cal.step_origin_ = step_origin_;
-        cal.sb_bits_ = sb_bits_;  // and its roles already batch these sliced labels
-        cal.group_bits_ = group_bits_;
         CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
         CUDA_OK(cudaMemset(cal.d_max_, 0, nodes_.size() * sizeof(float)));
         cal.record_max_ = true;
@@ -1230,9 +1154,8 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
     reset_graph();
 }
 
-void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
-    const std::vector<uint64_t> groups = expand(ext_groups);
-    n_ext_groups_ = ext_groups.size();
+void Program::bind_groups(const std::vector<uint64_t>& groups) {
+    n_ext_groups_ = groups.size();
     bound_groups_.clear();
     level0_valid_ = false;
     phase3_valid_ = false;
@@ -1301,7 +1224,7 @@ void Program::bind_groups(const std::vector<uint64_t>& ext_groups) {
     plan_tables();
     build_tasks();
     chunk_cap_ = cap;
-    bound_groups_ = ext_groups;
+    bound_groups_ = groups;
 }
 
 // One (configuration, slice) pass after set_pass: level-1 steps, then every
@@ -1677,9 +1600,8 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     const std::vector<uint64_t>& cfgs = configs.empty() ? no_cfg : configs;
     // level 0 depends on no slice, configuration or group: computed once per
     // arena binding and kept (its results persist in the arena across calls)
-    const uint64_t S = uint64_t{1} << sb_bits_;  // slices per pass (batched low slice bits)
     if (!level0_valid_) {
-        launch_set_pass(d_state_, slice_begin & ~(S - 1), cfgs[0], 0, static_cast<uint32_t>(S), stream_);
+        launch_set_pass(d_state_, slice_begin, cfgs[0], 0, 1, stream_);
         exec_phase(0, nullptr);
         level0_valid_ = true;
     }
@@ -1694,12 +1616,8 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
     for (size_t ci = 0; ci < cfgs.size(); ++ci) {
         launch_fill(d_part_, 0.0, acc_n, stream_);
         ++launches_;
-        // one pass per block of S consecutive slices; its finalisation counts only
-        // the block's slices inside [slice_begin, slice_end), in ascending order
-        for (uint64_t base = slice_begin & ~(S - 1); base < slice_end; base += S) {
-            const uint64_t lo_b = std::max(slice_begin, base) - base, lo_e = std::min(slice_end, base + S) - base;
-            launch_set_pass(d_state_, base, cfgs[ci], static_cast<uint32_t>(lo_b), static_cast<uint32_t>(lo_e),
-                            stream_);
+        for (uint64_t s = slice_begin; s < slice_end; ++s) {  // slices ascending
+            launch_set_pass(d_state_, s, cfgs[ci], 0, 1, stream_);
             ++launches_;
             run_pass_body(P);
             passes += chunks_.size();

@@ -118,9 +118,6 @@ class Program {
     void run(const std::vector<uint64_t>& groups, const std::vector<uint64_t>& configs,
              uint64_t slice_begin, uint64_t slice_end, double* d_acc, rcsg_stats* stats, bool sync = true);
     void sync();
-    // group path: batch the low sliced labels as variant bits (set before the first run)
-    void allow_slice_batch(bool on) { allow_slice_batch_ = on; }
-    int slice_batch_bits() const { return sb_bits_; }
 
     int out_rank() const { return out_rank_; }
     void set_profile(bool on) { profile_ = on; }
@@ -130,9 +127,7 @@ class Program {
 
   private:
     void build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan);
-    void retree(const std::vector<uint64_t>& codes, bool rebuild);
-    bool setup_slice_batch();
-    std::vector<uint64_t> expand(const std::vector<uint64_t>& groups) const;
+    void retree(const std::vector<uint64_t>& groups);
     rcsg_network_desc stored_net();
     rcsg_plan_desc stored_plan();
     void build_steps();
@@ -211,9 +206,6 @@ class Program {
     std::vector<uint64_t> bound_groups_;  // group list the chunks/arena are bound to
     // batch-aware reassociation: done once, at the first run (group codes known)
     bool tree_fixed_ = false;
-    bool allow_slice_batch_ = false;
-    int sb_bits_ = 0;       // batched sliced labels: sliced[0 .. sb_bits_) are variant bits
-    int group_bits_ = 0;    // group-code width; batched slice bit j is code bit group_bits_ + j
     size_t n_ext_groups_ = 0;  // caller's group count of the current binding
     int64_t plan_codes_ = 0;   // distinct codes of the binding being planned (chunking test in plan_arena)
     bool level0_valid_ = false;  // level-0 (constant) results live in the arena

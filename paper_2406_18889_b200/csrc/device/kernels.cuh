@@ -72,9 +72,9 @@ struct LeafJob {
 };
 
 struct PassState {
-    uint64_t slice;        // current slice index (bit b <-> sliced[b]); batched low bits are 0
+    uint64_t slice;        // current slice index (bit b <-> sliced[b])
     uint64_t config;       // current broken-edge configuration bits
-    uint32_t lo_begin, lo_end;  // batched slices of this pass that count: slice + [lo_begin, lo_end)
+    uint32_t lo_begin, lo_end;  // finalize counts root entries with lo in [lo_begin, lo_end) (one slice: 0, 1)
 };
 
 // Pass-label source table: for a pass label, where its value comes from.
