@@ -166,6 +166,24 @@ int rcsg_execute_assignment(const rcsg_network_desc* net, const rcsg_plan_desc* 
                             int32_t precision, const int8_t* assign, double* out,
                             uint64_t* n_out);
 
+/* ---- exact statevector (XEB oracle) ----------------------------------------- */
+
+/* simulate_exact (statevector.cpp:79-86) on the device: |0..0> followed by the
+ * gates in order.  Gate g acts on n_targets[g] (1 or 2) qubits targets[2g],
+ * targets[2g+1] with the row-major unitary at unitaries[32g ..] (16 interleaved
+ * complex f64; a 1-qubit gate uses the first 4).  Basis of a 2-qubit block:
+ * (bit of targets[2g]) << 1 | bit of targets[2g+1] (statevector.cpp:42).
+ * d_state: DEVICE buffer of 2^n interleaved complex f64 (qubit q = index bit
+ * q).  Products and sums are rounded in the reference's order.
+ * Replaces: simulate_exact / apply_gate (statevector.hpp:29, statevector.cpp:60-86). */
+int rcsg_statevector(int32_t n_qubits, int32_t n_gates, const int32_t* n_targets, const int32_t* targets,
+                     const double* unitaries, double* d_state);
+
+/* |amplitude|^2 at the given basis indices of a device statevector (HOST
+ * indices in, HOST probabilities out).  Replaces: ideal_probability
+ * (statevector.hpp:32). */
+int rcsg_statevector_probs(const double* d_state, uint64_t n_indices, const uint64_t* indices, double* out);
+
 /* ---- post-processing (sampling.cpp) on device amplitudes ------------------ */
 
 /* Candidate-set description (CandidateSet, sampling.hpp:17-31). */

@@ -55,7 +55,8 @@ RCSG_SYMBOLS = [
     "rcsg_program_set_profile", "rcsg_program_stream", "rcsg_gemm_selftest", "rcsg_gemm_check_f16",
     "rcsg_contract_groups", "rcsg_contract_groups_device", "rcsg_execute_assignment", "rcsg_topk",
     "rcsg_topk_probs", "rcsg_direct_sample", "rcsg_direct_sample_probs", "rcsg_xeb",
-    "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy", "rcsg_program_sync",
+    "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy", "rcsg_program_sync", "rcsg_statevector",
+    "rcsg_statevector_probs",
 ]
 RCSH_SYMBOLS = [
     "rcsh_last_error", "rcsh_build", "rcsh_build_network", "rcsh_free", "rcsh_net_sizes",
@@ -63,7 +64,7 @@ RCSH_SYMBOLS = [
     "rcsh_circuit_gates", "rcsh_contract_groups", "rcsh_contract_groups_device", "rcsh_contract",
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
     "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
-    "rcsh_program_stream", "rcsh_program_sync",
+    "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector",
 ]
 
 _lib = None

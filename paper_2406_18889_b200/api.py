@@ -216,6 +216,25 @@ class Problem:
         _native.lib().rcsh_circuit_gates(self.handle, _p(out, C.c_int))
         return out[:4 * n].reshape(-1, 4)
 
+    # ---- exact oracle -------------------------------------
+    def exact_state_device(self, d_state: int):
+        """simulate_exact (statevector.cpp:79-86) into a DEVICE buffer of 2^n
+        interleaved complex f64 (e.g. a torch.complex128 tensor's data_ptr())."""
+        _check_h(_native.lib().rcsh_statevector(self.handle, C.c_void_p(d_state)))
+
+    def exact_probabilities(self, indices) -> np.ndarray:
+        """Ideal probabilities |<x|C|0>|^2 of the given basis indices (qubit q =
+        bit q), from the GPU statevector (n <= 33 fits one B200)."""
+        import torch
+        state = torch.empty(1 << self.n, dtype=torch.complex128, device="cuda")
+        self.exact_state_device(state.data_ptr())
+        idx = _u64(indices)
+        out = np.zeros(len(idx), np.float64)
+        _check_g(_native.lib().rcsg_statevector_probs(C.c_void_p(state.data_ptr()), C.c_uint64(len(idx)),
+                                                    _p(idx, C.c_uint64), _p(out, C.c_double)))
+        del state
+        return out
+
     # ---- hot path ---------------------------------------------------------
     def contract_groups(self, fixed, precision="f64", configs="all", slices=None, budget=0,
                         stats: rcsg_stats | None = None) -> np.ndarray:

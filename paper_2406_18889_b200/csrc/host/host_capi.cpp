@@ -286,6 +286,30 @@ std::int64_t rcsh_circuit_gates(void* hp, int* out) {
     return n;
 }
 
+// simulate_exact (statevector.cpp:79-86) of the handle's circuit into a DEVICE
+// buffer of 2^n interleaved complex f64 (rcsg_statevector).
+int rcsh_statevector(void* hp, double* d_state) {
+    return guarded([&] {
+        const Handle* h = static_cast<Handle*>(hp);
+        std::vector<std::int32_t> nt, tg;
+        std::vector<double> u;
+        for (const Layer& layer : h->circuit.layers)
+            for (const Gate& g : layer.gates) {
+                nt.push_back(static_cast<std::int32_t>(g.targets.size()));
+                tg.push_back(g.targets[0]);
+                tg.push_back(g.targets.size() > 1 ? g.targets[1] : -1);
+                for (int r = 0; r < 16; ++r) {
+                    const cplx v = r < static_cast<int>(g.unitary.size()) ? g.unitary[r] : cplx(0.0, 0.0);
+                    u.push_back(v.real());
+                    u.push_back(v.imag());
+                }
+            }
+        if (int rc = rcsg_statevector(h->circuit.n_qubits, static_cast<std::int32_t>(nt.size()), nt.data(),
+                                      tg.data(), u.data(), d_state))
+            raise_rcsg(rc);
+    });
+}
+
 // rcsg_contract_groups over the handle's plan; n_cfg < 0 uses the handle's
 // BrokenEdgeConfig (all m configurations), n_cfg == 0 the exact contraction.
 int rcsh_contract_groups(void* hp, int precision, std::uint64_t budget, std::uint64_t n_groups,
