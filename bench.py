@@ -200,6 +200,46 @@ def xeb_cfg1(pb, precision):
             "samples_per_s": (k + M) / (t1 - t0)}
 
 
+def xeb_cfg2(pb, p, fixed, precision):
+    """cfg2 end to end at n = 30 against the exact GPU statevector (SURVEY §8f
+    row 3): all 2^8 slices for the M groups (K = 0, so the amplitudes are the
+    exact ones up to the storage precision) -> top-k with k = M (the paper's k =
+    #groups) and one direct sample per group -> linear XEB from the ideal
+    probabilities; plus the amplitude fidelity of all M * 2^l candidates."""
+    import numpy as np
+    import torch
+    n, l, M = 30, 6, len(fixed)
+    P = 1 << l
+    acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
+    t0 = time.perf_counter()
+    for s0 in range(0, p.n_slices, 8):
+        p.contract_groups_device(fixed, acc.data_ptr(), precision=precision, configs=None, slices=(s0, s0 + 8),
+                                 sync=False)
+    p.sync(precision)
+    top = pb.api.top_k_from_device_amps(n, CFG2["open"], fixed, acc.data_ptr(), M)
+    direct = pb.api.direct_from_device_amps(n, CFG2["open"], fixed, acc.data_ptr(), pb.split_next(1, 0xD1EC7))
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+    p.exact_state_device(state.data_ptr())
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    probs = (state.real ** 2 + state.imag ** 2)
+    q_top = probs[torch.as_tensor(top.astype(np.int64), device="cuda")].cpu().numpy()
+    q_dir = probs[torch.as_tensor(direct.astype(np.int64), device="cuda")].cpu().numpy()
+    cand = np.array([pb.member(n, CFG2["open"], int(f), i) for f in fixed for i in range(P)], np.int64)
+    ex = state[torch.as_tensor(cand, device="cuda")].cpu().numpy()
+    del state, probs
+    ap = acc.cpu().numpy().view(np.complex128).reshape(-1)
+    fid = abs(np.vdot(ex, ap)) ** 2 / (np.vdot(ap, ap).real * np.vdot(ex, ex).real)
+    return {"config": f"cfg2 grid(5,6) n=30 cycles=14 l=6 M={M} K=0, all 256 slices, {precision}",
+            # Porter-Thomas: keeping the top fraction k / (M 2^l) of exact probabilities gives XEB = ln(M 2^l / k)
+            "xeb_topk": pb.xeb(n, q_top), "k": M, "predicted_topk_exact": float(np.log(M * P / M)),
+            "xeb_direct": pb.xeb(n, q_dir), "amplitude_fidelity_vs_exact": float(fid),
+            "contract_and_sample_s": t1 - t0, "statevector_s": t2 - t1,
+            "note": "ideal probabilities from the GPU statevector (simulate_exact, bit-exact with the reference)"}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -359,6 +399,11 @@ def main():
             xeb = xeb_cfg1(pb, args.precision)
         except Exception as e:  # pragma: no cover
             xeb = {"error": str(e)}
+        if world == 1:
+            try:
+                xeb = {"cfg1": xeb, "cfg2": xeb_cfg2(pb, p, fixed, args.precision)}
+            except Exception as e:  # pragma: no cover
+                xeb = {"cfg1": xeb, "cfg2": {"error": str(e)}}
 
     if rank == 0:
         line = {
