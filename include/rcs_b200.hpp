@@ -208,8 +208,24 @@ struct FidelityResult {
 };
 FidelityResult state_fidelity(std::span<const cplx> approx, std::span<const cplx> exact);
 
+// ---- exact statevector (reference statevector.hpp), computed on the GPU
+// (rcsg_statevector: bit-identical to the reference's complex<double> gate loop).
+// Qubit q maps to bit q of the array index.
+struct StateVector {
+    int n_qubits = 0;
+    std::vector<cplx> amps;
+    double norm_sq() const;
+};
+constexpr int kDefaultExactCap = 24;
+// Throws CapacityError above `cap` qubits (the host copy is 16 B x 2^n).
+StateVector simulate_exact(const Circuit& circuit, int cap = kDefaultExactCap);
+double ideal_probability(const StateVector& state, const std::string& bitstring);
+std::uint64_t bitstring_to_index(const std::string& bitstring);
+std::string index_to_bitstring(std::uint64_t index, int n_qubits);
+
 // Precision of the device executor: "f64" (default; reference-grade), "f32",
-// "tf32" (tcgen05 tensor cores), "3xtf32" (split-tf32 tensor cores, fp32-grade).
+// "tf32" (tcgen05 tensor cores), "3xtf32" (split-tf32 tensor cores, fp32-grade),
+// "bf16", "f16" (fp16 storage with per-tensor power-of-two scales).
 void set_precision(const std::string& precision);
 std::string get_precision();
 

@@ -217,3 +217,66 @@ FidelityResult state_fidelity(std::span<const cplx> approx, std::span<const cplx
 }
 
 }  // namespace rcs
+
+// ---- exact statevector (statevector.cpp), computed by rcsg_statevector ------
+namespace rcs {
+
+double StateVector::norm_sq() const {
+    double s = 0.0;
+    for (const cplx& a : amps) s += std::norm(a);
+    return s;
+}
+
+StateVector simulate_exact(const Circuit& circuit, int cap) {
+    if (circuit.n_qubits > cap)
+        throw CapacityError("exact simulation capped at " + std::to_string(cap) + " qubits, circuit has " +
+                            std::to_string(circuit.n_qubits));
+    std::vector<std::int32_t> nt, tg;
+    std::vector<double> u;
+    for (const Layer& layer : circuit.layers)
+        for (const Gate& g : layer.gates) {
+            nt.push_back(static_cast<std::int32_t>(g.targets.size()));
+            tg.push_back(g.targets[0]);
+            tg.push_back(g.targets.size() > 1 ? g.targets[1] : -1);
+            for (int r = 0; r < 16; ++r) {
+                const cplx v = r < static_cast<int>(g.unitary.size()) ? g.unitary[r] : cplx(0.0, 0.0);
+                u.push_back(v.real());
+                u.push_back(v.imag());
+            }
+        }
+    StateVector st;
+    st.n_qubits = circuit.n_qubits;
+    const std::size_t dim = std::size_t{1} << circuit.n_qubits;
+    void* d = nullptr;
+    ok(rcsg_device_alloc(dim * 2 * sizeof(double), &d));
+    std::unique_ptr<void, void (*)(void*)> hold(d, [](void* p) { rcsg_device_free(p); });
+    ok(rcsg_statevector(circuit.n_qubits, static_cast<std::int32_t>(nt.size()), nt.data(), tg.data(), u.data(),
+                        static_cast<double*>(d)));
+    st.amps.resize(dim);
+    ok(rcsg_memcpy(st.amps.data(), d, dim * 2 * sizeof(double), 2));
+    return st;
+}
+
+std::uint64_t bitstring_to_index(const std::string& bitstring) {
+    std::uint64_t idx = 0;
+    for (std::size_t q = 0; q < bitstring.size(); ++q) {
+        const char c = bitstring[q];
+        if (c != '0' && c != '1') throw ConfigError("bitstring must be 0/1");
+        if (c == '1') idx |= std::uint64_t{1} << q;
+    }
+    return idx;
+}
+
+std::string index_to_bitstring(std::uint64_t index, int n_qubits) {
+    std::string s(n_qubits, '0');
+    for (int q = 0; q < n_qubits; ++q)
+        if ((index >> q) & 1) s[q] = '1';
+    return s;
+}
+
+double ideal_probability(const StateVector& state, const std::string& bitstring) {
+    if (static_cast<int>(bitstring.size()) != state.n_qubits) throw ConfigError("bitstring length mismatch");
+    return std::norm(state.amps[bitstring_to_index(bitstring)]);
+}
+
+}  // namespace rcs
