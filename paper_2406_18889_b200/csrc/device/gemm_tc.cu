@@ -842,21 +842,29 @@ bool gemm_tc_supported(const GemmArgs& g) {
     return true;
 }
 
+// 2-byte operands: narrow K uses 32-B / 64-B stage rows (fewer zero-filled K
+// columns, deeper stage rings); RCSG_TC_NARROW_K=0 disables
+template <typename E>
+void launch_2byte(const GemmArgs& g, cudaStream_t st) {
+    static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
+    if (narrow && g.k <= 16) {
+        if (g.n >= 128) launch<128, 12, E, 32>(g, st);
+        else launch<64, 12, E, 32>(g, st);
+    } else if (narrow && g.k <= 32) {
+        if (g.n >= 128) launch<128, 6, E, 64>(g, st);
+        else launch<64, 8, E, 64>(g, st);
+    } else if (g.n >= 128) {
+        launch<128, 3, E>(g, st);
+    } else {
+        launch<64, 4, E>(g, st);
+    }
+}
+
 void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st) {
     if (elem == 1) {
-        if (g.n >= 128) launch<128, 3, bf16>(g, st);
-        else launch<64, 4, bf16>(g, st);
+        launch_2byte<bf16>(g, st);
     } else if (elem == 2) {
-        // narrow K: 32-B / 64-B stage rows (fewer zero-filled K columns, deeper stage rings)
-        static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
-        if (narrow && g.k <= 16) {
-            if (g.n >= 128) launch<128, 12, f16, 32>(g, st);
-            else launch<64, 12, f16, 32>(g, st);
-        } else if (narrow && g.k <= 32) {
-            if (g.n >= 128) launch<128, 6, f16, 64>(g, st);
-            else launch<64, 8, f16, 64>(g, st);
-        } else if (g.n >= 128) launch<128, 3, f16>(g, st);
-        else launch<64, 4, f16>(g, st);
+        launch_2byte<f16>(g, st);
     } else {
         if (g.n >= 128) launch<128, 3, float>(g, st);
         else launch<64, 4, float>(g, st);
