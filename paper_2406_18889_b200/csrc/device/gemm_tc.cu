@@ -192,6 +192,7 @@ struct TcParams {
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
     int32_t dbg;            // tuning knob (RCSG_TC_DBG): 1 = skip the epilogue's global stores
+    int32_t b_resident;     // B identical for every tile: loaded once per stage slot
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -602,12 +603,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
                         mbar_expect_tx(&full[s], 0);
                         continue;
                     }
-                    mbar_expect_tx(&full[s], S::kStage);
+                    // B resident: the same single B tile for every tile (one N tile, one
+                    // K block, unbatched B) is loaded once into each stage slot
+                    const bool load_b = !(p.b_resident && it >= STAGES);
+                    mbar_expect_tx(&full[s], load_b ? S::kStage : 2 * S::kATile);
                     const int kc = static_cast<int>(c.k_begin) + kb * kbk<E, RB>;
                     tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
                     tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
-                    tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
-                    tma_load_3d(st + 2 * S::kATile + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                    if (load_b) {
+                        tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
+                        tma_load_3d(st + 2 * S::kATile + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                    }
                 }
             }
         }
@@ -794,6 +800,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.splits = splits;
     p.k_chunk = chunk_blocks * kbk<E, RB>;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
+    p.b_resident = (p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
+                    !(getenv("RCSG_TC_NO_BRES") != nullptr)) ? 1 : 0;
     if (splits == 1) {
         p.c = g.c;
         p.c_plane = g.c_plane;
