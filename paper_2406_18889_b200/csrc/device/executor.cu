@@ -873,9 +873,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     const bool tc_ok = !std::is_same_v<R, double> &&
                        (precision_ == RCSG_PREC_TF32 || precision_ >= RCSG_PREC_BF16) && gemm_tc_supported(g);
     // K <= 16 goes to the register-blocked outer-product kernel, except large
-    // K = 9..16 products, which are CUDA-core FMA-bound there and memory-bound
-    // on the tensor cores (the TMA box zero-fills K up to 64)
-    const bool big_k16 = g.k > 8 && static_cast<double>(g.m) * g.n * std::max<int64_t>(g.batch, 1) >= 4194304.0;
+    // K = 5..16 products, which are CUDA-core FMA-bound there and memory-bound
+    // on the tensor cores (narrow-K tiles zero-fill K up to 16)
+    const bool big_k16 = g.k > 4 && static_cast<double>(g.m) * g.n * std::max<int64_t>(g.batch, 1) >= 4194304.0;
     if (gemm_smallk_supported(g) && !(tc_ok && big_k16)) {
         launch_gemm_smallk<R>(g, ls_);
         mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
