@@ -540,6 +540,56 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) 
     return c;
 }
 
+// Tile index t = ((v * n_hi + hi) * n_lo + lo) * splits + split, with (lo, hi) =
+// (m tile, n tile) when m_fast else (n tile, m tile).  A CTA walks t = blockIdx.x,
+// blockIdx.x + gridDim.x, ...: the digits advance by gridDim.x's mixed-radix
+// digits with carries, so no division per tile.
+struct TileIter {
+    uint32_t split, lo, hi, v;           // current digits
+    uint32_t d_split, d_lo, d_hi, d_v;   // gridDim.x in the same radix
+    uint32_t splits, n_lo, n_hi;
+    __device__ void init(const TcParams& p, uint32_t t, uint32_t step) {
+        splits = static_cast<uint32_t>(p.splits);
+        n_lo = static_cast<uint32_t>(p.m_fast ? p.mt : p.nt);
+        n_hi = static_cast<uint32_t>(p.m_fast ? p.nt : p.mt);
+        auto digits = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+            a = x % splits;
+            x /= splits;
+            b = x % n_lo;
+            x /= n_lo;
+            c = x % n_hi;
+            d = x / n_hi;
+        };
+        digits(t, split, lo, hi, v);
+        digits(step, d_split, d_lo, d_hi, d_v);
+    }
+    __device__ __forceinline__ void next() {
+        split += d_split;
+        uint32_t c = split >= splits;
+        split -= c ? splits : 0;
+        lo += d_lo + c;
+        c = lo >= n_lo;
+        lo -= c ? n_lo : 0;
+        hi += d_hi + c;
+        c = hi >= n_hi;
+        hi -= c ? n_hi : 0;
+        v += d_v + c;
+    }
+    template <int BN, typename E, int RB>
+    __device__ __forceinline__ TileCoord coord(const TcParams& p) const {
+        TileCoord c;
+        c.split = static_cast<int>(split);
+        const uint32_t mtile = p.m_fast ? lo : hi, ntile = p.m_fast ? hi : lo;
+        c.v = v;
+        c.m0 = static_cast<int>(mtile * kBM);
+        c.n0 = static_cast<int>(ntile * BN);
+        c.k_begin = c.split * p.k_chunk;
+        const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
+        c.kblocks = static_cast<int>((k_end - c.k_begin + kbk<E, RB> - 1) / kbk<E, RB>);
+        return c;
+    }
+};
+
 template <int BN, int STAGES, typename E, int RB>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
@@ -591,8 +641,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
             uint32_t it = 0;
-            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileCoord c = tile_coord<BN, E, RB>(p, t);
+            TileIter ti;
+            ti.init(p, blockIdx.x, gridDim.x);
+            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ti.next()) {
+                const TileCoord c = ti.coord<BN, E, RB>(p);
                 const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
@@ -621,8 +673,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (lane == 0) {  // ---- MMA issuer
             constexpr uint32_t id_pos = idesc_of<E>(BN, false), id_neg = idesc_of<E>(BN, true);
             uint32_t it = 0, j = 0;
-            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-                const TileCoord c = tile_coord<BN, E, RB>(p, t);
+            TileIter ti;
+            ti.init(p, blockIdx.x, gridDim.x);
+            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j, ti.next()) {
+                const TileCoord c = ti.coord<BN, E, RB>(p);
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -662,8 +716,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int64_t lane_off = split_rows ? scatter_bits(p.om.m_pos, 7, local) : 0;
         bool bad = false;
         uint32_t j = 0;
-        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j) {
-            const TileCoord c = tile_coord<BN, E, RB>(p, t);
+        TileIter ti;
+        ti.init(p, blockIdx.x, gridDim.x);
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j, ti.next()) {
+            const TileCoord c = ti.coord<BN, E, RB>(p);
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
             int64_t row_off;
