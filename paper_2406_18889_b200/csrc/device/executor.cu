@@ -1019,7 +1019,20 @@ void Program::run(const std::vector<uint64_t>& groups, const std::vector<uint64_
     if (groups != bound_groups_) bind_groups(groups);
     const int64_t P = nodes_[root_].payload;
     const int64_t acc_n = static_cast<int64_t>(groups.size()) * P * 2;
-    run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n, sync || profile_);
+    try {
+        run_bound(groups.size(), configs, slice_begin, slice_end, d_acc, stats, P, acc_n, sync || profile_);
+    } catch (const Failure& f) {
+        // fp16: an unstorable value means the calibrated scales (first slice, <= 16
+        // groups, 2^6 headroom) were too tight for this data, not a non-finite
+        // amplitude.  Widen every intermediate's headroom by 2^8, rebind (graph,
+        // caches, tables) and rerun; a synchronous call has not touched d_acc.
+        if (f.code != RCSG_ERR_NUMERIC || precision_ != RCSG_PREC_F16 || !(sync || profile_) || f16_widened_ >= 3)
+            throw;
+        ++f16_widened_;
+        for (const StepInfo& st : steps_) node_exp_[st.r] += 8;
+        bound_groups_.clear();
+        run(groups, configs, slice_begin, slice_end, d_acc, stats, sync);
+    }
 }
 
 void Program::sync() {
@@ -1145,9 +1158,11 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
         cudaFree(cal.d_max_);
         cal.d_max_ = nullptr;
     }
+    // RCSG_F16_BIAS (test knob): added to every calibrated exponent (negative = tighter)
+    const int bias = getenv("RCSG_F16_BIAS") ? atoi(getenv("RCSG_F16_BIAS")) : 0;
     for (const StepInfo& st : steps_) {
         const float m = mx[st.r];
-        node_exp_[st.r] = m > 0.f && std::isfinite(m) ? static_cast<int>(std::ceil(std::log2(m))) - 10
+        node_exp_[st.r] = m > 0.f && std::isfinite(m) ? static_cast<int>(std::ceil(std::log2(m))) - 10 + bias
                                                       : node_exp_[st.a] + node_exp_[st.b];
     }
     calibrated_ = true;
@@ -1624,6 +1639,16 @@ void Program::run_bound(size_t n_groups, const std::vector<uint64_t>& configs, u
         }
         launch_kahan(d_res_, d_comp_, d_part_, acc_n, stream_);
         ++launches_;
+    }
+    if (sync) {  // a fault must surface before the caller's buffer is touched (fp16 retry)
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        int32_t fault = INT_MAX;
+        CUDA_OK(cudaMemcpy(&fault, d_fault_, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (fault != INT_MAX) {
+            fault_pending_ = false;
+            throw Failure{RCSG_ERR_NUMERIC, "non-finite intermediate at contraction step " + std::to_string(fault),
+                          fault};
+        }
     }
     // d_acc += res
     launch_fill(d_comp_, 0.0, acc_n, stream_);

@@ -224,6 +224,7 @@ class Program {
     // fp16 mode: per-node storage exponents (value stored times 2^-e)
     std::vector<int> node_exp_;
     bool calibrated_ = false;
+    int f16_widened_ = 0;  // fp16 headroom widenings after overflow (at most 3 x 2^8)
     bool record_max_ = false;
     float* d_max_ = nullptr;
     // copies of the compile inputs (re-tree and the fp16 calibration program);

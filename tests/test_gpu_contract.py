@@ -289,3 +289,15 @@ def test_group_chunks_under_a_tight_memory_budget():
     assert st2.passes > st1.passes  # passes count (config, slice, chunk) triples
     for g in range(len(fixed)):
         assert rel(many[g], one[g]) < 1e-12, g
+
+
+def test_f16_overflow_widens_scales_and_retries(monkeypatch):
+    """fp16 scales 2^12 too tight (RCSG_F16_BIAS=-12) overflow on the first try;
+    a synchronous call then widens the headroom and reruns, and the amplitudes
+    still meet the fp16 tolerance against the oracle."""
+    monkeypatch.setenv("RCSG_F16_BIAS", "-12")
+    p, fixed = cfg1(32)
+    pn = port.PortNet(p.net, p.plan)
+    got = p.contract_groups(fixed, precision="f16")
+    for g, fb in enumerate(fixed):
+        assert rel(got[g], pn.contract_group(int(fb))) < TOL["f16"], g
