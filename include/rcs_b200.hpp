@@ -18,6 +18,7 @@
 #include <map>
 #include <span>
 #include <stdexcept>
+#include <iosfwd>
 #include <string>
 #include <utility>
 #include <vector>
@@ -222,6 +223,10 @@ StateVector simulate_exact(const Circuit& circuit, int cap = kDefaultExactCap);
 double ideal_probability(const StateVector& state, const std::string& bitstring);
 std::uint64_t bitstring_to_index(const std::string& bitstring);
 std::string index_to_bitstring(std::uint64_t index, int n_qubits);
+// Binary amplitude dump (reference format): 16-byte header {"QSVD", version u32 = 1,
+// n_qubits u32, pad u32}, then little-endian float64 (re, im) interleaved.
+void dump_amplitudes(const StateVector& state, std::ostream& out);
+StateVector load_amplitudes(std::istream& in);
 
 // Precision of the device executor: "f64" (default; reference-grade), "f32",
 // "tf32" (tcgen05 tensor cores), "3xtf32" (split-tf32 tensor cores, fp32-grade),

@@ -4,6 +4,8 @@
 // reference executor (contraction_engine.cpp:132-354); every contraction runs
 // on the GPU (rcsg.h) — there is no CPU execution path.
 #include <chrono>
+#include <istream>
+#include <ostream>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -272,6 +274,33 @@ std::string index_to_bitstring(std::uint64_t index, int n_qubits) {
     for (int q = 0; q < n_qubits; ++q)
         if ((index >> q) & 1) s[q] = '1';
     return s;
+}
+
+void dump_amplitudes(const StateVector& state, std::ostream& out) {
+    char header[16] = {0};
+    const std::uint32_t version = 1, n = static_cast<std::uint32_t>(state.n_qubits);
+    std::memcpy(header, "QSVD", 4);
+    std::memcpy(header + 4, &version, 4);
+    std::memcpy(header + 8, &n, 4);
+    out.write(header, 16);
+    // std::complex<double> is two contiguous doubles (re, im): one bulk write
+    out.write(reinterpret_cast<const char*>(state.amps.data()),
+              static_cast<std::streamsize>(state.amps.size() * sizeof(cplx)));
+}
+
+StateVector load_amplitudes(std::istream& in) {
+    char header[16];
+    in.read(header, 16);
+    if (!in || std::memcmp(header, "QSVD", 4) != 0) throw ConfigError("bad amplitude dump header");
+    std::uint32_t n = 0;
+    std::memcpy(&n, header + 8, 4);
+    if (n > 40) throw ConfigError("bad amplitude dump header");
+    StateVector st;
+    st.n_qubits = static_cast<int>(n);
+    st.amps.resize(std::size_t{1} << n);
+    in.read(reinterpret_cast<char*>(st.amps.data()), static_cast<std::streamsize>(st.amps.size() * sizeof(cplx)));
+    if (!in) throw ConfigError("truncated amplitude dump");
+    return st;
 }
 
 double ideal_probability(const StateVector& state, const std::string& bitstring) {

@@ -3,6 +3,7 @@
 // parts, so it runs without a GPU.  Prints a few values the Python test
 // compares with the reference library.
 #include <cstdio>
+#include <sstream>
 
 #include "rcs_b200.hpp"
 
@@ -15,6 +16,16 @@ int main() {
                 static_cast<double>(plan.flops_per_slice));
     std::printf("group0 %llu group63 %llu dup %d\n", static_cast<unsigned long long>(cs.group_fixed[0]),
                 static_cast<unsigned long long>(cs.group_fixed[63]), cs.duplicate_groups);
+    {  // QSVD round trip (reference format)
+        rcs::StateVector sv;
+        sv.n_qubits = 3;
+        for (int i = 0; i < 8; ++i) sv.amps.push_back(rcs::cplx(0.5 * i, -0.25 * i));
+        std::stringstream ss;
+        rcs::dump_amplitudes(sv, ss);
+        const std::string bytes = ss.str();
+        const auto back = rcs::load_amplitudes(ss);
+        std::printf("qsvd %zu %d %d\n", bytes.size(), back.n_qubits, back.amps == sv.amps ? 1 : 0);
+    }
     try {  // device calls raise DeviceError without a GPU (no silent CPU fallback)
         rcs::set_precision("f16");
         auto amps = rcs::contract_group(net, plan, nullptr, 0, cs.group_fixed[0]);

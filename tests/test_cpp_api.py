@@ -25,4 +25,5 @@ def test_cpp_drop_in_compiles_links_and_matches_reference(tmp_path, ref):
     fixed, dup = ref.candidates(30, list(range(6)), 64, ref.split_next(1, 0xCA11D))
     g0, g63 = out[1].split()[1], out[1].split()[3]
     assert int(g0) == int(fixed[0]) and int(g63) == int(fixed[63])
-    assert out[2].startswith("device")
+    assert out[2] == "qsvd 144 3 1"  # 16-byte header + 8 x 16 bytes, round trip exact
+    assert out[3].startswith("device")
