@@ -191,7 +191,6 @@ struct TcParams {
     int32_t* fault;
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
-    int32_t dbg;            // tuning knob (RCSG_TC_DBG): 1 = skip the epilogue's global stores
     int32_t b_resident;     // B identical for every tile: loaded once per stage slot
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
@@ -330,7 +329,7 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
             val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
         }
         const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
-        if (row0 + r < p.m && p.dbg != 1) *reinterpret_cast<uint4*>(base + roff + col_off[it]) = val;
+        if (row0 + r < p.m) *reinterpret_cast<uint4*>(base + roff + col_off[it]) = val;
     }
     __syncwarp();
     return bad;
@@ -651,10 +650,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const int s = it % STAGES;
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* st = smem + s * S::kStage;
-                    if (p.dbg == 3) {  // tuning: no loads
-                        mbar_expect_tx(&full[s], 0);
-                        continue;
-                    }
                     // B resident: the same single B tile for every tile (one N tile, one
                     // K block, unbatched B) is loaded once into each stage slot
                     const bool load_b = !(p.b_resident && it >= STAGES);
@@ -688,16 +683,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const uint8_t* st = smem + s * S::kStage;
                     const uint64_t dar = smem_desc<RB>(st), dai = smem_desc<RB>(st + S::kATile);
                     const uint64_t dbr = smem_desc<RB>(st + 2 * S::kATile), dbi = smem_desc<RB>(st + 2 * S::kATile + S::kBTile);
-                    if (p.dbg != 2) {  // tuning: dbg 2 skips the MMAs
 #pragma unroll
-                        for (int jj = 0; jj < RB / 32; ++jj) {  // 32-B K slices (one MMA K each)
-                            const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
-                            const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
-                            mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
-                            mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
-                            mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
-                            mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
-                        }
+                    for (int jj = 0; jj < RB / 32; ++jj) {  // 32-B K slices (one MMA K each)
+                        const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
+                        const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
+                        mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                        mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                        mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                        mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
                     }
                     mma_commit(&empty[s]);
                 }
@@ -844,8 +837,6 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.om = g.om;
     p.scale_exp = g.scale_exp;
     p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : 0;
-    static const int dbg = getenv("RCSG_TC_DBG") ? atoi(getenv("RCSG_TC_DBG")) : 0;
-    p.dbg = dbg;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + kbk<E, RB> - 1) / kbk<E, RB>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
