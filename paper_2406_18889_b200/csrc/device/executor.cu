@@ -132,7 +132,7 @@ struct TreeNode {
 
 struct TreeCost {
     const std::vector<uint64_t>& groups;
-    double pf, bw, elem;
+    double pf, bw, elem, lat;
     std::map<uint64_t, double> nv_cache;
     double nvar(uint64_t mask) {
         if (!mask) return 1.0;
@@ -168,7 +168,7 @@ struct TreeCost {
             mult = std::max(va, vb);
             rd = va * la + vb * lb;
         }
-        const double t = std::max(8.0 * un * mult / pf, 2.0 * elem * (rd + vz * lz) / bw) + 4e-6;
+        const double t = std::max(8.0 * un * mult / pf, 2.0 * elem * (rd + vz * lz) / bw) + lat;
         // level-0 steps run once per call, not per pass
         return std::max(x.level, y.level) == 0 ? 0.01 * t : t;
     }
@@ -1093,8 +1093,12 @@ void Program::retree(const std::vector<uint64_t>& groups) {
     std::vector<uint64_t> uniq = groups;
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    const double pf = precision_ >= RCSG_PREC_BF16 ? 1.2e15 : (precision_ == RCSG_PREC_TF32 ? 6e14 : 5e13);
-    TreeCost cost{uniq, pf, 6e12, static_cast<double>(elem_bytes_), {}};
+    double pf = precision_ >= RCSG_PREC_BF16 ? 1.2e15 : (precision_ == RCSG_PREC_TF32 ? 6e14 : 5e13);
+    double bw = 6e12, lat = 4e-6;
+    if (const char* e = getenv("RCSG_TREE_PF")) pf = atof(e);  // cost-model knobs (experiments)
+    if (const char* e = getenv("RCSG_TREE_BW")) bw = atof(e);
+    if (const char* e = getenv("RCSG_TREE_LAT")) lat = atof(e);
+    TreeCost cost{uniq, pf, bw, static_cast<double>(elem_bytes_), lat, {}};
     for (int i = 0; i < n_leaves_; ++i) {
         t[i].labels = nodes_[i].labels;
         std::sort(t[i].labels.begin(), t[i].labels.end());
