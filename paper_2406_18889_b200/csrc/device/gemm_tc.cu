@@ -174,6 +174,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 struct TcParams {
     int64_t m, n, k;        // per-variant GEMM shape
     int64_t batch;          // C variants
@@ -200,49 +212,49 @@ struct TcParams {
 // split-K workspace (fp32, row-major), or to C (element type) row-major
 // (vectorised for fp32) or through the output scatter map into the
 // consumer's layout.
-template <typename E>
+template <typename E, int CW = 32>
 __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_t v, int64_t row, int64_t col0,
                                             float* x, int plane, const int64_t* tn_lo, int64_t row_off,
                                             int64_t col_base) {
     bool bad = false;
     if (p.ws_split) {  // raw partials; the reduction scales and checks
 #pragma unroll
-        for (int i = 0; i < 32; ++i) bad |= !isfinite(x[i]);
+        for (int i = 0; i < CW; ++i) bad |= !isfinite(x[i]);
         float* pr = static_cast<float*>(p.c) + split * p.ws_split + v * p.c_batch + plane * p.c_plane + row * p.n + col0;
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) pr[i] = x[i];
+        for (int i = 0; i < CW && col0 + i < p.n; ++i) pr[i] = x[i];
         return bad;
     }
     if (p.scale_exp) {
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] *= sc;
+        for (int i = 0; i < CW; ++i) x[i] *= sc;
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) bad |= unstorable<E>(x[i]);
+    for (int i = 0; i < CW; ++i) bad |= unstorable<E>(x[i]);
     E* cpl = static_cast<E*>(p.c) + v * p.c_batch + plane * p.c_plane;
     if (!p.om.scatter) {
         E* pr = cpl + row * p.n + col0;
         if constexpr (sizeof(E) == 4) {
-            if (col0 + 32 <= p.n && (p.n & 3) == 0) {
+            if (col0 + CW <= p.n && (p.n & 3) == 0) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 4)
+                for (int i = 0; i < CW; i += 4)
                     *reinterpret_cast<float4*>(pr + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
                 return bad;
             }
         }
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) store_c(pr + i, x[i]);
+        for (int i = 0; i < CW && col0 + i < p.n; ++i) store_c(pr + i, x[i]);
         return bad;
     }
     const int64_t base = row_off + col_base;
     const int sh = p.om.n_pos[0];
     const bool contig = p.om.n_bits >= 5 && p.om.n_pos[1] == sh + 1 && p.om.n_pos[2] == sh + 2 &&
                         p.om.n_pos[3] == sh + 3 && p.om.n_pos[4] == sh + 4;
-    if (col0 + 32 <= p.n && contig) {
+    if (col0 + CW <= p.n && contig) {
         // column bits contiguous at bit sh (sh == 0: per-thread contiguous run)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) store_c(cpl + base + (static_cast<int64_t>(i) << sh), x[i]);
+        for (int i = 0; i < CW; ++i) store_c(cpl + base + (static_cast<int64_t>(i) << sh), x[i]);
     } else {
-        for (int i = 0; i < 32 && col0 + i < p.n; ++i) store_c(cpl + base + tn_lo[i], x[i]);
+        for (int i = 0; i < CW && col0 + i < p.n; ++i) store_c(cpl + base + tn_lo[i], x[i]);
     }
     return bad;
 }
@@ -276,7 +288,7 @@ __device__ __forceinline__ uint4 pack8(const float* x) {
 }
 
 // one plane of a warp's 32x32 chunk (rows row0.., columns col0..)
-template <typename E>
+template <typename E, int CW = 32>
 __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v, int64_t row0, E* stage, float* x,
                                                    int plane, const int64_t* tn_lo, int lane, int64_t my_off,
                                                    int64_t col_base) {
@@ -284,32 +296,35 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
     if (p.scale_exp) {
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] *= sc;
+        for (int i = 0; i < CW; ++i) x[i] *= sc;
     }
     const bool live = row0 + lane < p.m;
     if (live) {  // one range check on the max magnitude, plus NaN
         float mx = 0.f;
         bool nan = false;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < CW; ++i) {
             mx = fmaxf(mx, fabsf(x[i]));
             nan |= x[i] != x[i];
         }
         bad = nan || unstorable<E>(mx);
     }
     E* const base = static_cast<E*>(p.c) + v * p.c_batch + plane * p.c_plane + col_base;
-    int64_t col_off[4];  // this lane's column offset in each of the 4 rounds
+    // the chunk is 32 rows x CW columns = 4 * CW / 8 sixteen-byte vectors per lane... per warp:
+    // NIT rounds of 32 lanes; VPR vectors per row
+    constexpr int VPR = CW / 8, NIT = CW / 8;
+    int64_t col_off[NIT];  // this lane's column offset in each round
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
+    for (int it = 0; it < NIT; ++it) {
         const int id = it * 32 + lane;
-        col_off[it] = p.epi == 3 ? tn_lo[id >> 2] : tn_lo[(p.epi == 2 ? (id >> 5) : (id & 3)) * 8];
+        col_off[it] = p.epi == 3 ? tn_lo[id >> 2] : tn_lo[(p.epi == 2 ? (id >> 5) : (id % VPR)) * 8];
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < VPR; ++i)
         *reinterpret_cast<uint4*>(stage + epi_at(lane, 8 * i)) = pack8<E>(x + 8 * i);
     __syncwarp();
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
+    for (int it = 0; it < NIT; ++it) {
         const int id = it * 32 + lane;
         int r;
         uint4 val;
@@ -324,8 +339,8 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
             for (int e = 0; e < 8; ++e) t.e[e] = stage[epi_at(r + e, c)];
             val = t.u;
         } else {  // 8 consecutive columns of row r
-            const int cv = p.epi == 2 ? (id >> 5) : (id & 3);
-            r = p.epi == 2 ? (id & 31) : (id >> 2);
+            const int cv = p.epi == 2 ? (id >> 5) : (id % VPR);
+            r = p.epi == 2 ? (id & 31) : (id / VPR);
             val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
         }
         const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
@@ -724,22 +739,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
             mbar_wait(&tfull[ab], (j / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
+            constexpr int CW = BN / 2 < 32 ? BN / 2 : 32;  // columns per chunk (16 when BN = 32)
 #pragma unroll 1
-            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
-                const int64_t col0 = c.n0 + c0;  // multiple of 32
-                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, 5, col0, lane) +
+            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += CW) {
+                const int64_t col0 = c.n0 + c0;  // multiple of CW
+                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, CW == 32 ? 5 : 4, col0, lane) +
                                                             (col0 >> p.om.n_bits) * p.om.n_vstride
                                                       : col0;
-                float x[32];
-                tmem_ld32(base + c0, x);
+                float x[CW];
+                if constexpr (CW == 32) tmem_ld32(base + c0, x);
+                else tmem_ld16(base + c0, x);
                 if constexpr (sizeof(E) == 2) {
-                    if (p.epi && p.splits == 1 && col0 + 32 <= p.n) {
-                        bad |= store_chunk_staged<E>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
-                                                     row < p.m ? row_off : 0, col_base);
+                    if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
+                        bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
+                                                         row < p.m ? row_off : 0, col_base);
                         continue;
                     }
                 }
-                if (row < p.m) bad |= store_chunk<E>(p, c.split, c.v, row, col0, x, plane, tn_lo, row_off, col_base);
+                if (row < p.m)
+                    bad |= store_chunk<E, CW>(p, c.split, c.v, row, col0, x, plane, tn_lo, row_off, col_base);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -902,6 +920,13 @@ bool gemm_tc_supported(const GemmArgs& g) {
 template <typename E>
 void launch_2byte(const GemmArgs& g, cudaStream_t st) {
     static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
+    static const bool narrow_n = getenv("RCSG_TC_NARROW_N") == nullptr || atoi(getenv("RCSG_TC_NARROW_N")) != 0;
+    if (narrow_n && g.n <= 32) {  // BN = 32: every epilogue warp owns a 16-column chunk
+        if (narrow && g.k <= 16) launch<32, 12, E, 32>(g, st);
+        else if (narrow && g.k <= 32) launch<32, 8, E, 64>(g, st);
+        else launch<32, 4, E>(g, st);
+        return;
+    }
     if (narrow && g.k <= 16) {
         if (g.n >= 128) launch<128, 12, E, 32>(g, st);
         else launch<64, 12, E, 32>(g, st);
