@@ -52,7 +52,7 @@ class rcsg_candidates(C.Structure):
 # exported symbols and their restypes (everything else returns int status)
 RCSG_SYMBOLS = [
     "rcsg_last_error", "rcsg_set_device", "rcsg_compile", "rcsg_compile_pinned", "rcsg_program_free",
-    "rcsg_program_set_profile", "rcsg_program_stream", "rcsg_gemm_selftest", "rcsg_gemm_check_f16",
+    "rcsg_program_set_profile", "rcsg_program_stream", "rcsg_gemm_selftest", "rcsg_gemm_check_f16", "rcsg_gemm_check_bf16",
     "rcsg_contract_groups", "rcsg_contract_groups_device", "rcsg_execute_assignment", "rcsg_topk",
     "rcsg_topk_probs", "rcsg_direct_sample", "rcsg_direct_sample_probs", "rcsg_xeb",
     "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy", "rcsg_program_sync", "rcsg_statevector",

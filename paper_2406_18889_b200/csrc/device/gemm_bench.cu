@@ -178,21 +178,23 @@ extern "C" int rcsg_gemm_bench_f16(int64_t m, int64_t n, int64_t k, int32_t m_bi
 
 namespace rcsg {
 namespace {
-__global__ void fill_half(__half* p, int64_t n, uint64_t seed) {
+template <typename T>
+__global__ void fill_half(T* p, int64_t n, uint64_t seed) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ull;
         z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
         z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
         z ^= z >> 31;
-        p[i] = __float2half(static_cast<float>(static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0));
+        store_c(p + i, static_cast<float>(static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0));
     }
 }
-__global__ void diff_half(const __half* a, const __half* b, int64_t n, double* out) {
+template <typename T>
+__global__ void diff_half(const T* a, const T* b, int64_t n, double* out) {
     double num = 0, den = 0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double x = __half2float(a[i]), y = __half2float(b[i]);
+        const double x = load_c(a + i), y = load_c(b + i);
         num += (x - y) * (x - y);
         den += y * y;
     }
@@ -202,12 +204,13 @@ __global__ void diff_half(const __half* a, const __half* b, int64_t n, double* o
 }  // namespace
 }  // namespace rcsg
 
-// fp16 tensor-core GEMM vs the fp16 SIMT kernel on random operands, through an
+// 2-byte tensor-core GEMM vs the SIMT kernel of the same storage type on random operands, through an
 // explicit output map (every epilogue kind / K-tile width); rel = ||TC-SIMT|| / ||SIMT||.
-extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
-                                   const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+template <typename T>
+int gemm_check(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits, const int8_t* m_pos,
+               const int8_t* n_pos, double* out_rel) {
     try {
-        __half *a, *b, *c1, *c2;
+        T *a, *b, *c1, *c2;
         int32_t* fault;
         double* d;
         const int64_t c_el = m * n;
@@ -237,9 +240,9 @@ extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bi
         for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
         if (!gemm_tc_supported(g)) return RCSG_ERR_CONFIG;
         g.c = c1;
-        launch_gemm_tc(g, 2, 0);
+        launch_gemm_tc(g, elem, 0);
         g.c = c2;
-        launch_gemm_simt<f16>(g, 0);
+        launch_gemm_simt<T>(g, 0);
         cudaMemset(d, 0, 16);
         diff_half<<<1024, 256>>>(c1, c2, 2 * c_el, d);
         double h[2] = {0, 1};
@@ -256,4 +259,15 @@ extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bi
     } catch (...) {
         return RCSG_ERR_DEVICE;
     }
+}
+
+extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                   const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+    return gemm_check<f16>(2, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
+}
+
+// the same check for bf16 operands (tcgen05 kind::f16 with BF16 inputs)
+extern "C" int rcsg_gemm_check_bf16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                    const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+    return gemm_check<bf16>(1, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
 }

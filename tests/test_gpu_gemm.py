@@ -1,7 +1,8 @@
 """fp16 tensor-core complex GEMM (tcgen05, every epilogue kind and K-tile
 width) against the fp16 SIMT kernel on random operands through explicit output
-maps.  rel = ||TC - SIMT|| / ||SIMT||: both round the same fp32-accumulated
-values to fp16, so the bound is a few fp16 ulps (tolerance 2e-3)."""
+maps, for fp16 and bf16 storage.  rel = ||TC - SIMT|| / ||SIMT||: both round
+the same fp32-accumulated values to the storage type, so the bound is a few
+ulps (2e-3 fp16, 1.6e-2 bf16)."""
 import ctypes as C
 
 import pytest
@@ -24,12 +25,14 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("dtype,tol", [("f16", 2e-3), ("bf16", 1.6e-2)])
 @pytest.mark.parametrize("name,m,n,k,mp,npos", CASES, ids=[c[0] for c in CASES])
-def test_tc_gemm_matches_simt(name, m, n, k, mp, npos):
+def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol):
     lib = _native.lib()
+    check = lib.rcsg_gemm_check_f16 if dtype == "f16" else lib.rcsg_gemm_check_bf16
     a = (C.c_int8 * max(len(mp), 1))(*mp)
     b = (C.c_int8 * max(len(npos), 1))(*npos)
     rel = C.c_double()
-    rc = lib.rcsg_gemm_check_f16(C.c_int64(m), C.c_int64(n), C.c_int64(k), len(mp), len(npos), a, b, C.byref(rel))
+    rc = check(C.c_int64(m), C.c_int64(n), C.c_int64(k), len(mp), len(npos), a, b, C.byref(rel))
     assert rc == 0
-    assert rel.value < 2e-3, rel.value
+    assert rel.value < tol, rel.value
