@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (int b = 0; b < static_cast<int>(NBUF); ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 16);
+            mbar_init(&tempty[b], 8);  // one epilogue group (8 warps) drains each buffer
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -712,10 +712,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 mma_commit(&tfull[ab]);
             }
         }
-    } else {  // ---- epilogue warps 2..17: TMEM lane quarter warp % 4; plane and column half from (warp - 2) / 4
+    } else {  // ---- epilogue warps 2..17: two groups of 8 take alternate tiles; TMEM lane quarter warp % 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int sub = (warp - 2) >> 2;
-        const int plane = sub & 1, half = sub >> 1;
+        const int plane = sub & 1, grp = sub >> 1;
         E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
         // output row offset = tile part (bits >= 7 of the row, warp-uniform) + this
         // lane's part (bits 0..6, fixed), when the map's row bits cover a tile
@@ -725,8 +725,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         bool bad = false;
         uint32_t j = 0;
         TileIter ti;
-        ti.init(p, blockIdx.x, gridDim.x);
-        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j, ti.next()) {
+        const int64_t t0 = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x;
+        ti.init(p, static_cast<uint32_t>(t0), 2 * gridDim.x);
+        j = static_cast<uint32_t>(grp);
+        for (int64_t t = t0; t < total_tiles; t += 2 * static_cast<int64_t>(gridDim.x), j += 2, ti.next()) {
             const TileCoord c = ti.coord<BN, E, RB>(p);
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
             constexpr int CW = BN / 2 < 32 ? BN / 2 : 32;  // columns per chunk (16 when BN = 32)
 #pragma unroll 1
-            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += CW) {
+            for (int c0 = 0; c0 < BN; c0 += CW) {
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, CW == 32 ? 5 : 4, col0, lane) +
                                                             (col0 >> p.om.n_bits) * p.om.n_vstride
