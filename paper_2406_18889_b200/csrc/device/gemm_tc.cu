@@ -614,6 +614,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // so the MMA runs ahead of the epilogue by NBUF - 1 tiles
     constexpr uint32_t NBUF = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
     constexpr uint32_t kCols = NBUF * 2 * BN;
+    // epilogue groups = tiles in flight (NBUF % NG == 0): 4 for the narrow BN = 32 tiles, else 2
+    // (measured: 4 groups help n <= 32, slightly hurt BN = 64)
+    constexpr int NG = (BN == 32 && NBUF >= 4) ? 4 : 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (int b = 0; b < static_cast<int>(NBUF); ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 8);  // one epilogue group (8 warps) drains each buffer
+            mbar_init(&tempty[b], 16 / NG);  // one epilogue group drains each buffer
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -714,8 +717,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
     } else {  // ---- epilogue warps 2..17: two groups of 8 take alternate tiles; TMEM lane quarter warp % 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int sub = (warp - 2) >> 2;
-        const int plane = sub & 1, grp = sub >> 1;
+        const int sub = (warp - 2) >> 2;  // 0..3
+        // NG = 2: groups of 8 warps, one plane each; NG = 4: groups of 4 warps, both planes
+        const int grp = NG == 4 ? sub : (sub >> 1);
+        const int plane_lo = NG == 4 ? 0 : (sub & 1), plane_hi = NG == 4 ? 2 : plane_lo + 1;
         E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
         // output row offset = tile part (bits >= 7 of the row, warp-uniform) + this
         // lane's part (bits 0..6, fixed), when the map's row bits cover a tile
@@ -726,9 +731,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         uint32_t j = 0;
         TileIter ti;
         const int64_t t0 = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x;
-        ti.init(p, static_cast<uint32_t>(t0), 2 * gridDim.x);
+        ti.init(p, static_cast<uint32_t>(t0), NG * gridDim.x);
         j = static_cast<uint32_t>(grp);
-        for (int64_t t = t0; t < total_tiles; t += 2 * static_cast<int64_t>(gridDim.x), j += 2, ti.next()) {
+        for (int64_t t = t0; t < total_tiles; t += NG * static_cast<int64_t>(gridDim.x), j += NG, ti.next()) {
             const TileCoord c = ti.coord<BN, E, RB>(p);
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
@@ -740,10 +745,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
             else row_off = row < p.m ? out_row_off(p.om, p.n, row) : 0;
             mbar_wait(&tfull[ab], (j / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
             constexpr int CW = BN / 2 < 32 ? BN / 2 : 32;  // columns per chunk (16 when BN = 32)
 #pragma unroll 1
+            for (int plane = plane_lo; plane < plane_hi; ++plane)
+#pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += CW) {
+                const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, CW == 32 ? 5 : 4, col0, lane) +
                                                             (col0 >> p.om.n_bits) * p.om.n_vstride
