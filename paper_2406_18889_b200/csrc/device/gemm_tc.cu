@@ -204,6 +204,7 @@ struct TcParams {
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
     int32_t b_resident;     // B identical for every tile: loaded once per stage slot
+    int32_t ng;             // persistent kernel: epilogue warp groups (tiles in flight), 1 / 2 / 4
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -614,9 +615,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // so the MMA runs ahead of the epilogue by NBUF - 1 tiles
     constexpr uint32_t NBUF = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
     constexpr uint32_t kCols = NBUF * 2 * BN;
-    // epilogue groups = tiles in flight (NBUF % NG == 0): 4 for the narrow BN = 32 tiles, else 2
-    // (measured: 4 groups help n <= 32, slightly hurt BN = 64)
-    constexpr int NG = (BN == 32 && NBUF >= 4) ? 4 : 2;
+    // epilogue groups = tiles in flight (NBUF % NG == 0), chosen by the host (p.ng: 1, 2 or 4)
+    const int NG = p.ng;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
@@ -718,9 +718,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
     } else {  // ---- epilogue warps 2..17: two groups of 8 take alternate tiles; TMEM lane quarter warp % 4
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int sub = (warp - 2) >> 2;  // 0..3
-        // NG = 2: groups of 8 warps, one plane each; NG = 4: groups of 4 warps, both planes
-        const int grp = NG == 4 ? sub : (sub >> 1);
+        // NG = 1: all 16 warps on each tile (plane x column half); NG = 2: groups of 8 warps,
+        // one plane each, all columns; NG = 4: groups of 4 warps, both planes
+        const int grp = NG == 4 ? sub : (NG == 2 ? (sub >> 1) : 0);
         const int plane_lo = NG == 4 ? 0 : (sub & 1), plane_hi = NG == 4 ? 2 : plane_lo + 1;
+        const int col_lo = NG == 1 ? (sub >> 1) * (BN / 2) : 0, col_hi = NG == 1 ? col_lo + BN / 2 : BN;
         E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
         // output row offset = tile part (bits >= 7 of the row, warp-uniform) + this
         // lane's part (bits 0..6, fixed), when the map's row bits cover a tile
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll 1
             for (int plane = plane_lo; plane < plane_hi; ++plane)
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += CW) {
+            for (int c0 = col_lo; c0 < col_hi; c0 += CW) {
                 const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, CW == 32 ? 5 : 4, col0, lane) +
@@ -874,6 +876,16 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.splits = splits;
     p.k_chunk = chunk_blocks * kbk<E, RB>;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
+    {
+        // two tiles in flight help short (memory-bound) tiles and cost nothing on long K
+        // (measured); four help BN = 32.  NBUF must be a multiple of the group count.
+        constexpr int nbuf = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
+        int ng = (BN == 32 && nbuf >= 4) ? 4 : 2;
+        if (const char* e = getenv("RCSG_TC_NG")) ng = atoi(e);
+        if (ng != 1 && ng != 2 && ng != 4) ng = 1;
+        while (ng > 1 && nbuf % ng) ng /= 2;
+        p.ng = ng;
+    }
     p.b_resident = (p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
                     !(getenv("RCSG_TC_NO_BRES") != nullptr)) ? 1 : 0;
     if (splits == 1) {
