@@ -39,3 +39,21 @@ def test_statevector_30_qubits_norm():
     p.exact_state_device(state.data_ptr())
     norm = float(torch.sum(state.real ** 2 + state.imag ** 2))
     assert abs(norm - 1.0) < 1e-9
+
+
+def test_statevector_rejects_bad_input():
+    """Capacity and configuration errors, like simulate_exact / apply_gate
+    (statevector.cpp:79-82): CapacityError above the cap, ConfigError for bad
+    gate targets."""
+    import ctypes as C
+    import torch
+    from paper_2406_18889_b200 import _native
+    lib = _native.lib()
+    state = torch.empty(16, dtype=torch.complex128, device="cuda")
+    nt = (C.c_int32 * 1)(2)
+    tg = (C.c_int32 * 2)(1, 1)  # a two-qubit gate on the same qubit twice
+    u = (C.c_double * 32)(*([1.0] + [0.0] * 31))
+    assert lib.rcsg_statevector(4, 1, nt, tg, u, C.c_void_p(state.data_ptr())) == _native.RCSG_ERR_CONFIG
+    tg2 = (C.c_int32 * 2)(0, 7)  # target outside the register
+    assert lib.rcsg_statevector(4, 1, nt, tg2, u, C.c_void_p(state.data_ptr())) == _native.RCSG_ERR_CONFIG
+    assert lib.rcsg_statevector(40, 0, nt, tg, u, C.c_void_p(state.data_ptr())) == _native.RCSG_ERR_CAPACITY
