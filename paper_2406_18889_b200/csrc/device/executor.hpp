@@ -1,18 +1,27 @@
 // Device step-program executor (host side of the contraction path).
 //
 // compile(): turns (network, plan, label roles) into a static program:
-//   - every tree node gets a LEVEL: 0 = depends on nothing that changes
-//     (computed once per run), 1 = depends on per-pass labels (slice /
-//     broken-edge / pinned bits; recomputed each pass), 2 = depends on the
-//     candidate group (the non-open output legs; recomputed per group chunk);
+//   - every tree node gets a LEVEL: 0 = depends on nothing that changes, 1 =
+//     depends on per-pass labels (slice / broken-edge / pinned bits), 2 =
+//     depends on the candidate group (the non-open output legs); level-2 nodes
+//     without pass labels form PHASE 3 (group-only), so the execution phases are
+//     0 constant, 3 group-only (both cached per binding), 1 per pass, 2 per pass
+//     and group;
 //   - level-2 nodes are stored as [variants][payload]: one variant per DISTINCT
 //     projection of the chunk's group prefixes onto the output legs inside the
 //     node's subtree, so work shared by groups is done once (sparse-state
-//     group batching);
-//   - each plan step becomes permute(s) + one complex GEMM whose operand roles
-//     and layouts are fixed at compile time (TTGT, contraction_engine.cpp:87-128);
-//   - buffer offsets come from a first-fit simulation over the leveled
-//     schedule, so one arena allocation serves the whole run.
+//     group batching); a step with one varying operand folds its variants into
+//     M, two varying operands give a gathered batch or, for a full product with
+//     separable code bits, one GEMM with the variants in M and N;
+//   - each plan step is one complex GEMM whose operands are consumed K-major as
+//     [kept | contracted]; layouts are planned from the root backwards and
+//     every producer writes its consumer's layout through a bit-scatter map
+//     (no transposes; contract_pair, contraction_engine.cpp:87-128).
+// first run (group codes known): reassociate the tree for the batch (local
+// rotations under a time model), rebuild, calibrate fp16 scales, bind: chunk
+// capacity, first-fit arena plan over the phased schedule, slice tables for
+// small per-pass subtrees, and the per-pass task DAG (lane streams, captured
+// as a CUDA graph).
 // run(): loops configs x slices x group chunks, accumulating canonical-order
 // amplitudes per group (slices ascending, then compensated sum over configs,
 // contraction_engine.cpp:241-302).
