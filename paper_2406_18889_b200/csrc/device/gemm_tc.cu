@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const TcParams p) {
     using S = Smem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    // offset the __shared__ array itself (not via an integer cast) so the compiler keeps
+    // the shared address space and emits LDS/STS rather than generic loads and stores
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
     uint64_t* done = empty + STAGES;
@@ -618,7 +620,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // epilogue groups = tiles in flight (NBUF % NG == 0), chosen by the host (p.ng: 1, 2 or 4)
     const int NG = p.ng;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    // offset the __shared__ array itself (not via an integer cast) so the compiler keeps
+    // the shared address space and emits LDS/STS rather than generic loads and stores
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;

@@ -21,3 +21,4 @@ run("148-plain", 504, 16384, 2048, [], [])
 #run("big", 8192, 8192, 4096, [], [])
 run("618-real", 1 << 14, 1 << 11, 1 << 9, [0, 1, 2, 6, 8, 9, 12, 13, 15, 17, 19, 20, 21, 24], [3, 4, 5, 7, 10, 11, 14, 16, 18, 22, 23])
 run("148-real", 504, 16384, 2048, [7, 8, 9], list(range(0, 7)) + list(range(10, 17)))
+run("619-real", 1 << 21, 32, 16, [0, 1, 2, 3, 4, 7, 8, 9, 10, 11, 13, 14, 15, 16, 17, 18, 19, 20, 21, 24, 25], [5, 6, 12, 22, 23])
