@@ -195,6 +195,22 @@ def test_cfg2_full_size_properties():
         assert rel(both[g], exact[g]) < TOL["tf32"]
 
 
+@pytest.mark.parametrize("precision", ["f64", "tf32", "f16"])
+def test_sycamore53_sliced_matches_oracle(precision):
+    """Sycamore-53 layout (configs 3-4 topology) at m = 6, sliced to 2^7 slices by a
+    2^20 B budget: GPU groups vs the C restatement, plus slice-range linearity."""
+    p = pb.Problem(53, 6, "sycamore53", 1, list(range(6)), 1 << 20, "low").build()
+    assert p.n_slices == 128
+    pn = port.PortNet(p.net, p.plan)
+    fixed, _ = pb.build_candidate_set(53, list(range(6)), 4, pb.split_next(1, 0xCA11D))
+    got = p.contract_groups(fixed[:2], precision=precision)
+    for g in range(2):
+        assert rel(got[g], pn.contract_group(int(fixed[g]))) < TOL[precision], (g, precision)
+    a = p.contract_groups(fixed[:2], precision=precision, configs=None, slices=(0, 40))
+    b = p.contract_groups(fixed[:2], precision=precision, configs=None, slices=(40, 128))
+    assert rel(a + b, got) < (1e-12 if precision == "f64" else TOL[precision])
+
+
 def test_scheduler_blocks_on_gpu_equal_single_call():
     from paper_2406_18889_b200 import scheduler
     p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
