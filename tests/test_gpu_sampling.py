@@ -84,3 +84,38 @@ def test_topk_from_device_amplitudes_matches_port():
     seed = pb.split_next(1, 0xD1EC7)
     got = pb.api.direct_from_device_amps(12, [0, 1, 2], fixed, acc.data_ptr(), seed)
     assert np.array_equal(got, port.direct(12, [0, 1, 2], fixed, probs, seed))
+
+
+@pytest.mark.parametrize("precision", ["tf32", "bf16", "f16"])
+def test_topk_reduced_precision_matches_oracle_away_from_ties(precision):
+    """Top-k over reduced-precision GPU amplitudes against the f64 oracle's top-k
+    (selected bitstrings bit-exact wherever probabilities are not tied
+    within the precision's tolerance).  eps = the largest probability error of the
+    run; two picks are tied when their oracle probabilities differ by <= 2 eps."""
+    import torch
+    n, oq, M = 12, [0, 1, 2], 512
+    p = pb.Problem(n, 8, "grid(3,4)", 1, oq, 1 << 30, "low").build()
+    fixed, _ = pb.build_candidate_set(n, oq, M, pb.split_next(1, 0xCA11D))
+    pn = port.PortNet(p.net, p.plan)
+    want = np.array([pn.contract_group(int(f)) for f in fixed])
+    p_ref = np.abs(want) ** 2
+    acc = torch.zeros(M * 8 * 2, dtype=torch.float64, device="cuda")
+    p.contract_groups_device(fixed, acc.data_ptr(), precision=precision, configs=None)
+    got = acc.cpu().numpy().view(np.complex128).reshape(M, 8)
+    eps = np.abs(np.abs(got) ** 2 - p_ref).max()
+    assert eps < {"tf32": 1e-2, "f16": 1e-2, "bf16": 1e-1}[precision] * p_ref.max()
+    prob_of = {pb.member(n, oq, int(f), i): p_ref[g, i] for g, f in enumerate(fixed) for i in range(8)}
+    allp = np.array(sorted(prob_of.values()))
+    exact = 0
+    for k in (1, 16, 64, 256):
+        sel = pb.api.top_k_from_device_amps(n, oq, fixed, acc.data_ptr(), k)
+        ref_sel = port.top_k(n, oq, fixed, p_ref, k)
+        for a, b in zip(sel, ref_sel):
+            pa, pb_ = prob_of[int(a)], prob_of[int(b)]
+            assert abs(pa - pb_) <= 2 * eps, (k, a, b)
+            # isolated oracle probability (no other bitstring within 2 eps): the pick is exact
+            lo, hi = np.searchsorted(allp, pb_ - 2 * eps), np.searchsorted(allp, pb_ + 2 * eps, side="right")
+            if hi - lo == 1:
+                assert a == b, (k, a, b)
+                exact += 1
+    assert exact > 0
