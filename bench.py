@@ -148,9 +148,11 @@ def run_reference(args, rank, world):
                    CFG2["effort"]).build()
     fps = p.plan["flops_per_slice"]
     # one step = one (group, slice) pair of the reference executor; the W warm-up
-    # pairs and then the K timed pairs each run spread over all host threads
+    # pairs and then the timed pairs each run spread over all host threads
     cpu_reference_sample(threads, max(args.warmup, 1), 0)
-    rate, secs, f_sample, _ = cpu_reference_sample(threads, args.steps, args.warmup)
+    # at least one pair per host thread (whole waves), so a small K still uses every core
+    n_pairs = -(-max(args.steps, threads) // threads) * threads
+    rate, secs, f_sample, _ = cpu_reference_sample(threads, n_pairs, args.warmup)
     pairs_per_s = rate / fps
     value = pairs_per_s / args.groups
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -158,7 +160,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
             "config": {"workload": WORKLOAD, "groups_per_slice": args.groups},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"reference execute_assignment on {args.steps} (group, slice) pairs over "
+                             "sample": f"reference execute_assignment on {n_pairs} (group, slice) pairs over "
                                        f"{threads} threads in {secs:.1f} s, same circuit planned at budget 2^27 B "
                                        f"({f_sample:.3e} FLOP/pair); measured {rate / 1e9:.2f} GFLOP/s "
                                        f"extrapolated to the bench plan ({fps:.3e} FLOP/pair) x {args.groups} groups"},
