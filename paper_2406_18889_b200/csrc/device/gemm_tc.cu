@@ -314,38 +314,43 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
     // the chunk is 32 rows x CW columns = 4 * CW / 8 sixteen-byte vectors per lane... per warp:
     // NIT rounds of 32 lanes; VPR vectors per row
     constexpr int VPR = CW / 8, NIT = CW / 8;
-    int64_t col_off[NIT];  // this lane's column offset in each round
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int id = it * 32 + lane;
-        col_off[it] = p.epi == 3 ? tn_lo[id >> 2] : tn_lo[(p.epi == 2 ? (id >> 5) : (id % VPR)) * 8];
-    }
 #pragma unroll
     for (int i = 0; i < VPR; ++i)
         *reinterpret_cast<uint4*>(stage + epi_at(lane, 8 * i)) = pack8<E>(x + 8 * i);
     __syncwarp();
+    if (p.epi == 3) {
+        // 8 consecutive rows of a column pair (c, c + 1): eight 32-bit reads give
+        // both columns' vectors (low / high halves), half the shared loads of a
+        // per-column 16-bit gather
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int id = it * 32 + lane;
-        int r;
-        uint4 val;
-        if (p.epi == 3) {  // 8 consecutive rows of column c
-            const int c = id >> 2;
-            r = (id & 3) * 8;
-            union {
-                E e[8];
-                uint4 u;
-            } t;
+        for (int it = 0; it < NIT / 2; ++it) {
+            const int id = it * 32 + lane;
+            const int c = (id >> 2) * 2, r = (id & 3) * 8;
+            uint32_t w[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) t.e[e] = stage[epi_at(r + e, c)];
-            val = t.u;
-        } else {  // 8 consecutive columns of row r
-            const int cv = p.epi == 2 ? (id >> 5) : (id % VPR);
-            r = p.epi == 2 ? (id & 31) : (id / VPR);
-            val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
+            for (int e = 0; e < 8; ++e) w[e] = *reinterpret_cast<const uint32_t*>(stage + epi_at(r + e, c));
+            uint4 v0, v1;
+            v0.x = __byte_perm(w[0], w[1], 0x5410), v1.x = __byte_perm(w[0], w[1], 0x7632);
+            v0.y = __byte_perm(w[2], w[3], 0x5410), v1.y = __byte_perm(w[2], w[3], 0x7632);
+            v0.z = __byte_perm(w[4], w[5], 0x5410), v1.z = __byte_perm(w[4], w[5], 0x7632);
+            v0.w = __byte_perm(w[6], w[7], 0x5410), v1.w = __byte_perm(w[6], w[7], 0x7632);
+            const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
+            if (row0 + r < p.m) {
+                *reinterpret_cast<uint4*>(base + roff + tn_lo[c]) = v0;
+                *reinterpret_cast<uint4*>(base + roff + tn_lo[c + 1]) = v1;
+            }
         }
+        __syncwarp();
+        return bad;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {  // 8 consecutive columns of row r
+        const int id = it * 32 + lane;
+        const int cv = p.epi == 2 ? (id >> 5) : (id % VPR);
+        const int r = p.epi == 2 ? (id & 31) : (id / VPR);
+        const uint4 val = *reinterpret_cast<const uint4*>(stage + epi_at(r, cv * 8));
         const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
-        if (row0 + r < p.m) *reinterpret_cast<uint4*>(base + roff + col_off[it]) = val;
+        if (row0 + r < p.m) *reinterpret_cast<uint4*>(base + roff + tn_lo[cv * 8]) = val;
     }
     __syncwarp();
     return bad;
