@@ -335,7 +335,9 @@ def main():
     # roofline of the dominant kernel: the longest launch of the profiled pass,
     # bound by its arithmetic intensity (algorithmic FLOPs / algorithmic bytes)
     classes = {0: "SIMT GEMM", 1: "tcgen05 GEMM (gemm_tc_persistent / gemm_tc_kernel)", 2: "permute", 3: "GEMV"}
-    top_s = pst.top_ms * 1e-3
+    # average launch of the dominant plan step over the profiled pass (S launches), not its slowest
+    top_ms = pst.top_ms_sum / pst.top_launches if pst.top_launches else pst.top_ms
+    top_s = top_ms * 1e-3
     ai = pst.top_flops / pst.top_bytes if pst.top_bytes else float("inf")
     ridge = tc_peak * 1e12 / (hbm_peak * 1e9)
     if ai >= ridge:
@@ -356,10 +358,12 @@ def main():
         pass
     roofline = {"bound": bound, "kernel": f"plan step {pst.top_step}: {classes.get(int(pst.top_class), '?')}",
                 "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": traffic,
-                "algorithmic_per_launch": algo, "launch_ms": pst.top_ms, "flops": pst.top_flops,
+                "algorithmic_per_launch": algo, "launch_ms": top_ms, "launches_averaged": int(pst.top_launches),
+                "slowest_launch_ms": pst.top_ms, "flops": pst.top_flops,
                 "bytes": pst.top_bytes, "intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
                 "peak_note": pnote,
-                "share_of_step": pst.top_ms * S / pst.device_ms if pst.device_ms else None,  # profiled call = S passes
+                "share_of_step": pst.top_ms_sum / pst.device_ms if pst.device_ms and pst.top_launches
+                else (pst.top_ms * S / pst.device_ms if pst.device_ms else None),  # profiled call = S passes
                 "all_tensor_core_launches": {"achieved_tflops": tc_tflops, "frac_of_tensor_peak": tc_tflops / tc_peak,
                                              "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None}}
 

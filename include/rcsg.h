@@ -97,6 +97,9 @@ typedef struct rcsg_stats {
     uint64_t top_bytes;
     int64_t top_step;
     int64_t top_class;
+    double top_ms_sum;     /* summed time and count of every launch of plan step top_step */
+                           /* (same kernel class) in the profiled run: the average launch */
+    uint64_t top_launches;
 } rcsg_stats;
 
 typedef struct rcsg_program rcsg_program;

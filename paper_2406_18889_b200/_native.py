@@ -38,7 +38,8 @@ class rcsg_stats(C.Structure):
                 ("gemm_tc_ms", C.c_double), ("gemm_tc_flops", C.c_uint64),
                 ("permute_ms", C.c_double), ("permute_bytes", C.c_uint64),
                 ("gemm_tc_launches", C.c_uint64), ("top_ms", C.c_double), ("top_flops", C.c_uint64),
-                ("top_bytes", C.c_uint64), ("top_step", C.c_int64), ("top_class", C.c_int64)]
+                ("top_bytes", C.c_uint64), ("top_step", C.c_int64), ("top_class", C.c_int64),
+                ("top_ms_sum", C.c_double), ("top_launches", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -929,6 +929,7 @@ void Program::collect_marks(rcsg_stats* stats) {
     // RCSG_PROFILE_STEPS=N prints the N most expensive launches (stderr)
     const char* env = getenv("RCSG_PROFILE_STEPS");
     std::vector<std::pair<float, size_t>> order;
+    const int64_t prev_top = stats ? stats->top_step : -1;
     for (size_t i = 0; i < marks_.size(); ++i) {
         float ms = 0;
         CUDA_OK(cudaEventElapsedTime(&ms, ev_pool_[2 * i], ev_pool_[2 * i + 1]));
@@ -952,6 +953,17 @@ void Program::collect_marks(rcsg_stats* stats) {
             stats->top_step = m.step;
             stats->top_class = m.cat;
         }
+    }
+    if (stats) {  // every launch of the dominant plan step: its average launch time
+        if (stats->top_step != prev_top) {
+            stats->top_ms_sum = 0;
+            stats->top_launches = 0;
+        }
+        for (const auto& [ms, i] : order)
+            if (marks_[i].step == stats->top_step && marks_[i].cat == stats->top_class) {
+                stats->top_ms_sum += ms;
+                stats->top_launches += 1;
+            }
     }
     if (env) {
         std::sort(order.rbegin(), order.rend());
