@@ -332,7 +332,7 @@ def main():
     peak_note = (f"tf32 dense = 1/2 of {peak_kind} bf16 {bf16_peak:.1f} TF/s" if args.precision == "tf32"
                  else f"{peak_kind} dense bf16/fp16 peak {bf16_peak:.1f} TF/s")
 
-    # roofline of the dominant kernel: the longest launch of the profiled pass,
+    # roofline of the dominant kernel: the plan step with the longest launch of the profiled pass,
     # bound by its arithmetic intensity (algorithmic FLOPs / algorithmic bytes)
     classes = {0: "SIMT GEMM", 1: "tcgen05 GEMM (gemm_tc_persistent / gemm_tc_kernel)", 2: "permute", 3: "GEMV"}
     # average launch of the dominant plan step over the profiled pass (S launches), not its slowest
