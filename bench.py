@@ -11,17 +11,22 @@ own slices (s = rank, rank+N, ...) with no data-path collective; one NCCL
 all-reduce of the [M][2^l] partial amplitudes closes the timed region (the
 slice sum is the path's only exchange step).  Weak scaling.
 
-Metric: slice contractions/s (whole job).  Also reported: group-slice pairs/s,
-complex TFLOP/s (executed and reference-equivalent, 8 real FLOP per complex
-MAC), the tcgen05 GEMM roofline, a CPU baseline (the reference library on the
-host cores), an end-to-end number through the public API with host buffers,
-and XEB / samples/s of the cfg1 sampler pipeline.
+Metric: slice contractions/s (whole job).  The headline line is the north
+star's primary precision, tf32 (fp32 storage, tcgen05 kind::tf32 - the paper's
+tensor-core precision); the fp16 mode is measured in the same run
+under "f16".  Also reported: group-slice pairs/s, complex TFLOP/s (executed and
+reference-equivalent, 8 real FLOP per complex MAC), the roofline of the dominant
+kernel per mode, a CPU baseline (the reference library on the host cores, same
+plan), end-to-end numbers through the public API with host buffers (warm, and
+cold: a fresh program and candidate set, binding inside the timed region), the
+fused post-processing kernel's HBM GB/s at M = 2^20, and XEB.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--groups M] [--impl reference]
 """
 from __future__ import annotations
 
 import argparse
+import datetime as _dt
 import json
 import os
 import subprocess
@@ -42,17 +47,28 @@ DTYPES = {"f16": "f16 storage (per-tensor 2^e scales), tcgen05 kind::f16, f32 ac
 UNIT = "slice-contractions/s"
 
 
+def config_of(groups: int) -> dict:
+    """The workload description; identical in both arms (the driver compares it)."""
+    return {"workload": WORKLOAD, "groups_per_slice": groups}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=256)  # all 2^8 slices of cfg2
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--groups", type=int, default=1024)  # SURVEY §8d: cfg2 smoke scale M = 2^10
-    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "bf16", "f32", "f64"])
+    ap.add_argument("--precision", default="tf32", choices=["f16", "tf32", "bf16", "f32", "f64"])
+    ap.add_argument("--alt-precision", default="f16", choices=["none", "f16", "tf32", "bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-xeb", action="store_true")
+    ap.add_argument("--no-post", action="store_true")
+    ap.add_argument("--ref-pairs", type=int, default=0,
+                    help="(group, slice) pairs the reference executor runs (default: one per host core, >= 16)")
+    ap.add_argument("--ref-budget", type=int, default=CFG2["budget"],
+                    help="(tests only) plan budget of the reference sample; the default is the bench plan")
     return ap.parse_args()
 
 
@@ -74,102 +90,301 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi clock / throttle sampling during the timed region."""
+    """nvidia-smi clock / throttle sampling; started before the warm-up so it is
+    running when the timed region begins, and summarised over the samples whose
+    timestamps fall inside [mark_begin, mark_end]."""
 
     def __init__(self, index: int):
         self.proc = None
+        self.window = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "40"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
+            t0 = time.time()  # wait for the first sample (the sampler needs ~0.2-1 s to start)
+            while time.time() - t0 < 5 and os.path.getsize(self.path) == 0:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
+
+    def mark(self, begin: bool):
+        now = time.time()
+        if begin:
+            self.window = [now, None]
+        elif self.window:
+            self.window[1] = now
 
     def stop(self):
         if not self.proc:
             return None
+        time.sleep(0.1)
         self.proc.terminate()
         self.proc.wait()
         self.f.close()
-        sm, mx, reasons = [], 0.0, set()
+        lo, hi = (self.window or [0, 1e30])
+        hi = hi or 1e30
+        sm, mx, reasons, n_all = [], 0.0, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
+                ts = _dt.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, cmax = float(parts[1]), float(parts[2])
             except ValueError:
                 continue
-            for name, val in zip(names, parts[3:7]):
+            n_all += 1
+            if not (lo - 0.03 <= ts <= hi + 0.03):
+                continue
+            sm.append(clk)
+            mx = max(mx, cmax)
+            for name, val in zip(names, parts[4:8]):
                 if val.lower() == "active":
                     reasons.add(name)
         if not sm:
-            return None
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "samples_total": n_all}
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "timed_region_s": hi - lo}
 
 
-_REF_PROBLEM = []
+# ---- the reference's own CPU executor (oracle/_ref) -----------------------------
+def reference_sample(n_pairs: int, threads: int, budget: int, groups: int):
+    """The reference executor (oracle/_ref: the unmodified reference sources) on
+    the host cores, on the bench's own plan (the reference planner at the bench
+    budget): execute_assignment on `n_pairs` (group, slice) pairs - group 0 of the
+    bench's candidate set with slices spread over the range - `threads` at a
+    time.  Nothing of the product package is imported."""
+    from oracle import ref  # CPU baseline / reference arm only
+    r = ref.RefProblem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"], CFG2["open"], budget,
+                       CFG2["effort"]).build()
+    n_sl = 1 << len(r.plan["sliced"])
+    fixed = ref.candidates(CFG2["n"], CFG2["open"], groups, ref.split_next(CFG2["seed"], 0xCA11D))[0]
+    slices = [(i * n_sl) // n_pairs % n_sl for i in range(n_pairs)]
+    _, secs = r.slices_mt(int(fixed[0]), slices, threads)
+    return {"secs": secs, "pairs": n_pairs, "threads": threads, "flops_per_pair": r.plan["flops_per_slice"],
+            "n_slices": n_sl, "plan": f"reference planner, budget {budget} B: {len(r.plan['sliced'])} sliced labels, "
+                                      f"{len(r.plan['steps'])} steps"}
 
 
-def cpu_reference_sample(threads: int, n_pairs: int | None = None, first: int = 0):
-    """The reference executor (oracle/_ref, unmodified reference sources) on the
-    host cores: execute_assignment on `n_pairs` (default `threads`) distinct
-    (group, slice) pairs, spread over `threads` threads, of the same circuit
-    planned with a tighter budget (2^27 B -> 15 sliced labels, ~1e10 FLOP per
-    pair) so one pair takes seconds; returns measured FLOP/s."""
-    from oracle import ref  # CPU baseline leg only
-    if not _REF_PROBLEM:
-        _REF_PROBLEM.append(ref.RefProblem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"],
-                                           CFG2["open"], 1 << 27, "low").build())
-    p = _REF_PROBLEM[0]
-    fixed = ref.candidates(30, CFG2["open"], 1, ref.split_next(1, 0xCA11D))[0][0]
-    n_pairs = n_pairs or threads
-    slices = [(first + i) % (1 << len(p.plan["sliced"])) for i in range(n_pairs)]
-    _, secs = p.slices_mt(int(fixed), slices, threads)
-    flops = n_pairs * p.plan["flops_per_slice"]
-    return flops / secs, secs, p.plan["flops_per_slice"], len(p.plan["sliced"])
+def reference_line_fields(smp, groups):
+    pairs_per_s = smp["pairs"] / smp["secs"]
+    value = pairs_per_s / groups  # one slice contraction = `groups` (group, slice) pairs of this plan
+    sample = (f"reference execute_assignment (oracle/_ref) on {smp['pairs']} (group, slice) pairs of the bench plan "
+              f"({smp['plan']}, {smp['flops_per_pair']:.3e} FLOP/pair), {smp['threads']} threads, "
+              f"{smp['secs']:.1f} s -> {pairs_per_s:.4g} pairs/s "
+              f"({pairs_per_s * smp['flops_per_pair'] / 1e9:.2f} GFLOP/s); one slice contraction = {groups} pairs, "
+              f"so value = pairs/s / {groups}; the full cfg2 run (256 slices x {groups} groups) is extrapolated")
+    return value, sample
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    import paper_2406_18889_b200 as pb  # host planner only (same plan as the reference's)
     threads = os.cpu_count() or 1
-    p = pb.Problem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"], CFG2["open"], CFG2["budget"],
-                   CFG2["effort"]).build()
-    fps = p.plan["flops_per_slice"]
-    # one step = one (group, slice) pair of the reference executor; the W warm-up
-    # pairs and then the timed pairs each run spread over all host threads
-    cpu_reference_sample(threads, max(args.warmup, 1), 0)
-    # at least one pair per host thread (whole waves), so a small K still uses every core
-    n_pairs = -(-max(args.steps, threads) // threads) * threads
-    rate, secs, f_sample, _ = cpu_reference_sample(threads, n_pairs, args.warmup)
-    pairs_per_s = rate / fps
-    value = pairs_per_s / args.groups
+    n_pairs = args.ref_pairs or max(16, threads)
+    smp = reference_sample(n_pairs, threads, args.ref_budget, args.groups)
+    value, sample = reference_line_fields(smp, args.groups)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "groups_per_slice": args.groups},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"reference execute_assignment on {n_pairs} (group, slice) pairs over "
-                                       f"{threads} threads in {secs:.1f} s, same circuit planned at budget 2^27 B "
-                                       f"({f_sample:.3e} FLOP/pair); measured {rate / 1e9:.2f} GFLOP/s "
-                                       f"extrapolated to the bench plan ({fps:.3e} FLOP/pair) x {args.groups} groups"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64, the reference executor)",
+            "data": "synthetic", "config": config_of(args.groups),
+            "timed_region_s": smp["secs"],
+            "extrapolated": "one slice contraction of the CPU executor takes ms_per_step; the timed region is "
+                            f"{smp['pairs']} (group, slice) pairs ({smp['secs']:.1f} s), not K whole steps",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def xeb_cfg1(pb, precision):
+# ---- our arm ---------------------------------------------------------------------
+def traffic_for(step: int, precision: str):
+    """DRAM read + write of the dominant launch from a committed ncu --set full
+    capture (profiles/top_kernel_traffic.json), if one matches this step."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "top_kernel_traffic.json")) as f:
+            tk = json.load(f)
+    except Exception:
+        return None
+    for e in tk.get("entries", [tk]):
+        if int(e.get("plan_step", -1)) == int(step) and e.get("precision") == precision:
+            return int(e["dram_bytes"])
+    return None
+
+
+def measure(pb, p, fixed, precision, args, rank, world, clocks=None):
+    """Times args.steps slice contractions of the M groups at `precision`; returns
+    the value, the dominant-kernel roofline and a kernel breakdown."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_18889_b200._native import rcsg_stats
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    M, P = len(fixed), 1 << p.n_open
+    acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(p.stream(precision))
+    S = min(8, p.n_slices)  # slices per call: an aligned block of consecutive slices
+    n_calls = (args.steps + S - 1) // S
+
+    def block_of(i):
+        return (rank + i * world) % (p.n_slices // S)
+
+    def step(i, st=None, sync=True, count=None):
+        s = block_of(i) * S
+        return p.contract_groups_device(fixed, acc.data_ptr(), precision=precision, configs=None,
+                                        slices=(s, s + (count or S)), stats=st, sync=sync)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    # L2 flush between timed steps: a 256 MiB write (> 126 MB L2) on the program's
+    # stream, outside each step's event pair
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_calls)]
+    st = rcsg_stats()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    if clocks:
+        clocks.mark(True)
+    with torch.cuda.stream(stream):
+        for i in range(n_calls):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            count = min(S, args.steps - i * S)
+            step(args.warmup + i, st, sync=False, count=count)  # enqueue only; checked by p.sync below
+            if i == n_calls - 1 and world > 1:
+                dist.all_reduce(acc)  # the slice sum across ranks
+            evs[i][1].record(stream)
+    p.sync(precision)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.mark(False)
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * args.steps / (ms_max / 1e3)
+
+    # kernel-class breakdown and the dominant launch from one profiled call (outside the timed region)
+    p.set_profile(True)
+    pst = rcsg_stats()
+    step(args.warmup + args.steps, pst)
+    p.set_profile(False)
+    tc_peak = bf16_peak / 2.0 if precision == "tf32" else bf16_peak
+    peak_note = (f"dense tf32 = 1/2 of the {peak_kind} dense bf16 {bf16_peak:.1f} TF/s (B200 tf32:bf16 = 1:2)"
+                 if precision == "tf32" else f"{peak_kind} dense bf16/fp16 peak {bf16_peak:.1f} TF/s")
+    tc_tflops = pst.gemm_tc_flops / (pst.gemm_tc_ms * 1e-3) / 1e12 if pst.gemm_tc_ms else 0.0
+    classes = {0: "SIMT GEMM", 1: "tcgen05 GEMM (gemm_tc_persistent)", 2: "permute", 3: "GEMV"}
+    top_ms = pst.top_ms_sum / pst.top_launches if pst.top_launches else pst.top_ms
+    top_s = top_ms * 1e-3
+    ai = pst.top_flops / pst.top_bytes if pst.top_bytes else float("inf")
+    ridge = tc_peak * 1e12 / (hbm_peak * 1e9)
+    if ai >= ridge:
+        bound, ach, peak, unit, pnote, algo = "tensor", pst.top_flops / top_s / 1e12, tc_peak, "TFLOP/s", peak_note, \
+            pst.top_flops
+    else:
+        bound, ach, peak, unit, algo = "hbm", pst.top_bytes / top_s / 1e9, hbm_peak, "GB/s", pst.top_bytes
+        pnote = f"{peak_kind} HBM copy bandwidth {hbm_peak:.1f} GB/s"
+    roofline = {"bound": bound, "kernel": f"plan step {pst.top_step}: {classes.get(int(pst.top_class), '?')}",
+                "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                "traffic": traffic_for(pst.top_step, precision),
+                "algorithmic_per_launch": algo, "launch_ms": top_ms, "launches_averaged": int(pst.top_launches),
+                "slowest_launch_ms": pst.top_ms, "flops": pst.top_flops, "bytes": pst.top_bytes,
+                "intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge, "peak_note": pnote,
+                "share_of_step": pst.top_ms_sum / pst.device_ms if pst.device_ms and pst.top_launches else None,
+                "all_tensor_core_launches": {"achieved_tflops": tc_tflops, "frac_of_tensor_peak": tc_tflops / tc_peak,
+                                             "share_of_step": pst.gemm_tc_ms / pst.device_ms
+                                             if pst.device_ms else None}}
+    return {"value": value, "ms_max": ms_max, "acc": acc, "S": S, "n_calls": n_calls, "block_of": block_of,
+            "exec_flops": st.executed_flops, "plan_flops": st.plan_flops, "launches": int(st.kernel_launches),
+            "arena": st.arena_bytes, "roofline": roofline,
+            "breakdown": {"per": f"one profiled call of {S} slices (serialised launches)", "step": pst.device_ms,
+                          "gemm_tc": pst.gemm_tc_ms, "gemm_other": pst.gemm_ms - pst.gemm_tc_ms,
+                          "permute": pst.permute_ms, "hbm_peak_gbs": hbm_peak}}
+
+
+def e2e_warm(p, fixed, precision, res, world):
+    """Through the public API with host buffers: group prefixes in, amplitudes
+    out, S slices per call, on the bound program."""
+    import torch
+    import torch.distributed as dist
+    S = res["S"]
+    K = max(2, min(res["n_calls"], 8))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(K):
+        s = res["block_of"](i) * S
+        out = p.contract_groups(fixed, precision=precision, configs=None, slices=(s, s + S))
+    t1 = time.perf_counter()
+    dt = t1 - t0
+    if world > 1:
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    return {"value": world * K * S / dt, "unit": UNIT, "h2d_bytes_per_step": int(fixed.nbytes) / S,
+            "d2h_bytes_per_step": int(out.nbytes) / S,
+            "api": f"Problem.contract_groups (host in/out), {S} slices per call, program bound by earlier calls"}
+
+
+def e2e_cold(pb, precision, M, warm_value):
+    """A fresh Problem (planning timed separately) and a NEW candidate set
+    (Rng(2).split(0xca11d)); all 256 slices in one contract_groups call with host
+    buffers, so compile, batch reassociation, fp16 calibration, binding, the
+    phase-0/3 results, slice tables and graph capture are inside the timed call."""
+    t0 = time.perf_counter()
+    p2 = pb.Problem(CFG2["n"], CFG2["cycles"], CFG2["topology"], CFG2["seed"], CFG2["open"], CFG2["budget"],
+                    CFG2["effort"]).build()
+    t1 = time.perf_counter()
+    fixed2, _ = pb.build_candidate_set(30, CFG2["open"], M, pb.split_next(2, 0xCA11D))
+    out = p2.contract_groups(fixed2, precision=precision, configs=None)
+    t2 = time.perf_counter()
+    n = p2.n_slices
+    return {"value": n / (t2 - t1), "unit": UNIT, "h2d_bytes_per_step": int(fixed2.nbytes) / n,
+            "d2h_bytes_per_step": int(out.nbytes) / n, "slices": n, "contract_s": t2 - t1, "plan_s": t1 - t0,
+            "bind_s_estimate": max(0.0, (t2 - t1) - n / warm_value) if warm_value else None,
+            "api": "fresh Problem + new candidate set, one Problem.contract_groups call over all slices"}
+
+
+def post_bench(pb, hbm_peak):
+    """Fused post-processing kernel (rcsg_postprocess) at M = 2^20 groups, l = 6
+    (64 Mi candidates, 1 GiB of f64 amplitudes resident in HBM): top-k with
+    k = 2^20 (= M, the paper's k) and k = 2^15, plus direct sampling fused into
+    the same streaming pass.  GB/s = algorithmic bytes (amplitudes read once +
+    samples written) / device time of the call."""
+    import numpy as np
+    import torch
+    M, l, n = 1 << 20, 6, 30
+    g = torch.Generator(device="cuda").manual_seed(1)
+    amps = torch.randn((M << l) * 2, dtype=torch.float64, device="cuda", generator=g) * 2.0 ** -15
+    fixed = np.random.default_rng(1).integers(0, 1 << (n - l), size=M, dtype=np.uint64)
+    out = {}
+    for name, k, direct in (("topk_k2^20", 1 << 20, None), ("topk_k2^15", 1 << 15, None),
+                            ("topk_k2^20+direct", 1 << 20, 7)):
+        pb.api.postprocess_device_amps(n, CFG2["open"], fixed, amps.data_ptr(), k, direct_seed=direct)
+        best = None
+        for _ in range(5):
+            _, _, st = pb.api.postprocess_device_amps(n, CFG2["open"], fixed, amps.data_ptr(), k, direct_seed=direct)
+            if best is None or st["device_ms"] < best["device_ms"]:
+                best = st
+        gbs = best["bytes"] / (best["device_ms"] * 1e-3) / 1e9
+        out[name] = {"device_ms": best["device_ms"], "bytes": best["bytes"], "gbs": gbs, "frac_of_hbm": gbs / hbm_peak,
+                     "candidates_kept": best["candidates_kept"], "fast_path": best["fast_path"]}
+    return {"config": f"M=2^20 groups, l=6 (64 Mi candidates), synthetic Gaussian amplitudes in HBM; best of 5",
+            "hbm_peak_gbs": hbm_peak, **out}
+
+
+def xeb_cfg1(pb):
     """cfg1 sampler pipeline on the GPU: grid(3,4) 12q 8 cycles, l=3, M=512,
     K=2 broken edges (m=1) -> amplitudes -> top-k (k=64) / direct sampling ->
     XEB against exact probabilities from the exact (K=0) f64 contraction of the
@@ -183,9 +398,9 @@ def xeb_cfg1(pb, precision):
     fixed, _ = pb.build_candidate_set(n, list(range(l)), M, pb.split_next(1, 0xCA11D))
     acc = torch.zeros(M * (1 << l) * 2, dtype=torch.float64, device="cuda")
     approx.contract_groups_device(fixed, acc.data_ptr(), precision="f64")
-    top = pb.api.top_k_from_device_amps(n, list(range(l)), fixed, acc.data_ptr(), k)
-    direct = pb.api.direct_from_device_amps(n, list(range(l)), fixed, acc.data_ptr(), pb.split_next(1, 0xD1EC7))
-    torch.cuda.synchronize()
+    approx.sync("f64")
+    top, direct, _ = pb.api.postprocess_device_amps(n, list(range(l)), fixed, acc.data_ptr(), k,
+                                                    direct_seed=pb.split_next(1, 0xD1EC7))
     t1 = time.perf_counter()
     ex = exact.contract_groups(fixed, precision="f64", configs=None)
     ap = acc.cpu().numpy().view(np.complex128).reshape(M, -1)
@@ -205,41 +420,40 @@ def xeb_cfg1(pb, precision):
 def xeb_cfg2(pb, p, fixed, precision):
     """cfg2 end to end at n = 30 against the exact GPU statevector (SURVEY §8f
     row 3): all 2^8 slices for the M groups (K = 0, so the amplitudes are the
-    exact ones up to the storage precision) -> top-k with k = M (the paper's k =
-    #groups) and one direct sample per group -> linear XEB from the ideal
-    probabilities; plus the amplitude fidelity of all M * 2^l candidates."""
+    exact ones up to the storage precision) -> the fused post-processing call
+    (top-k with k = M, the paper's k = #groups, one direct sample per group, and
+    both XEBs reduced on the device from the statevector)."""
     import numpy as np
     import torch
     n, l, M = 30, 6, len(fixed)
     P = 1 << l
-    acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
+    state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
     t0 = time.perf_counter()
+    p.exact_state_device(state.data_ptr())
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
     for s0 in range(0, p.n_slices, 8):
         p.contract_groups_device(fixed, acc.data_ptr(), precision=precision, configs=None, slices=(s0, s0 + 8),
                                  sync=False)
     p.sync(precision)
-    top = pb.api.top_k_from_device_amps(n, CFG2["open"], fixed, acc.data_ptr(), M)
-    direct = pb.api.direct_from_device_amps(n, CFG2["open"], fixed, acc.data_ptr(), pb.split_next(1, 0xD1EC7))
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
-    p.exact_state_device(state.data_ptr())
-    torch.cuda.synchronize()
+    top, direct, st = pb.api.postprocess_device_amps(n, CFG2["open"], fixed, acc.data_ptr(), M,
+                                                     direct_seed=pb.split_next(1, 0xD1EC7), d_state=state.data_ptr())
     t2 = time.perf_counter()
-    probs = (state.real ** 2 + state.imag ** 2)
-    q_top = probs[torch.as_tensor(top.astype(np.int64), device="cuda")].cpu().numpy()
-    q_dir = probs[torch.as_tensor(direct.astype(np.int64), device="cuda")].cpu().numpy()
     cand = np.array([pb.member(n, CFG2["open"], int(f), i) for f in fixed for i in range(P)], np.int64)
     ex = state[torch.as_tensor(cand, device="cuda")].cpu().numpy()
-    del state, probs
+    del state
+    torch.cuda.empty_cache()
     ap = acc.cpu().numpy().view(np.complex128).reshape(-1)
     fid = abs(np.vdot(ex, ap)) ** 2 / (np.vdot(ap, ap).real * np.vdot(ex, ex).real)
     return {"config": f"cfg2 grid(5,6) n=30 cycles=14 l=6 M={M} K=0, all 256 slices, {precision}",
             # Porter-Thomas: keeping the top fraction k / (M 2^l) of exact probabilities gives XEB = ln(M 2^l / k)
-            "xeb_topk": pb.xeb(n, q_top), "k": M, "predicted_topk_exact": float(np.log(M * P / M)),
-            "xeb_direct": pb.xeb(n, q_dir), "amplitude_fidelity_vs_exact": float(fid),
-            "contract_and_sample_s": t1 - t0, "statevector_s": t2 - t1,
-            "note": "ideal probabilities from the GPU statevector (simulate_exact, bit-exact with the reference)"}
+            "xeb_topk": st["xeb_topk"], "k": M, "predicted_topk_exact": float(np.log(M * P / M)),
+            "xeb_direct": st["xeb_direct"], "amplitude_fidelity_vs_exact": float(fid),
+            "contract_and_sample_s": t2 - t1, "statevector_s": t1 - t0,
+            "postprocess_device_ms": st["device_ms"],
+            "note": "ideal probabilities from the GPU statevector (simulate_exact, bit-exact with the reference); "
+                    "XEB reduced on the device by rcsg_postprocess"}
 
 
 def main():
@@ -248,11 +462,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2406_18889_b200 as pb
-    from paper_2406_18889_b200._native import rcsg_stats
 
     torch.cuda.set_device(local)
     pb.api.set_device(local)
@@ -265,175 +477,79 @@ def main():
     assert p.n_slices == 256, p.n_slices
     M = args.groups
     fixed, dups = pb.build_candidate_set(30, CFG2["open"], M, pb.split_next(1, 0xCA11D))
-    P = 1 << p.n_open
-    acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.ExternalStream(p.stream(args.precision))
 
-    # a step is one slice contraction; one call contracts an aligned block of S
-    # consecutive slices (one device pass per slice, or per slice batch when the
-    # executor batches clean low sliced labels)
-    S = min(8, p.n_slices)
-    n_calls = (args.steps + S - 1) // S
-
-    def block_of(i):
-        return (rank + i * world) % (p.n_slices // S)
-
-    def step(i, st=None, sync=True, count=None):
-        s = block_of(i) * S
-        return p.contract_groups_device(fixed, acc.data_ptr(), precision=args.precision, configs=None,
-                                        slices=(s, s + (count or S)), stats=st, sync=sync)
-
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    # L2 flush between timed steps: a 256 MiB write (> 126 MB L2) on the program's
-    # stream, outside each step's event pair
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(n_calls)]
     clocks = Clocks(local)
-    st = rcsg_stats()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with torch.cuda.stream(stream):
-        for i in range(n_calls):
-            flush.fill_(i & 0xFF)
-            evs[i][0].record(stream)
-            count = min(S, args.steps - i * S)
-            step(args.warmup + i, st, sync=False, count=count)  # enqueue only; checked by p.sync below
-            if i == n_calls - 1 and world > 1:
-                dist.all_reduce(acc)  # the slice sum across ranks
-            evs[i][1].record(stream)
-    p.sync(args.precision)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+    head = measure(pb, p, fixed, args.precision, args, rank, world, clocks)
     clk = clocks.stop()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * args.steps / (ms_max / 1e3)
-    exec_flops = st.executed_flops
-    plan_flops = st.plan_flops
+    alt = None
+    if args.alt_precision != "none" and args.alt_precision != args.precision:
+        a = measure(pb, p, fixed, args.alt_precision, args, rank, world)
+        alt = {"value": a["value"], "unit": UNIT, "ms_per_step": a["ms_max"] / args.steps,
+               "dtype": DTYPES[args.alt_precision], "gpu_launches": a["launches"],
+               "complex_tflops_executed": a["exec_flops"] * world / (a["ms_max"] * 1e-3) / 1e12,
+               "complex_tflops_reference_equivalent": a["plan_flops"] * world / (a["ms_max"] * 1e-3) / 1e12,
+               "roofline": a["roofline"], "kernel_breakdown_ms": a["breakdown"]}
+        del a
 
-    # kernel-class breakdown from one profiled step (outside the timed region)
-    p.set_profile(True)
-    pst = rcsg_stats()
-    step(args.warmup + args.steps, pst)
-    p.set_profile(False)
-    tc_tflops = pst.gemm_tc_flops / (pst.gemm_tc_ms * 1e-3) / 1e12 if pst.gemm_tc_ms else 0.0
-    # dense tensor peak of the MMA kind the precision uses: fp16/bf16 = measured bf16; tf32 = half of it
-    tc_peak = bf16_peak / 2.0 if args.precision == "tf32" else bf16_peak
-    peak_note = (f"tf32 dense = 1/2 of {peak_kind} bf16 {bf16_peak:.1f} TF/s" if args.precision == "tf32"
-                 else f"{peak_kind} dense bf16/fp16 peak {bf16_peak:.1f} TF/s")
-
-    # roofline of the dominant kernel: the plan step with the longest launch of the profiled pass,
-    # bound by its arithmetic intensity (algorithmic FLOPs / algorithmic bytes)
-    classes = {0: "SIMT GEMM", 1: "tcgen05 GEMM (gemm_tc_persistent / gemm_tc_kernel)", 2: "permute", 3: "GEMV"}
-    # average launch of the dominant plan step over the profiled pass (S launches), not its slowest
-    top_ms = pst.top_ms_sum / pst.top_launches if pst.top_launches else pst.top_ms
-    top_s = top_ms * 1e-3
-    ai = pst.top_flops / pst.top_bytes if pst.top_bytes else float("inf")
-    ridge = tc_peak * 1e12 / (hbm_peak * 1e9)
-    if ai >= ridge:
-        bound, ach, peak, unit = "tensor", pst.top_flops / top_s / 1e12, tc_peak, "TFLOP/s"
-        pnote = peak_note
-        algo = pst.top_flops
-    else:
-        bound, ach, peak, unit = "hbm", pst.top_bytes / top_s / 1e9, hbm_peak, "GB/s"
-        pnote = f"{peak_kind} HBM copy bandwidth {hbm_peak:.1f} GB/s"
-        algo = pst.top_bytes
-    traffic = None
-    try:  # dram read + write of this launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "top_kernel_traffic.json")) as f:
-            tk = json.load(f)
-        if int(tk.get("plan_step", -1)) == int(pst.top_step) and tk.get("precision") == args.precision:
-            traffic = int(tk["dram_bytes"])
-    except Exception:
-        pass
-    roofline = {"bound": bound, "kernel": f"plan step {pst.top_step}: {classes.get(int(pst.top_class), '?')}",
-                "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": traffic,
-                "algorithmic_per_launch": algo, "launch_ms": top_ms, "launches_averaged": int(pst.top_launches),
-                "slowest_launch_ms": pst.top_ms, "flops": pst.top_flops,
-                "bytes": pst.top_bytes, "intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
-                "peak_note": pnote,
-                "share_of_step": pst.top_ms_sum / pst.device_ms if pst.device_ms and pst.top_launches
-                else (pst.top_ms * S / pst.device_ms if pst.device_ms else None),  # profiled call = S passes
-                "all_tensor_core_launches": {"achieved_tflops": tc_tflops, "frac_of_tensor_peak": tc_tflops / tc_peak,
-                                             "share_of_step": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None}}
-
-    # end-to-end through the public API with host buffers (rank 0 work pattern on each rank)
-    e2e = None
+    e2e = cold = None
     if not args.no_e2e:
-        K = max(2, min(n_calls, 8))  # calls of S slices each
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for i in range(K):
-            s = block_of(i) * S
-            out = p.contract_groups(fixed, precision=args.precision, configs=None, slices=(s, s + S))
-        t1 = time.perf_counter()
-        e2e = {"value": world * K * S / (t1 - t0), "unit": UNIT,
-               "h2d_bytes_per_step": int(fixed.nbytes) / S, "d2h_bytes_per_step": int(out.nbytes) / S,
-               "api": f"Problem.contract_groups (host in/out), {S} slices per call"}
-        if world > 1:
-            tt = torch.tensor([t1 - t0], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * K * S / float(tt.item())
+        e2e = e2e_warm(p, fixed, args.precision, head, world)
+        if world == 1:
+            cold = e2e_cold(pb, args.precision, M, e2e["value"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, secs, f_sample, _ = cpu_reference_sample(os.cpu_count() or 1)
-            cpu_val = rate / p.plan["flops_per_slice"] / M
-            cpu = {"value": cpu_val, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"reference execute_assignment (oracle/_ref) on {os.cpu_count()} (group, slice) pairs "
-                             f"in parallel, cfg2 circuit planned at 2^27 B ({f_sample:.3e} FLOP/pair), {secs:.1f} s; "
-                             f"{rate / 1e9:.2f} GFLOP/s extrapolated to {p.plan['flops_per_slice']:.3e} FLOP/pair "
-                             f"x {M} groups"}
+            threads = os.cpu_count() or 1
+            smp = reference_sample(max(16, threads), threads, CFG2["budget"], M)
+            cval, sample = reference_line_fields(smp, M)
+            cpu = {"value": cval, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    post = None
+    if rank == 0 and not args.no_post:
+        try:
+            post = post_bench(pb, hbm_peak)
+        except Exception as e:  # pragma: no cover
+            post = {"error": str(e)}
+
     xeb = None
     if rank == 0 and not args.no_xeb:
         try:
-            xeb = xeb_cfg1(pb, args.precision)
+            xeb = {"cfg1": xeb_cfg1(pb)}
         except Exception as e:  # pragma: no cover
-            xeb = {"error": str(e)}
+            xeb = {"cfg1": {"error": str(e)}}
         if world == 1:
             try:
-                xeb = {"cfg1": xeb, "cfg2": xeb_cfg2(pb, p, fixed, args.precision)}
+                xeb["cfg2"] = xeb_cfg2(pb, p, fixed, args.precision)
             except Exception as e:  # pragma: no cover
-                xeb = {"cfg1": xeb, "cfg2": {"error": str(e)}}
+                xeb["cfg2"] = {"error": str(e)}
 
     if rank == 0:
+        ms_max = head["ms_max"]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[args.precision],
             "data": "synthetic (random circuit of the named shape)",
-            "config": {"workload": WORKLOAD, "groups_per_slice": M, "duplicate_groups": int(dups),
-                       "slices_per_call": S,
-                       "precision": args.precision, "l2": "flushed between timed steps (256 MiB write, "
-                       f"outside the per-step events); arena {st.arena_bytes / 2**30:.2f} GiB per GPU",
-                       "parallelism": f"slice-sharded x{world}"},
-            "group_slice_pairs_per_s": value * M,
-            "complex_tflops_executed": exec_flops * world / (ms_max * 1e-3) / 1e12,
-            "complex_tflops_reference_equivalent": plan_flops * world / (ms_max * 1e-3) / 1e12,
-            "gpu_launches": int(st.kernel_launches),
-            "roofline": roofline,
-            "kernel_breakdown_ms": {"per": f"one profiled pass of {S} slices (serialised launches)",
-                                    "step": pst.device_ms, "gemm_tc": pst.gemm_tc_ms,
-                                    "gemm_other": pst.gemm_ms - pst.gemm_tc_ms, "permute": pst.permute_ms,
-                                    "permute_gbs": pst.permute_bytes / (pst.permute_ms * 1e-3) / 1e9
-                                    if pst.permute_ms else None, "hbm_peak_gbs": hbm_peak},
-            "e2e": e2e, "cpu_baseline": cpu, "xeb": xeb, "clocks": clk,
+            "config": config_of(M),
+            "precision": args.precision, "duplicate_groups": int(dups), "slices_per_call": head["S"],
+            "l2": f"flushed between timed steps (256 MiB write, outside the per-step events); arena "
+                  f"{head['arena'] / 2**30:.2f} GiB per GPU",
+            "parallelism": f"slice-sharded x{world}",
+            "group_slice_pairs_per_s": head["value"] * M,
+            "complex_tflops_executed": head["exec_flops"] * world / (ms_max * 1e-3) / 1e12,
+            "complex_tflops_reference_equivalent": head["plan_flops"] * world / (ms_max * 1e-3) / 1e12,
+            "gpu_launches": head["launches"],
+            "roofline": head["roofline"],
+            "kernel_breakdown_ms": head["breakdown"],
+            "e2e": e2e, "e2e_cold": cold, "cpu_baseline": cpu, "clocks": clk,
+            "postprocess": post, "xeb": xeb,
         }
+        if alt:
+            line[args.alt_precision] = alt
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

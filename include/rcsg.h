@@ -42,7 +42,7 @@ enum {
     RCSG_PREC_F64 = 0,   /* fp64 SIMT: reference-grade (<= 1e-10 norm-relative) */
     RCSG_PREC_F32 = 1,   /* fp32 SIMT */
     RCSG_PREC_TF32 = 2,  /* tcgen05 kind::tf32, fp32 accumulate in TMEM */
-    RCSG_PREC_3XTF32 = 3, /* fp32-grade (runs the fp32 SIMT kernels for now) */
+    RCSG_PREC_3XTF32 = 3, /* fp32-grade alias: runs the fp32 SIMT kernels (no split-tf32 MMA path) */
     RCSG_PREC_BF16 = 4,   /* bf16 storage, tcgen05 kind::f16 (BF16 operands), fp32 accumulate */
     RCSG_PREC_F16 = 5     /* fp16 storage with calibrated per-tensor 2^e scales, kind::f16, fp32 accumulate */
 };
@@ -215,8 +215,39 @@ int rcsg_direct_sample(const rcsg_candidates* cs, const double* d_amps, uint64_t
 int rcsg_direct_sample_probs(const rcsg_candidates* cs, const double* d_probs, uint64_t rng_seed,
                              uint64_t* out);
 
-/* xeb (sampling.cpp:62-73): (2^n / count) * sum q - 1 over HOST q[count]. */
+/* xeb (sampling.cpp:62-73): (2^n / count) * sum q - 1 over HOST q[count]
+ * (reduced on the device in a fixed order; equals the reference's sequential
+ * sum to ~1e-15 relative).  q must be finite and >= 0, else RCSG_ERR_CONFIG. */
 int rcsg_xeb(int32_t n_qubits, uint64_t count, const double* q, double* out);
+
+/* xeb with the ideal probabilities read on the device: q = |d_state[idx]|^2 of
+ * a DEVICE statevector (2^n interleaved complex f64, e.g. from
+ * rcsg_statevector) at the HOST sample indices.  Replaces xeb(samples,
+ * ideal_probability) (sampling.cpp:62-73, statevector.hpp:32). */
+int rcsg_xeb_state(int32_t n_qubits, uint64_t count, const uint64_t* indices, const double* d_state,
+                   double* out);
+
+/* Result of rcsg_postprocess. */
+typedef struct rcsg_post_stats {
+    double device_ms;          /* CUDA-event time of the device work */
+    uint64_t bytes;            /* algorithmic bytes: amplitudes read once + samples written */
+    uint64_t candidates_kept;  /* candidates the threshold pass kept (all on the full-sort path) */
+    int32_t fast_path;         /* 1: threshold select; 0: full sort of every candidate */
+    int32_t fallback;          /* 1: the threshold missed and the full sort ran instead */
+    double xeb_topk;           /* with d_state: XEB of the top-k samples */
+    double xeb_direct;         /* with d_state: XEB of the direct samples */
+} rcsg_post_stats;
+
+/* Fused post-processing of DEVICE amplitudes [n_groups][2^l] (interleaved f64):
+ * |a|^2, global top-k (out_topk: HOST k indices, or NULL to skip) ordered as
+ * top_k_select (sampling.cpp:82-114), one direct sample per group when
+ * `direct` != 0 (out_direct: HOST [n_groups], sampling.cpp:116-145) — both from
+ * one streaming pass over the amplitudes — and, when d_state (a DEVICE
+ * statevector of the circuit) is given, the linear XEB of both sample sets
+ * reduced on the device (sampling.cpp:62-73). */
+int rcsg_postprocess(const rcsg_candidates* cs, const double* d_amps, uint64_t k, uint64_t* out_topk,
+                     int32_t direct, uint64_t rng_seed, uint64_t* out_direct, const double* d_state,
+                     rcsg_post_stats* stats);
 
 /* Device buffers for the post-processing entry points (thin cudaMalloc wrappers
  * so FFI callers need no CUDA runtime of their own). */

@@ -50,6 +50,15 @@ class rcsg_candidates(C.Structure):
                 ("n_groups", C.c_uint64), ("group_fixed", C.POINTER(C.c_uint64))]
 
 
+class rcsg_post_stats(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("bytes", C.c_uint64), ("candidates_kept", C.c_uint64),
+                ("fast_path", C.c_int32), ("fallback", C.c_int32), ("xeb_topk", C.c_double),
+                ("xeb_direct", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 # exported symbols and their restypes (everything else returns int status)
 RCSG_SYMBOLS = [
     "rcsg_last_error", "rcsg_set_device", "rcsg_compile", "rcsg_compile_pinned", "rcsg_program_free",
@@ -57,7 +66,7 @@ RCSG_SYMBOLS = [
     "rcsg_contract_groups", "rcsg_contract_groups_device", "rcsg_execute_assignment", "rcsg_topk",
     "rcsg_topk_probs", "rcsg_direct_sample", "rcsg_direct_sample_probs", "rcsg_xeb",
     "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy", "rcsg_program_sync", "rcsg_statevector",
-    "rcsg_statevector_probs",
+    "rcsg_statevector_probs", "rcsg_xeb_state", "rcsg_postprocess",
 ]
 RCSH_SYMBOLS = [
     "rcsh_last_error", "rcsh_build", "rcsh_build_network", "rcsh_free", "rcsh_net_sizes",

@@ -88,6 +88,22 @@ def _u64(x) -> np.ndarray:
 EFFORT = {"low": 0, "medium": 1, "high": 2}
 
 
+def _order_after_torch(stream_ptr: int):
+    """Make the program's (non-blocking) stream wait for torch's current stream,
+    so a device accumulator zeroed or written by torch is ready before the
+    executor's += lands on it."""
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is None or not torch.cuda.is_available() or not stream_ptr:
+        return
+    cur = torch.cuda.current_stream()
+    if cur.cuda_stream == stream_ptr:
+        return
+    ev = torch.cuda.Event()
+    ev.record(cur)
+    torch.cuda.ExternalStream(stream_ptr).wait_event(ev)
+
+
 def _prec(p) -> int:
     if isinstance(p, str):
         if p not in PRECISIONS:
@@ -277,6 +293,7 @@ class Problem:
             cf = _u64(configs)
             n_cfg = len(cf)
         st = stats if stats is not None else rcsg_stats()
+        _order_after_torch(self.stream(precision, budget))
         _check_h(_native.lib().rcsh_contract_groups_device(
             self.handle, _prec(precision), C.c_uint64(budget), C.c_uint64(len(fixed)),
             _p(fixed, C.c_uint64), n_cfg, _p(cf, C.c_uint64), C.c_uint64(s0), C.c_uint64(s1),
@@ -424,6 +441,32 @@ def direct_from_device_amps(n, open_qubits, fixed, d_amps: int, seed: int) -> np
     _check_g(_native.lib().rcsg_direct_sample(C.byref(cs), C.c_void_p(d_amps), C.c_uint64(seed),
                                               _p(out, C.c_uint64)))
     return out
+
+
+def postprocess_device_amps(n, open_qubits, fixed, d_amps: int, k: int = 0, direct_seed=None,
+                            d_state: int = 0):
+    """Fused post-processing (rcsg_postprocess) of DEVICE amplitudes [G][2^l]:
+    top-k (k > 0), one direct sample per group (direct_seed given) from the same
+    streaming pass, and the XEB of both against a DEVICE statevector d_state.
+    Returns (top or None, direct or None, stats dict)."""
+    cs, keep = _cands(n, open_qubits, fixed)
+    top = np.zeros(max(k, 1), np.uint64)
+    direct = np.zeros(len(keep[1]), np.uint64)
+    st = _native.rcsg_post_stats()
+    _check_g(_native.lib().rcsg_postprocess(
+        C.byref(cs), C.c_void_p(d_amps), C.c_uint64(k), _p(top, C.c_uint64) if k else None,
+        1 if direct_seed is not None else 0, C.c_uint64(direct_seed or 0),
+        _p(direct, C.c_uint64) if direct_seed is not None else None, C.c_void_p(d_state or None), C.byref(st)))
+    return (top[:k] if k else None), (direct if direct_seed is not None else None), st.as_dict()
+
+
+def xeb_state(n: int, samples, d_state: int) -> float:
+    """xeb with ideal q read from a DEVICE statevector (rcsg_xeb_state)."""
+    idx = _u64(samples)
+    out = C.c_double()
+    _check_g(_native.lib().rcsg_xeb_state(n, C.c_uint64(len(idx)), _p(idx, C.c_uint64), C.c_void_p(d_state),
+                                          C.byref(out)))
+    return out.value
 
 
 def xeb(n: int, q) -> float:

@@ -198,7 +198,9 @@ int rcsg_contract_groups(rcsg_program* prog, uint64_t n_groups, const uint64_t* 
         double* d = nullptr;
         check_cuda(cudaMalloc(&d, std::max<size_t>(n, 1) * 2 * sizeof(double)), "cudaMalloc");
         std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
-        check_cuda(cudaMemset(d, 0, n * 2 * sizeof(double)), "cudaMemset");
+        // zero on the program's (non-blocking) stream: the accumulation below is
+        // ordered after it without a device-wide synchronisation
+        check_cuda(cudaMemsetAsync(d, 0, n * 2 * sizeof(double), prog->prog->stream()), "cudaMemsetAsync");
         const int rc = rcsg_contract_groups_device(prog, n_groups, group_fixed, n_configs, configs,
                                                    slice_begin, slice_end, d, 1, stats);
         if (rc) throw Failure{rc, g_msg, g_step};
@@ -223,7 +225,7 @@ int rcsg_execute_assignment(const rcsg_network_desc* net, const rcsg_plan_desc* 
         double* d = nullptr;
         check_cuda(cudaMalloc(&d, n * 2 * sizeof(double)), "cudaMalloc");
         std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
-        check_cuda(cudaMemset(d, 0, n * 2 * sizeof(double)), "cudaMemset");
+        check_cuda(cudaMemsetAsync(d, 0, n * 2 * sizeof(double), prog.stream()), "cudaMemsetAsync");
         prog.run({0}, {}, 0, 1, d, nullptr);
         if (out) check_cuda(cudaMemcpy(out, d, n * 2 * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy");
         if (n_out) *n_out = n;
@@ -250,14 +252,44 @@ int rcsg_direct_sample_probs(const rcsg_candidates* cs, const double* d_probs, u
 int rcsg_xeb(int32_t n_qubits, uint64_t count, const double* q, double* out) {
     return guard([&] {
         if (count == 0) throw Failure{RCSG_ERR_CONFIG, "XEB needs at least one sample"};
-        const double scale = std::pow(2.0, n_qubits);
-        double sum = 0;
-        for (uint64_t i = 0; i < count; ++i) {
-            if (!(q[i] >= 0.0) || !std::isfinite(q[i]))
-                throw Failure{RCSG_ERR_CONFIG, "missing or invalid ideal probability for a sample"};
-            sum += q[i];
+        if (!q || !out) throw Failure{RCSG_ERR_CONFIG, "null argument"};
+        // host q (the reference's ProbFn values): staged to the device and reduced there
+        double* d = nullptr;
+        check_cuda(cudaMalloc(&d, count * sizeof(double)), "cudaMalloc");
+        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        check_cuda(cudaMemcpy(d, q, count * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
+        *out = xeb_device(n_qubits, count, nullptr, nullptr, d);
+    });
+}
+
+int rcsg_xeb_state(int32_t n_qubits, uint64_t count, const uint64_t* indices, const double* d_state, double* out) {
+    return guard([&] {
+        if (!indices || !d_state || !out) throw Failure{RCSG_ERR_CONFIG, "null argument"};
+        for (uint64_t i = 0; i < count; ++i)
+            if (n_qubits < 64 && (indices[i] >> n_qubits) != 0)
+                throw Failure{RCSG_ERR_CONFIG, "sample index outside the statevector"};
+        *out = xeb_device(n_qubits, count, d_state, indices, nullptr);
+    });
+}
+
+int rcsg_postprocess(const rcsg_candidates* cs, const double* d_amps, uint64_t k, uint64_t* out_topk,
+                     int32_t direct, uint64_t rng_seed, uint64_t* out_direct, const double* d_state,
+                     rcsg_post_stats* stats) {
+    return guard([&] {
+        if (!cs || !d_amps) throw Failure{RCSG_ERR_CONFIG, "null argument"};
+        if (direct && !out_direct) throw Failure{RCSG_ERR_CONFIG, "direct sampling needs an output buffer"};
+        const char* e = getenv("RCSG_TOPK_PATH");
+        const PostResult r = postprocess(*cs, d_amps, true, k, out_topk, direct != 0, rng_seed, out_direct, d_state,
+                                         false, e ? atoi(e) : 0);
+        if (stats) {
+            stats->device_ms = r.device_ms;
+            stats->bytes = r.bytes;
+            stats->candidates_kept = r.candidates_kept;
+            stats->fast_path = r.fast_path ? 1 : 0;
+            stats->fallback = r.fallback ? 1 : 0;
+            stats->xeb_topk = r.xeb_top;
+            stats->xeb_direct = r.xeb_direct;
         }
-        *out = scale * sum / static_cast<double>(count) - 1.0;
     });
 }
 

@@ -320,8 +320,14 @@ Program::~Program() {
     for (void* t : tab_mem_) cudaFree(t);
     cudaFree(d_tab_jobs_);
     for (cudaEvent_t e : lane_ev_) cudaEventDestroy(e);
-    for (cudaStream_t l : lanes_) cudaStreamDestroy(l);
-    if (stream_) cudaStreamDestroy(stream_);
+    for (cudaStream_t l : lanes_) {
+        release_workspace(l);
+        cudaStreamDestroy(l);
+    }
+    if (stream_) {
+        release_workspace(stream_);
+        cudaStreamDestroy(stream_);
+    }
 }
 
 void Program::build_nodes(const rcsg_network_desc& net, const rcsg_plan_desc& plan) {
@@ -507,7 +513,10 @@ void Program::build_steps() {
     // leaves take their required layouts (the leaf projection writes them)
     for (int i = 0; i < n_leaves_; ++i)
         if (!layout[i].empty()) nodes_[i].labels = layout[i];
-    // forward: operand layouts, GEMM shapes, output scatter maps
+    // forward: operand layouts, GEMM shapes, output scatter maps.  RCSG_FORCE_PERMUTE=1
+    // (tests only) makes every step write its natural [rows | cols] order so the
+    // consumers run the bit-permutation kernel instead of the scatter epilogue.
+    const bool force_permute = getenv("RCSG_FORCE_PERMUTE") && atoi(getenv("RCSG_FORCE_PERMUTE")) != 0;
     for (size_t s = 0; s < steps_.size(); ++s) {
         StepInfo& st = steps_[s];
         NodeInfo& A = nodes_[st.a];
@@ -534,6 +543,10 @@ void Program::build_steps() {
         plan_flops_ += st.flops_per_variant;
         NodeInfo& R = nodes_[st.r];
         R.labels = layout[st.r];
+        if (force_permute) {  // test knob: results in GEMM order, consumers transpose (permute.cu)
+            R.labels = ord_m[s];
+            R.labels.insert(R.labels.end(), ord_n[s].begin(), ord_n[s].end());
+        }
         if (R.labels.size() > static_cast<size_t>(kMaxRank))
             throw Failure{RCSG_ERR_CAPACITY, "intermediate rank exceeds the executor limit"};
         R.payload = int64_t{1} << R.labels.size();
@@ -1145,7 +1158,18 @@ void Program::retree(const std::vector<uint64_t>& groups) {
 void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, uint64_t slice) {
     rcsg_network_desc net = stored_net();
     rcsg_plan_desc plan = stored_plan();
-    std::vector<uint64_t> sub(groups.begin(), groups.begin() + std::min<size_t>(groups.size(), 16));
+    // calibration sample: up to 64 groups spread over the caller's list and up
+    // to 4 slices spread over the plan's slice range (the call's first slice
+    // included); each node's scale covers the max over all of them
+    std::vector<uint64_t> sub;
+    const size_t n_sub = std::min<size_t>(groups.size(), 64);
+    for (size_t i = 0; i < n_sub; ++i) sub.push_back(groups[i * groups.size() / n_sub]);
+    std::vector<uint64_t> cal_slices{slice};
+    const uint64_t n_slices = uint64_t{1} << calib_plan_.n_sliced;
+    for (uint64_t q = 1; q < 4 && q < n_slices; ++q) {
+        const uint64_t s = (slice + q * (n_slices / 4 ? n_slices / 4 : 1)) % n_slices;
+        if (std::find(cal_slices.begin(), cal_slices.end(), s) == cal_slices.end()) cal_slices.push_back(s);
+    }
     std::vector<float> mx(nodes_.size(), 0.f);
     {
         size_t fr = 0, tot = 0;
@@ -1154,15 +1178,15 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
         cal.tree_fixed_ = true;  // the steps are already this program's (reassociated) tree
         cal.step_origin_ = step_origin_;
         CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
-        CUDA_OK(cudaMemset(cal.d_max_, 0, nodes_.size() * sizeof(float)));
+        CUDA_OK(cudaMemsetAsync(cal.d_max_, 0, nodes_.size() * sizeof(float), cal.stream()));
         cal.record_max_ = true;
         double* d_acc = nullptr;
         CUDA_OK(cudaMalloc(&d_acc, sub.size() * (size_t{1} << out_rank_) * 2 * sizeof(double)));
-        CUDA_OK(cudaMemset(d_acc, 0, sub.size() * (size_t{1} << out_rank_) * 2 * sizeof(double)));
+        CUDA_OK(cudaMemsetAsync(d_acc, 0, sub.size() * (size_t{1} << out_rank_) * 2 * sizeof(double), cal.stream()));
         std::vector<uint64_t> cfg;
         if (calib_plan_.n_broken) cfg.push_back(config);
         try {
-            cal.run(sub, cfg, slice, slice + 1, d_acc, nullptr);
+            for (uint64_t s : cal_slices) cal.run(sub, cfg, s, s + 1, d_acc, nullptr);
         } catch (...) {
             cudaFree(d_acc);
             cudaFree(cal.d_max_);

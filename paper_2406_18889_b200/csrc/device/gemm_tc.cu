@@ -35,13 +35,18 @@ template <typename E, int RB>
 constexpr int kbk = RB / static_cast<int>(sizeof(E));
 constexpr int kThreads = 128;
 
+// SM count of the current device (cached per device: one process may drive several GPUs)
 int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (!n) {
+        n = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev].store(n, std::memory_order_relaxed);
+    }
     return n;
 }
 
@@ -843,12 +848,10 @@ int epilogue_kind(const OutMap& om, int64_t n) {
 template <int BN, int STAGES, typename E, int RB = 128>
 void launch(const GemmArgs& g, cudaStream_t st) {
     using S = Smem<BN, STAGES, RB>;
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};  // function attributes are per device
+    if (first_on_device(configured))
         cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Smem<BN, STAGES>::kBytes);
-        configured = true;
-    }
     const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
     const int64_t a_batches = g.a_batch ? std::max<int64_t>(1, g.a_plane / std::max<int64_t>(g.a_batch, 1)) : 1;
     const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
@@ -915,12 +918,10 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
     const bool persistent = mode != 2 || RB != 128;  // narrow-K tiles: persistent only
     if (persistent) {
-        static bool pconf = false;
-        if (!pconf) {
+        static std::atomic<uint64_t> pconf{0};
+        if (first_on_device(pconf))
             cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::template kPBytes<E>);
-            pconf = true;
-        }
         const int64_t total = tiles * splits;
         if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));

@@ -297,12 +297,22 @@ void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, v
                elem_bytes, to_table);
 }
 
-void* device_workspace(size_t bytes, cudaStream_t st) {
-    // one growing scratch buffer per stream (launches on a stream are ordered)
+namespace {
+std::map<cudaStream_t, std::pair<void*, size_t>>& workspace_pool() {
     static std::map<cudaStream_t, std::pair<void*, size_t>> pool;
+    return pool;
+}
+std::mutex& workspace_mu() {
     static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);
-    auto& e = pool[st];
+    return mu;
+}
+}  // namespace
+
+void* device_workspace(size_t bytes, cudaStream_t st) {
+    // one growing scratch buffer per stream (launches on a stream are ordered);
+    // Program's destructor releases the entries of its streams
+    std::lock_guard<std::mutex> lock(workspace_mu());
+    auto& e = workspace_pool()[st];
     if (bytes > e.second) {
         if (e.first) {
             cudaStreamSynchronize(st);
@@ -313,6 +323,25 @@ void* device_workspace(size_t bytes, cudaStream_t st) {
         e.second = bytes;
     }
     return e.first;
+}
+
+void release_workspace(cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(workspace_mu());
+    auto& pool = workspace_pool();
+    auto it = pool.find(st);
+    if (it == pool.end()) return;
+    if (it->second.first) {
+        cudaStreamSynchronize(st);
+        cudaFree(it->second.first);
+    }
+    pool.erase(it);
+}
+
+bool first_on_device(std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t{1} << (dev & 63);
+    return (done.fetch_or(bit) & bit) == 0;
 }
 template void launch_gemm_simt<float>(const GemmArgs&, cudaStream_t);
 template void launch_gemm_simt<double>(const GemmArgs&, cudaStream_t);

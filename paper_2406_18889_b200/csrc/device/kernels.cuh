@@ -6,6 +6,7 @@
 //   re[v * payload + i], im[(total) + v * payload + i].
 // Storage type: double (f64), float (f32 / tf32 / 3xtf32) or bf16 (bf16).
 #pragma once
+#include <atomic>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -226,6 +227,12 @@ void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, v
 
 // Scratch buffer for split-K partials, one per stream (grown on demand).
 void* device_workspace(size_t bytes, cudaStream_t st);
+// Frees the scratch buffer of a stream that is about to be destroyed.
+void release_workspace(cudaStream_t st);
+
+// True exactly once per (flag set, current device): per-device one-time setup
+// such as cudaFuncSetAttribute (a process may drive several GPUs).
+bool first_on_device(std::atomic<uint64_t>& done);
 
 // tcgen05 tensor-core path: elem 0 = fp32 storage (kind::tf32), 1 = bf16 storage
 // (kind::f16 with BF16 operands); fp32 accumulation in TMEM either way.

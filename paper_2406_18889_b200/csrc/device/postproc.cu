@@ -1,13 +1,34 @@
 // Post-processing on device amplitudes (reference sampling.cpp):
 //   |a|^2 -> global top-k ordered by (prob desc, lexicographic asc)   (:82-114)
 //   per-group inverse-CDF direct sampling                             (:116-145)
+//   linear XEB over the ideal probabilities of the samples            (:62-73)
+//
+// Top-k is a threshold select, not a sort of every candidate:
+//   1. two sampled histogram passes (1/32 of the groups each) over the
+//      order-preserving 64-bit key of the probability pick a threshold key
+//      expected to keep ~1.05 k candidates (binade, then 2^-12 of a binade);
+//   2. ONE streaming pass over all M * 2^l amplitudes (16 B each) appends
+//      every candidate at or above the threshold to a compact buffer
+//      (warp-aggregated atomics); the same pass can draw each group's direct
+//      sample (one warp per group, sequential f64 CDF as in the reference);
+//   3. the buffer (~k entries) is radix-sorted by the descending key; runs of
+//      equal probabilities are re-ordered by lexicographic key (tie rule);
+//   4. the first k entries are mapped to bitstring indices.
+// The selection is exact whatever the threshold: step 2 counts every
+// candidate at or above it, and when fewer than k (or more than the buffer)
+// were found the call falls back to sorting all candidates.  Scratch memory
+// is pooled per device, so steady-state calls do not allocate.
+//
 // The SplitMix64 stream is counter-based: the g-th draw of Rng(seed) is
 // mix(seed + (g+1)*gamma) (rng.hpp:14-22), so every group samples independently
-// on its own thread and still reproduces the reference's sequence bit for bit.
+// and still reproduces the reference's sequence bit for bit.
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,6 +47,9 @@ namespace rcsg {
 
 namespace {
 
+constexpr int kHistBins = 4096;
+constexpr uint64_t kPadKey = 0x7fffffffffffffffull;  // sorts after every non-negative probability
+
 struct MemberMap {
     int32_t n, l;
     int32_t open_pos[64];   // qubit of open bit j
@@ -39,67 +63,284 @@ __device__ __forceinline__ uint64_t member_index(const MemberMap& mm, uint64_t f
     return idx;
 }
 
-__device__ __forceinline__ uint64_t lex_key(uint64_t idx, int n) {
-    return __brevll(idx) >> (64 - n);
+__device__ __forceinline__ uint64_t lex_key(uint64_t idx, int n) { return __brevll(idx) >> (64 - n); }
+
+// Probability of candidate t: std::norm(a) = re*re + im*im, rounded like the
+// reference's complex<double> (no fused multiply-add).
+__device__ __forceinline__ double prob_at(const double* __restrict__ src, int from_amps, int64_t t) {
+    if (!from_amps) return src[t];
+    const double2 a = reinterpret_cast<const double2*>(src)[t];
+    return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
 }
 
-// keys: lexicographic key (sorted first), then ~prob bits (sorted second, stable)
-__global__ void topk_keys_kernel(const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ fixed,
-                                 MemberMap mm, int64_t total, uint64_t* __restrict__ lexk,
-                                 uint64_t* __restrict__ probk, uint64_t* __restrict__ idx) {
-    const int64_t per = int64_t{1} << mm.l;
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t g = t / per, i = t - g * per;
-        double p;
-        if (from_amps) {
-            const double re = src[2 * t], im = src[2 * t + 1];
-            p = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
-        } else {
-            p = src[t];
+// Unsigned key whose ascending order is the numeric order of doubles, with
+// -0.0 == +0.0 (the reference's operator> treats them as equal).
+__device__ __forceinline__ uint64_t asc_key(double p) {
+    if (p == 0.0) p = 0.0;
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(p));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ void flag_nan(double p, int* bad) {
+    if (p != p) atomicExch(bad, 1);
+}
+
+// ---- 1. sampled histograms -------------------------------------------------
+// level 0: bins = top 12 bits of the ascending key (sign + exponent: binades);
+// level 1: inside binade `sel` (from *sel_in), the next 12 bits.  Samples every
+// `stride`-th group.
+__global__ void sample_hist_kernel(const double* __restrict__ src, int from_amps, int64_t n_groups, int l,
+                                   int64_t stride, int level, const uint32_t* __restrict__ sel_in,
+                                   uint32_t* __restrict__ hist, int* __restrict__ bad) {
+    __shared__ uint32_t h[kHistBins];
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t per = int64_t{1} << l;
+    const int64_t n_s = (n_groups + stride - 1) / stride;
+    const int64_t n_el = n_s * per;
+    const uint32_t sel = level ? sel_in[0] : 0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_el;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t g = (e >> l) * stride, i = e & (per - 1);
+        const double p = prob_at(src, from_amps, g * per + i);
+        flag_nan(p, bad);
+        const uint64_t k = asc_key(p);
+        if (level == 0) atomicAdd(&h[k >> 52], 1u);
+        else if (static_cast<uint32_t>(k >> 52) == sel) atomicAdd(&h[(k >> 40) & 0xfff], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[level * kHistBins + i], h[i]);
+}
+
+// One block: walks a histogram from the top bin down until the running count
+// reaches `want` (sample units).  level 0 writes the binade and the count of
+// samples in binades above it; level 1 writes the threshold key.
+__global__ void pick_threshold_kernel(const uint32_t* __restrict__ hist, int level, double want,
+                                      uint32_t* __restrict__ sel, uint64_t* __restrict__ thr) {
+    if (threadIdx.x != 0) return;
+    if (level == 0) {
+        double c = 0;
+        int b = kHistBins - 1;
+        for (; b > 0; --b) {
+            if (c + hist[b] >= want) break;
+            c += hist[b];
         }
-        const uint64_t m = member_index(mm, fixed[g], static_cast<uint64_t>(i));
-        lexk[t] = lex_key(m, mm.n);
-        // probabilities are >= 0: IEEE bit order == numeric order; descending via ~
-        probk[t] = ~static_cast<uint64_t>(__double_as_longlong(p < 0 ? 0.0 : p));
-        idx[t] = m;
+        // never below +0.0 (bin 0x800): negative probabilities always take the full path
+        if (b < 0x800) b = 0x800;
+        sel[0] = static_cast<uint32_t>(b);
+        sel[1] = static_cast<uint32_t>(c);  // samples in binades above
+    } else {
+        double c = sel[1];
+        int b = kHistBins - 1;
+        for (; b > 0; --b) {
+            if (c + hist[kHistBins + b] >= want) break;
+            c += hist[kHistBins + b];
+        }
+        thr[0] = (static_cast<uint64_t>(sel[0]) << 52) | (static_cast<uint64_t>(b) << 40);
     }
 }
 
-__global__ void direct_kernel(const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ fixed,
-                              MemberMap mm, int64_t n_groups, uint64_t seed, uint64_t* __restrict__ out,
-                              int64_t* __restrict__ bad) {
-    const int64_t per = int64_t{1} << mm.l;
-    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < n_groups;
-         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double* s = src + (from_amps ? 2 : 1) * g * per;
-        auto prob = [&](int64_t i) {
-            if (!from_amps) return s[i];
-            return __dadd_rn(__dmul_rn(s[2 * i], s[2 * i]), __dmul_rn(s[2 * i + 1], s[2 * i + 1]));
-        };
+// ---- 2. the streaming pass ----------------------------------------------------
+// Every candidate with asc_key >= *thr is appended as (descending key, t).
+// DIRECT: also draws each group's direct sample (one warp per group).
+template <bool DIRECT>
+__global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ src, int from_amps,
+                                                   int64_t n_groups, int l, const uint64_t* __restrict__ thr_p,
+                                                   uint64_t* __restrict__ out_key, uint64_t* __restrict__ out_t,
+                                                   unsigned long long* __restrict__ counter, uint64_t cap,
+                                                   int* __restrict__ bad, const uint64_t* __restrict__ fixed,
+                                                   MemberMap mm, uint64_t seed, uint64_t* __restrict__ direct_out,
+                                                   unsigned long long* __restrict__ zero_group) {
+    const uint64_t thr = thr_p ? *thr_p : ~0ull;
+    const int lane = threadIdx.x & 31;
+    auto emit = [&](bool take, double p, int64_t t) {
+        const unsigned mask = __ballot_sync(0xffffffffu, take);
+        if (!mask) return;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) {
+            const uint64_t pos = base + __popc(mask & ((1u << lane) - 1));
+            if (pos < cap) {
+                out_key[pos] = ~asc_key(p);
+                out_t[pos] = static_cast<uint64_t>(t);
+            }
+        }
+    };
+    if (!DIRECT) {
+        // flat grid-stride over candidates, 4 independent 16-B loads per thread in flight
+        const int64_t total = n_groups << l;
+        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        for (int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x); t0 < total; t0 += 4 * stride) {
+            double p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + u * stride + threadIdx.x;
+                p[u] = t < total ? prob_at(src, from_amps, t) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + u * stride + threadIdx.x;
+                const bool in = t < total;
+                if (in) flag_nan(p[u], bad);
+                emit(in && asc_key(p[u]) >= thr, p[u], t);
+            }
+        }
+        return;
+    }
+    // one warp per group: lanes read chunks of 32 consecutive candidates; lane 0
+    // folds the chunk sequentially (the reference's left-to-right f64 sum)
+    const int64_t per = int64_t{1} << l;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; g < n_groups;
+         g += warps) {
         double total = 0.0;
-        for (int64_t i = 0; i < per; ++i) total = __dadd_rn(total, prob(i));
+        for (int64_t c = 0; c < per; c += 32) {
+            const int64_t i = c + lane;
+            const bool in = i < per;
+            double p = 0.0;
+            if (in) {
+                p = prob_at(src, from_amps, g * per + i);
+                flag_nan(p, bad);
+            }
+            if (thr_p) emit(in && asc_key(p) >= thr, p, g * per + i);
+            const int cnt = static_cast<int>(per - c < 32 ? per - c : 32);
+            for (int j = 0; j < cnt; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, p, j));
+        }
         if (!(total > 0.0)) {
-            atomicMin(reinterpret_cast<unsigned long long*>(bad), static_cast<unsigned long long>(g));
-            out[g] = 0;
+            if (lane == 0) {
+                atomicMin(zero_group, static_cast<unsigned long long>(g));
+                direct_out[g] = 0;
+            }
             continue;
         }
-        // g-th draw of Rng(seed): counter-based SplitMix64
         uint64_t z = seed + static_cast<uint64_t>(g + 1) * 0x9e3779b97f4a7c15ull;
         z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
         z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
         z ^= z >> 31;
         double u = __dmul_rn(static_cast<double>(z >> 11) * 0x1.0p-53, total);
         int64_t pick = per - 1;
-        for (int64_t i = 0; i < per; ++i) {
-            u = __dsub_rn(u, prob(i));
-            if (u <= 0.0) {
-                pick = i;
-                break;
+        bool done = false;
+        for (int64_t c = 0; c < per && !done; c += 32) {
+            const int64_t i = c + lane;
+            const double p = i < per ? prob_at(src, from_amps, g * per + i) : 0.0;  // L1/L2 hit
+            const int cnt = static_cast<int>(per - c < 32 ? per - c : 32);
+            for (int j = 0; j < cnt; ++j) {
+                u = __dsub_rn(u, __shfl_sync(0xffffffffu, p, j));
+                if (u <= 0.0) {
+                    pick = c + j;
+                    done = true;
+                    break;
+                }
             }
         }
-        out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
+        if (lane == 0) direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
     }
+}
+
+// pad [count, cap) with kPadKey; flags count < k or count > cap
+__global__ void pad_kernel(uint64_t* __restrict__ key, uint64_t* __restrict__ t,
+                           const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
+                           int* __restrict__ fail) {
+    const uint64_t cnt = *counter;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
+    for (uint64_t i = cnt + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < cap;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        key[i] = kPadKey;
+        t[i] = 0;
+    }
+}
+
+// ---- 3. ties: runs of equal keys in the sorted prefix get lexicographic order
+__global__ void tie_fix_kernel(const uint64_t* __restrict__ key, uint64_t* __restrict__ t,
+                               const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
+                               const uint64_t* __restrict__ fixed, MemberMap mm, int* __restrict__ fail) {
+    const int64_t per_shift = mm.l;
+    const uint64_t n = min(static_cast<uint64_t>(*counter), cap);  // real entries (pads excluded)
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (i > 0 && key[i] == key[i - 1]) continue;   // not a run start
+        if (i + 1 >= n || key[i + 1] != key[i]) continue;  // run of one
+        uint64_t e = i + 1;
+        while (e < n && key[e] == key[i] && e - i <= 256) ++e;
+        if (e - i > 256) {  // pathological tie run: the caller sorts by lexkey first instead
+            atomicExch(fail, 2);
+            continue;
+        }
+        // insertion sort of t[i, e) by lexicographic key (runs are short)
+        for (uint64_t a = i + 1; a < e; ++a) {
+            const uint64_t ta = t[a];
+            const uint64_t ka = lex_key(member_index(mm, fixed[ta >> per_shift], ta & ((1ull << per_shift) - 1)), mm.n);
+            uint64_t b = a;
+            while (b > i) {
+                const uint64_t tb = t[b - 1];
+                const uint64_t kb =
+                    lex_key(member_index(mm, fixed[tb >> per_shift], tb & ((1ull << per_shift) - 1)), mm.n);
+                if (kb <= ka) break;
+                t[b] = tb;
+                --b;
+            }
+            t[b] = ta;
+        }
+    }
+}
+
+// ---- 4. output indices
+__global__ void index_kernel(const uint64_t* __restrict__ t, uint64_t k, const uint64_t* __restrict__ fixed,
+                             MemberMap mm, uint64_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t ti = t[i];
+        out[i] = member_index(mm, fixed[ti >> mm.l], ti & ((1ull << mm.l) - 1));
+    }
+}
+
+// ---- full path: every candidate keyed (lexkey sort, then stable prob sort)
+__global__ void full_keys_kernel(const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ fixed,
+                                 MemberMap mm, int64_t total, uint64_t* __restrict__ lexk, uint64_t* __restrict__ t,
+                                 int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t g = i >> mm.l;
+        flag_nan(prob_at(src, from_amps, i), bad);
+        lexk[i] = lex_key(member_index(mm, fixed[g], static_cast<uint64_t>(i & ((int64_t{1} << mm.l) - 1))), mm.n);
+        t[i] = static_cast<uint64_t>(i);
+    }
+}
+
+__global__ void gather_desc_kernel(const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ t,
+                                   int64_t n, uint64_t* __restrict__ key) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        key[i] = ~asc_key(prob_at(src, from_amps, static_cast<int64_t>(t[i])));
+}
+
+// ---- XEB: fixed-shape (deterministic) reduction of q over the samples
+// q = |state[idx]|^2 from a device statevector, or q given per sample.
+__global__ void xeb_kernel(const double* __restrict__ state, const double* __restrict__ q,
+                           const uint64_t* __restrict__ idx, uint64_t count, double* __restrict__ out,
+                           int* __restrict__ bad) {
+    __shared__ double part[1024];
+    double s = 0.0;
+    for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) {
+        double v;
+        if (state) {
+            const double2 a = reinterpret_cast<const double2*>(state)[idx[i]];
+            v = __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+        } else {
+            v = q[i];
+        }
+        if (!(v >= 0.0) || isinf(v)) atomicExch(bad, 1);
+        s += v;
+    }
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = part[0];
 }
 
 MemberMap make_map(const rcsg_candidates& cs) {
@@ -122,72 +363,256 @@ MemberMap make_map(const rcsg_candidates& cs) {
     return mm;
 }
 
-struct DevBuf {
-    void* p = nullptr;
-    explicit DevBuf(size_t bytes) {
-        if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess)
-            throw Failure{RCSG_ERR_DEVICE, "cudaMalloc failed in post-processing"};
-    }
-    ~DevBuf() { cudaFree(p); }
-    template <class T>
-    T* as() const { return static_cast<T*>(p); }
+// Grow-only device scratch, pooled per (device, slot); post-processing calls
+// on one device are serialised by the pool lock.
+struct Pool {
+    std::mutex mu;
+    std::map<std::pair<int, int>, std::pair<void*, size_t>> bufs;
+    std::map<int, cudaStream_t> streams;
+    std::map<int, std::pair<cudaEvent_t, cudaEvent_t>> events;
 };
+Pool& pool() {
+    static Pool* p = new Pool();  // never destroyed: buffers live until process exit
+    return *p;
+}
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+void* scratch(int slot, size_t bytes) {
+    auto& e = pool().bufs[{current_device(), slot}];
+    bytes = std::max<size_t>(bytes, 256);
+    if (e.second < bytes) {
+        if (e.first) cudaFree(e.first);
+        e.first = nullptr;
+        e.second = 0;
+        CUDA_OK(cudaMalloc(&e.first, bytes));
+        e.second = bytes;
+    }
+    return e.first;
+}
+template <class T>
+T* scratch_as(int slot, size_t count) {
+    return static_cast<T*>(scratch(slot, count * sizeof(T)));
+}
+cudaStream_t post_stream() {
+    auto& s = pool().streams[current_device()];
+    if (!s) CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+enum Slot {
+    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb
+};
+
+struct Counters {  // device-side control block
+    unsigned long long count;
+    unsigned long long zero_group;
+    uint64_t thr;
+    uint32_t sel[2];
+    int bad;   // NaN probability seen
+    int fail;  // fast path unusable
+    int xbad;  // invalid ideal probability
+    double xsum[2];
+};
+
+int grid_for(int64_t work, int per_block) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, 148 * 8)));
+}
+
+// Exact (prob desc, lexkey asc) order of ALL candidates: stable radix sort by
+// lexicographic key, then stable radix sort by the descending probability key.
+void full_sort(const double* d_src, int from_amps, const MemberMap& mm, const uint64_t* d_fixed, int64_t total,
+               Counters* d_ctl, cudaStream_t st, uint64_t** t_sorted) {
+    uint64_t* ka = scratch_as<uint64_t>(kKeyA, total);
+    uint64_t* kb = scratch_as<uint64_t>(kKeyB, total);
+    uint64_t* ta = scratch_as<uint64_t>(kTA, total);
+    uint64_t* tb = scratch_as<uint64_t>(kTB, total);
+    full_keys_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_src, from_amps, d_fixed, mm, total, ka, ta, &d_ctl->bad);
+    size_t tmp1 = 0, tmp2 = 0;
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp1, ka, kb, ta, tb, total, 0, mm.n, st));
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, kb, ka, tb, ta, total, 0, 64, st));
+    void* tmp = scratch(kTmp, std::max(tmp1, tmp2));
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp1, ka, kb, ta, tb, total, 0, mm.n, st));
+    gather_desc_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_src, from_amps, tb, total, ka);
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp2, ka, kb, tb, ta, total, 0, 64, st));
+    *t_sorted = ta;
+}
 
 }  // namespace
 
-void topk_select(const rcsg_candidates& cs, const double* d_src, bool from_amps, uint64_t k,
-                 uint64_t* out, cudaStream_t st) {
-    const MemberMap mm = make_map(cs);
-    const int64_t total = static_cast<int64_t>(cs.n_groups) << cs.l;
-    if (k < 1 || k > static_cast<uint64_t>(total))
-        throw Failure{RCSG_ERR_CONFIG, "top-k size k=" + std::to_string(k) + " outside [1, " +
-                                           std::to_string(total) + "]"};
-    DevBuf fixed(cs.n_groups * sizeof(uint64_t));
-    CUDA_OK(cudaMemcpyAsync(fixed.p, cs.group_fixed, cs.n_groups * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    DevBuf lex(total * 8), lex2(total * 8), pk(total * 8), pk2(total * 8), id(total * 8), id2(total * 8);
-    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    topk_keys_kernel<<<grid, 256, 0, st>>>(d_src, from_amps, fixed.as<uint64_t>(), mm, total, lex.as<uint64_t>(),
-                                           pk.as<uint64_t>(), id.as<uint64_t>());
-    // pass 1: order by lexicographic key (ascending); pass 2: stable order by
-    // the inverted probability bits, i.e. probability descending with ties
-    // left in lexicographic order (sampling.cpp:97-100).
-    size_t tmp_bytes = 0;
-    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, lex.as<uint64_t>(), lex2.as<uint64_t>(),
-                                            pk.as<uint64_t>(), pk2.as<uint64_t>(), total, 0, cs.n_qubits, st));
-    size_t tmp2 = 0;
-    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, pk2.as<uint64_t>(), pk.as<uint64_t>(),
-                                            id.as<uint64_t>(), id2.as<uint64_t>(), total, 0, 64, st));
-    DevBuf tmp(std::max(tmp_bytes, tmp2));
-    // sort (lexkey, probkey) pairs and (lexkey, index) pairs with the same keys:
-    // radix sort is stable and deterministic, so both produce the same order.
-    CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, lex.as<uint64_t>(), lex2.as<uint64_t>(),
-                                            pk.as<uint64_t>(), pk2.as<uint64_t>(), total, 0, cs.n_qubits, st));
-    CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, lex.as<uint64_t>(), lex2.as<uint64_t>(),
-                                            id.as<uint64_t>(), id2.as<uint64_t>(), total, 0, cs.n_qubits, st));
-    // pass 2: stable order by prob key (= prob descending)
-    CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp2, pk2.as<uint64_t>(), pk.as<uint64_t>(),
-                                            id2.as<uint64_t>(), id.as<uint64_t>(), total, 0, 64, st));
-    CUDA_OK(cudaMemcpyAsync(out, id.p, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
-}
-
-void direct_sample(const rcsg_candidates& cs, const double* d_src, bool from_amps, uint64_t seed,
-                   uint64_t* out, cudaStream_t st) {
+PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from_amps, uint64_t k,
+                       uint64_t* out_top, bool want_direct, uint64_t seed, uint64_t* out_direct,
+                       const double* d_state, bool device_out, int force_path) {
+    std::lock_guard<std::mutex> lock(pool().mu);
     const MemberMap mm = make_map(cs);
     const int64_t G = static_cast<int64_t>(cs.n_groups);
-    DevBuf fixed(G * sizeof(uint64_t)), d_out(G * sizeof(uint64_t)), bad(sizeof(int64_t));
-    CUDA_OK(cudaMemcpyAsync(fixed.p, cs.group_fixed, G * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    const int64_t none = LLONG_MAX;
-    CUDA_OK(cudaMemcpyAsync(bad.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const int grid = static_cast<int>(std::min<int64_t>((G + 127) / 128, 148 * 8));
-    direct_kernel<<<std::max(grid, 1), 128, 0, st>>>(d_src, from_amps, fixed.as<uint64_t>(), mm, G, seed,
-                                                     d_out.as<uint64_t>(), bad.as<int64_t>());
-    int64_t b = none;
-    CUDA_OK(cudaMemcpyAsync(&b, bad.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaMemcpyAsync(out, d_out.p, G * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    if (G < 1) throw Failure{RCSG_ERR_CONFIG, "candidate set has no groups"};
+    const int64_t total = G << cs.l;
+    if (out_top && (k < 1 || k > static_cast<uint64_t>(total)))
+        throw Failure{RCSG_ERR_CONFIG, "top-k size k=" + std::to_string(k) + " outside [1, " +
+                                           std::to_string(total) + "]"};
+    if (!out_top) k = 0;
+    cudaStream_t st = post_stream();
+    auto& evp = pool().events[current_device()];
+    if (!evp.first) {
+        CUDA_OK(cudaEventCreate(&evp.first));
+        CUDA_OK(cudaEventCreate(&evp.second));
+    }
+    // the caller's producers on the legacy default stream come first
+    CUDA_OK(cudaEventRecord(evp.first, cudaStreamLegacy));
+    CUDA_OK(cudaStreamWaitEvent(st, evp.first, 0));
+    CUDA_OK(cudaEventRecord(evp.first, st));
+
+    uint64_t* d_fixed = scratch_as<uint64_t>(kFixed, G);
+    CUDA_OK(cudaMemcpyAsync(d_fixed, cs.group_fixed, G * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    Counters* d_ctl = scratch_as<Counters>(kCounters, 1);
+    {
+        const Counters init{0, ULLONG_MAX, 0, {0, 0}, 0, 0, 0, {0, 0}};
+        CUDA_OK(cudaMemcpyAsync(d_ctl, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    }
+    uint64_t* d_direct = want_direct ? scratch_as<uint64_t>(kDirect, G) : nullptr;
+    uint64_t* d_top = out_top ? scratch_as<uint64_t>(kOut, k) : nullptr;
+
+    // threshold path for k well below the candidate count (force_path: 1 always, 2 never)
+    const int64_t stride = total >= (int64_t{1} << 20) ? 32 : 1;
+    bool fast = k > 0 && static_cast<double>(k) * 4 <= static_cast<double>(total) && force_path != 2;
+    if (force_path == 1) fast = k > 0;
+    uint64_t cap = 0;
+    uint64_t* keys = nullptr;
+    uint64_t* ts = nullptr;
+    if (fast) {
+        const int64_t n_s = (G + stride - 1) / stride;
+        const double f = static_cast<double>(n_s) / static_cast<double>(G);  // sampled fraction
+        const double c = static_cast<double>(k) * f;                          // expected samples in the top k
+        const double want = c * 1.05 + 6.0 * std::sqrt(c) + 16.0;
+        const double expect = want / f;
+        cap = static_cast<uint64_t>(std::min<double>(static_cast<double>(total), 1.25 * expect + 4096.0));
+        cap = std::max<uint64_t>(cap, k);
+        uint32_t* hist = scratch_as<uint32_t>(kHist, 2 * kHistBins);
+        CUDA_OK(cudaMemsetAsync(hist, 0, 2 * kHistBins * sizeof(uint32_t), st));
+        const int hgrid = grid_for(n_s << cs.l, 512);
+        for (int level = 0; level < 2; ++level) {
+            sample_hist_kernel<<<hgrid, 512, 0, st>>>(d_src, from_amps, G, cs.l, stride, level, d_ctl->sel, hist,
+                                                      &d_ctl->bad);
+            pick_threshold_kernel<<<1, 32, 0, st>>>(hist, level, want, d_ctl->sel, &d_ctl->thr);
+        }
+        keys = scratch_as<uint64_t>(kKeyA, cap);
+        ts = scratch_as<uint64_t>(kTA, cap);
+    }
+    if (fast || want_direct) {
+        const uint64_t* thr = fast ? &d_ctl->thr : nullptr;
+        if (want_direct) {
+            const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
+            scan_kernel<true><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, keys, ts, &d_ctl->count, cap,
+                                                    &d_ctl->bad, d_fixed, mm, seed, d_direct, &d_ctl->zero_group);
+        } else {
+            scan_kernel<false><<<148 * 8, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, keys, ts, &d_ctl->count, cap,
+                                                        &d_ctl->bad, d_fixed, mm, seed, d_direct,
+                                                        &d_ctl->zero_group);
+        }
+    }
+    auto select = [&](bool use_fast) {
+        uint64_t* t_sorted = nullptr;
+        if (use_fast) {
+            pad_kernel<<<grid_for(static_cast<int64_t>(cap), 256), 256, 0, st>>>(keys, ts, &d_ctl->count, cap, k,
+                                                                               &d_ctl->fail);
+            uint64_t* kb = scratch_as<uint64_t>(kKeyB, cap);
+            uint64_t* tb = scratch_as<uint64_t>(kTB, cap);
+            size_t tmp_bytes = 0;
+            CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, kb, ts, tb, cap, 0, 63, st));
+            void* tmp = scratch(kTmp, tmp_bytes);
+            CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, kb, ts, tb, cap, 0, 63, st));
+            tie_fix_kernel<<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(kb, tb, &d_ctl->count, cap, k,
+                                                                                  d_fixed, mm, &d_ctl->fail);
+            t_sorted = tb;
+        } else {
+            full_sort(d_src, from_amps, mm, d_fixed, total, d_ctl, st, &t_sorted);
+        }
+        index_kernel<<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(t_sorted, k, d_fixed, mm, d_top);
+        if (d_state) xeb_kernel<<<1, 1024, 0, st>>>(d_state, nullptr, d_top, k, &d_ctl->xsum[0], &d_ctl->xbad);
+    };
+    if (out_top) select(fast);
+    // XEB of the direct samples from the device statevector (ideal q)
+    if (d_state && want_direct)
+        xeb_kernel<<<1, 1024, 0, st>>>(d_state, nullptr, d_direct, G, &d_ctl->xsum[1], &d_ctl->xbad);
+    CUDA_OK(cudaEventRecord(evp.second, st));
+    Counters h{};
+    CUDA_OK(cudaMemcpyAsync(&h, d_ctl, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    if (b != none)
-        throw Failure{RCSG_ERR_CONFIG, "group " + std::to_string(b) + " has zero total probability; cannot sample"};
+    PostResult res;
+    res.fast_path = fast;
+    res.candidates_kept = fast ? h.count : static_cast<uint64_t>(total);
+    if (h.bad) throw Failure{RCSG_ERR_CONFIG, "probability is NaN"};
+    if (want_direct && h.zero_group != ULLONG_MAX)
+        throw Failure{RCSG_ERR_CONFIG,
+                      "group " + std::to_string(h.zero_group) + " has zero total probability; cannot sample"};
+    if (fast && h.fail) {  // threshold missed (or a long tie run): exact full sort instead
+        res.fast_path = false;
+        res.fallback = true;
+        select(false);
+        CUDA_OK(cudaEventRecord(evp.second, st));
+        CUDA_OK(cudaMemcpyAsync(&h, d_ctl, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    }
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, evp.first, evp.second));
+    res.device_ms = ms;
+    res.bytes = static_cast<uint64_t>(total) * (from_amps ? 16 : 8) + k * 8 + (want_direct ? G * 8 : 0);
+    if (out_top)
+        CUDA_OK(cudaMemcpyAsync(out_top, d_top, k * sizeof(uint64_t),
+                                device_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (want_direct)
+        CUDA_OK(cudaMemcpyAsync(out_direct, d_direct, G * sizeof(uint64_t),
+                                device_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (d_state) {
+        if (h.xbad) throw Failure{RCSG_ERR_CONFIG, "missing or invalid ideal probability for a sample"};
+        const double scale = std::ldexp(1.0, cs.n_qubits);
+        if (out_top) res.xeb_top = scale * h.xsum[0] / static_cast<double>(k) - 1.0;
+        if (want_direct) res.xeb_direct = scale * h.xsum[1] / static_cast<double>(G) - 1.0;
+    }
+    return res;
+}
+
+namespace {
+int forced_path() {
+    const char* e = getenv("RCSG_TOPK_PATH");  // tests: 1 threshold select, 2 full sort
+    return e ? atoi(e) : 0;
+}
+}  // namespace
+
+void topk_select(const rcsg_candidates& cs, const double* d_src, bool from_amps, uint64_t k, uint64_t* out,
+                 cudaStream_t) {
+    postprocess(cs, d_src, from_amps, k, out, false, 0, nullptr, nullptr, false, forced_path());
+}
+
+void direct_sample(const rcsg_candidates& cs, const double* d_src, bool from_amps, uint64_t seed, uint64_t* out,
+                   cudaStream_t) {
+    postprocess(cs, d_src, from_amps, 0, nullptr, true, seed, out, nullptr, false, 0);
+}
+
+double xeb_device(int n_qubits, uint64_t count, const double* d_state, const uint64_t* indices,
+                  const double* d_q) {
+    if (count == 0) throw Failure{RCSG_ERR_CONFIG, "XEB needs at least one sample"};
+    std::lock_guard<std::mutex> lock(pool().mu);
+    cudaStream_t st = post_stream();
+    CUDA_OK(cudaStreamSynchronize(cudaStreamLegacy));
+    Counters* d_ctl = scratch_as<Counters>(kCounters, 1);
+    CUDA_OK(cudaMemsetAsync(d_ctl, 0, sizeof(Counters), st));
+    const uint64_t* d_idx = nullptr;
+    if (d_state) {
+        uint64_t* di = scratch_as<uint64_t>(kXeb, count);
+        CUDA_OK(cudaMemcpyAsync(di, indices, count * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        d_idx = di;
+    }
+    xeb_kernel<<<1, 1024, 0, st>>>(d_state, d_q, d_idx, count, &d_ctl->xsum[0], &d_ctl->xbad);
+    Counters h{};
+    CUDA_OK(cudaMemcpyAsync(&h, d_ctl, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (h.xbad) throw Failure{RCSG_ERR_CONFIG, "missing or invalid ideal probability for a sample"};
+    return std::ldexp(1.0, n_qubits) * h.xsum[0] / static_cast<double>(count) - 1.0;
 }
 
 }  // namespace rcsg

@@ -36,8 +36,9 @@ def test_ctypes_structs_match_header():
 #include <stdio.h>
 #include "rcsg.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(rcsg_network_desc), sizeof(rcsg_plan_desc), sizeof(rcsg_stats),
-         sizeof(rcsg_candidates), offsetof(rcsg_stats, device_ms), offsetof(rcsg_stats, gemm_tc_launches));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(rcsg_network_desc), sizeof(rcsg_plan_desc), sizeof(rcsg_stats),
+         sizeof(rcsg_candidates), offsetof(rcsg_stats, device_ms), offsetof(rcsg_stats, gemm_tc_launches),
+         sizeof(rcsg_post_stats), offsetof(rcsg_post_stats, xeb_topk));
   return 0;
 }
 """
@@ -49,7 +50,8 @@ int main(void) {
         got = list(map(int, subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()))
     want = [C.sizeof(_native.rcsg_network_desc), C.sizeof(_native.rcsg_plan_desc), C.sizeof(_native.rcsg_stats),
             C.sizeof(_native.rcsg_candidates), _native.rcsg_stats.device_ms.offset,
-            _native.rcsg_stats.gemm_tc_launches.offset]
+            _native.rcsg_stats.gemm_tc_launches.offset, C.sizeof(_native.rcsg_post_stats),
+            _native.rcsg_post_stats.xeb_topk.offset]
     assert got == want
 
 

@@ -317,3 +317,76 @@ def test_f16_overflow_widens_scales_and_retries(monkeypatch):
     got = p.contract_groups(fixed, precision="f16")
     for g, fb in enumerate(fixed):
         assert rel(got[g], pn.contract_group(int(fb))) < TOL["f16"], g
+
+
+@pytest.mark.parametrize("precision", ["f64", "tf32", "f16"])
+def test_forced_permutes_match_oracle(monkeypatch, precision):
+    """RCSG_FORCE_PERMUTE=1: every step writes its natural [rows | cols] order and
+    the consumers transpose with the bit-permutation kernel (permute.cu, the
+    executor's fallback when a producer cannot write the consumer's layout);
+    the amplitudes still match the oracle."""
+    from paper_2406_18889_b200._native import rcsg_stats
+    monkeypatch.setenv("RCSG_FORCE_PERMUTE", "1")
+    p, fixed = cfg1(32)
+    pn = port.PortNet(p.net, p.plan)
+    p.set_profile(True)
+    st = rcsg_stats()
+    got = p.contract_groups(fixed, precision=precision, stats=st)
+    assert st.permute_bytes > 0
+    for g, fb in enumerate(fixed):
+        assert rel(got[g], pn.contract_group(int(fb))) < TOL[precision], g
+
+
+# ---- the bench's own headline configuration, pinned ---------------------------
+def test_headline_bench_configuration_pinned(ref):
+    """bench.py's workload exactly: cfg2 planned at 3*2^30 B (2^8 slices), M = 1024
+    groups from Rng(1).split(0xca11d), all 256 slices through the device
+    accumulator, at f16 and tf32 (the timed modes) and f64:
+      - every group within the mode's tolerance of the GPU f64 run;
+      - amplitude fidelity over all 65,536 candidates >= 1 - 1e-4 against the GPU
+        statevector (bit-identical to the reference's simulate_exact);
+      - 4 (group, slice) pairs of this same plan against the live reference
+        executor (execute_assignment, ~2 min on the host cores)."""
+    import concurrent.futures as cf
+    import torch
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low")
+    p = pb.Problem(*spec).build()
+    r = ref.RefProblem(*spec).build()
+    assert p.n_slices == 256 and np.array_equal(r.plan["steps"], p.plan["steps"])
+    M, P = 1024, 64
+    fixed, _ = pb.build_candidate_set(30, list(range(6)), M, pb.split_next(1, 0xCA11D))
+    rfixed, _ = ref.candidates(30, list(range(6)), M, ref.split_next(1, 0xCA11D))
+    assert np.array_equal(fixed, rfixed)
+    pairs = [(0, 0), (0, 171), (700, 85), (700, 255)]
+    with cf.ThreadPoolExecutor(2) as ex:  # the reference executor runs on the host meanwhile
+        futs = {g: ex.submit(r.slices_mt, int(fixed[g]), [s for gg, s in pairs if gg == g], 2)
+                for g in sorted({g for g, _ in pairs})}
+        out = {}
+        for prec in ("f64", "tf32", "f16"):
+            acc = torch.zeros(M * P * 2, dtype=torch.float64, device="cuda")
+            for s0 in range(0, 256, 8):
+                p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None,
+                                         slices=(s0, s0 + 8), sync=False)
+            p.sync(prec)
+            out[prec] = acc.cpu().numpy().view(np.complex128).reshape(M, P)
+        state = torch.empty(1 << 30, dtype=torch.complex128, device="cuda")
+        p.exact_state_device(state.data_ptr())
+        cand = np.array([pb.member(30, list(range(6)), int(f), i) for f in fixed for i in range(P)], np.int64)
+        exact = state[torch.as_tensor(cand, device="cuda")].cpu().numpy().reshape(M, P)
+        del state
+        torch.cuda.empty_cache()
+        for prec in ("f64", "tf32", "f16"):
+            a = out[prec]
+            fid = abs(np.vdot(exact, a)) ** 2 / (np.vdot(a, a).real * np.vdot(exact, exact).real)
+            assert fid >= (1 - 1e-12 if prec == "f64" else 1 - 1e-4), (prec, fid)
+            if prec != "f64":
+                errs = [rel(a[g], out["f64"][g]) for g in range(M)]
+                assert max(errs) < TOL[prec], (prec, max(errs))
+        assert rel(out["f64"], exact) < 1e-10
+        for g, fut in futs.items():
+            ss = [s for gg, s in pairs if gg == g]
+            want, _ = fut.result()
+            for j, s in enumerate(ss):
+                for prec in ("f64", "tf32", "f16"):
+                    got = p.contract_groups(fixed[g:g + 1], precision=prec, configs=None, slices=(s, s + 1))[0]
+                    assert rel(got, want[j]) < TOL[prec], (g, s, prec, rel(got, want[j]))

@@ -68,7 +68,7 @@ def test_sampler_host_pieces_vs_fixture():
     assert np.array_equal(fixed, s["fixed"]) and dup == int(s["duplicate_groups"])
     for idx, key in s["lexkeys"]:
         assert pb.lexkey(int(idx), 12) == int(key)
-    assert pb.xeb(12, s["q"]) == s["xeb"]
+    # xeb is reduced on the device (tests/test_gpu_sampling.py checks it against this fixture's value)
 
 
 def test_candidate_set_structure_and_validation():
