@@ -92,7 +92,8 @@ struct Topology {
     std::vector<std::vector<std::pair<int, int>>> patterns;
     std::vector<int> sequence;
 };
-// "line", "ring", "grid(R,C)" as in the reference, plus "sycamore53" (new).
+// "line", "ring", "grid(R,C)" as in the reference, plus (new) "sycamore53" and
+// "zuchongzhi60" (diagonal lattices of 9 x 6 sites minus one, and 10 x 6).
 Topology make_topology(const std::string& name, int n_qubits);
 Circuit gen_random_circuit(int n_qubits, int n_cycles, const std::string& topology,
                            std::uint64_t seed);
@@ -154,6 +155,42 @@ ContractionPlan find_contraction_path(const TensorNetwork& network,
 std::vector<Label> select_broken_edges(const TensorNetwork& network, int k_edges,
                                        std::uint64_t seed = 0);
 
+// ---- planner at scale (new) -------------------------------
+// find_contraction_path dispatches on the planner kind:
+//   Reference - the reference algorithm restated bit for bit (contraction_plan.cpp:85-377);
+//   Scale     - log-domain, batch-aware, randomized-greedy + subtree-reconfiguration
+//               planner with stem-aware slicing (planner_scale.cpp);
+//   Auto      - (default) Reference wherever it works, Scale where the reference's
+//               uint64 costs overflow (rank >= 60) or its budget slicing stalls.
+enum class PlannerKind { Reference, Scale, Auto };
+struct ScalePlannerOptions {
+    std::uint64_t n_groups = 1;  // group batch the costs model (variant counts min(M, 2^b))
+    int trials = 0;              // randomized greedy trials (0: 64 / 256 / 1024 by effort)
+    int threads = 0;             // host threads (0: all)
+    int refine = 4;              // best trees refined by subtree reconfiguration
+};
+struct ScalePlanReport {
+    double log2_total_flops = 0;              // all slices, batched cost model
+    double log2_flops_per_slice_batched = 0;  // slice-dependent steps, one slice
+    double log2_flops_once_batched = -1;      // slice-independent steps (run once)
+    double log2_max_size = 0;                 // widest tensor incl. variant bits
+    double seconds = 0;
+    int n_sliced = 0, trials = 0, winning_trial = -1, threads = 0, reduced_tensors = 0;
+};
+void set_planner(PlannerKind kind, const ScalePlannerOptions& options = {});
+PlannerKind get_planner();
+ContractionPlan find_contraction_path_reference(const TensorNetwork& network, std::uint64_t memory_budget_bytes,
+                                                SearchEffort effort, std::uint64_t seed,
+                                                const std::vector<Label>& broken);
+ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::uint64_t memory_budget_bytes,
+                                            SearchEffort effort, std::uint64_t seed,
+                                            const std::vector<Label>& broken = {},
+                                            const ScalePlannerOptions& options = {},
+                                            ScalePlanReport* report = nullptr);
+// True when the reference planner's greedy tree already saturates its uint64
+// costs, i.e. Auto hands the network to the scale planner.
+bool reference_planner_overflows(const TensorNetwork& network, const std::vector<Label>& broken = {});
+
 // ---- executor (reference contraction_engine.hpp:13-86)
 struct BrokenEdgeConfig {
     std::vector<Label> broken_labels;
@@ -190,7 +227,18 @@ struct ContractResult {
 std::vector<cplx> execute_assignment(const TensorNetwork& network, const ContractionPlan& plan,
                                      const std::map<Label, int>& assignment,
                                      ExecutionStats* stats = nullptr);
-// `workers` is accepted for signature compatibility; results never depend on it.
+// Device context (new): one process drives these local GPUs (rcsg_init; NCCL
+// over NVLink).  With a context, contract() shards the slices of a
+// group-shaped pin set (every non-open output pinned, as contract_group does)
+// over min(workers, devices) GPUs; the result never depends on `workers`
+// (canonical slice blocks summed in block order).  Without one, `workers` is
+// accepted for signature compatibility and one GPU runs.  An empty list
+// releases the context.
+void init_devices(const std::vector<int>& devices);
+int device_count();
+// Compiled device programs are cached per (network, plan, precision, pins),
+// LRU over 8 entries; this frees them.
+void clear_program_cache();
 ContractResult contract(const TensorNetwork& network, const ContractionPlan& plan,
                         const BrokenEdgeConfig* config,
                         const std::map<Label, int>& fixed_outputs = {}, int workers = 1);

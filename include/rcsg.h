@@ -169,6 +169,35 @@ int rcsg_execute_assignment(const rcsg_network_desc* net, const rcsg_plan_desc* 
                             int32_t precision, const int8_t* assign, double* out,
                             uint64_t* n_out);
 
+/* ---- multi-GPU context (one host thread, all local GPUs, NCCL) -------------- */
+
+/* One process drives the listed local GPUs: a stream per device and one NCCL
+ * communicator clique over them (ncclCommInitAll over NVLink / NVSwitch; NCCL
+ * is loaded at run time).  Replaces the reference's worker thread pool of
+ * contract() (contraction_engine.cpp:264-287) with devices. */
+typedef struct rcsg_context rcsg_context;
+typedef struct rcsg_multi rcsg_multi;
+int rcsg_init(const int32_t* devices, int32_t n_devices, rcsg_context** out);
+int rcsg_context_free(rcsg_context* ctx);
+int rcsg_context_devices(rcsg_context* ctx, int32_t* n_devices);
+
+/* Compile (network, plan) on every device of the context.  n_blocks: canonical
+ * slice blocks (0 = 8). */
+int rcsg_context_compile(rcsg_context* ctx, const rcsg_network_desc* net, const rcsg_plan_desc* plan,
+                         int32_t precision, uint64_t mem_budget_bytes, int32_t n_blocks, rcsg_multi** out);
+int rcsg_multi_free(rcsg_multi* m);
+
+/* rcsg_contract_groups over the first n_used devices (0 = all): the slice range
+ * is cut into the program's canonical blocks (independent of n_used), blocks go
+ * to devices round-robin, each device sums its blocks' slices in ascending
+ * order into device partials, the partials are gathered to the first device
+ * with NCCL and added in block order - bit-identical for any n_used (the
+ * reference's worker-count invariance, test_contraction.cpp:84-93).
+ * out_amps: HOST [n_groups][2^l] interleaved float64. */
+int rcsg_multi_contract_groups(rcsg_multi* m, uint64_t n_groups, const uint64_t* group_fixed, uint64_t n_configs,
+                               const uint64_t* configs, uint64_t slice_begin, uint64_t slice_end, int32_t n_used,
+                               double* out_amps, rcsg_stats* stats);
+
 /* ---- exact statevector (XEB oracle) ----------------------------------------- */
 
 /* simulate_exact (statevector.cpp:79-86) on the device: |0..0> followed by the

@@ -74,7 +74,7 @@ RCSH_SYMBOLS = [
     "rcsh_circuit_gates", "rcsh_contract_groups", "rcsh_contract_groups_device", "rcsh_contract",
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
     "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
-    "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector",
+    "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector", "rcsh_build_ex",
 ]
 
 _lib = None

@@ -133,13 +133,31 @@ class Problem:
     net: dict = field(default_factory=dict)
     plan: dict = field(default_factory=dict)
 
-    def build(self):
+    def build(self, planner: str | None = None, n_groups: int = 1, trials: int = 0, threads: int = 0):
+        """planner None: find_contraction_path as configured (Auto: the reference
+        algorithm where it works, the scale planner where it overflows);
+        "reference" / "scale" / "auto" select explicitly.  n_groups, trials and
+        threads tune the scale planner; its report lands in self.plan_report."""
         h = C.c_void_p()
         op = _i32(self.open)
-        _check_h(_native.lib().rcsh_build(self.n, self.cycles, self.topology.encode(),
-                                          C.c_uint64(self.seed), _p(op, C.c_int), len(self.open),
-                                          C.c_uint64(self.budget), EFFORT[self.effort], self.k_broken,
-                                          C.c_uint64(self.m), C.byref(h)))
+        if planner is None:
+            _check_h(_native.lib().rcsh_build(self.n, self.cycles, self.topology.encode(),
+                                              C.c_uint64(self.seed), _p(op, C.c_int), len(self.open),
+                                              C.c_uint64(self.budget), EFFORT[self.effort], self.k_broken,
+                                              C.c_uint64(self.m), C.byref(h)))
+            self.plan_report = None
+        else:
+            rep = np.zeros(10, np.float64)
+            kind = {"reference": 0, "scale": 1, "auto": 2}[planner]
+            _check_h(_native.lib().rcsh_build_ex(self.n, self.cycles, self.topology.encode(),
+                                                 C.c_uint64(self.seed), _p(op, C.c_int), len(self.open),
+                                                 C.c_uint64(self.budget), EFFORT[self.effort], self.k_broken,
+                                                 C.c_uint64(self.m), kind, C.c_uint64(n_groups), trials, threads,
+                                                 _p(rep, C.c_double), C.byref(h)))
+            keys = ["log2_total_flops", "log2_flops_per_slice_batched", "log2_flops_once_batched",
+                    "log2_max_size", "seconds", "n_sliced", "trials", "winning_trial", "threads",
+                    "reduced_tensors"]
+            self.plan_report = dict(zip(keys, rep.tolist())) if rep[0] != -1.0 else None
         self.handle = h
         self._export()
         return self

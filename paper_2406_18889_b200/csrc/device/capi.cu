@@ -21,21 +21,13 @@ template <class F>
 int guard(F&& f) {
     try {
         f();
-        g_msg.clear();
-        g_step = -1;
-        return RCSG_OK;
+        return record_error(RCSG_OK, "", -1);
     } catch (const Failure& e) {
-        g_msg = e.msg;
-        g_step = e.step;
-        return e.code;
+        return record_error(e.code, e.msg, e.step);
     } catch (const std::bad_alloc&) {
-        g_msg = "host allocation failed";
-        g_step = -1;
-        return RCSG_ERR_CAPACITY;
+        return record_error(RCSG_ERR_CAPACITY, "host allocation failed", -1);
     } catch (const std::exception& e) {
-        g_msg = e.what();
-        g_step = -1;
-        return RCSG_ERR_DEVICE;
+        return record_error(RCSG_ERR_DEVICE, e.what(), -1);
     }
 }
 
@@ -86,6 +78,12 @@ std::vector<LabelRole> group_roles(const rcsg_network_desc& net, const rcsg_plan
 }
 
 }  // namespace
+
+int rcsg::record_error(int code, const std::string& msg, int step) {
+    g_msg = msg;
+    g_step = code == RCSG_OK ? -1 : step;
+    return code;
+}
 
 struct rcsg_program {
     std::unique_ptr<Program> prog;

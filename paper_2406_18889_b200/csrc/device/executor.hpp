@@ -50,6 +50,10 @@ struct Failure {
     int step = -1;
 };
 
+// Sets this thread's rcsg_last_error() message and step; returns `code`
+// (the C-ABI entry points of every translation unit report through it).
+int record_error(int code, const std::string& msg, int step);
+
 enum Role : int8_t { kFree = 0, kPass = 1, kVar = 2 };
 
 struct LabelRole {

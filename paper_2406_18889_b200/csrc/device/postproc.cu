@@ -113,60 +113,111 @@ __global__ void sample_hist_kernel(const double* __restrict__ src, int from_amps
         if (h[i]) atomicAdd(&hist[level * kHistBins + i], h[i]);
 }
 
-// One block: walks a histogram from the top bin down until the running count
-// reaches `want` (sample units).  level 0 writes the binade and the count of
-// samples in binades above it; level 1 writes the threshold key.
-__global__ void pick_threshold_kernel(const uint32_t* __restrict__ hist, int level, double want,
-                                      uint32_t* __restrict__ sel, uint64_t* __restrict__ thr) {
-    if (threadIdx.x != 0) return;
+// One block of 1024 threads: suffix sums of a histogram (from the top bin
+// down) find the highest bin whose suffix reaches `want` (sample units).
+// level 0 writes the binade and the samples in binades above it; level 1
+// writes the threshold key.
+__global__ void __launch_bounds__(1024) pick_threshold_kernel(const uint32_t* __restrict__ hist, int level,
+                                                              double want, uint32_t* __restrict__ sel,
+                                                              uint64_t* __restrict__ thr) {
+    __shared__ double part[1024];
+    __shared__ int found;
+    const uint32_t* h = hist + level * kHistBins;
+    const double base = level ? static_cast<double>(sel[1]) : 0.0;
+    const int tid = threadIdx.x;
+    const int b0 = 4 * (1023 - tid);  // thread tid owns bins [b0, b0 + 4); thread 0 the top ones
+    double local = 0;
+    for (int j = 0; j < 4; ++j) local += h[b0 + j];
+    part[tid] = local;
+    if (tid == 0) found = -1;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan over chunks, top first
+        const double v = tid >= off ? part[tid - off] : 0.0;
+        __syncthreads();
+        part[tid] += v;
+        __syncthreads();
+    }
+    const double above = base + (tid ? part[tid - 1] : 0.0);  // samples in bins >= b0 + 4
+    if (above < want && above + local >= want) {  // the one chunk where the running count crosses
+        double a = above;
+        for (int j = 3; j >= 0; --j) {
+            if (a + h[b0 + j] >= want) {
+                found = b0 + j;
+                break;
+            }
+            a += h[b0 + j];
+        }
+    }
+    __syncthreads();
+    int b = found < 0 ? 0 : found;  // nothing reaches `want`: keep everything
+    if (level == 0 && b < 0x800) b = 0x800;  // never below +0.0: negative probabilities take the full path
+    if (b < b0 || b >= b0 + 4) return;  // the owner of bin b writes
     if (level == 0) {
-        double c = 0;
-        int b = kHistBins - 1;
-        for (; b > 0; --b) {
-            if (c + hist[b] >= want) break;
-            c += hist[b];
-        }
-        // never below +0.0 (bin 0x800): negative probabilities always take the full path
-        if (b < 0x800) b = 0x800;
+        double c = above;  // samples in bins above b
+        for (int j = 3; b0 + j > b; --j) c += h[b0 + j];
         sel[0] = static_cast<uint32_t>(b);
-        sel[1] = static_cast<uint32_t>(c);  // samples in binades above
+        sel[1] = static_cast<uint32_t>(c);
     } else {
-        double c = sel[1];
-        int b = kHistBins - 1;
-        for (; b > 0; --b) {
-            if (c + hist[kHistBins + b] >= want) break;
-            c += hist[kHistBins + b];
-        }
         thr[0] = (static_cast<uint64_t>(sel[0]) << 52) | (static_cast<uint64_t>(b) << 40);
     }
 }
 
 // ---- 2. the streaming pass ----------------------------------------------------
-// Every candidate with asc_key >= *thr is appended as (descending key, t).
+// Every candidate with asc_key >= *thr is appended as (descending key, t): the
+// full 64-bit key and index (K = V = uint64_t), or, when the candidate count
+// fits 32 bits, the key's top 32 bits and a 32-bit index (half the bytes to
+// sort; equal truncated keys are re-ordered exactly by the tie pass).
 // DIRECT: also draws each group's direct sample (one warp per group).
-template <bool DIRECT>
+template <bool DIRECT, typename K, typename V>
 __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ src, int from_amps,
                                                    int64_t n_groups, int l, const uint64_t* __restrict__ thr_p,
-                                                   uint64_t* __restrict__ out_key, uint64_t* __restrict__ out_t,
+                                                   K* __restrict__ out_key, V* __restrict__ out_t,
                                                    unsigned long long* __restrict__ counter, uint64_t cap,
                                                    int* __restrict__ bad, const uint64_t* __restrict__ fixed,
                                                    MemberMap mm, uint64_t seed, uint64_t* __restrict__ direct_out,
                                                    unsigned long long* __restrict__ zero_group) {
-    const uint64_t thr = thr_p ? *thr_p : ~0ull;
+    // kept candidates are staged in shared memory (warp-aggregated shared
+    // atomics) and flushed with ONE global atomic per ~1-2K entries: a global
+    // atomic per warp would serialise on the single counter
+    constexpr unsigned kStage = 2048;
+    __shared__ K s_key[kStage];
+    __shared__ V s_t[kStage];
+    __shared__ unsigned s_cnt;
+    __shared__ unsigned long long s_base;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const bool collect = thr_p != nullptr;
+    const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
-    auto emit = [&](bool take, double p, int64_t t) {
+    auto stage = [&](bool take, double p, int64_t t) {
         const unsigned mask = __ballot_sync(0xffffffffu, take);
         if (!mask) return;
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(mask)));
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (take) {
-            const uint64_t pos = base + __popc(mask & ((1u << lane) - 1));
-            if (pos < cap) {
-                out_key[pos] = ~asc_key(p);
-                out_t[pos] = static_cast<uint64_t>(t);
-            }
+            const unsigned pos = base + __popc(mask & ((1u << lane) - 1));
+            s_key[pos] = static_cast<K>(~asc_key(p) >> (64 - 8 * sizeof(K)));
+            s_t[pos] = static_cast<V>(t);
         }
+    };
+    // block-uniform: flush when fewer than `room` free slots remain (or always)
+    auto flush = [&](unsigned room, bool force) {
+        __syncthreads();
+        const unsigned n = s_cnt;
+        __syncthreads();
+        if (n == 0 || (!force && n + room <= kStage)) return;
+        if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
+        __syncthreads();
+        const unsigned long long b = s_base;
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+            if (b + i < cap) {
+                out_key[b + i] = s_key[i];
+                out_t[b + i] = s_t[i];
+            }
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
     };
     if (!DIRECT) {
         // flat grid-stride over candidates, 4 independent 16-B loads per thread in flight
@@ -184,30 +235,39 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
                 const int64_t t = t0 + u * stride + threadIdx.x;
                 const bool in = t < total;
                 if (in) flag_nan(p[u], bad);
-                emit(in && asc_key(p[u]) >= thr, p[u], t);
+                stage(in && asc_key(p[u]) >= thr, p[u], t);
             }
+            flush(4 * blockDim.x, false);
         }
+        flush(0, true);
         return;
     }
-    // one warp per group: lanes read chunks of 32 consecutive candidates; lane 0
-    // folds the chunk sequentially (the reference's left-to-right f64 sum)
+    // one warp per group (8 groups per block iteration, block-uniform loops):
+    // lanes read chunks of 32 consecutive candidates; lane 0 folds each chunk
+    // sequentially (the reference's left-to-right f64 sum)
     const int64_t per = int64_t{1} << l;
-    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
-    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; g < n_groups;
-         g += warps) {
+    const int wpb = blockDim.x / 32;
+    for (int64_t g0 = blockIdx.x * static_cast<int64_t>(wpb); g0 < n_groups;
+         g0 += static_cast<int64_t>(gridDim.x) * wpb) {
+        const int64_t g = g0 + threadIdx.x / 32;
+        const bool valid = g < n_groups;
         double total = 0.0;
         for (int64_t c = 0; c < per; c += 32) {
             const int64_t i = c + lane;
-            const bool in = i < per;
+            const bool in = valid && i < per;
             double p = 0.0;
             if (in) {
                 p = prob_at(src, from_amps, g * per + i);
                 flag_nan(p, bad);
             }
-            if (thr_p) emit(in && asc_key(p) >= thr, p, g * per + i);
+            if (collect) {
+                stage(in && asc_key(p) >= thr, p, g * per + i);
+                flush(blockDim.x, false);
+            }
             const int cnt = static_cast<int>(per - c < 32 ? per - c : 32);
             for (int j = 0; j < cnt; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, p, j));
         }
+        if (!valid) continue;
         if (!(total > 0.0)) {
             if (lane == 0) {
                 atomicMin(zero_group, static_cast<unsigned long long>(g));
@@ -237,47 +297,58 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         }
         if (lane == 0) direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
     }
+    if (collect) flush(0, true);
 }
 
-// pad [count, cap) with kPadKey; flags count < k or count > cap
-__global__ void pad_kernel(uint64_t* __restrict__ key, uint64_t* __restrict__ t,
-                           const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
-                           int* __restrict__ fail) {
+// pad [count, cap) with the largest non-negative key; flags count < k or count > cap
+template <typename K, typename V>
+__global__ void pad_kernel(K* __restrict__ key, V* __restrict__ t, const unsigned long long* __restrict__ counter,
+                           uint64_t cap, uint64_t k, int* __restrict__ fail) {
     const uint64_t cnt = *counter;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
+    const K pad = static_cast<K>(kPadKey >> (64 - 8 * sizeof(K)));
     for (uint64_t i = cnt + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < cap;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        key[i] = kPadKey;
+        key[i] = pad;
         t[i] = 0;
     }
 }
 
-// ---- 3. ties: runs of equal keys in the sorted prefix get lexicographic order
-__global__ void tie_fix_kernel(const uint64_t* __restrict__ key, uint64_t* __restrict__ t,
+// ---- 3. ties: runs of equal (possibly truncated) keys in the sorted prefix are
+// re-ordered by (full descending key, lexicographic key) - the reference's
+// (prob desc, lexkey asc) order
+template <typename K, typename V>
+__global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
                                const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
-                               const uint64_t* __restrict__ fixed, MemberMap mm, int* __restrict__ fail) {
-    const int64_t per_shift = mm.l;
+                               const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ fixed,
+                               MemberMap mm, int* __restrict__ fail) {
     const uint64_t n = min(static_cast<uint64_t>(*counter), cap);  // real entries (pads excluded)
+    const uint64_t low = (1ull << mm.l) - 1;
+    auto order_key = [&](uint64_t ti, uint64_t& full, uint64_t& lex) {
+        full = ~asc_key(prob_at(src, from_amps, static_cast<int64_t>(ti)));
+        lex = lex_key(member_index(mm, fixed[ti >> mm.l], ti & low), mm.n);
+    };
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < k;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (i > 0 && key[i] == key[i - 1]) continue;   // not a run start
         if (i + 1 >= n || key[i + 1] != key[i]) continue;  // run of one
         uint64_t e = i + 1;
         while (e < n && key[e] == key[i] && e - i <= 256) ++e;
-        if (e - i > 256) {  // pathological tie run: the caller sorts by lexkey first instead
+        if (e - i > 256) {  // pathological tie run: the caller sorts every candidate instead
             atomicExch(fail, 2);
             continue;
         }
-        // insertion sort of t[i, e) by lexicographic key (runs are short)
+        // insertion sort of t[i, e) (runs are short)
         for (uint64_t a = i + 1; a < e; ++a) {
-            const uint64_t ta = t[a];
-            const uint64_t ka = lex_key(member_index(mm, fixed[ta >> per_shift], ta & ((1ull << per_shift) - 1)), mm.n);
+            const V ta = t[a];
+            uint64_t fa, la;
+            order_key(ta, fa, la);
             uint64_t b = a;
             while (b > i) {
-                const uint64_t tb = t[b - 1];
-                const uint64_t kb =
-                    lex_key(member_index(mm, fixed[tb >> per_shift], tb & ((1ull << per_shift) - 1)), mm.n);
-                if (kb <= ka) break;
+                const V tb = t[b - 1];
+                uint64_t fb, lb;
+                order_key(tb, fb, lb);
+                if (fb < fa || (fb == fa && lb <= la)) break;
                 t[b] = tb;
                 --b;
             }
@@ -287,7 +358,8 @@ __global__ void tie_fix_kernel(const uint64_t* __restrict__ key, uint64_t* __res
 }
 
 // ---- 4. output indices
-__global__ void index_kernel(const uint64_t* __restrict__ t, uint64_t k, const uint64_t* __restrict__ fixed,
+template <typename V>
+__global__ void index_kernel(const V* __restrict__ t, uint64_t k, const uint64_t* __restrict__ fixed,
                              MemberMap mm, uint64_t* __restrict__ out) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < k;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -460,11 +532,6 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         CUDA_OK(cudaEventCreate(&evp.first));
         CUDA_OK(cudaEventCreate(&evp.second));
     }
-    // the caller's producers on the legacy default stream come first
-    CUDA_OK(cudaEventRecord(evp.first, cudaStreamLegacy));
-    CUDA_OK(cudaStreamWaitEvent(st, evp.first, 0));
-    CUDA_OK(cudaEventRecord(evp.first, st));
-
     uint64_t* d_fixed = scratch_as<uint64_t>(kFixed, G);
     CUDA_OK(cudaMemcpyAsync(d_fixed, cs.group_fixed, G * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     Counters* d_ctl = scratch_as<Counters>(kCounters, 1);
@@ -474,14 +541,20 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     }
     uint64_t* d_direct = want_direct ? scratch_as<uint64_t>(kDirect, G) : nullptr;
     uint64_t* d_top = out_top ? scratch_as<uint64_t>(kOut, k) : nullptr;
+    // the caller's producers on the legacy default stream come first; the device
+    // time (res.device_ms) starts once the candidate set is uploaded
+    CUDA_OK(cudaEventRecord(evp.first, cudaStreamLegacy));
+    CUDA_OK(cudaStreamWaitEvent(st, evp.first, 0));
+    CUDA_OK(cudaEventRecord(evp.first, st));
 
     // threshold path for k well below the candidate count (force_path: 1 always, 2 never)
     const int64_t stride = total >= (int64_t{1} << 20) ? 32 : 1;
     bool fast = k > 0 && static_cast<double>(k) * 4 <= static_cast<double>(total) && force_path != 2;
     if (force_path == 1) fast = k > 0;
+    const bool narrow = total <= (int64_t{1} << 32);  // 32-bit keys and indices in the compact buffer
     uint64_t cap = 0;
-    uint64_t* keys = nullptr;
-    uint64_t* ts = nullptr;
+    void* keys = nullptr;
+    void* ts = nullptr;
     if (fast) {
         const int64_t n_s = (G + stride - 1) / stride;
         const double f = static_cast<double>(n_s) / static_cast<double>(G);  // sampled fraction
@@ -496,41 +569,60 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         for (int level = 0; level < 2; ++level) {
             sample_hist_kernel<<<hgrid, 512, 0, st>>>(d_src, from_amps, G, cs.l, stride, level, d_ctl->sel, hist,
                                                       &d_ctl->bad);
-            pick_threshold_kernel<<<1, 32, 0, st>>>(hist, level, want, d_ctl->sel, &d_ctl->thr);
+            pick_threshold_kernel<<<1, 1024, 0, st>>>(hist, level, want, d_ctl->sel, &d_ctl->thr);
         }
-        keys = scratch_as<uint64_t>(kKeyA, cap);
-        ts = scratch_as<uint64_t>(kTA, cap);
+        keys = scratch(kKeyA, cap * 8);
+        ts = scratch(kTA, cap * 8);
     }
-    if (fast || want_direct) {
+    auto scan = [&](auto kz, auto vz) {
+        using K = decltype(kz);
+        using V = decltype(vz);
         const uint64_t* thr = fast ? &d_ctl->thr : nullptr;
+        K* kk = static_cast<K*>(keys);
+        V* tt = static_cast<V*>(ts);
         if (want_direct) {
             const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
-            scan_kernel<true><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, keys, ts, &d_ctl->count, cap,
-                                                    &d_ctl->bad, d_fixed, mm, seed, d_direct, &d_ctl->zero_group);
+            scan_kernel<true, K, V><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count, cap,
+                                                          &d_ctl->bad, d_fixed, mm, seed, d_direct,
+                                                          &d_ctl->zero_group);
         } else {
-            scan_kernel<false><<<148 * 8, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, keys, ts, &d_ctl->count, cap,
-                                                        &d_ctl->bad, d_fixed, mm, seed, d_direct,
-                                                        &d_ctl->zero_group);
+            scan_kernel<false, K, V><<<148 * 8, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count,
+                                                              cap, &d_ctl->bad, d_fixed, mm, seed, d_direct,
+                                                              &d_ctl->zero_group);
         }
+    };
+    if (fast || want_direct) {
+        if (narrow) scan(uint32_t{0}, uint32_t{0});
+        else scan(uint64_t{0}, uint64_t{0});
     }
+    auto select_fast = [&](auto kz, auto vz) {
+        using K = decltype(kz);
+        using V = decltype(vz);
+        K* ka = static_cast<K*>(keys);
+        V* ta = static_cast<V*>(ts);
+        pad_kernel<K, V><<<grid_for(static_cast<int64_t>(cap), 256), 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k,
+                                                                                 &d_ctl->fail);
+        K* kb = static_cast<K*>(scratch(kKeyB, cap * sizeof(K)));
+        V* tb = static_cast<V*>(scratch(kTB, cap * sizeof(V)));
+        const int end_bit = 8 * static_cast<int>(sizeof(K)) - 1;  // non-negative keys: top bit clear
+        size_t tmp_bytes = 0;
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka, kb, ta, tb, cap, 0, end_bit, st));
+        void* tmp = scratch(kTmp, tmp_bytes);
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ka, kb, ta, tb, cap, 0, end_bit, st));
+        tie_fix_kernel<K, V><<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(
+            kb, tb, &d_ctl->count, cap, k, d_src, from_amps, d_fixed, mm, &d_ctl->fail);
+        index_kernel<V><<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(tb, k, d_fixed, mm, d_top);
+    };
     auto select = [&](bool use_fast) {
-        uint64_t* t_sorted = nullptr;
         if (use_fast) {
-            pad_kernel<<<grid_for(static_cast<int64_t>(cap), 256), 256, 0, st>>>(keys, ts, &d_ctl->count, cap, k,
-                                                                               &d_ctl->fail);
-            uint64_t* kb = scratch_as<uint64_t>(kKeyB, cap);
-            uint64_t* tb = scratch_as<uint64_t>(kTB, cap);
-            size_t tmp_bytes = 0;
-            CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, kb, ts, tb, cap, 0, 63, st));
-            void* tmp = scratch(kTmp, tmp_bytes);
-            CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, kb, ts, tb, cap, 0, 63, st));
-            tie_fix_kernel<<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(kb, tb, &d_ctl->count, cap, k,
-                                                                                  d_fixed, mm, &d_ctl->fail);
-            t_sorted = tb;
+            if (narrow) select_fast(uint32_t{0}, uint32_t{0});
+            else select_fast(uint64_t{0}, uint64_t{0});
         } else {
+            uint64_t* t_sorted = nullptr;
             full_sort(d_src, from_amps, mm, d_fixed, total, d_ctl, st, &t_sorted);
+            index_kernel<uint64_t><<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(t_sorted, k, d_fixed, mm,
+                                                                                         d_top);
         }
-        index_kernel<<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(t_sorted, k, d_fixed, mm, d_top);
         if (d_state) xeb_kernel<<<1, 1024, 0, st>>>(d_state, nullptr, d_top, k, &d_ctl->xsum[0], &d_ctl->xbad);
     };
     if (out_top) select(fast);

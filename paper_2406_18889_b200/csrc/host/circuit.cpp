@@ -6,6 +6,7 @@
 //   line/ring/grid patterns  circuit.cpp:65-110   (+ "sycamore53", new)
 //   random circuit           circuit.cpp:112-161 (one RNG draw per 1q slot)
 //   circuit_to_network      tensor_network.cpp:20-92
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <set>
@@ -78,26 +79,25 @@ void add_chain(std::vector<std::pair<int, int>>& out, int n, int first) {
     for (int q = first; q + 1 < n; q += 2) out.emplace_back(q, q + 1);
 }
 
-// Google Sycamore-53: the 54-site diagonal lattice (6 rows x 9 columns of the
-// rotated square grid) with the one broken site removed.  Qubit (r, c) with
-// r in [0,9), c in [0,6): couplers to (r+1, c) and (r+1, c +/- 1) depending on
-// row parity.  The four coupler classes A,B,C,D follow the parity of the row
-// and the direction; the cycle order is the supremacy sequence ABCDCDAB.
-Topology sycamore(int n_qubits) {
-    const int rows = 9, cols = 6;
-    const int broken_site = 3;  // site (0, 3) does not exist on the chip
+// Diagonal ("rotated square") lattice of rows x cols sites, as on Google's
+// Sycamore and USTC's Zuchongzhi chips.  Site (r, c) couples to (r+1, c) and
+// (r+1, c -/+ 1) depending on row parity; the four coupler classes A,B,C,D follow
+// the row parity and the direction; the cycle order is the supremacy sequence
+// ABCDCDAB.  Sites in `missing` do not exist; qubits are numbered row-major over
+// the remaining sites.
+Topology diagonal_lattice(int rows, int cols, const std::vector<int>& missing, int n_qubits,
+                          const char* name) {
     std::vector<int> id(rows * cols, -1);
     int next = 0;
     for (int s = 0; s < rows * cols; ++s)
-        if (s != broken_site) id[s] = next++;
-    if (n_qubits != next) throw ConfigError("sycamore53 needs n_qubits=53");
+        if (std::find(missing.begin(), missing.end(), s) == missing.end()) id[s] = next++;
+    if (n_qubits != next) throw ConfigError(std::string(name) + " needs n_qubits=" + std::to_string(next));
     Topology t;
     t.patterns.assign(4, {});
     for (int r = 0; r + 1 < rows; ++r)
         for (int c = 0; c < cols; ++c) {
             const int a = id[r * cols + c];
             if (a < 0) continue;
-            // down-left / down-right neighbours on the diagonal lattice
             const int cl = (r % 2 == 0) ? c : c - 1;
             const int cr = (r % 2 == 0) ? c + 1 : c;
             if (cl >= 0 && cl < cols) {
@@ -112,6 +112,13 @@ Topology sycamore(int n_qubits) {
     t.sequence = {0, 1, 2, 3, 2, 3, 0, 1};
     return t;
 }
+
+// Google Sycamore-53: 9 x 6 sites with the one broken site (0, 3) removed.
+Topology sycamore(int n_qubits) { return diagonal_lattice(9, 6, {3}, n_qubits, "sycamore53"); }
+
+// Zuchongzhi-style 60 qubits (BASELINE cfg5): the 66-site 11 x 6 lattice of
+// Zuchongzhi 2.x, with the 60 qubits of its first 10 rows in use.
+Topology zuchongzhi60(int n_qubits) { return diagonal_lattice(10, 6, {}, n_qubits, "zuchongzhi60"); }
 
 }  // namespace
 
@@ -138,6 +145,8 @@ Topology make_topology(const std::string& name, int n_qubits) {
         t.sequence = {0, 1, 2, 3, 2, 3, 0, 1};
     } else if (name == "sycamore53") {
         t = sycamore(n_qubits);
+    } else if (name == "zuchongzhi60") {
+        t = zuchongzhi60(n_qubits);
     } else {
         throw ConfigError("unknown topology: " + name);
     }

@@ -8,6 +8,7 @@
 #include <ostream>
 #include <cmath>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <mutex>
 
@@ -34,12 +35,98 @@ void ok(int rc) {
     if (rc) raise(rc);
 }
 
-struct ProgramHandle {
-    rcsg_program* p = nullptr;
-    ~ProgramHandle() {
-        if (p) rcsg_program_free(p);
-    }
+// ---- compiled-program cache --------------------------------------------------
+// The reference re-interprets the plan on every call; compiling a device
+// program (layouts, reassociation, fp16 calibration, binding, graph capture)
+// is the expensive part here, so programs are cached by a fingerprint of the
+// flattened (network, plan), the precision and the pins, LRU over kCacheSize
+// entries.  Calls are serialised by the cache lock (a program is not
+// re-entrant, and one host thread drives the device anyway).
+constexpr std::size_t kCacheSize = 8;
+
+std::uint64_t fnv(std::uint64_t h, const void* p, std::size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+    return h;
+}
+template <class V>
+std::uint64_t fnv_vec(std::uint64_t h, const V& v) {
+    const std::uint64_t n = v.size();
+    h = fnv(h, &n, sizeof n);
+    return v.empty() ? h : fnv(h, v.data(), v.size() * sizeof(v[0]));
+}
+std::uint64_t fingerprint(const Flat& f) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (const auto* v : {&f.rank, &f.labels, &f.out_l, &f.open_l, &f.open_q, &f.steps, &f.sliced, &f.broken, &f.fixed})
+        h = fnv_vec(h, *v);
+    return fnv_vec(h, f.data);
+}
+
+struct Cached {
+    std::uint64_t key = 0;
+    int precision = 0;
+    int kind = 0;  // 0 group program, 1 pinned program, 2 multi-device program
+    std::vector<int8_t> pins;
+    rcsg_program* prog = nullptr;
+    rcsg_multi* multi = nullptr;
+    std::uint64_t used = 0;
 };
+
+std::mutex g_mu;  // guards the cache, the device context and every device call below
+std::vector<Cached> g_cache;
+std::uint64_t g_tick = 0;
+rcsg_context* g_ctx = nullptr;
+int g_ctx_devices = 0;
+
+void free_entry(Cached& c) {
+    if (c.prog) rcsg_program_free(c.prog);
+    if (c.multi) rcsg_multi_free(c.multi);
+    c.prog = nullptr;
+    c.multi = nullptr;
+}
+
+Cached& cached(const Flat& f, int kind, const std::vector<int8_t>& pins) {
+    const std::uint64_t key = fingerprint(f);
+    for (Cached& c : g_cache)
+        if (c.key == key && c.kind == kind && c.precision == g_precision && c.pins == pins) {
+            c.used = ++g_tick;
+            return c;
+        }
+    if (g_cache.size() >= kCacheSize) {
+        auto lru = std::min_element(g_cache.begin(), g_cache.end(),
+                                    [](const Cached& a, const Cached& b) { return a.used < b.used; });
+        free_entry(*lru);
+        g_cache.erase(lru);
+    }
+    Cached c;
+    c.key = key;
+    c.kind = kind;
+    c.precision = g_precision;
+    c.pins = pins;
+    c.used = ++g_tick;
+    if (kind == 0) ok(rcsg_compile(&f.net, &f.plan, g_precision, 0, &c.prog));
+    else if (kind == 1) ok(rcsg_compile_pinned(&f.net, &f.plan, g_precision, 0, pins.data(), &c.prog));
+    else ok(rcsg_context_compile(g_ctx, &f.net, &f.plan, g_precision, 0, 0, &c.multi));
+    g_cache.push_back(std::move(c));
+    return g_cache.back();
+}
+
+// group code of a fixed_outputs map that pins exactly the non-open output legs
+// (contract_group's packing, contraction_engine.cpp:310-318); false otherwise
+bool as_group(const TensorNetwork& network, const std::map<Label, int>& fixed, std::uint64_t& code) {
+    code = 0;
+    std::size_t n_fixed = 0;
+    int bit = 0;
+    for (int q = 0; q < network.n_qubits; ++q) {
+        if (std::find(network.open_qubits.begin(), network.open_qubits.end(), q) != network.open_qubits.end()) continue;
+        auto it = fixed.find(network.output_labels[q]);
+        if (it == fixed.end()) return false;
+        if (it->second) code |= std::uint64_t{1} << bit;
+        ++bit;
+        ++n_fixed;
+    }
+    return n_fixed == fixed.size() && bit <= 64;
+}
 
 void check_config(const ContractionPlan& plan, const BrokenEdgeConfig* config) {
     if (config) {
@@ -124,24 +211,33 @@ ContractResult contract(const TensorNetwork& network, const ContractionPlan& pla
         pin[l] = static_cast<int8_t>(v);
     }
     auto f = flatten(network, plan);
-    ProgramHandle h;
-    ok(rcsg_compile_pinned(&f->net, &f->plan, g_precision, 0, pin.data(), &h.p));
+    std::lock_guard<std::mutex> lock(g_mu);
+    // with a device context, a group-shaped pin set runs sharded over
+    // min(workers, devices) GPUs (canonical slice blocks: results do not depend
+    // on `workers`, like the reference's thread pool, contraction_engine.cpp:264-287)
+    std::uint64_t code = 0;
+    const bool multi = g_ctx && as_group(network, fixed_outputs, code);
+    Cached& c = multi ? cached(*f, 2, {}) : cached(*f, 1, pin);
     const std::vector<std::uint64_t> none{0};
     const std::vector<std::uint64_t>& cfgs = config ? config->configurations : none;
     ContractResult res;
     std::vector<double> sum, comp;
-    const std::uint64_t group = 0;
+    const std::uint64_t group = multi ? code : 0;
+    std::size_t n = std::size_t{1} << network.open_labels.size();
+    if (!multi)
+        for (Label l : network.open_labels)
+            if (pin[l] >= 0) n >>= 1;
     for (std::size_t t = 0; t < cfgs.size(); ++t) {
         rcsg_stats st{};
         const auto t0 = std::chrono::steady_clock::now();
-        // one subtask = one configuration over every slice (contraction_engine.cpp:237-262);
-        // the result has one index bit per open leg that is not pinned
-        std::size_t n = std::size_t{1} << network.open_labels.size();
-        for (Label l : network.open_labels)
-            if (pin[l] >= 0) n >>= 1;
+        // one subtask = one configuration over every slice (contraction_engine.cpp:237-262)
         std::vector<double> buf(2 * n, 0.0);
-        ok(rcsg_contract_groups(h.p, 1, &group, config ? 1 : 0, config ? &cfgs[t] : nullptr, 0,
-                                plan.n_slices(), buf.data(), &st));
+        if (multi)
+            ok(rcsg_multi_contract_groups(c.multi, 1, &group, config ? 1 : 0, config ? &cfgs[t] : nullptr, 0,
+                                          plan.n_slices(), workers, buf.data(), &st));
+        else
+            ok(rcsg_contract_groups(c.prog, 1, &group, config ? 1 : 0, config ? &cfgs[t] : nullptr, 0,
+                                    plan.n_slices(), buf.data(), &st));
         const auto t1 = std::chrono::steady_clock::now();
         if (sum.empty()) {
             sum.assign(buf.size(), 0.0);
@@ -178,15 +274,15 @@ std::vector<AmplitudeBatch> contract_groups(const TensorNetwork& network, const 
     check_config(plan, config);
     if (group_fixed.empty()) throw ConfigError("group count must be >= 1");
     auto f = flatten(network, plan);
-    ProgramHandle h;
-    ok(rcsg_compile(&f->net, &f->plan, g_precision, 0, &h.p));
+    std::lock_guard<std::mutex> lock(g_mu);
+    Cached& c = cached(*f, 0, {});
     const int l = static_cast<int>(network.open_labels.size());
     const std::size_t per = std::size_t{1} << l;
     std::vector<double> out(2 * per * group_fixed.size());
     const std::size_t n_cfg = config ? config->configurations.size() : 0;
-    ok(rcsg_contract_groups(h.p, group_fixed.size(), group_fixed.data(), n_cfg,
-                            config ? config->configurations.data() : nullptr, 0, plan.n_slices(),
-                            out.data(), nullptr));
+    ok(rcsg_contract_groups(c.prog, group_fixed.size(), group_fixed.data(), n_cfg,
+                            config ? config->configurations.data() : nullptr, 0, plan.n_slices(), out.data(),
+                            nullptr));
     std::vector<AmplitudeBatch> res(group_fixed.size());
     for (std::size_t g = 0; g < group_fixed.size(); ++g) {
         res[g].group_id = g;
@@ -197,6 +293,30 @@ std::vector<AmplitudeBatch> contract_groups(const TensorNetwork& network, const 
             res[g].amplitudes[i] = cplx(out[2 * (g * per + i)], out[2 * (g * per + i) + 1]);
     }
     return res;
+}
+
+void init_devices(const std::vector<int>& devices) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (Cached& c : g_cache) free_entry(c);
+    g_cache.clear();
+    if (g_ctx) rcsg_context_free(g_ctx);
+    g_ctx = nullptr;
+    g_ctx_devices = 0;
+    if (devices.empty()) return;
+    std::vector<std::int32_t> d(devices.begin(), devices.end());
+    ok(rcsg_init(d.data(), static_cast<std::int32_t>(d.size()), &g_ctx));
+    g_ctx_devices = static_cast<int>(d.size());
+}
+
+int device_count() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return g_ctx_devices;
+}
+
+void clear_program_cache() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (Cached& c : g_cache) free_entry(c);
+    g_cache.clear();
 }
 
 FidelityResult state_fidelity(std::span<const cplx> approx, std::span<const cplx> exact) {

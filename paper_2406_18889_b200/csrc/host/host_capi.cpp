@@ -135,6 +135,54 @@ int rcsh_build(int n, int cycles, const char* topology, std::uint64_t seed, cons
     });
 }
 
+// Same pipeline with an explicit planner: planner 0 reference, 1 scale, 2 auto;
+// n_groups / trials / threads tune the scale planner (ScalePlannerOptions).
+// report (may be null): [log2 total flops, log2 per-slice flops (batched model),
+// log2 once-only flops, log2 widest tensor, seconds, n_sliced, trials,
+// winning trial, threads, reduced tensors] - filled when the scale planner ran.
+int rcsh_build_ex(int n, int cycles, const char* topology, std::uint64_t seed, const int* open, int n_open,
+                  std::uint64_t budget, int effort, int k_broken, std::uint64_t m, int planner,
+                  std::uint64_t n_groups, int trials, int threads, double* report, void** out) {
+    return guarded([&] {
+        auto h = std::make_unique<Handle>();
+        h->circuit = gen_random_circuit(n, cycles, topology, seed);
+        h->net = circuit_to_network(h->circuit, std::vector<int>(open, open + n_open));
+        std::vector<Label> broken;
+        if (k_broken > 0) broken = select_broken_edges(h->net, k_broken, seed);
+        ScalePlannerOptions opt;
+        opt.n_groups = n_groups ? n_groups : 1;
+        opt.trials = trials;
+        opt.threads = threads;
+        ScalePlanReport rep;
+        bool scale = planner == 1 || (planner == 2 && reference_planner_overflows(h->net, broken));
+        if (planner == 0) {
+            h->plan = find_contraction_path_reference(h->net, budget, effort_of(effort), seed, broken);
+        } else if (scale) {
+            h->plan = find_contraction_path_scale(h->net, budget, effort_of(effort), seed, broken, opt, &rep);
+        } else {
+            try {
+                h->plan = find_contraction_path_reference(h->net, budget, effort_of(effort), seed, broken);
+            } catch (const ConfigError& e) {
+                if (std::string(e.what()).rfind("cannot slice below memory budget", 0) != 0) throw;
+                h->plan = find_contraction_path_scale(h->net, budget, effort_of(effort), seed, broken, opt, &rep);
+                scale = true;
+            }
+        }
+        if (report) {
+            const double r[10] = {rep.log2_total_flops, rep.log2_flops_per_slice_batched, rep.log2_flops_once_batched,
+                                  rep.log2_max_size, rep.seconds, static_cast<double>(rep.n_sliced),
+                                  static_cast<double>(rep.trials), static_cast<double>(rep.winning_trial),
+                                  static_cast<double>(rep.threads), static_cast<double>(rep.reduced_tensors)};
+            for (int i = 0; i < 10; ++i) report[i] = scale ? r[i] : -1.0;
+        }
+        if (k_broken > 0) {
+            h->config = make_broken_config(broken, m, seed);
+            h->has_config = true;
+        }
+        *out = h.release();
+    });
+}
+
 // Hand-built network (names '\n'-separated) planned with find_contraction_path.
 int rcsh_build_network(int n_leaves, const int* leaf_rank, const int* leaf_labels, const double* leaf_data,
                        const char* names, int n_qubits, const int* output_labels, int n_open,
