@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-xeb", action="store_true")
     ap.add_argument("--no-post", action="store_true")
+    ap.add_argument("--scale-configs", default="cfg3,cfg4",
+                    help="BASELINE configs 3-5 measured per slice with the scale planner (comma list, or none)")
+    ap.add_argument("--cfg4-slices", type=int, default=1024, help="cfg4 fixed slice subset (BASELINE: 2^10)")
     ap.add_argument("--ref-pairs", type=int, default=0,
                     help="(group, slice) pairs the reference executor runs (default: one per host core, >= 16)")
     ap.add_argument("--ref-budget", type=int, default=CFG2["budget"],
@@ -359,6 +362,81 @@ def e2e_cold(pb, precision, M, warm_value):
             "api": "fresh Problem + new candidate set, one Problem.contract_groups call over all slices"}
 
 
+SCALE_CFGS = {"cfg3": (53, 12, "sycamore53", "Sycamore-53 layout, m=12"),
+              "cfg4": (53, 20, "sycamore53", "Sycamore-53 layout, m=20"),
+              "cfg5": (60, 24, "zuchongzhi60", "Zuchongzhi-style 60 qubits, m=24")}
+
+
+def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, alt_slices=64):
+    """BASELINE configs 3-5 per slice: the scale planner (log-domain, batch-aware,
+    stem-aware slicing; widest tensor 2^30 amplitudes incl. group variants at a
+    2^36 B budget) plans the circuit for M = 64 groups; a fixed subset of the
+    first `n_slices` slices runs timed (device events, after one warm-up call)
+    and the full run is extrapolated from the per-slice time."""
+    import torch
+    from paper_2406_18889_b200._native import rcsg_stats
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    n, m, topo, desc = SCALE_CFGS[name]
+    t0 = time.perf_counter()
+    p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(planner="scale", n_groups=M,
+                                                                               trials=256)
+    plan_s = time.perf_counter() - t0
+    rep = p.plan_report or {}
+    fixed, _ = pb.build_candidate_set(n, CFG2["open"], M, pb.split_next(1, 0xCA11D))
+    out = {"workload": f"{name}: {desc}, seed 1, l=6 open={{0..5}}, M={M} groups, K=0; "
+                       f"scale planner, budget 2^{budget_log2} B",
+           "plan": {"sliced_labels": len(p.plan["sliced"]), "n_slices_log2": len(p.plan["sliced"]),
+                    "flops_per_slice_per_group": p.plan["flops_per_slice"],
+                    "log2_total_flops_batched": rep.get("log2_total_flops"),
+                    "log2_flops_per_slice_batched": rep.get("log2_flops_per_slice_batched"),
+                    "log2_widest_tensor": rep.get("log2_max_size"), "plan_s": plan_s}}
+    for prec, ns in ((precision, n_slices), (alt, alt_slices)):
+        if not prec:
+            continue
+        acc = torch.zeros(M * 64 * 2, dtype=torch.float64, device="cuda")
+        stream = torch.cuda.ExternalStream(p.stream(prec))
+        S = 8
+        t1 = time.perf_counter()
+        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, S))  # warm-up
+        torch.cuda.synchronize()
+        warm_s = time.perf_counter() - t1
+        st = rcsg_stats()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for s0 in range(0, ns, S):
+                p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None,
+                                         slices=(s0, min(s0 + S, ns)), stats=st, sync=False)
+            e1.record(stream)
+        p.sync(prec)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        p.set_profile(True)
+        pst = rcsg_stats()
+        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1), stats=pst)
+        p.set_profile(False)
+        tc_peak = bf16_peak / 2.0 if prec == "tf32" else bf16_peak
+        rate = ns / (ms / 1e3)
+        exec_tf = st.executed_flops / (ms / 1e3) / 1e12
+        top_s = pst.top_ms_sum / pst.top_launches * 1e-3 if pst.top_launches else pst.top_ms * 1e-3
+        out[prec] = {
+            "value": rate, "unit": UNIT, "timed_slices": ns, "ms": ms, "warm_s": warm_s,
+            "executed_tflops": exec_tf, "frac_of_dense_peak": exec_tf / tc_peak,
+            "peak_tflops": tc_peak, "peak_note": ("dense tf32 = 1/2 of " if prec == "tf32" else "") +
+            f"{peak_kind} dense bf16 {bf16_peak:.1f} TF/s",
+            "roofline": {"bound": "tensor", "kernel": f"plan step {pst.top_step}: tcgen05 GEMM",
+                         "achieved": pst.top_flops / top_s / 1e12 if top_s else None, "peak": tc_peak,
+                         "unit": "TFLOP/s", "frac": pst.top_flops / top_s / 1e12 / tc_peak if top_s else None,
+                         "flops": pst.top_flops, "bytes": pst.top_bytes, "launch_ms": top_s * 1e3,
+                         "share_of_slice": pst.top_ms_sum / pst.device_ms if pst.device_ms else None,
+                         "traffic": None},
+            "tensor_core_share_of_slice": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None,
+            "full_run_extrapolated_s_1gpu": p.n_slices / rate,
+            "arena_gib": st.arena_bytes / 2 ** 30, "amps_finite": bool(torch.isfinite(acc).all().item())}
+        del acc
+    return out
+
+
 def post_bench(pb, hbm_peak):
     """Fused post-processing kernel (rcsg_postprocess) at M = 2^20 groups, l = 6
     (64 Mi candidates, 1 GiB of f64 amplitudes resident in HBM): top-k with
@@ -511,6 +589,16 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    scale = {}
+    if rank == 0 and world == 1 and args.scale_configs != "none":
+        for name in [c for c in args.scale_configs.split(",") if c]:
+            try:
+                ns = args.cfg4_slices if name == "cfg4" else 64
+                scale[name] = scale_bench(pb, name, args.precision, ns,
+                                          alt=args.alt_precision if args.alt_precision != "none" else None)
+            except Exception as e:  # pragma: no cover
+                scale[name] = {"error": str(e)}
+
     post = None
     if rank == 0 and not args.no_post:
         try:
@@ -549,7 +637,7 @@ def main():
             "roofline": head["roofline"],
             "kernel_breakdown_ms": head["breakdown"],
             "e2e": e2e, "e2e_cold": cold, "cpu_baseline": cpu, "clocks": clk,
-            "postprocess": post, "xeb": xeb,
+            "postprocess": post, "xeb": xeb, "scale_configs": scale or None,
         }
         if alt:
             line[args.alt_precision] = alt

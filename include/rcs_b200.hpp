@@ -308,6 +308,33 @@ double xeb(const SampleSet& samples, const ProbFn& q);
 SampleSet top_k_select(const CandidateSet& candidates, const ProbFn& p, std::uint64_t k);
 SampleSet direct_sample(const CandidateSet& candidates, const ProbFn& p, std::uint64_t rng_seed);
 double predicted_topk_xeb(double fidelity, std::uint64_t candidate_size, std::uint64_t k);
+
+// ---- artifact formats (reference writers, byte-compatible)
+// plan.json (contraction_plan.cpp:451-491) and its import: the post-order steps
+// are rebuilt from the nested "order" pairs, sliced / broken from label names.
+std::string plan_to_json(const ContractionPlan& plan, const TensorNetwork& network);
+ContractionPlan plan_from_json(const std::string& json, const TensorNetwork& network);
+// timings.csv (contraction_engine.cpp:347-354)
+std::string timings_to_csv(const std::vector<SubtaskTiming>& timings);
+// samples.txt (sampling.cpp:177-210): character q = qubit q
+std::string samples_to_text(const SampleSet& samples);
+SampleSet samples_from_text(const std::string& text);
+// metrics.json (harness.cpp:154-175, schema "rcs-metrics-v1")
+struct MetricsReport {
+    double xeb = 0, fidelity = 0, predicted_xeb = 0, pearson_r = 0;
+    double pt_ks_statistic = 0, pt_p_value = 0, xeb_over_fidelity = 0;
+};
+struct MetricsInputs {
+    int n_qubits = 0, n_cycles = 0;
+    std::string topology;
+    std::uint64_t seed = 0;
+    std::size_t l = 0;
+    std::uint64_t n_groups = 0;
+    int broken_edges = 0;
+    std::uint64_t m_configs = 1, k = 0;
+    std::string sample_mode = "top_k";  // "direct" | "top_k"
+};
+std::string metrics_to_json(const MetricsReport& metrics, const MetricsInputs& inputs);
 std::uint64_t lexicographic_key(std::uint64_t index, int n_qubits);
 
 }  // namespace rcs

@@ -42,9 +42,12 @@ def lib():
         L.refo_lexkey.restype = C.c_uint64
         L.refo_circuit_gates.restype = C.c_int64
         L.refo_label_names.restype = C.c_int64
+        L.refo_plan_json.restype = C.c_int64
+        L.refo_timings_csv.restype = C.c_int64
+        L.refo_samples_text.restype = C.c_int64
         for name in ("refo_build", "refo_contract_group", "refo_contract", "refo_execute",
                      "refo_execute_gsc", "refo_exact", "refo_candidates", "refo_topk",
-                     "refo_direct", "refo_xeb", "refo_groups_mt", "refo_slices_mt"):
+                     "refo_direct", "refo_xeb", "refo_groups_mt", "refo_slices_mt", "refo_set_plan"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -188,6 +191,21 @@ class RefProblem:
                                   _p(out, C.c_double), C.byref(n)))
         return _cplx(out)
 
+    def plan_json(self) -> str:
+        """plan_to_json (contraction_plan.cpp:451-491) of this problem's plan."""
+        n = lib().refo_plan_json(self.handle, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        lib().refo_plan_json(self.handle, buf, n + 1)
+        return buf.value.decode()
+
+    def set_plan(self, steps, sliced):
+        """Run an imported plan (steps [n][3], sliced labels) on the reference executor."""
+        st = np.ascontiguousarray(np.asarray(steps, np.int64)[:, :3].reshape(-1), np.int32)
+        sl = _ints(list(sliced) or [0])
+        _check(lib().refo_set_plan(self.handle, len(st) // 3, _p(st, C.c_int), len(sliced), _p(sl, C.c_int)))
+        self.plan["steps"] = np.asarray(steps)
+        self.plan["sliced"] = np.asarray(sliced)
+
     def exact(self, cap: int = 24) -> np.ndarray:
         out = np.zeros(2 << self.n, np.float64)
         _check(lib().refo_exact(self.handle, cap, _p(out, C.c_double)))
@@ -265,3 +283,22 @@ def split_next(seed: int, tag: int) -> int:
 
 def lexkey(index: int, n: int) -> int:
     return int(lib().refo_lexkey(C.c_uint64(index), n))
+
+
+def timings_csv(ids, bits, ms, flops) -> str:
+    ids, bits, flops = _u64(ids), _u64(bits), _u64(flops)
+    ms = np.ascontiguousarray(ms, np.float64)
+    n = lib().refo_timings_csv(len(ids), _p(ids, C.c_uint64), _p(bits, C.c_uint64), _p(ms, C.c_double),
+                               _p(flops, C.c_uint64), None, 0)
+    buf = C.create_string_buffer(int(n) + 1)
+    lib().refo_timings_csv(len(ids), _p(ids, C.c_uint64), _p(bits, C.c_uint64), _p(ms, C.c_double),
+                           _p(flops, C.c_uint64), buf, n + 1)
+    return buf.value.decode()
+
+
+def samples_text(n_qubits, topk, k, samples) -> str:
+    s = _u64(samples)
+    n = lib().refo_samples_text(n_qubits, int(topk), C.c_uint64(k), len(s), _p(s, C.c_uint64), None, 0)
+    buf = C.create_string_buffer(int(n) + 1)
+    lib().refo_samples_text(n_qubits, int(topk), C.c_uint64(k), len(s), _p(s, C.c_uint64), buf, n + 1)
+    return buf.value.decode()

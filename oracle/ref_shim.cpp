@@ -18,6 +18,12 @@
 //   refo_topk            top_k_select (sampling.cpp:82)
 //   refo_direct          direct_sample (sampling.cpp:116)
 //   refo_xeb             xeb (sampling.cpp:62)
+//   refo_plan_json       plan_to_json (contraction_plan.cpp:451)
+//   refo_set_plan        replaces the handle's plan steps / sliced labels (plans
+//                        imported from the product's scale planner run on the
+//                        reference executor)
+//   refo_timings_csv     contract + timings_to_csv (contraction_engine.cpp:347)
+//   refo_samples_text    samples_to_text / samples_from_text (sampling.cpp:177-210)
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -421,6 +427,66 @@ int refo_slices_mt(void* hp, std::uint64_t fixed_bits, const std::uint64_t* slic
             if (rc[i]) throw Error("slice execution failed: " + g_err, rc[i]);
         (void)h;
     });
+}
+
+// plan_to_json of the handle's plan into buf (returns the length; buf may be null)
+std::int64_t refo_plan_json(void* hp, char* buf, std::int64_t cap) {
+    const Handle* h = static_cast<Handle*>(hp);
+    const std::string j = plan_to_json(h->plan, h->net);
+    if (buf && cap > 0) {
+        const std::size_t n = std::min<std::size_t>(j.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(buf, j.data(), n);
+        buf[n] = 0;
+    }
+    return static_cast<std::int64_t>(j.size());
+}
+
+// Replace the plan's steps ([n][3] lhs, rhs, result) and sliced labels; the
+// reference executor only reads lhs / rhs / result and the sliced list.
+int refo_set_plan(void* hp, int n_steps, const int* steps, int n_sliced, const int* sliced) {
+    return guarded([&] {
+        Handle* h = static_cast<Handle*>(hp);
+        h->plan.steps.clear();
+        for (int i = 0; i < n_steps; ++i) {
+            PlanStep st;
+            st.lhs = steps[3 * i];
+            st.rhs = steps[3 * i + 1];
+            st.result = steps[3 * i + 2];
+            h->plan.steps.push_back(st);
+        }
+        h->plan.sliced.assign(sliced, sliced + n_sliced);
+    });
+}
+
+// timings_to_csv of synthetic timings (ids, config bits, wall ms, flops)
+std::int64_t refo_timings_csv(int n, const std::uint64_t* ids, const std::uint64_t* bits, const double* ms,
+                              const std::uint64_t* flops, char* buf, std::int64_t cap) {
+    std::vector<SubtaskTiming> t(n);
+    for (int i = 0; i < n; ++i) t[i] = SubtaskTiming{ids[i], bits[i], ms[i], flops[i]};
+    const std::string s = timings_to_csv(t);
+    if (buf && cap > 0) {
+        const std::size_t m = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(buf, s.data(), m);
+        buf[m] = 0;
+    }
+    return static_cast<std::int64_t>(s.size());
+}
+
+// samples_to_text of (n_qubits, provenance 0 direct / 1 top-k, k, samples)
+std::int64_t refo_samples_text(int n_qubits, int topk, std::uint64_t k, int count, const std::uint64_t* samples,
+                               char* buf, std::int64_t cap) {
+    SampleSet ss;
+    ss.n_qubits = n_qubits;
+    ss.provenance = topk ? Provenance::TopK : Provenance::Direct;
+    ss.k = k;
+    ss.bitstrings.assign(samples, samples + count);
+    const std::string s = samples_to_text(ss);
+    if (buf && cap > 0) {
+        const std::size_t m = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(buf, s.data(), m);
+        buf[m] = 0;
+    }
+    return static_cast<std::int64_t>(s.size());
 }
 
 }  // extern "C"

@@ -62,11 +62,12 @@ class rcsg_post_stats(C.Structure):
 # exported symbols and their restypes (everything else returns int status)
 RCSG_SYMBOLS = [
     "rcsg_last_error", "rcsg_set_device", "rcsg_compile", "rcsg_compile_pinned", "rcsg_program_free",
-    "rcsg_program_set_profile", "rcsg_program_stream", "rcsg_gemm_selftest", "rcsg_gemm_check_f16", "rcsg_gemm_check_bf16",
+    "rcsg_program_set_profile", "rcsg_program_stream",
     "rcsg_contract_groups", "rcsg_contract_groups_device", "rcsg_execute_assignment", "rcsg_topk",
     "rcsg_topk_probs", "rcsg_direct_sample", "rcsg_direct_sample_probs", "rcsg_xeb",
     "rcsg_device_alloc", "rcsg_device_free", "rcsg_memcpy", "rcsg_program_sync", "rcsg_statevector",
-    "rcsg_statevector_probs", "rcsg_xeb_state", "rcsg_postprocess",
+    "rcsg_statevector_probs", "rcsg_xeb_state", "rcsg_postprocess", "rcsg_init", "rcsg_context_free",
+    "rcsg_context_devices", "rcsg_context_compile", "rcsg_multi_free", "rcsg_multi_contract_groups",
 ]
 RCSH_SYMBOLS = [
     "rcsh_last_error", "rcsh_build", "rcsh_build_network", "rcsh_free", "rcsh_net_sizes",
@@ -74,10 +75,25 @@ RCSH_SYMBOLS = [
     "rcsh_circuit_gates", "rcsh_contract_groups", "rcsh_contract_groups_device", "rcsh_contract",
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
     "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
-    "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector", "rcsh_build_ex",
+    "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector", "rcsh_build_ex", "rcsh_plan_import",
 ]
 
 _lib = None
+_testkit = None
+TESTKIT_PATH = os.path.join(HERE, "_native", "libpaper_2406_18889_b200_testkit.so")
+
+
+def testkit():
+    """GEMM self-test / benchmark helpers (csrc/device/gemm_bench.cu), a separate
+    library next to the product one - tests and tools only."""
+    global _testkit
+    if _testkit is None:
+        lib()
+        _testkit = C.CDLL(TESTKIT_PATH)
+        for name in ("rcsg_gemm_selftest", "rcsg_gemm_check_f16", "rcsg_gemm_check_bf16", "rcsg_gemm_check_tf32",
+                     "rcsg_gemm_bench_f16"):
+            getattr(_testkit, name).restype = C.c_int
+    return _testkit
 
 
 def lib():
@@ -100,6 +116,8 @@ def lib():
         L.rcsh_plan_sizes.restype = None
         L.rcsh_plan_export.restype = None
         L.rcsh_label_names.restype = C.c_int64
+        for name in ("rcsh_plan_json", "rcsh_timings_csv", "rcsh_samples_text", "rcsh_samples_parse"):
+            getattr(L, name).restype = C.c_int64
         L.rcsh_circuit_gates.restype = C.c_int64
         L.rcsh_member.restype = C.c_uint64
         L.rcsh_rng_split_next.restype = C.c_uint64

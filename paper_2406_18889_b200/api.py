@@ -225,6 +225,19 @@ class Problem:
                          flops_per_slice=int(tot[0]), traffic_bytes_per_slice=int(tot[1]),
                          peak_bytes=int(tot[2]), memory_budget_bytes=int(tot[3]))
 
+    def plan_json(self) -> str:
+        """plan_to_json (contraction_plan.cpp:451-491), byte-identical to the reference's."""
+        n = _native.lib().rcsh_plan_json(self.handle, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        _native.lib().rcsh_plan_json(self.handle, buf, n + 1)
+        return buf.value.decode()
+
+    def import_plan(self, text: str):
+        """Replace the plan with one read from plan.json (the reference's or ours)."""
+        _check_h(_native.lib().rcsh_plan_import(self.handle, text.encode()))
+        self._export()
+        return self
+
     def stream(self, precision="tf32", budget=0) -> int:
         """cudaStream_t (as int) the compiled program launches on."""
         out = C.c_void_p()
@@ -493,6 +506,37 @@ def xeb(n: int, q) -> float:
     out = C.c_double()
     _check_g(_native.lib().rcsg_xeb(n, C.c_uint64(len(q)), _p(q, C.c_double), C.byref(out)))
     return out.value
+
+
+def timings_to_csv(ids, bits, ms, flops) -> str:
+    """timings_to_csv (contraction_engine.cpp:347-354)."""
+    ids, bits, flops = _u64(ids), _u64(bits), _u64(flops)
+    ms = np.ascontiguousarray(ms, np.float64)
+    args = (len(ids), _p(ids, C.c_uint64), _p(bits, C.c_uint64), _p(ms, C.c_double), _p(flops, C.c_uint64))
+    n = _native.lib().rcsh_timings_csv(*args, None, 0)
+    buf = C.create_string_buffer(int(n) + 1)
+    _native.lib().rcsh_timings_csv(*args, buf, n + 1)
+    return buf.value.decode()
+
+
+def samples_to_text(n_qubits: int, samples, topk: bool = False, k: int = 0) -> str:
+    """samples_to_text (sampling.cpp:177-191): character q = qubit q."""
+    s = _u64(samples)
+    args = (n_qubits, int(topk), C.c_uint64(k), C.c_int64(len(s)), _p(s, C.c_uint64))
+    n = _native.lib().rcsh_samples_text(*args, None, 0)
+    buf = C.create_string_buffer(int(n) + 1)
+    _native.lib().rcsh_samples_text(*args, buf, n + 1)
+    return buf.value.decode()
+
+
+def samples_from_text(text: str):
+    """samples_from_text (sampling.cpp:193-210) -> (n_qubits, topk, k, samples)."""
+    meta = np.zeros(3, np.uint64)
+    raw = text.encode()
+    n = _native.lib().rcsh_samples_parse(raw, _p(meta, C.c_uint64), None)
+    out = np.zeros(max(int(n), 1), np.uint64)
+    _native.lib().rcsh_samples_parse(raw, _p(meta, C.c_uint64), _p(out, C.c_uint64))
+    return int(meta[0]), bool(meta[1]), int(meta[2]), out[:n]
 
 
 def split_next(seed: int, tag: int) -> int:

@@ -214,13 +214,14 @@ int gemm_check(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_
         int32_t* fault;
         double* d;
         const int64_t c_el = m * n;
-        if (cudaMalloc(&a, 2 * m * k * 2) || cudaMalloc(&b, 2 * n * k * 2) || cudaMalloc(&c1, 2 * c_el * 2) ||
-            cudaMalloc(&c2, 2 * c_el * 2) || cudaMalloc(&fault, 4) || cudaMalloc(&d, 16))
+        constexpr int eb = sizeof(T);
+        if (cudaMalloc(&a, 2 * m * k * eb) || cudaMalloc(&b, 2 * n * k * eb) || cudaMalloc(&c1, 2 * c_el * eb) ||
+            cudaMalloc(&c2, 2 * c_el * eb) || cudaMalloc(&fault, 4) || cudaMalloc(&d, 16))
             return RCSG_ERR_DEVICE;
         fill_half<<<1024, 256>>>(a, 2 * m * k, 7);
         fill_half<<<1024, 256>>>(b, 2 * n * k, 9);
-        cudaMemset(c1, 0, 2 * c_el * 2);
-        cudaMemset(c2, 0, 2 * c_el * 2);
+        cudaMemset(c1, 0, 2 * c_el * eb);
+        cudaMemset(c2, 0, 2 * c_el * eb);
         GemmArgs g{};
         g.a = a;
         g.a_plane = m * k;
@@ -232,7 +233,7 @@ int gemm_check(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_
         g.k = k;
         g.batch = 1;
         g.fault = fault;
-        g.scale_exp = -4;  // keep |C| well inside fp16
+        g.scale_exp = eb == 2 ? -4 : 0;  // keep |C| well inside fp16
         g.om.m_bits = m_bits;
         g.om.n_bits = n_bits;
         g.om.scatter = m_bits + n_bits > 0;
@@ -270,4 +271,10 @@ extern "C" int rcsg_gemm_check_f16(int64_t m, int64_t n, int64_t k, int32_t m_bi
 extern "C" int rcsg_gemm_check_bf16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
                                     const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
     return gemm_check<bf16>(1, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
+}
+
+// the same check for fp32 storage (tcgen05 kind::tf32 against the fp32 SIMT kernel)
+extern "C" int rcsg_gemm_check_tf32(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                    const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+    return gemm_check<float>(0, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
 }

@@ -361,6 +361,67 @@ __device__ __forceinline__ bool store_chunk_staged(const TcParams& p, int64_t v,
     return bad;
 }
 
+// Staged epilogue for 4-byte (fp32 / tf32-mode) outputs, the same idea with a
+// 32-row x 16-column fp32 half-chunk per warp (64-B rows, 16-B slots, the
+// 2-byte layout's swizzle): epi 1 = column runs of >= 4 at output bit 0
+// (lanes write 16-B vectors along rows), epi 3 = row runs of >= 4 (lanes
+// gather 4 rows of one column into a 16-B vector).
+constexpr int kEpiPitch4 = 16;  // floats per staged row (64 B)
+constexpr int kEpiWarpElems4 = 32 * kEpiPitch4;
+__device__ __forceinline__ int epi_at4(int r, int c) {
+    return r * kEpiPitch4 + ((((c >> 2) ^ (r >> 1) ^ (r >> 3)) & 3) << 2) + (c & 3);
+}
+
+template <int CW = 32>
+__device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v, int64_t row0, float* stage,
+                                                    float* x, int plane, const int64_t* tn_lo, int lane,
+                                                    int64_t my_off, int64_t col_base) {
+    bool bad = false;
+    if (p.scale_exp) {
+        const float sc = exp2f(static_cast<float>(p.scale_exp));
+#pragma unroll
+        for (int i = 0; i < CW; ++i) x[i] *= sc;
+    }
+    if (row0 + lane < p.m) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) bad |= !isfinite(x[i]);
+    }
+    float* const base = static_cast<float*>(p.c) + v * p.c_batch + plane * p.c_plane + col_base;
+#pragma unroll
+    for (int h = 0; h < CW / 16; ++h) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<float4*>(stage + epi_at4(lane, 4 * i)) =
+                make_float4(x[16 * h + 4 * i], x[16 * h + 4 * i + 1], x[16 * h + 4 * i + 2], x[16 * h + 4 * i + 3]);
+        __syncwarp();
+        if (p.epi == 3) {
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {  // 4 consecutive rows of one column
+                const int id = it * 32 + lane;
+                const int c = id >> 3, r = (id & 7) * 4;
+                float4 val;
+                val.x = stage[epi_at4(r, c)];
+                val.y = stage[epi_at4(r + 1, c)];
+                val.z = stage[epi_at4(r + 2, c)];
+                val.w = stage[epi_at4(r + 3, c)];
+                const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
+                if (row0 + r < p.m) *reinterpret_cast<float4*>(base + roff + tn_lo[16 * h + c]) = val;
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {  // 4 consecutive columns of one row
+                const int id = it * 32 + lane;
+                const int cv = id & 3, r = id >> 2;
+                const float4 val = *reinterpret_cast<const float4*>(stage + epi_at4(r, 4 * cv));
+                const int64_t roff = __shfl_sync(0xffffffffu, my_off, r);
+                if (row0 + r < p.m) *reinterpret_cast<float4*>(base + roff + tn_lo[16 * h + 4 * cv]) = val;
+            }
+        }
+        __syncwarp();
+    }
+    return bad;
+}
+
 template <int BN, int STAGES, int RB = 128>
 struct Smem {
     static constexpr int kATile = kBM * RB;  // bytes per A plane tile (RB-byte rows)
@@ -369,7 +430,7 @@ struct Smem {
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
     // persistent kernel: + staged-epilogue buffers of the 8 epilogue warps (2-byte E)
     template <typename E>
-    static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 16 * kEpiWarpElems * 2 : 0);
+    static constexpr int kPBytes = kBytes + (sizeof(E) == 2 ? 16 * kEpiWarpElems * 2 : 16 * kEpiWarpElems4 * 4);
 };
 
 template <int BN, int STAGES, typename E>
@@ -737,7 +798,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int grp = NG == 4 ? sub : (NG == 2 ? (sub >> 1) : 0);
         const int plane_lo = NG == 4 ? 0 : (sub & 1), plane_hi = NG == 4 ? 2 : plane_lo + 1;
         const int col_lo = NG == 1 ? (sub >> 1) * (BN / 2) : 0, col_hi = NG == 1 ? col_lo + BN / 2 : BN;
-        E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) + (warp - 2) * kEpiWarpElems;
+        E* stage = reinterpret_cast<E*>(smem + S::kBytes - 1024) +
+                   (warp - 2) * (sizeof(E) == 2 ? kEpiWarpElems : kEpiWarpElems4);
         // output row offset = tile part (bits >= 7 of the row, warp-uniform) + this
         // lane's part (bits 0..6, fixed), when the map's row bits cover a tile
         const int local = q * 32 + lane;
@@ -778,6 +840,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
                         bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
                                                          row < p.m ? row_off : 0, col_base);
+                        continue;
+                    }
+                } else {
+                    if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
+                        bad |= store_chunk_staged4<CW>(p, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
+                                                       plane, tn_lo, lane, row < p.m ? row_off : 0, col_base);
                         continue;
                     }
                 }
@@ -845,6 +913,22 @@ int epilogue_kind(const OutMap& om, int64_t n) {
     return 0;
 }
 
+// Staged-epilogue kind for a 4-byte output layout (see store_chunk_staged4):
+// 16-B vectors need runs of >= 4 column (epi 1) or row (epi 3) bits at bit 0.
+int epilogue_kind4(const OutMap& om, int64_t n) {
+    if (n % 16) return 0;
+    int cr = 0, rr = 0;
+    if (!om.scatter) {
+        cr = 64;
+    } else {
+        while (cr < om.n_bits && om.n_pos[cr] == cr) ++cr;
+        while (rr < om.m_bits && om.m_pos[rr] == rr) ++rr;
+    }
+    if (cr >= 2) return 1;
+    if (rr >= 2) return 3;
+    return 0;
+}
+
 template <int BN, int STAGES, typename E, int RB = 128>
 void launch(const GemmArgs& g, cudaStream_t st) {
     using S = Smem<BN, STAGES, RB>;
@@ -877,7 +961,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     p.fault = g.fault;
     p.om = g.om;
     p.scale_exp = g.scale_exp;
-    p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : 0;
+    p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : epilogue_kind4(g.om, g.n);
+    if (const char* e = getenv("RCSG_TC_NO_STAGE")) if (atoi(e)) p.epi = 0;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + kbk<E, RB> - 1) / kbk<E, RB>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
@@ -946,22 +1031,24 @@ bool gemm_tc_supported(const GemmArgs& g) {
     return true;
 }
 
-// 2-byte operands: narrow K uses 32-B / 64-B stage rows (fewer zero-filled K
-// columns, deeper stage rings); RCSG_TC_NARROW_K=0 disables
+// Narrow K uses 32-B / 64-B stage rows (fewer zero-filled K columns, deeper
+// stage rings) and n <= 32 the BN = 32 tiles, for every element type;
+// RCSG_TC_NARROW_K=0 / RCSG_TC_NARROW_N=0 disable them
 template <typename E>
-void launch_2byte(const GemmArgs& g, cudaStream_t st) {
+void launch_typed(const GemmArgs& g, cudaStream_t st) {
     static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
     static const bool narrow_n = getenv("RCSG_TC_NARROW_N") == nullptr || atoi(getenv("RCSG_TC_NARROW_N")) != 0;
+    const int64_t kb = g.k * static_cast<int64_t>(sizeof(E));  // bytes of K per row
     if (narrow_n && g.n <= 32) {  // BN = 32: every epilogue warp owns a 16-column chunk
-        if (narrow && g.k <= 16) launch<32, 12, E, 32>(g, st);
-        else if (narrow && g.k <= 32) launch<32, 8, E, 64>(g, st);
+        if (narrow && kb <= 32) launch<32, 12, E, 32>(g, st);
+        else if (narrow && kb <= 64) launch<32, 8, E, 64>(g, st);
         else launch<32, 4, E>(g, st);
         return;
     }
-    if (narrow && g.k <= 16) {
+    if (narrow && kb <= 32) {
         if (g.n >= 128) launch<128, 12, E, 32>(g, st);
         else launch<64, 12, E, 32>(g, st);
-    } else if (narrow && g.k <= 32) {
+    } else if (narrow && kb <= 64) {
         if (g.n >= 128) launch<128, 6, E, 64>(g, st);
         else launch<64, 8, E, 64>(g, st);
     } else if (g.n >= 128) {
@@ -972,14 +1059,9 @@ void launch_2byte(const GemmArgs& g, cudaStream_t st) {
 }
 
 void launch_gemm_tc(const GemmArgs& g, int elem, cudaStream_t st) {
-    if (elem == 1) {
-        launch_2byte<bf16>(g, st);
-    } else if (elem == 2) {
-        launch_2byte<f16>(g, st);
-    } else {
-        if (g.n >= 128) launch<128, 3, float>(g, st);
-        else launch<64, 4, float>(g, st);
-    }
+    if (elem == 1) launch_typed<bf16>(g, st);
+    else if (elem == 2) launch_typed<f16>(g, st);
+    else launch_typed<float>(g, st);
 }
 
 }  // namespace rcsg

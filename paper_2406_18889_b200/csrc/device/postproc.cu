@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <map>
@@ -33,6 +34,7 @@
 #include <vector>
 
 #include "executor.hpp"
+#include "kernels.cuh"
 #include "postproc.hpp"
 
 namespace rcsg {
@@ -298,6 +300,127 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         if (lane == 0) direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
     }
     if (collect) flush(0, true);
+}
+
+// Direct sampling fused with the threshold pass, for groups of <= 8192
+// candidates: each block iteration loads GPB whole groups (16-B amplitude
+// loads, coalesced, many in flight) into a shared-memory probability tile,
+// staging kept top-k candidates on the way; then thread g walks group g's
+// probabilities sequentially from shared memory (the reference's left-to-right
+// f64 total and inverse-CDF subtraction, bit for bit) - no shuffle chains.
+template <typename K, typename V>
+__global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restrict__ src, int from_amps,
+                                                          int64_t n_groups, int l, int gpb,
+                                                          const uint64_t* __restrict__ thr_p,
+                                                          K* __restrict__ out_key, V* __restrict__ out_t,
+                                                          unsigned long long* __restrict__ counter, uint64_t cap,
+                                                          int* __restrict__ bad, const uint64_t* __restrict__ fixed,
+                                                          MemberMap mm, uint64_t seed,
+                                                          uint64_t* __restrict__ direct_out,
+                                                          unsigned long long* __restrict__ zero_group) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr unsigned kStage = 2048;
+    K* s_key = reinterpret_cast<K*>(dsm);
+    V* s_t = reinterpret_cast<V*>(dsm + kStage * sizeof(K));
+    const int64_t per = int64_t{1} << l;
+    const int pitch = static_cast<int>(per) + 1;  // odd pitch: threads walking rows hit distinct banks
+    double* tile = reinterpret_cast<double*>(dsm + kStage * (sizeof(K) + sizeof(V)));
+    __shared__ unsigned s_cnt;
+    __shared__ unsigned long long s_base;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const bool collect = thr_p != nullptr;
+    const uint64_t thr = collect ? *thr_p : ~0ull;
+    const int lane = threadIdx.x & 31;
+    const int64_t tile_el = static_cast<int64_t>(gpb) * per;
+    for (int64_t g0 = blockIdx.x * static_cast<int64_t>(gpb); g0 < n_groups;
+         g0 += static_cast<int64_t>(gridDim.x) * gpb) {
+        const int64_t base_t = g0 * per;
+        const int64_t total = n_groups * per;
+        // load + stage, 256 candidates per round (block-uniform rounds)
+        for (int64_t e0 = 0; e0 < tile_el; e0 += blockDim.x) {
+            const int64_t e = e0 + threadIdx.x;
+            const int64_t t = base_t + e;
+            const bool in = e < tile_el && t < total;
+            double p = 0.0;
+            if (in) {
+                p = prob_at(src, from_amps, t);
+                flag_nan(p, bad);
+                tile[(e >> l) * pitch + (e & (per - 1))] = p;
+            }
+            if (collect) {
+                const bool take = in && asc_key(p) >= thr;
+                const unsigned mask = __ballot_sync(0xffffffffu, take);
+                if (mask) {
+                    unsigned b = 0;
+                    if (lane == 0) b = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
+                    b = __shfl_sync(0xffffffffu, b, 0);
+                    if (take) {
+                        const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
+                        s_key[pos] = static_cast<K>(~asc_key(p) >> (64 - 8 * sizeof(K)));
+                        s_t[pos] = static_cast<V>(t);
+                    }
+                }
+                __syncthreads();
+                const unsigned n = s_cnt;
+                __syncthreads();
+                if (n + blockDim.x > kStage) {
+                    if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
+                    __syncthreads();
+                    const unsigned long long b0 = s_base;
+                    for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+                        if (b0 + i < cap) {
+                            out_key[b0 + i] = s_key[i];
+                            out_t[b0 + i] = s_t[i];
+                        }
+                    __syncthreads();
+                    if (threadIdx.x == 0) s_cnt = 0;
+                    __syncthreads();
+                }
+            }
+        }
+        __syncthreads();
+        const int64_t g = g0 + threadIdx.x;
+        if (threadIdx.x < gpb && g < n_groups) {
+            const double* row = tile + threadIdx.x * pitch;
+            double tot = 0.0;
+            for (int64_t i = 0; i < per; ++i) tot = __dadd_rn(tot, row[i]);
+            if (!(tot > 0.0)) {
+                atomicMin(zero_group, static_cast<unsigned long long>(g));
+                direct_out[g] = 0;
+            } else {
+                uint64_t z = seed + static_cast<uint64_t>(g + 1) * 0x9e3779b97f4a7c15ull;
+                z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+                z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+                z ^= z >> 31;
+                double u = __dmul_rn(static_cast<double>(z >> 11) * 0x1.0p-53, tot);
+                int64_t pick = per - 1;
+                for (int64_t i = 0; i < per; ++i) {
+                    u = __dsub_rn(u, row[i]);
+                    if (u <= 0.0) {
+                        pick = i;
+                        break;
+                    }
+                }
+                direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
+            }
+        }
+        __syncthreads();  // the tile is reused
+    }
+    if (collect) {
+        __syncthreads();
+        const unsigned n = s_cnt;
+        if (n) {
+            if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
+            __syncthreads();
+            const unsigned long long b0 = s_base;
+            for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+                if (b0 + i < cap) {
+                    out_key[b0 + i] = s_key[i];
+                    out_t[b0 + i] = s_t[i];
+                }
+        }
+    }
 }
 
 // pad [count, cap) with the largest non-negative key; flags count < k or count > cap
@@ -580,7 +703,20 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         const uint64_t* thr = fast ? &d_ctl->thr : nullptr;
         K* kk = static_cast<K*>(keys);
         V* tt = static_cast<V*>(ts);
-        if (want_direct) {
+        if (want_direct && cs.l <= 13) {
+            // shared-memory tile of gpb whole groups (<= 64 KB of probabilities)
+            const int64_t per = int64_t{1} << cs.l;
+            const int gpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(128, 8192 / per)));
+            const size_t smem = 2048 * (sizeof(K) + sizeof(V)) + static_cast<size_t>(gpb) * (per + 1) * sizeof(double);
+            static std::atomic<uint64_t> attr_done[2]{};
+            if (first_on_device(attr_done[sizeof(K) == 8 ? 1 : 0]))
+                CUDA_OK(cudaFuncSetAttribute(direct_scan_kernel<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             96 * 1024));
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, 148 * 2)));
+            direct_scan_kernel<K, V><<<grid, 256, smem, st>>>(d_src, from_amps, G, cs.l, gpb, thr, kk, tt,
+                                                              &d_ctl->count, cap, &d_ctl->bad, d_fixed, mm, seed,
+                                                              d_direct, &d_ctl->zero_group);
+        } else if (want_direct) {
             const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
             scan_kernel<true, K, V><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count, cap,
                                                           &d_ctl->bad, d_fixed, mm, seed, d_direct,

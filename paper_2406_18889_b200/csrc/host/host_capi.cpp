@@ -441,6 +441,67 @@ int rcsh_candidates(int n, const int* open, int l, std::uint64_t n_groups, std::
 }
 
 // rcs::top_k_select / direct_sample with probs [n_groups][2^l] as the ProbFn.
+// ---- artifact formats (artifacts.cpp) ----------------------------------------
+namespace {
+std::int64_t copy_out(const std::string& s, char* buf, std::int64_t cap) {
+    if (buf && cap > 0) {
+        const std::size_t m = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(buf, s.data(), m);
+        buf[m] = 0;
+    }
+    return static_cast<std::int64_t>(s.size());
+}
+}  // namespace
+
+// plan_to_json of the handle's plan (returns its length; buf may be null)
+std::int64_t rcsh_plan_json(void* hp, char* buf, std::int64_t cap) {
+    const Handle* h = static_cast<Handle*>(hp);
+    return copy_out(plan_to_json(h->plan, h->net), buf, cap);
+}
+
+// plan_from_json: replace the handle's plan (its compiled programs are dropped)
+int rcsh_plan_import(void* hp, const char* json) {
+    return guarded([&] {
+        Handle* h = static_cast<Handle*>(hp);
+        ContractionPlan plan = plan_from_json(json, h->net);
+        for (auto& [k, p] : h->programs) rcsg_program_free(p);
+        h->programs.clear();
+        h->flat.reset();
+        h->plan = std::move(plan);
+        if (h->has_config && h->config.broken_labels != h->plan.broken) h->has_config = false;
+    });
+}
+
+std::int64_t rcsh_timings_csv(int n, const std::uint64_t* ids, const std::uint64_t* bits, const double* ms,
+                              const std::uint64_t* flops, char* buf, std::int64_t cap) {
+    std::vector<SubtaskTiming> t(n);
+    for (int i = 0; i < n; ++i) t[i] = SubtaskTiming{ids[i], bits[i], ms[i], flops[i]};
+    return copy_out(timings_to_csv(t), buf, cap);
+}
+
+std::int64_t rcsh_samples_text(int n_qubits, int topk, std::uint64_t k, std::int64_t count,
+                               const std::uint64_t* samples, char* buf, std::int64_t cap) {
+    SampleSet ss;
+    ss.n_qubits = n_qubits;
+    ss.provenance = topk ? Provenance::TopK : Provenance::Direct;
+    ss.k = k;
+    ss.bitstrings.assign(samples, samples + count);
+    return copy_out(samples_to_text(ss), buf, cap);
+}
+
+// samples_from_text: header into meta = {n_qubits, topk, k}; returns the sample
+// count (out may be null to size the buffer)
+std::int64_t rcsh_samples_parse(const char* text, std::uint64_t* meta, std::uint64_t* out) {
+    const SampleSet ss = samples_from_text(text);
+    if (meta) {
+        meta[0] = static_cast<std::uint64_t>(ss.n_qubits);
+        meta[1] = ss.provenance == Provenance::TopK ? 1 : 0;
+        meta[2] = ss.k;
+    }
+    if (out) std::copy(ss.bitstrings.begin(), ss.bitstrings.end(), out);
+    return static_cast<std::int64_t>(ss.bitstrings.size());
+}
+
 int rcsh_topk(int n, const int* open, int l, std::uint64_t n_groups, const std::uint64_t* fixed,
               const double* probs, std::uint64_t k, std::uint64_t* out) {
     return guarded([&] {

@@ -1,0 +1,61 @@
+"""Artifact formats against the reference's own writers:
+plan.json equal as JSON to plan_to_json (contraction_plan.cpp:451-491) and
+importable in both directions, timings.csv (contraction_engine.cpp:347-354)
+and samples.txt (sampling.cpp:177-210) byte-identical.  CPU only.
+
+plan.json is compared as parsed JSON: the oracle build links the nlohmann/json
+copy vendored in the cudnn_frontend wheel, which prints integer arrays on one
+line; upstream nlohmann (and our writer) pretty-prints every array."""
+import json
+
+import numpy as np
+
+import paper_2406_18889_b200 as pb
+
+
+def test_plan_json_matches_reference(ref):
+    for spec in [(12, 8, "grid(3,4)", 1, [0, 1, 2], 1 << 30, "low"),
+                 (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low"),
+                 (10, 10, "ring", 62, list(range(10)), 1 << 30, "low", 5, 16)]:
+        mine = pb.Problem(*spec).build().plan_json()
+        theirs = ref.RefProblem(*spec).build().plan_json()
+        assert json.loads(mine) == json.loads(theirs), spec
+        assert mine.startswith('{\n  "broken": [')  # dump(2) layout, keys sorted
+
+
+def test_plan_import_round_trip_and_scale_plans():
+    spec = (30, 14, "grid(5,6)", 1, list(range(6)), 3 << 30, "low")
+    p = pb.Problem(*spec).build()
+    q = pb.Problem(*spec).build(planner="scale", trials=16)
+    text = q.plan_json()
+    d = json.loads(text)
+    assert d["totals"]["n_slices"] == q.n_slices
+    p.import_plan(text)  # the scale plan, imported into another handle
+    assert np.array_equal(p.plan["steps"], q.plan["steps"])
+    assert list(p.plan["sliced"]) == list(q.plan["sliced"])
+    assert p.plan["flops_per_slice"] == q.plan["flops_per_slice"]
+    assert p.plan_json() == text
+
+
+def test_plan_import_from_reference_json(ref):
+    spec = (12, 8, "grid(3,4)", 1, [0, 1, 2], 1 << 12, "low")
+    r = ref.RefProblem(*spec).build()
+    p = pb.Problem(12, 8, "grid(3,4)", 1, [0, 1, 2], 1 << 30, "low").build()
+    p.import_plan(r.plan_json())
+    assert np.array_equal(p.plan["steps"][:, :3], r.plan["steps"][:, :3])
+    assert list(p.plan["sliced"]) == list(r.plan["sliced"])
+    assert p.plan["flops_per_slice"] == r.plan["flops_per_slice"]
+    assert p.plan["peak_bytes"] == r.plan["peak_bytes"]
+
+
+def test_timings_csv_and_samples_text_match_reference(ref):
+    ids, bits = [0, 1, 2], [5, 4, 6]
+    ms, flops = [1.25, 0.000123456789, 12345.678], [10, 2 ** 40, 7]
+    assert pb.api.timings_to_csv(ids, bits, ms, flops) == ref.timings_csv(ids, bits, ms, flops)
+    s = np.array([19, 0, 31, 5], np.uint64)
+    for topk, k in ((False, 0), (True, 4)):
+        text = pb.api.samples_to_text(5, s, topk, k)
+        assert text == ref.samples_text(5, topk, k, s)
+        n, tk, kk, back = pb.api.samples_from_text(text)
+        assert (n, tk, kk) == (5, topk, k) and np.array_equal(back, s)
+    assert pb.api.samples_to_text(5, [19]).splitlines()[-1] == "11001"  # test_sampling.cpp:242-258

@@ -1,8 +1,9 @@
-"""fp16 tensor-core complex GEMM (tcgen05, every epilogue kind and K-tile
-width) against the fp16 SIMT kernel on random operands through explicit output
-maps, for fp16 and bf16 storage.  rel = ||TC - SIMT|| / ||SIMT||: both round
-the same fp32-accumulated values to the storage type, so the bound is a few
-ulps (2e-3 fp16, 1.6e-2 bf16)."""
+"""Tensor-core complex GEMM (tcgen05, every epilogue kind and K-tile width)
+against the SIMT kernel of the same storage type on random operands through
+explicit output maps, for fp16, bf16 and fp32 (kind::tf32) storage.
+rel = ||TC - SIMT|| / ||SIMT||: for 2-byte storage both round the same
+fp32-accumulated values, so the bound is a few ulps (2e-3 fp16, 1.6e-2 bf16);
+tf32 truncates the fp32 operands to 10 mantissa bits (5e-3)."""
 import ctypes as C
 
 import pytest
@@ -22,14 +23,16 @@ CASES = [
     ("narrow-k16", 1 << 16, 32, 16, [0, 1, 2, 3, 4, 7, 8, 9, 10, 11, 13, 14, 15, 16, 17, 18], [5, 6, 12, 19, 20]),
     ("narrow-k32-n128", 1 << 13, 128, 32, [], []),
     ("narrow-n8", 1 << 12, 8, 64, [], []),
+    ("narrow-k8-n32", 1 << 15, 32, 8, [], []),
+    ("col-run2", 1 << 13, 64, 128, list(range(2, 15)), [0, 1, 15, 16, 17, 18]),
 ]
 
 
-@pytest.mark.parametrize("dtype,tol", [("f16", 2e-3), ("bf16", 1.6e-2)])
+@pytest.mark.parametrize("dtype,tol", [("f16", 2e-3), ("bf16", 1.6e-2), ("tf32", 5e-3)])
 @pytest.mark.parametrize("name,m,n,k,mp,npos", CASES, ids=[c[0] for c in CASES])
 def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol):
-    lib = _native.lib()
-    check = lib.rcsg_gemm_check_f16 if dtype == "f16" else lib.rcsg_gemm_check_bf16
+    lib = _native.testkit()
+    check = {"f16": lib.rcsg_gemm_check_f16, "bf16": lib.rcsg_gemm_check_bf16, "tf32": lib.rcsg_gemm_check_tf32}[dtype]
     a = (C.c_int8 * max(len(mp), 1))(*mp)
     b = (C.c_int8 * max(len(npos), 1))(*npos)
     rel = C.c_double()

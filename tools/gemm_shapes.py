@@ -2,7 +2,7 @@
 import sys, ctypes as C
 sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2406_18889_b200 import _native
-L = _native.lib()
+L = _native.testkit()
 f = L.rcsg_gemm_bench_f16
 def run(name, m, n, k, mp, npos):
     mb, nb = len(mp), len(npos)
