@@ -165,7 +165,7 @@ std::vector<Label> select_broken_edges(const TensorNetwork& network, int k_edges
 enum class PlannerKind { Reference, Scale, Auto };
 struct ScalePlannerOptions {
     std::uint64_t n_groups = 1;  // group batch the costs model (variant counts min(M, 2^b))
-    int trials = 0;              // randomized greedy trials (0: 64 / 256 / 1024 by effort)
+    int trials = 0;              // hyper-optimisation trials (0: 256 / 1024 / 4096 by effort)
     int threads = 0;             // host threads (0: all)
     int refine = 4;              // best trees refined by subtree reconfiguration
 };

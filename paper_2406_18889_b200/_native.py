@@ -76,6 +76,7 @@ RCSH_SYMBOLS = [
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
     "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
     "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector", "rcsh_build_ex", "rcsh_plan_import",
+    "rcsh_state_fidelity", "rcsh_predicted_topk_xeb",
 ]
 
 _lib = None

@@ -508,6 +508,26 @@ def xeb(n: int, q) -> float:
     return out.value
 
 
+def state_fidelity(approx, exact):
+    """state_fidelity (contraction_engine.cpp:327-345) -> (value, zero_norm_warning)."""
+    a = np.ascontiguousarray(np.asarray(approx, np.complex128)).view(np.float64)
+    e = np.ascontiguousarray(np.asarray(exact, np.complex128)).view(np.float64)
+    if a.size != e.size:
+        raise ConfigError("fidelity requires identical index sets")
+    out, warn = C.c_double(), C.c_int()
+    _check_h(_native.lib().rcsh_state_fidelity(C.c_uint64(a.size // 2), _p(a, C.c_double), _p(e, C.c_double),
+                                               C.byref(out), C.byref(warn)))
+    return out.value, bool(warn.value)
+
+
+def predicted_topk_xeb(fidelity: float, candidate_size: int, k: int) -> float:
+    """predicted_topk_xeb (sampling.cpp:147-151): F * ln(|S| / k)."""
+    out = C.c_double()
+    _check_h(_native.lib().rcsh_predicted_topk_xeb(C.c_double(fidelity), C.c_uint64(candidate_size),
+                                                   C.c_uint64(k), C.byref(out)))
+    return out.value
+
+
 def timings_to_csv(ids, bits, ms, flops) -> str:
     """timings_to_csv (contraction_engine.cpp:347-354)."""
     ids, bits, flops = _u64(ids), _u64(bits), _u64(flops)

@@ -441,6 +441,26 @@ int rcsh_candidates(int n, const int* open, int l, std::uint64_t n_groups, std::
 }
 
 // rcs::top_k_select / direct_sample with probs [n_groups][2^l] as the ProbFn.
+// state_fidelity (contraction_engine.cpp:327-345) over interleaved complex
+// arrays; *warn = 1 for the zero-norm-approximation warning
+int rcsh_state_fidelity(std::uint64_t n, const double* approx, const double* exact, double* out, int* warn) {
+    return guarded([&] {
+        std::vector<cplx> a(n), e(n);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            a[i] = cplx(approx[2 * i], approx[2 * i + 1]);
+            e[i] = cplx(exact[2 * i], exact[2 * i + 1]);
+        }
+        const FidelityResult r = state_fidelity(a, e);
+        *out = r.value;
+        if (warn) *warn = r.zero_norm_warning ? 1 : 0;
+    });
+}
+
+// predicted_topk_xeb (sampling.cpp:147-151)
+int rcsh_predicted_topk_xeb(double fidelity, std::uint64_t candidate_size, std::uint64_t k, double* out) {
+    return guarded([&] { *out = predicted_topk_xeb(fidelity, candidate_size, k); });
+}
+
 // ---- artifact formats (artifacts.cpp) ----------------------------------------
 namespace {
 std::int64_t copy_out(const std::string& s, char* buf, std::int64_t cap) {

@@ -822,7 +822,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
     for (int i = 0; i < static_cast<int>(rd.node.size()); ++i)
         rd.labels[i].each([&](int l) { lab_holders[l].push_back(i); });
     const int trials = opt.trials > 0 ? opt.trials
-                                      : (effort == SearchEffort::Low ? 64 : effort == SearchEffort::Medium ? 256 : 1024);
+                                      : (effort == SearchEffort::Low ? 256 : effort == SearchEffort::Medium ? 1024 : 4096);
     int threads = opt.threads > 0 ? opt.threads : static_cast<int>(std::thread::hardware_concurrency());
     threads = std::max(1, std::min(threads, trials));
     struct Result {
@@ -854,7 +854,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
                 greedy(pb, rd, t, gp);
             } else {            // the rest: recursive multilevel bisection, greedy below the cutoff
                 PartParams pp;
-                pp.eps = std::exp(std::log(0.01) + U(rng) * (std::log(0.6) - std::log(0.01)));
+                pp.eps = std::exp(std::log(0.01) + U(rng) * (std::log(0.99) - std::log(0.01)));
                 pp.cutoff = 4 + static_cast<int>(U(rng) * 36);
                 pp.gp = gp;
                 pp.gp.temp *= 0.1;

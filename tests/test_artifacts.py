@@ -9,6 +9,7 @@ line; upstream nlohmann (and our writer) pretty-prints every array."""
 import json
 
 import numpy as np
+import pytest
 
 import paper_2406_18889_b200 as pb
 
@@ -59,3 +60,23 @@ def test_timings_csv_and_samples_text_match_reference(ref):
         n, tk, kk, back = pb.api.samples_from_text(text)
         assert (n, tk, kk) == (5, topk, k) and np.array_equal(back, s)
     assert pb.api.samples_to_text(5, [19]).splitlines()[-1] == "11001"  # test_sampling.cpp:242-258
+
+
+def test_state_fidelity_and_predicted_topk_xeb():
+    """state_fidelity (contraction_engine.cpp:327-345) and predicted_topk_xeb
+    (sampling.cpp:147-151), host-side, against their closed forms."""
+    rng = np.random.default_rng(3)
+    e = rng.normal(size=64) + 1j * rng.normal(size=64)
+    a = 0.7 * e + 0.3 * (rng.normal(size=64) + 1j * rng.normal(size=64))
+    want = abs(np.vdot(e, a)) ** 2 / (np.vdot(a, a).real * np.vdot(e, e).real)
+    got, warn = pb.api.state_fidelity(a, e)
+    assert abs(got - want) < 1e-14 and not warn
+    assert pb.api.state_fidelity(e * 2j, e)[0] == pytest.approx(1.0, abs=1e-14)
+    assert pb.api.state_fidelity(np.zeros(64), e) == (0.0, True)  # zero-norm approximation -> 0 + warning
+    with pytest.raises(pb.ConfigError):
+        pb.api.state_fidelity(np.ones(4), np.zeros(4))  # exact collection of zero norm
+    with pytest.raises(pb.ConfigError):
+        pb.api.state_fidelity(np.ones(4), np.ones(8))
+    assert abs(pb.api.predicted_topk_xeb(1.0, 1 << 30, 1 << 15) - 10.3972) <= 1e-4  # acceptance.cpp:224-226
+    with pytest.raises(pb.ConfigError):
+        pb.api.predicted_topk_xeb(1.0 + 1e-12, 100, 10)  # F > 1 rejected (SURVEY F6)

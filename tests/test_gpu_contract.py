@@ -217,7 +217,8 @@ def test_scheduler_blocks_on_gpu_equal_single_call():
     fixed = np.array([0, 5, 22, 63], np.uint64)
     full = p.contract_groups(fixed, precision="f64", configs=None)
     got = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "f64"), p.n_slices)
-    assert rel(got, full) < 1e-12
+    assert got.is_cuda
+    assert rel(got.cpu().numpy(), full) < 1e-12
 
 
 # ---- batch-aware reassociation, level-0 caching, async calls ------------------

@@ -24,7 +24,8 @@ def _worker(rank, world, port_no, q):
         p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
         fixed = np.array([0, 5, 22, 63], np.uint64)
         out = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "tf32"), p.n_slices, rank, world)
-        q.put((rank, out.view(np.float64).tobytes()))
+        assert out.is_cuda  # partials and their sum stay on the device
+        q.put((rank, out.cpu().numpy().view(np.float64).tobytes()))
     finally:
         dist.destroy_process_group()
 
@@ -38,7 +39,7 @@ def test_two_gpu_scheduler_bit_identical():
     from paper_2406_18889_b200 import scheduler
     p = pb.Problem(10, 10, "line", 17, [0, 3, 5, 8], 20000, "low").build()
     fixed = np.array([0, 5, 22, 63], np.uint64)
-    single = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "tf32"), p.n_slices, 0, 1)
+    single = scheduler.contract_sharded(scheduler.gpu_block_fn(p, fixed, "tf32"), p.n_slices, 0, 1).cpu().numpy()
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port_no = s.getsockname()[1]
