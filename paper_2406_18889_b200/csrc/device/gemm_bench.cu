@@ -125,55 +125,19 @@ extern "C" int rcsg_gemm_selftest(int64_t m, int64_t n, int64_t k, int64_t batch
 
 // fp16 complex GEMM timing with an explicit output scatter map (kernel tuning):
 // C[m][n] (through the map) = A[m][k] B[n][k]^T; returns ms per launch.
+template <typename T>
+int gemm_bench(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits, const int8_t* m_pos,
+               const int8_t* n_pos, int32_t iters, double* out_ms);
+
 extern "C" int rcsg_gemm_bench_f16(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
                                    const int8_t* m_pos, const int8_t* n_pos, int32_t iters, double* out_ms) {
-    try {
-        __half *a, *b, *c;
-        int32_t* fault;
-        if (cudaMalloc(&a, 2 * m * k * 2) || cudaMalloc(&b, 2 * n * k * 2) || cudaMalloc(&c, 2 * m * n * 2) ||
-            cudaMalloc(&fault, 4))
-            return RCSG_ERR_DEVICE;
-        cudaMemset(a, 0, 2 * m * k * 2);
-        cudaMemset(b, 0, 2 * n * k * 2);
-        GemmArgs g{};
-        g.a = a;
-        g.a_plane = m * k;
-        g.b = b;
-        g.b_plane = n * k;
-        g.c = c;
-        g.c_plane = m * n;
-        g.m = m;
-        g.n = n;
-        g.k = k;
-        g.batch = 1;
-        g.fault = fault;
-        g.om.m_bits = m_bits;
-        g.om.n_bits = n_bits;
-        g.om.scatter = m_bits + n_bits > 0;
-        for (int j = 0; j < m_bits; ++j) g.om.m_pos[j] = m_pos[j];
-        for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        launch_gemm_tc(g, 2, 0);
-        cudaEventRecord(e0);
-        for (int i = 0; i < iters; ++i) launch_gemm_tc(g, 2, 0);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        *out_ms = ms / iters;
-        const cudaError_t err = cudaGetLastError();
-        cudaFree(a);
-        cudaFree(b);
-        cudaFree(c);
-        cudaFree(fault);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return err == cudaSuccess ? RCSG_OK : RCSG_ERR_DEVICE;
-    } catch (...) {
-        return RCSG_ERR_DEVICE;
-    }
+    return gemm_bench<__half>(2, m, n, k, m_bits, n_bits, m_pos, n_pos, iters, out_ms);
+}
+
+// fp32 storage, kind::tf32
+extern "C" int rcsg_gemm_bench_tf32(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                    const int8_t* m_pos, const int8_t* n_pos, int32_t iters, double* out_ms) {
+    return gemm_bench<float>(0, m, n, k, m_bits, n_bits, m_pos, n_pos, iters, out_ms);
 }
 
 namespace rcsg {
@@ -277,4 +241,59 @@ extern "C" int rcsg_gemm_check_bf16(int64_t m, int64_t n, int64_t k, int32_t m_b
 extern "C" int rcsg_gemm_check_tf32(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
                                     const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
     return gemm_check<float>(0, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
+}
+
+// tcgen05 GEMM timing on random operands through an explicit output map (tools only)
+template <typename T>
+int gemm_bench(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits, const int8_t* m_pos,
+               const int8_t* n_pos, int32_t iters, double* out_ms) {
+    try {
+        T *a, *b, *c;
+        int32_t* fault;
+        constexpr int eb = sizeof(T);
+        if (cudaMalloc(&a, 2 * m * k * eb) || cudaMalloc(&b, 2 * n * k * eb) || cudaMalloc(&c, 2 * m * n * eb) ||
+            cudaMalloc(&fault, 4))
+            return RCSG_ERR_DEVICE;
+        rcsg::fill_half<<<1024, 256>>>(a, 2 * m * k, 7);
+        rcsg::fill_half<<<1024, 256>>>(b, 2 * n * k, 9);
+        GemmArgs g{};
+        g.a = a;
+        g.a_plane = m * k;
+        g.b = b;
+        g.b_plane = n * k;
+        g.c = c;
+        g.c_plane = m * n;
+        g.m = m;
+        g.n = n;
+        g.k = k;
+        g.batch = 1;
+        g.fault = fault;
+        g.scale_exp = eb == 2 ? -12 : 0;
+        g.om.m_bits = m_bits;
+        g.om.n_bits = n_bits;
+        g.om.scatter = m_bits + n_bits > 0;
+        for (int j = 0; j < m_bits; ++j) g.om.m_pos[j] = m_pos[j];
+        for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        launch_gemm_tc(g, elem, 0);
+        cudaEventRecord(e0);
+        for (int i = 0; i < iters; ++i) launch_gemm_tc(g, elem, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *out_ms = ms / iters;
+        const cudaError_t err = cudaGetLastError();
+        cudaFree(a);
+        cudaFree(b);
+        cudaFree(c);
+        cudaFree(fault);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return err == cudaSuccess ? RCSG_OK : RCSG_ERR_DEVICE;
+    } catch (...) {
+        return RCSG_ERR_DEVICE;
+    }
 }

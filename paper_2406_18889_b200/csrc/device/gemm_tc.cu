@@ -210,6 +210,7 @@ struct TcParams {
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
     int32_t b_resident;     // B identical for every tile: loaded once per stage slot
     int32_t ng;             // persistent kernel: epilogue warp groups (tiles in flight), 1 / 2 / 4
+    int32_t group;          // grouped raster: G "hi" tiles per super-row (0: plain mixed-radix order)
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -663,6 +664,33 @@ struct TileIter {
         hi -= c ? n_hi : 0;
         v += d_v + c;
     }
+    // Grouped raster (long-K GEMMs): consecutive tiles - the ones in flight
+    // together - cover G "hi" tiles x (in flight / G) "lo" tiles instead of a few
+    // whole "lo" rows, so each operand panel streamed from HBM is shared by ~G
+    // (resp. in flight / G) CTAs through L2.  One 32-bit division chain per
+    // tile, for tiles that run >= 32 k-blocks.
+    template <int BN, typename E, int RB>
+    __device__ __forceinline__ TileCoord coord_at(const TcParams& p, int64_t t64) const {
+        if (!p.group) return coord<BN, E, RB>(p);
+        TileCoord c;
+        uint32_t t = static_cast<uint32_t>(t64);
+        const uint32_t q = t / splits;
+        c.split = static_cast<int>(t - q * splits);
+        const uint32_t per_v = n_lo * n_hi;
+        const uint32_t v = q / per_v, r = q - v * per_v;
+        const uint32_t G = static_cast<uint32_t>(p.group);
+        const uint32_t grp = r / (G * n_lo), rg = r - grp * (G * n_lo);
+        const uint32_t first = grp * G, gsz = min(G, n_hi - first);
+        const uint32_t hi_d = first + rg % gsz, lo_d = rg / gsz;
+        const uint32_t mtile = p.m_fast ? lo_d : hi_d, ntile = p.m_fast ? hi_d : lo_d;
+        c.v = v;
+        c.m0 = static_cast<int>(mtile * kBM);
+        c.n0 = static_cast<int>(ntile * BN);
+        c.k_begin = c.split * p.k_chunk;
+        const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
+        c.kblocks = static_cast<int>((k_end - c.k_begin + kbk<E, RB> - 1) / kbk<E, RB>);
+        return c;
+    }
     template <int BN, typename E, int RB>
     __device__ __forceinline__ TileCoord coord(const TcParams& p) const {
         TileCoord c;
@@ -736,7 +764,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             TileIter ti;
             ti.init(p, blockIdx.x, gridDim.x);
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ti.next()) {
-                const TileCoord c = ti.coord<BN, E, RB>(p);
+                const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
                 const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
@@ -764,7 +792,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             TileIter ti;
             ti.init(p, blockIdx.x, gridDim.x);
             for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j, ti.next()) {
-                const TileCoord c = ti.coord<BN, E, RB>(p);
+                const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -812,7 +840,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         ti.init(p, static_cast<uint32_t>(t0), NG * gridDim.x);
         j = static_cast<uint32_t>(grp);
         for (int64_t t = t0; t < total_tiles; t += NG * static_cast<int64_t>(gridDim.x), j += NG, ti.next()) {
-            const TileCoord c = ti.coord<BN, E, RB>(p);
+            const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
             int64_t row_off;
@@ -982,6 +1010,14 @@ void launch(const GemmArgs& g, cudaStream_t st) {
         if (ng != 1 && ng != 2 && ng != 4) ng = 1;
         while (ng > 1 && nbuf % ng) ng /= 2;
         p.ng = ng;
+    }
+    {
+        // grouped raster for long-K GEMMs with enough tiles in both directions
+        // (RCSG_TC_GROUP: override; 0 disables)
+        const int64_t n_lo = p.m_fast ? p.mt : p.nt, n_hi = p.m_fast ? p.nt : p.mt;
+        int grp = (chunk_blocks >= 32 && n_lo >= 16 && n_hi >= 8) ? 8 : 0;
+        if (const char* e = getenv("RCSG_TC_GROUP")) grp = atoi(e);
+        p.group = grp > 0 && n_hi > grp ? grp : 0;
     }
     p.b_resident = (p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
                     !(getenv("RCSG_TC_NO_BRES") != nullptr)) ? 1 : 0;

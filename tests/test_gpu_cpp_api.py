@@ -33,5 +33,5 @@ def test_cpp_cache_and_device_context(tmp_path):
     assert float(m1[-1]) < 1e-2  # tf32, blocked vs unblocked summation order
     if n_gpus >= 2:
         m2 = lines["multi devices2"]
-        assert m2[2] == "1", out
+        assert m2[3] == "1", out
         assert float(m2[-1]) < 1e-2

@@ -1,0 +1,22 @@
+"""Post-processing kernels at M = 2^20 groups (l = 6): top-k (k = 2^20, 2^15)
+and direct sampling, one call each after a warm-up - for an ncu launch list."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2406_18889_b200 as pb
+
+M, l, n = 1 << 20, 6, 30
+g = torch.Generator(device="cuda").manual_seed(1)
+amps = torch.randn((M << l) * 2, dtype=torch.float64, device="cuda", generator=g) * 2.0 ** -15
+fixed = np.random.default_rng(1).integers(0, 1 << (n - l), size=M, dtype=np.uint64)
+op = list(range(6))
+for k, d in ((1 << 20, None), (1 << 15, None), (0, 7), (1 << 20, 7)):
+    pb.api.postprocess_device_amps(n, op, fixed, amps.data_ptr(), k, direct_seed=d)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+for k, d in ((1 << 20, None), (1 << 15, None), (0, 7)):
+    _, _, st = pb.api.postprocess_device_amps(n, op, fixed, amps.data_ptr(), k, direct_seed=d)
+    print(k, d, st, flush=True)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
