@@ -993,9 +993,18 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     if (const char* e = getenv("RCSG_TC_NO_STAGE")) if (atoi(e)) p.epi = 0;
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + kbk<E, RB> - 1) / kbk<E, RB>;
-    // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split
+    // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split;
+    // then, for long-K work, keep doubling while it cuts the last-wave idle time by > 5% (wave
+    // quantisation: 256 tiles on 148 SMs leave 13% of the machine idle at any split in {1, 2})
     int splits = 1;
     while (tiles * splits < 296 && kblocks / (splits * 2) >= 8) splits *= 2;
+    {
+        const int64_t sms = num_sms();
+        auto eff = [&](int64_t units) {
+            return static_cast<double>(units) / static_cast<double>(((units + sms - 1) / sms) * sms);
+        };
+        while (kblocks / (splits * 2) >= 64 && eff(tiles * splits * 2) > eff(tiles * splits) + 0.05) splits *= 2;
+    }
     const int64_t chunk_blocks = (kblocks + splits - 1) / splits;
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;

@@ -83,6 +83,24 @@ __device__ __forceinline__ uint64_t asc_key(double p) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Sort key of a kept candidate (ascending = probability descending).  64-bit:
+// the full descending key.  32-bit: the distance of the ascending key above the
+// threshold, shifted so that probabilities up to 1 fit (distinct probabilities
+// collide only within ~1e-8 relative), inverted; equal keys are re-ordered
+// exactly by tie_fix_kernel.
+template <typename K>
+__device__ __forceinline__ K sort_key(double p, uint64_t thr) {
+    const uint64_t a = asc_key(p);
+    if constexpr (sizeof(K) == 8) {
+        return ~a;
+    } else {
+        const uint64_t span = asc_key(1.0) - thr;
+        const int sh = max(0, 64 - __clzll(static_cast<long long>(span | 1)) - 32);
+        const uint64_t d = (a - thr) >> sh;
+        return ~static_cast<K>(d > 0xffffffffull ? 0xffffffffull : d);
+    }
+}
+
 __device__ __forceinline__ void flag_nan(double p, int* bad) {
     if (p != p) atomicExch(bad, 1);
 }
@@ -199,7 +217,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         base = __shfl_sync(0xffffffffu, base, 0);
         if (take) {
             const unsigned pos = base + __popc(mask & ((1u << lane) - 1));
-            s_key[pos] = static_cast<K>(~asc_key(p) >> (64 - 8 * sizeof(K)));
+            s_key[pos] = sort_key<K>(p, thr);
             s_t[pos] = static_cast<V>(t);
         }
     };
@@ -337,45 +355,55 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
          g0 += static_cast<int64_t>(gridDim.x) * gpb) {
         const int64_t base_t = g0 * per;
         const int64_t total = n_groups * per;
-        // load + stage, 256 candidates per round (block-uniform rounds)
-        for (int64_t e0 = 0; e0 < tile_el; e0 += blockDim.x) {
-            const int64_t e = e0 + threadIdx.x;
-            const int64_t t = base_t + e;
-            const bool in = e < tile_el && t < total;
-            double p = 0.0;
-            if (in) {
-                p = prob_at(src, from_amps, t);
-                flag_nan(p, bad);
-                tile[(e >> l) * pitch + (e & (per - 1))] = p;
+        // load + stage: rounds of U x blockDim.x candidates with U independent 16-B
+        // loads per thread in flight (block-uniform rounds)
+        constexpr int U = 8;
+        for (int64_t e0 = 0; e0 < tile_el; e0 += U * static_cast<int64_t>(blockDim.x)) {
+            double pv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+                pv[u] = (e < tile_el && base_t + e < total) ? prob_at(src, from_amps, base_t + e) : 0.0;
             }
-            if (collect) {
-                const bool take = in && asc_key(p) >= thr;
-                const unsigned mask = __ballot_sync(0xffffffffu, take);
-                if (mask) {
-                    unsigned b = 0;
-                    if (lane == 0) b = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
-                    b = __shfl_sync(0xffffffffu, b, 0);
-                    if (take) {
-                        const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
-                        s_key[pos] = static_cast<K>(~asc_key(p) >> (64 - 8 * sizeof(K)));
-                        s_t[pos] = static_cast<V>(t);
-                    }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+                const int64_t t = base_t + e;
+                const bool in = e < tile_el && t < total;
+                const double p = pv[u];
+                if (in) {
+                    flag_nan(p, bad);
+                    tile[(e >> l) * pitch + (e & (per - 1))] = p;
                 }
-                __syncthreads();
-                const unsigned n = s_cnt;
-                __syncthreads();
-                if (n + blockDim.x > kStage) {
-                    if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
-                    __syncthreads();
-                    const unsigned long long b0 = s_base;
-                    for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
-                        if (b0 + i < cap) {
-                            out_key[b0 + i] = s_key[i];
-                            out_t[b0 + i] = s_t[i];
+                if (collect) {
+                    const bool take = in && asc_key(p) >= thr;
+                    const unsigned mask = __ballot_sync(0xffffffffu, take);
+                    if (mask) {
+                        unsigned b = 0;
+                        if (lane == 0) b = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
+                        b = __shfl_sync(0xffffffffu, b, 0);
+                        if (take) {
+                            const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
+                            s_key[pos] = sort_key<K>(p, thr);
+                            s_t[pos] = static_cast<V>(t);
                         }
+                    }
                     __syncthreads();
-                    if (threadIdx.x == 0) s_cnt = 0;
+                    const unsigned n = s_cnt;
                     __syncthreads();
+                    if (n + blockDim.x > kStage) {
+                        if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
+                        __syncthreads();
+                        const unsigned long long b0 = s_base;
+                        for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+                            if (b0 + i < cap) {
+                                out_key[b0 + i] = s_key[i];
+                                out_t[b0 + i] = s_t[i];
+                            }
+                        __syncthreads();
+                        if (threadIdx.x == 0) s_cnt = 0;
+                        __syncthreads();
+                    }
                 }
             }
         }
@@ -429,7 +457,7 @@ __global__ void pad_kernel(K* __restrict__ key, V* __restrict__ t, const unsigne
                            uint64_t cap, uint64_t k, int* __restrict__ fail) {
     const uint64_t cnt = *counter;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
-    const K pad = static_cast<K>(kPadKey >> (64 - 8 * sizeof(K)));
+    const K pad = sizeof(K) == 8 ? static_cast<K>(kPadKey) : static_cast<K>(~K{0});  // sorts after every kept key
     for (uint64_t i = cnt + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < cap;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         key[i] = pad;
@@ -740,7 +768,8 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
                                                                                  &d_ctl->fail);
         K* kb = static_cast<K*>(scratch(kKeyB, cap * sizeof(K)));
         V* tb = static_cast<V*>(scratch(kTB, cap * sizeof(V)));
-        const int end_bit = 8 * static_cast<int>(sizeof(K)) - 1;  // non-negative keys: top bit clear
+        // 64-bit keys of non-negative probabilities have the top bit clear; 32-bit keys use every bit
+        const int end_bit = sizeof(K) == 8 ? 63 : 32;
         size_t tmp_bytes = 0;
         CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka, kb, ta, tb, cap, 0, end_bit, st));
         void* tmp = scratch(kTmp, tmp_bytes);
