@@ -629,40 +629,43 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) 
     return c;
 }
 
-// Tile index t = ((v * n_hi + hi) * n_lo + lo) * splits + split, with (lo, hi) =
+// Tile index t = ((split * n_v + v) * n_hi + hi) * n_lo + lo, with (lo, hi) =
 // (m tile, n tile) when m_fast else (n tile, m tile).  A CTA walks t = blockIdx.x,
 // blockIdx.x + gridDim.x, ...: the digits advance by gridDim.x's mixed-radix
 // digits with carries, so no division per tile.
 struct TileIter {
     uint32_t split, lo, hi, v;           // current digits
     uint32_t d_split, d_lo, d_hi, d_v;   // gridDim.x in the same radix
-    uint32_t splits, n_lo, n_hi;
+    uint32_t splits, n_lo, n_hi, n_v;
     __device__ void init(const TcParams& p, uint32_t t, uint32_t step) {
         splits = static_cast<uint32_t>(p.splits);
         n_lo = static_cast<uint32_t>(p.m_fast ? p.mt : p.nt);
         n_hi = static_cast<uint32_t>(p.m_fast ? p.nt : p.mt);
+        n_v = static_cast<uint32_t>(p.batch < 1 ? 1 : p.batch);
+        // split is the slowest digit: the tiles in flight together work on the
+        // same K range, so their A / B panels are shared through L2
         auto digits = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
-            a = x % splits;
-            x /= splits;
             b = x % n_lo;
             x /= n_lo;
             c = x % n_hi;
-            d = x / n_hi;
+            x /= n_hi;
+            d = x % n_v;
+            a = x / n_v;
         };
         digits(t, split, lo, hi, v);
         digits(step, d_split, d_lo, d_hi, d_v);
     }
     __device__ __forceinline__ void next() {
-        split += d_split;
-        uint32_t c = split >= splits;
-        split -= c ? splits : 0;
-        lo += d_lo + c;
-        c = lo >= n_lo;
+        lo += d_lo;
+        uint32_t c = lo >= n_lo;
         lo -= c ? n_lo : 0;
         hi += d_hi + c;
         c = hi >= n_hi;
         hi -= c ? n_hi : 0;
         v += d_v + c;
+        c = v >= n_v;
+        v -= c ? n_v : 0;
+        split += d_split + c;
     }
     // Grouped raster (long-K GEMMs): consecutive tiles - the ones in flight
     // together - cover G "hi" tiles x (in flight / G) "lo" tiles instead of a few
@@ -673,10 +676,10 @@ struct TileIter {
     __device__ __forceinline__ TileCoord coord_at(const TcParams& p, int64_t t64) const {
         if (!p.group) return coord<BN, E, RB>(p);
         TileCoord c;
-        uint32_t t = static_cast<uint32_t>(t64);
-        const uint32_t q = t / splits;
-        c.split = static_cast<int>(t - q * splits);
-        const uint32_t per_v = n_lo * n_hi;
+        const uint32_t t = static_cast<uint32_t>(t64);
+        const uint32_t per_v = n_lo * n_hi, per_split = per_v * n_v;
+        c.split = static_cast<int>(t / per_split);
+        const uint32_t q = t - static_cast<uint32_t>(c.split) * per_split;
         const uint32_t v = q / per_v, r = q - v * per_v;
         const uint32_t G = static_cast<uint32_t>(p.group);
         const uint32_t grp = r / (G * n_lo), rg = r - grp * (G * n_lo);
