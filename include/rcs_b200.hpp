@@ -167,7 +167,8 @@ struct ScalePlannerOptions {
     std::uint64_t n_groups = 1;  // group batch the costs model (variant counts min(M, 2^b))
     int trials = 0;              // hyper-optimisation trials (0: 256 / 1024 / 4096 by effort)
     int threads = 0;             // host threads (0: all)
-    int refine = 4;              // best trees refined by subtree reconfiguration
+    int refine = 16;             // best trees refined by subtree reconfiguration
+    int phases = 1;              // 2: search again on the network with phase 1's slice set cut
 };
 struct ScalePlanReport {
     double log2_total_flops = 0;              // all slices, batched cost model

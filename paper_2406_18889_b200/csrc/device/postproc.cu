@@ -472,7 +472,7 @@ template <typename K, typename V>
 __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
                                const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
                                const double* __restrict__ src, int from_amps, const uint64_t* __restrict__ fixed,
-                               MemberMap mm, int* __restrict__ fail) {
+                               MemberMap mm, int* __restrict__ fail, uint64_t* __restrict__ out) {
     const uint64_t n = min(static_cast<uint64_t>(*counter), cap);  // real entries (pads excluded)
     const uint64_t low = (1ull << mm.l) - 1;
     auto order_key = [&](uint64_t ti, uint64_t& full, uint64_t& lex) {
@@ -481,14 +481,19 @@ __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
     };
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < k;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        if (i > 0 && key[i] == key[i - 1]) continue;   // not a run start
-        if (i + 1 >= n || key[i + 1] != key[i]) continue;  // run of one
+        if (i > 0 && key[i] == key[i - 1]) continue;   // inside a run: its start writes it
+        if (i + 1 >= n || key[i + 1] != key[i]) {      // run of one: the index straight out
+            const uint64_t ti = t[i];
+            out[i] = member_index(mm, fixed[ti >> mm.l], ti & low);
+            continue;
+        }
         uint64_t e = i + 1;
         while (e < n && key[e] == key[i] && e - i <= 256) ++e;
         if (e - i > 256) {  // pathological tie run: the caller sorts every candidate instead
             atomicExch(fail, 2);
             continue;
         }
+        // (runs are re-ordered then written out below, up to k)
         // insertion sort of t[i, e) (runs are short)
         for (uint64_t a = i + 1; a < e; ++a) {
             const V ta = t[a];
@@ -504,6 +509,10 @@ __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
                 --b;
             }
             t[b] = ta;
+        }
+        for (uint64_t a = i; a < e && a < k; ++a) {
+            const uint64_t ta = t[a];
+            out[a] = member_index(mm, fixed[ta >> mm.l], ta & low);
         }
     }
 }
@@ -716,7 +725,8 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         cap = std::max<uint64_t>(cap, k);
         uint32_t* hist = scratch_as<uint32_t>(kHist, 2 * kHistBins);
         CUDA_OK(cudaMemsetAsync(hist, 0, 2 * kHistBins * sizeof(uint32_t), st));
-        const int hgrid = grid_for(n_s << cs.l, 512);
+        // few blocks: each merges its shared histogram into the global one with one atomic per bin
+        const int hgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(((n_s << cs.l) + 4095) / 4096, 296)));
         for (int level = 0; level < 2; ++level) {
             sample_hist_kernel<<<hgrid, 512, 0, st>>>(d_src, from_amps, G, cs.l, stride, level, d_ctl->sel, hist,
                                                       &d_ctl->bad);
@@ -734,13 +744,14 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         if (want_direct && cs.l <= 13) {
             // shared-memory tile of gpb whole groups (<= 64 KB of probabilities)
             const int64_t per = int64_t{1} << cs.l;
-            const int gpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(128, 8192 / per)));
+            // 32 groups per tile (16.6 KB at l = 6): ~6 blocks per SM hide the load latency
+            const int gpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, 8192 / per)));
             const size_t smem = 2048 * (sizeof(K) + sizeof(V)) + static_cast<size_t>(gpb) * (per + 1) * sizeof(double);
             static std::atomic<uint64_t> attr_done[2]{};
             if (first_on_device(attr_done[sizeof(K) == 8 ? 1 : 0]))
                 CUDA_OK(cudaFuncSetAttribute(direct_scan_kernel<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              96 * 1024));
-            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, 148 * 2)));
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, 148 * 6)));
             direct_scan_kernel<K, V><<<grid, 256, smem, st>>>(d_src, from_amps, G, cs.l, gpb, thr, kk, tt,
                                                               &d_ctl->count, cap, &d_ctl->bad, d_fixed, mm, seed,
                                                               d_direct, &d_ctl->zero_group);
@@ -775,8 +786,7 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         void* tmp = scratch(kTmp, tmp_bytes);
         CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ka, kb, ta, tb, cap, 0, end_bit, st));
         tie_fix_kernel<K, V><<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(
-            kb, tb, &d_ctl->count, cap, k, d_src, from_amps, d_fixed, mm, &d_ctl->fail);
-        index_kernel<V><<<grid_for(static_cast<int64_t>(k), 256), 256, 0, st>>>(tb, k, d_fixed, mm, d_top);
+            kb, tb, &d_ctl->count, cap, k, d_src, from_amps, d_fixed, mm, &d_ctl->fail, d_top);
     };
     auto select = [&](bool use_fast) {
         if (use_fast) {

@@ -558,37 +558,60 @@ int partition_tree(const Problem& pb, const Reduced& rd, const std::vector<std::
 // ---------------------------------------------------------------- slicing
 // Adds sliced labels until the widest tensor fits; each pick is the label of a
 // widest tensor that minimises the total (sliced) cost.
+bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width);
+
+// One slicing step: the label of a widest tensor that minimises the total
+// (sliced) cost.  Returns false when the widest tensor already fits.
+bool slice_one(const Problem& pb, const Tree& t, LSet& sliced, int& n_sliced) {
+    Eval e = evaluate(pb, t, sliced, n_sliced);
+    if (e.max_size <= pb.width + 1e-9) return false;
+    const int n = static_cast<int>(t.l.size());
+    // candidates: labels of the widest tensors
+    LSet cand(pb.n_labels);
+    for (int v = 0; v < n; ++v)
+        if (e.labels[v].count() + e.var[v] >= e.max_size - 1e-9)
+            for (std::size_t k = 0; k < cand.w.size(); ++k) cand.w[k] |= e.labels[v].w[k];
+    for (std::size_t k = 0; k < cand.w.size(); ++k) cand.w[k] &= ~pb.open.w[k];
+    const std::vector<int> order = post_order(t);
+    const double mult1 = std::ldexp(1.0, n_sliced + 1);
+    int best = -1;
+    double best_total = std::numeric_limits<double>::infinity();
+    cand.each([&](int l) {
+        double tot = 0;
+        for (int v : order) {
+            const int a = t.l[v], b = t.r[v];
+            const bool in = e.labels[a].has(l) || e.labels[b].has(l);
+            const bool dep = e.dep[v] || e.sub[v].has(l);
+            tot += std::exp2(e.cost[v] - (in ? 1.0 : 0.0)) * (dep ? mult1 : 1.0);
+        }
+        if (tot < best_total) {
+            best_total = tot;
+            best = l;
+        }
+    });
+    if (best < 0) throw ConfigError("scale planner: cannot slice below the memory budget (open legs too wide)");
+    sliced.set(best);
+    ++n_sliced;
+    return true;
+}
+
+// Adds sliced labels until the widest tensor fits.
 void slice_to_width(const Problem& pb, const Tree& t, LSet& sliced, int& n_sliced) {
+    for (int guard = 0; guard < pb.n_labels; ++guard)
+        if (!slice_one(pb, t, sliced, n_sliced)) return;
+    throw ConfigError("scale planner: slicing did not converge");
+}
+
+// Slice-and-reconfigure from the unsliced tree: one label at a time, each
+// followed by a reconfiguration pass that may not widen the tree, so the tree
+// adapts to every cut before the next one is chosen.
+void slice_and_reconfigure(const Problem& pb, Tree& t, LSet& sliced, int& n_sliced) {
+    sliced = LSet(pb.n_labels);
+    n_sliced = 0;
     for (int guard = 0; guard < pb.n_labels; ++guard) {
-        Eval e = evaluate(pb, t, sliced, n_sliced);
-        if (e.max_size <= pb.width + 1e-9) return;
-        const int n = static_cast<int>(t.l.size());
-        // candidates: labels of the widest tensors
-        LSet cand(pb.n_labels);
-        for (int v = 0; v < n; ++v)
-            if (e.labels[v].count() + e.var[v] >= e.max_size - 1e-9)
-                for (std::size_t k = 0; k < cand.w.size(); ++k) cand.w[k] |= e.labels[v].w[k];
-        for (std::size_t k = 0; k < cand.w.size(); ++k) cand.w[k] &= ~pb.open.w[k];
-        const std::vector<int> order = post_order(t);
-        const double mult1 = std::ldexp(1.0, n_sliced + 1);
-        int best = -1;
-        double best_total = std::numeric_limits<double>::infinity();
-        cand.each([&](int l) {
-            double tot = 0;
-            for (int v : order) {
-                const int a = t.l[v], b = t.r[v];
-                const bool in = e.labels[a].has(l) || e.labels[b].has(l);
-                const bool dep = e.dep[v] || e.sub[v].has(l);
-                tot += std::exp2(e.cost[v] - (in ? 1.0 : 0.0)) * (dep ? mult1 : 1.0);
-            }
-            if (tot < best_total) {
-                best_total = tot;
-                best = l;
-            }
-        });
-        if (best < 0) throw ConfigError("scale planner: cannot slice below the memory budget (open legs too wide)");
-        sliced.set(best);
-        ++n_sliced;
+        const double w = evaluate(pb, t, sliced, n_sliced).max_size;
+        reconfigure_pass(pb, t, sliced, n_sliced, std::max(w, pb.width));
+        if (!slice_one(pb, t, sliced, n_sliced)) return;
     }
     throw ConfigError("scale planner: slicing did not converge");
 }
@@ -598,7 +621,8 @@ void slice_to_width(const Problem& pb, const Tree& t, LSet& sliced, int& n_slice
 // over input subsets.  Returns true if the subtree's cost dropped.
 constexpr int kMaxIn = 8;
 
-bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_sliced, std::vector<int>& free_ids) {
+bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_sliced, std::vector<int>& free_ids,
+                    double width) {
     if (t.l[v] < 0) return false;
     // frontier: expand the widest internal node until kMaxIn inputs
     std::vector<int> in{t.l[v], t.r[v]}, inner{v};
@@ -660,7 +684,7 @@ bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_slic
         if (std::popcount(static_cast<unsigned>(S)) < 2) continue;
         const double var = vbits(pb, outs[S]);
         const double size = pc(L[S]) + var;
-        if (S != full && size > pb.width + 1e-9) continue;
+        if (S != full && size > width + 1e-9) continue;
         const double w = dep[S] ? mult : 1.0;
         const int low = S & -S;
         // A contains the lowest input (each unordered split once)
@@ -703,14 +727,14 @@ bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_slic
 
 // One pass over every internal node, costliest steps first (internal ids are
 // arbitrary here; emit() numbers the steps in post-order).
-bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced) {
+bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width) {
     bool any = false;
     Eval e = evaluate(pb, t, sliced, n_sliced);
     std::vector<int> order = post_order(t);
     std::sort(order.begin(), order.end(), [&](int a, int b) { return e.cost[a] > e.cost[b]; });
     std::vector<int> free_ids;
     for (int v : order) {
-        if (reconfigure_at(pb, t, e, v, n_sliced, free_ids)) {
+        if (reconfigure_at(pb, t, e, v, n_sliced, free_ids, width < 0 ? pb.width : width)) {
             any = true;
             e = evaluate(pb, t, sliced, n_sliced);  // the subtree's node ids now hold new contractions
         }
@@ -812,19 +836,12 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
             throw ConfigError("memory budget " + std::to_string(memory_budget_bytes) +
                               " B is infeasible: smaller than a single tensor");
     }
-    // simplification (deterministic), shared by every trial
-    Tree base;
-    base.l.assign(pb.n_leaves, -1);
-    base.r.assign(pb.n_leaves, -1);
-    const Reduced rd = simplify(pb, base);
-
-    std::vector<std::vector<int>> lab_holders(pb.n_labels);
-    for (int i = 0; i < static_cast<int>(rd.node.size()); ++i)
-        rd.labels[i].each([&](int l) { lab_holders[l].push_back(i); });
     const int trials = opt.trials > 0 ? opt.trials
                                       : (effort == SearchEffort::Low ? 256 : effort == SearchEffort::Medium ? 1024 : 4096);
     int threads = opt.threads > 0 ? opt.threads : static_cast<int>(std::thread::hardware_concurrency());
     threads = std::max(1, std::min(threads, trials));
+    const bool debug = getenv("RCSG_PLAN_DEBUG") != nullptr;
+    std::mutex debug_mu;
     struct Result {
         double total = std::numeric_limits<double>::infinity();
         Tree tree;
@@ -832,74 +849,106 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
         int n_sliced = 0;
         int trial = -1;
     };
-    std::vector<Result> best_of(threads);
-    std::atomic<int> next_trial{0};
-    const bool debug = getenv("RCSG_PLAN_DEBUG") != nullptr;
-    std::mutex debug_mu;
-    auto worker = [&](int w) {
-        for (int tr; (tr = next_trial.fetch_add(1)) < trials;) {
-            std::mt19937_64 rng(seed * 0x9e3779b97f4a7c15ull + static_cast<std::uint64_t>(tr) * 0xd1b54a32d192ed03ull + 1);
-            std::uniform_real_distribution<double> U(0.0, 1.0);
-            GreedyParams gp;
-            if (tr == 0) {  // one plain greedy (alpha 1, no noise)
-                gp.alpha = 1.0;
-                gp.temp = 0.0;
-            } else {
-                gp.alpha = 2.0 * U(rng);
-                gp.temp = std::exp(std::log(1e-3) + U(rng) * (std::log(1.0) - std::log(1e-3)));
+    int reduced_tensors = 0;
+    // One search phase: trees are built on the network with `pre` labels removed
+    // (phase 1: none; phase 2: the best phase-1 slice set, so the partitions see
+    // the sliced network), sliced further to the width limit starting from
+    // `pre`, and the best few are refined by reconfiguration.
+    auto phase = [&](const LSet& pre, int n_pre, int phase_id) {
+        Problem tb = pb;  // tree-building view: pre-sliced labels cut
+        for (auto& lf : tb.leaf)
+            for (std::size_t k = 0; k < lf.w.size(); ++k) lf.w[k] &= ~pre.w[k];
+        Tree base;
+        base.l.assign(pb.n_leaves, -1);
+        base.r.assign(pb.n_leaves, -1);
+        const Reduced rd = simplify(tb, base);
+        reduced_tensors = static_cast<int>(rd.node.size());
+        std::vector<std::vector<int>> lab_holders(pb.n_labels);
+        for (int i = 0; i < static_cast<int>(rd.node.size()); ++i)
+            rd.labels[i].each([&](int l) { lab_holders[l].push_back(i); });
+        const int keep = std::max(1, opt.refine);
+        std::vector<std::vector<Result>> tops(threads);  // per worker: its `keep` best trees
+        std::atomic<int> next_trial{0};
+        auto worker = [&](int w) {
+            for (int tr; (tr = next_trial.fetch_add(1)) < trials;) {
+                std::mt19937_64 rng(seed * 0x9e3779b97f4a7c15ull + static_cast<std::uint64_t>(tr) * 0xd1b54a32d192ed03ull +
+                                    1 + static_cast<std::uint64_t>(phase_id) * 0x632be59bd9b4e019ull);
+                std::uniform_real_distribution<double> U(0.0, 1.0);
+                GreedyParams gp;
+                if (tr == 0) {  // one plain greedy (alpha 1, no noise)
+                    gp.alpha = 1.0;
+                    gp.temp = 0.0;
+                } else {
+                    gp.alpha = 2.0 * U(rng);
+                    gp.temp = std::exp(std::log(1e-3) + U(rng) * (std::log(1.0) - std::log(1e-3)));
+                }
+                gp.seed = rng();
+                Tree t = base;
+                if (tr % 4 == 0) {  // a quarter of the trials: randomized greedy on the whole network
+                    greedy(tb, rd, t, gp);
+                } else {            // the rest: recursive multilevel bisection, greedy below the cutoff
+                    PartParams pp;
+                    pp.eps = std::exp(std::log(0.01) + U(rng) * (std::log(0.99) - std::log(0.01)));
+                    pp.cutoff = 4 + static_cast<int>(U(rng) * 36);
+                    pp.gp = gp;
+                    pp.gp.temp *= 0.1;
+                    std::vector<int> all(rd.node.size());
+                    std::iota(all.begin(), all.end(), 0);
+                    t.root = partition_tree(tb, rd, lab_holders, all, t, pp, rng);
+                }
+                LSet sl = pre;
+                int ns = n_pre;
+                try {
+                    slice_to_width(pb, t, sl, ns);
+                } catch (const ConfigError&) {
+                    continue;
+                }
+                const double tot = evaluate(pb, t, sl, ns).total;
+                if (debug) {
+                    std::lock_guard<std::mutex> lk(debug_mu);
+                    fprintf(stderr, "[plan] phase %d trial %d %s log2 total %.2f sliced %d\n", phase_id, tr,
+                            tr % 4 == 0 ? "greedy" : "partition", std::log2(tot), ns);
+                }
+                auto& top = tops[w];
+                if (static_cast<int>(top.size()) < keep || tot < top.back().total) {
+                    top.push_back(Result{tot, std::move(t), sl, ns, tr});
+                    std::sort(top.begin(), top.end(), [](const Result& a, const Result& b) { return a.total < b.total; });
+                    if (static_cast<int>(top.size()) > keep) top.pop_back();
+                }
             }
-            gp.seed = rng();
-            Tree t = base;
-            if (tr % 4 == 0) {  // a quarter of the trials: randomized greedy on the whole network
-                greedy(pb, rd, t, gp);
-            } else {            // the rest: recursive multilevel bisection, greedy below the cutoff
-                PartParams pp;
-                pp.eps = std::exp(std::log(0.01) + U(rng) * (std::log(0.99) - std::log(0.01)));
-                pp.cutoff = 4 + static_cast<int>(U(rng) * 36);
-                pp.gp = gp;
-                pp.gp.temp *= 0.1;
-                std::vector<int> all(rd.node.size());
-                std::iota(all.begin(), all.end(), 0);
-                t.root = partition_tree(pb, rd, lab_holders, all, t, pp, rng);
-            }
-            LSet sl(pb.n_labels);
-            int ns = 0;
-            try {
-                slice_to_width(pb, t, sl, ns);
-            } catch (const ConfigError&) {
-                continue;
-            }
-            const double tot = evaluate(pb, t, sl, ns).total;
-            if (debug) {
-                std::lock_guard<std::mutex> lk(debug_mu);
-                fprintf(stderr, "[plan] trial %d %s log2 total %.2f sliced %d\n", tr, tr % 4 == 0 ? "greedy" : "partition",
-                        std::log2(tot), ns);
-            }
-            if (tot < best_of[w].total) best_of[w] = Result{tot, std::move(t), sl, ns, tr};
+        };
+        {
+            std::vector<std::thread> pool;
+            for (int w = 1; w < threads; ++w) pool.emplace_back(worker, w);
+            worker(0);
+            for (auto& th : pool) th.join();
         }
-    };
-    {
-        std::vector<std::thread> pool;
-        for (int w = 1; w < threads; ++w) pool.emplace_back(worker, w);
-        worker(0);
-        for (auto& th : pool) th.join();
-    }
-    std::sort(best_of.begin(), best_of.end(), [](const Result& a, const Result& b) {
-        return a.total < b.total || (a.total == b.total && a.trial < b.trial);
-    });
-    if (!(best_of[0].total < std::numeric_limits<double>::infinity()))
-        throw ConfigError("scale planner: no trial fits the memory budget");
-    // reconfigure the best few trees (in parallel), re-slicing as needed
-    const int n_refine = std::min<int>(std::max(1, opt.refine), static_cast<int>(best_of.size()));
-    {
+        std::vector<Result> best_of;
+        for (auto& top : tops)
+            for (auto& r : top) best_of.push_back(std::move(r));
+        if (best_of.empty()) best_of.resize(1);
+        std::sort(best_of.begin(), best_of.end(), [](const Result& a, const Result& b) {
+            return a.total < b.total || (a.total == b.total && a.trial < b.trial);
+        });
+        // reconfigure the best few trees (in parallel), re-slicing as needed
+        const int n_refine = std::min<int>(std::max(1, opt.refine), static_cast<int>(best_of.size()));
         std::vector<std::thread> pool;
         for (int i = 0; i < n_refine; ++i)
             pool.emplace_back([&, i] {
                 Result& r = best_of[i];
                 if (r.trial < 0) return;
+                if (i < 8 && r.n_sliced > 0) {  // the best few also try slice-and-reconfigure
+                    Result alt = r;
+                    try {
+                        slice_and_reconfigure(pb, alt.tree, alt.sliced, alt.n_sliced);
+                        alt.total = evaluate(pb, alt.tree, alt.sliced, alt.n_sliced).total;
+                        if (alt.total < r.total) r = std::move(alt);
+                    } catch (const ConfigError&) {
+                    }
+                }
                 for (int round = 0; round < 8; ++round) {
                     bool changed = false;
-                    for (int pass = 0; pass < 6 && reconfigure_pass(pb, r.tree, r.sliced, r.n_sliced); ++pass)
+                    for (int pass = 0; pass < 6 && reconfigure_pass(pb, r.tree, r.sliced, r.n_sliced, -1); ++pass)
                         changed = true;
                     // try dropping sliced labels the reconfigured tree no longer needs
                     std::vector<int> sl;
@@ -920,16 +969,28 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
                 r.total = evaluate(pb, r.tree, r.sliced, r.n_sliced).total;
                 if (debug) {
                     std::lock_guard<std::mutex> lk(debug_mu);
-                    fprintf(stderr, "[plan] refine trial %d: log2 total %.2f -> %.2f sliced %d\n", r.trial,
-                            std::log2(before), std::log2(r.total), r.n_sliced);
+                    fprintf(stderr, "[plan] phase %d refine trial %d: log2 total %.2f -> %.2f sliced %d\n", phase_id,
+                            r.trial, std::log2(before), std::log2(r.total), r.n_sliced);
                 }
             });
         for (auto& th : pool) th.join();
+        std::sort(best_of.begin(), best_of.begin() + n_refine, [](const Result& a, const Result& b) {
+            return a.total < b.total || (a.total == b.total && a.trial < b.trial);
+        });
+        return best_of[0];
+    };
+    Result best = phase(LSet(pb.n_labels), 0, 0);
+    if (!(best.total < std::numeric_limits<double>::infinity()))
+        throw ConfigError("scale planner: no trial fits the memory budget");
+    // phase 2 (sliced plans): search again on the network with the phase-1 slice set cut
+    if (best.n_sliced > 0 && opt.phases > 1) {
+        Result second = phase(best.sliced, best.n_sliced, 1);
+        if (second.total < best.total) {
+            second.trial += trials;  // report phase-2 winners after phase-1 trial ids
+            best = std::move(second);
+        }
     }
-    std::sort(best_of.begin(), best_of.begin() + n_refine, [](const Result& a, const Result& b) {
-        return a.total < b.total || (a.total == b.total && a.trial < b.trial);
-    });
-    const Result& win = best_of[0];
+    const Result& win = best;
     // sliced labels in ascending label order (slice bit b <-> sliced[b])
     std::vector<Label> sliced;
     win.sliced.each([&](int l) { sliced.push_back(l); });
@@ -949,7 +1010,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
         report->trials = trials;
         report->winning_trial = win.trial;
         report->threads = threads;
-        report->reduced_tensors = static_cast<int>(rd.node.size());
+        report->reduced_tensors = reduced_tensors;
         report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     }
     return plan;
