@@ -379,7 +379,7 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
     n, m, topo, desc = SCALE_CFGS[name]
     t0 = time.perf_counter()
     p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(planner="scale", n_groups=M,
-                                                                               trials=256)
+                                                                               trials=1024)
     plan_s = time.perf_counter() - t0
     rep = p.plan_report or {}
     fixed, _ = pb.build_candidate_set(n, CFG2["open"], M, pb.split_next(1, 0xCA11D))

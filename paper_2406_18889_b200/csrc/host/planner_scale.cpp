@@ -937,7 +937,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
             pool.emplace_back([&, i] {
                 Result& r = best_of[i];
                 if (r.trial < 0) return;
-                if (i < 8 && r.n_sliced > 0) {  // the best few also try slice-and-reconfigure
+                if (i < 16 && r.n_sliced > 0) {  // the best few also try slice-and-reconfigure
                     Result alt = r;
                     try {
                         slice_and_reconfigure(pb, alt.tree, alt.sliced, alt.n_sliced);
