@@ -391,3 +391,38 @@ def test_headline_bench_configuration_pinned(ref):
                 for prec in ("f64", "tf32", "f16"):
                     got = p.contract_groups(fixed[g:g + 1], precision=prec, configs=None, slices=(s, s + 1))[0]
                     assert rel(got, want[j]) < TOL[prec], (g, s, prec, rel(got, want[j]))
+
+
+# ---- the scale planner's plans on both executors -------------------------------
+def test_scale_planner_plan_on_reference_executor(ref):
+    """A 54-qubit grid(6,9) m = 10 circuit planned by the scale planner (the
+    reference planner's uint64 costs overflow at this size), imported
+    into the reference executor (refo_set_plan): GPU amplitudes of (group, slice)
+    pairs equal the reference's execute_assignment of the same plan."""
+    spec = (54, 10, "grid(6,9)", 1, list(range(6)), 1 << 27, "low")
+    p = pb.Problem(*spec).build(planner="scale", n_groups=1, trials=64)
+    assert len(p.plan["sliced"]) >= 1
+    r = ref.RefProblem(54, 10, "grid(6,9)", 1, list(range(6)), 1 << 62, "low").build()
+    assert r.net["n_labels"] == p.net["n_labels"] and r.net["label_names"] == p.net["label_names"]
+    r.set_plan(p.plan["steps"], p.plan["sliced"])
+    fixed, _ = pb.build_candidate_set(54, list(range(6)), 4, pb.split_next(1, 0xCA11D))
+    for g, s in ((0, 0), (3, p.n_slices - 1)):
+        want = r.execute_gsc(int(fixed[g]), s)
+        for prec in ("f64", "tf32", "f16"):
+            got = p.contract_groups(fixed[g:g + 1], precision=prec, configs=None, slices=(s, s + 1))[0]
+            assert rel(got, want) < TOL[prec], (g, s, prec, rel(got, want))
+
+
+@pytest.mark.parametrize("precision", ["f64", "tf32"])
+def test_scale_planner_sycamore_matches_oracle(precision):
+    """Sycamore-53 m = 8 planned by the scale planner for a 16-group batch: GPU
+    group amplitudes over two slices equal the C restatement's execution of the
+    same plan."""
+    p = pb.Problem(53, 8, "sycamore53", 1, list(range(6)), 1 << 26, "low").build(planner="scale", n_groups=16,
+                                                                               trials=64)
+    pn = port.PortNet(p.net, p.plan)
+    fixed, _ = pb.build_candidate_set(53, list(range(6)), 16, pb.split_next(1, 0xCA11D))
+    got = p.contract_groups(fixed, precision=precision, configs=None, slices=(0, 2))
+    for g in (0, 7, 15):
+        want = pn.contract_group(int(fixed[g]), slices=(0, 2))
+        assert rel(got[g], want) < TOL[precision], (g, rel(got[g], want))
