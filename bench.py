@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-xeb", action="store_true")
     ap.add_argument("--no-post", action="store_true")
-    ap.add_argument("--scale-configs", default="cfg3,cfg4",
+    ap.add_argument("--scale-configs", default="cfg3,cfg4,cfg5",
                     help="BASELINE configs 3-5 measured per slice with the scale planner (comma list, or none)")
     ap.add_argument("--cfg4-slices", type=int, default=1024, help="cfg4 fixed slice subset (BASELINE: 2^10)")
     ap.add_argument("--ref-pairs", type=int, default=0,
@@ -367,7 +367,8 @@ SCALE_CFGS = {"cfg3": (53, 12, "sycamore53", "Sycamore-53 layout, m=12"),
               "cfg5": (60, 24, "zuchongzhi60", "Zuchongzhi-style 60 qubits, m=24")}
 
 
-def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, alt_slices=64):
+def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, alt_slices=64, trials=1024,
+                compare=False):
     """BASELINE configs 3-5 per slice: the scale planner (log-domain, batch-aware,
     stem-aware slicing; widest tensor 2^30 amplitudes incl. group variants at a
     2^36 B budget) plans the circuit for M = 64 groups; a fixed subset of the
@@ -379,7 +380,7 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
     n, m, topo, desc = SCALE_CFGS[name]
     t0 = time.perf_counter()
     p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(planner="scale", n_groups=M,
-                                                                               trials=1024)
+                                                                               trials=trials)
     plan_s = time.perf_counter() - t0
     rep = p.plan_report or {}
     fixed, _ = pb.build_candidate_set(n, CFG2["open"], M, pb.split_next(1, 0xCA11D))
@@ -397,7 +398,7 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
         stream = torch.cuda.ExternalStream(p.stream(prec))
         S = 8
         t1 = time.perf_counter()
-        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, S))  # warm-up
+        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1))  # warm-up
         torch.cuda.synchronize()
         warm_s = time.perf_counter() - t1
         st = rcsg_stats()
@@ -434,6 +435,15 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
             "full_run_extrapolated_s_1gpu": p.n_slices / rate,
             "arena_gib": st.arena_bytes / 2 ** 30, "amps_finite": bool(torch.isfinite(acc).all().item())}
         del acc
+    if compare and alt:
+        # fp16-complex tensor-core mode against the fp32-storage (tf32) mode on the same two slices
+        a = p.contract_groups(fixed, precision=precision, configs=None, slices=(0, 2))
+        b = p.contract_groups(fixed, precision=alt, configs=None, slices=(0, 2))
+        import numpy as np
+        errs = np.linalg.norm(b - a, axis=1) / np.maximum(np.linalg.norm(a, axis=1), 1e-300)
+        out[f"{alt}_vs_{precision}"] = {"slices": [0, 2], "groups": M, "max_norm_rel": float(errs.max()),
+                                        "median_norm_rel": float(np.median(errs)),
+                                        "tolerance": 1e-2}
     return out
 
 
@@ -593,9 +603,13 @@ def main():
     if rank == 0 and world == 1 and args.scale_configs != "none":
         for name in [c for c in args.scale_configs.split(",") if c]:
             try:
-                ns = args.cfg4_slices if name == "cfg4" else 64
-                scale[name] = scale_bench(pb, name, args.precision, ns,
-                                          alt=args.alt_precision if args.alt_precision != "none" else None)
+                alt = args.alt_precision if args.alt_precision != "none" else None
+                if name == "cfg5":  # 60 qubits, 24 cycles: width 2^32 at a 2^38 B budget, 8 slices per mode
+                    scale[name] = scale_bench(pb, name, args.precision, 8, budget_log2=38, alt=alt, alt_slices=8,
+                                              trials=256, compare=True)
+                else:
+                    ns = args.cfg4_slices if name == "cfg4" else 64
+                    scale[name] = scale_bench(pb, name, args.precision, ns, alt=alt)
             except Exception as e:  # pragma: no cover
                 scale[name] = {"error": str(e)}
 

@@ -89,6 +89,11 @@ struct rcsg_program {
     std::unique_ptr<Program> prog;
     int n_broken = 0;
     int n_sliced = 0;
+    double* d_out = nullptr;  // device accumulator of rcsg_contract_groups, reused across calls
+    size_t out_cap = 0;
+    ~rcsg_program() {
+        if (d_out) cudaFree(d_out);
+    }
 };
 
 extern "C" {
@@ -193,9 +198,17 @@ int rcsg_contract_groups(rcsg_program* prog, uint64_t n_groups, const uint64_t* 
     return guard([&] {
         if (!prog) throw Failure{RCSG_ERR_CONFIG, "null program"};
         const size_t n = static_cast<size_t>(n_groups) << prog->prog->out_rank();
-        double* d = nullptr;
-        check_cuda(cudaMalloc(&d, std::max<size_t>(n, 1) * 2 * sizeof(double)), "cudaMalloc");
-        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        if (prog->out_cap < std::max<size_t>(n, 1)) {  // grow-only; the program's stream orders its reuse
+            if (prog->d_out) {
+                check_cuda(cudaStreamSynchronize(prog->prog->stream()), "cudaStreamSynchronize");
+                cudaFree(prog->d_out);
+                prog->d_out = nullptr;
+                prog->out_cap = 0;
+            }
+            check_cuda(cudaMalloc(&prog->d_out, std::max<size_t>(n, 1) * 2 * sizeof(double)), "cudaMalloc");
+            prog->out_cap = std::max<size_t>(n, 1);
+        }
+        double* d = prog->d_out;
         // zero on the program's (non-blocking) stream: the accumulation below is
         // ordered after it without a device-wide synchronisation
         check_cuda(cudaMemsetAsync(d, 0, n * 2 * sizeof(double), prog->prog->stream()), "cudaMemsetAsync");

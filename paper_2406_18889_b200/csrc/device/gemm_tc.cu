@@ -15,6 +15,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -72,6 +73,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+
+// The same wait with a suspend-time hint: the thread sleeps in the barrier
+// until the phase completes (or ~20 us pass) instead of re-issuing try_wait,
+// which frees issue slots for the other epilogue warps of the SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(20000)
         : "memory");
 }
 
@@ -852,18 +868,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 row_off = (static_cast<int64_t>(c.m0) >> p.om.m_bits) * out_row_vstride(p.om) +
                           warp_scatter(p.om.m_pos, p.om.m_bits, 7, c.m0, lane) + lane_off;
             else row_off = row < p.m ? out_row_off(p.om, p.n, row) : 0;
-            mbar_wait(&tfull[ab], (j / NBUF) & 1);
+            mbar_wait_sleep(&tfull[ab], (j / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            constexpr int CW = BN / 2 < 32 ? BN / 2 : 32;  // columns per chunk (16 when BN = 32)
-#pragma unroll 1
-            for (int plane = plane_lo; plane < plane_hi; ++plane)
-#pragma unroll 1
-            for (int c0 = col_lo; c0 < col_hi; c0 += CW) {
+            // one chunk = CW columns of one plane; BN = 32 tiles drained by a group of
+            // warps that owns all columns (NG >= 2) take the whole 32-column row at once
+            auto chunk = [&](auto cw_tag, int plane, int c0, int64_t col_base) {
+                constexpr int CW = decltype(cw_tag)::value;
                 const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
-                const int64_t col_base = p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, CW == 32 ? 5 : 4, col0, lane) +
-                                                            (col0 >> p.om.n_bits) * p.om.n_vstride
-                                                      : col0;
                 float x[CW];
                 if constexpr (CW == 32) tmem_ld32(base + c0, x);
                 else tmem_ld16(base + c0, x);
@@ -871,17 +883,36 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
                         bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
                                                          row < p.m ? row_off : 0, col_base);
-                        continue;
+                        return;
                     }
                 } else {
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
                         bad |= store_chunk_staged4<CW>(p, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
                                                        plane, tn_lo, lane, row < p.m ? row_off : 0, col_base);
-                        continue;
+                        return;
                     }
                 }
                 if (row < p.m)
                     bad |= store_chunk<E, CW>(p, c.split, c.v, row, col0, x, plane, tn_lo, row_off, col_base);
+            };
+            auto col_base_of = [&](int64_t col0, int cw_bits) {
+                // single column tile (nt == 1): the first chunk's offset is 0 for every tile (no warp reductions)
+                if (p.nt == 1 && col0 == 0) return int64_t{0};
+                return p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, cw_bits, col0, lane) +
+                                          (col0 >> p.om.n_bits) * p.om.n_vstride
+                                    : col0;
+            };
+            if (BN == 32 && NG != 1) {
+#pragma unroll 1
+                for (int plane = plane_lo; plane < plane_hi; ++plane)
+                    chunk(std::integral_constant<int, 32>{}, plane, 0, col_base_of(c.n0, 5));
+            } else {
+                constexpr int CWD = BN / 2 < 32 ? BN / 2 : 32;  // 16 when BN = 32 and NG = 1
+#pragma unroll 1
+                for (int plane = plane_lo; plane < plane_hi; ++plane)
+#pragma unroll 1
+                    for (int c0 = col_lo; c0 < col_hi; c0 += CWD)
+                        chunk(std::integral_constant<int, CWD>{}, plane, c0, col_base_of(c.n0 + c0, CWD == 32 ? 5 : 4));
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();

@@ -558,7 +558,10 @@ int partition_tree(const Problem& pb, const Reduced& rd, const std::vector<std::
 // ---------------------------------------------------------------- slicing
 // Adds sliced labels until the widest tensor fits; each pick is the label of a
 // widest tensor that minimises the total (sliced) cost.
-bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width);
+constexpr int kMaxIn = 8;       // inputs per reconfigured subtree (3^8 DP splits)
+constexpr int kMaxInDeep = 10;  // the winner's final polish (3^10)
+bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width,
+                      int max_in = kMaxIn);
 
 // One slicing step: the label of a widest tensor that minimises the total
 // (sliced) cost.  Returns false when the widest tensor already fits.
@@ -605,12 +608,12 @@ void slice_to_width(const Problem& pb, const Tree& t, LSet& sliced, int& n_slice
 // Slice-and-reconfigure from the unsliced tree: one label at a time, each
 // followed by a reconfiguration pass that may not widen the tree, so the tree
 // adapts to every cut before the next one is chosen.
-void slice_and_reconfigure(const Problem& pb, Tree& t, LSet& sliced, int& n_sliced) {
+void slice_and_reconfigure(const Problem& pb, Tree& t, LSet& sliced, int& n_sliced, int max_in) {
     sliced = LSet(pb.n_labels);
     n_sliced = 0;
     for (int guard = 0; guard < pb.n_labels; ++guard) {
         const double w = evaluate(pb, t, sliced, n_sliced).max_size;
-        reconfigure_pass(pb, t, sliced, n_sliced, std::max(w, pb.width));
+        reconfigure_pass(pb, t, sliced, n_sliced, std::max(w, pb.width), max_in);
         if (!slice_one(pb, t, sliced, n_sliced)) return;
     }
     throw ConfigError("scale planner: slicing did not converge");
@@ -619,14 +622,13 @@ void slice_and_reconfigure(const Problem& pb, Tree& t, LSet& sliced, int& n_slic
 // ---------------------------------------------------------------- reconfiguration
 // Re-contracts the subtree at v, cut at up to kMaxIn inputs, optimally by DP
 // over input subsets.  Returns true if the subtree's cost dropped.
-constexpr int kMaxIn = 8;
 
 bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_sliced, std::vector<int>& free_ids,
-                    double width) {
+                    double width, int max_in) {
     if (t.l[v] < 0) return false;
     // frontier: expand the widest internal node until kMaxIn inputs
     std::vector<int> in{t.l[v], t.r[v]}, inner{v};
-    while (static_cast<int>(in.size()) < kMaxIn) {
+    while (static_cast<int>(in.size()) < max_in) {
         int pick = -1;
         double ps = -1;
         for (std::size_t i = 0; i < in.size(); ++i) {
@@ -727,14 +729,14 @@ bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_slic
 
 // One pass over every internal node, costliest steps first (internal ids are
 // arbitrary here; emit() numbers the steps in post-order).
-bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width) {
+bool reconfigure_pass(const Problem& pb, Tree& t, const LSet& sliced, int n_sliced, double width, int max_in) {
     bool any = false;
     Eval e = evaluate(pb, t, sliced, n_sliced);
     std::vector<int> order = post_order(t);
     std::sort(order.begin(), order.end(), [&](int a, int b) { return e.cost[a] > e.cost[b]; });
     std::vector<int> free_ids;
     for (int v : order) {
-        if (reconfigure_at(pb, t, e, v, n_sliced, free_ids, width < 0 ? pb.width : width)) {
+        if (reconfigure_at(pb, t, e, v, n_sliced, free_ids, width < 0 ? pb.width : width, max_in)) {
             any = true;
             e = evaluate(pb, t, sliced, n_sliced);  // the subtree's node ids now hold new contractions
         }
@@ -940,7 +942,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
                 if (i < 16 && r.n_sliced > 0) {  // the best few also try slice-and-reconfigure
                     Result alt = r;
                     try {
-                        slice_and_reconfigure(pb, alt.tree, alt.sliced, alt.n_sliced);
+                        slice_and_reconfigure(pb, alt.tree, alt.sliced, alt.n_sliced, kMaxIn);
                         alt.total = evaluate(pb, alt.tree, alt.sliced, alt.n_sliced).total;
                         if (alt.total < r.total) r = std::move(alt);
                     } catch (const ConfigError&) {
@@ -982,6 +984,26 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
     Result best = phase(LSet(pb.n_labels), 0, 0);
     if (!(best.total < std::numeric_limits<double>::infinity()))
         throw ConfigError("scale planner: no trial fits the memory budget");
+    // final polish of the winner: deeper subtrees (10 inputs), then drop unneeded slices
+    for (int round = 0; round < 4; ++round) {
+        bool changed = false;
+        for (int pass = 0; pass < 4 && reconfigure_pass(pb, best.tree, best.sliced, best.n_sliced, -1, kMaxInDeep);
+             ++pass)
+            changed = true;
+        std::vector<int> sl;
+        best.sliced.each([&](int l) { sl.push_back(l); });
+        for (int l : sl) {
+            LSet trial = best.sliced;
+            trial.reset(l);
+            if (evaluate(pb, best.tree, trial, best.n_sliced - 1).max_size <= pb.width + 1e-9) {
+                best.sliced = trial;
+                --best.n_sliced;
+                changed = true;
+            }
+        }
+        if (!changed) break;
+    }
+    best.total = evaluate(pb, best.tree, best.sliced, best.n_sliced).total;
     // phase 2 (sliced plans): search again on the network with the phase-1 slice set cut
     if (best.n_sliced > 0 && opt.phases > 1) {
         Result second = phase(best.sliced, best.n_sliced, 1);
