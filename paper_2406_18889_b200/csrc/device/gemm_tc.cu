@@ -439,11 +439,12 @@ __device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v
     return bad;
 }
 
-template <int BN, int STAGES, int RB = 128>
+template <int BN, int STAGES, int RB = 128, int NPL = 2>
 struct Smem {
     static constexpr int kATile = kBM * RB;  // bytes per A plane tile (RB-byte rows)
     static constexpr int kBTile = BN * RB;
-    static constexpr int kStage = 2 * kATile + 2 * kBTile;
+    // NPL planes per operand: {Ar, Ai, Br, Bi} (4M), {Ar, Ai, Ar+Ai, Br, Bi, Br+Bi} (3M)
+    static constexpr int kStage = NPL * kATile + NPL * kBTile;
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
     // persistent kernel: + staged-epilogue buffers of the 8 epilogue warps (2-byte E)
     template <typename E>
@@ -725,16 +726,31 @@ struct TileIter {
     }
 };
 
-template <int BN, int STAGES, typename E, int RB>
+// THREE (3M complex product): T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi), then
+// Re = T1 - T2, Im = T3 - T1 - T2 in the epilogue - three real MMAs per K slice
+// instead of four, with the operand sum planes staged by the host-side pre-pass.
+template <bool THREE>
+constexpr uint32_t tc_nbuf(int bn) {
+    return (512 / ((THREE ? 3 : 2) * bn)) < 4 ? (512 / ((THREE ? 3 : 2) * bn)) : 4;
+}
+constexpr uint32_t pow2_ceil(uint32_t x) {
+    uint32_t r = 32;
+    while (r < x) r <<= 1;
+    return r;
+}
+
+template <int BN, int STAGES, typename E, int RB, bool THREE = false>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
+                       const __grid_constant__ CUtensorMap map_as, const __grid_constant__ CUtensorMap map_bs,
                        const TcParams p, int64_t total_tiles) {
-    using S = Smem<BN, STAGES, RB>;
-    // TMEM accumulator buffers {Re, Im}: as many as fit in 512 columns (max 4),
-    // so the MMA runs ahead of the epilogue by NBUF - 1 tiles
-    constexpr uint32_t NBUF = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
-    constexpr uint32_t kCols = NBUF * 2 * BN;
+    constexpr int NPL = THREE ? 3 : 2;
+    using S = Smem<BN, STAGES, RB, NPL>;
+    // TMEM accumulator buffers ({Re, Im}, or {T1, T2, T3} for 3M): as many as fit in
+    // 512 columns (max 4), so the MMA runs ahead of the epilogue by NBUF - 1 tiles
+    constexpr uint32_t NBUF = tc_nbuf<THREE>(BN);
+    constexpr uint32_t kCols = pow2_ceil(NBUF * NPL * BN);
     // epilogue groups = tiles in flight (NBUF % NG == 0), chosen by the host (p.ng: 1, 2 or 4)
     const int NG = p.ng;
     extern __shared__ uint8_t smem_raw[];
@@ -750,7 +766,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     __shared__ int64_t tn_lo[32];
     if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
     if (threadIdx.x == 32) {  // fetch the TMA descriptors while the CTA sets up
-        for (const CUtensorMap* m : {&map_ar, &map_ai, &map_br, &map_bi})
+        for (const CUtensorMap* m : {&map_ar, &map_ai, &map_br, &map_bi, &map_as, &map_bs})
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     }
 
@@ -793,13 +809,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     // B resident: the same single B tile for every tile (one N tile, one
                     // K block, unbatched B) is loaded once into each stage slot
                     const bool load_b = !(p.b_resident && it >= STAGES);
-                    mbar_expect_tx(&full[s], load_b ? S::kStage : 2 * S::kATile);
+                    mbar_expect_tx(&full[s], load_b ? S::kStage : NPL * S::kATile);
                     const int kc = static_cast<int>(c.k_begin) + kb * kbk<E, RB>;
                     tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
                     tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
+                    if constexpr (THREE) tma_load_3d(st + 2 * S::kATile, &map_as, &full[s], kc, c.m0, av);
                     if (load_b) {
-                        tma_load_3d(st + 2 * S::kATile, &map_br, &full[s], kc, c.n0, bv);
-                        tma_load_3d(st + 2 * S::kATile + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                        uint8_t* sb = st + NPL * S::kATile;
+                        tma_load_3d(sb, &map_br, &full[s], kc, c.n0, bv);
+                        tma_load_3d(sb + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                        if constexpr (THREE) tma_load_3d(sb + 2 * S::kBTile, &map_bs, &full[s], kc, c.n0, bv);
                     }
                 }
             }
@@ -815,22 +834,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t t_re = tmem + ab * 2 * BN, t_im = t_re + BN;
+                const uint32_t t_re = tmem + ab * NPL * BN, t_im = t_re + BN;  // 3M: T1, T2 (, T3 = t_re + 2 BN)
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint8_t* st = smem + s * S::kStage;
+                    const uint8_t* sb = st + NPL * S::kATile;
                     const uint64_t dar = smem_desc<RB>(st), dai = smem_desc<RB>(st + S::kATile);
-                    const uint64_t dbr = smem_desc<RB>(st + 2 * S::kATile), dbi = smem_desc<RB>(st + 2 * S::kATile + S::kBTile);
+                    const uint64_t dbr = smem_desc<RB>(sb), dbi = smem_desc<RB>(sb + S::kBTile);
 #pragma unroll
                     for (int jj = 0; jj < RB / 32; ++jj) {  // 32-B K slices (one MMA K each)
                         const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
                         const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
-                        mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
-                        mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
-                        mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
-                        mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
+                        if constexpr (THREE) {
+                            const uint64_t das = smem_desc<RB>(st + 2 * S::kATile), dbs = smem_desc<RB>(sb + 2 * S::kBTile);
+                            mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);           // T1 = Ar Br
+                            mma_e<E>(t_im, dai + o, dbi + o, id_pos, acc);           // T2 = Ai Bi
+                            mma_e<E>(t_re + 2 * BN, das + o, dbs + o, id_pos, acc);  // T3 = As Bs
+                        } else {
+                            mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                            mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                            mma_e<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                            mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
+                        }
                     }
                     mma_commit(&empty[s]);
                 }
@@ -874,11 +901,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // warps that owns all columns (NG >= 2) take the whole 32-column row at once
             auto chunk = [&](auto cw_tag, int plane, int c0, int64_t col_base) {
                 constexpr int CW = decltype(cw_tag)::value;
-                const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * 2 * BN + plane * BN;
+                const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * NPL * BN + c0;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 float x[CW];
-                if constexpr (CW == 32) tmem_ld32(base + c0, x);
-                else tmem_ld16(base + c0, x);
+                auto ld = [&](uint32_t addr, float* v) {
+                    if constexpr (CW == 32) tmem_ld32(addr, v);
+                    else tmem_ld16(addr, v);
+                };
+                if constexpr (THREE) {  // Re = T1 - T2, Im = T3 - T1 - T2
+                    float y[CW];
+                    ld(lanes + (plane == 0 ? 0 : 2 * BN), x);
+                    ld(lanes + (plane == 0 ? BN : 0), y);
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) x[i] -= y[i];
+                    if (plane == 1) {
+                        ld(lanes + BN, y);
+#pragma unroll
+                        for (int i = 0; i < CW; ++i) x[i] -= y[i];
+                    }
+                } else {
+                    ld(lanes + plane * BN, x);
+                }
                 if constexpr (sizeof(E) == 2) {
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
                         bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
@@ -991,9 +1034,9 @@ int epilogue_kind4(const OutMap& om, int64_t n) {
     return 0;
 }
 
-template <int BN, int STAGES, typename E, int RB = 128>
-void launch(const GemmArgs& g, cudaStream_t st) {
-    using S = Smem<BN, STAGES, RB>;
+template <int BN, int STAGES, typename E, int RB = 128, bool THREE = false>
+void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, const void* b_sum = nullptr) {
+    using S = Smem<BN, STAGES, RB, THREE ? 3 : 2>;
     static std::atomic<uint64_t> configured{0};  // function attributes are per device
     if (first_on_device(configured))
         cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1007,6 +1050,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     const CUtensorMap ai = make_map<E, RB>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
     const CUtensorMap br = make_map<E, RB>(b, g.k, g.n, b_batches, BN);
     const CUtensorMap bi = make_map<E, RB>(b + g.b_plane, g.k, g.n, b_batches, BN);
+    const CUtensorMap as = THREE ? make_map<E, RB>(static_cast<const E*>(a_sum), g.k, a_rows, a_batches, kBM) : ar;
+    const CUtensorMap bs = THREE ? make_map<E, RB>(static_cast<const E*>(b_sum), g.k, g.n, b_batches, BN) : br;
     TcParams p{};
     p.m = g.m;
     p.n = g.n;
@@ -1047,7 +1092,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     {
         // two tiles in flight help short (memory-bound) tiles and cost nothing on long K
         // (measured); four help BN = 32.  NBUF must be a multiple of the group count.
-        constexpr int nbuf = (512 / (2 * BN)) < 4 ? (512 / (2 * BN)) : 4;
+        constexpr int nbuf = static_cast<int>(tc_nbuf<THREE>(BN));
         int ng = (BN == 32 && nbuf >= 4) ? 4 : 2;
         if (const char* e = getenv("RCSG_TC_NG")) ng = atoi(e);
         if (ng != 1 && ng != 2 && ng != 4) ng = 1;
@@ -1080,17 +1125,17 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     // the epilogue overlaps the next tile's MMAs) for every shape: on long K it
     // measured ~1.9x the one-CTA-per-tile kernel (RCSG_TC_MODE=2 selects that one)
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
-    const bool persistent = mode != 2 || RB != 128;  // narrow-K tiles: persistent only
+    const bool persistent = THREE || mode != 2 || RB != 128;  // narrow-K tiles and 3M: persistent only
     if (persistent) {
         static std::atomic<uint64_t> pconf{0};
         if (first_on_device(pconf))
-            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 S::template kPBytes<E>);
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB, THREE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, S::template kPBytes<E>);
         const int64_t total = tiles * splits;
         if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
         const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-        launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB>, dim3(grid), dim3(kPThreads), S::template kPBytes<E>, st, ar, ai,
-                   br, bi, p, total);
+        launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, THREE>, dim3(grid), dim3(kPThreads), S::template kPBytes<E>,
+                   st, ar, ai, br, bi, as, bs, p, total);
     } else {
         launch_pdl(gemm_tc_kernel<BN, STAGES, E>, dim3(static_cast<unsigned>(tiles * splits)), dim3(kThreads),
                    Smem<BN, STAGES>::kBytes, st, ar, ai, br, bi, p);
@@ -1113,8 +1158,62 @@ bool gemm_tc_supported(const GemmArgs& g) {
 // Narrow K uses 32-B / 64-B stage rows (fewer zero-filled K columns, deeper
 // stage rings) and n <= 32 the BN = 32 tiles, for every element type;
 // RCSG_TC_NARROW_K=0 / RCSG_TC_NARROW_N=0 disable them
+// Re + Im of a plane pair, into `out` (3M operand sum planes), 16-B vectors
+template <typename E>
+__global__ void plane_sum_kernel(const E* __restrict__ re, const E* __restrict__ im, E* __restrict__ out, int64_t n) {
+    pdl_enter();
+    constexpr int V = 16 / static_cast<int>(sizeof(E));
+    const int64_t nv = n / V;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+        const uint4 a = reinterpret_cast<const uint4*>(re)[i], b = reinterpret_cast<const uint4*>(im)[i];
+        uint4 o;
+        const E* pa = reinterpret_cast<const E*>(&a);
+        const E* pb = reinterpret_cast<const E*>(&b);
+        E* po = reinterpret_cast<E*>(&o);
+#pragma unroll
+        for (int j = 0; j < V; ++j) store_c(po + j, load_c(pa + j) + load_c(pb + j));
+        reinterpret_cast<uint4*>(out)[i] = o;
+    }
+    for (int64_t i = nv * V + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        store_c(out + i, load_c(re + i) + load_c(im + i));
+}
+
+// 3M for large unbatched GEMMs (opt-in, RCSG_TC_3M=1): the sum planes cost one
+// extra pass over each operand and the MMAs drop by a quarter, but each stage
+// streams six operand planes for three MMAs instead of four for four, so the
+// kernel turns L2/HBM-bound: measured 1.2-2x SLOWER than 4M on every long-K
+// shape of the plans (profiles/r02/gemm_3m.log).  Kept for kernels that share
+// operand tiles across CTAs (multicast / 2-CTA), where the ratio flips.
+template <typename E>
+bool launch_3m(const GemmArgs& g, cudaStream_t st) {
+    const char* env = getenv("RCSG_TC_3M");
+    const bool on = env && atoi(env) != 0;
+    const double flops = 8.0 * static_cast<double>(g.m) * g.n * g.k;
+    if (!on || g.batch > 1 || g.ia || g.ib || g.k < 512 || g.n < 64 || flops < 2.7e11) return false;
+    const int64_t a_el = g.a_plane, b_el = g.b_plane;
+    const int64_t a_pad = (a_el + 127) / 128 * 128;  // keep the B sum plane 256-B aligned
+    E* sums = static_cast<E*>(device_workspace(static_cast<size_t>(a_pad + b_el) * sizeof(E), st, 1));
+    E* as = sums;
+    E* bs = sums + a_pad;
+    const E* a = static_cast<const E*>(g.a);
+    const E* b = static_cast<const E*>(g.b);
+    auto grid_of = [](int64_t n) {
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / (16 / sizeof(E)) + 255) / 256, 148 * 8)));
+    };
+    launch_pdl(plane_sum_kernel<E>, dim3(grid_of(a_el)), dim3(256), 0, st, a, a + g.a_plane, as, a_el);
+    launch_pdl(plane_sum_kernel<E>, dim3(grid_of(b_el)), dim3(256), 0, st, b, b + g.b_plane, bs, b_el);
+    if (g.n >= 128) {  // 2 stages of 6 x 16 KB (RB = 128) measured best of the 3M tilings
+        launch<128, 2, E, 128, true>(g, st, as, bs);
+    } else {
+        launch<64, 5, E, 64, true>(g, st, as, bs);
+    }
+    return true;
+}
+
 template <typename E>
 void launch_typed(const GemmArgs& g, cudaStream_t st) {
+    if (launch_3m<E>(g, st)) return;
     static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
     static const bool narrow_n = getenv("RCSG_TC_NARROW_N") == nullptr || atoi(getenv("RCSG_TC_NARROW_N")) != 0;
     const int64_t kb = g.k * static_cast<int64_t>(sizeof(E));  // bytes of K per row

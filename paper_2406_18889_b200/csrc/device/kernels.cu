@@ -298,8 +298,8 @@ void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, v
 }
 
 namespace {
-std::map<cudaStream_t, std::pair<void*, size_t>>& workspace_pool() {
-    static std::map<cudaStream_t, std::pair<void*, size_t>> pool;
+std::map<std::pair<cudaStream_t, int>, std::pair<void*, size_t>>& workspace_pool() {
+    static std::map<std::pair<cudaStream_t, int>, std::pair<void*, size_t>> pool;
     return pool;
 }
 std::mutex& workspace_mu() {
@@ -308,11 +308,11 @@ std::mutex& workspace_mu() {
 }
 }  // namespace
 
-void* device_workspace(size_t bytes, cudaStream_t st) {
-    // one growing scratch buffer per stream (launches on a stream are ordered);
-    // Program's destructor releases the entries of its streams
+void* device_workspace(size_t bytes, cudaStream_t st, int slot) {
+    // one growing scratch buffer per (stream, slot) (launches on a stream are
+    // ordered); Program's destructor releases the entries of its streams
     std::lock_guard<std::mutex> lock(workspace_mu());
-    auto& e = workspace_pool()[st];
+    auto& e = workspace_pool()[{st, slot}];
     if (bytes > e.second) {
         if (e.first) {
             cudaStreamSynchronize(st);
@@ -328,13 +328,19 @@ void* device_workspace(size_t bytes, cudaStream_t st) {
 void release_workspace(cudaStream_t st) {
     std::lock_guard<std::mutex> lock(workspace_mu());
     auto& pool = workspace_pool();
-    auto it = pool.find(st);
-    if (it == pool.end()) return;
-    if (it->second.first) {
-        cudaStreamSynchronize(st);
-        cudaFree(it->second.first);
+    bool synced = false;
+    for (auto it = pool.begin(); it != pool.end();) {
+        if (it->first.first != st) {
+            ++it;
+            continue;
+        }
+        if (it->second.first) {
+            if (!synced) cudaStreamSynchronize(st);
+            synced = true;
+            cudaFree(it->second.first);
+        }
+        it = pool.erase(it);
     }
-    pool.erase(it);
 }
 
 bool first_on_device(std::atomic<uint64_t>& done) {

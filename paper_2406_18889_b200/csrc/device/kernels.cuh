@@ -225,8 +225,9 @@ struct TableJob {
 void launch_table_io(const TableJob* jobs, int n_jobs, const PassState* state, void* arena, int elem_bytes,
                      int to_table, cudaStream_t st);
 
-// Scratch buffer for split-K partials, one per stream (grown on demand).
-void* device_workspace(size_t bytes, cudaStream_t st);
+// Scratch buffer per (stream, slot), grown on demand: slot 0 split-K partials,
+// slot 1 the operand sum planes of 3M tensor-core GEMMs.
+void* device_workspace(size_t bytes, cudaStream_t st, int slot = 0);
 // Frees the scratch buffer of a stream that is about to be destroyed.
 void release_workspace(cudaStream_t st);
 

@@ -25,12 +25,17 @@ CASES = [
     ("narrow-n8", 1 << 12, 8, 64, [], []),
     ("narrow-k8-n32", 1 << 15, 32, 8, [], []),
     ("col-run2", 1 << 13, 64, 128, list(range(2, 15)), [0, 1, 15, 16, 17, 18]),
+    # 8 m n k >= 2.7e11, k >= 512, n >= 64: the 3M path (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi))
+    ("3m-n1024", 4096, 1024, 8192, [], []),
+    ("3m-n64-scatter", 1 << 14, 64, 32768, [7, 8, 9, 10, 11, 12, 13] + list(range(0, 7)), list(range(14, 20))),
 ]
 
 
 @pytest.mark.parametrize("dtype,tol", [("f16", 2e-3), ("bf16", 1.6e-2), ("tf32", 5e-3)])
 @pytest.mark.parametrize("name,m,n,k,mp,npos", CASES, ids=[c[0] for c in CASES])
-def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol):
+def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol, monkeypatch):
+    if name.startswith("3m"):
+        monkeypatch.setenv("RCSG_TC_3M", "1")  # the opt-in 3M kernel
     lib = _native.testkit()
     check = {"f16": lib.rcsg_gemm_check_f16, "bf16": lib.rcsg_gemm_check_bf16, "tf32": lib.rcsg_gemm_check_tf32}[dtype]
     a = (C.c_int8 * max(len(mp), 1))(*mp)
