@@ -435,10 +435,13 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
             "full_run_extrapolated_s_1gpu": p.n_slices / rate,
             "arena_gib": st.arena_bytes / 2 ** 30, "amps_finite": bool(torch.isfinite(acc).all().item())}
         del acc
+        p.release()  # one mode's arena at a time (cfg5's is ~80 GiB at tf32)
     if compare and alt:
         # fp16-complex tensor-core mode against the fp32-storage (tf32) mode on the same two slices
         a = p.contract_groups(fixed, precision=precision, configs=None, slices=(0, 2))
+        p.release()
         b = p.contract_groups(fixed, precision=alt, configs=None, slices=(0, 2))
+        p.release()
         import numpy as np
         errs = np.linalg.norm(b - a, axis=1) / np.maximum(np.linalg.norm(a, axis=1), 1e-300)
         out[f"{alt}_vs_{precision}"] = {"slices": [0, 2], "groups": M, "max_norm_rel": float(errs.max()),

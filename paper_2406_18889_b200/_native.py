@@ -76,7 +76,7 @@ RCSH_SYMBOLS = [
     "rcsh_execute", "rcsh_candidates", "rcsh_topk", "rcsh_direct", "rcsh_member",
     "rcsh_rng_split_next", "rcsh_lexkey", "rcsh_broken_configs", "rcsh_set_profile",
     "rcsh_program_stream", "rcsh_program_sync", "rcsh_statevector", "rcsh_build_ex", "rcsh_plan_import",
-    "rcsh_state_fidelity", "rcsh_predicted_topk_xeb",
+    "rcsh_state_fidelity", "rcsh_predicted_topk_xeb", "rcsh_release_programs",
 ]
 
 _lib = None
@@ -111,6 +111,7 @@ def lib():
         L.rcsh_last_error.restype = C.c_char_p
         L.rcsh_free.restype = None
         L.rcsh_set_profile.restype = None
+        L.rcsh_release_programs.restype = None
         L.rcsh_net_sizes.restype = None
         L.rcsh_net_export.restype = None
         L.rcsh_wire_edges.restype = None

@@ -245,6 +245,10 @@ class Problem:
                                                    C.byref(out)))
         return out.value or 0
 
+    def release(self):
+        """Free the compiled device programs (and their arenas) of this problem."""
+        _native.lib().rcsh_release_programs(self.handle)
+
     def set_profile(self, on: bool):
         """Per-kernel-class CUDA-event timing into rcsg_stats (gemm_ms, permute_ms, ...)."""
         _native.lib().rcsh_set_profile(self.handle, 1 if on else 0)

@@ -223,6 +223,13 @@ void rcsh_free(void* h) { delete static_cast<Handle*>(h); }
 
 void rcsh_set_profile(void* h, int on) { static_cast<Handle*>(h)->profile = on != 0; }
 
+// Frees the handle's compiled programs (their device arenas); the next call compiles again.
+void rcsh_release_programs(void* hp) {
+    Handle* h = static_cast<Handle*>(hp);
+    for (auto& [k, p] : h->programs) rcsg_program_free(p);
+    h->programs.clear();
+}
+
 // Stream of the handle's compiled program for (precision, budget); compiles it if needed.
 int rcsh_program_stream(void* hp, int precision, std::uint64_t budget, void** out) {
     return guarded([&] {

@@ -16,7 +16,7 @@ NS = int(os.environ.get("SLICES", "16"))
 blog = int(os.environ.get("BUDGET_LOG2", "36"))
 t0 = time.time()
 p = pb.Problem(n, m, topo, 1, list(range(6)), 1 << blog, "low").build(planner="scale", n_groups=M,
-                                                                     trials=int(os.environ.get("TRIALS", "256")))
+                                                                     trials=int(os.environ.get("TRIALS", "1024")))
 plan_s = time.time() - t0
 print(json.dumps({"cfg": cfg, "plan_s": plan_s, "report": p.plan_report, "sliced": len(p.plan["sliced"]),
                   "flops_per_slice_plan": p.plan["flops_per_slice"]}), flush=True)
@@ -43,7 +43,7 @@ for prec in os.environ.get("PREC", "f16,tf32").split(","):
     ms = e0.elapsed_time(e1)
     p.set_profile(True)
     pst = rcsg_stats()
-    os.environ["RCSG_PROFILE_STEPS"] = "6"
+    os.environ["RCSG_PROFILE_STEPS"] = os.environ.get("TOPN", "6")
     p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1), stats=pst)
     os.environ.pop("RCSG_PROFILE_STEPS")
     p.set_profile(False)
@@ -55,3 +55,5 @@ for prec in os.environ.get("PREC", "f16,tf32").split(","):
                       "gemm_tc_share": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None,
                       "full_run_extrapolated_s": p.n_slices / rate,
                       "amps_finite": bool(torch.isfinite(acc).all().item())}), flush=True)
+    del acc
+    p.release()
