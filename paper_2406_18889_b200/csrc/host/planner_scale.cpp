@@ -113,11 +113,30 @@ struct Eval {
     std::vector<int> var;       // variant bits
     std::vector<double> cost;   // log2 of the step's FLOPs (8 per complex MAC); leaves: -inf
     std::vector<char> dep;      // subtree holds a sliced label (runs once per slice)
-    double total = 0;           // total FLOPs of all slices (linear)
+    double total = 0;           // total cost of all slices (FLOP-equivalents of step_cost, linear)
+    double flops = 0;           // total FLOPs of all slices
     double max_size = 0;        // max log2 size over nodes
 };
 
 double vbits(const Problem& pb, int outs) { return std::min<double>(pb.log_m, outs); }
+
+// Step cost in FLOP-equivalents, the executor's time model: max(FLOPs, ridge x
+// bytes), with the operands and the result read / written once at 8 B per
+// complex element (tf32 storage) - the tcgen05 GEMMs are tensor-bound above the
+// ridge and HBM-bound below it.  Off by default (FLOPs only): with every operand
+// charged at HBM rates (ridge 128, RCSG_PLAN_RIDGE=128) the search on Sycamore-53
+// m = 20 traded 3x more FLOPs for fewer narrow steps, more than the measured
+// efficiency gap can repay - most small intermediates stay in the 126 MB L2.
+double plan_ridge() {
+    static const double r = getenv("RCSG_PLAN_RIDGE") ? atof(getenv("RCSG_PLAN_RIDGE")) : 0.0;
+    return r;
+}
+double step_cost(double flops_log2, double sa, double sb, double sc) {
+    const double f = std::exp2(flops_log2);
+    const double r = plan_ridge();
+    if (r <= 0) return f;
+    return std::max(f, r * 8.0 * (std::exp2(sa) + std::exp2(sb) + std::exp2(sc)));
+}
 
 // post-order of internal nodes (children before parents)
 std::vector<int> post_order(const Tree& t) {
@@ -172,8 +191,11 @@ Eval evaluate(const Problem& pb, const Tree& t, const LSet& sliced, int n_sliced
         outs[v] = outs[a] + outs[b];
         e.var[v] = static_cast<int>(vbits(pb, outs[v]));
         e.dep[v] = e.dep[a] || e.dep[b];
-        e.cost[v] = uni + e.var[v] + 3.0;
+        const double fl = uni + e.var[v] + 3.0;
+        e.cost[v] = std::log2(step_cost(fl, e.labels[a].count() + e.var[a], e.labels[b].count() + e.var[b],
+                                        e.labels[v].count() + e.var[v]));
         e.total += std::exp2(e.cost[v]) * (e.dep[v] ? mult : 1.0);
+        e.flops += std::exp2(fl) * (e.dep[v] ? mult : 1.0);
         e.max_size = std::max(e.max_size, e.labels[v].count() + static_cast<double>(e.var[v]));
     }
     return e;
@@ -696,7 +718,9 @@ bool reconfigure_at(const Problem& pb, Tree& t, const Eval& e, int v, int n_slic
             if (best[A] == inf || best[Bm] == inf) continue;
             B4 u;
             for (int q = 0; q < 4; ++q) u[q] = L[A][q] | L[Bm][q];
-            const double c = best[A] + best[Bm] + std::exp2(pc(u) + var + 3.0) * w;
+            const double c = best[A] + best[Bm] +
+                             step_cost(pc(u) + var + 3.0, pc(L[A]) + vbits(pb, outs[A]), pc(L[Bm]) + vbits(pb, outs[Bm]),
+                                       size) * w;
             if (c < best[S]) {
                 best[S] = c;
                 split[S] = A;
@@ -1019,11 +1043,12 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
     ContractionPlan plan = emit(pb, win.tree, network, win.sliced, sliced, broken, fixed, memory_budget_bytes);
     if (report) {
         const Eval e = evaluate(pb, win.tree, win.sliced, win.n_sliced);
-        report->log2_total_flops = std::log2(e.total);
+        report->log2_total_flops = std::log2(e.flops);
         double per_slice = 0, once = 0;
         for (int v = pb.n_leaves; v < static_cast<int>(win.tree.l.size()); ++v) {
             if (win.tree.l[v] < 0) continue;
-            (e.dep[v] ? per_slice : once) += std::exp2(e.cost[v]);
+            const int a = win.tree.l[v], b = win.tree.r[v];
+            (e.dep[v] ? per_slice : once) += std::exp2(e.labels[a].union_count(e.labels[b]) + e.var[v] + 3.0);
         }
         report->log2_flops_per_slice_batched = std::log2(per_slice);
         report->log2_flops_once_batched = once > 0 ? std::log2(once) : -1;
