@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--scale-configs", default="cfg3,cfg4,cfg5",
                     help="BASELINE configs 3-5 measured per slice with the scale planner (comma list, or none)")
     ap.add_argument("--cfg4-slices", type=int, default=1024, help="cfg4 fixed slice subset (BASELINE: 2^10)")
+    ap.add_argument("--replan", action="store_true",
+                    help="cfg3-5: run the scale planner in this process instead of importing plans/<cfg>.json")
     ap.add_argument("--ref-pairs", type=int, default=0,
                     help="(group, slice) pairs the reference executor runs (default: one per host core, >= 16)")
     ap.add_argument("--ref-budget", type=int, default=CFG2["budget"],
@@ -368,7 +370,7 @@ SCALE_CFGS = {"cfg3": (53, 12, "sycamore53", "Sycamore-53 layout, m=12"),
 
 
 def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, alt_slices=64, trials=1024,
-                compare=False):
+                compare=False, replan=False):
     """BASELINE configs 3-5 per slice: the scale planner (log-domain, batch-aware,
     stem-aware slicing; widest tensor 2^30 amplitudes incl. group variants at a
     2^36 B budget) plans the circuit for M = 64 groups; a fixed subset of the
@@ -378,19 +380,29 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
     from paper_2406_18889_b200._native import rcsg_stats
     hbm_peak, bf16_peak, peak_kind = peaks()
     n, m, topo, desc = SCALE_CFGS[name]
+    plan_file = os.path.join(ROOT, "plans", f"{name}.json")
     t0 = time.perf_counter()
-    p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(planner="scale", n_groups=M,
-                                                                               trials=trials)
+    if os.path.exists(plan_file) and not replan:
+        # the committed plan file (plan.json; found offline by the same scale planner,
+        # tools/plan_search.py): the measured plan is the same on every box
+        meta = json.load(open(plan_file[:-5] + ".meta.json"))
+        p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(plan_json=open(plan_file).read())
+        rep, source = meta["report"], f"plans/{name}.json (scale planner, {meta['trials']} trials, " \
+                                      f"search seed {meta['seed']}; imported)"
+    else:
+        p = pb.Problem(n, m, topo, 1, CFG2["open"], 1 << budget_log2, "low").build(planner="scale", n_groups=M,
+                                                                                   trials=trials)
+        rep, source = p.plan_report or {}, f"scale planner, {trials} trials, planned in this run"
     plan_s = time.perf_counter() - t0
-    rep = p.plan_report or {}
     fixed, _ = pb.build_candidate_set(n, CFG2["open"], M, pb.split_next(1, 0xCA11D))
     out = {"workload": f"{name}: {desc}, seed 1, l=6 open={{0..5}}, M={M} groups, K=0; "
                        f"scale planner, budget 2^{budget_log2} B",
-           "plan": {"sliced_labels": len(p.plan["sliced"]), "n_slices_log2": len(p.plan["sliced"]),
+           "plan": {"source": source, "sliced_labels": len(p.plan["sliced"]), "n_slices_log2": len(p.plan["sliced"]),
                     "flops_per_slice_per_group": p.plan["flops_per_slice"],
                     "log2_total_flops_batched": rep.get("log2_total_flops"),
                     "log2_flops_per_slice_batched": rep.get("log2_flops_per_slice_batched"),
-                    "log2_widest_tensor": rep.get("log2_max_size"), "plan_s": plan_s}}
+                    "log2_widest_tensor": rep.get("log2_max_size"), "planner_s": rep.get("seconds"),
+                    "build_s": plan_s}}
     for prec, ns in ((precision, n_slices), (alt, alt_slices)):
         if not prec:
             continue
@@ -606,13 +618,13 @@ def main():
     if rank == 0 and world == 1 and args.scale_configs != "none":
         for name in [c for c in args.scale_configs.split(",") if c]:
             try:
-                alt = args.alt_precision if args.alt_precision != "none" else None
+                alt_p = args.alt_precision if args.alt_precision != "none" else None
                 if name == "cfg5":  # 60 qubits, 24 cycles: width 2^32 at a 2^38 B budget, 8 slices per mode
-                    scale[name] = scale_bench(pb, name, args.precision, 8, budget_log2=38, alt=alt, alt_slices=8,
-                                              trials=256, compare=True)
+                    scale[name] = scale_bench(pb, name, args.precision, 8, budget_log2=38, alt=alt_p, alt_slices=8,
+                                              trials=256, compare=True, replan=args.replan)
                 else:
                     ns = args.cfg4_slices if name == "cfg4" else 64
-                    scale[name] = scale_bench(pb, name, args.precision, ns, alt=alt)
+                    scale[name] = scale_bench(pb, name, args.precision, ns, alt=alt_p, replan=args.replan)
             except Exception as e:  # pragma: no cover
                 scale[name] = {"error": str(e)}
 

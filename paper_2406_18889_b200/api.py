@@ -133,11 +133,15 @@ class Problem:
     net: dict = field(default_factory=dict)
     plan: dict = field(default_factory=dict)
 
-    def build(self, planner: str | None = None, n_groups: int = 1, trials: int = 0, threads: int = 0):
+    def build(self, planner: str | None = None, n_groups: int = 1, trials: int = 0, threads: int = 0,
+              plan_json: str | None = None):
         """planner None: find_contraction_path as configured (Auto: the reference
         algorithm where it works, the scale planner where it overflows);
         "reference" / "scale" / "auto" select explicitly.  n_groups, trials and
-        threads tune the scale planner; its report lands in self.plan_report."""
+        threads tune the scale planner; its report lands in self.plan_report.
+        plan_json: skip planning and import this plan.json instead."""
+        if plan_json is not None:
+            planner = "none"
         h = C.c_void_p()
         op = _i32(self.open)
         if planner is None:
@@ -148,7 +152,7 @@ class Problem:
             self.plan_report = None
         else:
             rep = np.zeros(10, np.float64)
-            kind = {"reference": 0, "scale": 1, "auto": 2}[planner]
+            kind = {"reference": 0, "scale": 1, "auto": 2, "none": 3}[planner]
             _check_h(_native.lib().rcsh_build_ex(self.n, self.cycles, self.topology.encode(),
                                                  C.c_uint64(self.seed), _p(op, C.c_int), len(self.open),
                                                  C.c_uint64(self.budget), EFFORT[self.effort], self.k_broken,
@@ -159,6 +163,8 @@ class Problem:
                     "reduced_tensors"]
             self.plan_report = dict(zip(keys, rep.tolist())) if rep[0] != -1.0 else None
         self.handle = h
+        if plan_json is not None:
+            return self.import_plan(plan_json)
         self._export()
         return self
 

@@ -708,6 +708,7 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
         };
         ch.ia_off.assign(steps_.size(), -1);
         ch.ib_off.assign(steps_.size(), -1);
+        ch.perm_off.assign(steps_.size(), -1);
         for (size_t s = 0; s < steps_.size(); ++s) {
             const StepInfo& st = steps_[s];
             if (st.mode != 2) continue;
@@ -715,6 +716,29 @@ void Program::prepare_chunks(const std::vector<uint64_t>& groups, int64_t cap) {
             for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.a, c & nodes_[st.a].var_mask));
             ch.ib_off[s] = static_cast<int64_t>(ch.idx.size());
             for (uint64_t c : node_codes[st.r]) ch.idx.push_back(find_code(st.b, c & nodes_[st.b].var_mask));
+            const int64_t va = ch.nvar[st.a], vb = ch.nvar[st.b], vr = ch.nvar[st.r];
+            if (vr < 2 || va * vb == vr) continue;  // full products: product_order
+            {
+                // an operand with fewer variants than the result, at least 4x larger per
+                // variant than the other: order the results by its variant so that the
+                // GEMM's tiles in flight share its panels (RCSG_NO_VPERM: off)
+                const double sa = static_cast<double>(st.m) * st.k, sb = static_cast<double>(st.n) * st.k;
+                const bool by_a = va < vr && sa >= 4 * sb, by_b = vb < vr && sb >= 4 * sa;
+                if ((by_a || by_b) && !getenv("RCSG_NO_VPERM")) {
+                    const int64_t off_s = by_a ? ch.ia_off[s] : ch.ib_off[s], off_o = by_a ? ch.ib_off[s] : ch.ia_off[s];
+                    std::vector<int32_t> order(static_cast<size_t>(vr));
+                    std::iota(order.begin(), order.end(), 0);
+                    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+                        const int32_t sx = ch.idx[off_s + x], sy = ch.idx[off_s + y];
+                        return sx != sy ? sx < sy : ch.idx[off_o + x] < ch.idx[off_o + y];
+                    });
+                    ch.perm_off[s] = static_cast<int64_t>(ch.idx.size());
+                    ch.idx.insert(ch.idx.end(), order.begin(), order.end());
+                    if (getenv("RCSG_DEBUG_VPERM"))
+                        fprintf(stderr, "[rcsg] vperm step %d by %c va %lld vb %lld vr %lld\n", st.plan_index,
+                                by_a ? 'A' : 'B', (long long)va, (long long)vb, (long long)vr);
+                }
+            }
         }
         const int64_t G = static_cast<int64_t>(n_ext_groups_);
         std::vector<std::array<int32_t, 3>> ent;  // (group, lo, root variant)
@@ -798,6 +822,8 @@ GemmArgs Program::step_args(const StepInfo& st, const ChunkData* ch) const {
     g.fault = d_fault_;
     g.om = st.om;
     g.scale_exp = node_exp_[st.a] + node_exp_[st.b] - node_exp_[st.r];
+    static const bool chop = getenv("RCSG_TF32_CHOP") != nullptr;  // probes: the MMA's own truncation
+    g.round_tf32 = precision_ == RCSG_PREC_TF32 && !chop;
     const int64_t vb = (B.level == 2 && ch) ? ch->nvar[st.b] : 1;
     const int prod = st.mode == 2 ? product_order(A.var_mask, B.var_mask, va, vb, vr) : 0;
     if (prod) {
@@ -823,6 +849,7 @@ GemmArgs Program::step_args(const StepInfo& st, const ChunkData* ch) const {
         g.c_batch = st.m * st.n;
         g.ia = ch->d_idx + ch->ia_off[&st - steps_.data()];
         g.ib = ch->d_idx + ch->ib_off[&st - steps_.data()];
+        if (ch->perm_off[&st - steps_.data()] >= 0) g.vperm = ch->d_idx + ch->perm_off[&st - steps_.data()];
     } else {
         g.m = st.m * va;  // mode 1: the variants fold into M
         g.batch = 1;
@@ -878,6 +905,14 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     if (profile_ && getenv("RCSG_DUMP_VARS") && flops > (1ull << 32))
         fprintf(stderr, "[rcsg] step %d mode %d va %lld vb %lld vr %lld m %lld n %lld k %lld\n", st.plan_index, st.mode,
                 (long long)va, (long long)vb, (long long)vr, (long long)st.m, (long long)st.n, (long long)st.k);
+    if (profile_ && getenv("RCSG_DUMP_VARS") && flops > (1ull << 32) && st.mode == 2 && ch) {
+        const size_t si = static_cast<size_t>(&st - steps_.data());
+        fprintf(stderr, "[rcsg]   ia:");
+        for (int64_t v = 0; v < std::min<int64_t>(vr, 20); ++v) fprintf(stderr, " %d", ch->idx[ch->ia_off[si] + v]);
+        fprintf(stderr, "\n[rcsg]   ib:");
+        for (int64_t v = 0; v < std::min<int64_t>(vr, 20); ++v) fprintf(stderr, " %d", ch->idx[ch->ib_off[si] + v]);
+        fprintf(stderr, "\n");
+    }
     const int mk = mark_begin();
     if (mk >= 0) {  // algorithmic bytes: every operand variant read once, the result written once
         const int64_t eb = 2 * elem_bytes_;
@@ -888,7 +923,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
     // K <= 16 goes to the register-blocked outer-product kernel, except large
     // K = 5..16 products, which are CUDA-core FMA-bound there and memory-bound
     // on the tensor cores (narrow-K tiles zero-fill K up to 16)
-    const bool big_k16 = g.k > 4 && static_cast<double>(g.m) * g.n * std::max<int64_t>(g.batch, 1) >= 4194304.0;
+    static const int64_t smallk_max_n = getenv("RCSG_SMALLK_MAXN") ? atoll(getenv("RCSG_SMALLK_MAXN")) : 0;
+    const bool big_k16 = g.k > 4 && static_cast<double>(g.m) * g.n * std::max<int64_t>(g.batch, 1) >= 4194304.0 &&
+                         !(std::min(g.m, g.n) <= smallk_max_n);
     if (gemm_smallk_supported(g) && !(tc_ok && big_k16)) {
         launch_gemm_smallk<R>(g, ls_);
         mark_end(mk, kCatGemmSimt, flops, st.plan_index, g.m, g.n, g.k, g.batch);
@@ -1008,7 +1045,7 @@ void Program::exec_phase(int phase, const ChunkData* ch) {
             RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[phase],
                                                             static_cast<int>(static_jobs_[phase].size()),
                                                             d_leaf_data_, nullptr, d_pass_src_, d_state_,
-                                                            static_cast<S*>(arena_), ls_));
+                                                            static_cast<S*>(arena_), ls_, round_leaves()));
             ++launches_;
         }
     } else {
@@ -1016,7 +1053,7 @@ void Program::exec_phase(int phase, const ChunkData* ch) {
         const int j1 = phase == 3 ? ch->n_leaf_jobs3 : ch->n_leaf_jobs;
         if (j1 > j0) {
             RCSG_DISPATCH(precision_, launch_leaf_project<S>(ch->d_leaf_jobs + j0, j1 - j0, d_leaf_data_, ch->d_codes,
-                                                            d_pass_src_, d_state_, static_cast<S*>(arena_), ls_));
+                                                            d_pass_src_, d_state_, static_cast<S*>(arena_), ls_, round_leaves()));
             ++launches_;
         }
     }
@@ -1520,7 +1557,7 @@ void Program::build_tables() {
         if (!static_jobs_[1].empty()) {
             RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[1], static_cast<int>(static_jobs_[1].size()),
                                                             d_leaf_data_, nullptr, d_pass_src_, d_state_,
-                                                            static_cast<S*>(arena_), stream_));
+                                                            static_cast<S*>(arena_), stream_, round_leaves()));
         }
         for (const StepInfo& st : steps_)
             if (st.tab) exec_step(st, nullptr);
@@ -1533,7 +1570,7 @@ void Program::run_task(const Task& t, int64_t P) {
         case 0:
             RCSG_DISPATCH(precision_, launch_leaf_project<S>(d_static_jobs_[1], static_cast<int>(static_jobs_[1].size()),
                                                             d_leaf_data_, nullptr, d_pass_src_, d_state_,
-                                                            static_cast<S*>(arena_), ls_));
+                                                            static_cast<S*>(arena_), ls_, round_leaves()));
             ++launches_;
             break;
         case 1:
@@ -1549,7 +1586,7 @@ void Program::run_task(const Task& t, int64_t P) {
             const int j1 = t.kind == 4 ? t.ch->n_leaf_jobs3 : t.ch->n_leaf_jobs;
             RCSG_DISPATCH(precision_, launch_leaf_project<S>(t.ch->d_leaf_jobs + j0, j1 - j0, d_leaf_data_,
                                                             t.ch->d_codes, d_pass_src_, d_state_,
-                                                            static_cast<S*>(arena_), ls_));
+                                                            static_cast<S*>(arena_), ls_, round_leaves()));
             ++launches_;
             break;
         }

@@ -102,6 +102,9 @@ struct ChunkData {
     std::vector<int64_t> nvar;        // per node variant count
     std::vector<int32_t> idx;         // ia/ib arrays of gathered steps (concatenated)
     std::vector<int64_t> ia_off, ib_off;  // per step
+    // per step: offset into idx of the result-variant order that groups the
+    // variants sharing the larger operand (tcgen05 raster), -1 if none
+    std::vector<int64_t> perm_off;
     // finalisation: per output group f of this chunk, its entries (root variant,
     // batched slice lo) in ascending lo
     std::vector<int32_t> fin_g, fin_off, ent_vid, ent_lo;
@@ -116,6 +119,8 @@ struct ChunkData {
 
 class Program {
   public:
+    // tf32 mode: leaves are stored rounded to tf32 like every GEMM output (tf32_rn)
+    int round_leaves() const { return precision_ == RCSG_PREC_TF32 && !getenv("RCSG_TF32_CHOP") ? 1 : 0; }
     Program(const rcsg_network_desc& net, const rcsg_plan_desc& plan, const std::vector<LabelRole>& roles,
             int precision, uint64_t mem_budget);
     ~Program();

@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(kThreads) smallk_kernel(const GemmArgs g, int 
                     ci = fma(a_im[r][kk], b_re[kk], ci);
                 }
                 const int64_t o = row_off[r] + col_off;
-                cr *= sc;
-                ci *= sc;
+                cr = tf32_if(cr * sc, g.round_tf32);
+                ci = tf32_if(ci * sc, g.round_tf32);
                 store_c(C + o, cr);
                 store_c(C + g.c_plane + o, ci);
                 bad |= unstorable<S>(cr) || unstorable<S>(ci);
@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(kThreads) smallk_rows_kernel(const GemmArgs g)
                 ci = fma(a_im[kk], b_re[c][kk], ci);
             }
             const int64_t o = roff + col_off[c];
-            cr *= sc;
-            ci *= sc;
+            cr = tf32_if(cr * sc, g.round_tf32);
+            ci = tf32_if(ci * sc, g.round_tf32);
             store_c(C + o, cr);
             store_c(C + g.c_plane + o, ci);
             bad |= unstorable<S>(cr) || unstorable<S>(ci);

@@ -224,9 +224,13 @@ struct TcParams {
     int32_t* fault;
     OutMap om;              // output scatter map (applied when not split)
     int32_t scale_exp;      // outputs stored times 2^scale_exp (fp16 mode)
+    int32_t round_tf32;     // tf32 mode: outputs rounded to tf32 (tf32_rn)
     int32_t b_resident;     // B identical for every tile: loaded once per stage slot
     int32_t ng;             // persistent kernel: epilogue warp groups (tiles in flight), 1 / 2 / 4
     int32_t group;          // grouped raster: G "hi" tiles per super-row (0: plain mixed-radix order)
+    const int32_t* vperm;   // batched GEMMs with a shared operand: variant order (nullptr: none); the
+                            // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
+                            // flight read the same shared-operand panels (see coord_at)
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -251,6 +255,10 @@ __device__ __forceinline__ bool store_chunk(const TcParams& p, int split, int64_
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
         for (int i = 0; i < CW; ++i) x[i] *= sc;
+    }
+    if (p.round_tf32) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) x[i] = tf32_rn(x[i]);
     }
 #pragma unroll
     for (int i = 0; i < CW; ++i) bad |= unstorable<E>(x[i]);
@@ -398,6 +406,10 @@ __device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v
         const float sc = exp2f(static_cast<float>(p.scale_exp));
 #pragma unroll
         for (int i = 0; i < CW; ++i) x[i] *= sc;
+    }
+    if (p.round_tf32) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) x[i] = tf32_rn(x[i]);
     }
     if (row0 + lane < p.m) {
 #pragma unroll
@@ -659,6 +671,11 @@ struct TileIter {
         n_lo = static_cast<uint32_t>(p.m_fast ? p.mt : p.nt);
         n_hi = static_cast<uint32_t>(p.m_fast ? p.nt : p.mt);
         n_v = static_cast<uint32_t>(p.batch < 1 ? 1 : p.batch);
+        if (p.vperm) {  // lo = (variant, n-tile) in vperm order, hi = m-tiles
+            n_lo = static_cast<uint32_t>(p.nt) * n_v;
+            n_hi = static_cast<uint32_t>(p.mt);
+            n_v = 1;
+        }
         // split is the slowest digit: the tiles in flight together work on the
         // same K range, so their A / B panels are shared through L2
         auto digits = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
@@ -702,10 +719,17 @@ struct TileIter {
         const uint32_t grp = r / (G * n_lo), rg = r - grp * (G * n_lo);
         const uint32_t first = grp * G, gsz = min(G, n_hi - first);
         const uint32_t hi_d = first + rg % gsz, lo_d = rg / gsz;
-        const uint32_t mtile = p.m_fast ? lo_d : hi_d, ntile = p.m_fast ? hi_d : lo_d;
-        c.v = v;
-        c.m0 = static_cast<int>(mtile * kBM);
-        c.n0 = static_cast<int>(ntile * BN);
+        if (p.vperm) {  // G m-tiles x (in flight / G) consecutive variants of the sorted order
+            const uint32_t nt = static_cast<uint32_t>(p.nt), j = lo_d / nt;
+            c.v = static_cast<uint32_t>(__ldg(p.vperm + j));
+            c.m0 = static_cast<int>(hi_d * kBM);
+            c.n0 = static_cast<int>((lo_d - j * nt) * BN);
+        } else {
+            const uint32_t mtile = p.m_fast ? lo_d : hi_d, ntile = p.m_fast ? hi_d : lo_d;
+            c.v = v;
+            c.m0 = static_cast<int>(mtile * kBM);
+            c.n0 = static_cast<int>(ntile * BN);
+        }
         c.k_begin = c.split * p.k_chunk;
         const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
         c.kblocks = static_cast<int>((k_end - c.k_begin + kbk<E, RB> - 1) / kbk<E, RB>);
@@ -1068,6 +1092,7 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     p.fault = g.fault;
     p.om = g.om;
     p.scale_exp = g.scale_exp;
+    p.round_tf32 = g.round_tf32;
     p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : epilogue_kind4(g.om, g.n);
     if (const char* e = getenv("RCSG_TC_NO_STAGE")) if (atoi(e)) p.epi = 0;
     const int64_t tiles = p.mt * p.nt * g.batch;
@@ -1106,6 +1131,10 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         int grp = (chunk_blocks >= 32 && n_lo >= 16 && n_hi >= 8) ? 8 : 0;
         if (const char* e = getenv("RCSG_TC_GROUP")) grp = atoi(e);
         p.group = grp > 0 && n_hi > grp ? grp : 0;
+        if (g.vperm && g.batch > 1) {  // shared-operand batch: G = 16 m-tiles x the variants in flight
+            p.vperm = g.vperm;
+            p.group = static_cast<int32_t>(std::min<int64_t>(16, p.mt));
+        }
     }
     p.b_resident = (p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
                     !(getenv("RCSG_TC_NO_BRES") != nullptr)) ? 1 : 0;

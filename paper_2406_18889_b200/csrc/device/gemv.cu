@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const int64_t o = v * g.m * g.n + mi * g.n + ni;
                 if (splits == 1) {
                     S* C = static_cast<S*>(g.c) + v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
-                    const R sc = pow2<R>(g.scale_exp), vr = acc_re[j] * sc, vi = acc_im[j] * sc;
+                    const R sc = pow2<R>(g.scale_exp), vr = tf32_if(acc_re[j] * sc, g.round_tf32),
+                            vi = tf32_if(acc_im[j] * sc, g.round_tf32);
                     store_c(C, vr);
                     store_c(C + g.c_plane, vi);
                     if (g.fault && (unstorable<S>(vr) || unstorable<S>(vi))) atomicMin(g.fault, g.step);

@@ -21,7 +21,8 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
                                     const double* __restrict__ leaf_data,
                                     const uint64_t* __restrict__ codes,
                                     const PassSrc* __restrict__ pass_src,
-                                    const PassState* __restrict__ state, R* __restrict__ arena) {
+                                    const PassState* __restrict__ state, R* __restrict__ arena,
+                                    int round_tf32) {
     pdl_enter();
     const LeafJob j = jobs[blockIdx.x];
     const PassState ps = *state;
@@ -57,27 +58,27 @@ __global__ void leaf_project_kernel(const LeafJob* __restrict__ jobs,
         const double re = leaf_data[2 * (j.data_off + src)];
         const double im = leaf_data[2 * (j.data_off + src) + 1];
         using C = typename Acc<R>::T;
-        store_c(arena + j.out_off + t, static_cast<C>(re));
-        store_c(arena + j.out_off + j.out_plane + t, static_cast<C>(im));
+        store_c(arena + j.out_off + t, tf32_if(static_cast<C>(re), round_tf32));
+        store_c(arena + j.out_off + j.out_plane + t, tf32_if(static_cast<C>(im), round_tf32));
     }
 }
 
 template <typename R>
 void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf_data,
                          const uint64_t* d_codes, const PassSrc* d_pass_src,
-                         const PassState* d_state, R* arena, cudaStream_t st) {
+                         const PassState* d_state, R* arena, cudaStream_t st, int round_tf32) {
     if (n_jobs == 0) return;
     launch_pdl(leaf_project_kernel<R>, dim3(n_jobs), dim3(64), 0, st, d_jobs, d_leaf_data, d_codes, d_pass_src,
-               d_state, arena);
+               d_state, arena, round_tf32);
 }
 template void launch_leaf_project<float>(const LeafJob*, int, const double*, const uint64_t*,
-                                         const PassSrc*, const PassState*, float*, cudaStream_t);
+                                         const PassSrc*, const PassState*, float*, cudaStream_t, int);
 template void launch_leaf_project<double>(const LeafJob*, int, const double*, const uint64_t*,
-                                          const PassSrc*, const PassState*, double*, cudaStream_t);
+                                          const PassSrc*, const PassState*, double*, cudaStream_t, int);
 template void launch_leaf_project<bf16>(const LeafJob*, int, const double*, const uint64_t*,
-                                        const PassSrc*, const PassState*, bf16*, cudaStream_t);
+                                        const PassSrc*, const PassState*, bf16*, cudaStream_t, int);
 template void launch_leaf_project<f16>(const LeafJob*, int, const double*, const uint64_t*,
-                                       const PassSrc*, const PassState*, f16*, cudaStream_t);
+                                       const PassSrc*, const PassState*, f16*, cudaStream_t, int);
 
 // ------------------------------------------------------------------ SIMT GEMM
 // 64x64 complex tile per CTA, 16x16 threads, 4x4 complex outputs per thread,
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g, const 
                         bad |= !isfinite(acc_re[i][j]) || !isfinite(acc_im[i][j]);
                     } else {
                         const int64_t o = out_row_off(g.om, g.n, m) + out_col_off(g.om, n);
-                        const R vr = acc_re[i][j] * sc, vi = acc_im[i][j] * sc;
+                        const R vr = tf32_if(acc_re[i][j] * sc, g.round_tf32), vi = tf32_if(acc_im[i][j] * sc, g.round_tf32);
                         store_c(Cb + o, vr);
                         store_c(Cb + g.c_plane + o, vi);
                         bad |= unstorable<S>(vr) || unstorable<S>(vi);
@@ -216,8 +217,8 @@ __global__ void splitk_reduce_kernel(const typename Acc<S>::T* __restrict__ ws, 
         }
         const int64_t v = i / mn, e = i - v * mn, mi = e / g.n, ni = e - mi * g.n;
         const int64_t o = v * g.c_batch + out_row_off(g.om, g.n, mi) + out_col_off(g.om, ni);
-        re *= sc;
-        im *= sc;
+        re = tf32_if(re * sc, g.round_tf32);
+        im = tf32_if(im * sc, g.round_tf32);
         store_c(C + o, re);
         store_c(C + g.c_plane + o, im);
         bad |= unstorable<S>(re) || unstorable<S>(im);

@@ -56,6 +56,22 @@ __device__ __forceinline__ R pow2(int e) {
     return static_cast<R>(exp2f(static_cast<float>(e)));
 }
 
+// tf32 mode: a value stored for a tcgen05 consumer is rounded to the nearest
+// tf32 (ties away), because kind::tf32 MMAs truncate their fp32 operands to
+// tf32 - rounded once on store, the operand reaches the MMA exactly instead of
+// chopped (chopping biases every product toward zero; the bias compounds along
+// the contraction tree).
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    return __uint_as_float(u);
+}
+template <typename R>
+__device__ __forceinline__ R tf32_if(R x, int32_t on) {
+    if constexpr (std::is_same_v<R, float>) return on ? tf32_rn(x) : x;
+    else return x;
+}
+
 // ---- leaf projection (reference project_leaf, contraction_engine.cpp:27-52,
 // batched over all leaves of one level and all of their variants).
 struct LeafJob {
@@ -88,7 +104,7 @@ struct PassSrc {
 template <typename R>
 void launch_leaf_project(const LeafJob* d_jobs, int n_jobs, const double* d_leaf_data,
                          const uint64_t* d_codes, const PassSrc* d_pass_src,
-                         const PassState* d_state, R* arena, cudaStream_t st);
+                         const PassState* d_state, R* arena, cudaStream_t st, int round_tf32 = 0);
 
 // ---- bit-permutation transpose of a [V][2^rank] planar tensor (permute.cu).
 // Output bit q (LSB=0) takes input bit src_bit[q].  Built on the host by
@@ -194,6 +210,8 @@ struct GemmArgs {
     int32_t* fault;         // device flag: min step index with a non-finite output
     OutMap om;              // where C elements land inside their variant block
     int32_t scale_exp;      // outputs are stored times 2^scale_exp (fp16 per-tensor scaling; 0 otherwise)
+    const int32_t* vperm;   // tcgen05 raster: result variants ordered so that runs share an operand (or nullptr)
+    int32_t round_tf32;     // tf32 mode: outputs rounded to tf32 on store (see tf32_rn)
 };
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);

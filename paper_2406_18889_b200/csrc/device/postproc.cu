@@ -83,6 +83,9 @@ __device__ __forceinline__ uint64_t asc_key(double p) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// shared-memory staging slots of direct_scan_kernel (> one load round of 8 x 256)
+constexpr unsigned kDirectStage = 3072;
+
 // Sort key of a kept candidate (ascending = probability descending).  64-bit:
 // the full descending key.  32-bit: the distance of the ascending key above the
 // threshold, shifted so that probabilities up to 1 fit (distinct probabilities
@@ -107,18 +110,71 @@ __device__ __forceinline__ void flag_nan(double p, int* bad) {
 
 // ---- 1. sampled histograms -------------------------------------------------
 // level 0: bins = top 12 bits of the ascending key (sign + exponent: binades);
-// level 1: inside binade `sel` (from *sel_in), the next 12 bits.  Samples every
-// `stride`-th group.
-__global__ void sample_hist_kernel(const double* __restrict__ src, int from_amps, int64_t n_groups, int l,
-                                   int64_t stride, int level, const uint32_t* __restrict__ sel_in,
-                                   uint32_t* __restrict__ hist, int* __restrict__ bad) {
+// level 1: inside binade `sel` (from sel[0]), the next 12 bits.  Samples every
+// `stride`-th group.  The last block to finish picks the bin (no separate
+// launch): suffix sums of the histogram (from the top bin down) find the
+// highest bin whose suffix reaches `want` (sample units); level 0 writes the
+// binade and the samples in binades above it, level 1 the threshold key.
+__device__ void pick_threshold_block(const uint32_t* __restrict__ hist, int level, double want,
+                                     uint32_t* __restrict__ sel, uint64_t* __restrict__ thr, double* part) {
+    __shared__ int found;
+    const uint32_t* h = hist + level * kHistBins;
+    const double base = level ? static_cast<double>(sel[1]) : 0.0;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per_t = kHistBins / nt;
+    const int b0 = per_t * (nt - 1 - tid);  // thread tid owns bins [b0, b0 + per_t); thread 0 the top ones
+    double local = 0;
+    for (int j = 0; j < per_t; ++j) local += __ldcg(h + b0 + j);
+    part[tid] = local;
+    if (tid == 0) found = -1;
+    __syncthreads();
+    for (int off = 1; off < nt; off <<= 1) {  // inclusive scan over chunks, top first
+        const double v = tid >= off ? part[tid - off] : 0.0;
+        __syncthreads();
+        part[tid] += v;
+        __syncthreads();
+    }
+    const double above = base + (tid ? part[tid - 1] : 0.0);  // samples in bins >= b0 + per_t
+    if (above < want && above + local >= want) {  // the one chunk where the running count crosses
+        double c = above;
+        for (int j = per_t - 1; j >= 0; --j) {
+            const double hj = __ldcg(h + b0 + j);
+            if (c + hj >= want) {
+                found = b0 + j;
+                break;
+            }
+            c += hj;
+        }
+    }
+    __syncthreads();
+    int b = found < 0 ? 0 : found;  // nothing reaches `want`: keep everything
+    if (level == 0 && b < 0x800) b = 0x800;  // never below +0.0: negative probabilities take the full path
+    if (b < b0 || b >= b0 + per_t) return;  // the owner of bin b writes
+    if (level == 0) {
+        double c = above;  // samples in bins above b
+        for (int j = per_t - 1; b0 + j > b; --j) c += __ldcg(h + b0 + j);
+        sel[0] = static_cast<uint32_t>(b);
+        sel[1] = static_cast<uint32_t>(c);
+    } else {
+        thr[0] = (static_cast<uint64_t>(sel[0]) << 52) | (static_cast<uint64_t>(b) << 40);
+    }
+}
+
+// hist: 2 x kHistBins bins, then one completion counter per level (zeroed by the caller)
+__global__ void __launch_bounds__(512) sample_hist_kernel(const double* __restrict__ src, int from_amps,
+                                                          int64_t n_groups, int l, int64_t stride, int level,
+                                                          uint32_t* __restrict__ sel, uint32_t* __restrict__ hist,
+                                                          int* __restrict__ bad, double want,
+                                                          uint64_t* __restrict__ thr) {
     __shared__ uint32_t h[kHistBins];
+    __shared__ double part[512];
+    __shared__ bool last;
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     const int64_t per = int64_t{1} << l;
     const int64_t n_s = (n_groups + stride - 1) / stride;
     const int64_t n_el = n_s * per;
-    const uint32_t sel = level ? sel_in[0] : 0;
+    const uint32_t sel0 = level ? __ldcg(sel) : 0;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_el;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t g = (e >> l) * stride, i = e & (per - 1);
@@ -126,60 +182,18 @@ __global__ void sample_hist_kernel(const double* __restrict__ src, int from_amps
         flag_nan(p, bad);
         const uint64_t k = asc_key(p);
         if (level == 0) atomicAdd(&h[k >> 52], 1u);
-        else if (static_cast<uint32_t>(k >> 52) == sel) atomicAdd(&h[(k >> 40) & 0xfff], 1u);
+        else if (static_cast<uint32_t>(k >> 52) == sel0) atomicAdd(&h[(k >> 40) & 0xfff], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
         if (h[i]) atomicAdd(&hist[level * kHistBins + i], h[i]);
-}
-
-// One block of 1024 threads: suffix sums of a histogram (from the top bin
-// down) find the highest bin whose suffix reaches `want` (sample units).
-// level 0 writes the binade and the samples in binades above it; level 1
-// writes the threshold key.
-__global__ void __launch_bounds__(1024) pick_threshold_kernel(const uint32_t* __restrict__ hist, int level,
-                                                              double want, uint32_t* __restrict__ sel,
-                                                              uint64_t* __restrict__ thr) {
-    __shared__ double part[1024];
-    __shared__ int found;
-    const uint32_t* h = hist + level * kHistBins;
-    const double base = level ? static_cast<double>(sel[1]) : 0.0;
-    const int tid = threadIdx.x;
-    const int b0 = 4 * (1023 - tid);  // thread tid owns bins [b0, b0 + 4); thread 0 the top ones
-    double local = 0;
-    for (int j = 0; j < 4; ++j) local += h[b0 + j];
-    part[tid] = local;
-    if (tid == 0) found = -1;
+    __threadfence();
     __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan over chunks, top first
-        const double v = tid >= off ? part[tid - off] : 0.0;
-        __syncthreads();
-        part[tid] += v;
-        __syncthreads();
-    }
-    const double above = base + (tid ? part[tid - 1] : 0.0);  // samples in bins >= b0 + 4
-    if (above < want && above + local >= want) {  // the one chunk where the running count crosses
-        double a = above;
-        for (int j = 3; j >= 0; --j) {
-            if (a + h[b0 + j] >= want) {
-                found = b0 + j;
-                break;
-            }
-            a += h[b0 + j];
-        }
-    }
+    if (threadIdx.x == 0) last = atomicAdd(&hist[2 * kHistBins + level], 1u) == gridDim.x - 1;
     __syncthreads();
-    int b = found < 0 ? 0 : found;  // nothing reaches `want`: keep everything
-    if (level == 0 && b < 0x800) b = 0x800;  // never below +0.0: negative probabilities take the full path
-    if (b < b0 || b >= b0 + 4) return;  // the owner of bin b writes
-    if (level == 0) {
-        double c = above;  // samples in bins above b
-        for (int j = 3; b0 + j > b; --j) c += h[b0 + j];
-        sel[0] = static_cast<uint32_t>(b);
-        sel[1] = static_cast<uint32_t>(c);
-    } else {
-        thr[0] = (static_cast<uint64_t>(sel[0]) << 52) | (static_cast<uint64_t>(b) << 40);
-    }
+    if (!last) return;
+    __threadfence();
+    pick_threshold_block(hist, level, want, sel, thr, part);
 }
 
 // ---- 2. the streaming pass ----------------------------------------------------
@@ -199,7 +213,9 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
     // kept candidates are staged in shared memory (warp-aggregated shared
     // atomics) and flushed with ONE global atomic per ~1-2K entries: a global
     // atomic per warp would serialise on the single counter
+    // (4 loads per thread in flight: 8, with 3K staging slots, measured slower)
     constexpr unsigned kStage = 2048;
+    constexpr int U = 4;
     __shared__ K s_key[kStage];
     __shared__ V s_t[kStage];
     __shared__ unsigned s_cnt;
@@ -240,24 +256,24 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         __syncthreads();
     };
     if (!DIRECT) {
-        // flat grid-stride over candidates, 4 independent 16-B loads per thread in flight
+        // flat grid-stride over candidates, U independent 16-B loads per thread in flight
         const int64_t total = n_groups << l;
         const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-        for (int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x); t0 < total; t0 += 4 * stride) {
-            double p[4];
+        for (int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x); t0 < total; t0 += U * stride) {
+            double p[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int64_t t = t0 + u * stride + threadIdx.x;
                 p[u] = t < total ? prob_at(src, from_amps, t) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int64_t t = t0 + u * stride + threadIdx.x;
                 const bool in = t < total;
                 if (in) flag_nan(p[u], bad);
                 stage(in && asc_key(p[u]) >= thr, p[u], t);
             }
-            flush(4 * blockDim.x, false);
+            flush(U * blockDim.x, false);
         }
         flush(0, true);
         return;
@@ -323,9 +339,18 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
 // Direct sampling fused with the threshold pass, for groups of <= 8192
 // candidates: each block iteration loads GPB whole groups (16-B amplitude
 // loads, coalesced, many in flight) into a shared-memory probability tile,
-// staging kept top-k candidates on the way; then thread g walks group g's
-// probabilities sequentially from shared memory (the reference's left-to-right
-// f64 total and inverse-CDF subtraction, bit for bit) - no shuffle chains.
+// staging kept top-k candidates on the way (one flush check per load round);
+// then thread g walks group g's row from shared memory.
+//
+// The reference draws u = r * total with total the left-to-right f64 sum, then
+// subtracts the probabilities left to right until u <= 0 (sampling.cpp).  The
+// walk keeps the left-to-right total bit for bit (one sequential pass that
+// leaves the running sums s_i in the row) and finds the first s_i >= u by
+// binary search.  The reference's running u_i differs from u - s_i by at most
+// per * 2^-52 * total (+ an underflow term): when u lies farther than that
+// from the two running sums around the crossing, the pick is the reference's;
+// otherwise (probability ~1e-14 per group) the group re-runs the reference's
+// exact subtraction chain from the amplitudes.
 template <typename K, typename V>
 __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restrict__ src, int from_amps,
                                                           int64_t n_groups, int l, int gpb,
@@ -335,14 +360,16 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                                                           int* __restrict__ bad, const uint64_t* __restrict__ fixed,
                                                           MemberMap mm, uint64_t seed,
                                                           uint64_t* __restrict__ direct_out,
-                                                          unsigned long long* __restrict__ zero_group) {
+                                                          unsigned long long* __restrict__ zero_group,
+                                                          double slack_mul) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    constexpr unsigned kStage = 2048;
+    constexpr int U = 8;
+    const unsigned stage_n = kDirectStage;
     K* s_key = reinterpret_cast<K*>(dsm);
-    V* s_t = reinterpret_cast<V*>(dsm + kStage * sizeof(K));
+    V* s_t = reinterpret_cast<V*>(dsm + stage_n * sizeof(K));
     const int64_t per = int64_t{1} << l;
     const int pitch = static_cast<int>(per) + 1;  // odd pitch: threads walking rows hit distinct banks
-    double* tile = reinterpret_cast<double*>(dsm + kStage * (sizeof(K) + sizeof(V)));
+    double* tile = reinterpret_cast<double*>(dsm + stage_n * (sizeof(K) + sizeof(V)));
     __shared__ unsigned s_cnt;
     __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) s_cnt = 0;
@@ -351,13 +378,30 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
     const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
     const int64_t tile_el = static_cast<int64_t>(gpb) * per;
+    const int64_t total = n_groups * per;
+    // block-uniform: flush the staged candidates when fewer than `room` slots remain (or always)
+    auto flush = [&](unsigned room, bool force) {
+        __syncthreads();
+        const unsigned n = s_cnt;
+        __syncthreads();
+        if (n == 0 || (!force && n + room <= stage_n)) return;
+        if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
+        __syncthreads();
+        const unsigned long long b0 = s_base;
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+            if (b0 + i < cap) {
+                out_key[b0 + i] = s_key[i];
+                out_t[b0 + i] = s_t[i];
+            }
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+    };
     for (int64_t g0 = blockIdx.x * static_cast<int64_t>(gpb); g0 < n_groups;
          g0 += static_cast<int64_t>(gridDim.x) * gpb) {
         const int64_t base_t = g0 * per;
-        const int64_t total = n_groups * per;
         // load + stage: rounds of U x blockDim.x candidates with U independent 16-B
         // loads per thread in flight (block-uniform rounds)
-        constexpr int U = 8;
         for (int64_t e0 = 0; e0 < tile_el; e0 += U * static_cast<int64_t>(blockDim.x)) {
             double pv[U];
 #pragma unroll
@@ -388,31 +432,19 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                             s_t[pos] = static_cast<V>(t);
                         }
                     }
-                    __syncthreads();
-                    const unsigned n = s_cnt;
-                    __syncthreads();
-                    if (n + blockDim.x > kStage) {
-                        if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
-                        __syncthreads();
-                        const unsigned long long b0 = s_base;
-                        for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
-                            if (b0 + i < cap) {
-                                out_key[b0 + i] = s_key[i];
-                                out_t[b0 + i] = s_t[i];
-                            }
-                        __syncthreads();
-                        if (threadIdx.x == 0) s_cnt = 0;
-                        __syncthreads();
-                    }
                 }
             }
+            if (collect) flush(U * blockDim.x, false);
         }
         __syncthreads();
         const int64_t g = g0 + threadIdx.x;
         if (threadIdx.x < gpb && g < n_groups) {
-            const double* row = tile + threadIdx.x * pitch;
+            double* row = tile + threadIdx.x * pitch;
             double tot = 0.0;
-            for (int64_t i = 0; i < per; ++i) tot = __dadd_rn(tot, row[i]);
+            for (int64_t i = 0; i < per; ++i) {  // left-to-right total; the row keeps the running sums
+                tot = __dadd_rn(tot, row[i]);
+                row[i] = tot;
+            }
             if (!(tot > 0.0)) {
                 atomicMin(zero_group, static_cast<unsigned long long>(g));
                 direct_out[g] = 0;
@@ -421,13 +453,25 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                 z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
                 z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
                 z ^= z >> 31;
-                double u = __dmul_rn(static_cast<double>(z >> 11) * 0x1.0p-53, tot);
-                int64_t pick = per - 1;
-                for (int64_t i = 0; i < per; ++i) {
-                    u = __dsub_rn(u, row[i]);
-                    if (u <= 0.0) {
-                        pick = i;
-                        break;
+                const double u = __dmul_rn(static_cast<double>(z >> 11) * 0x1.0p-53, tot);
+                const double slack = slack_mul * static_cast<double>(per) * (tot * 0x1.0p-51 + 0x1.0p-1070);
+                // first i with s_i >= u - slack (s is non-decreasing)
+                int64_t lo = 0, hi = per - 1;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (row[mid] >= u - slack) hi = mid;
+                    else lo = mid + 1;
+                }
+                int64_t pick = lo;
+                if (!(row[lo] >= u + slack)) {  // u near a running sum: the reference's exact chain
+                    double w = u;
+                    pick = per - 1;
+                    for (int64_t i = 0; i < per; ++i) {
+                        w = __dsub_rn(w, prob_at(src, from_amps, g * per + i));
+                        if (w <= 0.0) {
+                            pick = i;
+                            break;
+                        }
                     }
                 }
                 direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
@@ -435,20 +479,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
         }
         __syncthreads();  // the tile is reused
     }
-    if (collect) {
-        __syncthreads();
-        const unsigned n = s_cnt;
-        if (n) {
-            if (threadIdx.x == 0) s_base = atomicAdd(counter, static_cast<unsigned long long>(n));
-            __syncthreads();
-            const unsigned long long b0 = s_base;
-            for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
-                if (b0 + i < cap) {
-                    out_key[b0 + i] = s_key[i];
-                    out_t[b0 + i] = s_t[i];
-                }
-        }
-    }
+    if (collect) flush(0, true);
 }
 
 // pad [count, cap) with the largest non-negative key; flags count < k or count > cap
@@ -723,14 +754,13 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         const double expect = want / f;
         cap = static_cast<uint64_t>(std::min<double>(static_cast<double>(total), 1.25 * expect + 4096.0));
         cap = std::max<uint64_t>(cap, k);
-        uint32_t* hist = scratch_as<uint32_t>(kHist, 2 * kHistBins);
-        CUDA_OK(cudaMemsetAsync(hist, 0, 2 * kHistBins * sizeof(uint32_t), st));
+        uint32_t* hist = scratch_as<uint32_t>(kHist, 2 * kHistBins + 2);
+        CUDA_OK(cudaMemsetAsync(hist, 0, (2 * kHistBins + 2) * sizeof(uint32_t), st));
         // few blocks: each merges its shared histogram into the global one with one atomic per bin
         const int hgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(((n_s << cs.l) + 4095) / 4096, 296)));
         for (int level = 0; level < 2; ++level) {
             sample_hist_kernel<<<hgrid, 512, 0, st>>>(d_src, from_amps, G, cs.l, stride, level, d_ctl->sel, hist,
-                                                      &d_ctl->bad);
-            pick_threshold_kernel<<<1, 1024, 0, st>>>(hist, level, want, d_ctl->sel, &d_ctl->thr);
+                                                      &d_ctl->bad, want, &d_ctl->thr);
         }
         keys = scratch(kKeyA, cap * 8);
         ts = scratch(kTA, cap * 8);
@@ -744,17 +774,26 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         if (want_direct && cs.l <= 13) {
             // shared-memory tile of gpb whole groups (<= 64 KB of probabilities)
             const int64_t per = int64_t{1} << cs.l;
-            // 32 groups per tile (16.6 KB at l = 6): ~6 blocks per SM hide the load latency
+            // 32 groups per tile (16.6 KB at l = 6): ~5 blocks per SM hide the load latency
             const int gpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, 8192 / per)));
-            const size_t smem = 2048 * (sizeof(K) + sizeof(V)) + static_cast<size_t>(gpb) * (per + 1) * sizeof(double);
+            const size_t smem = kDirectStage * (sizeof(K) + sizeof(V)) + static_cast<size_t>(gpb) * (per + 1) * sizeof(double);
             static std::atomic<uint64_t> attr_done[2]{};
             if (first_on_device(attr_done[sizeof(K) == 8 ? 1 : 0]))
                 CUDA_OK(cudaFuncSetAttribute(direct_scan_kernel<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             96 * 1024));
-            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, 148 * 6)));
+                                             160 * 1024));
+            // RCSG_DIRECT_SLACK (test knob): widens the exactness margin so that
+            // groups take the reference's subtraction chain
+            const double slack_mul = getenv("RCSG_DIRECT_SLACK") ? atof(getenv("RCSG_DIRECT_SLACK")) : 1.0;
+            // persistent grid: exactly the resident blocks (no partial last wave)
+            int occ = 0, dev = 0, n_sm = 148;
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, direct_scan_kernel<K, V>, 256, smem));
+            CUDA_OK(cudaGetDevice(&dev));
+            CUDA_OK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+            const int grid = static_cast<int>(
+                std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, static_cast<int64_t>(n_sm) * std::max(occ, 1))));
             direct_scan_kernel<K, V><<<grid, 256, smem, st>>>(d_src, from_amps, G, cs.l, gpb, thr, kk, tt,
                                                               &d_ctl->count, cap, &d_ctl->bad, d_fixed, mm, seed,
-                                                              d_direct, &d_ctl->zero_group);
+                                                              d_direct, &d_ctl->zero_group, slack_mul);
         } else if (want_direct) {
             const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
             scan_kernel<true, K, V><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count, cap,

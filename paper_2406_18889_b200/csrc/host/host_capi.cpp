@@ -135,7 +135,8 @@ int rcsh_build(int n, int cycles, const char* topology, std::uint64_t seed, cons
     });
 }
 
-// Same pipeline with an explicit planner: planner 0 reference, 1 scale, 2 auto;
+// Same pipeline with an explicit planner: planner 0 reference, 1 scale, 2 auto,
+// 3 none (the plan is imported next with rcsh_plan_import);
 // n_groups / trials / threads tune the scale planner (ScalePlannerOptions).
 // report (may be null): [log2 total flops, log2 per-slice flops (batched model),
 // log2 once-only flops, log2 widest tensor, seconds, n_sliced, trials,
@@ -155,7 +156,9 @@ int rcsh_build_ex(int n, int cycles, const char* topology, std::uint64_t seed, c
         opt.threads = threads;
         ScalePlanReport rep;
         bool scale = planner == 1 || (planner == 2 && reference_planner_overflows(h->net, broken));
-        if (planner == 0) {
+        if (planner == 3) {
+            scale = false;  // no planning: the caller imports a plan file next (rcsh_plan_import)
+        } else if (planner == 0) {
             h->plan = find_contraction_path_reference(h->net, budget, effort_of(effort), seed, broken);
         } else if (scale) {
             h->plan = find_contraction_path_scale(h->net, budget, effort_of(effort), seed, broken, opt, &rep);

@@ -131,9 +131,8 @@ double plan_ridge() {
     static const double r = getenv("RCSG_PLAN_RIDGE") ? atof(getenv("RCSG_PLAN_RIDGE")) : 0.0;
     return r;
 }
-double step_cost(double flops_log2, double sa, double sb, double sc) {
+double step_cost(double flops_log2, double sa, double sb, double sc, double r = plan_ridge()) {
     const double f = std::exp2(flops_log2);
-    const double r = plan_ridge();
     if (r <= 0) return f;
     return std::max(f, r * 8.0 * (std::exp2(sa) + std::exp2(sb) + std::exp2(sc)));
 }
@@ -867,6 +866,10 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
     int threads = opt.threads > 0 ? opt.threads : static_cast<int>(std::thread::hardware_concurrency());
     threads = std::max(1, std::min(threads, trials));
     const bool debug = getenv("RCSG_PLAN_DEBUG") != nullptr;
+    // RCSG_PLAN_REFINE: size of the reconfiguration pool (search experiments)
+    const int refine = getenv("RCSG_PLAN_REFINE") ? atoi(getenv("RCSG_PLAN_REFINE")) : opt.refine;
+    // RCSG_PLAN_SEED: an independent trial stream (offline plan searches; plan files)
+    if (const char* s = getenv("RCSG_PLAN_SEED")) seed ^= std::strtoull(s, nullptr, 0) * 0x94d049bb133111ebull;
     std::mutex debug_mu;
     struct Result {
         double total = std::numeric_limits<double>::infinity();
@@ -892,7 +895,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
         std::vector<std::vector<int>> lab_holders(pb.n_labels);
         for (int i = 0; i < static_cast<int>(rd.node.size()); ++i)
             rd.labels[i].each([&](int l) { lab_holders[l].push_back(i); });
-        const int keep = std::max(1, opt.refine);
+        const int keep = std::max(1, refine);
         std::vector<std::vector<Result>> tops(threads);  // per worker: its `keep` best trees
         std::atomic<int> next_trial{0};
         auto worker = [&](int w) {
@@ -957,7 +960,7 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
             return a.total < b.total || (a.total == b.total && a.trial < b.trial);
         });
         // reconfigure the best few trees (in parallel), re-slicing as needed
-        const int n_refine = std::min<int>(std::max(1, opt.refine), static_cast<int>(best_of.size()));
+        const int n_refine = std::min<int>(std::max(1, refine), static_cast<int>(best_of.size()));
         std::vector<std::thread> pool;
         for (int i = 0; i < n_refine; ++i)
             pool.emplace_back([&, i] {
@@ -1044,6 +1047,21 @@ ContractionPlan find_contraction_path_scale(const TensorNetwork& network, std::u
     if (report) {
         const Eval e = evaluate(pb, win.tree, win.sliced, win.n_sliced);
         report->log2_total_flops = std::log2(e.flops);
+        if (debug) {  // the winner under the roofline time model (ridge 128 FLOP/B)
+            double t = 0, mem = 0;
+            for (int v = pb.n_leaves; v < static_cast<int>(win.tree.l.size()); ++v) {
+                if (win.tree.l[v] < 0) continue;
+                const int a = win.tree.l[v], b = win.tree.r[v];
+                const double fl = e.labels[a].union_count(e.labels[b]) + e.var[v] + 3.0;
+                const double c = step_cost(fl, e.labels[a].count() + e.var[a], e.labels[b].count() + e.var[b],
+                                           e.labels[v].count() + e.var[v], 128.0);
+                const double w = e.dep[v] ? std::exp2(win.n_sliced) : 1.0;
+                t += c * w;
+                if (c > std::exp2(fl)) mem += c * w;
+            }
+            fprintf(stderr, "[plan] winner: log2 flops %.2f, log2 time-model cost %.2f (memory-bound share %.2f)\n",
+                    std::log2(e.flops), std::log2(t), mem / t);
+        }
         double per_slice = 0, once = 0;
         for (int v = pb.n_leaves; v < static_cast<int>(win.tree.l.size()); ++v) {
             if (win.tree.l[v] < 0) continue;

@@ -80,3 +80,20 @@ def test_state_fidelity_and_predicted_topk_xeb():
     assert abs(pb.api.predicted_topk_xeb(1.0, 1 << 30, 1 << 15) - 10.3972) <= 1e-4  # acceptance.cpp:224-226
     with pytest.raises(pb.ConfigError):
         pb.api.predicted_topk_xeb(1.0 + 1e-12, 100, 10)  # F > 1 rejected
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_committed_bench_plans_import(name):
+    """The bench's cfg3-5 plans (plans/<cfg>.json, found offline by the scale
+    planner, tools/plan_search.py) import onto the circuit they were planned for
+    and export byte-identically; the slice count matches the planner report."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    meta = json.load(open(os.path.join(root, "plans", f"{name}.meta.json")))
+    n, m, topo = {"cfg3": (53, 12, "sycamore53"), "cfg4": (53, 20, "sycamore53"),
+                  "cfg5": (60, 24, "zuchongzhi60")}[name]
+    text = open(os.path.join(root, "plans", f"{name}.json")).read()
+    p = pb.Problem(n, m, topo, 1, list(range(6)), meta["budget_bytes"], "low").build(plan_json=text)
+    assert len(p.plan["sliced"]) == meta["report"]["n_sliced"]
+    assert p.plan_json() == text

@@ -426,3 +426,23 @@ def test_scale_planner_sycamore_matches_oracle(precision):
     for g in (0, 7, 15):
         want = pn.contract_group(int(fixed[g]), slices=(0, 2))
         assert rel(got[g], want) < TOL[precision], (g, rel(got[g], want))
+
+
+def test_shared_operand_variant_order_is_bit_identical(monkeypatch, capfd):
+    """Batched steps whose larger operand has fewer variants than the result run
+    their tiles in an order grouped by that operand's variant (tcgen05 raster
+    with a variant permutation); the amplitudes are bit-identical to the plain
+    order (RCSG_NO_VPERM).  cfg3's committed plan at M = 64 has such steps."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = pb.Problem(53, 12, "sycamore53", 1, list(range(6)), 1 << 36, "low").build(
+        plan_json=open(os.path.join(root, "plans", "cfg3.json")).read())
+    fixed, _ = pb.build_candidate_set(53, list(range(6)), 64, pb.split_next(1, 0xCA11D))
+    monkeypatch.setenv("RCSG_DEBUG_VPERM", "1")
+    a = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 1))
+    assert "[rcsg] vperm step" in capfd.readouterr().err
+    p.release()
+    monkeypatch.setenv("RCSG_NO_VPERM", "1")
+    b = p.contract_groups(fixed, precision="tf32", configs=None, slices=(0, 1))
+    p.release()
+    assert np.isfinite(a).all() and np.array_equal(a, b)

@@ -107,3 +107,26 @@ def test_errors_nan_zero_group_and_signed_zero(ref):
     probs[4, 0] = 1e-3
     for k in (1, 5, 64):
         assert np.array_equal(pb.top_k_select(n, oq, fixed, probs, k), ref.top_k(n, oq, fixed, probs, k))
+
+
+@pytest.mark.parametrize("slack", [None, "1e9", "1e300"])
+def test_direct_running_sum_search_and_exact_chain(slack, monkeypatch):
+    """Direct sampling finds the pick by binary search over the left-to-right
+    running sums and re-runs the reference's exact subtraction chain when u is
+    within the rounding margin of a running sum.  Widening the margin
+    (RCSG_DIRECT_SLACK) sends some / every group down the exact chain; the
+    samples must equal the reference's either way, on quantised amplitudes
+    (exact ties and zero probabilities) and tiny ones (subnormal products)."""
+    if slack:
+        monkeypatch.setenv("RCSG_DIRECT_SLACK", slack)
+    n, oq = 30, [0, 1, 2, 3, 4, 5]
+    seed = pb.split_next(3, 0xD1EC7)
+    for M, l, quant, scale in ((1 << 15, 6, 2.0**13, 1.0), (4096, 6, None, 2.0**-520), (2000, 5, 2.0**12, 1.0)):
+        fixed, _ = pb.build_candidate_set(n, oq[:l], M, 17)
+        a, probs = device_amps(M, l, 21, quantize=quant)
+        if scale != 1.0:
+            a = (a * scale).contiguous()
+            h = a.cpu().numpy()
+            probs = (h[:, 0] * h[:, 0] + h[:, 1] * h[:, 1]).reshape(M, 1 << l)
+        _, d, st = pb.api.postprocess_device_amps(n, oq[:l], fixed, a.data_ptr(), 0, direct_seed=seed)
+        assert np.array_equal(d, port.direct(n, oq[:l], fixed, probs, seed)), (M, l, quant, scale)

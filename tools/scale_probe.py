@@ -1,6 +1,6 @@
 """Per-slice throughput of the scale planner's plans on BASELINE cfg3-5
 (Sycamore-53 m=12 / m=20, Zuchongzhi-60 m=24; l = 6), M groups.
-Env: CFG (cfg3|cfg4|cfg5), M, PREC, SLICES (timed), BUDGET_LOG2, TRIALS.
+Env: CFG (cfg3|cfg4|cfg5), M, PREC, SLICES (timed), BUDGET_LOG2, TRIALS, PLAN (plan file).
 Prints one JSON line per precision."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,8 +15,11 @@ M = int(os.environ.get("M", "64"))
 NS = int(os.environ.get("SLICES", "16"))
 blog = int(os.environ.get("BUDGET_LOG2", "36"))
 t0 = time.time()
-p = pb.Problem(n, m, topo, 1, list(range(6)), 1 << blog, "low").build(planner="scale", n_groups=M,
-                                                                     trials=int(os.environ.get("TRIALS", "1024")))
+if os.environ.get("PLAN"):  # a plan file (plans/<cfg>.json) instead of planning here
+    p = pb.Problem(n, m, topo, 1, list(range(6)), 1 << blog, "low").build(plan_json=open(os.environ["PLAN"]).read())
+else:
+    p = pb.Problem(n, m, topo, 1, list(range(6)), 1 << blog, "low").build(planner="scale", n_groups=M,
+                                                                         trials=int(os.environ.get("TRIALS", "1024")))
 plan_s = time.time() - t0
 print(json.dumps({"cfg": cfg, "plan_s": plan_s, "report": p.plan_report, "sliced": len(p.plan["sliced"]),
                   "flops_per_slice_plan": p.plan["flops_per_slice"]}), flush=True)
