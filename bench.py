@@ -395,6 +395,10 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
         rep, source = p.plan_report or {}, f"scale planner, {trials} trials, planned in this run"
     plan_s = time.perf_counter() - t0
     fixed, _ = pb.build_candidate_set(n, CFG2["open"], M, pb.split_next(1, 0xCA11D))
+    # device arena budget: 85% of the free HBM after torch returns its cache (the
+    # executor's default is 70%; cfg5's tf32 arena is ~120 GB)
+    torch.cuda.empty_cache()
+    bud = int(torch.cuda.mem_get_info()[0] * 0.85)
     out = {"workload": f"{name}: {desc}, seed 1, l=6 open={{0..5}}, M={M} groups, K=0; "
                        f"scale planner, budget 2^{budget_log2} B",
            "plan": {"source": source, "sliced_labels": len(p.plan["sliced"]), "n_slices_log2": len(p.plan["sliced"]),
@@ -406,60 +410,79 @@ def scale_bench(pb, name, precision, n_slices, M=64, budget_log2=36, alt=None, a
     for prec, ns in ((precision, n_slices), (alt, alt_slices)):
         if not prec:
             continue
-        acc = torch.zeros(M * 64 * 2, dtype=torch.float64, device="cuda")
-        stream = torch.cuda.ExternalStream(p.stream(prec))
-        S = 8
-        t1 = time.perf_counter()
-        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1))  # warm-up
-        torch.cuda.synchronize()
-        warm_s = time.perf_counter() - t1
-        st = rcsg_stats()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for s0 in range(0, ns, S):
-                p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None,
-                                         slices=(s0, min(s0 + S, ns)), stats=st, sync=False)
-            e1.record(stream)
-        p.sync(prec)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        p.set_profile(True)
-        pst = rcsg_stats()
-        p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1), stats=pst)
-        p.set_profile(False)
-        tc_peak = bf16_peak / 2.0 if prec == "tf32" else bf16_peak
-        rate = ns / (ms / 1e3)
-        exec_tf = st.executed_flops / (ms / 1e3) / 1e12
-        top_s = pst.top_ms_sum / pst.top_launches * 1e-3 if pst.top_launches else pst.top_ms * 1e-3
-        out[prec] = {
-            "value": rate, "unit": UNIT, "timed_slices": ns, "ms": ms, "warm_s": warm_s,
-            "executed_tflops": exec_tf, "frac_of_dense_peak": exec_tf / tc_peak,
-            "peak_tflops": tc_peak, "peak_note": ("dense tf32 = 1/2 of " if prec == "tf32" else "") +
-            f"{peak_kind} dense bf16 {bf16_peak:.1f} TF/s",
-            "roofline": {"bound": "tensor", "kernel": f"plan step {pst.top_step}: tcgen05 GEMM",
-                         "achieved": pst.top_flops / top_s / 1e12 if top_s else None, "peak": tc_peak,
-                         "unit": "TFLOP/s", "frac": pst.top_flops / top_s / 1e12 / tc_peak if top_s else None,
-                         "flops": pst.top_flops, "bytes": pst.top_bytes, "launch_ms": top_s * 1e3,
-                         "share_of_slice": pst.top_ms_sum / pst.device_ms if pst.device_ms else None,
-                         "traffic": None},
-            "tensor_core_share_of_slice": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None,
-            "full_run_extrapolated_s_1gpu": p.n_slices / rate,
-            "arena_gib": st.arena_bytes / 2 ** 30, "amps_finite": bool(torch.isfinite(acc).all().item())}
-        del acc
-        p.release()  # one mode's arena at a time (cfg5's is ~80 GiB at tf32)
-    if compare and alt:
+        try:
+            out[prec] = scale_mode(pb, p, fixed, prec, ns, M, bud, bf16_peak, peak_kind)
+        except Exception as e:  # pragma: no cover - reported per mode
+            out[prec] = {"error": str(e)}
+        p.release()  # one mode's arena at a time (cfg5's is ~120 GB at tf32)
+    if compare and alt and all("error" not in out.get(x, {"error": 1}) for x in (precision, alt)):
         # fp16-complex tensor-core mode against the fp32-storage (tf32) mode on the same two slices
-        a = p.contract_groups(fixed, precision=precision, configs=None, slices=(0, 2))
+        a = p.contract_groups(fixed, precision=precision, configs=None, slices=(0, 2), budget=bud)
         p.release()
-        b = p.contract_groups(fixed, precision=alt, configs=None, slices=(0, 2))
+        b = p.contract_groups(fixed, precision=alt, configs=None, slices=(0, 2), budget=bud)
         p.release()
         import numpy as np
         errs = np.linalg.norm(b - a, axis=1) / np.maximum(np.linalg.norm(a, axis=1), 1e-300)
-        out[f"{alt}_vs_{precision}"] = {"slices": [0, 2], "groups": M, "max_norm_rel": float(errs.max()),
-                                        "median_norm_rel": float(np.median(errs)),
-                                        "tolerance": 1e-2}
+        out[f"{alt}_vs_{precision}"] = {
+            "slices": [0, 2], "groups": M, "max_norm_rel": float(errs.max()),
+            "median_norm_rel": float(np.median(errs)), "tolerance": 1e-2,
+            "within_tolerance": bool(errs.max() <= 1e-2),
+            "note": "both modes round every stored intermediate to an 11-bit significand (fp16 storage; tf32 "
+                    "operands); over ~2000 steps each drifts ~1-2% from the fp32 SIMT result "
+                    "(tools/precision_probe.py, profiles/r02/precision_probe.log), so the cfg2 tolerance "
+                    "of 1e-2 does not hold between them at this depth"}
     return out
+
+
+def scale_mode(pb, p, fixed, prec, ns, M, bud, bf16_peak, peak_kind):
+    """One precision mode of scale_bench: warm-up slice, `ns` timed slices in
+    calls of 8 (device events on the program's stream), one profiled slice."""
+    import torch
+    from paper_2406_18889_b200._native import rcsg_stats
+    acc = torch.zeros(M * 64 * 2, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(p.stream(prec, bud))
+    S = 8
+    t1 = time.perf_counter()
+    p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1),
+                             budget=bud)  # warm-up
+    torch.cuda.synchronize()
+    warm_s = time.perf_counter() - t1
+    st = rcsg_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for s0 in range(0, ns, S):
+            p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None,
+                                     slices=(s0, min(s0 + S, ns)), budget=bud, stats=st, sync=False)
+        e1.record(stream)
+    p.sync(prec, bud)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    p.set_profile(True)
+    pst = rcsg_stats()
+    p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1), budget=bud,
+                             stats=pst)
+    p.set_profile(False)
+    tc_peak = bf16_peak / 2.0 if prec == "tf32" else bf16_peak
+    rate = ns / (ms / 1e3)
+    exec_tf = st.executed_flops / (ms / 1e3) / 1e12
+    top_s = pst.top_ms_sum / pst.top_launches * 1e-3 if pst.top_launches else pst.top_ms * 1e-3
+    res = {
+        "value": rate, "unit": UNIT, "timed_slices": ns, "ms": ms, "warm_s": warm_s,
+        "executed_tflops": exec_tf, "frac_of_dense_peak": exec_tf / tc_peak,
+        "peak_tflops": tc_peak, "peak_note": ("dense tf32 = 1/2 of " if prec == "tf32" else "") +
+        f"{peak_kind} dense bf16 {bf16_peak:.1f} TF/s",
+        "roofline": {"bound": "tensor", "kernel": f"plan step {pst.top_step}: tcgen05 GEMM",
+                     "achieved": pst.top_flops / top_s / 1e12 if top_s else None, "peak": tc_peak,
+                     "unit": "TFLOP/s", "frac": pst.top_flops / top_s / 1e12 / tc_peak if top_s else None,
+                     "flops": pst.top_flops, "bytes": pst.top_bytes, "launch_ms": top_s * 1e3,
+                     "share_of_slice": pst.top_ms_sum / pst.device_ms if pst.device_ms else None,
+                     "traffic": None},
+        "tensor_core_share_of_slice": pst.gemm_tc_ms / pst.device_ms if pst.device_ms else None,
+        "full_run_extrapolated_s_1gpu": p.n_slices / rate,
+        "arena_gib": st.arena_bytes / 2 ** 30, "amps_finite": bool(torch.isfinite(acc).all().item())}
+    del acc
+    return res
 
 
 def post_bench(pb, hbm_peak):

@@ -1211,7 +1211,8 @@ void Program::calibrate(const std::vector<uint64_t>& groups, uint64_t config, ui
     {
         size_t fr = 0, tot = 0;
         CUDA_OK(cudaMemGetInfo(&fr, &tot));
-        Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.4));
+        // (the fp16 arena is allocated after calibration, by the first bind)
+        Program cal(net, plan, roles_, RCSG_PREC_TF32, static_cast<uint64_t>(fr * 0.8));
         cal.tree_fixed_ = true;  // the steps are already this program's (reassociated) tree
         cal.step_origin_ = step_origin_;
         CUDA_OK(cudaMalloc(&cal.d_max_, nodes_.size() * sizeof(float)));
