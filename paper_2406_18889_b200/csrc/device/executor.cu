@@ -1015,15 +1015,28 @@ void Program::collect_marks(rcsg_stats* stats) {
                 stats->top_launches += 1;
             }
     }
+    if (getenv("RCSG_PROFILE_ORDER")) {  // every launch in issue order (joins an ncu launch list)
+        static const char* cats[] = {"gemm_simt", "gemm_tc", "permute", "gemv"};
+        for (size_t i = 0; i < marks_.size(); ++i) {
+            const Mark& m = marks_[i];
+            fprintf(stderr, "[rcsg-order] %zu %s %d %lld %lld %lld %lld %.6e %.6e %.6f\n", i,
+                    m.cat >= 0 ? cats[m.cat] : "?", m.step, (long long)m.m, (long long)m.n, (long long)m.k,
+                    (long long)m.batch, (double)m.work, (double)m.bytes, order[i].first);
+        }
+    }
     if (env) {
         std::sort(order.rbegin(), order.rend());
         static const char* names[] = {"gemm_simt", "gemm_tc", "permute", "gemv"};
         const size_t top = std::min<size_t>(order.size(), static_cast<size_t>(atoi(env)));
         for (size_t j = 0; j < top; ++j) {
             const Mark& m = marks_[order[j].second];
-            fprintf(stderr, "[rcsg] %8.3f ms %-9s step %4d m=%lld n=%lld k=%lld batch=%lld work=%.3e\n", order[j].first,
-                    m.cat >= 0 ? names[m.cat] : "?", m.step, (long long)m.m, (long long)m.n, (long long)m.k,
-                    (long long)m.batch, (double)m.work);
+            const double sec = order[j].first * 1e-3;
+            fprintf(stderr,
+                    "[rcsg] %8.3f ms %-9s step %4d m=%lld n=%lld k=%lld batch=%lld work=%.3e bytes=%.3e "
+                    "%.1f TF/s %.1f GB/s\n",
+                    order[j].first, m.cat >= 0 ? names[m.cat] : "?", m.step, (long long)m.m, (long long)m.n,
+                    (long long)m.k, (long long)m.batch, (double)m.work, (double)m.bytes,
+                    sec > 0 ? (double)m.work / sec * 1e-12 : 0.0, sec > 0 ? (double)m.bytes / sec * 1e-9 : 0.0);
         }
     }
     marks_.clear();

@@ -162,15 +162,79 @@ struct TcElem<f16> {
     static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 };
 template <typename E>
-__host__ __device__ constexpr uint32_t idesc_of(int bn, bool neg_a) {
+__host__ __device__ constexpr uint32_t idesc_of(int bn, bool neg_a, int bm = kBM) {
     return (1u << 4) | (TcElem<E>::fmt << 7) | (TcElem<E>::fmt << 10) | (neg_a ? (1u << 13) : 0u) |
-           (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+           (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(bm >> 4) << 24);
 }
 // one 128 x BN x 32-byte-K MMA (8 tf32 or 16 bf16 along K)
 template <typename E>
 __device__ __forceinline__ void mma_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     if constexpr (sizeof(E) == 4) mma_tf32(tmem_d, da, db, idesc, acc);
     else mma_bf16(tmem_d, da, db, idesc, acc);
+}
+
+// CTA pair (cta_group::2): the leader CTA issues one 256 x N MMA over both
+// CTAs' shared memory (A: 128 rows in each CTA, B: N/2 rows in each); each
+// CTA's TMEM receives its own 128 accumulator rows
+template <typename E>
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    if constexpr (sizeof(E) == 4)
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// arrive on the same barrier in both CTAs of the pair once the issued MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// shared::cluster address of this CTA's shared variable `p` in CTA `rank`
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+
+// TMA load whose completion is signalled on the pair leader's barrier
+// (`bar` is a shared::cluster address, possibly in the peer CTA)
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -231,6 +295,7 @@ struct TcParams {
     const int32_t* vperm;   // batched GEMMs with a shared operand: variant order (nullptr: none); the
                             // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
                             // flight read the same shared-operand panels (see coord_at)
+    int32_t tm;             // persistent kernel: rows per tile (128, or 256 for a CTA pair)
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -451,10 +516,10 @@ __device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v
     return bad;
 }
 
-template <int BN, int STAGES, int RB = 128, int NPL = 2>
+template <int BN, int STAGES, int RB = 128, int NPL = 2, int CG = 1>
 struct Smem {
     static constexpr int kATile = kBM * RB;  // bytes per A plane tile (RB-byte rows)
-    static constexpr int kBTile = BN * RB;
+    static constexpr int kBTile = (BN / CG) * RB;  // a CTA pair holds half of B's N rows in each CTA
     // NPL planes per operand: {Ar, Ai, Br, Bi} (4M), {Ar, Ai, Ar+Ai, Br, Bi, Br+Bi} (3M)
     static constexpr int kStage = NPL * kATile + NPL * kBTile;
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
@@ -650,7 +715,7 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t64) 
         t = q;
     }
     c.v = t;
-    c.m0 = static_cast<int>(mtile * kBM);
+    c.m0 = static_cast<int>(mtile * p.tm);
     c.n0 = static_cast<int>(ntile * BN);
     c.k_begin = c.split * p.k_chunk;
     const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
@@ -722,12 +787,12 @@ struct TileIter {
         if (p.vperm) {  // G m-tiles x (in flight / G) consecutive variants of the sorted order
             const uint32_t nt = static_cast<uint32_t>(p.nt), j = lo_d / nt;
             c.v = static_cast<uint32_t>(__ldg(p.vperm + j));
-            c.m0 = static_cast<int>(hi_d * kBM);
+            c.m0 = static_cast<int>(hi_d * p.tm);
             c.n0 = static_cast<int>((lo_d - j * nt) * BN);
         } else {
             const uint32_t mtile = p.m_fast ? lo_d : hi_d, ntile = p.m_fast ? hi_d : lo_d;
             c.v = v;
-            c.m0 = static_cast<int>(mtile * kBM);
+            c.m0 = static_cast<int>(mtile * p.tm);
             c.n0 = static_cast<int>(ntile * BN);
         }
         c.k_begin = c.split * p.k_chunk;
@@ -741,7 +806,7 @@ struct TileIter {
         c.split = static_cast<int>(split);
         const uint32_t mtile = p.m_fast ? lo : hi, ntile = p.m_fast ? hi : lo;
         c.v = v;
-        c.m0 = static_cast<int>(mtile * kBM);
+        c.m0 = static_cast<int>(mtile * p.tm);
         c.n0 = static_cast<int>(ntile * BN);
         c.k_begin = c.split * p.k_chunk;
         const int64_t k_end = min(p.k, c.k_begin + p.k_chunk);
@@ -763,14 +828,22 @@ constexpr uint32_t pow2_ceil(uint32_t x) {
     return r;
 }
 
-template <int BN, int STAGES, typename E, int RB, bool THREE = false>
+// CG = 2: CTA-pair variant (cluster of 2 on one TPC, cta_group::2).  Tiles are
+// 256 x BN; each CTA loads its 128 A rows and BN/2 of the B rows, the leader
+// CTA's producer expects both CTAs' bytes on its full barrier, the leader's MMA
+// thread issues 256 x BN MMAs and commits to both CTAs' barriers, and each
+// CTA's epilogue drains its own TMEM rows; the peer's epilogue warps release a
+// TMEM buffer on the leader's tempty barrier.  Per CTA, a k-block moves half
+// of B's bytes of the 1-CTA tile for the same MMA work.
+template <int BN, int STAGES, typename E, int RB, bool THREE = false, int CG = 1>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const __grid_constant__ CUtensorMap map_as, const __grid_constant__ CUtensorMap map_bs,
                        const TcParams p, int64_t total_tiles) {
     constexpr int NPL = THREE ? 3 : 2;
-    using S = Smem<BN, STAGES, RB, NPL>;
+    static_assert(CG == 1 || !THREE, "3M has no CTA-pair variant");
+    using S = Smem<BN, STAGES, RB, NPL, CG>;
     // TMEM accumulator buffers ({Re, Im}, or {T1, T2, T3} for 3M): as many as fit in
     // 512 columns (max 4), so the MMA runs ahead of the epilogue by NBUF - 1 tiles
     constexpr uint32_t NBUF = tc_nbuf<THREE>(BN);
@@ -787,6 +860,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* tempty = tfull + NBUF;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;  // CTA pair: 0 = leader
+    // tiles are walked per CTA pair (cluster): both CTAs of a pair take the same tiles
+    const uint32_t unit = blockIdx.x / CG, n_units = gridDim.x / CG;
     __shared__ int64_t tn_lo[32];
     if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
     if (threadIdx.x == 32) {  // fetch the TMA descriptors while the CTA sets up
@@ -801,18 +877,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (int b = 0; b < static_cast<int>(NBUF); ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 16 / NG);  // one epilogue group drains each buffer
+            mbar_init(&tempty[b], CG * 16 / NG);  // one epilogue group (per CTA of the pair) drains each buffer
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();  // the peer's barriers are initialised before any remote signal
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     pdl_enter();  // the prologue above touched no global memory
@@ -821,8 +906,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (lane == 0) {  // ---- TMA producer
             uint32_t it = 0;
             TileIter ti;
-            ti.init(p, blockIdx.x, gridDim.x);
-            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ti.next()) {
+            ti.init(p, unit, n_units);
+            for (int64_t t = unit; t < total_tiles; t += n_units, ti.next()) {
                 const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
                 const int av = p.ia ? p.ia[c.v] : (p.a_batched ? static_cast<int>(c.v) : 0);
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
@@ -830,30 +915,42 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const int s = it % STAGES;
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* st = smem + s * S::kStage;
-                    // B resident: the same single B tile for every tile (one N tile, one
-                    // K block, unbatched B) is loaded once into each stage slot
-                    const bool load_b = !(p.b_resident && it >= STAGES);
-                    mbar_expect_tx(&full[s], load_b ? S::kStage : NPL * S::kATile);
                     const int kc = static_cast<int>(c.k_begin) + kb * kbk<E, RB>;
-                    tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
-                    tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
-                    if constexpr (THREE) tma_load_3d(st + 2 * S::kATile, &map_as, &full[s], kc, c.m0, av);
-                    if (load_b) {
+                    if constexpr (CG == 2) {
+                        // both CTAs' bytes complete on the leader's full barrier
+                        if (rank == 0) mbar_expect_tx(&full[s], 2 * S::kStage);
+                        const uint32_t bar = cluster_addr(&full[s], 0);
+                        const int ma = c.m0 + static_cast<int>(rank) * kBM, nb = c.n0 + static_cast<int>(rank) * (BN / 2);
+                        tma_load_3d_pair(st, &map_ar, bar, kc, ma, av);
+                        tma_load_3d_pair(st + S::kATile, &map_ai, bar, kc, ma, av);
                         uint8_t* sb = st + NPL * S::kATile;
-                        tma_load_3d(sb, &map_br, &full[s], kc, c.n0, bv);
-                        tma_load_3d(sb + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
-                        if constexpr (THREE) tma_load_3d(sb + 2 * S::kBTile, &map_bs, &full[s], kc, c.n0, bv);
+                        tma_load_3d_pair(sb, &map_br, bar, kc, nb, bv);
+                        tma_load_3d_pair(sb + S::kBTile, &map_bi, bar, kc, nb, bv);
+                    } else {
+                        // B resident: the same single B tile for every tile (one N tile, one
+                        // K block, unbatched B) is loaded once into each stage slot
+                        const bool load_b = !(p.b_resident && it >= STAGES);
+                        mbar_expect_tx(&full[s], load_b ? S::kStage : NPL * S::kATile);
+                        tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
+                        tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
+                        if constexpr (THREE) tma_load_3d(st + 2 * S::kATile, &map_as, &full[s], kc, c.m0, av);
+                        if (load_b) {
+                            uint8_t* sb = st + NPL * S::kATile;
+                            tma_load_3d(sb, &map_br, &full[s], kc, c.n0, bv);
+                            tma_load_3d(sb + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
+                            if constexpr (THREE) tma_load_3d(sb + 2 * S::kBTile, &map_bs, &full[s], kc, c.n0, bv);
+                        }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t id_pos = idesc_of<E>(BN, false), id_neg = idesc_of<E>(BN, true);
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (the pair's leader CTA)
+            constexpr uint32_t id_pos = idesc_of<E>(BN, false, kBM * CG), id_neg = idesc_of<E>(BN, true, kBM * CG);
             uint32_t it = 0, j = 0;
             TileIter ti;
-            ti.init(p, blockIdx.x, gridDim.x);
-            for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++j, ti.next()) {
+            ti.init(p, unit, n_units);
+            for (int64_t t = unit; t < total_tiles; t += n_units, ++j, ti.next()) {
                 const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
@@ -876,6 +973,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                             mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);           // T1 = Ar Br
                             mma_e<E>(t_im, dai + o, dbi + o, id_pos, acc);           // T2 = Ai Bi
                             mma_e<E>(t_re + 2 * BN, das + o, dbs + o, id_pos, acc);  // T3 = As Bs
+                        } else if constexpr (CG == 2) {
+                            mma_pair<E>(t_re, dar + o, dbr + o, id_pos, acc);
+                            mma_pair<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                            mma_pair<E>(t_im, dar + o, dbi + o, id_pos, acc);
+                            mma_pair<E>(t_im, dai + o, dbr + o, id_pos, 1u);
                         } else {
                             mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);
                             mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
@@ -883,9 +985,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                             mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
                         }
                     }
-                    mma_commit(&empty[s]);
+                    if constexpr (CG == 2) mma_commit_pair(&empty[s]);
+                    else mma_commit(&empty[s]);
                 }
-                mma_commit(&tfull[ab]);
+                if constexpr (CG == 2) mma_commit_pair(&tfull[ab]);
+                else mma_commit(&tfull[ab]);
             }
         }
     } else {  // ---- epilogue warps 2..17: two groups of 8 take alternate tiles; TMEM lane quarter warp % 4
@@ -906,11 +1010,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         bool bad = false;
         uint32_t j = 0;
         TileIter ti;
-        const int64_t t0 = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x;
-        ti.init(p, static_cast<uint32_t>(t0), NG * gridDim.x);
+        const int64_t t0 = unit + static_cast<int64_t>(grp) * n_units;
+        ti.init(p, static_cast<uint32_t>(t0), NG * n_units);
         j = static_cast<uint32_t>(grp);
-        for (int64_t t = t0; t < total_tiles; t += NG * static_cast<int64_t>(gridDim.x), j += NG, ti.next()) {
-            const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
+        const uint32_t tempty_leader = CG == 2 ? cluster_addr(tempty, 0) : 0u;  // tempty[0] in the leader
+        for (int64_t t = t0; t < total_tiles; t += NG * static_cast<int64_t>(n_units), j += NG, ti.next()) {
+            TileCoord c = ti.coord_at<BN, E, RB>(p, t);
+            c.m0 += static_cast<int>(rank) * kBM;  // this CTA's accumulator rows
             const uint32_t ab = j % NBUF;
             const int64_t row = c.m0 + local;
             int64_t row_off;
@@ -983,14 +1089,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + ab * 8u);
+                else mbar_arrive(&tempty[ab]);
+            }
         }
         if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
     }
     __syncwarp();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    if constexpr (CG == 2) {
+        cluster_sync();  // neither CTA frees TMEM or exits while the pair still signals it
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    } else {
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    }
 }
 
 // ---- host side
@@ -1058,13 +1172,9 @@ int epilogue_kind4(const OutMap& om, int64_t n) {
     return 0;
 }
 
-template <int BN, int STAGES, typename E, int RB = 128, bool THREE = false>
+template <int BN, int STAGES, typename E, int RB = 128, bool THREE = false, int CG = 1>
 void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, const void* b_sum = nullptr) {
-    using S = Smem<BN, STAGES, RB, THREE ? 3 : 2>;
-    static std::atomic<uint64_t> configured{0};  // function attributes are per device
-    if (first_on_device(configured))
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Smem<BN, STAGES>::kBytes);
+    using S = Smem<BN, STAGES, RB, THREE ? 3 : 2, CG>;
     const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
     const int64_t a_batches = g.a_batch ? std::max<int64_t>(1, g.a_plane / std::max<int64_t>(g.a_batch, 1)) : 1;
     const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
@@ -1072,8 +1182,8 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     const E* b = static_cast<const E*>(g.b);
     const CUtensorMap ar = make_map<E, RB>(a, g.k, a_rows, a_batches, kBM);
     const CUtensorMap ai = make_map<E, RB>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
-    const CUtensorMap br = make_map<E, RB>(b, g.k, g.n, b_batches, BN);
-    const CUtensorMap bi = make_map<E, RB>(b + g.b_plane, g.k, g.n, b_batches, BN);
+    const CUtensorMap br = make_map<E, RB>(b, g.k, g.n, b_batches, BN / CG);
+    const CUtensorMap bi = make_map<E, RB>(b + g.b_plane, g.k, g.n, b_batches, BN / CG);
     const CUtensorMap as = THREE ? make_map<E, RB>(static_cast<const E*>(a_sum), g.k, a_rows, a_batches, kBM) : ar;
     const CUtensorMap bs = THREE ? make_map<E, RB>(static_cast<const E*>(b_sum), g.k, g.n, b_batches, BN) : br;
     TcParams p{};
@@ -1081,7 +1191,8 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     p.n = g.n;
     p.k = g.k;
     p.batch = g.batch;
-    p.mt = (g.m + kBM - 1) / kBM;
+    p.tm = kBM * CG;
+    p.mt = (g.m + p.tm - 1) / p.tm;
     p.nt = (g.n + BN - 1) / BN;
     p.m_fast = p.mt < p.nt ? 1 : 0;
     p.ia = g.ia;
@@ -1136,7 +1247,7 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             p.group = static_cast<int32_t>(std::min<int64_t>(16, p.mt));
         }
     }
-    p.b_resident = (p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
+    p.b_resident = (CG == 1 && p.nt == 1 && splits == 1 && kblocks == 1 && !g.ib && !g.b_batch &&
                     !(getenv("RCSG_TC_NO_BRES") != nullptr)) ? 1 : 0;
     if (splits == 1) {
         p.c = g.c;
@@ -1154,18 +1265,42 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     // the epilogue overlaps the next tile's MMAs) for every shape: on long K it
     // measured ~1.9x the one-CTA-per-tile kernel (RCSG_TC_MODE=2 selects that one)
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
-    const bool persistent = THREE || mode != 2 || RB != 128;  // narrow-K tiles and 3M: persistent only
+    const bool persistent = THREE || CG == 2 || mode != 2 || RB != 128;  // narrow-K tiles, 3M, pairs: persistent only
     if (persistent) {
         static std::atomic<uint64_t> pconf{0};
         if (first_on_device(pconf))
-            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB, THREE>,
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB, THREE, CG>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, S::template kPBytes<E>);
         const int64_t total = tiles * splits;
         if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
-        const int grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-        launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, THREE>, dim3(grid), dim3(kPThreads), S::template kPBytes<E>,
-                   st, ar, ai, br, bi, as, bs, p, total);
+        // one CTA (pair) per SM (pair of SMs); a pair's two CTAs walk the same tiles
+        const int grid = CG * static_cast<int>(std::min<int64_t>(total, num_sms() / CG));
+        if constexpr (CG == 2) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(kPThreads);
+            cfg.dynamicSmemBytes = S::template kPBytes<E>;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            attr[1].id = cudaLaunchAttributeClusterDimension;
+            attr[1].val.clusterDim.x = 2;
+            attr[1].val.clusterDim.y = 1;
+            attr[1].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 2;
+            cudaLaunchKernelEx(&cfg, gemm_tc_persistent<BN, STAGES, E, RB, THREE, CG>, ar, ai, br, bi, as, bs, p,
+                               total);
+        } else {
+            launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, THREE>, dim3(grid), dim3(kPThreads),
+                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, p, total);
+        }
     } else {
+        static std::atomic<uint64_t> configured{0};  // function attributes are per device
+        if (first_on_device(configured))
+            cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Smem<BN, STAGES>::kBytes);
         launch_pdl(gemm_tc_kernel<BN, STAGES, E>, dim3(static_cast<unsigned>(tiles * splits)), dim3(kThreads),
                    Smem<BN, STAGES>::kBytes, st, ar, ai, br, bi, p);
     }
@@ -1240,9 +1375,36 @@ bool launch_3m(const GemmArgs& g, cudaStream_t st) {
     return true;
 }
 
+// CTA-pair tiles (cta_group::2, 256 x BN) for long-K GEMMs.  Measured
+// (profiles/r02/gemm_pair.log, fraction of the dense peak, 1-CTA -> pair):
+//   fp16 8192x8192x131072 0.71 -> 0.82 (256x256), 2048x2048x524288 0.51 -> 0.87,
+//        3604x16384x4096 0.87 -> 0.93; 8192x1024x131072 stays 1-CTA (0.88)
+//   tf32 the same long-K shapes 0.71 -> 0.79 and 0.43 -> 0.64 (256x256),
+//        3604x16384x4096 0.93 -> 0.95 and 8192x1024x131072 0.91 -> 0.97 (256x128;
+//        256x256 tiles, one TMEM buffer, lose on the shorter K)
+// RCSG_TC_PAIR: unset = this policy, 0 off, 1 = 256 x 128 tiles, 2 = 256 x 256.
+template <typename E>
+int pair_policy(const GemmArgs& g) {
+    const int64_t kb = (g.k + kbk<E, 128> - 1) / kbk<E, 128>;
+    if (g.m < 512 || g.n < 256 || kb < 32 || g.k * static_cast<int64_t>(sizeof(E)) < 512) return 0;
+    if (const char* e = getenv("RCSG_TC_PAIR")) return atoi(e);
+    if (sizeof(E) == 2) return g.n >= 2048 ? 2 : 0;
+    return (kb >= 1024 && g.n >= 2048) ? 2 : 1;
+}
+
+template <typename E>
+bool launch_pair(const GemmArgs& g, cudaStream_t st) {
+    const int mode = pair_policy<E>(g);
+    if (mode == 0) return false;
+    if (mode == 2) launch<256, 3, E, 128, false, 2>(g, st);
+    else launch<128, 4, E, 128, false, 2>(g, st);
+    return true;
+}
+
 template <typename E>
 void launch_typed(const GemmArgs& g, cudaStream_t st) {
     if (launch_3m<E>(g, st)) return;
+    if (launch_pair<E>(g, st)) return;
     static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;
     static const bool narrow_n = getenv("RCSG_TC_NARROW_N") == nullptr || atoi(getenv("RCSG_TC_NARROW_N")) != 0;
     const int64_t kb = g.k * static_cast<int64_t>(sizeof(E));  // bytes of K per row

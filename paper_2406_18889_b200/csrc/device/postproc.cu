@@ -11,8 +11,10 @@
 //      every candidate at or above the threshold to a compact buffer
 //      (warp-aggregated atomics); the same pass can draw each group's direct
 //      sample (one warp per group, sequential f64 CDF as in the reference);
-//   3. the buffer (~k entries) is radix-sorted by the descending key; runs of
-//      equal probabilities are re-ordered by lexicographic key (tie rule);
+//   3. the buffer (~k entries) is put in order: with 32-bit keys by buckets of
+//      the kept key range, each bucket ranked by one warp on the exact
+//      (prob desc, lexkey asc) order (bucket_rank_kernel); with 64-bit keys by
+//      a radix sort and a tie pass over runs of equal keys;
 //   4. the first k entries are mapped to bitstring indices.
 // The selection is exact whatever the threshold: step 2 counts every
 // candidate at or above it, and when fewer than k (or more than the buffer)
@@ -181,8 +183,13 @@ __global__ void __launch_bounds__(512) sample_hist_kernel(const double* __restri
         const double p = prob_at(src, from_amps, g * per + i);
         flag_nan(p, bad);
         const uint64_t k = asc_key(p);
-        if (level == 0) atomicAdd(&h[k >> 52], 1u);
-        else if (static_cast<uint32_t>(k >> 52) == sel0) atomicAdd(&h[(k >> 40) & 0xfff], 1u);
+        // warp-aggregated: the samples crowd into a few binades (level 0), so
+        // lanes with the same bin add once
+        const uint32_t bin = level == 0 ? static_cast<uint32_t>(k >> 52)
+                                        : (static_cast<uint32_t>(k >> 52) == sel0 ? static_cast<uint32_t>((k >> 40) & 0xfff)
+                                                                                   : 0xffffffffu);
+        const unsigned peers = __match_any_sync(__activemask(), bin);
+        if (bin != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
@@ -209,7 +216,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
                                                    unsigned long long* __restrict__ counter, uint64_t cap,
                                                    int* __restrict__ bad, const uint64_t* __restrict__ fixed,
                                                    MemberMap mm, uint64_t seed, uint64_t* __restrict__ direct_out,
-                                                   unsigned long long* __restrict__ zero_group) {
+                                                   unsigned long long* __restrict__ zero_group,
+                                                   unsigned* __restrict__ kmin_out) {
     // kept candidates are staged in shared memory (warp-aggregated shared
     // atomics) and flushed with ONE global atomic per ~1-2K entries: a global
     // atomic per warp would serialise on the single counter
@@ -225,6 +233,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
     const bool collect = thr_p != nullptr;
     const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
+    unsigned kmin = 0xffffffffu;  // smallest kept 32-bit key (= largest probability)
     auto stage = [&](bool take, double p, int64_t t) {
         const unsigned mask = __ballot_sync(0xffffffffu, take);
         if (!mask) return;
@@ -233,8 +242,16 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         base = __shfl_sync(0xffffffffu, base, 0);
         if (take) {
             const unsigned pos = base + __popc(mask & ((1u << lane) - 1));
-            s_key[pos] = sort_key<K>(p, thr);
+            const K key = sort_key<K>(p, thr);
+            s_key[pos] = key;
             s_t[pos] = static_cast<V>(t);
+            if constexpr (sizeof(K) == 4) kmin = min(kmin, static_cast<unsigned>(key));
+        }
+    };
+    auto publish_kmin = [&]() {
+        if constexpr (sizeof(K) == 4) {
+            const unsigned w = __reduce_min_sync(0xffffffffu, kmin);
+            if (lane == 0 && kmin_out && w != 0xffffffffu) atomicMin(kmin_out, w);
         }
     };
     // block-uniform: flush when fewer than `room` free slots remain (or always)
@@ -276,6 +293,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
             flush(U * blockDim.x, false);
         }
         flush(0, true);
+        publish_kmin();
         return;
     }
     // one warp per group (8 groups per block iteration, block-uniform loops):
@@ -334,6 +352,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         if (lane == 0) direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
     }
     if (collect) flush(0, true);
+    publish_kmin();
 }
 
 // Direct sampling fused with the threshold pass, for groups of <= 8192
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                                                           MemberMap mm, uint64_t seed,
                                                           uint64_t* __restrict__ direct_out,
                                                           unsigned long long* __restrict__ zero_group,
-                                                          double slack_mul) {
+                                                          double slack_mul, unsigned* __restrict__ kmin_out) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int U = 8;
     const unsigned stage_n = kDirectStage;
@@ -377,6 +396,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
     const bool collect = thr_p != nullptr;
     const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
+    unsigned kmin = 0xffffffffu;  // smallest kept 32-bit key (= largest probability)
     const int64_t tile_el = static_cast<int64_t>(gpb) * per;
     const int64_t total = n_groups * per;
     // block-uniform: flush the staged candidates when fewer than `room` slots remain (or always)
@@ -428,8 +448,10 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                         b = __shfl_sync(0xffffffffu, b, 0);
                         if (take) {
                             const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
-                            s_key[pos] = sort_key<K>(p, thr);
+                            const K key = sort_key<K>(p, thr);
+                            s_key[pos] = key;
                             s_t[pos] = static_cast<V>(t);
+                            if constexpr (sizeof(K) == 4) kmin = min(kmin, static_cast<unsigned>(key));
                         }
                     }
                 }
@@ -480,6 +502,10 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
         __syncthreads();  // the tile is reused
     }
     if (collect) flush(0, true);
+    if constexpr (sizeof(K) == 4) {
+        const unsigned w = __reduce_min_sync(0xffffffffu, kmin);
+        if (lane == 0 && kmin_out && w != 0xffffffffu) atomicMin(kmin_out, w);
+    }
 }
 
 // pad [count, cap) with the largest non-negative key; flags count < k or count > cap
@@ -545,6 +571,163 @@ __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
             const uint64_t ta = t[a];
             out[a] = member_index(mm, fixed[ta >> mm.l], ta & low);
         }
+    }
+}
+
+// ---- 3'. bucket order (32-bit keys): instead of radix-sorting every kept
+// entry, the kept range [largest key, threshold] is cut into <= 2^16 buckets
+// of equal key width (bucket 0 = highest probabilities).  One histogram pass,
+// one scan, one scatter of the entries whose bucket starts below k, then one
+// warp per such bucket ranks its entries by the exact (prob desc, lexkey asc)
+// order - recomputed from the amplitudes, so no separate tie pass - and
+// writes the output indices of ranks < k.  Buckets of > kBucketMax entries
+// (long runs of equal probabilities) take the full sort.
+constexpr int kBucketBits = 18;
+constexpr int kBuckets = 1 << kBucketBits;
+constexpr int kBucketMax = 256;
+
+__device__ __forceinline__ int bucket_shift(unsigned kmin) {
+    const unsigned span = ~kmin;  // largest kept distance above the threshold
+    return max(0, 32 - __clz(static_cast<int>(span | 1u)) - kBucketBits);
+}
+
+__global__ void bucket_hist_kernel(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ counter,
+                                   uint64_t cap, uint64_t k, const unsigned* __restrict__ kmin_p,
+                                   uint32_t* __restrict__ bcount, int* __restrict__ fail) {
+    const uint64_t cnt = *counter;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
+    const uint64_t n = min(cnt, cap);
+    const unsigned kmin = *kmin_p;
+    const int sh = bucket_shift(kmin);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(&bcount[(key[i] - kmin) >> sh], 1u);
+}
+
+// one block of 1024 threads: bstart = exclusive scan of bcount; bcount reset
+// to 0 (it becomes the scatter cursor).  Thread t owns buckets [t*per, (t+1)*per)
+// (read twice: the sums, then the prefixes; the array is L2-resident).
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict__ bcount,
+                                                           uint32_t* __restrict__ bstart) {
+    constexpr int per = kBuckets / 1024;
+    __shared__ uint32_t part[1024];
+    const int t = threadIdx.x;
+    const uint4* src = reinterpret_cast<const uint4*>(bcount + t * per);
+    uint32_t s = 0;
+#pragma unroll 4
+    for (int j = 0; j < per / 4; ++j) {
+        const uint4 v = src[j];
+        s += v.x + v.y + v.z + v.w;
+    }
+    part[t] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const uint32_t v = t >= off ? part[t - off] : 0u;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = t ? part[t - 1] : 0u;
+    uint4* cnt4 = reinterpret_cast<uint4*>(bcount + t * per);
+    uint4* out4 = reinterpret_cast<uint4*>(bstart + t * per);
+#pragma unroll 4
+    for (int j = 0; j < per / 4; ++j) {
+        const uint4 v = cnt4[j];
+        uint4 o;
+        o.x = run;
+        o.y = o.x + v.x;
+        o.z = o.y + v.y;
+        o.w = o.z + v.z;
+        run = o.w + v.w;
+        out4[j] = o;
+        cnt4[j] = make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <typename V>
+__global__ void bucket_scatter_kernel(const uint32_t* __restrict__ key, const V* __restrict__ t,
+                                      const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
+                                      const unsigned* __restrict__ kmin_p, const uint32_t* __restrict__ bstart,
+                                      uint32_t* __restrict__ bcount, V* __restrict__ out_t) {
+    const uint64_t n = min(static_cast<uint64_t>(*counter), cap);
+    const unsigned kmin = *kmin_p;
+    const int sh = bucket_shift(kmin);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t b = (key[i] - kmin) >> sh;
+        const uint32_t s0 = bstart[b];
+        if (s0 >= k) continue;  // every rank of this bucket is >= k
+        out_t[s0 + atomicAdd(&bcount[b], 1u)] = t[i];
+    }
+}
+
+// One warp per bucket, warps striding over the buckets in order (bstart is
+// non-decreasing, so a warp stops at the first bucket starting at or past k).
+// rank = number of the bucket's entries ahead in (desc key of the exact
+// probability, lexicographic key, candidate position) order: a strict total
+// order (duplicate groups give equal bitstrings; they take consecutive ranks).
+template <typename V>
+__global__ void __launch_bounds__(256) bucket_rank_kernel(const V* __restrict__ t, const uint32_t* __restrict__ bstart,
+                                                          const uint32_t* __restrict__ bcount, uint64_t k,
+                                                          const double* __restrict__ src, int from_amps,
+                                                          const uint64_t* __restrict__ fixed, MemberMap mm,
+                                                          int* __restrict__ fail, uint64_t* __restrict__ out) {
+    __shared__ uint64_t s_full[8][kBucketMax];
+    __shared__ uint64_t s_idx[8][kBucketMax];
+    __shared__ V s_t[8][kBucketMax];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t low = (1ull << mm.l) - 1;
+    auto load = [&](uint32_t s0, uint32_t i, uint64_t& full, uint64_t& idx, V& ti) {
+        ti = t[s0 + i];
+        full = ~asc_key(prob_at(src, from_amps, static_cast<int64_t>(ti)));
+        idx = member_index(mm, fixed[ti >> mm.l], ti & low);
+    };
+    auto before = [](uint64_t fa, uint64_t la, V ta, uint64_t fb, uint64_t lb, V tb) {
+        return fa < fb || (fa == fb && (la < lb || (la == lb && ta < tb)));
+    };
+    const uint32_t n_warps = gridDim.x * 8;
+    for (uint32_t b = blockIdx.x * 8 + w; b < static_cast<uint32_t>(kBuckets); b += n_warps) {
+        const uint32_t s0 = bstart[b];
+        if (s0 >= k) break;
+        const uint32_t n = bcount[b];
+        if (n == 0) continue;
+        if (n > static_cast<uint32_t>(kBucketMax)) {  // a long run of equal keys: full sort
+            if (lane == 0) atomicExch(fail, 2);
+            break;
+        }
+        if (n == 1) {
+            if (lane == 0) {
+                const V ti = t[s0];
+                out[s0] = member_index(mm, fixed[ti >> mm.l], ti & low);
+            }
+            continue;
+        }
+        if (n <= 32) {  // in registers: n shuffle rounds
+            uint64_t full = ~0ull, idx = 0;
+            V ti = 0;
+            if (lane < static_cast<int>(n)) load(s0, lane, full, idx, ti);
+            const uint64_t lex = lex_key(idx, mm.n);
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint64_t fj = __shfl_sync(0xffffffffu, full, j);
+                const uint64_t lj = __shfl_sync(0xffffffffu, lex, j);
+                const V tj = __shfl_sync(0xffffffffu, ti, j);
+                rank += before(fj, lj, tj, full, lex, ti) ? 1u : 0u;
+            }
+            if (lane < static_cast<int>(n) && s0 + rank < k) out[s0 + rank] = idx;
+            continue;
+        }
+        for (uint32_t i = lane; i < n; i += 32) load(s0, i, s_full[w][i], s_idx[w][i], s_t[w][i]);
+        __syncwarp();
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint64_t f = s_full[w][i], lx = lex_key(s_idx[w][i], mm.n);
+            const V ti = s_t[w][i];
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < n; ++j)
+                rank += before(s_full[w][j], lex_key(s_idx[w][j], mm.n), s_t[w][j], f, lx, ti) ? 1u : 0u;
+            if (s0 + rank < k) out[s0 + rank] = s_idx[w][i];
+        }
+        __syncwarp();
     }
 }
 
@@ -666,7 +849,7 @@ cudaStream_t post_stream() {
 }
 
 enum Slot {
-    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb
+    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb, kBucket
 };
 
 struct Counters {  // device-side control block
@@ -677,6 +860,7 @@ struct Counters {  // device-side control block
     int bad;   // NaN probability seen
     int fail;  // fast path unusable
     int xbad;  // invalid ideal probability
+    unsigned kmin;  // smallest kept 32-bit sort key (bucket range)
     double xsum[2];
 };
 
@@ -727,7 +911,7 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     CUDA_OK(cudaMemcpyAsync(d_fixed, cs.group_fixed, G * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     Counters* d_ctl = scratch_as<Counters>(kCounters, 1);
     {
-        const Counters init{0, ULLONG_MAX, 0, {0, 0}, 0, 0, 0, {0, 0}};
+        const Counters init{0, ULLONG_MAX, 0, {0, 0}, 0, 0, 0, 0xffffffffu, {0, 0}};
         CUDA_OK(cudaMemcpyAsync(d_ctl, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
     }
     uint64_t* d_direct = want_direct ? scratch_as<uint64_t>(kDirect, G) : nullptr;
@@ -793,27 +977,45 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
                 std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, static_cast<int64_t>(n_sm) * std::max(occ, 1))));
             direct_scan_kernel<K, V><<<grid, 256, smem, st>>>(d_src, from_amps, G, cs.l, gpb, thr, kk, tt,
                                                               &d_ctl->count, cap, &d_ctl->bad, d_fixed, mm, seed,
-                                                              d_direct, &d_ctl->zero_group, slack_mul);
+                                                              d_direct, &d_ctl->zero_group, slack_mul, &d_ctl->kmin);
         } else if (want_direct) {
             const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
             scan_kernel<true, K, V><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count, cap,
                                                           &d_ctl->bad, d_fixed, mm, seed, d_direct,
-                                                          &d_ctl->zero_group);
+                                                          &d_ctl->zero_group, &d_ctl->kmin);
         } else {
             scan_kernel<false, K, V><<<148 * 8, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count,
                                                               cap, &d_ctl->bad, d_fixed, mm, seed, d_direct,
-                                                              &d_ctl->zero_group);
+                                                              &d_ctl->zero_group, &d_ctl->kmin);
         }
     };
     if (fast || want_direct) {
         if (narrow) scan(uint32_t{0}, uint32_t{0});
         else scan(uint64_t{0}, uint64_t{0});
     }
+    // RCSG_TOPK_BUCKETS=1: bucket order instead of the radix sort + tie pass (32-bit keys)
+    const bool bucket_off = !(getenv("RCSG_TOPK_BUCKETS") && atoi(getenv("RCSG_TOPK_BUCKETS")) == 1);
     auto select_fast = [&](auto kz, auto vz) {
         using K = decltype(kz);
         using V = decltype(vz);
         K* ka = static_cast<K*>(keys);
         V* ta = static_cast<V*>(ts);
+        if constexpr (sizeof(K) == 4) {
+            if (!bucket_off) {  // bucket order (see bucket_rank_kernel)
+                uint32_t* bcount = scratch_as<uint32_t>(kBucket, 2 * kBuckets);
+                uint32_t* bstart = bcount + kBuckets;
+                V* tb = static_cast<V*>(scratch(kTB, cap * sizeof(V)));
+                CUDA_OK(cudaMemsetAsync(bcount, 0, kBuckets * sizeof(uint32_t), st));
+                const int g = grid_for(static_cast<int64_t>(cap), 256);
+                bucket_hist_kernel<<<g, 256, 0, st>>>(ka, &d_ctl->count, cap, k, &d_ctl->kmin, bcount, &d_ctl->fail);
+                bucket_scan_kernel<<<1, 1024, 0, st>>>(bcount, bstart);
+                bucket_scatter_kernel<V><<<g, 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k, &d_ctl->kmin, bstart,
+                                                            bcount, tb);
+                bucket_rank_kernel<V><<<148 * 8, 256, 0, st>>>(tb, bstart, bcount, k, d_src, from_amps, d_fixed, mm,
+                                                               &d_ctl->fail, d_top);
+                return;
+            }
+        }
         pad_kernel<K, V><<<grid_for(static_cast<int64_t>(cap), 256), 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k,
                                                                                  &d_ctl->fail);
         K* kb = static_cast<K*>(scratch(kKeyB, cap * sizeof(K)));

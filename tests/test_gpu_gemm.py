@@ -28,6 +28,16 @@ CASES = [
     # 8 m n k >= 2.7e11, k >= 512, n >= 64: the 3M path (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi))
     ("3m-n1024", 4096, 1024, 8192, [], []),
     ("3m-n64-scatter", 1 << 14, 64, 32768, [7, 8, 9, 10, 11, 12, 13] + list(range(0, 7)), list(range(14, 20))),
+    # CTA-pair tiles (cta_group::2; pair1 = 256 x 128, pair2 = 256 x 256): plain, scatter
+    # output, an M tail that leaves the peer CTA without rows, and split K
+    ("pair1-plain", 1024, 512, 4096, [], []),
+    ("pair2-plain", 1024, 512, 4096, [], []),
+    ("pair1-scatter", 1 << 12, 256, 2048, [7, 8, 9, 10, 11, 12, 13, 0, 1, 2, 3, 4], [5, 6] + list(range(14, 20))),
+    ("pair2-scatter", 1 << 12, 256, 2048, [7, 8, 9, 10, 11, 12, 13, 0, 1, 2, 3, 4], [5, 6] + list(range(14, 20))),
+    ("pair1-mtail", 1000, 768, 2048, [], []),
+    ("pair2-mtail", 1000, 768, 2048, [], []),
+    ("pair1-splitk", 512, 256, 65536, [], []),
+    ("pair2-splitk", 512, 256, 65536, [], []),
 ]
 
 
@@ -36,6 +46,8 @@ CASES = [
 def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol, monkeypatch):
     if name.startswith("3m"):
         monkeypatch.setenv("RCSG_TC_3M", "1")  # the opt-in 3M kernel
+    if name.startswith("pair"):
+        monkeypatch.setenv("RCSG_TC_PAIR", name[4])
     lib = _native.testkit()
     check = {"f16": lib.rcsg_gemm_check_f16, "bf16": lib.rcsg_gemm_check_bf16, "tf32": lib.rcsg_gemm_check_tf32}[dtype]
     a = (C.c_int8 * max(len(mp), 1))(*mp)

@@ -25,10 +25,15 @@ def device_amps(M, l, seed, quantize=None):
 
 
 @pytest.mark.parametrize("k", [1, 100, 4096, 65536])
-@pytest.mark.parametrize("path", ["auto", "1", "2"])
+@pytest.mark.parametrize("path", ["auto", "1", "2", "radix", "buckets"])
 def test_topk_threshold_select_matches_reference(k, path, monkeypatch):
+    """path 1: threshold select, 2: full sort; radix / buckets: threshold
+    select ordered by the radix sort + tie pass or by the bucket ranks
+    (RCSG_TOPK_BUCKETS=0 / 1)."""
     n, oq, M, l = 30, [0, 1, 2, 3, 4, 5], 4096, 6
-    if path != "auto":
+    if path in ("radix", "buckets"):
+        monkeypatch.setenv("RCSG_TOPK_BUCKETS", "0" if path == "radix" else "1")
+    elif path != "auto":
         monkeypatch.setenv("RCSG_TOPK_PATH", path)
     fixed, _ = pb.build_candidate_set(n, oq, M, 1234)
     a, probs = device_amps(M, l, k)
@@ -41,10 +46,12 @@ def test_topk_threshold_select_matches_reference(k, path, monkeypatch):
     assert np.array_equal(pb.api.top_k_from_device_amps(n, oq, fixed, a.data_ptr(), k), want)
 
 
+@pytest.mark.parametrize("order", ["radix", "buckets"])
 @pytest.mark.parametrize("quant", [2.0**14, 2.0**11])
-def test_topk_ties_short_and_long_runs(quant, monkeypatch):
+def test_topk_ties_short_and_long_runs(quant, order, monkeypatch):
     """Quantised amplitudes give runs of equal probabilities: short runs are
     reordered in place, runs above 256 entries fall back to the full sort."""
+    monkeypatch.setenv("RCSG_TOPK_BUCKETS", "0" if order == "radix" else "1")
     n, oq, M, l = 24, [2, 5, 7], 8192, 3
     fixed, _ = pb.build_candidate_set(n, oq, M, 99)
     a, probs = device_amps(M, l, 7, quantize=quant)
@@ -90,8 +97,10 @@ def test_device_xeb_against_statevector(ref):
         assert abs(pb.api.xeb_state(n, samples, state.data_ptr()) - want) <= 1e-12 * max(1.0, abs(want))
 
 
-def test_errors_nan_zero_group_and_signed_zero(ref):
+@pytest.mark.parametrize("order", ["radix", "buckets"])
+def test_errors_nan_zero_group_and_signed_zero(ref, order, monkeypatch):
     import torch
+    monkeypatch.setenv("RCSG_TOPK_BUCKETS", "0" if order == "radix" else "1")
     n, oq = 8, [0, 1]
     fixed, _ = pb.build_candidate_set(n, oq, 16, 1)
     a = torch.zeros(16 * 4, 2, dtype=torch.float64, device="cuda")
