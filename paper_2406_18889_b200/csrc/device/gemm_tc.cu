@@ -296,6 +296,8 @@ struct TcParams {
                             // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
                             // flight read the same shared-operand panels (see coord_at)
     int32_t tm;             // persistent kernel: rows per tile (128, or 256 for a CTA pair)
+    int32_t sleepy;         // persistent kernel: producer / MMA threads wait with a suspend-time hint
+                            // (they stop competing for issue slots with the epilogue warps)
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
                             // with row-fast lanes, 3 row runs (see store_chunk_staged)
 };
@@ -913,7 +915,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int bv = p.ib ? p.ib[c.v] : (p.b_batched ? static_cast<int>(c.v) : 0);
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
                     const int s = it % STAGES;
-                    if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                    if (it >= STAGES) {
+                        if (p.sleepy) mbar_wait_sleep(&empty[s], ((it / STAGES) - 1) & 1);
+                        else mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                    }
                     uint8_t* st = smem + s * S::kStage;
                     const int kc = static_cast<int>(c.k_begin) + kb * kbk<E, RB>;
                     if constexpr (CG == 2) {
@@ -953,12 +958,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int64_t t = unit; t < total_tiles; t += n_units, ++j, ti.next()) {
                 const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
                 const uint32_t ab = j % NBUF;
-                if (j >= NBUF) mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
+                if (j >= NBUF) {
+                    if (p.sleepy) mbar_wait_sleep(&tempty[ab], ((j / NBUF) - 1) & 1);
+                    else mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
+                }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t t_re = tmem + ab * NPL * BN, t_im = t_re + BN;  // 3M: T1, T2 (, T3 = t_re + 2 BN)
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
                     const int s = it % STAGES;
-                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    if (p.sleepy) mbar_wait_sleep(&full[s], (it / STAGES) & 1);
+                    else mbar_wait(&full[s], (it / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint8_t* st = smem + s * S::kStage;
                     const uint8_t* sb = st + NPL * S::kATile;
@@ -1206,6 +1215,16 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     p.round_tf32 = g.round_tf32;
     p.epi = sizeof(E) == 2 ? epilogue_kind(g.om, g.n) : epilogue_kind4(g.om, g.n);
     if (const char* e = getenv("RCSG_TC_NO_STAGE")) if (atoi(e)) p.epi = 0;
+    p.sleepy = getenv("RCSG_TC_SLEEPY") ? atoi(getenv("RCSG_TC_SLEEPY")) : 0;
+    if (getenv("RCSG_DUMP_EPI")) {  // diagnostics: the output layout of every tcgen05 GEMM
+        fprintf(stderr, "[rcsg-epi] m=%lld n=%lld k=%lld batch=%lld elem=%d epi=%d scatter=%d m_pos:",
+                (long long)g.m, (long long)g.n, (long long)g.k, (long long)g.batch, (int)sizeof(E), p.epi,
+                g.om.scatter);
+        for (int j = 0; j < g.om.m_bits; ++j) fprintf(stderr, " %d", g.om.m_pos[j]);
+        fprintf(stderr, " n_pos:");
+        for (int j = 0; j < g.om.n_bits; ++j) fprintf(stderr, " %d", g.om.n_pos[j]);
+        fprintf(stderr, "\n");
+    }
     const int64_t tiles = p.mt * p.nt * g.batch;
     const int64_t kblocks = (g.k + kbk<E, RB> - 1) / kbk<E, RB>;
     // split K until the grid covers the machine (>= ~2 waves of 148 SMs), keeping >= 8 k-blocks per split;

@@ -4,7 +4,7 @@
 //   linear XEB over the ideal probabilities of the samples            (:62-73)
 //
 // Top-k is a threshold select, not a sort of every candidate:
-//   1. two sampled histogram passes (1/32 of the groups each) over the
+//   1. two sampled histogram passes (1/32 - 1/256 of the groups) over the
 //      order-preserving 64-bit key of the probability pick a threshold key
 //      expected to keep ~1.05 k candidates (binade, then 2^-12 of a binade);
 //   2. ONE streaming pass over all M * 2^l amplitudes (16 B each) appends
@@ -162,6 +162,14 @@ __device__ void pick_threshold_block(const uint32_t* __restrict__ hist, int leve
     }
 }
 
+// The sample: runs of kSampleRun consecutive groups, one run in every
+// kSampleRun * stride groups (contiguous reads; 1/stride of the groups)
+constexpr int64_t kSampleRun = 32;
+__host__ __device__ __forceinline__ int64_t sampled_groups(int64_t n_groups, int64_t stride) {
+    const int64_t period = kSampleRun * stride, full = n_groups / period, rem = n_groups - full * period;
+    return full * kSampleRun + (rem < kSampleRun ? rem : kSampleRun);
+}
+
 // hist: 2 x kHistBins bins, then one completion counter per level (zeroed by the caller)
 __global__ void __launch_bounds__(512) sample_hist_kernel(const double* __restrict__ src, int from_amps,
                                                           int64_t n_groups, int l, int64_t stride, int level,
@@ -174,22 +182,35 @@ __global__ void __launch_bounds__(512) sample_hist_kernel(const double* __restri
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     const int64_t per = int64_t{1} << l;
-    const int64_t n_s = (n_groups + stride - 1) / stride;
+    const int64_t n_s = sampled_groups(n_groups, stride);
     const int64_t n_el = n_s * per;
     const uint32_t sel0 = level ? __ldcg(sel) : 0;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_el;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t g = (e >> l) * stride, i = e & (per - 1);
-        const double p = prob_at(src, from_amps, g * per + i);
-        flag_nan(p, bad);
-        const uint64_t k = asc_key(p);
-        // warp-aggregated: the samples crowd into a few binades (level 0), so
-        // lanes with the same bin add once
-        const uint32_t bin = level == 0 ? static_cast<uint32_t>(k >> 52)
-                                        : (static_cast<uint32_t>(k >> 52) == sel0 ? static_cast<uint32_t>((k >> 40) & 0xfff)
-                                                                                   : 0xffffffffu);
-        const unsigned peers = __match_any_sync(__activemask(), bin);
-        if (bin != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
+    // U independent loads per thread in flight
+    constexpr int U = 4;
+    const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e0 < n_el; e0 += U * gs) {
+        double pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * gs;
+            const int64_t j = e >> l;  // sampled group ordinal -> group (runs of kSampleRun groups)
+            const int64_t g = (j / kSampleRun) * kSampleRun * stride + (j % kSampleRun);
+            pv[u] = e < n_el ? prob_at(src, from_amps, g * per + (e & (per - 1))) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool in = e0 + u * gs < n_el;
+            if (in) flag_nan(pv[u], bad);
+            const uint64_t k = asc_key(pv[u]);
+            // warp-aggregated: the samples crowd into a few binades (level 0), so
+            // lanes with the same bin add once
+            uint32_t bin = level == 0 ? static_cast<uint32_t>(k >> 52)
+                                      : (static_cast<uint32_t>(k >> 52) == sel0 ? static_cast<uint32_t>((k >> 40) & 0xfff)
+                                                                                 : 0xffffffffu);
+            if (!in) bin = 0xffffffffu;
+            const unsigned peers = __match_any_sync(__activemask(), bin);
+            if (bin != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
@@ -201,6 +222,19 @@ __global__ void __launch_bounds__(512) sample_hist_kernel(const double* __restri
     if (!last) return;
     __threadfence();
     pick_threshold_block(hist, level, want, sel, thr, part);
+}
+
+// warp minimum of the kept keys, one atomic per warp (whole warp converged)
+template <typename K>
+__device__ __forceinline__ void publish_min(K v, K* out, int lane) {
+    if constexpr (sizeof(K) == 4) {
+        v = __reduce_min_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    if (lane == 0 && out && v != ~K{0})
+        atomicMin(reinterpret_cast<std::conditional_t<sizeof(K) == 4, unsigned, unsigned long long>*>(out), v);
 }
 
 // ---- 2. the streaming pass ----------------------------------------------------
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
                                                    int* __restrict__ bad, const uint64_t* __restrict__ fixed,
                                                    MemberMap mm, uint64_t seed, uint64_t* __restrict__ direct_out,
                                                    unsigned long long* __restrict__ zero_group,
-                                                   unsigned* __restrict__ kmin_out) {
+                                                   K* __restrict__ kmin_out) {
     // kept candidates are staged in shared memory (warp-aggregated shared
     // atomics) and flushed with ONE global atomic per ~1-2K entries: a global
     // atomic per warp would serialise on the single counter
@@ -233,7 +267,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
     const bool collect = thr_p != nullptr;
     const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
-    unsigned kmin = 0xffffffffu;  // smallest kept 32-bit key (= largest probability)
+    K kmin = ~K{0};  // smallest kept key (= largest probability)
     auto stage = [&](bool take, double p, int64_t t) {
         const unsigned mask = __ballot_sync(0xffffffffu, take);
         if (!mask) return;
@@ -245,15 +279,10 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
             const K key = sort_key<K>(p, thr);
             s_key[pos] = key;
             s_t[pos] = static_cast<V>(t);
-            if constexpr (sizeof(K) == 4) kmin = min(kmin, static_cast<unsigned>(key));
+            kmin = min(kmin, key);
         }
     };
-    auto publish_kmin = [&]() {
-        if constexpr (sizeof(K) == 4) {
-            const unsigned w = __reduce_min_sync(0xffffffffu, kmin);
-            if (lane == 0 && kmin_out && w != 0xffffffffu) atomicMin(kmin_out, w);
-        }
-    };
+    auto publish_kmin = [&]() { publish_min<K>(kmin, kmin_out, lane); };
     // block-uniform: flush when fewer than `room` free slots remain (or always)
     auto flush = [&](unsigned room, bool force) {
         __syncthreads();
@@ -380,7 +409,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                                                           MemberMap mm, uint64_t seed,
                                                           uint64_t* __restrict__ direct_out,
                                                           unsigned long long* __restrict__ zero_group,
-                                                          double slack_mul, unsigned* __restrict__ kmin_out) {
+                                                          double slack_mul, K* __restrict__ kmin_out) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int U = 8;
     const unsigned stage_n = kDirectStage;
@@ -396,7 +425,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
     const bool collect = thr_p != nullptr;
     const uint64_t thr = collect ? *thr_p : ~0ull;
     const int lane = threadIdx.x & 31;
-    unsigned kmin = 0xffffffffu;  // smallest kept 32-bit key (= largest probability)
+    K kmin = ~K{0};  // smallest kept key (= largest probability)
     const int64_t tile_el = static_cast<int64_t>(gpb) * per;
     const int64_t total = n_groups * per;
     // block-uniform: flush the staged candidates when fewer than `room` slots remain (or always)
@@ -451,7 +480,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                             const K key = sort_key<K>(p, thr);
                             s_key[pos] = key;
                             s_t[pos] = static_cast<V>(t);
-                            if constexpr (sizeof(K) == 4) kmin = min(kmin, static_cast<unsigned>(key));
+                            kmin = min(kmin, key);
                         }
                     }
                 }
@@ -502,10 +531,7 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
         __syncthreads();  // the tile is reused
     }
     if (collect) flush(0, true);
-    if constexpr (sizeof(K) == 4) {
-        const unsigned w = __reduce_min_sync(0xffffffffu, kmin);
-        if (lane == 0 && kmin_out && w != 0xffffffffu) atomicMin(kmin_out, w);
-    }
+    publish_min<K>(kmin, kmin_out, lane);
 }
 
 // pad [count, cap) with the largest non-negative key; flags count < k or count > cap
@@ -574,160 +600,134 @@ __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
     }
 }
 
-// ---- 3'. bucket order (32-bit keys): instead of radix-sorting every kept
-// entry, the kept range [largest key, threshold] is cut into <= 2^16 buckets
-// of equal key width (bucket 0 = highest probabilities).  One histogram pass,
-// one scan, one scatter of the entries whose bucket starts below k, then one
-// warp per such bucket ranks its entries by the exact (prob desc, lexkey asc)
-// order - recomputed from the amplitudes, so no separate tie pass - and
-// writes the output indices of ranks < k.  Buckets of > kBucketMax entries
-// (long runs of equal probabilities) take the full sort.
+// ---- 3'. bucket order: instead of radix-sorting every kept entry, the kept
+// key range [largest probability, threshold] is cut into 2^18 buckets of
+// equal width in the 64-bit descending key (bucket 0 = highest probabilities):
+//   hist     counts per bucket (bcount, zero on entry);
+//   scan     bstart = exclusive sum (cub), bstart[kBuckets] = total;
+//   scatter  entries of buckets starting below k go to their bucket's range
+//            (key, candidate, bucket); every entry decrements its bucket's
+//            count, so bcount is zero again for the next call;
+//   rank     one thread per placed entry counts the entries of its bucket
+//            ahead of it in (prob desc, lexkey asc, candidate position) order -
+//            a strict total order: the exact key decides unless equal, so the
+//            bitstring keys are computed only for ties - and writes its
+//            bitstring index at bucket start + rank when that is below k.
+// Buckets of more than kBucketMax entries (long runs of equal probabilities)
+// take the full sort.  The scan pass writes the full 64-bit keys for this
+// path, so nothing re-reads the amplitudes.
 constexpr int kBucketBits = 18;
 constexpr int kBuckets = 1 << kBucketBits;
-constexpr int kBucketMax = 256;
+constexpr uint32_t kBucketMax = 4096;
 
-__device__ __forceinline__ int bucket_shift(unsigned kmin) {
-    const unsigned span = ~kmin;  // largest kept distance above the threshold
-    return max(0, 32 - __clz(static_cast<int>(span | 1u)) - kBucketBits);
+// keys lie in [kmin, ~thr]; shift so that the span fits kBucketBits
+__device__ __forceinline__ int bucket_shift(uint64_t kmin, uint64_t thr) {
+    const uint64_t span = ~thr - kmin;
+    return max(0, 64 - __clzll(static_cast<long long>(span | 1)) - kBucketBits);
 }
 
-__global__ void bucket_hist_kernel(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ counter,
-                                   uint64_t cap, uint64_t k, const unsigned* __restrict__ kmin_p,
-                                   uint32_t* __restrict__ bcount, int* __restrict__ fail) {
+__global__ void bucket_hist_kernel(const uint64_t* __restrict__ key, const unsigned long long* __restrict__ counter,
+                                   uint64_t cap, uint64_t k, const unsigned long long* __restrict__ kmin_p,
+                                   const uint64_t* __restrict__ thr_p, uint32_t* __restrict__ bcount,
+                                   int* __restrict__ fail) {
     const uint64_t cnt = *counter;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
     const uint64_t n = min(cnt, cap);
-    const unsigned kmin = *kmin_p;
-    const int sh = bucket_shift(kmin);
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        atomicAdd(&bcount[(key[i] - kmin) >> sh], 1u);
-}
-
-// one block of 1024 threads: bstart = exclusive scan of bcount; bcount reset
-// to 0 (it becomes the scatter cursor).  Thread t owns buckets [t*per, (t+1)*per)
-// (read twice: the sums, then the prefixes; the array is L2-resident).
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict__ bcount,
-                                                           uint32_t* __restrict__ bstart) {
-    constexpr int per = kBuckets / 1024;
-    __shared__ uint32_t part[1024];
-    const int t = threadIdx.x;
-    const uint4* src = reinterpret_cast<const uint4*>(bcount + t * per);
-    uint32_t s = 0;
-#pragma unroll 4
-    for (int j = 0; j < per / 4; ++j) {
-        const uint4 v = src[j];
-        s += v.x + v.y + v.z + v.w;
-    }
-    part[t] = s;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        const uint32_t v = t >= off ? part[t - off] : 0u;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
-    }
-    uint32_t run = t ? part[t - 1] : 0u;
-    uint4* cnt4 = reinterpret_cast<uint4*>(bcount + t * per);
-    uint4* out4 = reinterpret_cast<uint4*>(bstart + t * per);
-#pragma unroll 4
-    for (int j = 0; j < per / 4; ++j) {
-        const uint4 v = cnt4[j];
-        uint4 o;
-        o.x = run;
-        o.y = o.x + v.x;
-        o.z = o.y + v.y;
-        o.w = o.z + v.z;
-        run = o.w + v.w;
-        out4[j] = o;
-        cnt4[j] = make_uint4(0, 0, 0, 0);
+    const uint64_t kmin = *kmin_p;
+    const int sh = bucket_shift(kmin, *thr_p);
+    const uint64_t gs = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * gs) {
+        uint64_t kk[4];  // 4 independent entries per thread in flight
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kk[u] = i0 + u * gs < n ? key[i0 + u * gs] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * gs < n) atomicAdd(&bcount[(kk[u] - kmin) >> sh], 1u);
     }
 }
 
 template <typename V>
-__global__ void bucket_scatter_kernel(const uint32_t* __restrict__ key, const V* __restrict__ t,
+__global__ void bucket_scatter_kernel(const uint64_t* __restrict__ key, const V* __restrict__ t,
                                       const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
-                                      const unsigned* __restrict__ kmin_p, const uint32_t* __restrict__ bstart,
-                                      uint32_t* __restrict__ bcount, V* __restrict__ out_t) {
+                                      const unsigned long long* __restrict__ kmin_p, const uint64_t* __restrict__ thr_p,
+                                      const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcount,
+                                      uint64_t* __restrict__ out_key, V* __restrict__ out_t,
+                                      uint32_t* __restrict__ out_b) {
     const uint64_t n = min(static_cast<uint64_t>(*counter), cap);
-    const unsigned kmin = *kmin_p;
-    const int sh = bucket_shift(kmin);
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t b = (key[i] - kmin) >> sh;
-        const uint32_t s0 = bstart[b];
-        if (s0 >= k) continue;  // every rank of this bucket is >= k
-        out_t[s0 + atomicAdd(&bcount[b], 1u)] = t[i];
+    const uint64_t kmin = *kmin_p;
+    const int sh = bucket_shift(kmin, *thr_p);
+    const uint64_t gs = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * gs) {
+        // 4 independent entries per thread in flight (key -> bucket start -> slot)
+        uint64_t kk[4];
+        uint32_t b[4], s0[4], pos[4];
+        V tv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool in = i0 + u * gs < n;
+            kk[u] = in ? key[i0 + u * gs] : kmin;
+            tv[u] = in ? t[i0 + u * gs] : V{0};
+            b[u] = static_cast<uint32_t>((kk[u] - kmin) >> sh);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s0[u] = bstart[b[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)  // any order inside the bucket
+            pos[u] = i0 + u * gs < n ? s0[u] + atomicSub(&bcount[b[u]], 1u) - 1u : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i0 + u * gs >= n || s0[u] >= k) continue;  // every rank of the bucket is >= k
+            out_key[pos[u]] = kk[u];
+            out_t[pos[u]] = tv[u];
+            out_b[pos[u]] = b[u];
+        }
     }
 }
 
-// One warp per bucket, warps striding over the buckets in order (bstart is
-// non-decreasing, so a warp stops at the first bucket starting at or past k).
-// rank = number of the bucket's entries ahead in (desc key of the exact
-// probability, lexicographic key, candidate position) order: a strict total
-// order (duplicate groups give equal bitstrings; they take consecutive ranks).
 template <typename V>
-__global__ void __launch_bounds__(256) bucket_rank_kernel(const V* __restrict__ t, const uint32_t* __restrict__ bstart,
-                                                          const uint32_t* __restrict__ bcount, uint64_t k,
-                                                          const double* __restrict__ src, int from_amps,
-                                                          const uint64_t* __restrict__ fixed, MemberMap mm,
-                                                          int* __restrict__ fail, uint64_t* __restrict__ out) {
-    __shared__ uint64_t s_full[8][kBucketMax];
-    __shared__ uint64_t s_idx[8][kBucketMax];
-    __shared__ V s_t[8][kBucketMax];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__global__ void bucket_rank_kernel(const uint64_t* __restrict__ key, const V* __restrict__ t,
+                                   const uint32_t* __restrict__ bid, const uint32_t* __restrict__ bstart,
+                                   const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
+                                   const uint64_t* __restrict__ fixed, MemberMap mm, int* __restrict__ fail,
+                                   uint64_t* __restrict__ out) {
+    const uint64_t n = min(static_cast<uint64_t>(*counter), cap);
+    if (n < k) return;  // the call falls back to the full sort
     const uint64_t low = (1ull << mm.l) - 1;
-    auto load = [&](uint32_t s0, uint32_t i, uint64_t& full, uint64_t& idx, V& ti) {
-        ti = t[s0 + i];
-        full = ~asc_key(prob_at(src, from_amps, static_cast<int64_t>(ti)));
-        idx = member_index(mm, fixed[ti >> mm.l], ti & low);
-    };
-    auto before = [](uint64_t fa, uint64_t la, V ta, uint64_t fb, uint64_t lb, V tb) {
-        return fa < fb || (fa == fb && (la < lb || (la == lb && ta < tb)));
-    };
-    const uint32_t n_warps = gridDim.x * 8;
-    for (uint32_t b = blockIdx.x * 8 + w; b < static_cast<uint32_t>(kBuckets); b += n_warps) {
-        const uint32_t s0 = bstart[b];
-        if (s0 >= k) break;
-        const uint32_t n = bcount[b];
-        if (n == 0) continue;
-        if (n > static_cast<uint32_t>(kBucketMax)) {  // a long run of equal keys: full sort
-            if (lane == 0) atomicExch(fail, 2);
-            break;
-        }
-        if (n == 1) {
-            if (lane == 0) {
-                const V ti = t[s0];
-                out[s0] = member_index(mm, fixed[ti >> mm.l], ti & low);
-            }
+    // positions >= k matter only inside the bucket that straddles k
+    const uint64_t end = bstart[bid[k - 1] + 1];
+    for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < end;
+         p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t b = bid[p];
+        const uint32_t s0 = bstart[b], nb = bstart[b + 1] - s0;
+        const V tp = t[p];
+        if (nb > kBucketMax) {  // a long run of equal keys: full sort
+            atomicExch(fail, 2);
             continue;
         }
-        if (n <= 32) {  // in registers: n shuffle rounds
-            uint64_t full = ~0ull, idx = 0;
-            V ti = 0;
-            if (lane < static_cast<int>(n)) load(s0, lane, full, idx, ti);
-            const uint64_t lex = lex_key(idx, mm.n);
-            uint32_t rank = 0;
-            for (uint32_t j = 0; j < n; ++j) {
-                const uint64_t fj = __shfl_sync(0xffffffffu, full, j);
-                const uint64_t lj = __shfl_sync(0xffffffffu, lex, j);
-                const V tj = __shfl_sync(0xffffffffu, ti, j);
-                rank += before(fj, lj, tj, full, lex, ti) ? 1u : 0u;
+        const uint64_t kp = key[p];
+        uint32_t rank = 0, ties = 0;
+        const uint32_t e = s0 + nb;
+        uint32_t j = s0;
+        for (; j + 4 <= e; j += 4) {  // 4 loads in flight
+            const uint64_t k0 = key[j], k1 = key[j + 1], k2 = key[j + 2], k3 = key[j + 3];
+            rank += (k0 < kp) + (k1 < kp) + (k2 < kp) + (k3 < kp);
+            ties += (k0 == kp) + (k1 == kp) + (k2 == kp) + (k3 == kp);
+        }
+        for (; j < e; ++j) {
+            const uint64_t kj = key[j];
+            rank += kj < kp;
+            ties += kj == kp;
+        }
+        if (ties > 1) {  // equal probabilities (besides itself): lexicographic key, then position
+            const uint64_t lx = lex_key(member_index(mm, fixed[tp >> mm.l], tp & low), mm.n);
+            for (j = s0; j < e; ++j) {
+                if (key[j] != kp || j == p) continue;
+                const V tj = t[j];
+                const uint64_t lj = lex_key(member_index(mm, fixed[tj >> mm.l], tj & low), mm.n);
+                rank += (lj < lx || (lj == lx && tj < tp)) ? 1u : 0u;
             }
-            if (lane < static_cast<int>(n) && s0 + rank < k) out[s0 + rank] = idx;
-            continue;
         }
-        for (uint32_t i = lane; i < n; i += 32) load(s0, i, s_full[w][i], s_idx[w][i], s_t[w][i]);
-        __syncwarp();
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint64_t f = s_full[w][i], lx = lex_key(s_idx[w][i], mm.n);
-            const V ti = s_t[w][i];
-            uint32_t rank = 0;
-            for (uint32_t j = 0; j < n; ++j)
-                rank += before(s_full[w][j], lex_key(s_idx[w][j], mm.n), s_t[w][j], f, lx, ti) ? 1u : 0u;
-            if (s0 + rank < k) out[s0 + rank] = s_idx[w][i];
-        }
-        __syncwarp();
+        if (s0 + rank < k) out[s0 + rank] = member_index(mm, fixed[tp >> mm.l], tp & low);
     }
 }
 
@@ -849,8 +849,17 @@ cudaStream_t post_stream() {
 }
 
 enum Slot {
-    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb, kBucket
+    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb, kBucket, kEnt, kBid
 };
+
+// per-bucket counts (kBuckets + 1, zero between calls: the scatter pass
+// decrements them back) followed by the bucket starts (kBuckets + 1)
+uint32_t* bucket_counts(cudaStream_t st) {
+    const bool fresh = pool().bufs.count({current_device(), kBucket}) == 0;
+    uint32_t* b = scratch_as<uint32_t>(kBucket, 2 * (kBuckets + 1));
+    if (fresh) CUDA_OK(cudaMemsetAsync(b, 0, 2 * (kBuckets + 1) * sizeof(uint32_t), st));
+    return b;
+}
 
 struct Counters {  // device-side control block
     unsigned long long count;
@@ -860,9 +869,17 @@ struct Counters {  // device-side control block
     int bad;   // NaN probability seen
     int fail;  // fast path unusable
     int xbad;  // invalid ideal probability
-    unsigned kmin;  // smallest kept 32-bit sort key (bucket range)
+    unsigned kmin;  // smallest kept 32-bit sort key
+    unsigned long long kmin64;  // smallest kept 64-bit key (bucket range)
     double xsum[2];
 };
+
+template <typename K>
+K* kmin_of(Counters* c) {
+    if constexpr (sizeof(K) == 4) return reinterpret_cast<K*>(&c->kmin);
+    else return reinterpret_cast<K*>(&c->kmin64);
+}
+
 
 int grid_for(int64_t work, int per_block) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, 148 * 8)));
@@ -911,7 +928,7 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     CUDA_OK(cudaMemcpyAsync(d_fixed, cs.group_fixed, G * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     Counters* d_ctl = scratch_as<Counters>(kCounters, 1);
     {
-        const Counters init{0, ULLONG_MAX, 0, {0, 0}, 0, 0, 0, 0xffffffffu, {0, 0}};
+        const Counters init{0, ULLONG_MAX, 0, {0, 0}, 0, 0, 0, 0xffffffffu, ULLONG_MAX, {0, 0}};
         CUDA_OK(cudaMemcpyAsync(d_ctl, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
     }
     uint64_t* d_direct = want_direct ? scratch_as<uint64_t>(kDirect, G) : nullptr;
@@ -923,7 +940,10 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     CUDA_OK(cudaEventRecord(evp.first, st));
 
     // threshold path for k well below the candidate count (force_path: 1 always, 2 never)
-    const int64_t stride = total >= (int64_t{1} << 20) ? 32 : 1;
+    // sample 1/stride of the groups: >= ~1024 expected top-k entries in the
+    // sample keep the threshold tight (k / stride), 1/32 .. 1/256 of the groups
+    const int64_t stride =
+        total >= (int64_t{1} << 20) ? std::max<int64_t>(32, std::min<int64_t>(256, static_cast<int64_t>(k) / 1024)) : 1;
     bool fast = k > 0 && static_cast<double>(k) * 4 <= static_cast<double>(total) && force_path != 2;
     if (force_path == 1) fast = k > 0;
     const bool narrow = total <= (int64_t{1} << 32);  // 32-bit keys and indices in the compact buffer
@@ -931,7 +951,7 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     void* keys = nullptr;
     void* ts = nullptr;
     if (fast) {
-        const int64_t n_s = (G + stride - 1) / stride;
+        const int64_t n_s = sampled_groups(G, stride);
         const double f = static_cast<double>(n_s) / static_cast<double>(G);  // sampled fraction
         const double c = static_cast<double>(k) * f;                          // expected samples in the top k
         const double want = c * 1.05 + 6.0 * std::sqrt(c) + 16.0;
@@ -961,8 +981,8 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
             // 32 groups per tile (16.6 KB at l = 6): ~5 blocks per SM hide the load latency
             const int gpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, 8192 / per)));
             const size_t smem = kDirectStage * (sizeof(K) + sizeof(V)) + static_cast<size_t>(gpb) * (per + 1) * sizeof(double);
-            static std::atomic<uint64_t> attr_done[2]{};
-            if (first_on_device(attr_done[sizeof(K) == 8 ? 1 : 0]))
+            static std::atomic<uint64_t> attr_done[3]{};  // per (K, V) instantiation
+            if (first_on_device(attr_done[sizeof(K) == 4 ? 0 : (sizeof(V) == 8 ? 1 : 2)]))
                 CUDA_OK(cudaFuncSetAttribute(direct_scan_kernel<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              160 * 1024));
             // RCSG_DIRECT_SLACK (test knob): widens the exactness margin so that
@@ -977,45 +997,51 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
                 std::max<int64_t>(1, std::min<int64_t>((G + gpb - 1) / gpb, static_cast<int64_t>(n_sm) * std::max(occ, 1))));
             direct_scan_kernel<K, V><<<grid, 256, smem, st>>>(d_src, from_amps, G, cs.l, gpb, thr, kk, tt,
                                                               &d_ctl->count, cap, &d_ctl->bad, d_fixed, mm, seed,
-                                                              d_direct, &d_ctl->zero_group, slack_mul, &d_ctl->kmin);
+                                                              d_direct, &d_ctl->zero_group, slack_mul, kmin_of<K>(d_ctl));
         } else if (want_direct) {
             const int grid = grid_for(G, 8);  // 8 warps per block, one group per warp
             scan_kernel<true, K, V><<<grid, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count, cap,
                                                           &d_ctl->bad, d_fixed, mm, seed, d_direct,
-                                                          &d_ctl->zero_group, &d_ctl->kmin);
+                                                          &d_ctl->zero_group, kmin_of<K>(d_ctl));
         } else {
             scan_kernel<false, K, V><<<148 * 8, 256, 0, st>>>(d_src, from_amps, G, cs.l, thr, kk, tt, &d_ctl->count,
                                                               cap, &d_ctl->bad, d_fixed, mm, seed, d_direct,
-                                                              &d_ctl->zero_group, &d_ctl->kmin);
+                                                              &d_ctl->zero_group, kmin_of<K>(d_ctl));
         }
     };
+    // bucket order (RCSG_TOPK_BUCKETS=0: the radix sort + tie pass instead):
+    // the scan writes full 64-bit keys with 32-bit candidate indices
+    const bool buckets = fast && narrow && !(getenv("RCSG_TOPK_BUCKETS") && atoi(getenv("RCSG_TOPK_BUCKETS")) == 0);
     if (fast || want_direct) {
-        if (narrow) scan(uint32_t{0}, uint32_t{0});
+        if (buckets) scan(uint64_t{0}, uint32_t{0});
+        else if (narrow) scan(uint32_t{0}, uint32_t{0});
         else scan(uint64_t{0}, uint64_t{0});
     }
-    // RCSG_TOPK_BUCKETS=1: bucket order instead of the radix sort + tie pass (32-bit keys)
-    const bool bucket_off = !(getenv("RCSG_TOPK_BUCKETS") && atoi(getenv("RCSG_TOPK_BUCKETS")) == 1);
+    auto select_buckets = [&]() {
+        const uint64_t* ka = static_cast<const uint64_t*>(keys);
+        const uint32_t* ta = static_cast<const uint32_t*>(ts);
+        uint32_t* bcount = bucket_counts(st);
+        uint32_t* bstart = bcount + (kBuckets + 1);
+        uint64_t* kb = scratch_as<uint64_t>(kKeyB, cap);
+        uint32_t* tb = scratch_as<uint32_t>(kTB, cap);
+        uint32_t* bid = scratch_as<uint32_t>(kBid, cap);
+        size_t scan_bytes = 0;
+        CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, bcount, bstart, kBuckets + 1, st));
+        void* scan_tmp = scratch(kTmp, scan_bytes);
+        const int g = grid_for(static_cast<int64_t>(cap), 256);
+        bucket_hist_kernel<<<g, 256, 0, st>>>(ka, &d_ctl->count, cap, k, &d_ctl->kmin64, &d_ctl->thr, bcount,
+                                              &d_ctl->fail);
+        CUDA_OK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, bcount, bstart, kBuckets + 1, st));
+        bucket_scatter_kernel<uint32_t><<<g, 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k, &d_ctl->kmin64,
+                                                           &d_ctl->thr, bstart, bcount, kb, tb, bid);
+        bucket_rank_kernel<uint32_t><<<g, 256, 0, st>>>(kb, tb, bid, bstart, &d_ctl->count, cap, k, d_fixed, mm,
+                                                        &d_ctl->fail, d_top);
+    };
     auto select_fast = [&](auto kz, auto vz) {
         using K = decltype(kz);
         using V = decltype(vz);
         K* ka = static_cast<K*>(keys);
         V* ta = static_cast<V*>(ts);
-        if constexpr (sizeof(K) == 4) {
-            if (!bucket_off) {  // bucket order (see bucket_rank_kernel)
-                uint32_t* bcount = scratch_as<uint32_t>(kBucket, 2 * kBuckets);
-                uint32_t* bstart = bcount + kBuckets;
-                V* tb = static_cast<V*>(scratch(kTB, cap * sizeof(V)));
-                CUDA_OK(cudaMemsetAsync(bcount, 0, kBuckets * sizeof(uint32_t), st));
-                const int g = grid_for(static_cast<int64_t>(cap), 256);
-                bucket_hist_kernel<<<g, 256, 0, st>>>(ka, &d_ctl->count, cap, k, &d_ctl->kmin, bcount, &d_ctl->fail);
-                bucket_scan_kernel<<<1, 1024, 0, st>>>(bcount, bstart);
-                bucket_scatter_kernel<V><<<g, 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k, &d_ctl->kmin, bstart,
-                                                            bcount, tb);
-                bucket_rank_kernel<V><<<148 * 8, 256, 0, st>>>(tb, bstart, bcount, k, d_src, from_amps, d_fixed, mm,
-                                                               &d_ctl->fail, d_top);
-                return;
-            }
-        }
         pad_kernel<K, V><<<grid_for(static_cast<int64_t>(cap), 256), 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k,
                                                                                  &d_ctl->fail);
         K* kb = static_cast<K*>(scratch(kKeyB, cap * sizeof(K)));
@@ -1031,7 +1057,8 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
     };
     auto select = [&](bool use_fast) {
         if (use_fast) {
-            if (narrow) select_fast(uint32_t{0}, uint32_t{0});
+            if (buckets) select_buckets();
+            else if (narrow) select_fast(uint32_t{0}, uint32_t{0});
             else select_fast(uint64_t{0}, uint64_t{0});
         } else {
             uint64_t* t_sorted = nullptr;
