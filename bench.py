@@ -464,23 +464,31 @@ def scale_mode(pb, p, fixed, prec, ns, M, bud, bf16_peak, peak_kind):
     p.sync(prec, bud)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    # two profiled slices, the second one reported (the first sets up the per-launch events)
     p.set_profile(True)
-    pst = rcsg_stats()
     p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(0, 1), budget=bud,
+                             stats=rcsg_stats())
+    pst = rcsg_stats()
+    p.contract_groups_device(fixed, acc.data_ptr(), precision=prec, configs=None, slices=(1, 2), budget=bud,
                              stats=pst)
     p.set_profile(False)
     tc_peak = bf16_peak / 2.0 if prec == "tf32" else bf16_peak
+    hbm_peak = peaks()[0]
     rate = ns / (ms / 1e3)
     exec_tf = st.executed_flops / (ms / 1e3) / 1e12
     top_s = pst.top_ms_sum / pst.top_launches * 1e-3 if pst.top_launches else pst.top_ms * 1e-3
+    ai = pst.top_flops / pst.top_bytes if pst.top_bytes else float("inf")
+    if ai >= tc_peak * 1e12 / (hbm_peak * 1e9):
+        bound, ach, peak, unit = "tensor", pst.top_flops / top_s / 1e12 if top_s else None, tc_peak, "TFLOP/s"
+    else:
+        bound, ach, peak, unit = "hbm", pst.top_bytes / top_s / 1e9 if top_s else None, hbm_peak, "GB/s"
     res = {
         "value": rate, "unit": UNIT, "timed_slices": ns, "ms": ms, "warm_s": warm_s,
         "executed_tflops": exec_tf, "frac_of_dense_peak": exec_tf / tc_peak,
         "peak_tflops": tc_peak, "peak_note": ("dense tf32 = 1/2 of " if prec == "tf32" else "") +
         f"{peak_kind} dense bf16 {bf16_peak:.1f} TF/s",
-        "roofline": {"bound": "tensor", "kernel": f"plan step {pst.top_step}: tcgen05 GEMM",
-                     "achieved": pst.top_flops / top_s / 1e12 if top_s else None, "peak": tc_peak,
-                     "unit": "TFLOP/s", "frac": pst.top_flops / top_s / 1e12 / tc_peak if top_s else None,
+        "roofline": {"bound": bound, "kernel": f"plan step {pst.top_step}: tcgen05 GEMM",
+                     "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak if ach else None,
                      "flops": pst.top_flops, "bytes": pst.top_bytes, "launch_ms": top_s * 1e3,
                      "share_of_slice": pst.top_ms_sum / pst.device_ms if pst.device_ms else None,
                      "traffic": None},

@@ -1084,7 +1084,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                           (col0 >> p.om.n_bits) * p.om.n_vstride
                                     : col0;
             };
-            if (BN == 32 && NG != 1) {
+            if (BN == 32 && NG != 1 && p.n >= 32) {
 #pragma unroll 1
                 for (int plane = plane_lo; plane < plane_hi; ++plane)
                     chunk(std::integral_constant<int, 32>{}, plane, 0, col_base_of(c.n0, 5));
@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll 1
                 for (int plane = plane_lo; plane < plane_hi; ++plane)
 #pragma unroll 1
-                    for (int c0 = col_lo; c0 < col_hi; c0 += CWD)
+                    for (int c0 = col_lo; c0 < col_hi && c.n0 + c0 < p.n; c0 += CWD)  // no chunks past n
                         chunk(std::integral_constant<int, CWD>{}, plane, c0, col_base_of(c.n0 + c0, CWD == 32 ? 5 : 4));
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1245,10 +1245,13 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     p.k_chunk = chunk_blocks * kbk<E, RB>;
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     {
-        // two tiles in flight help short (memory-bound) tiles and cost nothing on long K
-        // (measured); four help BN = 32.  NBUF must be a multiple of the group count.
+        // NBUF must be a multiple of the group count.
         constexpr int nbuf = static_cast<int>(tc_nbuf<THREE>(BN));
-        int ng = (BN == 32 && nbuf >= 4) ? 4 : 2;
+        // BN >= 64: all 16 epilogue warps on each tile (NG = 1) measured 5-12 % faster on the
+        // HBM-bound (small-K) steps than two groups, and the same on long K; BN = 32: 4 groups
+        // (profiles/r02/ng_probe)
+        static const int ng_wide = getenv("RCSG_TC_NG_WIDE") ? atoi(getenv("RCSG_TC_NG_WIDE")) : 1;
+        int ng = (BN == 32 && nbuf >= 4) ? 4 : ng_wide;
         if (const char* e = getenv("RCSG_TC_NG")) ng = atoi(e);
         if (ng != 1 && ng != 2 && ng != 4) ng = 1;
         while (ng > 1 && nbuf % ng) ng /= 2;
@@ -1259,6 +1262,11 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         // (RCSG_TC_GROUP: override; 0 disables)
         const int64_t n_lo = p.m_fast ? p.mt : p.nt, n_hi = p.m_fast ? p.nt : p.mt;
         int grp = (chunk_blocks >= 32 && n_lo >= 16 && n_hi >= 8) ? 8 : 0;
+        // tf32 CTA pairs with a short "lo" side (cfg2 step 149: 15 row pairs): 16 "hi" tiles in
+        // flight cut the DRAM reads by a fifth (profiles/r02/raster_probe.log)
+        static const bool pair_group = !(getenv("RCSG_TC_PAIR_GROUP") && atoi(getenv("RCSG_TC_PAIR_GROUP")) == 0);
+        if (pair_group && CG == 2 && sizeof(E) == 4 && chunk_blocks >= 32 && n_lo >= 8 && n_lo < 16 && n_hi >= 32)
+            grp = 16;
         if (const char* e = getenv("RCSG_TC_GROUP")) grp = atoi(e);
         p.group = grp > 0 && n_hi > grp ? grp : 0;
         if (g.vperm && g.batch > 1) {  // shared-operand batch: G = 16 m-tiles x the variants in flight

@@ -19,6 +19,6 @@ PY
 echo "top gemm_tc_persistent launch index: $IDX" > "$OUT/ncu_top_$PREC.txt"
 ncu --profile-from-start off --set full --import-source on --clock-control none \
     --kernel-name regex:gemm_tc_persistent --launch-skip "$IDX" --launch-count 1 \
-    -o "$OUT/top_$PREC" -f python tools/one_slice.py >> "$OUT/ncu_top_$PREC.txt" 2>&1
-ncu -i "$OUT/top_$PREC.ncu-rep" --page raw --csv > "$OUT/top_${PREC}_raw.csv" 2>/dev/null
-ncu -i "$OUT/top_$PREC.ncu-rep" --page details --csv > "$OUT/top_${PREC}_details.csv" 2>/dev/null
+    -o "/tmp/top_$PREC" -f python tools/one_slice.py >> "$OUT/ncu_top_$PREC.txt" 2>&1
+ncu -i "/tmp/top_$PREC.ncu-rep" --page raw --csv > "$OUT/top_${PREC}_raw.csv" 2>/dev/null
+ncu -i "/tmp/top_$PREC.ncu-rep" --page details --csv > "$OUT/top_${PREC}_details.csv" 2>/dev/null
