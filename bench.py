@@ -77,6 +77,20 @@ def parse():
     return ap.parse_args()
 
 
+# stdout carries exactly one JSON line: library banners (NCCL version, ...) that
+# write to fd 1 are sent to stderr, the result line goes to the original stdout
+_RESULT_FD = None
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _RESULT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, data)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -206,7 +220,7 @@ def run_reference(args, rank, world):
                             f"{smp['pairs']} (group, slice) pairs ({smp['secs']:.1f} s), not K whole steps",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -612,6 +626,9 @@ def main():
     torch.cuda.set_device(local)
     pb.api.set_device(local)
     if world > 1:
+        # stdout carries exactly one JSON line: no NCCL version banner
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm_peak, bf16_peak, peak_kind = peaks()
 
@@ -707,11 +724,14 @@ def main():
         }
         if alt:
             line[args.alt_precision] = alt
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
 if __name__ == "__main__":
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
     sys.exit(main())

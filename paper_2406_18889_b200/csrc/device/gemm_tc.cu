@@ -1413,7 +1413,8 @@ bool launch_3m(const GemmArgs& g, cudaStream_t st) {
 template <typename E>
 int pair_policy(const GemmArgs& g) {
     const int64_t kb = (g.k + kbk<E, 128> - 1) / kbk<E, 128>;
-    if (g.m < 512 || g.n < 256 || kb < 32 || g.k * static_cast<int64_t>(sizeof(E)) < 512) return 0;
+    static const int64_t min_kb = getenv("RCSG_TC_PAIR_MINKB") ? atoll(getenv("RCSG_TC_PAIR_MINKB")) : 32;
+    if (g.m < 512 || g.n < 256 || kb < min_kb || g.k * static_cast<int64_t>(sizeof(E)) < 512) return 0;
     if (const char* e = getenv("RCSG_TC_PAIR")) return atoi(e);
     if (sizeof(E) == 2) return g.n >= 2048 ? 2 : 0;
     return (kb >= 1024 && g.n >= 2048) ? 2 : 1;
