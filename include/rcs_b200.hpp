@@ -278,8 +278,8 @@ void dump_amplitudes(const StateVector& state, std::ostream& out);
 StateVector load_amplitudes(std::istream& in);
 
 // Precision of the device executor: "f64" (default; reference-grade), "f32",
-// "tf32" (tcgen05 tensor cores), "3xtf32" (fp32-grade accuracy; an alias that runs
-// the fp32 SIMT kernels — no split-tf32 tensor-core path is implemented),
+// "tf32" (tcgen05 tensor cores), "3xtf32" (fp32-grade accuracy on the tf32 tensor
+// cores: fp32 operands split into hi + lo halves, three products per real product),
 // "bf16", "f16" (fp16 storage with per-tensor power-of-two scales).
 void set_precision(const std::string& precision);
 std::string get_precision();

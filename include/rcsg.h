@@ -42,7 +42,7 @@ enum {
     RCSG_PREC_F64 = 0,   /* fp64 SIMT: reference-grade (<= 1e-10 norm-relative) */
     RCSG_PREC_F32 = 1,   /* fp32 SIMT */
     RCSG_PREC_TF32 = 2,  /* tcgen05 kind::tf32, fp32 accumulate in TMEM */
-    RCSG_PREC_3XTF32 = 3, /* fp32-grade alias: runs the fp32 SIMT kernels (no split-tf32 MMA path) */
+    RCSG_PREC_3XTF32 = 3, /* fp32 storage, split hi + lo operands on tcgen05 kind::tf32 (fp32-grade) */
     RCSG_PREC_BF16 = 4,   /* bf16 storage, tcgen05 kind::f16 (BF16 operands), fp32 accumulate */
     RCSG_PREC_F16 = 5     /* fp16 storage with calibrated per-tensor 2^e scales, kind::f16, fp32 accumulate */
 };

@@ -92,6 +92,7 @@ def testkit():
         lib()
         _testkit = C.CDLL(TESTKIT_PATH)
         for name in ("rcsg_gemm_selftest", "rcsg_gemm_check_f16", "rcsg_gemm_check_bf16", "rcsg_gemm_check_tf32",
+                     "rcsg_gemm_check_3xtf32",
                      "rcsg_gemm_bench_f16", "rcsg_gemm_bench_tf32"):
             getattr(_testkit, name).restype = C.c_int
     return _testkit

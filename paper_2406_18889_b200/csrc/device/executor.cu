@@ -824,6 +824,7 @@ GemmArgs Program::step_args(const StepInfo& st, const ChunkData* ch) const {
     g.scale_exp = node_exp_[st.a] + node_exp_[st.b] - node_exp_[st.r];
     static const bool chop = getenv("RCSG_TF32_CHOP") != nullptr;  // probes: the MMA's own truncation
     g.round_tf32 = precision_ == RCSG_PREC_TF32 && !chop;
+    g.split_tf32 = precision_ == RCSG_PREC_3XTF32;
     const int64_t vb = (B.level == 2 && ch) ? ch->nvar[st.b] : 1;
     const int prod = st.mode == 2 ? product_order(A.var_mask, B.var_mask, va, vb, vr) : 0;
     if (prod) {
@@ -919,7 +920,9 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         marks_[mk].bytes = static_cast<uint64_t>(eb * (va * st.m * st.k + vb * st.n * st.k + vr * st.m * st.n));
     }
     const bool tc_ok = !std::is_same_v<R, double> &&
-                       (precision_ == RCSG_PREC_TF32 || precision_ >= RCSG_PREC_BF16) && gemm_tc_supported(g);
+                       (precision_ == RCSG_PREC_TF32 || precision_ == RCSG_PREC_3XTF32 ||
+                        precision_ >= RCSG_PREC_BF16) &&
+                       gemm_tc_supported(g);
     // K <= 16 goes to the register-blocked outer-product kernel, except large
     // K = 5..16 products, which are CUDA-core FMA-bound there and memory-bound
     // on the tensor cores (narrow-K tiles zero-fill K up to 16)
@@ -939,8 +942,8 @@ void Program::exec_step_t(const StepInfo& st, const ChunkData* ch) {
         return;
     }
     if constexpr (!std::is_same_v<R, double>) {
-        // 3xTF32 stays on the fp32 SIMT kernel until its split-operand tensor-core path lands
-        if ((precision_ == RCSG_PREC_TF32 || precision_ >= RCSG_PREC_BF16) && gemm_tc_supported(g)) {
+        // tf32, fp16, bf16 and 3xtf32 (split fp32 operands, gemm_tc.cu launch_split) on tcgen05
+        if (tc_ok) {
             launch_gemm_tc(g, precision_ == RCSG_PREC_BF16 ? 1 : (precision_ == RCSG_PREC_F16 ? 2 : 0), ls_);
             mark_end(mk, kCatGemmTc, flops, st.plan_index, g.m, g.n, g.k, g.batch);
             ++launches_;
@@ -1168,7 +1171,8 @@ void Program::retree(const std::vector<uint64_t>& groups) {
     std::vector<uint64_t> uniq = groups;
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    double pf = precision_ >= RCSG_PREC_BF16 ? 1.2e15 : (precision_ == RCSG_PREC_TF32 ? 6e14 : 5e13);
+    double pf = precision_ >= RCSG_PREC_BF16 ? 1.2e15
+                : (precision_ == RCSG_PREC_TF32 ? 6e14 : (precision_ == RCSG_PREC_3XTF32 ? 2e14 : 5e13));
     double bw = 6e12, lat = 4e-6;
     if (const char* e = getenv("RCSG_TREE_PF")) pf = atof(e);  // cost-model knobs (experiments)
     if (const char* e = getenv("RCSG_TREE_BW")) bw = atof(e);
@@ -1275,7 +1279,8 @@ void Program::bind_groups(const std::vector<uint64_t>& groups) {
     if (!budget) {
         size_t fr = 0, tot = 0;
         CUDA_OK(cudaMemGetInfo(&fr, &tot));
-        budget = static_cast<uint64_t>(fr * 0.7);
+        // 3xtf32 stages the hi / lo halves of a GEMM's operands in a workspace next to the arena
+        budget = static_cast<uint64_t>(fr * (precision_ == RCSG_PREC_3XTF32 ? 0.3 : 0.7));
     }
     const int64_t n_uniq = static_cast<int64_t>(uniq.size());
     plan_codes_ = n_uniq;

@@ -172,7 +172,7 @@ __global__ void diff_half(const T* a, const T* b, int64_t n, double* out) {
 // explicit output map (every epilogue kind / K-tile width); rel = ||TC-SIMT|| / ||SIMT||.
 template <typename T>
 int gemm_check(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits, const int8_t* m_pos,
-               const int8_t* n_pos, double* out_rel) {
+               const int8_t* n_pos, double* out_rel, int split_tf32 = 0) {
     try {
         T *a, *b, *c1, *c2;
         int32_t* fault;
@@ -205,7 +205,9 @@ int gemm_check(int elem, int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_
         for (int j = 0; j < n_bits; ++j) g.om.n_pos[j] = n_pos[j];
         if (!gemm_tc_supported(g)) return RCSG_ERR_CONFIG;
         g.c = c1;
+        g.split_tf32 = split_tf32;
         launch_gemm_tc(g, elem, 0);
+        g.split_tf32 = 0;
         g.c = c2;
         launch_gemm_simt<T>(g, 0);
         cudaMemset(d, 0, 16);
@@ -241,6 +243,12 @@ extern "C" int rcsg_gemm_check_bf16(int64_t m, int64_t n, int64_t k, int32_t m_b
 extern "C" int rcsg_gemm_check_tf32(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
                                     const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
     return gemm_check<float>(0, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel);
+}
+
+// split tf32 ("3xTF32": hi + lo fp32 operand halves on kind::tf32) against the fp32 SIMT kernel
+extern "C" int rcsg_gemm_check_3xtf32(int64_t m, int64_t n, int64_t k, int32_t m_bits, int32_t n_bits,
+                                      const int8_t* m_pos, const int8_t* n_pos, double* out_rel) {
+    return gemm_check<float>(0, m, n, k, m_bits, n_bits, m_pos, n_pos, out_rel, 1);
 }
 
 // tcgen05 GEMM timing on random operands through an explicit output map (tools only)

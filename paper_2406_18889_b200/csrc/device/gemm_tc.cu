@@ -820,9 +820,10 @@ struct TileIter {
 // THREE (3M complex product): T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi), then
 // Re = T1 - T2, Im = T3 - T1 - T2 in the epilogue - three real MMAs per K slice
 // instead of four, with the operand sum planes staged by the host-side pre-pass.
-template <bool THREE>
+// VAR: 0 = 4M, 1 = 3M (three accumulators), 2 = split tf32 (3xTF32, two accumulators)
+template <int VAR>
 constexpr uint32_t tc_nbuf(int bn) {
-    return (512 / ((THREE ? 3 : 2) * bn)) < 4 ? (512 / ((THREE ? 3 : 2) * bn)) : 4;
+    return (512 / ((VAR == 1 ? 3 : 2) * bn)) < 4 ? (512 / ((VAR == 1 ? 3 : 2) * bn)) : 4;
 }
 constexpr uint32_t pow2_ceil(uint32_t x) {
     uint32_t r = 32;
@@ -837,19 +838,28 @@ constexpr uint32_t pow2_ceil(uint32_t x) {
 // CTA's epilogue drains its own TMEM rows; the peer's epilogue warps release a
 // TMEM buffer on the leader's tempty barrier.  Per CTA, a k-block moves half
 // of B's bytes of the 1-CTA tile for the same MMA work.
-template <int BN, int STAGES, typename E, int RB, bool THREE = false, int CG = 1>
+// VAR = 2 (split tf32, "3xTF32"): fp32 operands x = hi + lo, hi = rna_tf32(x),
+// lo = rna_tf32(x - hi), staged by a pre-pass (map_ar / map_ai / map_br / map_bi
+// read the hi planes, map_as / map_as2 / map_bs / map_bs2 the lo planes); each
+// real product is hi*hi + hi*lo + lo*hi (12 MMAs per K slice for the complex
+// 4M form), which carries ~fp32 accuracy on the tf32 tensor cores.
+template <int BN, int STAGES, typename E, int RB, int VAR = 0, int CG = 1>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ai,
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const __grid_constant__ CUtensorMap map_as, const __grid_constant__ CUtensorMap map_bs,
+                       const __grid_constant__ CUtensorMap map_as2, const __grid_constant__ CUtensorMap map_bs2,
                        const TcParams p, int64_t total_tiles) {
-    constexpr int NPL = THREE ? 3 : 2;
-    static_assert(CG == 1 || !THREE, "3M has no CTA-pair variant");
+    constexpr bool THREE = VAR == 1, SPLIT = VAR == 2;
+    constexpr int NPL = VAR == 0 ? 2 : (VAR == 1 ? 3 : 4);  // shared-memory planes per operand
+    constexpr int NACC = VAR == 1 ? 3 : 2;                  // TMEM accumulators per tile
+    static_assert(CG == 1 || VAR == 0, "3M / split tf32 have no CTA-pair variant");
+    static_assert(!SPLIT || sizeof(E) == 4, "split tf32 needs fp32 operands");
     using S = Smem<BN, STAGES, RB, NPL, CG>;
     // TMEM accumulator buffers ({Re, Im}, or {T1, T2, T3} for 3M): as many as fit in
     // 512 columns (max 4), so the MMA runs ahead of the epilogue by NBUF - 1 tiles
-    constexpr uint32_t NBUF = tc_nbuf<THREE>(BN);
-    constexpr uint32_t kCols = pow2_ceil(NBUF * NPL * BN);
+    constexpr uint32_t NBUF = tc_nbuf<VAR>(BN);
+    constexpr uint32_t kCols = pow2_ceil(NBUF * NACC * BN);
     // epilogue groups = tiles in flight (NBUF % NG == 0), chosen by the host (p.ng: 1, 2 or 4)
     const int NG = p.ng;
     extern __shared__ uint8_t smem_raw[];
@@ -868,7 +878,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     __shared__ int64_t tn_lo[32];
     if (threadIdx.x < 32) tn_lo[threadIdx.x] = out_col_off(p.om, threadIdx.x);
     if (threadIdx.x == 32) {  // fetch the TMA descriptors while the CTA sets up
-        for (const CUtensorMap* m : {&map_ar, &map_ai, &map_br, &map_bi, &map_as, &map_bs})
+        for (const CUtensorMap* m : {&map_ar, &map_ai, &map_br, &map_bi, &map_as, &map_bs, &map_as2, &map_bs2})
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     }
 
@@ -938,12 +948,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                         mbar_expect_tx(&full[s], load_b ? S::kStage : NPL * S::kATile);
                         tma_load_3d(st, &map_ar, &full[s], kc, c.m0, av);
                         tma_load_3d(st + S::kATile, &map_ai, &full[s], kc, c.m0, av);
-                        if constexpr (THREE) tma_load_3d(st + 2 * S::kATile, &map_as, &full[s], kc, c.m0, av);
+                        if constexpr (THREE || SPLIT) tma_load_3d(st + 2 * S::kATile, &map_as, &full[s], kc, c.m0, av);
+                        if constexpr (SPLIT) tma_load_3d(st + 3 * S::kATile, &map_as2, &full[s], kc, c.m0, av);
                         if (load_b) {
                             uint8_t* sb = st + NPL * S::kATile;
                             tma_load_3d(sb, &map_br, &full[s], kc, c.n0, bv);
                             tma_load_3d(sb + S::kBTile, &map_bi, &full[s], kc, c.n0, bv);
-                            if constexpr (THREE) tma_load_3d(sb + 2 * S::kBTile, &map_bs, &full[s], kc, c.n0, bv);
+                            if constexpr (THREE || SPLIT) tma_load_3d(sb + 2 * S::kBTile, &map_bs, &full[s], kc, c.n0, bv);
+                            if constexpr (SPLIT) tma_load_3d(sb + 3 * S::kBTile, &map_bs2, &full[s], kc, c.n0, bv);
                         }
                     }
                 }
@@ -963,7 +975,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     else mbar_wait(&tempty[ab], ((j / NBUF) - 1) & 1);
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t t_re = tmem + ab * NPL * BN, t_im = t_re + BN;  // 3M: T1, T2 (, T3 = t_re + 2 BN)
+                const uint32_t t_re = tmem + ab * NACC * BN, t_im = t_re + BN;  // 3M: T1, T2 (, T3 = t_re + 2 BN)
                 for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
                     const int s = it % STAGES;
                     if (p.sleepy) mbar_wait_sleep(&full[s], (it / STAGES) & 1);
@@ -982,6 +994,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
                             mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);           // T1 = Ar Br
                             mma_e<E>(t_im, dai + o, dbi + o, id_pos, acc);           // T2 = Ai Bi
                             mma_e<E>(t_re + 2 * BN, das + o, dbs + o, id_pos, acc);  // T3 = As Bs
+                        } else if constexpr (SPLIT) {
+                            // lo planes: Ar_lo, Ai_lo at A tiles 2, 3; Br_lo, Bi_lo at B tiles 2, 3.
+                            // Small cross terms first, then hi * hi
+                            const uint64_t darl = smem_desc<RB>(st + 2 * S::kATile), dail = smem_desc<RB>(st + 3 * S::kATile);
+                            const uint64_t dbrl = smem_desc<RB>(sb + 2 * S::kBTile), dbil = smem_desc<RB>(sb + 3 * S::kBTile);
+                            mma_e<E>(t_re, darl + o, dbr + o, id_pos, acc);   // Re += Arl Br + Ar Brl + Ar Br
+                            mma_e<E>(t_re, dar + o, dbrl + o, id_pos, 1u);
+                            mma_e<E>(t_re, dail + o, dbi + o, id_neg, 1u);    //      - (Ail Bi + Ai Bil + Ai Bi)
+                            mma_e<E>(t_re, dai + o, dbil + o, id_neg, 1u);
+                            mma_e<E>(t_re, dar + o, dbr + o, id_pos, 1u);
+                            mma_e<E>(t_re, dai + o, dbi + o, id_neg, 1u);
+                            mma_e<E>(t_im, darl + o, dbi + o, id_pos, acc);   // Im += Arl Bi + Ar Bil + Ar Bi
+                            mma_e<E>(t_im, dar + o, dbil + o, id_pos, 1u);
+                            mma_e<E>(t_im, dail + o, dbr + o, id_pos, 1u);    //      + Ail Br + Ai Brl + Ai Br
+                            mma_e<E>(t_im, dai + o, dbrl + o, id_pos, 1u);
+                            mma_e<E>(t_im, dar + o, dbi + o, id_pos, 1u);
+                            mma_e<E>(t_im, dai + o, dbr + o, id_pos, 1u);
                         } else if constexpr (CG == 2) {
                             mma_pair<E>(t_re, dar + o, dbr + o, id_pos, acc);
                             mma_pair<E>(t_re, dai + o, dbi + o, id_neg, 1u);
@@ -1040,7 +1069,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // warps that owns all columns (NG >= 2) take the whole 32-column row at once
             auto chunk = [&](auto cw_tag, int plane, int c0, int64_t col_base) {
                 constexpr int CW = decltype(cw_tag)::value;
-                const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * NPL * BN + c0;
+                const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * NACC * BN + c0;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 float x[CW];
                 auto ld = [&](uint32_t addr, float* v) {
@@ -1181,9 +1210,11 @@ int epilogue_kind4(const OutMap& om, int64_t n) {
     return 0;
 }
 
-template <int BN, int STAGES, typename E, int RB = 128, bool THREE = false, int CG = 1>
-void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, const void* b_sum = nullptr) {
-    using S = Smem<BN, STAGES, RB, THREE ? 3 : 2, CG>;
+template <int BN, int STAGES, typename E, int RB = 128, int VAR = 0, int CG = 1>
+void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, const void* b_sum = nullptr,
+            const void* a_sum2 = nullptr, const void* b_sum2 = nullptr) {
+    constexpr bool THREE = VAR == 1;
+    using S = Smem<BN, STAGES, RB, VAR == 0 ? 2 : (VAR == 1 ? 3 : 4), CG>;
     const int64_t a_rows = g.ia ? g.m : g.m;  // rows per A variant (mode 1 folds variants into m)
     const int64_t a_batches = g.a_batch ? std::max<int64_t>(1, g.a_plane / std::max<int64_t>(g.a_batch, 1)) : 1;
     const int64_t b_batches = g.b_batch ? std::max<int64_t>(1, g.b_plane / std::max<int64_t>(g.b_batch, 1)) : 1;
@@ -1193,8 +1224,11 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     const CUtensorMap ai = make_map<E, RB>(a + g.a_plane, g.k, a_rows, a_batches, kBM);
     const CUtensorMap br = make_map<E, RB>(b, g.k, g.n, b_batches, BN / CG);
     const CUtensorMap bi = make_map<E, RB>(b + g.b_plane, g.k, g.n, b_batches, BN / CG);
-    const CUtensorMap as = THREE ? make_map<E, RB>(static_cast<const E*>(a_sum), g.k, a_rows, a_batches, kBM) : ar;
-    const CUtensorMap bs = THREE ? make_map<E, RB>(static_cast<const E*>(b_sum), g.k, g.n, b_batches, BN) : br;
+    // 3M: the Re+Im sum planes; split tf32: the lo planes (Re, Im)
+    const CUtensorMap as = VAR ? make_map<E, RB>(static_cast<const E*>(a_sum), g.k, a_rows, a_batches, kBM) : ar;
+    const CUtensorMap bs = VAR ? make_map<E, RB>(static_cast<const E*>(b_sum), g.k, g.n, b_batches, BN) : br;
+    const CUtensorMap as2 = VAR == 2 ? make_map<E, RB>(static_cast<const E*>(a_sum2), g.k, a_rows, a_batches, kBM) : ar;
+    const CUtensorMap bs2 = VAR == 2 ? make_map<E, RB>(static_cast<const E*>(b_sum2), g.k, g.n, b_batches, BN) : br;
     TcParams p{};
     p.m = g.m;
     p.n = g.n;
@@ -1239,6 +1273,11 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         };
         while (kblocks / (splits * 2) >= 64 && eff(tiles * splits * 2) > eff(tiles * splits) + 0.05) splits *= 2;
     }
+    // at most max_kb k-blocks per split (RCSG_TC_MAX_KB; experiments on the accumulation chain length)
+    if (const char* e = getenv("RCSG_TC_MAX_KB")) {
+        const int64_t max_kb = std::max<int64_t>(1, atoll(e));
+        while ((kblocks + splits - 1) / splits > max_kb && splits < 4096) splits *= 2;
+    }
     const int64_t chunk_blocks = (kblocks + splits - 1) / splits;
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
@@ -1246,7 +1285,7 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     {
         // NBUF must be a multiple of the group count.
-        constexpr int nbuf = static_cast<int>(tc_nbuf<THREE>(BN));
+        constexpr int nbuf = static_cast<int>(tc_nbuf<VAR>(BN));
         // BN >= 64: all 16 epilogue warps on each tile (NG = 1) measured 5-12 % faster on the
         // HBM-bound (small-K) steps than two groups, and the same on long K; BN = 32: 4 groups
         // (profiles/r02/ng_probe)
@@ -1292,11 +1331,11 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     // the epilogue overlaps the next tile's MMAs) for every shape: on long K it
     // measured ~1.9x the one-CTA-per-tile kernel (RCSG_TC_MODE=2 selects that one)
     static const int mode = getenv("RCSG_TC_MODE") ? atoi(getenv("RCSG_TC_MODE")) : 0;
-    const bool persistent = THREE || CG == 2 || mode != 2 || RB != 128;  // narrow-K tiles, 3M, pairs: persistent only
+    const bool persistent = VAR != 0 || CG == 2 || mode != 2 || RB != 128;  // narrow-K, 3M, split, pairs: persistent only
     if (persistent) {
         static std::atomic<uint64_t> pconf{0};
         if (first_on_device(pconf))
-            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB, THREE, CG>,
+            cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES, E, RB, VAR, CG>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, S::template kPBytes<E>);
         const int64_t total = tiles * splits;
         if (total >= (int64_t{1} << 31)) throw std::runtime_error("GEMM tile count exceeds 2^31");
@@ -1317,11 +1356,11 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             attr[1].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 2;
-            cudaLaunchKernelEx(&cfg, gemm_tc_persistent<BN, STAGES, E, RB, THREE, CG>, ar, ai, br, bi, as, bs, p,
-                               total);
+            cudaLaunchKernelEx(&cfg, gemm_tc_persistent<BN, STAGES, E, RB, VAR, CG>, ar, ai, br, bi, as, bs, as2, bs2,
+                               p, total);
         } else {
-            launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, THREE>, dim3(grid), dim3(kPThreads),
-                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, p, total);
+            launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, VAR>, dim3(grid), dim3(kPThreads),
+                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, as2, bs2, p, total);
         }
     } else {
         static std::atomic<uint64_t> configured{0};  // function attributes are per device
@@ -1395,9 +1434,9 @@ bool launch_3m(const GemmArgs& g, cudaStream_t st) {
     launch_pdl(plane_sum_kernel<E>, dim3(grid_of(a_el)), dim3(256), 0, st, a, a + g.a_plane, as, a_el);
     launch_pdl(plane_sum_kernel<E>, dim3(grid_of(b_el)), dim3(256), 0, st, b, b + g.b_plane, bs, b_el);
     if (g.n >= 128) {  // 2 stages of 6 x 16 KB (RB = 128) measured best of the 3M tilings
-        launch<128, 2, E, 128, true>(g, st, as, bs);
+        launch<128, 2, E, 128, 1>(g, st, as, bs);
     } else {
-        launch<64, 5, E, 64, true>(g, st, as, bs);
+        launch<64, 5, E, 64, 1>(g, st, as, bs);
     }
     return true;
 }
@@ -1424,13 +1463,67 @@ template <typename E>
 bool launch_pair(const GemmArgs& g, cudaStream_t st) {
     const int mode = pair_policy<E>(g);
     if (mode == 0) return false;
-    if (mode == 2) launch<256, 3, E, 128, false, 2>(g, st);
-    else launch<128, 4, E, 128, false, 2>(g, st);
+    if (mode == 2) launch<256, 3, E, 128, 0, 2>(g, st);
+    else launch<128, 4, E, 128, 0, 2>(g, st);
     return true;
+}
+
+// hi = rna_tf32(x), lo = rna_tf32(x - hi): the "big + small" split of an fp32
+// operand into two tf32 values (|lo| <= 2^-11 |x|, dropped lo * lo <= 2^-22), 16-B vectors
+__global__ void tf32_split_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t n) {
+    pdl_enter();
+    const int64_t nv = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    auto split = [](float v, float& h, float& l) {
+        h = tf32_rn(v);
+        l = tf32_rn(v - h);
+    };
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+        const float4 v = reinterpret_cast<const float4*>(x)[i];
+        float4 h, l;
+        split(v.x, h.x, l.x);
+        split(v.y, h.y, l.y);
+        split(v.z, h.z, l.z);
+        split(v.w, h.w, l.w);
+        reinterpret_cast<float4*>(hi)[i] = h;
+        reinterpret_cast<float4*>(lo)[i] = l;
+    }
+    for (int64_t i = nv * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        split(x[i], hi[i], lo[i]);
+}
+
+// Split tf32 ("3xTF32", precision mode 3xtf32): a pre-pass writes the hi and lo
+// planes of both operands (whole operand buffers in the same [Re][Im] plane
+// layout, so batched / gathered variants keep their offsets), then the
+// persistent kernel runs hi*hi + hi*lo + lo*hi (12 MMAs per K slice) on 64-B K rows.
+void launch_split(const GemmArgs& g, cudaStream_t st) {
+    const int64_t a_el = 2 * g.a_plane, b_el = 2 * g.b_plane;  // Re and Im planes
+    const int64_t a_pad = (a_el + 63) / 64 * 64, b_pad = (b_el + 63) / 64 * 64;  // 256-B aligned planes
+    float* ws = static_cast<float*>(
+        device_workspace(static_cast<size_t>(2 * a_pad + 2 * b_pad) * sizeof(float), st, 1));
+    float *ah = ws, *al = ws + a_pad, *bh = ws + 2 * a_pad, *bl = ws + 2 * a_pad + b_pad;
+    auto grid_of = [](int64_t n) {
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 8)));
+    };
+    launch_pdl(tf32_split_kernel, dim3(grid_of(a_el)), dim3(256), 0, st, static_cast<const float*>(g.a), ah, al, a_el);
+    launch_pdl(tf32_split_kernel, dim3(grid_of(b_el)), dim3(256), 0, st, static_cast<const float*>(g.b), bh, bl, b_el);
+    GemmArgs h = g;  // the kernel reads the hi planes as its A / B
+    h.a = ah;
+    h.b = bh;
+    if (g.n > 64) launch<128, 3, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
+    else if (g.n > 32) launch<64, 4, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
+    else launch<32, 4, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
 }
 
 template <typename E>
 void launch_typed(const GemmArgs& g, cudaStream_t st) {
+    if constexpr (sizeof(E) == 4) {
+        if (g.split_tf32) {
+            launch_split(g, st);
+            return;
+        }
+    }
     if (launch_3m<E>(g, st)) return;
     if (launch_pair<E>(g, st)) return;
     static const bool narrow = getenv("RCSG_TC_NARROW_K") == nullptr || atoi(getenv("RCSG_TC_NARROW_K")) != 0;

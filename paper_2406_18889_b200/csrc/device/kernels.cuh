@@ -212,6 +212,7 @@ struct GemmArgs {
     int32_t scale_exp;      // outputs are stored times 2^scale_exp (fp16 per-tensor scaling; 0 otherwise)
     const int32_t* vperm;   // tcgen05 raster: result variants ordered so that runs share an operand (or nullptr)
     int32_t round_tf32;     // tf32 mode: outputs rounded to tf32 on store (see tf32_rn)
+    int32_t split_tf32;     // 3xtf32 mode: fp32 operands split hi + lo on the tf32 tensor cores
 };
 template <typename R>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
