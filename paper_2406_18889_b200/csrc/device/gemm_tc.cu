@@ -296,6 +296,8 @@ struct TcParams {
                             // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
                             // flight read the same shared-operand panels (see coord_at)
     int32_t tm;             // persistent kernel: rows per tile (128, or 256 for a CTA pair)
+    int32_t seg;            // > 0: k-blocks per TMEM accumulation segment; the epilogue sums the
+                            // segments in fp32 registers (split tf32: short tensor-core accumulation chains)
     int32_t sleepy;         // persistent kernel: producer / MMA threads wait with a suspend-time hint
                             // (they stop competing for issue slots with the epilogue warps)
     int32_t epi;            // staged epilogue (2-byte E): 0 off, 1 column runs, 2 column runs
@@ -967,8 +969,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
             uint32_t it = 0, j = 0;
             TileIter ti;
             ti.init(p, unit, n_units);
-            for (int64_t t = unit; t < total_tiles; t += n_units, ++j, ti.next()) {
-                const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
+            for (int64_t t = unit; t < total_tiles; t += n_units, ti.next()) {
+              const TileCoord c = ti.coord_at<BN, E, RB>(p, t);
+              // one TMEM buffer per segment of seg k-blocks (the whole tile unless p.seg > 0)
+              const int seg = p.seg > 0 ? p.seg : (c.kblocks > 0 ? c.kblocks : 1);
+              for (int s0 = 0;;) {
                 const uint32_t ab = j % NBUF;
                 if (j >= NBUF) {
                     if (p.sleepy) mbar_wait_sleep(&tempty[ab], ((j / NBUF) - 1) & 1);
@@ -976,7 +981,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t t_re = tmem + ab * NACC * BN, t_im = t_re + BN;  // 3M: T1, T2 (, T3 = t_re + 2 BN)
-                for (int kb = 0; kb < c.kblocks; ++kb, ++it) {
+                const int s1 = min(c.kblocks, s0 + seg);
+                for (int kb = s0; kb < s1; ++kb, ++it) {
                     const int s = it % STAGES;
                     if (p.sleepy) mbar_wait_sleep(&full[s], (it / STAGES) & 1);
                     else mbar_wait(&full[s], (it / STAGES) & 1);
@@ -988,7 +994,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
                     for (int jj = 0; jj < RB / 32; ++jj) {  // 32-B K slices (one MMA K each)
                         const uint64_t o = static_cast<uint64_t>(jj * 32) >> 4;
-                        const uint32_t acc = (kb > 0 || jj > 0) ? 1u : 0u;
+                        const uint32_t acc = (kb > s0 || jj > 0) ? 1u : 0u;
                         if constexpr (THREE) {
                             const uint64_t das = smem_desc<RB>(st + 2 * S::kATile), dbs = smem_desc<RB>(sb + 2 * S::kBTile);
                             mma_e<E>(t_re, dar + o, dbr + o, id_pos, acc);           // T1 = Ar Br
@@ -1028,6 +1034,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
                 if constexpr (CG == 2) mma_commit_pair(&tfull[ab]);
                 else mma_commit(&tfull[ab]);
+                ++j;
+                s0 += seg;
+                if (s0 >= c.kblocks) break;
+              }
             }
         }
     } else {  // ---- epilogue warps 2..17: two groups of 8 take alternate tiles; TMEM lane quarter warp % 4
@@ -1065,31 +1075,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
             else row_off = row < p.m ? out_row_off(p.om, p.n, row) : 0;
             mbar_wait_sleep(&tfull[ab], (j / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            // one chunk = CW columns of one plane; BN = 32 tiles drained by a group of
-            // warps that owns all columns (NG >= 2) take the whole 32-column row at once
-            auto chunk = [&](auto cw_tag, int plane, int c0, int64_t col_base) {
+            // store one CW-column chunk of one plane (x: this lane's row)
+            auto store_x = [&](auto cw_tag, int plane, int c0, int64_t col_base, float* x) {
                 constexpr int CW = decltype(cw_tag)::value;
-                const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * NACC * BN + c0;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
-                float x[CW];
-                auto ld = [&](uint32_t addr, float* v) {
-                    if constexpr (CW == 32) tmem_ld32(addr, v);
-                    else tmem_ld16(addr, v);
-                };
-                if constexpr (THREE) {  // Re = T1 - T2, Im = T3 - T1 - T2
-                    float y[CW];
-                    ld(lanes + (plane == 0 ? 0 : 2 * BN), x);
-                    ld(lanes + (plane == 0 ? BN : 0), y);
-#pragma unroll
-                    for (int i = 0; i < CW; ++i) x[i] -= y[i];
-                    if (plane == 1) {
-                        ld(lanes + BN, y);
-#pragma unroll
-                        for (int i = 0; i < CW; ++i) x[i] -= y[i];
-                    }
-                } else {
-                    ld(lanes + plane * BN, x);
-                }
                 if constexpr (sizeof(E) == 2) {
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
                         bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
@@ -1112,6 +1101,65 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 return p.om.scatter ? warp_scatter(p.om.n_pos, p.om.n_bits, cw_bits, col0, lane) +
                                           (col0 >> p.om.n_bits) * p.om.n_vstride
                                     : col0;
+            };
+            if constexpr (SPLIT) {
+                if (p.seg > 0) {
+                    // segmented accumulation (host: NG = 1, BN <= 64): this warp's one chunk
+                    // (plane, column half) summed over the tile's K segments in fp32 registers
+                    constexpr int CWS = BN / 2 < 32 ? BN / 2 : 32;
+                    const int plane = sub & 1, c0 = (sub >> 1) * (BN / 2);
+                    const int nseg = c.kblocks > 0 ? (c.kblocks + p.seg - 1) / p.seg : 1;
+                    float acc[CWS], x[16];
+                    for (int sg = 0; sg < nseg; ++sg, ++j) {
+                        const uint32_t abs = j % NBUF;
+                        mbar_wait_sleep(&tfull[abs], (j / NBUF) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t addr =
+                            tmem + (static_cast<uint32_t>(q * 32) << 16) + abs * NACC * BN + plane * BN + c0;
+#pragma unroll
+                        for (int h = 0; h < CWS / 16; ++h) {  // 16 columns at a time (registers)
+                            tmem_ld16(addr + 16 * h, x);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) acc[16 * h + i] = sg ? acc[16 * h + i] + x[i] : x[i];
+                        }
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[abs]);
+                    }
+                    if (c.n0 + c0 < p.n)
+                        store_x(std::integral_constant<int, CWS>{}, plane, c0, col_base_of(c.n0 + c0, CWS == 32 ? 5 : 4),
+                                acc);
+                    j -= NG;  // the loop header advances j by NG per tile
+                    continue;
+                }
+            }
+            mbar_wait_sleep(&tfull[ab], (j / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // one chunk = CW columns of one plane; BN = 32 tiles drained by a group of
+            // warps that owns all columns (NG >= 2) take the whole 32-column row at once
+            auto chunk = [&](auto cw_tag, int plane, int c0, int64_t col_base) {
+                constexpr int CW = decltype(cw_tag)::value;
+                const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16) + ab * NACC * BN + c0;
+                float x[CW];
+                auto ld = [&](uint32_t addr, float* v) {
+                    if constexpr (CW == 32) tmem_ld32(addr, v);
+                    else tmem_ld16(addr, v);
+                };
+                if constexpr (THREE) {  // Re = T1 - T2, Im = T3 - T1 - T2
+                    float y[CW];
+                    ld(lanes + (plane == 0 ? 0 : 2 * BN), x);
+                    ld(lanes + (plane == 0 ? BN : 0), y);
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) x[i] -= y[i];
+                    if (plane == 1) {
+                        ld(lanes + BN, y);
+#pragma unroll
+                        for (int i = 0; i < CW; ++i) x[i] -= y[i];
+                    }
+                } else {
+                    ld(lanes + plane * BN, x);
+                }
+                store_x(cw_tag, plane, c0, col_base, x);
             };
             if (BN == 32 && NG != 1 && p.n >= 32) {
 #pragma unroll 1
@@ -1294,6 +1342,14 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         if (const char* e = getenv("RCSG_TC_NG")) ng = atoi(e);
         if (ng != 1 && ng != 2 && ng != 4) ng = 1;
         while (ng > 1 && nbuf % ng) ng /= 2;
+        if (VAR == 2) {
+            // split tf32: TMEM accumulation segments of 16 k-blocks (K = 256), summed by the
+            // epilogue in fp32 (the tensor cores' fp32 accumulation over long K chains costs
+            // ~3e-9 per k-block, profiles/r02/split_acc.log); needs NG = 1 and BN <= 64
+            static const int seg = getenv("RCSG_TC_SPLIT_SEG") ? atoi(getenv("RCSG_TC_SPLIT_SEG")) : 16;
+            p.seg = BN <= 64 ? seg : 0;
+            if (p.seg > 0) ng = 1;
+        }
         p.ng = ng;
     }
     {
@@ -1511,8 +1567,8 @@ void launch_split(const GemmArgs& g, cudaStream_t st) {
     GemmArgs h = g;  // the kernel reads the hi planes as its A / B
     h.a = ah;
     h.b = bh;
-    if (g.n > 64) launch<128, 3, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
-    else if (g.n > 32) launch<64, 4, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
+    // 64-column tiles: one 32-column chunk per epilogue warp, summed over the K segments
+    if (g.n > 32) launch<64, 4, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
     else launch<32, 4, float, 64, 2>(h, st, al, bl, al + g.a_plane, bl + g.b_plane);
 }
 
