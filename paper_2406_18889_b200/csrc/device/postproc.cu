@@ -56,11 +56,13 @@ constexpr uint64_t kPadKey = 0x7fffffffffffffffull;  // sorts after every non-ne
 
 struct MemberMap {
     int32_t n, l;
+    int32_t low_open;       // open qubits are 0..l-1: index = fixed << l | i
     int32_t open_pos[64];   // qubit of open bit j
     int32_t fixed_pos[64];  // qubit of fixed bit b
 };
 
 __device__ __forceinline__ uint64_t member_index(const MemberMap& mm, uint64_t fixed, uint64_t i) {
+    if (mm.low_open) return (fixed << mm.l) | i;
     uint64_t idx = 0;
     for (int j = 0; j < mm.l; ++j) idx |= ((i >> j) & 1ull) << mm.open_pos[j];
     for (int b = 0; b < mm.n - mm.l; ++b) idx |= ((fixed >> b) & 1ull) << mm.fixed_pos[b];
@@ -302,9 +304,29 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
         __syncthreads();
     };
     if (!DIRECT) {
-        // flat grid-stride over candidates, U independent 16-B loads per thread in flight
+        // flat grid-stride over candidates, U independent 16-B loads per thread in flight.
+        // Kept entries go to a warp-private slice of the staging buffer, flushed by the
+        // warp alone (one global atomic per ~100-250 entries): no block barriers, so a
+        // warp waiting on its loads never stalls the others (blockDim = 256: 8 slices)
+        constexpr unsigned kWarpStage = kStage / 8;
         const int64_t total = n_groups << l;
         const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        K* w_key = s_key + (threadIdx.x >> 5) * kWarpStage;
+        V* w_t = s_t + (threadIdx.x >> 5) * kWarpStage;
+        unsigned wcnt = 0;  // warp-uniform
+        auto wflush = [&]() {
+            __syncwarp();
+            unsigned long long b = 0;
+            if (lane == 0 && wcnt) b = atomicAdd(counter, static_cast<unsigned long long>(wcnt));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            for (unsigned i = lane; i < wcnt; i += 32)
+                if (b + i < cap) {
+                    out_key[b + i] = w_key[i];
+                    out_t[b + i] = w_t[i];
+                }
+            __syncwarp();
+            wcnt = 0;
+        };
         for (int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x); t0 < total; t0 += U * stride) {
             double p[U];
 #pragma unroll
@@ -317,11 +339,20 @@ __global__ void __launch_bounds__(256) scan_kernel(const double* __restrict__ sr
                 const int64_t t = t0 + u * stride + threadIdx.x;
                 const bool in = t < total;
                 if (in) flag_nan(p[u], bad);
-                stage(in && asc_key(p[u]) >= thr, p[u], t);
+                const bool take = in && asc_key(p[u]) >= thr;
+                const unsigned mask = __ballot_sync(0xffffffffu, take);
+                if (take) {
+                    const unsigned pos = wcnt + __popc(mask & ((1u << lane) - 1));
+                    const K key = sort_key<K>(p[u], thr);
+                    w_key[pos] = key;
+                    w_t[pos] = static_cast<V>(t);
+                    kmin = min(kmin, key);
+                }
+                wcnt += __popc(mask);
             }
-            flush(U * blockDim.x, false);
+            if (wcnt + U * 32 > kWarpStage) wflush();
         }
-        flush(0, true);
+        wflush();
         publish_kmin();
         return;
     }
@@ -806,6 +837,8 @@ MemberMap make_map(const rcsg_candidates& cs) {
     int b = 0;
     for (int q = 0; q < cs.n_qubits; ++q)
         if (!is_open[q]) mm.fixed_pos[b++] = q;
+    mm.low_open = 1;
+    for (int j = 0; j < cs.l; ++j) mm.low_open &= cs.open_qubits[j] == j ? 1 : 0;
     return mm;
 }
 

@@ -24,7 +24,7 @@ def main():
     trials = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
     seeds = (sys.argv[3] if len(sys.argv) > 3 else "0").split(",")
     n, m, topo, blog = CFGS[name]
-    out = os.path.join(ROOT, "plans", f"{name}.json")
+    out = os.path.join(os.environ.get("PLAN_OUT", os.path.join(ROOT, "plans")), f"{name}.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     best = None
     for sd in seeds:
