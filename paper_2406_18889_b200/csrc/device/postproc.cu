@@ -477,48 +477,46 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
         if (threadIdx.x == 0) s_cnt = 0;
         __syncthreads();
     };
-    for (int64_t g0 = blockIdx.x * static_cast<int64_t>(gpb); g0 < n_groups;
-         g0 += static_cast<int64_t>(gridDim.x) * gpb) {
-        const int64_t base_t = g0 * per;
-        // load + stage: rounds of U x blockDim.x candidates with U independent 16-B
-        // loads per thread in flight (block-uniform rounds)
-        for (int64_t e0 = 0; e0 < tile_el; e0 += U * static_cast<int64_t>(blockDim.x)) {
-            double pv[U];
+    // one load round: U independent 16-B loads per thread in flight
+    auto load_round = [&](int64_t base_t, int64_t e0, double* pv) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-                pv[u] = (e < tile_el && base_t + e < total) ? prob_at(src, from_amps, base_t + e) : 0.0;
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+            pv[u] = (e < tile_el && base_t + e < total) ? prob_at(src, from_amps, base_t + e) : 0.0;
+        }
+    };
+    // the round's probabilities into the tile, kept top-k candidates into the staging buffer
+    auto consume_round = [&](int64_t base_t, int64_t e0, const double* pv) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+            const int64_t t = base_t + e;
+            const bool in = e < tile_el && t < total;
+            const double p = pv[u];
+            if (in) {
+                flag_nan(p, bad);
+                tile[(e >> l) * pitch + (e & (per - 1))] = p;
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-                const int64_t t = base_t + e;
-                const bool in = e < tile_el && t < total;
-                const double p = pv[u];
-                if (in) {
-                    flag_nan(p, bad);
-                    tile[(e >> l) * pitch + (e & (per - 1))] = p;
-                }
-                if (collect) {
-                    const bool take = in && asc_key(p) >= thr;
-                    const unsigned mask = __ballot_sync(0xffffffffu, take);
-                    if (mask) {
-                        unsigned b = 0;
-                        if (lane == 0) b = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
-                        b = __shfl_sync(0xffffffffu, b, 0);
-                        if (take) {
-                            const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
-                            const K key = sort_key<K>(p, thr);
-                            s_key[pos] = key;
-                            s_t[pos] = static_cast<V>(t);
-                            kmin = min(kmin, key);
-                        }
+            if (collect) {
+                const bool take = in && asc_key(p) >= thr;
+                const unsigned mask = __ballot_sync(0xffffffffu, take);
+                if (mask) {
+                    unsigned b = 0;
+                    if (lane == 0) b = atomicAdd(&s_cnt, static_cast<unsigned>(__popc(mask)));
+                    b = __shfl_sync(0xffffffffu, b, 0);
+                    if (take) {
+                        const unsigned pos = b + __popc(mask & ((1u << lane) - 1));
+                        const K key = sort_key<K>(p, thr);
+                        s_key[pos] = key;
+                        s_t[pos] = static_cast<V>(t);
+                        kmin = min(kmin, key);
                     }
                 }
             }
-            if (collect) flush(U * blockDim.x, false);
         }
-        __syncthreads();
+    };
+    // thread g walks group g0 + g of the tile
+    auto walk = [&](int64_t g0) {
         const int64_t g = g0 + threadIdx.x;
         if (threadIdx.x < gpb && g < n_groups) {
             double* row = tile + threadIdx.x * pitch;
@@ -559,7 +557,36 @@ __global__ void __launch_bounds__(256) direct_scan_kernel(const double* __restri
                 direct_out[g] = member_index(mm, fixed[g], static_cast<uint64_t>(pick));
             }
         }
-        __syncthreads();  // the tile is reused
+    };
+    if (tile_el <= U * static_cast<int64_t>(blockDim.x)) {
+        // single-round tiles (gpb * 2^l <= U * 256): software pipeline - the next tile's
+        // loads are in flight while this tile's groups are walked
+        double pv[U];
+        int64_t g0 = blockIdx.x * static_cast<int64_t>(gpb);
+        if (g0 < n_groups) load_round(g0 * per, 0, pv);
+        for (; g0 < n_groups; g0 += static_cast<int64_t>(gridDim.x) * gpb) {
+            consume_round(g0 * per, 0, pv);
+            if (collect) flush(U * blockDim.x, false);
+            __syncthreads();
+            const int64_t g1 = g0 + static_cast<int64_t>(gridDim.x) * gpb;
+            if (g1 < n_groups) load_round(g1 * per, 0, pv);
+            walk(g0);
+            __syncthreads();  // the tile is reused
+        }
+    } else {
+        for (int64_t g0 = blockIdx.x * static_cast<int64_t>(gpb); g0 < n_groups;
+             g0 += static_cast<int64_t>(gridDim.x) * gpb) {
+            const int64_t base_t = g0 * per;
+            for (int64_t e0 = 0; e0 < tile_el; e0 += U * static_cast<int64_t>(blockDim.x)) {
+                double pv[U];
+                load_round(base_t, e0, pv);
+                consume_round(base_t, e0, pv);
+                if (collect) flush(U * blockDim.x, false);
+            }
+            __syncthreads();
+            walk(g0);
+            __syncthreads();  // the tile is reused
+        }
     }
     if (collect) flush(0, true);
     publish_min<K>(kmin, kmin_out, lane);
