@@ -1515,9 +1515,53 @@ int pair_policy(const GemmArgs& g) {
     return (kb >= 1024 && g.n >= 2048) ? 2 : 1;
 }
 
+// C = A B^T computed as (B A^T)^T: the operands trade places and the output map's
+// row and column parts swap (the 4M complex product is symmetric in A and B).
+GemmArgs swapped(const GemmArgs& g) {
+    GemmArgs h = g;
+    h.a = g.b;
+    h.b = g.a;
+    h.a_plane = g.b_plane;
+    h.b_plane = g.a_plane;
+    h.a_batch = g.b_batch;
+    h.b_batch = g.a_batch;
+    h.m = g.n;
+    h.n = g.m;
+    OutMap& o = h.om;
+    o.m_bits = g.om.n_bits;
+    o.n_bits = g.om.m_bits;
+    for (int j = 0; j < kMaxRank; ++j) {
+        o.m_pos[j] = g.om.n_pos[j];
+        o.n_pos[j] = g.om.m_pos[j];
+    }
+    o.n_vstride = out_row_vstride(g.om);
+    o.m_vstride = g.om.n_vstride ? g.om.n_vstride : 1;  // 1: the columns never exceed 2^n_bits (unused)
+    return h;
+}
+
+// A CTA-pair tile spans 256 rows: when m pads badly to 256 (cfg2 step 149: 3604 rows ->
+// 3840, 6.5 % zero rows) and n is a multiple of 256, the swapped GEMM pads m to the
+// column tile instead (3712 with 128-wide tiles).  Scatter outputs, unbatched only.
+template <typename E>
+bool swap_for_pair(const GemmArgs& g, int bn) {
+    static const bool on = !(getenv("RCSG_TC_SWAP") && atoi(getenv("RCSG_TC_SWAP")) == 0);
+    if (!on || !g.om.scatter || g.batch > 1 || g.ia || g.ib || g.vperm || g.n % 256 || g.m < 256) return false;
+    if (g.om.n_vstride == 0 && g.n > (int64_t{1} << g.om.n_bits)) return false;
+    auto waste = [](int64_t x, int64_t t) { return static_cast<double>((x + t - 1) / t * t) / static_cast<double>(x) - 1.0; };
+    return waste(g.m, 256) > waste(g.m, bn) + 0.02;
+}
+
 template <typename E>
 bool launch_pair(const GemmArgs& g, cudaStream_t st) {
-    const int mode = pair_policy<E>(g);
+    int mode = pair_policy<E>(g);
+    if (mode != 0 && swap_for_pair<E>(g, mode == 2 ? 256 : 128)) {
+        const GemmArgs h = swapped(g);
+        if (pair_policy<E>(h) == mode) {
+            if (mode == 2) launch<256, 3, E, 128, 0, 2>(h, st);
+            else launch<128, 4, E, 128, 0, 2>(h, st);
+            return true;
+        }
+    }
     if (mode == 0) return false;
     if (mode == 2) launch<256, 3, E, 128, 0, 2>(g, st);
     else launch<128, 4, E, 128, 0, 2>(g, st);

@@ -38,6 +38,8 @@ CASES = [
     ("pair1-mtail", 1000, 768, 2048, [], []),
     ("pair2-mtail", 1000, 768, 2048, [], []),
     ("pair1-splitk", 512, 256, 65536, [], []),
+    # m = 3604 (901 row blocks of 4) pads to 3840 on 256-row pairs: computed as the swapped GEMM
+    ("pair1-swap", 3604, 512, 2048, [3, 7], [0, 1, 2, 4, 5, 6, 8, 9, 10]),
     ("pair2-splitk", 512, 256, 65536, [], []),
 ]
 
