@@ -477,10 +477,18 @@ __device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v
         for (int i = 0; i < CW; ++i) x[i] *= sc;
     }
     if (p.round_tf32) {
+        // non-finite check by FFMA (x * 0 is NaN exactly for Inf / NaN x) before and after an
+        // integer round-to-nearest-away to tf32 (cvt.rna.tf32.f32 is emulated with a per-element
+        // Inf test; the checks here cover NaN inputs and a rounding overflow instead)
+        float z0 = 0.f, z1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < CW; ++i) x[i] = tf32_rn(x[i]);
-    }
-    if (row0 + lane < p.m) {
+        for (int i = 0; i < CW; ++i) {
+            z0 = fmaf(x[i], 0.f, z0);
+            x[i] = __uint_as_float((__float_as_uint(x[i]) + 0x1000u) & 0xffffe000u);
+            z1 = fmaf(x[i], 0.f, z1);
+        }
+        if (row0 + lane < p.m) bad = z0 != z0 || z1 != z1;
+    } else if (row0 + lane < p.m) {
 #pragma unroll
         for (int i = 0; i < CW; ++i) bad |= !isfinite(x[i]);
     }
