@@ -296,6 +296,8 @@ struct TcParams {
                             // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
                             // flight read the same shared-operand panels (see coord_at)
     int32_t tm;             // persistent kernel: rows per tile (128, or 256 for a CTA pair)
+    int32_t blk;            // 4-byte outputs stored by TMA from shared memory in 16 x 16 blocks: 1 =
+                            // columns 0-3 at output bits 0-3 (64-B column runs), 2 = rows 0-3 at bits 0-3
     int32_t seg;            // > 0: k-blocks per TMEM accumulation segment; the epilogue sums the
                             // segments in fp32 registers (split tf32: short tensor-core accumulation chains)
     int32_t sleepy;         // persistent kernel: producer / MMA threads wait with a suspend-time hint
@@ -524,6 +526,80 @@ __device__ __forceinline__ bool store_chunk_staged4(const TcParams& p, int64_t v
             }
         }
         __syncwarp();
+    }
+    return bad;
+}
+
+// TMA-store epilogue for 4-byte outputs with a 64-B run at output bits 0-3 (p.blk
+// 1: four column bits, 2: four row bits): the warp stages each 16-column half of
+// its 32 x CW chunk as two 16 x 16 blocks (SWIZZLE_64B, the run innermost) and two
+// lanes issue one TMA tensor store each through map_c, a 5-D view of the C buffer
+// {element offset, then one extent-2 dimension per output bit of the other four
+// bits 0-3 (stride 2^pos)}.  The global writes leave the LSU / L1 path: the staged
+// epilogue spends it on shared loads plus 16-B stores, and those steps were
+// L1-pipe-bound (profiles/r02/ncu_s3/cfg4_k8_*).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(smem)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t smem, int x) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %2, %2, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(x), "r"(0), "r"(smem)
+        : "memory");
+}
+
+template <int CW = 32>
+__device__ __forceinline__ bool store_chunk_tma4(const TcParams& p, const CUtensorMap* map_c, int64_t v, int64_t row0,
+                                                 float* stage, float* x, int plane, const int64_t* tn_lo, int lane,
+                                                 int64_t my_off, int64_t col_base) {
+    if (p.scale_exp) {
+        const float sc = exp2f(static_cast<float>(p.scale_exp));
+#pragma unroll
+        for (int i = 0; i < CW; ++i) x[i] *= sc;
+    }
+    bool bad = false;
+    if (p.round_tf32) {
+        float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+            z0 = fmaf(x[i], 0.f, z0);
+            x[i] = __uint_as_float((__float_as_uint(x[i]) + 0x1000u) & 0xffffe000u);
+            z1 = fmaf(x[i], 0.f, z1);
+        }
+        bad = z0 != z0 || z1 != z1;
+    } else {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) bad |= !isfinite(x[i]);
+    }
+    const int r = lane & 15;
+    float* blk = stage + (lane >> 4) * 256;  // lanes 0-15: block 0, lanes 16-31: block 1 (1 KB each)
+    const bool issuer = (lane & 15) == 0;
+    const int64_t base_el = plane * p.c_plane + v * p.c_batch + my_off + col_base;
+#pragma unroll
+    for (int h = 0; h < CW / 16; ++h) {
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the buffer is free
+        __syncwarp();
+        if (p.blk & 1) {  // [row][16 columns]: 64-B rows, 16-B slot i ^ (row / 2) % 4
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4*>(blk + r * 16 + ((i ^ ((r >> 1) & 3)) << 2)) =
+                    make_float4(x[16 * h + 4 * i], x[16 * h + 4 * i + 1], x[16 * h + 4 * i + 2], x[16 * h + 4 * i + 3]);
+        } else {  // [column][16 rows]: lane r scatters its 16 columns into the 64-B column rows
+#pragma unroll
+            for (int c = 0; c < 16; ++c) blk[c * 16 + ((((r >> 2) ^ (c >> 1)) & 3) << 2) + (r & 3)] = x[16 * h + c];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (issuer) {
+            const int64_t off = base_el + tn_lo[16 * h];  // block origin (row and column bits 0-3 zero)
+            if (p.blk >= 3) tma_store_2d(map_c, smem_u32(blk), 0, static_cast<int>(off >> 4));  // one 1-KB run
+            else tma_store_5d(map_c, smem_u32(blk), static_cast<int>(off));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
     }
     return bad;
 }
@@ -859,7 +935,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const __grid_constant__ CUtensorMap map_as, const __grid_constant__ CUtensorMap map_bs,
                        const __grid_constant__ CUtensorMap map_as2, const __grid_constant__ CUtensorMap map_bs2,
-                       const TcParams p, int64_t total_tiles) {
+                       const __grid_constant__ CUtensorMap map_c, const TcParams p, int64_t total_tiles) {
     constexpr bool THREE = VAR == 1, SPLIT = VAR == 2;
     constexpr int NPL = VAR == 0 ? 2 : (VAR == 1 ? 3 : 4);  // shared-memory planes per operand
     constexpr int NACC = VAR == 1 ? 3 : 2;                  // TMEM accumulators per tile
@@ -1094,7 +1170,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
                         return;
                     }
                 } else {
+                    if (p.blk && p.splits == 1 && col0 + CW <= p.n && c.m0 + q * 32 + 32 <= p.m) {
+                        bad |= store_chunk_tma4<CW>(p, &map_c, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
+                                                    plane, tn_lo, lane, row_off, col_base);
+                        return;
+                    }
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
+                        if (p.blk)  // the buffer may still be read by an earlier TMA store
+                            if ((lane & 15) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
                         bad |= store_chunk_staged4<CW>(p, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
                                                        plane, tn_lo, lane, row < p.m ? row_off : 0, col_base);
                         return;
@@ -1189,6 +1273,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
         }
         if (bad && p.fault && p.splits == 1) atomicMin(p.fault, p.step);
+        if (p.blk && (lane & 15) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores done
     }
     __syncwarp();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1338,6 +1423,52 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
     p.k_chunk = chunk_blocks * kbk<E, RB>;
+    // TMA-store epilogue (store_chunk_tma4): 4-byte outputs with four column bits (blk 1) or four
+    // row bits (blk 2) at output bits 0-3; RCSG_TC_BLK=0 disables
+    CUtensorMap mc = ar;
+    {
+        static const bool blk_on = !(getenv("RCSG_TC_BLK") && atoi(getenv("RCSG_TC_BLK")) == 0);
+        int kind = 0;
+        // short K only (<= 16 k-blocks per tile): on long-K, compute-bound tiles the stores compete with
+        // the operand loads for the TMA unit (cfg2 step 149: 5 % slower, profiles/r02/blk/ab_blk.log)
+        if (blk_on && sizeof(E) == 4 && VAR == 0 && splits == 1 && chunk_blocks <= 16 && g.om.scatter && g.om.n_bits >= 4 &&
+            g.om.m_bits >= 4 && 2 * g.c_plane < (int64_t{1} << 31) && (reinterpret_cast<uintptr_t>(g.c) & 255) == 0) {
+            bool cols = true, rows = true;
+            for (int j = 0; j < 4; ++j) {
+                cols &= g.om.n_pos[j] == j;
+                rows &= g.om.m_pos[j] == j;
+            }
+            kind = cols ? 1 : (rows ? 2 : 0);
+        }
+        if (kind) {
+            const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;  // the four bits of the other index
+            bool run = true;  // the other four bits at 4-7: each 16 x 16 block is one 1-KB run (2-D map)
+            for (int j = 0; j < 4; ++j) run &= other[j] == 4 + j;
+            if (run) {
+                cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(2 * g.c_plane / 16)};
+                cuuint64_t strides[1] = {64};
+                cuuint32_t box[2] = {16, 16};
+                cuuint32_t estr[2] = {1, 1};
+                const CUresult r = encode_fn()(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.c, dims, strides, box, estr,
+                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                kind = r == CUDA_SUCCESS && g.c_plane % 16 == 0 ? kind + 2 : 0;
+            }
+        }
+        if (kind == 1 || kind == 2) {
+            const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;
+            cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * g.c_plane), 2, 2, 2, 2};
+            cuuint64_t strides[4];
+            for (int j = 0; j < 4; ++j) strides[j] = cuuint64_t{4} << other[j];
+            cuuint32_t box[5] = {16, 2, 2, 2, 2};
+            cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+            const CUresult r = encode_fn()(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, g.c, dims, strides, box, estr,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) kind = 0;
+        }
+        p.blk = kind;
+    }
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     {
         // NBUF must be a multiple of the group count.
@@ -1421,10 +1552,10 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             cfg.attrs = attr;
             cfg.numAttrs = 2;
             cudaLaunchKernelEx(&cfg, gemm_tc_persistent<BN, STAGES, E, RB, VAR, CG>, ar, ai, br, bi, as, bs, as2, bs2,
-                               p, total);
+                               mc, p, total);
         } else {
             launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, VAR>, dim3(grid), dim3(kPThreads),
-                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, as2, bs2, p, total);
+                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, as2, bs2, mc, p, total);
         }
     } else {
         static std::atomic<uint64_t> configured{0};  // function attributes are per device

@@ -29,6 +29,11 @@ CASES = [
     # 8 m n k >= 2.7e11, k >= 512, n >= 64: the 3M path (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi))
     ("3m-n1024", 4096, 1024, 8192, [], []),
     ("3m-n64-scatter", 1 << 14, 64, 32768, [7, 8, 9, 10, 11, 12, 13] + list(range(0, 7)), list(range(14, 20))),
+    # 4-byte outputs with contiguous 16 x 16 blocks (columns at bits 0-3, rows at 4-7): TMA stores
+    ("blk16", 1 << 12, 1 << 10, 64, [4, 5, 6, 7] + list(range(14, 22)), [0, 1, 2, 3] + list(range(8, 14))),
+    ("blk16-mtail", 4000, 1 << 10, 128, [4, 5, 6, 7] + list(range(14, 22)), [0, 1, 2, 3] + list(range(8, 14))),
+    ("blk16-rows", 1 << 12, 1 << 10, 64, [0, 1, 2, 3] + list(range(8, 16)), [4, 5, 6, 7] + list(range(16, 22))),
+    ("blk-cols-5d", 1 << 12, 1 << 10, 64, [5, 9, 11, 13] + list(range(14, 22)), [0, 1, 2, 3, 4, 6, 7, 8, 10, 12]),
     # CTA-pair tiles (cta_group::2; pair1 = 256 x 128, pair2 = 256 x 256): plain, scatter
     # output, an M tail that leaves the peer CTA without rows, and split K
     ("pair1-plain", 1024, 512, 4096, [], []),
