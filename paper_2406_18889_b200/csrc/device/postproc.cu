@@ -661,11 +661,11 @@ __global__ void tie_fix_kernel(const K* __restrict__ key, V* __restrict__ t,
 // ---- 3'. bucket order: instead of radix-sorting every kept entry, the kept
 // key range [largest probability, threshold] is cut into 2^18 buckets of
 // equal width in the 64-bit descending key (bucket 0 = highest probabilities):
-//   hist     counts per bucket (bcount, zero on entry);
+//   hist     counts per bucket (bcount, zeroed first), each entry keeping the
+//            slot its atomic returned (its place inside the bucket);
 //   scan     bstart = exclusive sum (cub), bstart[kBuckets] = total;
-//   scatter  entries of buckets starting below k go to their bucket's range
-//            (key, candidate, bucket); every entry decrements its bucket's
-//            count, so bcount is zero again for the next call;
+//   scatter  entries of buckets starting below k go to bucket start + slot
+//            (key, candidate, bucket), no atomics;
 //   rank     one thread per placed entry counts the entries of its bucket
 //            ahead of it in (prob desc, lexkey asc, candidate position) order -
 //            a strict total order: the exact key decides unless equal, so the
@@ -687,7 +687,7 @@ __device__ __forceinline__ int bucket_shift(uint64_t kmin, uint64_t thr) {
 __global__ void bucket_hist_kernel(const uint64_t* __restrict__ key, const unsigned long long* __restrict__ counter,
                                    uint64_t cap, uint64_t k, const unsigned long long* __restrict__ kmin_p,
                                    const uint64_t* __restrict__ thr_p, uint32_t* __restrict__ bcount,
-                                   int* __restrict__ fail) {
+                                   uint32_t* __restrict__ rank_in, int* __restrict__ fail) {
     const uint64_t cnt = *counter;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (cnt < k || cnt > cap)) *fail = 1;
     const uint64_t n = min(cnt, cap);
@@ -698,9 +698,13 @@ __global__ void bucket_hist_kernel(const uint64_t* __restrict__ key, const unsig
         uint64_t kk[4];  // 4 independent entries per thread in flight
 #pragma unroll
         for (int u = 0; u < 4; ++u) kk[u] = i0 + u * gs < n ? key[i0 + u * gs] : 0;
+        uint32_t rk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)  // the entry's slot inside its bucket (any order)
+            rk[u] = i0 + u * gs < n ? atomicAdd(&bcount[(kk[u] - kmin) >> sh], 1u) : 0u;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (i0 + u * gs < n) atomicAdd(&bcount[(kk[u] - kmin) >> sh], 1u);
+            if (i0 + u * gs < n) rank_in[i0 + u * gs] = rk[u];
     }
 }
 
@@ -708,7 +712,7 @@ template <typename V>
 __global__ void bucket_scatter_kernel(const uint64_t* __restrict__ key, const V* __restrict__ t,
                                       const unsigned long long* __restrict__ counter, uint64_t cap, uint64_t k,
                                       const unsigned long long* __restrict__ kmin_p, const uint64_t* __restrict__ thr_p,
-                                      const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcount,
+                                      const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ rank_in,
                                       uint64_t* __restrict__ out_key, V* __restrict__ out_t,
                                       uint32_t* __restrict__ out_b) {
     const uint64_t n = min(static_cast<uint64_t>(*counter), cap);
@@ -725,13 +729,14 @@ __global__ void bucket_scatter_kernel(const uint64_t* __restrict__ key, const V*
             const bool in = i0 + u * gs < n;
             kk[u] = in ? key[i0 + u * gs] : kmin;
             tv[u] = in ? t[i0 + u * gs] : V{0};
+            pos[u] = in ? rank_in[i0 + u * gs] : 0u;
             b[u] = static_cast<uint32_t>((kk[u] - kmin) >> sh);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) s0[u] = bstart[b[u]];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)  // any order inside the bucket
-            pos[u] = i0 + u * gs < n ? s0[u] + atomicSub(&bcount[b[u]], 1u) - 1u : 0u;
+        for (int u = 0; u < 4; ++u) {
+            s0[u] = bstart[b[u]];
+            pos[u] += s0[u];
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (i0 + u * gs >= n || s0[u] >= k) continue;  // every rank of the bucket is >= k
@@ -909,11 +914,11 @@ cudaStream_t post_stream() {
 }
 
 enum Slot {
-    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb, kBucket, kEnt, kBid
+    kFixed = 0, kKeyA, kKeyB, kTA, kTB, kTmp, kHist, kCounters, kOut, kDirect, kSel, kXeb, kBucket, kEnt, kBid, kRank
 };
 
-// per-bucket counts (kBuckets + 1, zero between calls: the scatter pass
-// decrements them back) followed by the bucket starts (kBuckets + 1)
+// per-bucket counts (kBuckets + 1, zeroed by each call) followed by the
+// bucket starts (kBuckets + 1)
 uint32_t* bucket_counts(cudaStream_t st) {
     const bool fresh = pool().bufs.count({current_device(), kBucket}) == 0;
     uint32_t* b = scratch_as<uint32_t>(kBucket, 2 * (kBuckets + 1));
@@ -1085,15 +1090,17 @@ PostResult postprocess(const rcsg_candidates& cs, const double* d_src, bool from
         uint64_t* kb = scratch_as<uint64_t>(kKeyB, cap);
         uint32_t* tb = scratch_as<uint32_t>(kTB, cap);
         uint32_t* bid = scratch_as<uint32_t>(kBid, cap);
+        uint32_t* rk = scratch_as<uint32_t>(kRank, cap);
+        CUDA_OK(cudaMemsetAsync(bcount, 0, (kBuckets + 1) * sizeof(uint32_t), st));
         size_t scan_bytes = 0;
         CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, bcount, bstart, kBuckets + 1, st));
         void* scan_tmp = scratch(kTmp, scan_bytes);
         const int g = grid_for(static_cast<int64_t>(cap), 256);
-        bucket_hist_kernel<<<g, 256, 0, st>>>(ka, &d_ctl->count, cap, k, &d_ctl->kmin64, &d_ctl->thr, bcount,
+        bucket_hist_kernel<<<g, 256, 0, st>>>(ka, &d_ctl->count, cap, k, &d_ctl->kmin64, &d_ctl->thr, bcount, rk,
                                               &d_ctl->fail);
         CUDA_OK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, bcount, bstart, kBuckets + 1, st));
         bucket_scatter_kernel<uint32_t><<<g, 256, 0, st>>>(ka, ta, &d_ctl->count, cap, k, &d_ctl->kmin64,
-                                                           &d_ctl->thr, bstart, bcount, kb, tb, bid);
+                                                           &d_ctl->thr, bstart, rk, kb, tb, bid);
         bucket_rank_kernel<uint32_t><<<g, 256, 0, st>>>(kb, tb, bid, bstart, &d_ctl->count, cap, k, d_fixed, mm,
                                                         &d_ctl->fail, d_top);
     };
