@@ -604,6 +604,68 @@ __device__ __forceinline__ bool store_chunk_tma4(const TcParams& p, const CUtens
     return bad;
 }
 
+// The same for 2-byte outputs with a 64-B (32-element) run at output bits 0-4 (p.blk
+// 1: five column bits, 2: five row bits; 3 / 4: the other index's four low bits at
+// 5-8, one 1-KB run per block through a 2-D map).  Column runs: two 16-row x 32-column
+// blocks per chunk (lanes 0-15, 16-31); row runs: two 16-column x 32-row blocks
+// (every lane writes its row into both).
+template <typename E>
+__device__ __forceinline__ bool store_chunk_tma2(const TcParams& p, const CUtensorMap* map_c, int64_t v,
+                                                 int64_t row0, E* stage, float* x, int plane, const int64_t* tn_lo,
+                                                 int lane, int64_t my_off, int64_t col_base) {
+    constexpr int CW = 32;
+    if (p.scale_exp) {
+        const float sc = exp2f(static_cast<float>(p.scale_exp));
+#pragma unroll
+        for (int i = 0; i < CW; ++i) x[i] *= sc;
+    }
+    float mx = 0.f;
+    bool nan = false;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) {
+        mx = fmaxf(mx, fabsf(x[i]));
+        nan |= x[i] != x[i];
+    }
+    const bool bad = nan || unstorable<E>(mx);
+    const int64_t base_el = plane * p.c_plane + v * p.c_batch + col_base;
+    if (lane == 0 || lane == 16) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buffer free
+    __syncwarp();
+    if (p.blk & 1) {  // [row][32 columns] per 16-row block: 64-B rows, 16-B slot i ^ (row / 2) % 4
+        const int r = lane & 15;
+        E* blk = stage + (lane >> 4) * 512;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(blk + r * 32 + ((i ^ ((r >> 1) & 3)) << 3)) = pack8<E>(x + 8 * i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if ((lane & 15) == 0) {
+            const int64_t off = base_el + my_off;  // block origin: row bits 0-3 and column bits 0-4 zero
+            if (p.blk >= 3) tma_store_2d(map_c, smem_u32(blk), 0, static_cast<int>(off >> 5));
+            else tma_store_5d(map_c, smem_u32(blk), static_cast<int>(off));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    } else {  // [column][32 rows] per 16-column block: lane = row, slot (row / 8) ^ (column / 2) % 4
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            E* blk = stage + (c >> 4) * 512;
+            const int cc = c & 15;
+            store_c(blk + cc * 32 + ((((lane >> 3) ^ (cc >> 1)) & 3) << 3) + (lane & 7), x[c]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        const int64_t roff = __shfl_sync(0xffffffffu, my_off, 0);
+        if (lane == 0 || lane == 16) {
+            const int b = lane >> 4;
+            const int64_t off = base_el + roff + tn_lo[16 * b];  // row bits 0-4 and column bits 0-3 zero
+            E* blk = stage + b * 512;
+            if (p.blk >= 3) tma_store_2d(map_c, smem_u32(blk), 0, static_cast<int>(off >> 5));
+            else tma_store_5d(map_c, smem_u32(blk), static_cast<int>(off));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    return bad;
+}
+
 template <int BN, int STAGES, int RB = 128, int NPL = 2, int CG = 1>
 struct Smem {
     static constexpr int kATile = kBM * RB;  // bytes per A plane tile (RB-byte rows)
@@ -1164,7 +1226,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 constexpr int CW = decltype(cw_tag)::value;
                 const int64_t col0 = c.n0 + c0;  // multiple of CW
                 if constexpr (sizeof(E) == 2) {
+                    if constexpr (CW == 32) {
+                        if (p.blk && p.splits == 1 && col0 + CW <= p.n && c.m0 + q * 32 + 32 <= p.m) {
+                            bad |= store_chunk_tma2<E>(p, &map_c, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
+                                                       row_off, col_base);
+                            return;
+                        }
+                    }
                     if (p.epi && p.splits == 1 && col0 + CW <= p.n) {
+                        if (p.blk)  // the buffer may still be read by an earlier TMA store
+                            if (lane == 0 || lane == 16) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
                         bad |= store_chunk_staged<E, CW>(p, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
                                                          row < p.m ? row_off : 0, col_base);
                         return;
@@ -1423,52 +1495,6 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     splits = static_cast<int>((kblocks + chunk_blocks - 1) / chunk_blocks);  // no empty split
     p.splits = splits;
     p.k_chunk = chunk_blocks * kbk<E, RB>;
-    // TMA-store epilogue (store_chunk_tma4): 4-byte outputs with four column bits (blk 1) or four
-    // row bits (blk 2) at output bits 0-3; RCSG_TC_BLK=0 disables
-    CUtensorMap mc = ar;
-    {
-        static const bool blk_on = !(getenv("RCSG_TC_BLK") && atoi(getenv("RCSG_TC_BLK")) == 0);
-        int kind = 0;
-        // short K only (<= 16 k-blocks per tile): on long-K, compute-bound tiles the stores compete with
-        // the operand loads for the TMA unit (cfg2 step 149: 5 % slower, profiles/r02/blk/ab_blk.log)
-        if (blk_on && sizeof(E) == 4 && VAR == 0 && splits == 1 && chunk_blocks <= 16 && g.om.scatter && g.om.n_bits >= 4 &&
-            g.om.m_bits >= 4 && 2 * g.c_plane < (int64_t{1} << 31) && (reinterpret_cast<uintptr_t>(g.c) & 255) == 0) {
-            bool cols = true, rows = true;
-            for (int j = 0; j < 4; ++j) {
-                cols &= g.om.n_pos[j] == j;
-                rows &= g.om.m_pos[j] == j;
-            }
-            kind = cols ? 1 : (rows ? 2 : 0);
-        }
-        if (kind) {
-            const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;  // the four bits of the other index
-            bool run = true;  // the other four bits at 4-7: each 16 x 16 block is one 1-KB run (2-D map)
-            for (int j = 0; j < 4; ++j) run &= other[j] == 4 + j;
-            if (run) {
-                cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(2 * g.c_plane / 16)};
-                cuuint64_t strides[1] = {64};
-                cuuint32_t box[2] = {16, 16};
-                cuuint32_t estr[2] = {1, 1};
-                const CUresult r = encode_fn()(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.c, dims, strides, box, estr,
-                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                kind = r == CUDA_SUCCESS && g.c_plane % 16 == 0 ? kind + 2 : 0;
-            }
-        }
-        if (kind == 1 || kind == 2) {
-            const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;
-            cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * g.c_plane), 2, 2, 2, 2};
-            cuuint64_t strides[4];
-            for (int j = 0; j < 4; ++j) strides[j] = cuuint64_t{4} << other[j];
-            cuuint32_t box[5] = {16, 2, 2, 2, 2};
-            cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-            const CUresult r = encode_fn()(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, g.c, dims, strides, box, estr,
-                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) kind = 0;
-        }
-        p.blk = kind;
-    }
     const int64_t c_elems = g.batch * g.m * g.n;  // per plane
     {
         // NBUF must be a multiple of the group count.
@@ -1490,6 +1516,56 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             if (p.seg > 0) ng = 1;
         }
         p.ng = ng;
+    }
+    // TMA-store epilogue (store_chunk_tma4 / tma2): a 64-B run at output bits 0.. (4-byte: four
+    // column (blk 1) or row (blk 2) bits; 2-byte: five), short-K GEMMs; RCSG_TC_BLK=0 disables
+    CUtensorMap mc = ar;
+    {
+        static const bool blk_on = !(getenv("RCSG_TC_BLK") && atoi(getenv("RCSG_TC_BLK")) == 0);
+        // 2-byte outputs: opt-in (RCSG_TC_BLK2=1); measured +1 % on cfg2 fp16 and -1 to -3 % on cfg4
+        // fp16 (profiles/r02/blk/ab_blk2.log), where the staged 16-B stores were not L1-bound
+        const bool blk2_on = getenv("RCSG_TC_BLK2") && atoi(getenv("RCSG_TC_BLK2")) == 1;
+        constexpr int RUN = sizeof(E) == 4 ? 4 : 5;  // run bits: 64 B
+        constexpr int OTH = 4;                       // the other index's bits per block
+        const int cw = BN / 2 < 32 ? BN / 2 : 32;    // epilogue chunk width (NG = 1)
+        int kind = 0;
+        // short K only (<= 16 k-blocks per tile): on long-K, compute-bound tiles the stores compete with
+        // the operand loads for the TMA unit (cfg2 step 149: 5 % slower, profiles/r02/blk/ab_blk.log)
+        if (blk_on && VAR == 0 && splits == 1 && chunk_blocks <= 16 && g.om.scatter && 2 * g.c_plane < (int64_t{1} << 31) &&
+            (reinterpret_cast<uintptr_t>(g.c) & 255) == 0 && (sizeof(E) == 4 || (cw == 32 && p.ng == 1 && blk2_on))) {
+            bool cols = g.om.n_bits >= RUN && g.om.m_bits >= OTH, rows = g.om.m_bits >= RUN && g.om.n_bits >= OTH;
+            for (int j = 0; j < RUN; ++j) {
+                cols = cols && g.om.n_pos[j] == j;
+                rows = rows && g.om.m_pos[j] == j;
+            }
+            kind = cols ? 1 : (rows ? 2 : 0);
+        }
+        if (kind) {
+            const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;  // the four low bits of the other index
+            bool run = true;  // at RUN..RUN+3: each block is one 1-KB run (2-D map)
+            for (int j = 0; j < OTH; ++j) run &= other[j] == RUN + j;
+            if (run && g.c_plane % (1 << RUN) == 0) {
+                cuuint64_t dims[2] = {cuuint64_t{1} << RUN, static_cast<cuuint64_t>(2 * g.c_plane >> RUN)};
+                cuuint64_t strides[1] = {64};
+                cuuint32_t box[2] = {1u << RUN, 16};
+                cuuint32_t estr[2] = {1, 1};
+                const CUresult r = encode_fn()(&mc, TcElem<E>::tma, 2, g.c, dims, strides, box, estr,
+                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                kind = r == CUDA_SUCCESS ? kind + 2 : 0;
+            } else {
+                cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * g.c_plane), 2, 2, 2, 2};
+                cuuint64_t strides[4];
+                for (int j = 0; j < 4; ++j) strides[j] = cuuint64_t{sizeof(E)} << other[j];
+                cuuint32_t box[5] = {1u << RUN, 2, 2, 2, 2};
+                cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+                const CUresult r = encode_fn()(&mc, TcElem<E>::tma, 5, g.c, dims, strides, box, estr,
+                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) kind = 0;
+            }
+        }
+        p.blk = kind;
     }
     {
         // grouped raster for long-K GEMMs with enough tiles in both directions

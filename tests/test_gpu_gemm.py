@@ -34,6 +34,9 @@ CASES = [
     ("blk16-mtail", 4000, 1 << 10, 128, [4, 5, 6, 7] + list(range(14, 22)), [0, 1, 2, 3] + list(range(8, 14))),
     ("blk16-rows", 1 << 12, 1 << 10, 64, [0, 1, 2, 3] + list(range(8, 16)), [4, 5, 6, 7] + list(range(16, 22))),
     ("blk-cols-5d", 1 << 12, 1 << 10, 64, [5, 9, 11, 13] + list(range(14, 22)), [0, 1, 2, 3, 4, 6, 7, 8, 10, 12]),
+    # 2-byte outputs: 32-element runs (five column / row bits at output bit 0)
+    ("blk2-cols-2d", 1 << 12, 1 << 10, 64, [5, 6, 7, 8] + list(range(14, 22)), [0, 1, 2, 3, 4] + list(range(9, 14))),
+    ("blk2-rows-5d", 1 << 12, 1 << 10, 128, [0, 1, 2, 3, 4] + list(range(9, 16)), [5, 7, 8, 16, 6, 17, 18, 19, 20, 21]),
     # CTA-pair tiles (cta_group::2; pair1 = 256 x 128, pair2 = 256 x 256): plain, scatter
     # output, an M tail that leaves the peer CTA without rows, and split K
     ("pair1-plain", 1024, 512, 4096, [], []),
@@ -56,6 +59,8 @@ def test_tc_gemm_matches_simt(name, m, n, k, mp, npos, dtype, tol, monkeypatch):
         monkeypatch.setenv("RCSG_TC_3M", "1")  # the opt-in 3M kernel
     if name.startswith("pair"):
         monkeypatch.setenv("RCSG_TC_PAIR", name[4])
+    if name.startswith("blk2"):
+        monkeypatch.setenv("RCSG_TC_BLK2", "1")  # the opt-in 2-byte TMA-store epilogue
     lib = _native.testkit()
     check = {"f16": lib.rcsg_gemm_check_f16, "bf16": lib.rcsg_gemm_check_bf16, "tf32": lib.rcsg_gemm_check_tf32,
              "3xtf32": lib.rcsg_gemm_check_3xtf32}[dtype]
