@@ -1724,7 +1724,10 @@ template <typename E>
 int pair_policy(const GemmArgs& g) {
     const int64_t kb = (g.k + kbk<E, 128> - 1) / kbk<E, 128>;
     static const int64_t min_kb = getenv("RCSG_TC_PAIR_MINKB") ? atoll(getenv("RCSG_TC_PAIR_MINKB")) : 32;
-    if (g.m < 512 || g.n < 256 || kb < min_kb || g.k * static_cast<int64_t>(sizeof(E)) < 512) return 0;
+    // tf32 from n = 128 (cfg4's batched 8192 x 128 x 32768 step: +1.3 % per slice, amplitudes
+    // bit-identical to 1-CTA tiles, profiles/r02/ab_minn.log)
+    const int64_t min_n = getenv("RCSG_TC_PAIR_MINN") ? atoll(getenv("RCSG_TC_PAIR_MINN")) : (sizeof(E) == 4 ? 128 : 256);
+    if (g.m < 512 || g.n < min_n || kb < min_kb || g.k * static_cast<int64_t>(sizeof(E)) < 512) return 0;
     if (const char* e = getenv("RCSG_TC_PAIR")) return atoi(e);
     if (sizeof(E) == 2) return g.n >= 2048 ? 2 : 0;
     return (kb >= 1024 && g.n >= 2048) ? 2 : 1;
