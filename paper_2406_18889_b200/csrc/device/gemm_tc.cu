@@ -1572,8 +1572,9 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         // (RCSG_TC_GROUP: override; 0 disables)
         const int64_t n_lo = p.m_fast ? p.mt : p.nt, n_hi = p.m_fast ? p.nt : p.mt;
         int grp = (chunk_blocks >= 32 && n_lo >= 16 && n_hi >= 8) ? 8 : 0;
-        // tf32 CTA pairs with a short "lo" side (cfg2 step 149: 15 row pairs): 16 "hi" tiles in
-        // flight cut the DRAM reads by a fifth (profiles/r02/raster_probe.log)
+        // tf32 CTA pairs with a short "lo" side (15 row pairs: cfg2 step 149 unswapped): 16 "hi" tiles
+        // in flight cut the DRAM reads (profiles/r02/raster_probe.log); the swapped form (29 column
+        // tiles) is faster with the default 8 (profiles/r02/ab_pgroup.log)
         static const bool pair_group = !(getenv("RCSG_TC_PAIR_GROUP") && atoi(getenv("RCSG_TC_PAIR_GROUP")) == 0);
         if (pair_group && CG == 2 && sizeof(E) == 4 && chunk_blocks >= 32 && n_lo >= 8 && n_lo < 16 && n_hi >= 32)
             grp = 16;
