@@ -1531,7 +1531,7 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
         int kind = 0;
         // short K only (<= 16 k-blocks per tile): on long-K, compute-bound tiles the stores compete with
         // the operand loads for the TMA unit (cfg2 step 149: 5 % slower, profiles/r02/blk/ab_blk.log)
-        if (blk_on && VAR == 0 && splits == 1 && chunk_blocks <= 16 && g.om.scatter && 2 * g.c_plane < (int64_t{1} << 31) &&
+        if (blk_on && VAR == 0 && splits == 1 && chunk_blocks <= 16 && g.om.scatter &&
             (reinterpret_cast<uintptr_t>(g.c) & 255) == 0 && (sizeof(E) == 4 || (cw == 32 && p.ng == 1 && blk2_on))) {
             bool cols = g.om.n_bits >= RUN && g.om.m_bits >= OTH, rows = g.om.m_bits >= RUN && g.om.n_bits >= OTH;
             for (int j = 0; j < RUN; ++j) {
@@ -1544,7 +1544,8 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             const int8_t* other = kind == 1 ? g.om.m_pos : g.om.n_pos;  // the four low bits of the other index
             bool run = true;  // at RUN..RUN+3: each block is one 1-KB run (2-D map)
             for (int j = 0; j < OTH; ++j) run &= other[j] == RUN + j;
-            if (run && g.c_plane % (1 << RUN) == 0) {
+            // coordinates are int32: the 2-D map counts 64-B rows, the 5-D one elements
+            if (run && g.c_plane % (1 << RUN) == 0 && (2 * g.c_plane >> RUN) < (int64_t{1} << 31)) {
                 cuuint64_t dims[2] = {cuuint64_t{1} << RUN, static_cast<cuuint64_t>(2 * g.c_plane >> RUN)};
                 cuuint64_t strides[1] = {64};
                 cuuint32_t box[2] = {1u << RUN, 16};
@@ -1553,6 +1554,8 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
                                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 kind = r == CUDA_SUCCESS ? kind + 2 : 0;
+            } else if (2 * g.c_plane >= (int64_t{1} << 31)) {
+                kind = 0;
             } else {
                 cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * g.c_plane), 2, 2, 2, 2};
                 cuuint64_t strides[4];
