@@ -296,6 +296,7 @@ struct TcParams {
                             // raster then runs over m-tiles x (variant, n-tile) so that the tiles in
                             // flight read the same shared-operand panels (see coord_at)
     int32_t tm;             // persistent kernel: rows per tile (128, or 256 for a CTA pair)
+    int32_t blk_planes;     // TMA-store map per C plane (map_c: Re, map_c2: Im; offsets within a plane)
     int32_t blk;            // 4-byte outputs stored by TMA from shared memory in 16 x 16 blocks: 1 =
                             // columns 0-3 at output bits 0-3 (64-B column runs), 2 = rows 0-3 at bits 0-3
     int32_t seg;            // > 0: k-blocks per TMEM accumulation segment; the epilogue sums the
@@ -578,7 +579,7 @@ __device__ __forceinline__ bool store_chunk_tma4(const TcParams& p, const CUtens
     const int r = lane & 15;
     float* blk = stage + (lane >> 4) * 256;  // lanes 0-15: block 0, lanes 16-31: block 1 (1 KB each)
     const bool issuer = (lane & 15) == 0;
-    const int64_t base_el = plane * p.c_plane + v * p.c_batch + my_off + col_base;
+    const int64_t base_el = (p.blk_planes ? 0 : plane * p.c_plane) + v * p.c_batch + my_off + col_base;
 #pragma unroll
     for (int h = 0; h < CW / 16; ++h) {
         if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the buffer is free
@@ -627,7 +628,7 @@ __device__ __forceinline__ bool store_chunk_tma2(const TcParams& p, const CUtens
         nan |= x[i] != x[i];
     }
     const bool bad = nan || unstorable<E>(mx);
-    const int64_t base_el = plane * p.c_plane + v * p.c_batch + col_base;
+    const int64_t base_el = (p.blk_planes ? 0 : plane * p.c_plane) + v * p.c_batch + col_base;
     if (lane == 0 || lane == 16) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buffer free
     __syncwarp();
     if (p.blk & 1) {  // [row][32 columns] per 16-row block: 64-B rows, 16-B slot i ^ (row / 2) % 4
@@ -997,7 +998,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                        const __grid_constant__ CUtensorMap map_br, const __grid_constant__ CUtensorMap map_bi,
                        const __grid_constant__ CUtensorMap map_as, const __grid_constant__ CUtensorMap map_bs,
                        const __grid_constant__ CUtensorMap map_as2, const __grid_constant__ CUtensorMap map_bs2,
-                       const __grid_constant__ CUtensorMap map_c, const TcParams p, int64_t total_tiles) {
+                       const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
+                       const TcParams p, int64_t total_tiles) {
     constexpr bool THREE = VAR == 1, SPLIT = VAR == 2;
     constexpr int NPL = VAR == 0 ? 2 : (VAR == 1 ? 3 : 4);  // shared-memory planes per operand
     constexpr int NACC = VAR == 1 ? 3 : 2;                  // TMEM accumulators per tile
@@ -1228,7 +1230,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 if constexpr (sizeof(E) == 2) {
                     if constexpr (CW == 32) {
                         if (p.blk && p.splits == 1 && col0 + CW <= p.n && c.m0 + q * 32 + 32 <= p.m) {
-                            bad |= store_chunk_tma2<E>(p, &map_c, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
+                            bad |= store_chunk_tma2<E>(p, plane && p.blk_planes ? &map_c2 : &map_c, c.v, c.m0 + q * 32, stage, x, plane, tn_lo, lane,
                                                        row_off, col_base);
                             return;
                         }
@@ -1243,7 +1245,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     }
                 } else {
                     if (p.blk && p.splits == 1 && col0 + CW <= p.n && c.m0 + q * 32 + 32 <= p.m) {
-                        bad |= store_chunk_tma4<CW>(p, &map_c, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
+                        bad |= store_chunk_tma4<CW>(p, plane && p.blk_planes ? &map_c2 : &map_c, c.v, c.m0 + q * 32, reinterpret_cast<float*>(stage), x,
                                                     plane, tn_lo, lane, row_off, col_base);
                         return;
                     }
@@ -1519,7 +1521,8 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
     }
     // TMA-store epilogue (store_chunk_tma4 / tma2): a 64-B run at output bits 0.. (4-byte: four
     // column (blk 1) or row (blk 2) bits; 2-byte: five), short-K GEMMs; RCSG_TC_BLK=0 disables
-    CUtensorMap mc = ar;
+    CUtensorMap mc = ar, mc2 = ar;
+    p.blk_planes = 0;
     {
         static const bool blk_on = !(getenv("RCSG_TC_BLK") && atoi(getenv("RCSG_TC_BLK")) == 0);
         // 2-byte outputs: opt-in (RCSG_TC_BLK2=1); measured +1 % on cfg2 fp16 and -1 to -3 % on cfg4
@@ -1555,7 +1558,23 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
                                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 kind = r == CUDA_SUCCESS ? kind + 2 : 0;
             } else if (2 * g.c_plane >= (int64_t{1} << 31)) {
-                kind = 0;
+                // element offsets past int32: one 5-D map per plane (opt-in, RCSG_TC_BLK_PLANES=1)
+                static const bool planes_on = getenv("RCSG_TC_BLK_PLANES") && atoi(getenv("RCSG_TC_BLK_PLANES")) == 1;
+                bool ok = planes_on && g.c_plane < (int64_t{1} << 31) && (g.c_plane * sizeof(E)) % 256 == 0;
+                for (int pl = 0; ok && pl < 2; ++pl) {
+                    cuuint64_t dims[5] = {static_cast<cuuint64_t>(g.c_plane), 2, 2, 2, 2};
+                    cuuint64_t strides[4];
+                    for (int j = 0; j < 4; ++j) strides[j] = cuuint64_t{sizeof(E)} << other[j];
+                    cuuint32_t box[5] = {1u << RUN, 2, 2, 2, 2};
+                    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+                    const CUresult r = encode_fn()(pl ? &mc2 : &mc, TcElem<E>::tma, 5,
+                                                   static_cast<E*>(g.c) + pl * g.c_plane, dims, strides, box, estr,
+                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    ok = r == CUDA_SUCCESS;
+                }
+                if (ok) p.blk_planes = 1;
+                else kind = 0;
             } else {
                 cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * g.c_plane), 2, 2, 2, 2};
                 cuuint64_t strides[4];
@@ -1632,10 +1651,10 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
             cfg.attrs = attr;
             cfg.numAttrs = 2;
             cudaLaunchKernelEx(&cfg, gemm_tc_persistent<BN, STAGES, E, RB, VAR, CG>, ar, ai, br, bi, as, bs, as2, bs2,
-                               mc, p, total);
+                               mc, mc2, p, total);
         } else {
             launch_pdl(gemm_tc_persistent<BN, STAGES, E, RB, VAR>, dim3(grid), dim3(kPThreads),
-                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, as2, bs2, mc, p, total);
+                       S::template kPBytes<E>, st, ar, ai, br, bi, as, bs, as2, bs2, mc, mc2, p, total);
         }
     } else {
         static std::atomic<uint64_t> configured{0};  // function attributes are per device
