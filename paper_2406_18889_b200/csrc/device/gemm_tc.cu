@@ -1558,8 +1558,9 @@ void launch(const GemmArgs& g, cudaStream_t st, const void* a_sum = nullptr, con
                                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 kind = r == CUDA_SUCCESS ? kind + 2 : 0;
             } else if (2 * g.c_plane >= (int64_t{1} << 31)) {
-                // element offsets past int32: one 5-D map per plane (opt-in, RCSG_TC_BLK_PLANES=1)
-                static const bool planes_on = getenv("RCSG_TC_BLK_PLANES") && atoi(getenv("RCSG_TC_BLK_PLANES")) == 1;
+                // element offsets past int32: one 5-D map per plane (RCSG_TC_BLK_PLANES=0 disables;
+                // cfg4 amplitudes bit-identical, +0.9 % per slice, profiles/r02/blk/ab_planes.log)
+                static const bool planes_on = !(getenv("RCSG_TC_BLK_PLANES") && atoi(getenv("RCSG_TC_BLK_PLANES")) == 0);
                 bool ok = planes_on && g.c_plane < (int64_t{1} << 31) && (g.c_plane * sizeof(E)) % 256 == 0;
                 for (int pl = 0; ok && pl < 2; ++pl) {
                     cuuint64_t dims[5] = {static_cast<cuuint64_t>(g.c_plane), 2, 2, 2, 2};
